@@ -1,0 +1,222 @@
+"""CPU oracle of the HCAttention decode hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product path
+(paper_2507_19823_b200) never imports it and shares no code with it.
+
+Thin ctypes marshalling over oracle/hc_oracle.c (plain C, -O2
+-ffp-contract=off, no fast-math); every function there cites the PAPER.md
+passage / DESIGN.md reading it implements.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hc_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (gcc, OpenMP, no fast-math, no FP contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-std=gnu11",
+               "-fPIC", "-shared", "-o", _LIB_PATH + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_LIB_PATH)
+            p = C.c_void_p
+            i64, i32, f32 = C.c_int64, C.c_int, C.c_float
+            L.or_half_to_float.argtypes = [C.c_uint16]; L.or_half_to_float.restype = f32
+            L.or_encode.argtypes = [p, i64, i32, i32, i32, i32, p, p]
+            L.or_reconstruct.argtypes = [p, i64, i32, i32, i32, i32, p, p]
+            L.or_scale_exponent.argtypes = [f32]; L.or_scale_exponent.restype = i32
+            L.or_table.argtypes = [p, i32, i32, i32, i32, i32, p, p, p, p]
+            L.or_scores.argtypes = [p, p, i64, i64, i32, i32, p]
+            L.or_resident_scores.argtypes = [p, p, i64, i32, i32, p]
+            L.or_kappa.argtypes = [i32, i32]; L.or_kappa.restype = f32
+            L.or_exp2_poly.argtypes = [f32]; L.or_exp2_poly.restype = f32
+            L.or_mass.argtypes = [C.c_uint32, f32]; L.or_mass.restype = C.c_uint64
+            L.or_threshold.argtypes = [C.c_uint32, C.c_uint64]; L.or_threshold.restype = C.c_uint64
+            L.or_tau_q.argtypes = [f32]; L.or_tau_q.restype = C.c_uint32
+            L.or_select.argtypes = [p, i64, i32, i32, f32, i64, i32, p, p, p, p, p, p]
+            L.or_select.restype = i32
+            L.or_select_float.argtypes = [p, i64, i32, f32, i64, i32, p, p, p]
+            L.or_select_float.restype = i32
+            L.or_gather.argtypes = [p, p, i64, p, i32, p]
+            L.or_exact_attention.argtypes = [p, p, p, i64, i32, p]
+            L.or_decode_unit.argtypes = [p, i32, i32, i32, i32, i32, p, p, i64, i64, p, p, p, i64,
+                                         f32, i64, i32, p, p, p, p, p, p, p, p, p]
+            L.or_decode_unit.restype = i32
+            _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def encode(keys, C_, g: int) -> np.ndarray:
+    """keys fp16 [rows][d], C fp32 [cbg][c][dbar] -> codes uint16 [rows][g] (R1)."""
+    keys = _c(keys, np.float16); C_ = _c(C_, np.float32)
+    rows, d = keys.shape
+    cbg, c, dbar = C_.shape
+    assert dbar * g == d
+    out = np.empty((rows, g), dtype=np.uint16)
+    lib().or_encode(_ptr(keys.view(np.uint16)), rows, d, g, c, cbg, _ptr(C_), _ptr(out))
+    return out
+
+
+def reconstruct(codes, C_, d: int) -> np.ndarray:
+    codes = _c(codes, np.uint16); C_ = _c(C_, np.float32)
+    n, g = codes.shape
+    cbg, c, dbar = C_.shape
+    out = np.empty((n, d), dtype=np.float32)
+    lib().or_reconstruct(_ptr(codes), n, d, g, c, cbg, _ptr(C_), _ptr(out))
+    return out
+
+
+def table(q, C_, g: int):
+    """q fp16 [G][d] -> (T32 fp32 [G][g][c], Tfx int16 [G][g][c], e int32 [G]) (R2)."""
+    q = _c(q, np.float16); C_ = _c(C_, np.float32)
+    G, d = q.shape
+    cbg, c, dbar = C_.shape
+    T32 = np.empty((G, g, c), dtype=np.float32)
+    Tfx = np.empty((G, g, c), dtype=np.int16)
+    e = np.empty(G, dtype=np.int32)
+    lib().or_table(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(T32), _ptr(Tfx), _ptr(e))
+    return T32, Tfx, e
+
+
+def scores(Tfx_head, P_groupmajor, n: int) -> np.ndarray:
+    """Eq. 3: Tfx [g][c] int16, P [g][stride] uint16 -> z int32 [n]."""
+    T = _c(Tfx_head, np.int16); P = _c(P_groupmajor, np.uint16)
+    g, c = T.shape
+    z = np.empty(n, dtype=np.int32)
+    lib().or_scores(_ptr(T), _ptr(P), n, P.shape[1], g, c, _ptr(z))
+    return z
+
+
+def resident_scores(q_head, rk, e_h: int) -> np.ndarray:
+    q = _c(q_head, np.float16); rk = _c(rk, np.float16)
+    z = np.empty(rk.shape[0], dtype=np.int32)
+    lib().or_resident_scores(_ptr(q.view(np.uint16)), _ptr(rk.view(np.uint16)), rk.shape[0],
+                             q.shape[0], e_h, _ptr(z))
+    return z
+
+
+def scale_exponent(A: float) -> int:
+    return lib().or_scale_exponent(A)
+
+
+def kappa(d: int, e_h: int) -> float:
+    return lib().or_kappa(d, e_h)
+
+
+def exp2_poly(f: float) -> float:
+    return lib().or_exp2_poly(f)
+
+
+def mass(delta: int, kap: float) -> int:
+    return lib().or_mass(delta, kap)
+
+
+def threshold(tau_q: int, S: int) -> int:
+    return lib().or_threshold(tau_q, S)
+
+
+def tau_q(tau: float) -> int:
+    return lib().or_tau_q(tau)
+
+
+def select(z, e_h: int, d: int, tau: float, k_max: int, renorm: int = 0):
+    """Eq. 4 on int32 fixed-point scores -> dict(idx, w, k_sel, S, M, kstar)."""
+    z = _c(z, np.int32)
+    n = z.shape[0]
+    idx = np.empty(max(k_max, 1), dtype=np.int32)
+    w = np.empty(max(k_max, 1), dtype=np.float64)
+    ks = np.zeros(1, np.int64); S = np.zeros(1, np.uint64); M = np.zeros(1, np.int32)
+    kst = np.zeros(1, np.int64)
+    rc = lib().or_select(_ptr(z), n, e_h, d, tau, k_max, renorm, _ptr(idx), _ptr(w), _ptr(ks),
+                         _ptr(S), _ptr(M), _ptr(kst))
+    if rc:
+        raise ValueError(f"or_select rc={rc}")
+    k = int(ks[0])
+    return dict(idx=idx[:k].copy(), w=w[:k].copy(), k_sel=k, S=int(S[0]), M=int(M[0]), kstar=int(kst[0]))
+
+
+def select_float(zf, d: int, tau: float, k_max: int, renorm: int = 0):
+    zf = _c(zf, np.float32)
+    n = zf.shape[0]
+    idx = np.empty(max(k_max, 1), dtype=np.int32)
+    w = np.empty(max(k_max, 1), dtype=np.float64)
+    ks = np.zeros(1, np.int64)
+    rc = lib().or_select_float(_ptr(zf), n, d, tau, k_max, renorm, _ptr(idx), _ptr(w), _ptr(ks))
+    if rc:
+        raise ValueError(f"or_select_float rc={rc}")
+    k = int(ks[0])
+    return dict(idx=idx[:k].copy(), w=w[:k].copy(), k_sel=k)
+
+
+def gather(idx, w, V) -> np.ndarray:
+    idx = _c(idx, np.int32); w = _c(w, np.float64); V = _c(V, np.float16)
+    out = np.empty(V.shape[1], dtype=np.float64)
+    lib().or_gather(_ptr(idx), _ptr(w), idx.shape[0], _ptr(V.view(np.uint16)), V.shape[1], _ptr(out))
+    return out
+
+
+def exact_attention(q_head, K, V) -> np.ndarray:
+    """Eq. 1 in double."""
+    q = _c(q_head, np.float16); K = _c(K, np.float16); V = _c(V, np.float16)
+    out = np.empty(K.shape[1], dtype=np.float64)
+    lib().or_exact_attention(_ptr(q.view(np.uint16)), _ptr(K.view(np.uint16)), _ptr(V.view(np.uint16)),
+                             K.shape[0], K.shape[1], _ptr(out))
+    return out
+
+
+def decode_unit(q, C_, P_groupmajor, nq: int, V, tau: float, k_max: int, renorm: int = 0,
+                rk=None, rv=None):
+    """Full decode of one (b, l, kv) unit for its G query heads (R2->R6)."""
+    q = _c(q, np.float16); C_ = _c(C_, np.float32); P = _c(P_groupmajor, np.uint16)
+    V = _c(V, np.float16)
+    G, d = q.shape
+    cbg, c, dbar = C_.shape
+    g = d // dbar
+    nres = 0 if rk is None else rk.shape[0]
+    if rk is None:
+        rk = np.zeros((1, d), np.float16); rv = np.zeros((1, d), np.float16)
+    rk = _c(rk, np.float16); rv = _c(rv, np.float16)
+    n = nq + nres
+    z = np.empty((G, max(n, 1)), np.int32)
+    e = np.empty(G, np.int32)
+    km = max(k_max, 1)
+    idx = np.empty((G, km), np.int32); w = np.empty((G, km), np.float64)
+    ks = np.empty(G, np.int64); S = np.empty(G, np.uint64); M = np.empty(G, np.int32)
+    kst = np.empty(G, np.int64); out = np.empty((G, d), np.float64)
+    rc = lib().or_decode_unit(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(P), nq,
+                              P.shape[1], _ptr(V.view(np.uint16)), _ptr(rk.view(np.uint16)),
+                              _ptr(rv.view(np.uint16)), nres, tau, k_max, renorm, _ptr(z), _ptr(e),
+                              _ptr(idx), _ptr(w), _ptr(ks), _ptr(S), _ptr(M), _ptr(kst), _ptr(out))
+    if rc:
+        raise ValueError(f"or_decode_unit rc={rc}")
+    return dict(z=z[:, :n], e=e, idx=[idx[h, :ks[h]].copy() for h in range(G)],
+                w=[w[h, :ks[h]].copy() for h in range(G)], k_sel=ks, S=S, M=M, kstar=kst, out=out)

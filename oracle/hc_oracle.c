@@ -1,0 +1,434 @@
+/*
+ * oracle/hc_oracle.c -- plain, slow, obviously-correct CPU reference of the
+ * HCAttention decode hot path (arXiv 2507.19823, §3.2 "Heterogeneous
+ * Attention Computation", Eqs. 1-5).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * (paper_2507_19823_b200/csrc).  Citations: "P:n" = line n of
+ * /root/reference/PAPER.md; "R<k>" = the numbered reading in DESIGN.md §2.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC (no fast-math), so
+ * every float operation below is one IEEE-754 binary32 operation, in the
+ * order written.  fmaf() is the correctly-rounded fused multiply-add.
+ *
+ * Parity status: every function is pinned by tests/test_oracle_pins.py
+ * except or_decode_unit's absolute accuracy at tau<1 ("parity unpinned",
+ * DESIGN.md C-P10 -- the paper prints no numbers for it).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_EXPORT __attribute__((visibility("default")))
+
+/* IEEE binary16 -> binary32, exact (bit-level). */
+static float or_h2f(uint16_t h)
+{
+    uint32_t sign = (uint32_t)(h >> 15) << 31;
+    uint32_t exp = (h >> 10) & 0x1f;
+    uint32_t man = h & 0x3ff;
+    uint32_t bits;
+    if (exp == 0) {
+        if (man == 0) {
+            bits = sign;
+        } else { /* subnormal: value = man * 2^-24 */
+            float v = (float)man * 0x1p-24f;
+            memcpy(&bits, &v, 4);
+            bits |= sign;
+        }
+    } else if (exp == 31) {
+        bits = sign | 0x7f800000u | (man << 13);
+    } else {
+        bits = sign | ((exp + 112u) << 23) | (man << 13);
+    }
+    float f;
+    memcpy(&f, &bits, 4);
+    return f;
+}
+
+OR_EXPORT float or_half_to_float(uint16_t h) { return or_h2f(h); }
+
+/* ------------------------------------------------------------------------
+ * R1 -- key encoding.  P:227 (§3.2): "Each sub-group is represented as nearest
+ * neighbor of the centroids in the codebook ... an index matrix P".  Metric
+ * unstated -> squared Euclidean; ties -> lowest centroid index (DESIGN R1).
+ *   dist = 0; for e: diff = k[e] - C[m][e]; dist = fmaf(diff, diff, dist)
+ *   code = argmin_m dist, strict '<' in ascending m.
+ * keys [rows][d] fp16; C [cbg][c][dbar] fp32; codes out row-major [rows][g].
+ * ---------------------------------------------------------------------- */
+OR_EXPORT void or_encode(const uint16_t *keys, int64_t rows, int d, int g, int c, int cbg,
+                         const float *C, uint16_t *codes)
+{
+    const int dbar = d / g;
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r) {
+        for (int i = 0; i < g; ++i) {
+            const float *Ci = C + (size_t)(cbg == 1 ? 0 : i) * c * dbar;
+            float kbar[64];
+            for (int e = 0; e < dbar; ++e) kbar[e] = or_h2f(keys[r * d + i * dbar + e]);
+            int best = 0;
+            float best_dist = 0.0f;
+            for (int m = 0; m < c; ++m) {
+                float dist = 0.0f;
+                for (int e = 0; e < dbar; ++e) {
+                    float diff = kbar[e] - Ci[(size_t)m * dbar + e];
+                    dist = fmaf(diff, diff, dist);
+                }
+                if (m == 0 || dist < best_dist) {
+                    best_dist = dist;
+                    best = m;
+                }
+            }
+            codes[r * g + i] = (uint16_t)best;
+        }
+    }
+}
+
+/* Eq. 2 Q(K): row j = concat_i C[i][P[j][i]]. codes [n][g] row-major. */
+OR_EXPORT void or_reconstruct(const uint16_t *codes, int64_t n, int d, int g, int c, int cbg,
+                              const float *C, float *out)
+{
+    const int dbar = d / g;
+    for (int64_t j = 0; j < n; ++j)
+        for (int i = 0; i < g; ++i) {
+            const float *Ci = C + (size_t)(cbg == 1 ? 0 : i) * c * dbar;
+            for (int e = 0; e < dbar; ++e)
+                out[j * d + i * dbar + e] = Ci[(size_t)codes[j * g + i] * dbar + e];
+        }
+}
+
+/* ------------------------------------------------------------------------
+ * R2 -- query/codebook table.  P:229: "T = q̄·C where T ∈ R^{g×c}".
+ *   t = q[i*dbar]*C[i][m][0]; t = fmaf(q[i*dbar+e], C[i][m][e], t), e=1..dbar-1
+ * Fixed-point storage (DESIGN R2): A = max |t| over the head's whole table;
+ *   e_h = 100 if A < 2^-100 else clamp(14 - floor(log2 A), -100, 100);
+ *   T_fx = clamp(rint(t * 2^e_h), -32767, 32767)   (rint = ties-to-even).
+ * q [G][d] fp16 -> T32 [G][g][c] fp32 (may be NULL), Tfx [G][g][c] int16, e [G].
+ * ---------------------------------------------------------------------- */
+static float or_pow2f(int e) /* exact 2^e for -126 <= e <= 127 */
+{
+    uint32_t bits = (uint32_t)(e + 127) << 23;
+    float f;
+    memcpy(&f, &bits, 4);
+    return f;
+}
+
+OR_EXPORT int or_scale_exponent(float A)
+{
+    if (!(A >= 0x1p-100f)) return 100;
+    int ex;
+    (void)frexpf(A, &ex); /* A = f * 2^ex, f in [0.5, 1) -> floor(log2 A) = ex - 1 */
+    int e = 14 - (ex - 1);
+    if (e < -100) e = -100;
+    if (e > 100) e = 100;
+    return e;
+}
+
+OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
+                        float *T32, int16_t *Tfx, int32_t *e_out)
+{
+    const int dbar = d / g;
+    float *t = (float *)malloc(sizeof(float) * (size_t)g * c);
+    for (int h = 0; h < G; ++h) {
+        float A = 0.0f;
+        for (int i = 0; i < g; ++i) {
+            const float *Ci = C + (size_t)(cbg == 1 ? 0 : i) * c * dbar;
+            for (int m = 0; m < c; ++m) {
+                float acc = or_h2f(q[h * d + i * dbar]) * Ci[(size_t)m * dbar];
+                for (int e = 1; e < dbar; ++e)
+                    acc = fmaf(or_h2f(q[h * d + i * dbar + e]), Ci[(size_t)m * dbar + e], acc);
+                t[(size_t)i * c + m] = acc;
+                float a = fabsf(acc);
+                if (a > A) A = a;
+            }
+        }
+        int e_h = or_scale_exponent(A);
+        float s = or_pow2f(e_h);
+        for (size_t k = 0; k < (size_t)g * c; ++k) {
+            float v = rintf(t[k] * s);
+            if (v > 32767.0f) v = 32767.0f;
+            if (v < -32767.0f) v = -32767.0f;
+            Tfx[(size_t)h * g * c + k] = (int16_t)v;
+            if (T32) T32[(size_t)h * g * c + k] = t[k];
+        }
+        e_out[h] = e_h;
+    }
+    free(t);
+}
+
+/* ------------------------------------------------------------------------
+ * R3 -- approximate scores, Eq. 3: z̃_j = Σ_{i=1..g} T_{i,P_{j,i}}.
+ * Integer (exact) sum of the fixed-point table entries.  P is group-major:
+ * P[i*stride + j].  Tfx for ONE head [g][c].
+ * ---------------------------------------------------------------------- */
+OR_EXPORT void or_scores(const int16_t *Tfx, const uint16_t *P, int64_t n, int64_t stride, int g,
+                         int c, int32_t *z)
+{
+    for (int64_t j = 0; j < n; ++j) {
+        int32_t acc = 0;
+        for (int i = 0; i < g; ++i) acc += Tfx[(size_t)i * c + P[(size_t)i * stride + j]];
+        z[j] = acc;
+    }
+}
+
+/* Resident (unquantized recent-window) tokens score exactly (SPEC S:449,
+ * DESIGN R3b): acc = fmaf chain over e = 0..d-1; then onto the same grid:
+ *   z_fx = rint(clamp(acc * 2^e_h, -2^22, 2^22)). */
+OR_EXPORT void or_resident_scores(const uint16_t *q, const uint16_t *rk, int64_t nres, int d,
+                                  int e_h, int32_t *z)
+{
+    float s = or_pow2f(e_h);
+    for (int64_t r = 0; r < nres; ++r) {
+        float acc = 0.0f;
+        for (int e = 0; e < d; ++e) acc = fmaf(or_h2f(q[e]), or_h2f(rk[r * d + e]), acc);
+        float v = acc * s;
+        if (v > 4194304.0f) v = 4194304.0f;
+        if (v < -4194304.0f) v = -4194304.0f;
+        z[r] = (int32_t)rintf(v);
+    }
+}
+
+/* ------------------------------------------------------------------------
+ * R4 -- normalisation ã = softmax(z̃/√d) as exact fixed-point mass.
+ *   kappa_h = fp32(log2(e)/sqrt(d)) * 2^-e_h
+ *   x = -(float)Δ * kappa_h, Δ = M - z_j
+ *   exp2_det(x): x < -40 -> W = 0; n = floor(x); f = x - n;
+ *                p = Horner(c6..c0, f) with fmaf;  W = trunc(p * 2^(40+n))
+ *   ã_j = W_j / S,  S = Σ_j W_j  (uint64, exact).
+ * Coefficients: degree-6 fit of 2^f on [0,1), DESIGN R4 (max rel err 6.2e-8).
+ * ---------------------------------------------------------------------- */
+OR_EXPORT float or_kappa(int d, int e_h)
+{
+    float k0 = (float)(1.4426950408889634 / sqrt((double)d));
+    return k0 * or_pow2f(-e_h);
+}
+
+OR_EXPORT float or_exp2_poly(float f)
+{
+    const float c0 = 0x1.000000p+0f, c1 = 0x1.62e42ap-1f, c2 = 0x1.ebfd9ap-3f,
+                c3 = 0x1.c68562p-5f, c4 = 0x1.3d24eap-7f, c5 = 0x1.46301cp-10f,
+                c6 = 0x1.c6e292p-13f;
+    float p = c6;
+    p = fmaf(p, f, c5);
+    p = fmaf(p, f, c4);
+    p = fmaf(p, f, c3);
+    p = fmaf(p, f, c2);
+    p = fmaf(p, f, c1);
+    p = fmaf(p, f, c0);
+    return p;
+}
+
+OR_EXPORT uint64_t or_mass(uint32_t delta, float kappa)
+{
+    float x = -((float)delta * kappa);
+    if (x < -40.0f) return 0;
+    float nf = floorf(x);
+    float f = x - nf;
+    float p = or_exp2_poly(f);
+    float v = p * or_pow2f(40 + (int)nf);
+    return (uint64_t)v; /* truncation toward zero */
+}
+
+/* ------------------------------------------------------------------------
+ * R5 -- cumulative-magnitude eviction, Eq. 4:
+ *   sort ã descending (ties: lower index first, DESIGN R5);
+ *   k* = min{k : Σ_{r<=k} a_(r) >= τ}  evaluated exactly as
+ *        Σ_{r<=k} W_(r) >= Θ,  Θ = ceil(τ_q·S / 2^24), τ_q = rint(τ·2^24);
+ *   τ_q >= 2^24 (τ = 1) -> k* = n;   k_sel = min(k*, k_max).
+ * Outputs idx ascending, weights W_j/S (renorm: W_j / Σ_sel W).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    uint32_t delta;
+    int64_t j;
+} or_item;
+
+static int or_cmp(const void *a, const void *b)
+{
+    const or_item *x = (const or_item *)a, *y = (const or_item *)b;
+    if (x->delta != y->delta) return x->delta < y->delta ? -1 : 1;
+    return x->j < y->j ? -1 : (x->j > y->j ? 1 : 0);
+}
+
+static int or_cmp_i64(const void *a, const void *b)
+{
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+OR_EXPORT uint64_t or_threshold(uint32_t tau_q, uint64_t S)
+{
+    unsigned __int128 p = (unsigned __int128)tau_q * (unsigned __int128)S;
+    p += ((unsigned __int128)1 << 24) - 1;
+    return (uint64_t)(p >> 24);
+}
+
+OR_EXPORT uint32_t or_tau_q(float tau) { return (uint32_t)rint((double)tau * 16777216.0); }
+
+/* z [n] int32 fixed-point scores of one head (quantized then resident). */
+OR_EXPORT int or_select(const int32_t *z, int64_t n, int e_h, int d, float tau, int64_t k_max,
+                        int renorm, int32_t *idx_out, double *w_out, int64_t *k_sel_out,
+                        uint64_t *S_out, int32_t *M_out, int64_t *kstar_out)
+{
+    if (n <= 0) return 5;
+    int32_t M = z[0];
+    for (int64_t j = 1; j < n; ++j)
+        if (z[j] > M) M = z[j];
+    float kappa = or_kappa(d, e_h);
+    or_item *it = (or_item *)malloc(sizeof(or_item) * (size_t)n);
+    uint64_t S = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        it[j].delta = (uint32_t)((int64_t)M - (int64_t)z[j]);
+        it[j].j = j;
+        S += or_mass(it[j].delta, kappa);
+    }
+    qsort(it, (size_t)n, sizeof(or_item), or_cmp);
+    uint32_t tq = or_tau_q(tau);
+    int64_t kstar;
+    if (tq >= 16777216u) {
+        kstar = n;
+    } else {
+        uint64_t theta = or_threshold(tq, S);
+        uint64_t cum = 0;
+        kstar = n;
+        for (int64_t k = 1; k <= n; ++k) {
+            cum += or_mass(it[k - 1].delta, kappa);
+            if (cum >= theta) {
+                kstar = k;
+                break;
+            }
+        }
+    }
+    int64_t ksel = kstar < k_max ? kstar : k_max;
+    int64_t *sel = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ksel > 0 ? ksel : 1));
+    uint64_t selmass = 0;
+    for (int64_t k = 0; k < ksel; ++k) {
+        sel[k] = it[k].j;
+        selmass += or_mass(it[k].delta, kappa);
+    }
+    qsort(sel, (size_t)ksel, sizeof(int64_t), or_cmp_i64);
+    double denom = renorm ? (double)selmass : (double)S;
+    for (int64_t k = 0; k < ksel; ++k) {
+        idx_out[k] = (int32_t)sel[k];
+        uint64_t W = or_mass((uint32_t)((int64_t)M - (int64_t)z[sel[k]]), kappa);
+        w_out[k] = (double)W / denom;
+    }
+    *k_sel_out = ksel;
+    if (S_out) *S_out = S;
+    if (M_out) *M_out = M;
+    if (kstar_out) *kstar_out = kstar;
+    free(sel);
+    free(it);
+    return 0;
+}
+
+/* Standalone selection on real-valued scores (hc_select_topk's input), DESIGN
+ * R5b: A = max|z|; e = 100 if A < 2^-100 else clamp(22 - floor(log2 A) - 1, -100,
+ * 100) so |z·2^e| < 2^22; z_fx = rint(clamp(z·2^e, ±2^22)); then or_select. */
+OR_EXPORT int or_select_float(const float *zf, int64_t n, int d, float tau, int64_t k_max,
+                              int renorm, int32_t *idx_out, double *w_out, int64_t *k_sel_out)
+{
+    if (n <= 0) return 5;
+    float A = 0.0f;
+    for (int64_t j = 0; j < n; ++j)
+        if (fabsf(zf[j]) > A) A = fabsf(zf[j]);
+    int e = 100;
+    if (A >= 0x1p-100f) {
+        int ex;
+        (void)frexpf(A, &ex);
+        e = 21 - (ex - 1);
+        if (e < -100) e = -100;
+        if (e > 100) e = 100;
+    }
+    float s = or_pow2f(e);
+    int32_t *z = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) {
+        float v = zf[j] * s;
+        if (v > 4194304.0f) v = 4194304.0f;
+        if (v < -4194304.0f) v = -4194304.0f;
+        z[j] = (int32_t)rintf(v);
+    }
+    int rc = or_select(z, n, e, d, tau, k_max, renorm, idx_out, w_out, k_sel_out, 0, 0, 0);
+    free(z);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------
+ * R6 -- sparse weighted sum, Eq. 5: ỹ = Σ_{i∈Π_k*} ã*_i V_i,
+ * accumulated in double, in ascending-index order.  V rows fp16 [*][d].
+ * ---------------------------------------------------------------------- */
+OR_EXPORT void or_gather(const int32_t *idx, const double *w, int64_t k, const uint16_t *V, int d,
+                         double *out)
+{
+    for (int e = 0; e < d; ++e) out[e] = 0.0;
+    for (int64_t r = 0; r < k; ++r)
+        for (int e = 0; e < d; ++e) out[e] += w[r] * (double)or_h2f(V[(size_t)idx[r] * d + e]);
+}
+
+/* Eq. 1: exact attention y = softmax(q·Kᵀ/√d)·V in double. */
+OR_EXPORT void or_exact_attention(const uint16_t *q, const uint16_t *K, const uint16_t *V, int64_t n,
+                                  int d, double *out)
+{
+    double *z = (double *)malloc(sizeof(double) * (size_t)n);
+    double M = -INFINITY;
+    for (int64_t j = 0; j < n; ++j) {
+        double acc = 0.0;
+        for (int e = 0; e < d; ++e) acc += (double)or_h2f(q[e]) * (double)or_h2f(K[j * d + e]);
+        z[j] = acc / sqrt((double)d);
+        if (z[j] > M) M = z[j];
+    }
+    double S = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        z[j] = exp(z[j] - M);
+        S += z[j];
+    }
+    for (int e = 0; e < d; ++e) out[e] = 0.0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int e = 0; e < d; ++e) out[e] += (z[j] / S) * (double)or_h2f(V[j * d + e]);
+    free(z);
+}
+
+/* ------------------------------------------------------------------------
+ * One decode unit (batch b, layer l, KV head kv) for its G GQA query heads
+ * (head h of the unit uses KV head kv, DESIGN R7), steps R2 -> R6 in the
+ * paper's order.  Candidates j in [0, nq) are quantized (codes P, group-major,
+ * stride), j in [nq, nq+nres) are resident exact tokens (rk, rv).
+ * V [nq][d] fp16 holds the offloaded values of the quantized tokens.
+ * Outputs per head h: z [G][nq+nres], e [G], idx [G][k_max], w [G][k_max],
+ * k_sel [G], S [G], M [G], kstar [G], out [G][d] (double).
+ * ---------------------------------------------------------------------- */
+OR_EXPORT int or_decode_unit(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
+                             const uint16_t *P, int64_t nq, int64_t stride, const uint16_t *V,
+                             const uint16_t *rk, const uint16_t *rv, int64_t nres, float tau,
+                             int64_t k_max, int renorm, int32_t *z, int32_t *e_out,
+                             int32_t *idx, double *w, int64_t *k_sel, uint64_t *S, int32_t *M,
+                             int64_t *kstar, double *out)
+{
+    int64_t n = nq + nres;
+    if (n <= 0) return 5;
+    int16_t *Tfx = (int16_t *)malloc(sizeof(int16_t) * (size_t)G * g * c);
+    or_table(q, G, d, g, c, cbg, C, NULL, Tfx, e_out);
+    for (int h = 0; h < G; ++h) {
+        int32_t *zh = z + (size_t)h * n;
+        or_scores(Tfx + (size_t)h * g * c, P, nq, stride, g, c, zh);
+        if (nres > 0) or_resident_scores(q + (size_t)h * d, rk, nres, d, e_out[h], zh + nq);
+        int rc = or_select(zh, n, e_out[h], d, tau, k_max, renorm, idx + (size_t)h * k_max,
+                           w + (size_t)h * k_max, k_sel + h, S + h, M + h, kstar + h);
+        if (rc) {
+            free(Tfx);
+            return rc;
+        }
+        double *oh = out + (size_t)h * d;
+        for (int e = 0; e < d; ++e) oh[e] = 0.0;
+        for (int64_t r = 0; r < k_sel[h]; ++r) {
+            int64_t j = idx[(size_t)h * k_max + r];
+            const uint16_t *row = j < nq ? V + (size_t)j * d : rv + (size_t)(j - nq) * d;
+            double wr = w[(size_t)h * k_max + r];
+            for (int e = 0; e < d; ++e) oh[e] += wr * (double)or_h2f(row[e]);
+        }
+    }
+    free(Tfx);
+    return 0;
+}
