@@ -1,0 +1,161 @@
+/*
+ * hc.h -- C ABI of the B200 (sm_100a) HCAttention decode hot path (libhc.so).
+ *
+ * HCAttention (arXiv 2507.19823) §3.2 "Heterogeneous Attention Computation":
+ * keys are grouped-vector quantized, scores are table
+ * lookups z̃_j = Σ_i T[i][P_ji] with T = q̄·C (Eq. 3), ã =
+ * softmax(z̃/√d), tokens are selected by cumulative mass τ (Eq. 4,
+ * P:240-252) and the output is Σ_{i∈Π_k*} ã*_i V_i (Eq. 5).
+ * Citations "P:n" are lines of PAPER.md; "R<k>" are DESIGN.md §2 readings.
+ *
+ * Conventions (all entry points):
+ *  - Tensors are caller-owned.  Pointers are DEVICE pointers unless stated;
+ *    fp16 tensors are passed as uint16_t* (IEEE binary16 bit patterns).
+ *  - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default)
+ *    and never allocate or synchronise; they are CUDA-graph capturable.
+ *  - Argument validation is synchronous: a non-HC_OK status is returned and
+ *    nothing is launched; hc_last_error() gives a one-line reason (thread-local).
+ *    Asynchronous CUDA faults surface as HC_ERR_CUDA from a later call.
+ *  - Layouts are row-major, innermost index last.
+ */
+#ifndef HC_H_
+#define HC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HC_OK = 0,
+    HC_ERR_ARG = 1,         /* bad scalar argument (tau outside (0,1], k_max < 1, NULL ptr) */
+    HC_ERR_SHAPE = 2,       /* dimension mismatch (g does not divide d, ...) */
+    HC_ERR_RANGE = 3,       /* index / layer / value out of range */
+    HC_ERR_CAPACITY = 4,    /* append beyond n_cap */
+    HC_ERR_EMPTY = 5,       /* no candidates (n_q + n_res == 0) */
+    HC_ERR_CUDA = 6,        /* a CUDA runtime error (launch or earlier async fault) */
+    HC_ERR_NCCL = 7,        /* reserved for the sequence-sharded path */
+    HC_ERR_UNSUPPORTED = 8, /* valid but not built for (e.g. c > 8192, G not in {1,2,4}) */
+    HC_ERR_WORKSPACE = 9    /* workspace NULL or smaller than *_workspace_bytes() */
+} hc_status;
+
+typedef void *hc_stream_t; /* cudaStream_t */
+
+/* Grouped vector quantizer (§3.1): d-dim keys split into g groups of
+ * dbar = d/g dims; c centroids per codebook slice; cbg codebook slices
+ * (cbg == g: one codebook per group as C ∈ R^{g×c×dbar}; cbg == 1: one
+ * codebook shared by all groups, Table 4b).
+ * Supported by the kernels: d % g == 0, dbar in {1,2,4,8,16}, 1 <= c <= 8192. */
+typedef struct {
+    int32_t d, g, c, cbg;
+} hc_vq;
+
+/* Budget (R5): tau ∈ (0,1] is Eq. 4's cumulative-mass threshold (τ = 0.9 in
+ * §4.1); k_max >= 1 caps the kept set: k_sel = min(k*(τ), k_max);
+ * renorm = 0 keeps Eq. 5's unrenormalised ã* (default), 1 divides by the kept mass. */
+typedef struct {
+    float tau;
+    int64_t k_max;
+    int32_t renorm;
+} hc_budget;
+
+#define HC_MAX_LAYERS 256
+
+/* Quantized key cache of one model (all layers).  Host struct; device buffers.
+ *  codes    [B][L][Hkv][g][n_cap] uint16, GROUP-MAJOR (the index matrix P of P:227,
+ *           0-based, one contiguous strip per (b,l,kv,group)); n_cap % 64 == 0.
+ *  codebook [L][cbg][c][dbar] fp32 (one codebook set per layer, shared by its KV heads).
+ *  Recent window (R7, optional, res_cap = W >= 0): the newest n_res[l] <= W tokens keep
+ *  exact keys/values resident: res_k/res_v [B][L][Hkv][W][d] fp16, token at global
+ *  position p lives in slot p % W.  Candidates of a layer are the quantized tokens
+ *  0..n_q-1 followed by the resident tokens n_q..n_q+n_res-1.
+ *  n_q[l], n_res[l] are host-side counts, advanced by hc_append_kv. */
+typedef struct {
+    int32_t B, L, Hkv, G; /* batch, layers, KV heads, GQA group size (Hq = G*Hkv) */
+    hc_vq vq;
+    int64_t n_cap;
+    uint16_t *codes;
+    const float *codebook;
+    int32_t res_cap;
+    uint16_t *res_k;
+    uint16_t *res_v;
+    int64_t n_q[HC_MAX_LAYERS];
+    int32_t n_res[HC_MAX_LAYERS];
+} hc_kcache;
+
+/* Value store (A8, "fully offloading the value matrix V").
+ *  base [B][L][Hkv][n_cap][d] fp16.  placement HC_V_DEVICE: HBM pointer.
+ *  HC_V_HOST_MAPPED: pinned host memory mapped into the device address space
+ *  (cudaHostAlloc Mapped/Portable or cudaHostRegister Mapped), passed as its
+ *  device-accessible address; rows are read zero-copy over the host link by the
+ *  gather kernel, only the selected ones. */
+enum { HC_V_DEVICE = 0, HC_V_HOST_MAPPED = 1 };
+typedef struct {
+    int32_t placement;
+    uint16_t *base;
+    int64_t n_cap;
+} hc_vstore;
+
+/* Optional debug taps of hc_decode_attention (any member may be NULL).
+ *  z     [B][Hq][n_q+n_res] int32  fixed-point scores z̃ (R3), scale 2^-e
+ *  e     [B][Hq] int32             table scale exponents (R2)
+ *  S     [B][Hq] uint64            total mass Σ W (R4)
+ *  M     [B][Hq] int32             max score
+ *  kstar [B][Hq] int64             k*(τ) when τ decides the cut, -1 when the cap does */
+typedef struct {
+    int32_t *z;
+    int32_t *e;
+    uint64_t *S;
+    int32_t *M;
+    int64_t *kstar;
+} hc_decode_debug;
+
+const char *hc_last_error(void);
+const char *hc_version(void);
+
+/* Key encoding, R1 ("represented as nearest neighbor of the centroids"):
+ *   codes[i*code_stride + r] = argmin_m ||keys[r][i*dbar:(i+1)*dbar] - C[ci][m]||², ties -> lowest m.
+ * keys [rows][d] fp16; codebook [cbg][c][dbar] fp32 (ONE layer's codebook);
+ * codes uint16 group-major with code_stride >= rows.  rows == 0 is a no-op. */
+hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *codebook, hc_vq vq,
+                           uint16_t *codes, int64_t code_stride, hc_stream_t stream);
+
+/* Append one decode token for layer `layer` (all B sequences, all Hkv heads).
+ * k_new, v_new [B][Hkv][d] fp16.  With res_cap == 0 the key is encoded (R1) into
+ * codes at position n_q[layer] and v is written to the value store there.  With a
+ * window, the token enters the window; if it was full, the oldest resident token is
+ * encoded into P and its value moved to the value store first.
+ * Advances kc->n_q[layer] / kc->n_res[layer].  HC_ERR_CAPACITY if n_q would exceed n_cap. */
+hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const uint16_t *k_new,
+                       const uint16_t *v_new, hc_stream_t stream);
+
+/* Bytes of device workspace hc_decode_attention needs for this cache shape
+ * (independent of the current n; sized for n_cap + res_cap). */
+size_t hc_decode_workspace_bytes(const hc_kcache *kc, hc_budget budget);
+
+/* One decode step of one layer for all B×Hq query heads (rows a1-a5):
+ *   q [B][Hq][d] fp16 (query head h uses KV head h / G)
+ *   out [B][Hq][d] fp32 = Σ_{j∈sel} ã_j V_j  (Eq. 5)
+ *   sel_idx [B][Hq][k_max] int32 (optional): kept global token indices, ascending
+ *   sel_w   [B][Hq][k_max] fp32  (optional): their weights ã_j
+ *   sel_k   [B][Hq] int64        (optional): k_sel
+ * HC_ERR_EMPTY if the layer has no tokens.  ws: >= hc_decode_workspace_bytes. */
+hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
+                              int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
+                              float *sel_w, int64_t *sel_k, const hc_decode_debug *dbg, void *ws,
+                              size_t ws_bytes, hc_stream_t stream);
+
+/* Standalone Eq. 4 selection on real-valued scores (R5b):
+ *   scores [rows][n] fp32 (z̃ = q·Kᵀ, unscaled; softmax uses 1/√d)
+ *   idx [rows][k_max] int32 ascending, w [rows][k_max] fp32, k [rows] int64. */
+size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget);
+hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d, hc_budget budget,
+                         int32_t *idx, float *w, int64_t *k, void *ws, size_t ws_bytes,
+                         hc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HC_H_ */

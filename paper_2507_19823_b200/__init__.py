@@ -1,0 +1,261 @@
+"""hcattn-b200: B200-native (sm_100a) HCAttention decode hot path.
+
+Thin ctypes binding over the C ABI in include/hc.h (libhc.so, built in-tree by
+paper_2507_19823_b200/build.py).  Argument marshalling only: every stage of the
+path runs in our CUDA kernels.  PyTorch provides device / pinned memory and the
+stream.  There is NO CPU fallback: if libhc.so is missing, or no CUDA device is
+present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhc.so")
+MAX_LAYERS = 256
+
+HC_OK, HC_ERR_ARG, HC_ERR_SHAPE, HC_ERR_RANGE, HC_ERR_CAPACITY, HC_ERR_EMPTY, HC_ERR_CUDA, \
+    HC_ERR_NCCL, HC_ERR_UNSUPPORTED, HC_ERR_WORKSPACE = range(10)
+HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
+
+EXPORTS = ["hc_last_error", "hc_version", "hc_quantize_keys", "hc_append_kv",
+           "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
+           "hc_select_topk"]
+
+
+class HcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hc status {status}: {msg}")
+        self.status = status
+
+
+class hc_vq(C.Structure):
+    _fields_ = [("d", C.c_int32), ("g", C.c_int32), ("c", C.c_int32), ("cbg", C.c_int32)]
+
+
+class hc_budget(C.Structure):
+    _fields_ = [("tau", C.c_float), ("k_max", C.c_int64), ("renorm", C.c_int32)]
+
+
+class hc_kcache(C.Structure):
+    _fields_ = [("B", C.c_int32), ("L", C.c_int32), ("Hkv", C.c_int32), ("G", C.c_int32),
+                ("vq", hc_vq), ("n_cap", C.c_int64), ("codes", C.c_void_p),
+                ("codebook", C.c_void_p), ("res_cap", C.c_int32), ("res_k", C.c_void_p),
+                ("res_v", C.c_void_p), ("n_q", C.c_int64 * MAX_LAYERS),
+                ("n_res", C.c_int32 * MAX_LAYERS)]
+
+
+class hc_vstore(C.Structure):
+    _fields_ = [("placement", C.c_int32), ("base", C.c_void_p), ("n_cap", C.c_int64)]
+
+
+class hc_decode_debug(C.Structure):
+    _fields_ = [("z", C.c_void_p), ("e", C.c_void_p), ("S", C.c_void_p), ("M", C.c_void_p),
+                ("kstar", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhc.so; raise loudly if it was not built (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2507_19823_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        p, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+        L.hc_last_error.restype = C.c_char_p
+        L.hc_version.restype = C.c_char_p
+        L.hc_quantize_keys.argtypes = [p, i64, p, hc_vq, p, i64, p]
+        L.hc_quantize_keys.restype = i32
+        L.hc_append_kv.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, p]
+        L.hc_append_kv.restype = i32
+        L.hc_decode_workspace_bytes.argtypes = [C.POINTER(hc_kcache), hc_budget]
+        L.hc_decode_workspace_bytes.restype = C.c_size_t
+        L.hc_decode_attention.argtypes = [p, C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32,
+                                          hc_budget, p, p, p, p, C.POINTER(hc_decode_debug), p,
+                                          C.c_size_t, p]
+        L.hc_decode_attention.restype = i32
+        L.hc_select_workspace_bytes.argtypes = [i64, i64, hc_budget]
+        L.hc_select_workspace_bytes.restype = C.c_size_t
+        L.hc_select_topk.argtypes = [p, i64, i64, i32, hc_budget, p, p, p, p, C.c_size_t, p]
+        L.hc_select_topk.restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != HC_OK:
+        raise HcError(st, lib().hc_last_error().decode())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def version() -> str:
+    return lib().hc_version().decode()
+
+
+def budget(tau: float, k_max: int, renorm: bool = False) -> hc_budget:
+    return hc_budget(float(tau), int(k_max), int(bool(renorm)))
+
+
+# ----------------------------------------------------------------------------- encode
+def quantize_keys(keys, codebook, g: int, codes=None, stream=None):
+    """R1: keys fp16 [rows][d] (cuda), codebook fp32 [cbg][c][d/g]
+    -> codes int16-view-of-u16 [g][rows] (group-major)."""
+    import torch
+    rows, d = keys.shape
+    cbg, c, dbar = codebook.shape
+    if codes is None:
+        codes = torch.empty((g, max(rows, 1)), dtype=torch.int16, device=keys.device)
+    st = lib().hc_quantize_keys(_ptr(keys), rows, _ptr(codebook), hc_vq(d, g, c, cbg), _ptr(codes),
+                                codes.shape[1], _stream(stream))
+    _check(st)
+    return codes
+
+
+# ----------------------------------------------------------------------------- caches
+@dataclass
+class VStore:
+    """Value store [B][L][Hkv][n_cap][d] fp16, in HBM or host-pinned mapped memory."""
+    tensor: object           # torch fp16 tensor (cuda, or pinned cpu)
+    placement: int
+    n_cap: int
+
+    @staticmethod
+    def allocate(B, L, Hkv, n_cap, d, placement=HC_V_DEVICE, device="cuda"):
+        import torch
+        if placement == HC_V_DEVICE:
+            t = torch.empty((B, L, Hkv, n_cap, d), dtype=torch.float16, device=device)
+        else:
+            t = torch.empty((B, L, Hkv, n_cap, d), dtype=torch.float16, pin_memory=True)
+        return VStore(t, placement, n_cap)
+
+    def struct(self) -> hc_vstore:
+        ptr = self.tensor.data_ptr()
+        if self.placement == HC_V_HOST_MAPPED:
+            ptr = host_device_pointer(ptr)
+        return hc_vstore(self.placement, ptr, self.n_cap)
+
+
+def host_device_pointer(host_ptr: int) -> int:
+    """Device-accessible alias of pinned host memory.  With unified virtual addressing
+    (always on for 64-bit Linux + sm_100), memory from cudaHostAlloc / pin_memory is
+    mapped into every device's address space at the same address."""
+    return host_ptr
+
+
+class KCache:
+    """Quantized key cache of all layers (hc_kcache).  Device tensors:
+    codes [B][L][Hkv][g][n_cap] (u16 as int16), codebook [L][cbg][c][d/g] fp32,
+    optional recent window res_k/res_v [B][L][Hkv][W][d] fp16."""
+
+    def __init__(self, B, L, Hkv, G, d, g, c, n_cap, codebook, cbg=None, res_cap=0,
+                 codes=None, device="cuda"):
+        import torch
+        cbg = g if cbg is None else cbg
+        self.B, self.L, self.Hkv, self.G, self.d, self.g, self.c, self.cbg = B, L, Hkv, G, d, g, c, cbg
+        self.n_cap, self.res_cap = n_cap, res_cap
+        self.codebook = codebook
+        self.codes = codes if codes is not None else torch.zeros(
+            (B, L, Hkv, g, n_cap), dtype=torch.int16, device=device)
+        if res_cap > 0:
+            self.res_k = torch.zeros((B, L, Hkv, res_cap, d), dtype=torch.float16, device=device)
+            self.res_v = torch.zeros((B, L, Hkv, res_cap, d), dtype=torch.float16, device=device)
+        else:
+            self.res_k = self.res_v = None
+        s = hc_kcache()
+        s.B, s.L, s.Hkv, s.G = B, L, Hkv, G
+        s.vq = hc_vq(d, g, c, cbg)
+        s.n_cap = n_cap
+        s.codes = self.codes.data_ptr()
+        s.codebook = codebook.data_ptr()
+        s.res_cap = res_cap
+        s.res_k = self.res_k.data_ptr() if self.res_k is not None else None
+        s.res_v = self.res_v.data_ptr() if self.res_v is not None else None
+        self.s = s
+
+    @property
+    def Hq(self):
+        return self.G * self.Hkv
+
+    def n_q(self, layer):
+        return self.s.n_q[layer]
+
+    def n_res(self, layer):
+        return self.s.n_res[layer]
+
+    def set_counts(self, layer, n_q, n_res=0):
+        self.s.n_q[layer] = n_q
+        self.s.n_res[layer] = n_res
+
+    def append(self, layer, k_new, v_new, vstore: VStore, stream=None):
+        """hc_append_kv: k_new, v_new fp16 [B][Hkv][d] (cuda)."""
+        vs = vstore.struct()
+        _check(lib().hc_append_kv(C.byref(self.s), C.byref(vs), layer, _ptr(k_new), _ptr(v_new),
+                                  _stream(stream)))
+
+    def workspace_bytes(self, bud: hc_budget) -> int:
+        return int(lib().hc_decode_workspace_bytes(C.byref(self.s), bud))
+
+
+class Workspace:
+    def __init__(self, nbytes, device="cuda"):
+        import torch
+        self.t = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+    @property
+    def nbytes(self):
+        return self.t.numel()
+
+
+def decode_attention(q, kc: KCache, vstore: VStore, layer: int, bud: hc_budget, out=None,
+                     sel_idx=None, sel_w=None, sel_k=None, ws: Workspace | None = None,
+                     debug: dict | None = None, stream=None):
+    """hc_decode_attention for one layer: q fp16 [B][Hq][d] -> out fp32 [B][Hq][d]."""
+    import torch
+    if out is None:
+        out = torch.empty((kc.B, kc.Hq, kc.d), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = Workspace(kc.workspace_bytes(bud), device=q.device)
+    vs = vstore.struct()
+    dbg = None
+    if debug is not None:
+        dbg = hc_decode_debug(*(debug[k].data_ptr() if debug.get(k) is not None else None
+                                for k in ("z", "e", "S", "M", "kstar")))
+    st = lib().hc_decode_attention(_ptr(q), C.byref(kc.s), C.byref(vs), layer, bud, _ptr(out),
+                                   _ptr(sel_idx), _ptr(sel_w), _ptr(sel_k),
+                                   C.byref(dbg) if dbg is not None else None,
+                                   _ptr(ws.t), ws.nbytes, _stream(stream))
+    _check(st)
+    return out
+
+
+def select_topk(scores, d: int, bud: hc_budget, idx=None, w=None, k=None, ws=None, stream=None):
+    """hc_select_topk: scores fp32 [rows][n] (cuda) -> (idx int32 [rows][k_max] ascending,
+    w fp32 [rows][k_max], k int64 [rows])."""
+    import torch
+    rows, n = scores.shape
+    km = int(bud.k_max)
+    if idx is None:
+        idx = torch.full((rows, km), -1, dtype=torch.int32, device=scores.device)
+        w = torch.zeros((rows, km), dtype=torch.float32, device=scores.device)
+        k = torch.zeros((rows,), dtype=torch.int64, device=scores.device)
+    need = int(lib().hc_select_workspace_bytes(rows, n, bud))
+    if ws is None:
+        ws = Workspace(need, device=scores.device)
+    _check(lib().hc_select_topk(_ptr(scores), rows, n, d, bud, _ptr(idx), _ptr(w), _ptr(k),
+                                _ptr(ws.t), ws.nbytes, _stream(stream)))
+    return idx, w, k

@@ -1,0 +1,393 @@
+// hc_api.cu -- the C ABI of include/hc.h: argument validation, workspace layout,
+// and the stream-ordered launch sequence of one decode step.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/hc.h"
+#include "hc_internal.h"
+
+using namespace hc;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+hc_status fail(hc_status st, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+hc_status cuda_check(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) return fail(HC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HC_OK;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+int next_pow2(int c) {
+  int p = 1;
+  while (p < c) p <<= 1;
+  return p;
+}
+
+constexpr int kGatherRows = 512;
+constexpr int kChunkTokens = 4096;
+
+struct Layout {
+  int cpow2;
+  int64_t z_stride;
+  int nchunks_max;
+  int gchunks;
+  int64_t k_eff;
+  size_t o_hs, o_T, o_z, o_h1c, o_h2c, o_h1m, o_chunk, o_part, o_idx, o_w, total;
+  size_t hist_bytes;  // h1c + h2c + h1m (contiguous)
+};
+
+Layout make_layout(const hc_kcache *kc, int64_t k_max) {
+  Layout L{};
+  const int64_t B = kc->B, Hkv = kc->Hkv, G = kc->G, Hq = G * Hkv;
+  const int64_t rows = B * Hq;
+  const int g = kc->vq.g, d = kc->vq.d;
+  L.cpow2 = next_pow2(kc->vq.c);
+  if (L.cpow2 < 256) L.cpow2 = 256;
+  const int64_t ncand_max = kc->n_cap + kc->res_cap;
+  L.z_stride = round_up(ncand_max > 0 ? ncand_max : 1, 64);
+  L.nchunks_max = (int)((L.z_stride + kChunkTokens - 1) / kChunkTokens);
+  L.k_eff = k_max < ncand_max ? k_max : ncand_max;
+  if (L.k_eff < 1) L.k_eff = 1;
+  L.gchunks = (int)((L.k_eff + kGatherRows - 1) / kGatherRows);
+  size_t o = 0;
+  L.o_hs = o; o += align256((size_t)rows * sizeof(HeadState));
+  L.o_T = o; o += align256((size_t)B * Hkv * g * L.cpow2 * G * 2);
+  L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
+  L.o_h1c = o; o += (size_t)rows * kNB * 4;
+  L.o_h2c = o; o += (size_t)rows * kNB * 4;
+  L.o_h1m = o; o += (size_t)rows * kNB * 8;
+  L.hist_bytes = o - L.o_h1c;
+  o = align256(o);
+  L.o_chunk = o; o += align256((size_t)rows * L.nchunks_max * 2 * 4);
+  L.o_part = o; o += align256((size_t)rows * L.gchunks * d * 4);
+  L.o_idx = o; o += align256((size_t)rows * L.k_eff * 4);
+  L.o_w = o; o += align256((size_t)rows * L.k_eff * 4);
+  L.total = o;
+  return L;
+}
+
+hc_status check_vq(const hc_vq &vq) {
+  if (vq.d <= 0 || vq.g <= 0 || vq.c <= 0) return fail(HC_ERR_SHAPE, "d, g, c must be positive");
+  if (vq.d % vq.g) return fail(HC_ERR_SHAPE, "g=%d does not divide d=%d", vq.g, vq.d);
+  const int dbar = vq.d / vq.g;
+  if (!(dbar == 1 || dbar == 2 || dbar == 4 || dbar == 8 || dbar == 16))
+    return fail(HC_ERR_UNSUPPORTED, "dbar=%d not in {1,2,4,8,16}", dbar);
+  if (vq.c > 65536) return fail(HC_ERR_RANGE, "c=%d exceeds the 16-bit index range", vq.c);
+  if (!(vq.cbg == 1 || vq.cbg == vq.g)) return fail(HC_ERR_SHAPE, "cbg must be 1 or g");
+  if (vq.d % 8 || vq.d > 256 || (32 % (vq.d / 8)))
+    return fail(HC_ERR_UNSUPPORTED, "d=%d not in {64,128,256}", vq.d);
+  return HC_OK;
+}
+
+hc_status check_kcache(const hc_kcache *kc) {
+  if (!kc) return fail(HC_ERR_ARG, "kcache is NULL");
+  hc_status st = check_vq(kc->vq);
+  if (st) return st;
+  if (kc->B <= 0 || kc->L <= 0 || kc->Hkv <= 0 || kc->L > HC_MAX_LAYERS)
+    return fail(HC_ERR_SHAPE, "bad B/L/Hkv");
+  if (!(kc->G == 1 || kc->G == 2 || kc->G == 4)) return fail(HC_ERR_UNSUPPORTED, "G=%d not in {1,2,4}", kc->G);
+  if (kc->n_cap < 0 || kc->n_cap % 64) return fail(HC_ERR_SHAPE, "n_cap must be a multiple of 64");
+  if (kc->res_cap < 0) return fail(HC_ERR_SHAPE, "res_cap < 0");
+  if (kc->vq.c > 8192) return fail(HC_ERR_UNSUPPORTED, "c=%d > 8192 (shared-memory table slices)", kc->vq.c);
+  if (kc->n_cap > 0 && !kc->codes) return fail(HC_ERR_ARG, "codes is NULL");
+  if (!kc->codebook) return fail(HC_ERR_ARG, "codebook is NULL");
+  if (kc->res_cap > 0 && (!kc->res_k || !kc->res_v)) return fail(HC_ERR_ARG, "res_k/res_v NULL");
+  if ((int64_t)kc->B * kc->G * kc->Hkv > 65535) return fail(HC_ERR_UNSUPPORTED, "B*Hq > 65535");
+  return HC_OK;
+}
+
+__global__ void k_hs_init(HeadState *hs, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  HeadState h;
+  memset(&h, 0, sizeof(h));
+  h.M = INT_MIN;
+  h.zmin = INT_MAX;
+  h.bstar = kNB;
+  hs[r] = h;
+}
+
+__global__ void k_z_to_int(const float *z, int64_t zs, int32_t *out, int64_t n) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) out[(int64_t)blockIdx.y * n + j] = __float2int_rn(z[(int64_t)blockIdx.y * zs + j]);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *hc_last_error(void) { return g_err; }
+const char *hc_version(void) { return "hcattn-b200 0.1 (sm_100a)"; }
+
+hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *codebook, hc_vq vq,
+                           uint16_t *codes, int64_t code_stride, hc_stream_t stream) {
+  hc_status st = check_vq(vq);
+  if (st) return st;
+  if (rows < 0) return fail(HC_ERR_ARG, "rows < 0");
+  if (rows == 0) return HC_OK;
+  if (!keys || !codebook || !codes) return fail(HC_ERR_ARG, "NULL pointer");
+  if (code_stride < rows) return fail(HC_ERR_SHAPE, "code_stride < rows");
+  if (rows > 0x7fffffff) return fail(HC_ERR_UNSUPPORTED, "rows > 2^31-1");
+  EncodeArgs a{};
+  a.keys = keys;
+  a.kmap = RowMap{1, vq.d, 0, 0};
+  a.rows = rows;
+  a.C = codebook;
+  a.d = vq.d; a.g = vq.g; a.c = vq.c; a.cbg = vq.cbg;
+  a.codes = codes;
+  a.omap = RowMap{1, 1, 0, 0};
+  a.gstride = code_stride;
+  return cuda_check(launch_encode(a, (cudaStream_t)stream), "hc_quantize_keys");
+}
+
+hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const uint16_t *k_new,
+                       const uint16_t *v_new, hc_stream_t stream) {
+  hc_status st = check_kcache(kc);
+  if (st) return st;
+  if (!vs || !vs->base) return fail(HC_ERR_ARG, "vstore is NULL");
+  if (vs->n_cap != kc->n_cap) return fail(HC_ERR_SHAPE, "vstore.n_cap != kcache.n_cap");
+  if (layer < 0 || layer >= kc->L) return fail(HC_ERR_RANGE, "layer %d out of range", layer);
+  if (!k_new || !v_new) return fail(HC_ERR_ARG, "k_new/v_new NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t B = kc->B, L = kc->L, H = kc->Hkv, d = kc->vq.d, g = kc->vq.g, W = kc->res_cap;
+  const int64_t ncap = kc->n_cap;
+  const int64_t nq = kc->n_q[layer];
+  const int64_t nr = kc->n_res[layer];
+  const int64_t rows = B * H;
+  const RowMap codes_at = {H, L * H * g * ncap, g * ncap, (int64_t)layer * H * g * ncap + nq};
+  const RowMap vstore_at = {H, L * H * ncap * d, ncap * d, ((int64_t)layer * H * ncap + nq) * d};
+  const RowMap flat = {1, d, 0, 0};
+  auto encode_from = [&](const uint16_t *src, RowMap km) -> cudaError_t {
+    EncodeArgs a{};
+    a.keys = src; a.kmap = km; a.rows = rows;
+    a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
+    a.d = (int)d; a.g = (int)g; a.c = kc->vq.c; a.cbg = kc->vq.cbg;
+    a.codes = kc->codes; a.omap = codes_at; a.gstride = ncap;
+    return launch_encode(a, s);
+  };
+  auto copy = [&](const uint16_t *src, RowMap sm, uint16_t *dst, RowMap dm) -> cudaError_t {
+    RowCopyArgs a{src, sm, dst, dm, rows, (int)d};
+    return launch_rowcopy(a, s);
+  };
+  cudaError_t e = cudaSuccess;
+  if (W == 0) {
+    if (nq >= ncap) return fail(HC_ERR_CAPACITY, "layer %d full (n_cap=%lld)", layer, (long long)ncap);
+    e = encode_from(k_new, flat);
+    if (e == cudaSuccess) e = copy(v_new, flat, vs->base, vstore_at);
+    if (e != cudaSuccess) return cuda_check(e, "hc_append_kv");
+    kc->n_q[layer] = nq + 1;
+    return HC_OK;
+  }
+  const int64_t p = nq + nr;
+  if (nr < W) {
+    const int64_t slot = p % W;
+    const RowMap res_at = {H, L * H * W * d, W * d, ((int64_t)layer * H * W + slot) * d};
+    e = copy(k_new, flat, kc->res_k, res_at);
+    if (e == cudaSuccess) e = copy(v_new, flat, kc->res_v, res_at);
+    if (e != cudaSuccess) return cuda_check(e, "hc_append_kv");
+    kc->n_res[layer] = (int32_t)(nr + 1);
+    return HC_OK;
+  }
+  if (nq >= ncap) return fail(HC_ERR_CAPACITY, "layer %d full (n_cap=%lld)", layer, (long long)ncap);
+  const int64_t slot = nq % W;  // the oldest resident token (position nq)
+  const RowMap res_at = {H, L * H * W * d, W * d, ((int64_t)layer * H * W + slot) * d};
+  e = encode_from(kc->res_k, res_at);
+  if (e == cudaSuccess) e = copy(kc->res_v, res_at, vs->base, vstore_at);
+  if (e == cudaSuccess) e = copy(k_new, flat, kc->res_k, res_at);
+  if (e == cudaSuccess) e = copy(v_new, flat, kc->res_v, res_at);
+  if (e != cudaSuccess) return cuda_check(e, "hc_append_kv");
+  kc->n_q[layer] = nq + 1;
+  return HC_OK;
+}
+
+size_t hc_decode_workspace_bytes(const hc_kcache *kc, hc_budget budget) {
+  if (check_kcache(kc) != HC_OK) return 0;
+  return make_layout(kc, budget.k_max).total;
+}
+
+hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
+                              int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
+                              float *sel_w, int64_t *sel_k, const hc_decode_debug *dbg, void *ws,
+                              size_t ws_bytes, hc_stream_t stream) {
+  hc_status st = check_kcache(kc);
+  if (st) return st;
+  if (!vs || !vs->base) return fail(HC_ERR_ARG, "vstore is NULL");
+  if (vs->n_cap != kc->n_cap) return fail(HC_ERR_SHAPE, "vstore.n_cap != kcache.n_cap");
+  if (!(vs->placement == HC_V_DEVICE || vs->placement == HC_V_HOST_MAPPED))
+    return fail(HC_ERR_ARG, "bad vstore placement");
+  if (layer < 0 || layer >= kc->L) return fail(HC_ERR_RANGE, "layer %d out of range", layer);
+  if (!q || !out) return fail(HC_ERR_ARG, "q/out NULL");
+  if (!(budget.tau > 0.0f && budget.tau <= 1.0f)) return fail(HC_ERR_ARG, "tau=%g not in (0,1]", budget.tau);
+  if (budget.k_max < 1) return fail(HC_ERR_ARG, "k_max < 1");
+  if (!!sel_idx != !!sel_w) return fail(HC_ERR_ARG, "pass both sel_idx and sel_w, or neither");
+  const int64_t n_q = kc->n_q[layer], n_res = kc->n_res[layer];
+  if (n_q < 0 || n_q > kc->n_cap || n_res < 0 || n_res > kc->res_cap)
+    return fail(HC_ERR_RANGE, "cache counts out of range");
+  const int64_t n_cand = n_q + n_res;
+  if (n_cand == 0) return fail(HC_ERR_EMPTY, "layer %d has no tokens", layer);
+  const Layout Lw = make_layout(kc, budget.k_max);
+  if (!ws || ws_bytes < Lw.total)
+    return fail(HC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, Lw.total);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t *w8 = (uint8_t *)ws;
+  const int64_t B = kc->B, H = kc->Hkv, G = kc->G, Hq = G * H, d = kc->vq.d, g = kc->vq.g;
+  const int64_t L = kc->L, W = kc->res_cap, ncap = kc->n_cap;
+  const int rows = (int)(B * Hq);
+
+  LayerArgs a{};
+  a.B = (int)B; a.Hkv = (int)H; a.G = (int)G; a.Hq = (int)Hq; a.d = (int)d; a.g = (int)g;
+  a.c = kc->vq.c; a.cbg = kc->vq.cbg; a.dbar = (int)(d / g); a.cpow2 = Lw.cpow2;
+  a.n_q = n_q; a.n_res = n_res; a.n_cand = n_cand; a.n_cap = ncap; a.res_cap = W > 0 ? W : 1;
+  a.q = q;
+  a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
+  a.codes = kc->codes + (int64_t)layer * H * g * ncap;
+  a.code_b_stride = L * H * g * ncap;
+  a.res_k = W > 0 ? kc->res_k + (int64_t)layer * H * W * d : nullptr;
+  a.res_v = W > 0 ? kc->res_v + (int64_t)layer * H * W * d : nullptr;
+  a.res_b_stride = L * H * (W > 0 ? W : 1) * d;
+  a.res_slot0 = W > 0 ? n_q % W : 0;
+  a.V = vs->base + (int64_t)layer * H * ncap * d;
+  a.v_b_stride = L * H * ncap * d;
+  a.v_kv_stride = ncap * d;
+  a.tau_q = (uint32_t)rint((double)budget.tau * 16777216.0);
+  a.renorm = budget.renorm ? 1 : 0;
+  a.kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
+  a.hs = (HeadState *)(w8 + Lw.o_hs);
+  a.T = (int16_t *)(w8 + Lw.o_T);
+  a.z = (float *)(w8 + Lw.o_z);
+  a.z_stride = Lw.z_stride;
+  a.h1c = (uint32_t *)(w8 + Lw.o_h1c);
+  a.h2c = (uint32_t *)(w8 + Lw.o_h2c);
+  a.h1m = (unsigned long long *)(w8 + Lw.o_h1m);
+  a.chunk_cnt = (uint32_t *)(w8 + Lw.o_chunk);
+  a.chunk_tokens = kChunkTokens;
+  a.nchunks = (int)((n_cand + kChunkTokens - 1) / kChunkTokens);
+  a.partial = (float *)(w8 + Lw.o_part);
+  a.grows = kGatherRows;
+  const int64_t k_cap = sel_idx ? budget.k_max : Lw.k_eff;  // row stride of idx / w
+  a.k_max = k_cap;
+  a.gchunks = (int)(((k_cap < n_cand ? k_cap : n_cand) + kGatherRows - 1) / kGatherRows);
+  a.sel_idx = sel_idx ? sel_idx : (int32_t *)(w8 + Lw.o_idx);
+  a.sel_w = sel_w ? sel_w : (float *)(w8 + Lw.o_w);
+  a.sel_k = sel_k;
+  a.out = out;
+  a.num_sms = num_sms();
+  a.scan_tpt = 16;
+  {  // choose the token tile so the scan fills the machine
+    const int64_t units = B * H;
+    const int64_t tiles16 = units * ((n_q + 8191) / 8192);
+    if (tiles16 < a.num_sms) a.scan_tpt = 8;
+  }
+
+  cudaError_t e;
+  k_hs_init<<<(rows + 127) / 128, 128, 0, s>>>(a.hs, rows);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "init");
+  if ((e = cudaMemsetAsync(w8 + Lw.o_h1c, 0, Lw.hist_bytes, s)) != cudaSuccess) return cuda_check(e, "memset");
+  if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
+  if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
+  if (n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
+  SelArgs sa{};
+  sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
+  sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
+  sa.h1c = a.h1c; sa.h1m = a.h1m; sa.h2c = a.h2c; sa.chunk_cnt = a.chunk_cnt;
+  sa.nchunks = a.nchunks; sa.chunk_tokens = kChunkTokens;
+  sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
+  if ((e = launch_select(sa, s)) != cudaSuccess) return cuda_check(e, "select");
+  if ((e = launch_gather(a, s)) != cudaSuccess) return cuda_check(e, "gather");
+  if (dbg) {
+    if (dbg->z) {
+      dim3 gz((unsigned)((n_cand + 255) / 256), (unsigned)rows);
+      k_z_to_int<<<gz, 256, 0, s>>>(a.z, a.z_stride, dbg->z, n_cand);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "debug z");
+    }
+    if (dbg->e || dbg->S || dbg->M || dbg->kstar) {
+      // strided fields of HeadState -> dense arrays
+      if (dbg->e) cudaMemcpy2DAsync(dbg->e, 4, &a.hs->e, sizeof(HeadState), 4, rows, cudaMemcpyDeviceToDevice, s);
+      if (dbg->S) cudaMemcpy2DAsync(dbg->S, 8, &a.hs->S, sizeof(HeadState), 8, rows, cudaMemcpyDeviceToDevice, s);
+      if (dbg->M) cudaMemcpy2DAsync(dbg->M, 4, &a.hs->M, sizeof(HeadState), 4, rows, cudaMemcpyDeviceToDevice, s);
+      if (dbg->kstar) cudaMemcpy2DAsync(dbg->kstar, 8, &a.hs->kstar, sizeof(HeadState), 8, rows, cudaMemcpyDeviceToDevice, s);
+      if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "debug");
+    }
+  }
+  return HC_OK;
+}
+
+size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {
+  (void)budget;
+  if (rows <= 0 || n <= 0) return 0;
+  const int64_t zs = round_up(n, 64);
+  const int64_t nch = (zs + kChunkTokens - 1) / kChunkTokens;
+  size_t o = 0;
+  o += align256((size_t)rows * sizeof(HeadState));
+  o += align256((size_t)rows * zs * 4);
+  o += align256((size_t)rows * kNB * 16);
+  o += align256((size_t)rows * nch * 8);
+  return o;
+}
+
+hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d, hc_budget budget,
+                         int32_t *idx, float *w, int64_t *k, void *ws, size_t ws_bytes,
+                         hc_stream_t stream) {
+  if (rows <= 0 || rows > 65535) return fail(HC_ERR_ARG, "rows must be in [1, 65535]");
+  if (n <= 0) return fail(HC_ERR_EMPTY, "n == 0");
+  if (n >= (1ll << 31)) return fail(HC_ERR_UNSUPPORTED, "n >= 2^31");
+  if (d <= 0) return fail(HC_ERR_ARG, "d <= 0");
+  if (!scores || !idx || !w) return fail(HC_ERR_ARG, "NULL pointer");
+  if (!(budget.tau > 0.0f && budget.tau <= 1.0f)) return fail(HC_ERR_ARG, "tau=%g not in (0,1]", budget.tau);
+  if (budget.k_max < 1) return fail(HC_ERR_ARG, "k_max < 1");
+  const size_t need = hc_select_workspace_bytes(rows, n, budget);
+  if (!ws || ws_bytes < need) return fail(HC_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t *w8 = (uint8_t *)ws;
+  const int64_t zs = round_up(n, 64);
+  const int nch = (int)((n + kChunkTokens - 1) / kChunkTokens);
+  size_t o = 0;
+  HeadState *hs = (HeadState *)(w8 + o); o += align256((size_t)rows * sizeof(HeadState));
+  float *z = (float *)(w8 + o); o += align256((size_t)rows * zs * 4);
+  uint8_t *hist = w8 + o; o += align256((size_t)rows * kNB * 16);
+  uint32_t *chunk = (uint32_t *)(w8 + o);
+  cudaError_t e;
+  k_hs_init<<<(int)((rows + 127) / 128), 128, 0, s>>>(hs, (int)rows);
+  if ((e = cudaMemsetAsync(hist, 0, (size_t)rows * kNB * 16, s)) != cudaSuccess) return cuda_check(e, "memset");
+  const float kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
+  if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s)) != cudaSuccess)
+    return cuda_check(e, "prep");
+  SelArgs sa{};
+  sa.hs = hs; sa.z = z; sa.z_stride = zs; sa.rows = (int)rows; sa.n = n;
+  sa.tau_q = (uint32_t)rint((double)budget.tau * 16777216.0);
+  sa.k_max = budget.k_max; sa.renorm = budget.renorm ? 1 : 0;
+  sa.h1c = (uint32_t *)hist;
+  sa.h2c = (uint32_t *)(hist + (size_t)rows * kNB * 4);
+  sa.h1m = (unsigned long long *)(hist + (size_t)rows * kNB * 8);
+  sa.chunk_cnt = chunk; sa.nchunks = nch; sa.chunk_tokens = kChunkTokens;
+  sa.sel_idx = idx; sa.sel_w = w; sa.sel_k = k;
+  return cuda_check(launch_select(sa, s), "hc_select_topk");
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// hc_device.cuh -- device-side arithmetic of the CUDA path (sm_100a).
+// Implements DESIGN.md §2 readings R1-R6 with explicit IEEE intrinsics so the
+// results are bit-identical to the independent CPU oracle (no code shared).
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#ifndef HC_HD
+#define HC_HD __device__ __forceinline__
+#endif
+
+namespace hc {
+
+constexpr int kNB = 4096;        // buckets per histogram level (12 bits)
+constexpr int kNBBits = 12;
+
+HC_HD float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+// exact 2^e for -126 <= e <= 127
+HC_HD float pow2f(int e) { return __int_as_float((e + 127) << 23); }
+
+// R2: e_h = 100 if A < 2^-100 else clamp(14 - floor(log2 A), -100, 100)
+HC_HD int scale_exponent(float A) {
+  if (!(A >= 0x1p-100f)) return 100;
+  int ex = ((__float_as_int(A) >> 23) & 0xff) - 127;  // A is normal here
+  int e = 14 - ex;
+  return e < -100 ? -100 : (e > 100 ? 100 : e);
+}
+
+// R2: T_fx = clamp(rint(t * 2^e), +-32767)
+HC_HD int quant_t(float t, float s) {
+  float v = rintf(__fmul_rn(t, s));
+  v = fminf(fmaxf(v, -32767.0f), 32767.0f);
+  return (int)v;
+}
+
+// R3 resident: rint(clamp(acc * 2^e, +-2^22))
+HC_HD int quant_res(float acc, float s) {
+  float v = __fmul_rn(acc, s);
+  v = fminf(fmaxf(v, -4194304.0f), 4194304.0f);
+  return __float2int_rn(v);
+}
+
+// R4: exp2_det polynomial (degree 6 on [0,1))
+HC_HD float exp2_poly(float f) {
+  float p = 0x1.c6e292p-13f;
+  p = __fmaf_rn(p, f, 0x1.46301cp-10f);
+  p = __fmaf_rn(p, f, 0x1.3d24eap-7f);
+  p = __fmaf_rn(p, f, 0x1.c68562p-5f);
+  p = __fmaf_rn(p, f, 0x1.ebfd9ap-3f);
+  p = __fmaf_rn(p, f, 0x1.62e42ap-1f);
+  p = __fmaf_rn(p, f, 0x1.000000p+0f);
+  return p;
+}
+
+// R4: W(Δ) = trunc(2^40 * exp2_det(-(Δ·κ)))
+HC_HD uint64_t mass(uint32_t delta, float kappa) {
+  float x = -__fmul_rn(__uint2float_rn(delta), kappa);
+  if (x < -40.0f) return 0ull;
+  float nf = floorf(x);
+  float f = __fsub_rn(x, nf);
+  float p = exp2_poly(f);
+  float v = __fmul_rn(p, pow2f(40 + (int)nf));
+  return __float2ull_rz(v);
+}
+
+// R5: Θ = ceil(τ_q · S / 2^24)  (τ_q <= 2^24, S < 2^63)
+HC_HD uint64_t threshold(uint32_t tau_q, uint64_t S) {
+  uint64_t lo = (uint64_t)tau_q * S;
+  uint64_t hi = __umul64hi((uint64_t)tau_q, S);
+  uint64_t add = (1ull << 24) - 1;
+  uint64_t lo2 = lo + add;
+  hi += (lo2 < lo) ? 1ull : 0ull;
+  return (hi << 40) | (lo2 >> 24);
+}
+
+// per-(b, query head) selection state, 128 B, in the workspace
+struct alignas(16) HeadState {
+  int32_t M;            // max z (atomicMax), init INT_MIN
+  int32_t zmin;         // min z (atomicMin), init INT_MAX
+  uint32_t amax;        // bits of max|t| (atomicMax on non-negative float bits), init 0
+  int32_t e;            // table scale exponent
+  float kappa;          // κ_h = κ0 · 2^-e
+  int32_t shift;        // coarse bucket = Δ >> shift
+  int32_t bstar;        // boundary coarse bucket, kNB = "all strict"
+  uint32_t cnt_before;  // #tokens in buckets < bstar
+  uint64_t mass_before; // mass in buckets < bstar
+  uint64_t S;           // total mass
+  uint64_t theta;       // Θ
+  uint32_t delta_star;  // exact boundary Δ* (tokens with Δ < Δ* are kept)
+  uint32_t r_ties;      // #ties at Δ* kept (lowest indices)
+  int64_t ksel;         // k_sel
+  int64_t kstar;        // k* if τ decided, else -1
+  uint64_t sel_mass;    // mass of the kept set (renorm)
+  uint32_t gather_done; // completion counter of the gather's last-block reduction
+  uint32_t pad[9];
+};
+static_assert(sizeof(HeadState) == 128, "HeadState size");
+
+}  // namespace hc

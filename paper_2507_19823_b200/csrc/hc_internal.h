@@ -1,0 +1,116 @@
+// hc_internal.h -- launch interfaces between the C-ABI host layer (hc_api.cu)
+// and the sm_100a kernels.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hc_device.cuh"
+
+namespace hc {
+
+// row -> element offset:  (r / R1) * s1 + (r % R1) * s2 + s0
+struct RowMap {
+  int64_t R1, s1, s2, s0;
+};
+
+struct EncodeArgs {
+  const uint16_t *keys;
+  RowMap kmap;           // key row offset (elements)
+  int64_t rows;
+  const float *C;        // [cbg][c][dbar]
+  int d, g, c, cbg;
+  uint16_t *codes;
+  RowMap omap;           // code offset of (r, group 0)
+  int64_t gstride;       // elements between groups
+};
+cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s);
+
+struct RowCopyArgs {
+  const uint16_t *src;
+  RowMap smap;
+  uint16_t *dst;
+  RowMap dmap;
+  int64_t rows;
+  int d;
+};
+cudaError_t launch_rowcopy(const RowCopyArgs &a, cudaStream_t s);
+
+struct LayerArgs {
+  // shape
+  int B, Hkv, G, Hq, d, g, c, cbg, dbar, cpow2;
+  int64_t n_q, n_res, n_cand, n_cap, res_cap;
+  // inputs
+  const uint16_t *q;      // [B][Hq][d]
+  const float *C;         // layer codebook [cbg][c][dbar]
+  const uint16_t *codes;  // layer 0 of batch 0 base + l*Hkv*g*n_cap ; batch stride below
+  int64_t code_b_stride;  // elements between batches
+  const uint16_t *res_k;  // [B][L][Hkv][W][d] at layer l (batch stride below)
+  const uint16_t *res_v;
+  int64_t res_b_stride;   // elements between batches
+  int64_t res_slot0;      // slot of candidate n_q: (n_q) % W
+  const uint16_t *V;      // value store at layer l, batch 0
+  int64_t v_b_stride;     // elements between batches
+  int64_t v_kv_stride;    // elements between KV heads
+  // budget
+  uint32_t tau_q;
+  int64_t k_max;
+  int renorm;
+  float kappa0;
+  // workspace
+  HeadState *hs;          // [B*Hq]
+  int16_t *T;             // [units][g][cpow2][G]
+  float *z;               // [B*Hq][z_stride]
+  int64_t z_stride;
+  uint32_t *h1c;          // [B*Hq][kNB]
+  unsigned long long *h1m;
+  uint32_t *h2c;          // [B*Hq][kNB]
+  uint32_t *chunk_cnt;    // [B*Hq][nchunks][2]
+  int nchunks;            // chunks per head for count/write
+  int chunk_tokens;
+  float *partial;         // gather partials [B*Hq][gchunks][d]
+  int gchunks;
+  int grows;              // rows per gather CTA
+  // outputs
+  int32_t *sel_idx;       // [B*Hq][k_max]
+  float *sel_w;
+  int64_t *sel_k;         // [B*Hq] (may be null)
+  float *out;             // [B*Hq][d]
+  int num_sms;
+  int scan_tpt;
+};
+
+cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);
+cudaError_t launch_table(const LayerArgs &a, cudaStream_t s);
+cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s);
+cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s);
+cudaError_t launch_gather(const LayerArgs &a, cudaStream_t s);
+
+// Eq. 4 selection over `rows` independent score rows (query heads):
+// z [rows][z_stride] (exact integers stored as fp32), hs[row].{M,zmin,kappa} set.
+struct SelArgs {
+  HeadState *hs;
+  const float *z;
+  int64_t z_stride;
+  int rows;
+  int64_t n;              // candidates per row
+  uint32_t tau_q;
+  int64_t k_max;
+  int renorm;
+  uint32_t *h1c;
+  unsigned long long *h1m;
+  uint32_t *h2c;
+  uint32_t *chunk_cnt;
+  int nchunks;
+  int chunk_tokens;
+  int32_t *sel_idx;       // [rows][k_max]
+  float *sel_w;           // [rows][k_max]
+  int64_t *sel_k;         // [rows] (may be null)
+};
+cudaError_t launch_select(const SelArgs &a, cudaStream_t s);
+
+// standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
+cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
+                                     int64_t z_stride, HeadState *hs, float kappa0,
+                                     cudaStream_t s);
+
+}  // namespace hc

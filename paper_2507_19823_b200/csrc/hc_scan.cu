@@ -1,0 +1,264 @@
+// hc_scan.cu -- row a2: approximate scores against the quantized key cache,
+// Eq. 3:  z̃_j = Σ_{i=1..g} T_{i, P_{j,i}}.
+//
+// B200 design:
+//  * one CTA per SM (persistent over token tiles), 512 threads;
+//  * a tile = TPT*512 consecutive tokens of one (b, kv) unit; every thread owns
+//    2 chunks of 8 consecutive tokens and keeps G int32 accumulators per token in
+//    registers across the whole group loop (the sum is exact integer, R2/R3, so the
+//    association is free);
+//  * the group loop streams the unit's T slice i (cpow2 × G × int16 = 64 KiB at
+//    c = 8192, G = 4) into shared memory with cp.async.bulk (TMA bulk copy engine)
+//    on an mbarrier, double-buffered: slice i+2 is in flight while slice i is used;
+//  * the P strip of group i (group-major layout, contiguous per group) is read
+//    with 128-bit L1-bypassing loads, one group ahead of use;
+//  * one 8-byte LDS per (token, group) returns the 4 GQA heads' table entries.
+#include "hc_internal.h"
+
+namespace hc {
+
+constexpr int kScanThreads = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <int G>
+struct Lut;
+template <>
+struct Lut<4> {  // 8-byte entries: 4 x int16
+  static constexpr int kShift = 3;
+  __device__ __forceinline__ static void add(const uint8_t *sb, uint32_t off, int (&acc)[4]) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(sb + off);
+    acc[0] += (int)(int16_t)(v.x & 0xffffu);
+    acc[1] += ((int)v.x) >> 16;
+    acc[2] += (int)(int16_t)(v.y & 0xffffu);
+    acc[3] += ((int)v.y) >> 16;
+  }
+};
+template <>
+struct Lut<2> {
+  static constexpr int kShift = 2;
+  __device__ __forceinline__ static void add(const uint8_t *sb, uint32_t off, int (&acc)[2]) {
+    const uint32_t v = *reinterpret_cast<const uint32_t *>(sb + off);
+    acc[0] += (int)(int16_t)(v & 0xffffu);
+    acc[1] += ((int)v) >> 16;
+  }
+};
+template <>
+struct Lut<1> {
+  static constexpr int kShift = 1;
+  __device__ __forceinline__ static void add(const uint8_t *sb, uint32_t off, int (&acc)[1]) {
+    acc[0] += (int)*reinterpret_cast<const int16_t *>(sb + off);
+  }
+};
+
+// 8 codes (one uint4) -> 8 tokens' accumulators.  Codes are masked to cpow2-1, so
+// any 16-bit pattern stays inside the slice (valid codes are < c <= cpow2).
+template <int G>
+__device__ __forceinline__ void lookup8(const uint4 &c, const uint8_t *sb, uint32_t mask,
+                                        int (&acc)[8][G]) {
+  const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t o0 = (w[q] << Lut<G>::kShift) & mask;
+    const uint32_t o1 = (w[q] >> (16 - Lut<G>::kShift)) & mask;
+    Lut<G>::add(sb, o0, acc[2 * q]);
+    Lut<G>::add(sb, o1, acc[2 * q + 1]);
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void store_chunk(const LayerArgs &a, int b, int kv, int64_t tok,
+                                            const int (&acc)[8][G], int (&mx)[G], int (&mn)[G]) {
+  if (tok >= a.n_q) return;
+  const int64_t rem_ = a.n_q - tok;
+  const int nval = rem_ < 8 ? (int)rem_ : 8;
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float *zp = a.z + ((int64_t)b * a.Hq + kv * G + h) * a.z_stride + tok;
+    if (nval == 8) {
+      float4 v0 = make_float4((float)acc[0][h], (float)acc[1][h], (float)acc[2][h], (float)acc[3][h]);
+      float4 v1 = make_float4((float)acc[4][h], (float)acc[5][h], (float)acc[6][h], (float)acc[7][h]);
+      reinterpret_cast<float4 *>(zp)[0] = v0;
+      reinterpret_cast<float4 *>(zp)[1] = v1;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        mx[h] = max(mx[h], acc[u][h]);
+        mn[h] = min(mn[h], acc[u][h]);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u < nval) {
+          zp[u] = (float)acc[u][h];
+          mx[h] = max(mx[h], acc[u][h]);
+          mn[h] = min(mn[h], acc[u][h]);
+        }
+      }
+    }
+  }
+}
+
+template <int G, int TPT>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles_per_unit,
+                                                           int total_tiles) {
+  static_assert(TPT == 8 || TPT == 16, "TPT");
+  constexpr int kChunks = TPT / 8;                     // 8-token chunks per thread
+  constexpr int kTile = kScanThreads * TPT;            // tokens per tile
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t slice_bytes = (uint32_t)a.cpow2 * G * 2;
+  uint8_t *buf0 = smem;
+  uint8_t *buf1 = smem + slice_bytes;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * slice_bytes);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t parity0 = 0, parity1 = 0;
+  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const int u = tile / tiles_per_unit;
+    const int tk = tile - u * tiles_per_unit;
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int64_t t0 = (int64_t)tk * kTile + (int64_t)warp * (32 * TPT);
+    const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride + (int64_t)kv * a.g * a.n_cap;
+    const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + (int64_t)u * a.g * slice_bytes;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bar[0], slice_bytes);
+      bulk_g2s(buf0, Tu, slice_bytes, &bar[0]);
+      if (a.g > 1) {
+        mbar_expect_tx(&bar[1], slice_bytes);
+        bulk_g2s(buf1, Tu + slice_bytes, slice_bytes, &bar[1]);
+      }
+    }
+    int64_t tok[kChunks];
+    bool val[kChunks];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      tok[k] = t0 + k * 256 + lane * 8;
+      val[k] = tok[k] < a.n_q;
+    }
+    int acc[kChunks][8][G];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+      for (int u8 = 0; u8 < 8; ++u8)
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[k][u8][h] = 0;
+    uint4 cur[kChunks];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) cur[k] = val[k] ? ld_stream(P + tok[k]) : make_uint4(0, 0, 0, 0);
+
+    for (int i = 0; i < a.g; ++i) {
+      uint4 nxt[kChunks];
+      if (i + 1 < a.g) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k)
+          nxt[k] = val[k] ? ld_stream(P + (int64_t)(i + 1) * a.n_cap + tok[k]) : make_uint4(0, 0, 0, 0);
+      }
+      const bool odd = i & 1;
+      if (!odd) { mbar_wait(&bar[0], parity0); parity0 ^= 1u; }
+      else { mbar_wait(&bar[1], parity1); parity1 ^= 1u; }
+      const uint8_t *sb = odd ? buf1 : buf0;
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) lookup8<G>(cur[k], sb, mask, acc[k]);
+      __syncthreads();
+      if (threadIdx.x == 0 && i + 2 < a.g) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint64_t *bb = odd ? &bar[1] : &bar[0];
+        mbar_expect_tx(bb, slice_bytes);
+        bulk_g2s(odd ? buf1 : buf0, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, bb);
+      }
+      if (i + 1 < a.g) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) cur[k] = nxt[k];
+      }
+    }
+    int mx[G], mn[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) store_chunk<G>(a, b, kv, tok[k], acc[k], mx, mn);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const int vmx = __reduce_max_sync(0xffffffffu, mx[h]);
+      const int vmn = __reduce_min_sync(0xffffffffu, mn[h]);
+      if (lane == 0 && vmx != INT_MIN) {
+        HeadState *hs = a.hs + (int64_t)b * a.Hq + kv * G + h;
+        atomicMax(&hs->M, vmx);
+        atomicMin(&hs->zmin, vmn);
+      }
+    }
+  }
+}
+
+template <int G, int TPT>
+static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
+  constexpr int kTile = kScanThreads * TPT;
+  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
+  const int units = a.B * a.Hkv;
+  const int total = tiles_per_unit * units;
+  if (total == 0) return cudaSuccess;
+  const size_t smem = (size_t)2 * a.cpow2 * G * 2 + 16;
+  cudaError_t e = cudaFuncSetAttribute(k_scan<G, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = total < a.num_sms ? total : a.num_sms;
+  k_scan<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total);
+  return cudaGetLastError();
+}
+
+template <int G>
+static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
+  if (a.scan_tpt == 8) return scan_launch<G, 8>(a, s);
+  return scan_launch<G, 16>(a, s);
+}
+
+cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s) {
+  switch (a.G) {
+    case 1: return scan_g<1>(a, s);
+    case 2: return scan_g<2>(a, s);
+    case 4: return scan_g<4>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hc

@@ -1,0 +1,86 @@
+"""CPU-side checks of the boundary (no GPU needed): libhc.so loads and exports every
+entry point include/hc.h declares; the binding mirrors the header's structs; the
+product package never imports the oracle."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "hc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hc_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_north_star_entry_points():
+    fns = _header_functions()
+    for name in ("hc_quantize_keys", "hc_append_kv", "hc_decode_attention", "hc_select_topk"):
+        assert name in fns
+
+
+def test_library_exports_every_header_symbol():
+    import paper_2507_19823_b200 as hc
+    L = hc.lib()
+    for name in _header_functions():
+        assert hasattr(L, name), name
+    assert set(hc.EXPORTS) == set(_header_functions())
+    assert "sm_100a" in hc.version()
+
+
+def test_struct_layout_matches_header():
+    import paper_2507_19823_b200 as hc
+    # hc_kcache: 4 int32 + hc_vq(16) + int64 + 2 ptr + int32(+pad) + 2 ptr + 256 int64 + 256 int32
+    assert ctypes.sizeof(hc.hc_vq) == 16
+    assert ctypes.sizeof(hc.hc_budget) == 24
+    assert ctypes.sizeof(hc.hc_kcache) == 16 + 16 + 8 + 16 + 8 + 16 + 256 * 8 + 256 * 4
+    assert ctypes.sizeof(hc.hc_vstore) == 24
+
+
+def test_validation_without_gpu():
+    """Argument validation is synchronous and needs no device."""
+    import paper_2507_19823_b200 as hc
+    L = hc.lib()
+    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 3, 16, 3), None, 10, None)
+    assert st == hc.HC_ERR_SHAPE
+    st = L.hc_quantize_keys(None, 0, None, hc.hc_vq(128, 32, 16, 32), None, 0, None)
+    assert st == hc.HC_OK
+    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 32, 70000, 32), None, 10, None)
+    assert st == hc.HC_ERR_RANGE
+    kc = hc.hc_kcache()
+    kc.B, kc.L, kc.Hkv, kc.G = 1, 1, 1, 4
+    kc.vq = hc.hc_vq(128, 32, 8192, 32)
+    kc.n_cap = 100  # not a multiple of 64
+    assert L.hc_decode_workspace_bytes(ctypes.byref(kc), hc.budget(0.9, 10)) == 0
+    kc.n_cap = 4096
+    kc.codes = 1
+    kc.codebook = 1
+    assert L.hc_decode_workspace_bytes(ctypes.byref(kc), hc.budget(0.9, 512)) > 0
+    vs = hc.hc_vstore(0, 1, 4096)
+    st = L.hc_decode_attention(1, ctypes.byref(kc), ctypes.byref(vs), 0, hc.budget(0.0, 10), 1,
+                               None, None, None, None, 1, 1 << 40, None)
+    assert st == hc.HC_ERR_ARG  # tau outside (0,1]
+    st = L.hc_decode_attention(1, ctypes.byref(kc), ctypes.byref(vs), 0, hc.budget(0.9, 10), 1,
+                               None, None, None, None, 1, 1 << 40, None)
+    assert st == hc.HC_ERR_EMPTY  # n_q = n_res = 0
+    st = L.hc_decode_attention(1, ctypes.byref(kc), ctypes.byref(vs), 5, hc.budget(0.9, 10), 1,
+                               None, None, None, None, 1, 1 << 40, None)
+    assert st == hc.HC_ERR_RANGE
+    kc.n_q[0] = 10
+    st = L.hc_decode_attention(1, ctypes.byref(kc), ctypes.byref(vs), 0, hc.budget(0.9, 10), 1,
+                               None, None, None, None, 1, 16, None)
+    assert st == hc.HC_ERR_WORKSPACE
+    assert b"workspace" in L.hc_last_error()
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2507_19823_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "hc_oracle" not in txt and "liboracle" not in txt, f
