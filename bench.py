@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the HCAttention decode hot path on B200 (one JSON line on rank 0).
+
+A "step" is one full decode step of a Llama-3-8B-shaped model (BASELINE.json
+configs): for each of the L = 32 layers in order, hc_append_kv (encode the new key
+into the quantized cache, append the value) then hc_decode_attention (table, Eq. 3
+scan, softmax mass, Eq. 4 selection, Eq. 5 gather) for all B x 32 query heads.
+The step is captured once in a CUDA graph and replayed (steady state: the append
+rewrites position n-1, the decode covers n tokens).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|3|1] [--impl ours|reference]
+
+N = 1 default workload: BASELINE config 2 (configs[1]): 32 layers, 8 KV heads x GQA 4,
+d = 128, 32K context, g = 64 (the 25 % budget), c = 8192, k_max = 8192, tau = 0.9,
+batch 1, values in HBM.  N > 1 (torchrun): independent replicas of the same step
+on each GPU (weak scaling) -- the sequence-sharded path is not built yet.
+--impl reference times the CPU oracle (oracle/, plain C) as it stands.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode steps/sec and quantized-key GB/s vs HBM peak at 128K–4M ctx, 1/2/4/8 GPU"
+
+CONFIGS = {
+    1: dict(B=1, L=1, Hkv=1, G=4, d=128, g=32, c=8192, n=4096, k_max=512, tau=0.9, placement=0,
+            workload="config1: 1 layer, 1 KV head x 4 GQA heads, d=128, 4K ctx, g=32 (12.5%), "
+                     "c=8192, k_max=512, tau=0.9, batch 1, V in HBM"),
+    2: dict(B=1, L=32, Hkv=8, G=4, d=128, g=64, c=8192, n=32768, k_max=8192, tau=0.9, placement=0,
+            workload="config2: Llama-3-8B-shaped full decode step (32 layers, 8 KV heads, GQA 4, "
+                     "d=128), 32K ctx, 25% KV budget (g=64, c=8192), k_max=8192, tau=0.9, batch 1, "
+                     "V in HBM, 1xB200"),
+    3: dict(B=4, L=32, Hkv=8, G=4, d=128, g=32, c=8192, n=131072, k_max=16384, tau=0.9,
+            placement=1,
+            workload="config3: Llama-3-8B-shaped, 128K ctx, 12.5% KV budget (g=32, c=8192), "
+                     "k_max=16384, tau=0.9, batch 4, V in host pinned memory (zero-copy), 1xB200"),
+}
+Q_SCALE = 2.29  # calibrates tau=0.9 to Table 3's 15.6 % selection ratio
+SEED = 0x48434154
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + clock-event reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int, period_s: float = 0.005):
+        self.samples, self.reason_bits = [], 0
+        self.period = period_s
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            import torch
+            pr = torch.cuda.get_device_properties(dev_index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reason_bits |= int(r) & ~0x1
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": [v for k, v in self.REASONS.items() if self.reason_bits & k],
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+class Workload:
+    def __init__(self, cfg: dict, device: str):
+        import numpy as np
+        import torch
+
+        import paper_2507_19823_b200 as hc
+        import synth
+        import synth.device as sd
+        self.cfg = cfg
+        B, L, H, G, d, g, c, n = (cfg[k] for k in ("B", "L", "Hkv", "G", "d", "g", "c", "n"))
+        self.Hq = G * H
+        n_cap = (n + 63) // 64 * 64
+        cb = np.stack([synth.gen_codebook(SEED, l, g, c, d // g) for l in range(L)])
+        self.codebook = torch.from_numpy(cb).to(device)
+        self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device)
+        self.vs = hc.VStore.allocate(B, L, H, n_cap, d, placement=cfg["placement"], device=device)
+        sd.fill_codes(self.kc.codes, SEED, c, n)
+        sd.fill_values(self.vs.tensor, SEED, n, device=device)
+        for l in range(L):
+            self.kc.set_counts(l, n - 1)
+        # per-step inputs: q for every layer, the new token's k and v
+        q = np.stack([np.stack([synth.gen_query(SEED + 1, b, l, self.Hq, d, Q_SCALE)
+                                for b in range(B)]) for l in range(L)])
+        kn = synth.gen_keys(SEED + 2, 1, L * B * H, d).reshape(L, B, H, d)
+        vn = synth.gen_keys(SEED + 2, 2, L * B * H, d).reshape(L, B, H, d)
+        self.q_host = torch.from_numpy(q).pin_memory()
+        self.k_host = torch.from_numpy(kn).pin_memory()
+        self.v_host = torch.from_numpy(vn).pin_memory()
+        self.q = self.q_host.to(device)
+        self.k_new = self.k_host.to(device)
+        self.v_new = self.v_host.to(device)
+        self.out = torch.zeros((L, B, self.Hq, d), dtype=torch.float32, device=device)
+        self.out_host = torch.zeros_like(self.out, device="cpu").pin_memory()
+        self.bud = hc.budget(cfg["tau"], cfg["k_max"])
+        self.ws = hc.Workspace(self.kc.workspace_bytes(self.bud), device=device)
+        self.sel_k = torch.zeros((L, B, self.Hq), dtype=torch.int64, device=device)
+        self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(L)]
+        for b_, e_ in self.ev:  # torch creates the CUDA event lazily on first record
+            b_.record()
+            e_.record()
+        torch.cuda.synchronize()
+
+    def reset_counts(self):
+        for l in range(self.cfg["L"]):
+            self.kc.set_counts(l, self.cfg["n"] - 1)
+
+    def step(self, profile=False):
+        import paper_2507_19823_b200 as hc
+        for l in range(self.cfg["L"]):
+            self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
+            if profile:
+                hc.profile_scan_events(*self.ev[l])
+            hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
+                                sel_k=self.sel_k[l], ws=self.ws)
+
+    def step_e2e(self):
+        self.q.copy_(self.q_host, non_blocking=True)
+        self.k_new.copy_(self.k_host, non_blocking=True)
+        self.v_new.copy_(self.v_host, non_blocking=True)
+        self.step()
+        self.out_host.copy_(self.out, non_blocking=True)
+
+    def capture(self, fn):
+        import torch
+
+        import paper_2507_19823_b200 as hc
+        self.reset_counts()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        before = hc.launch_count()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        launches = hc.launch_count() - before
+        self.reset_counts()
+        return g, launches
+
+
+def event_ms(b, e) -> float:
+    """cudaEventElapsedTime for events recorded by the library inside the graph (torch's
+    Event object does not know they were recorded, so ask the driver directly)."""
+    import ctypes
+    cu = ctypes.CDLL("libcuda.so.1")
+    f = ctypes.c_float()
+    rc = cu.cuEventElapsedTime(ctypes.byref(f), ctypes.c_void_p(b.cuda_event),
+                               ctypes.c_void_p(e.cuda_event))
+    if rc != 0:
+        raise RuntimeError(f"cuEventElapsedTime rc={rc}")
+    return f.value
+
+
+def time_graph(g, K, W, dist=None):
+    import torch
+    for _ in range(W):
+        g.replay()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_wave(cfg, units, threads):
+    """Run the oracle on `units` (b, l, kv) decode units in parallel threads (the C calls
+    release the GIL); returns wall seconds.  Inputs are generated before timing."""
+    import concurrent.futures as cf
+
+    import oracle
+    import synth
+    d, g, c, n, G = cfg["d"], cfg["g"], cfg["c"], cfg["n"], cfg["G"]
+    Hq = G * cfg["Hkv"]
+    inputs = []
+    for (b, l, kv) in units:
+        q = synth.gen_query(SEED + 1, b, l, Hq, d, Q_SCALE)[kv * G:(kv + 1) * G]
+        inputs.append((q, synth.gen_codebook(SEED, l, g, c, d // g),
+                       synth.gen_codes(SEED, b, l, kv, g, c, 0, n),
+                       synth.gen_values(SEED, b, l, kv, d, 0, n)))
+    oracle.lib()
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda a: oracle.decode_unit(a[0], a[1], a[2], n, a[3], cfg["tau"],
+                                                  cfg["k_max"]), inputs))
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, budget_s=12.0):
+    cores = os.cpu_count() or 1
+    units_total = cfg["B"] * cfg["L"] * cfg["Hkv"]
+    wave = min(cores, units_total)
+    units = [(0, l % cfg["L"], kv % cfg["Hkv"]) for l, kv in
+             ((i // cfg["Hkv"], i % cfg["Hkv"]) for i in range(wave))]
+    t_first = oracle_wave(cfg, units, wave)
+    reps = max(1, int(budget_s / max(t_first, 1e-3)) - 1)
+    ts = [t_first] + [oracle_wave(cfg, units, wave) for _ in range(min(reps, 20))]
+    t_wave = statistics.median(ts)
+    step_s = math.ceil(units_total / wave) * t_wave
+    return {"value": 1.0 / step_s, "unit": "steps/s", "cores": wave, "kind": "oracle",
+            "sample": f"{wave} of the step's {units_total} (layer, KV-head) units, one per thread, "
+                      f"{len(ts)} waves, median wave {t_wave:.3f}s; step = ceil({units_total}/{wave}) "
+                      f"waves"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    units_total = cfg["B"] * cfg["L"] * cfg["Hkv"]
+    wave = min(cores, units_total)
+    units = [(0, i // cfg["Hkv"] % cfg["L"], i % cfg["Hkv"]) for i in range(wave)]
+    for _ in range(args.warmup):
+        oracle_wave(cfg, units, wave)
+    ts = [oracle_wave(cfg, units, wave) for _ in range(args.steps)]
+    step_s = math.ceil(units_total / wave) * statistics.mean(ts)
+    v = 1.0 / step_s
+    line = {"metric": METRIC, "value": v, "unit": "steps/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "i16+f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "reference": "CPU oracle (oracle/hc_oracle.c)"},
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": wave, "kind": "oracle",
+                             "sample": f"each step = {wave} of {units_total} units in parallel, "
+                                       f"extrapolated x ceil({units_total}/{wave})"},
+            "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    torch.cuda.set_device(local)
+    dev = "cuda"
+    args.warmup = max(args.warmup, 3)
+
+    wl = Workload(cfg, dev)
+    torch.cuda.synchronize()
+    # eager correctness sanity (one step) then capture the step with scan events
+    wl.reset_counts()
+    wl.step()
+    torch.cuda.synchronize()
+    g_step, launches_per_step = wl.capture(lambda: wl.step(profile=True))
+    g_e2e, _ = wl.capture(wl.step_e2e)
+
+    with ClockSampler(local) as clk:
+        ms = time_graph(g_step, args.steps, args.warmup, dist)
+    ms_per_step = ms / args.steps
+    scan_ms = [event_ms(b, e) for (b, e) in wl.ev]  # last replay of the timed region
+    scan_avg_ms = statistics.mean(scan_ms)
+    K2 = args.e2e_steps or max(args.steps // 2, 3)
+    ms_e2e = time_graph(g_e2e, K2, args.warmup, dist) / K2
+
+    B, L, H, g, n, d = (cfg[k] for k in ("B", "L", "Hkv", "g", "n", "d"))
+    p_bytes_layer = B * H * n * g * 2
+    achieved = p_bytes_layer / (scan_avg_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"scan_traffic_config{args.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    ksel = wl.sel_k.float().mean().item()
+    value = world * 1000.0 / ms_per_step
+    h2d = (wl.q.numel() + wl.k_new.numel() + wl.v_new.numel()) * 2
+    d2h = wl.out.numel() * 4
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "i16+f32", "data": "synthetic (seeded splitmix64; codes uniform, C,q,V ~ Irwin-Hall normal)",
+        "config": {"workload": cfg["workload"], "parallelism": "replicas" if world > 1 else "single",
+                   "l2": f"inputs > L2: P = {B * L * H * n * g * 2 / 1e9:.2f} GB/step, V = "
+                         f"{B * L * H * n * d * 2 / 1e9:.2f} GB",
+                   "graph": "one CUDA graph per step (32 x append + decode)"},
+        "quantized_key_gbs": achieved,
+        "quantized_key_frac_hbm": achieved / peak,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_scan (Eq. 3 quantized-key scan)",
+                     "algorithmic_bytes_per_launch": p_bytes_layer,
+                     "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L / ms_per_step,
+                     "peak_source": peak_src},
+        "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / n},
+        "e2e": {"value": world * 1000.0 / ms_e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

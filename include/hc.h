@@ -115,6 +115,16 @@ typedef struct {
 const char *hc_last_error(void);
 const char *hc_version(void);
 
+/* Number of kernels this library has enqueued on streams (or captured into CUDA graphs)
+ * since load.  Used by bench.py to report gpu_launches. */
+uint64_t hc_launch_count(void);
+
+/* Profiling hook (bench.py's roofline): record the two cudaEvent_t's (passed as void*)
+ * on the call's stream immediately before and after the NEXT quantized-key scan kernel
+ * launched by hc_decode_attention from this thread (one-shot; NULLs disable).  Inside
+ * stream capture they become external event-record nodes of the graph. */
+hc_status hc_profile_scan_events(void *begin_event, void *end_event);
+
 /* Key encoding, R1 ("represented as nearest neighbor of the centroids"):
  *   codes[i*code_stride + r] = argmin_m ||keys[r][i*dbar:(i+1)*dbar] - C[ci][m]||², ties -> lowest m.
  * keys [rows][d] fp16; codebook [cbg][c][dbar] fp32 (ONE layer's codebook);

@@ -20,7 +20,8 @@ HC_OK, HC_ERR_ARG, HC_ERR_SHAPE, HC_ERR_RANGE, HC_ERR_CAPACITY, HC_ERR_EMPTY, HC
     HC_ERR_NCCL, HC_ERR_UNSUPPORTED, HC_ERR_WORKSPACE = range(10)
 HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
 
-EXPORTS = ["hc_last_error", "hc_version", "hc_quantize_keys", "hc_append_kv",
+EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_events",
+           "hc_quantize_keys", "hc_append_kv",
            "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
            "hc_select_topk"]
 
@@ -70,6 +71,9 @@ def lib():
         p, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
         L.hc_last_error.restype = C.c_char_p
         L.hc_version.restype = C.c_char_p
+        L.hc_launch_count.restype = C.c_uint64
+        L.hc_profile_scan_events.argtypes = [p, p]
+        L.hc_profile_scan_events.restype = i32
         L.hc_quantize_keys.argtypes = [p, i64, p, hc_vq, p, i64, p]
         L.hc_quantize_keys.restype = i32
         L.hc_append_kv.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, p]
@@ -105,6 +109,17 @@ def _ptr(t):
 
 def version() -> str:
     return lib().hc_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels enqueued/captured by libhc so far (bench.py's gpu_launches)."""
+    return int(lib().hc_launch_count())
+
+
+def profile_scan_events(begin, end):
+    """Record torch.cuda.Event's around the next scan launch (one-shot)."""
+    _check(lib().hc_profile_scan_events(C.c_void_p(begin.cuda_event) if begin is not None else None,
+                                        C.c_void_p(end.cuda_event) if end is not None else None))
 
 
 def budget(tau: float, k_max: int, renorm: bool = False) -> hc_budget:

@@ -6,10 +6,23 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "../../include/hc.h"
 #include "hc_internal.h"
 
 using namespace hc;
+
+namespace hc {
+static std::atomic<unsigned long long> g_launches{0};
+static thread_local cudaEvent_t g_scan_ev[2] = {nullptr, nullptr};
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+void scan_events(cudaEvent_t *begin, cudaEvent_t *end) {
+  *begin = g_scan_ev[0];
+  *end = g_scan_ev[1];
+  g_scan_ev[0] = g_scan_ev[1] = nullptr;  // one-shot
+}
+}  // namespace hc
 
 namespace {
 
@@ -49,7 +62,32 @@ int next_pow2(int c) {
   return p;
 }
 
-constexpr int kGatherRows = 512;
+constexpr int kGatherRows = 256;
+constexpr int kMaxTSplit = 8;
+constexpr int kMaxScanSplit = 4;
+
+// Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
+// the group split so the work fills the SMs with the least shared-memory time, modelled
+// per SM as  lookups/5.2 + slice_bytes_streamed/100  cycles (+ partial write/reduce).
+void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int *tpt, int *split) {
+  double best = 1e300;
+  *tpt = 16; *split = 1;
+  for (int t : {8, 16}) {
+    const int64_t tile = 512LL * t;
+    const int64_t tiles = units * ((n + tile - 1) / tile);
+    for (int sp : {1, 2, 4}) {
+      if (sp > g) continue;
+      const int64_t items = tiles * sp;
+      const int64_t waves = (items + sms - 1) / sms;
+      const double gper = (double)((g + sp - 1) / sp);
+      double item = tile * gper / 5.2 + gper * cpow2 * G * 2 / 100.0;
+      if (sp > 1) item += tile * G * 4.0 / 64.0;  // partial stores
+      double cost = waves * item;
+      if (sp > 1) cost += (double)units * n * G * 4.0 * (sp + 1) / (sms * 64.0);  // reduce pass
+      if (cost < best * 0.999) { best = cost; *tpt = t; *split = sp; }
+    }
+  }
+}
 constexpr int kChunkTokens = 4096;
 
 struct Layout {
@@ -58,7 +96,7 @@ struct Layout {
   int nchunks_max;
   int gchunks;
   int64_t k_eff;
-  size_t o_hs, o_T, o_z, o_h1c, o_h2c, o_h1m, o_chunk, o_part, o_idx, o_w, total;
+  size_t o_hs, o_T, o_amax, o_z, o_zpart, o_h1c, o_h2c, o_h1m, o_chunk, o_part, o_idx, o_w, total;
   size_t hist_bytes;  // h1c + h2c + h1m (contiguous)
 };
 
@@ -78,7 +116,9 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
   size_t o = 0;
   L.o_hs = o; o += align256((size_t)rows * sizeof(HeadState));
   L.o_T = o; o += align256((size_t)B * Hkv * g * L.cpow2 * G * 2);
+  L.o_amax = o; o += align256((size_t)B * Hkv * g * kMaxTSplit * G * 4);
   L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
+  L.o_zpart = o; o += align256((size_t)kMaxScanSplit * rows * L.z_stride * 4);
   L.o_h1c = o; o += (size_t)rows * kNB * 4;
   L.o_h2c = o; o += (size_t)rows * kNB * 4;
   L.o_h1m = o; o += (size_t)rows * kNB * 8;
@@ -144,6 +184,14 @@ extern "C" {
 
 const char *hc_last_error(void) { return g_err; }
 const char *hc_version(void) { return "hcattn-b200 0.1 (sm_100a)"; }
+
+uint64_t hc_launch_count(void) { return g_launches.load(); }
+
+hc_status hc_profile_scan_events(void *begin_event, void *end_event) {
+  hc::g_scan_ev[0] = (cudaEvent_t)begin_event;
+  hc::g_scan_ev[1] = (cudaEvent_t)end_event;
+  return HC_OK;
+}
 
 hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *codebook, hc_vq vq,
                            uint16_t *codes, int64_t code_stride, hc_stream_t stream) {
@@ -280,6 +328,13 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   a.kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
   a.hs = (HeadState *)(w8 + Lw.o_hs);
   a.T = (int16_t *)(w8 + Lw.o_T);
+  a.amax_part = (float *)(w8 + Lw.o_amax);
+  {  // centroid splits: ~2 waves of 256-thread CTAs over units x groups
+    const int64_t base = B * H * g;
+    int ts = 1;
+    while (ts < kMaxTSplit && base * ts * 2 <= 2 * 148 * 8 && Lw.cpow2 / (ts * 2) >= 256) ts *= 2;
+    a.tsplit = ts;
+  }
   a.z = (float *)(w8 + Lw.o_z);
   a.z_stride = Lw.z_stride;
   a.h1c = (uint32_t *)(w8 + Lw.o_h1c);
@@ -298,15 +353,12 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   a.sel_k = sel_k;
   a.out = out;
   a.num_sms = num_sms();
-  a.scan_tpt = 16;
-  {  // choose the token tile so the scan fills the machine
-    const int64_t units = B * H;
-    const int64_t tiles16 = units * ((n_q + 8191) / 8192);
-    if (tiles16 < a.num_sms) a.scan_tpt = 8;
-  }
+  choose_scan(B * H, n_q, (int)g, Lw.cpow2, (int)G, a.num_sms, &a.scan_tpt, &a.scan_split);
+  a.zpart = (float *)(w8 + Lw.o_zpart);
 
   cudaError_t e;
   k_hs_init<<<(rows + 127) / 128, 128, 0, s>>>(a.hs, rows);
+  note_launch();
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "init");
   if ((e = cudaMemsetAsync(w8 + Lw.o_h1c, 0, Lw.hist_bytes, s)) != cudaSuccess) return cuda_check(e, "memset");
   if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
@@ -324,6 +376,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     if (dbg->z) {
       dim3 gz((unsigned)((n_cand + 255) / 256), (unsigned)rows);
       k_z_to_int<<<gz, 256, 0, s>>>(a.z, a.z_stride, dbg->z, n_cand);
+      note_launch();
       if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "debug z");
     }
     if (dbg->e || dbg->S || dbg->M || dbg->kstar) {
@@ -374,6 +427,7 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   uint32_t *chunk = (uint32_t *)(w8 + o);
   cudaError_t e;
   k_hs_init<<<(int)((rows + 127) / 128), 128, 0, s>>>(hs, (int)rows);
+  note_launch();
   if ((e = cudaMemsetAsync(hist, 0, (size_t)rows * kNB * 16, s)) != cudaSuccess) return cuda_check(e, "memset");
   const float kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
   if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s)) != cudaSuccess)

@@ -93,7 +93,9 @@ struct alignas(16) HeadState {
   int64_t kstar;        // k* if τ decided, else -1
   uint64_t sel_mass;    // mass of the kept set (renorm)
   uint32_t gather_done; // completion counter of the gather's last-block reduction
-  uint32_t pad[9];
+  uint32_t h1_done;     // completion counter of hist1 (last CTA runs bound1)
+  uint32_t h2_done;     // completion counter of hist2 (last CTA runs bound2)
+  uint32_t pad[7];
 };
 static_assert(sizeof(HeadState) == 128, "HeadState size");
 

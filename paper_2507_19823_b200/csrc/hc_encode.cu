@@ -28,9 +28,11 @@ __device__ __forceinline__ void load_centroid(const float *p, float (&c)[DBAR]) 
   }
 }
 
-// One CTA per (key row, group): lanes stride over centroids, each keeps the first
-// strict minimum in ascending m; the CTA reduces (dist, m) lexicographically, so the
-// result is argmin with ties to the lowest index -- identical to a sequential scan.
+// One CTA per (key row, group).  Thread t owns the contiguous centroid block
+// [t*per, (t+1)*per) and scans it in ascending m keeping the first strict minimum
+// (loads unrolled by 8 so they are all in flight together); the CTA then reduces
+// (dist, m) lexicographically.  Result: argmin with ties to the lowest index --
+// identical to a sequential scan (R1).
 template <int DBAR>
 __global__ void __launch_bounds__(256) k_encode(EncodeArgs a) {
   const int64_t r = blockIdx.x;
@@ -40,18 +42,28 @@ __global__ void __launch_bounds__(256) k_encode(EncodeArgs a) {
 #pragma unroll
   for (int e = 0; e < DBAR; ++e) kb[e] = h2f(krow[e]);
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
+  const int per = (a.c + blockDim.x - 1) / blockDim.x;
+  const int m0 = threadIdx.x * per;
+  const int m1 = min(a.c, m0 + per);
   float best = INFINITY;
   int bm = 0x7fffffff;
-  for (int m = threadIdx.x; m < a.c; m += blockDim.x) {
-    float cm[DBAR];
-    load_centroid<DBAR>(Ci + (int64_t)m * DBAR, cm);
-    float dist = 0.0f;
+  for (int mb = m0; mb < m1; mb += 8) {
+    float cm[8][DBAR];
 #pragma unroll
-    for (int e = 0; e < DBAR; ++e) {
-      float diff = __fsub_rn(kb[e], cm[e]);
-      dist = __fmaf_rn(diff, diff, dist);
+    for (int u = 0; u < 8; ++u)
+      if (mb + u < m1) load_centroid<DBAR>(Ci + (int64_t)(mb + u) * DBAR, cm[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (mb + u < m1) {
+        float dist = 0.0f;
+#pragma unroll
+        for (int e = 0; e < DBAR; ++e) {
+          const float diff = __fsub_rn(kb[e], cm[u][e]);
+          dist = __fmaf_rn(diff, diff, dist);
+        }
+        if (dist < best) { best = dist; bm = mb + u; }
+      }
     }
-    if (dist < best) { best = dist; bm = m; }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -83,11 +95,11 @@ cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s) {
   dim3 grid((unsigned)a.rows, (unsigned)a.g);
   const int dbar = a.d / a.g;
   switch (dbar) {
-    case 1: k_encode<1><<<grid, 256, 0, s>>>(a); break;
-    case 2: k_encode<2><<<grid, 256, 0, s>>>(a); break;
-    case 4: k_encode<4><<<grid, 256, 0, s>>>(a); break;
-    case 8: k_encode<8><<<grid, 256, 0, s>>>(a); break;
-    case 16: k_encode<16><<<grid, 256, 0, s>>>(a); break;
+    case 1: k_encode<1><<<grid, 256, 0, s>>>(a); note_launch(); break;
+    case 2: k_encode<2><<<grid, 256, 0, s>>>(a); note_launch(); break;
+    case 4: k_encode<4><<<grid, 256, 0, s>>>(a); note_launch(); break;
+    case 8: k_encode<8><<<grid, 256, 0, s>>>(a); note_launch(); break;
+    case 16: k_encode<16><<<grid, 256, 0, s>>>(a); note_launch(); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(256) k_rowcopy(RowCopyArgs a) {
 cudaError_t launch_rowcopy(const RowCopyArgs &a, cudaStream_t s) {
   if (a.rows <= 0) return cudaSuccess;
   k_rowcopy<<<(unsigned)((a.rows + 7) / 8), 256, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@
 namespace hc {
 
 constexpr int kGThreads = 256;
-constexpr int kGUnroll = 4;
+constexpr int kGUnroll = 8;
 
 __device__ __forceinline__ uint4 ld_nc(const uint16_t *p) {
   uint4 v;
@@ -113,6 +113,7 @@ cudaError_t launch_gather(const LayerArgs &a, cudaStream_t s) {
   const int slots = (kGThreads / 32) * (32 / lpr);
   const size_t smem = (size_t)slots * a.d * sizeof(float);
   k_gather<<<grid, kGThreads, smem, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 

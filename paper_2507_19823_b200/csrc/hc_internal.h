@@ -8,6 +8,11 @@
 
 namespace hc {
 
+// number of kernels this library has enqueued (or captured into a graph)
+void note_launch(int n = 1);
+// profiling hook: events recorded around the next scan launch (may be null)
+void scan_events(cudaEvent_t *begin, cudaEvent_t *end);
+
 // row -> element offset:  (r / R1) * s1 + (r % R1) * s2 + s0
 struct RowMap {
   int64_t R1, s1, s2, s0;
@@ -59,6 +64,8 @@ struct LayerArgs {
   // workspace
   HeadState *hs;          // [B*Hq]
   int16_t *T;             // [units][g][cpow2][G]
+  float *amax_part;       // [units][g][tsplit][G] partial max |t|
+  int tsplit;             // centroid splits per (unit, group) in the table kernels
   float *z;               // [B*Hq][z_stride]
   int64_t z_stride;
   uint32_t *h1c;          // [B*Hq][kNB]
@@ -76,7 +83,9 @@ struct LayerArgs {
   int64_t *sel_k;         // [B*Hq] (may be null)
   float *out;             // [B*Hq][d]
   int num_sms;
-  int scan_tpt;
+  int scan_tpt;           // tokens per thread in the scan (8 or 16)
+  int scan_split;         // group splits per token tile (1 = write z directly)
+  float *zpart;           // [scan_split][B*Hq][z_stride] partial sums when scan_split > 1
 };
 
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);

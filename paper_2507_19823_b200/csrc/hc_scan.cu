@@ -101,14 +101,15 @@ __device__ __forceinline__ void lookup8(const uint4 &c, const uint8_t *sb, uint3
 }
 
 template <int G>
-__device__ __forceinline__ void store_chunk(const LayerArgs &a, int b, int kv, int64_t tok,
-                                            const int (&acc)[8][G], int (&mx)[G], int (&mn)[G]) {
+__device__ __forceinline__ void store_chunk(const LayerArgs &a, float *zbase, int b, int kv,
+                                            int64_t tok, const int (&acc)[8][G], int (&mx)[G],
+                                            int (&mn)[G]) {
   if (tok >= a.n_q) return;
   const int64_t rem_ = a.n_q - tok;
   const int nval = rem_ < 8 ? (int)rem_ : 8;
 #pragma unroll
   for (int h = 0; h < G; ++h) {
-    float *zp = a.z + ((int64_t)b * a.Hq + kv * G + h) * a.z_stride + tok;
+    float *zp = zbase + ((int64_t)b * a.Hq + kv * G + h) * a.z_stride + tok;
     if (nval == 8) {
       float4 v0 = make_float4((float)acc[0][h], (float)acc[1][h], (float)acc[2][h], (float)acc[3][h]);
       float4 v1 = make_float4((float)acc[4][h], (float)acc[5][h], (float)acc[6][h], (float)acc[7][h]);
@@ -132,9 +133,13 @@ __device__ __forceinline__ void store_chunk(const LayerArgs &a, int b, int kv, i
   }
 }
 
+// Work item = (unit, token tile, group split).  With nsplit > 1 each item sums only
+// its groups [i0, i1) and writes the exact integer partial to zpart[split]; k_zreduce
+// adds the partials (exact: integers < 2^24 in fp32) -- so small-context configs can
+// spread one unit's tokens AND groups over all SMs without re-streaming every slice.
 template <int G, int TPT>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles_per_unit,
-                                                           int total_tiles) {
+                                                           int total_tiles, int nsplit) {
   static_assert(TPT == 8 || TPT == 16, "TPT");
   constexpr int kChunks = TPT / 8;                     // 8-token chunks per thread
   constexpr int kTile = kScanThreads * TPT;            // tokens per tile
@@ -153,18 +158,25 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
   const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+  const int gper = (a.g + nsplit - 1) / nsplit;
+  for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
+    const int sp = item % nsplit;
+    const int tile = item / nsplit;
     const int u = tile / tiles_per_unit;
     const int tk = tile - u * tiles_per_unit;
+    const int i0 = sp * gper;
+    const int i1 = min(a.g, i0 + gper);
+    const int ng = i1 - i0;
     const int b = u / a.Hkv, kv = u - b * a.Hkv;
     const int64_t t0 = (int64_t)tk * kTile + (int64_t)warp * (32 * TPT);
     const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride + (int64_t)kv * a.g * a.n_cap;
-    const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + (int64_t)u * a.g * slice_bytes;
+    const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
+    P += (int64_t)i0 * a.n_cap;
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bar[0], slice_bytes);
       bulk_g2s(buf0, Tu, slice_bytes, &bar[0]);
-      if (a.g > 1) {
+      if (ng > 1) {
         mbar_expect_tx(&bar[1], slice_bytes);
         bulk_g2s(buf1, Tu + slice_bytes, slice_bytes, &bar[1]);
       }
@@ -187,9 +199,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) cur[k] = val[k] ? ld_stream(P + tok[k]) : make_uint4(0, 0, 0, 0);
 
-    for (int i = 0; i < a.g; ++i) {
+    for (int i = 0; i < ng; ++i) {
       uint4 nxt[kChunks];
-      if (i + 1 < a.g) {
+      if (i + 1 < ng) {
 #pragma unroll
         for (int k = 0; k < kChunks; ++k)
           nxt[k] = val[k] ? ld_stream(P + (int64_t)(i + 1) * a.n_cap + tok[k]) : make_uint4(0, 0, 0, 0);
@@ -201,13 +213,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
 #pragma unroll
       for (int k = 0; k < kChunks; ++k) lookup8<G>(cur[k], sb, mask, acc[k]);
       __syncthreads();
-      if (threadIdx.x == 0 && i + 2 < a.g) {
+      if (threadIdx.x == 0 && i + 2 < ng) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         uint64_t *bb = odd ? &bar[1] : &bar[0];
         mbar_expect_tx(bb, slice_bytes);
         bulk_g2s(odd ? buf1 : buf0, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, bb);
       }
-      if (i + 1 < a.g) {
+      if (i + 1 < ng) {
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) cur[k] = nxt[k];
       }
@@ -215,8 +227,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
     int mx[G], mn[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
+    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
 #pragma unroll
-    for (int k = 0; k < kChunks; ++k) store_chunk<G>(a, b, kv, tok[k], acc[k], mx, mn);
+    for (int k = 0; k < kChunks; ++k) store_chunk<G>(a, zbase, b, kv, tok[k], acc[k], mx, mn);
+    if (nsplit > 1) continue;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       const int vmx = __reduce_max_sync(0xffffffffu, mx[h]);
@@ -230,19 +244,78 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
   }
 }
 
+// exact sum of the split partials -> z, and the per-head max / min
+__global__ void __launch_bounds__(256) k_zreduce(LayerArgs a, int nsplit) {
+  const int row = blockIdx.y;
+  const int64_t j = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+  int mx = INT_MIN, mn = INT_MAX;
+  if (j < a.n_q) {
+    const int64_t plane = (int64_t)a.B * a.Hq * a.z_stride;
+    const float *src = a.zpart + (int64_t)row * a.z_stride + j;
+    float4 acc = *reinterpret_cast<const float4 *>(src);
+    for (int sp = 1; sp < nsplit; ++sp) {
+      const float4 v = *reinterpret_cast<const float4 *>(src + sp * plane);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
+    float *dst = a.z + (int64_t)row * a.z_stride + j;
+    if (j + 4 <= a.n_q) {
+      *reinterpret_cast<float4 *>(dst) = acc;
+    } else {  // never touch z[n_q..]: the resident tokens' scores live there
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j + u < a.n_q) dst[u] = vv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j + u < a.n_q) {
+        const int zi = (int)vv[u];
+        mx = max(mx, zi);
+        mn = min(mn, zi);
+      }
+    }
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  if ((threadIdx.x & 31) == 0 && mx != INT_MIN) {
+    atomicMax(&a.hs[row].M, mx);
+    atomicMin(&a.hs[row].zmin, mn);
+  }
+}
+
 template <int G, int TPT>
 static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   constexpr int kTile = kScanThreads * TPT;
   const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
   const int units = a.B * a.Hkv;
-  const int total = tiles_per_unit * units;
+  const int nsplit = a.scan_split;
+  const int total = tiles_per_unit * units * nsplit;
   if (total == 0) return cudaSuccess;
   const size_t smem = (size_t)2 * a.cpow2 * G * 2 + 16;
-  cudaError_t e = cudaFuncSetAttribute(k_scan<G, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
+  static int configured[64] = {0};  // per device: opt in to the full 227 KB once
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan<G, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured[dev] = 1;
+  }
   const int grid = total < a.num_sms ? total : a.num_sms;
-  k_scan<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total);
+  cudaEvent_t eb, ee;
+  scan_events(&eb, &ee);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
+  k_scan<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  note_launch();
+  if (nsplit > 1) {
+    dim3 gr((unsigned)((a.n_q + 1023) / 1024), (unsigned)(a.B * a.Hq));
+    k_zreduce<<<gr, 256, 0, s>>>(a, nsplit);
+    note_launch();
+  }
+  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
 }
 

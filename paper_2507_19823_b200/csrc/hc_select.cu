@@ -33,10 +33,30 @@ __device__ __forceinline__ uint32_t delta_of(const HeadState &h, float zf) {
   return (uint32_t)(h.M - __float2int_rn(zf));
 }
 
+__device__ void bound1_row(const SelArgs &a, int row);
+__device__ void bound2_row(const SelArgs &a, int row);
+
+// "last CTA done" for per-row multi-CTA passes: every CTA fences its global atomics,
+// bumps the row counter, and the CTA that completes it runs the row's bound step.
+__device__ __forceinline__ bool last_cta(uint32_t *counter, unsigned nctas) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counter, 1u);
+    s_last = (prev == nctas - 1);
+    if (s_last) *counter = 0;  // reset for the next use of the workspace
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
 // ---------------------------------------------------------------- pass 1
 __global__ void __launch_bounds__(kSelThreads) k_hist1(SelArgs a, int64_t per_cta) {
-  __shared__ uint32_t cnt[kNB];
-  __shared__ unsigned long long ms[kNB];
+  extern __shared__ __align__(16) uint8_t hsm[];  // 48 KiB dynamic: mass u64[kNB], count u32[kNB]
+  unsigned long long *ms = reinterpret_cast<unsigned long long *>(hsm);
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(hsm + kNB * 8);
   const int row = blockIdx.y;
   const HeadState h = a.hs[row];
   const int shift = row_shift(h);
@@ -72,6 +92,7 @@ __global__ void __launch_bounds__(kSelThreads) k_hist1(SelArgs a, int64_t per_ct
       if (ms[i]) atomicAdd(&a.h1m[(int64_t)row * kNB + i], ms[i]);
     }
   }
+  if (last_cta(&a.hs[row].h1_done, gridDim.x)) bound1_row(a, row);
 }
 
 // block-wide exclusive scan of (uint64, uint64) pairs, returns totals
@@ -101,15 +122,19 @@ __device__ __forceinline__ void block_scan2(T &x, T &y, T &tx, T &ty) {
 }
 
 // ---------------------------------------------------------------- bound 1
-__global__ void __launch_bounds__(kSelThreads) k_bound1(SelArgs a) {
-  const int row = blockIdx.x;
+__device__ void bound1_row(const SelArgs &a, int row) {
   HeadState *hs = a.hs + row;
   const uint32_t *hc = a.h1c + (int64_t)row * kNB + threadIdx.x * kBinsPerThread;
   const unsigned long long *hm = a.h1m + (int64_t)row * kNB + threadIdx.x * kBinsPerThread;
   uint64_t c[kBinsPerThread], m[kBinsPerThread];
   uint64_t lc = 0, lm = 0;
 #pragma unroll
-  for (int k = 0; k < kBinsPerThread; ++k) { c[k] = hc[k]; m[k] = hm[k]; lc += c[k]; lm += m[k]; }
+  for (int k = 0; k < kBinsPerThread; ++k) {
+    c[k] = __ldcg(hc + k);
+    m[k] = __ldcg(hm + k);
+    lc += c[k];
+    lm += m[k];
+  }
   uint64_t pc = lc, pm = lm, tc, tm;
   block_scan2<uint64_t>(pc, pm, tc, tm);  // pc, pm: exclusive prefix of this thread's bins
   const uint64_t S = tm;
@@ -183,13 +208,19 @@ __global__ void __launch_bounds__(kSelThreads) k_hist2(SelArgs a, int64_t per_ct
   __syncthreads();
   for (int i = threadIdx.x; i < kNB; i += kSelThreads)
     if (cnt[i]) atomicAdd(&a.h2c[(int64_t)row * kNB + i], cnt[i]);
+  if (last_cta(&a.hs[row].h2_done, gridDim.x)) bound2_row(a, row);
 }
 
 // ---------------------------------------------------------------- bound 2
-__global__ void __launch_bounds__(kSelThreads) k_bound2(SelArgs a) {
-  const int row = blockIdx.x;
+__device__ void bound2_row(const SelArgs &a, int row) {
   HeadState *hs = a.hs + row;
-  const HeadState h = *hs;
+  HeadState h;
+  h.bstar = __ldcg(&hs->bstar);
+  h.shift = __ldcg(&hs->shift);
+  h.kappa = __ldcg(&hs->kappa);
+  h.cnt_before = __ldcg(&hs->cnt_before);
+  h.mass_before = __ldcg(&hs->mass_before);
+  h.theta = __ldcg(&hs->theta);
   if (h.bstar >= kNB) return;
   const uint32_t dbase = (uint32_t)h.bstar << h.shift;
   const int v0 = threadIdx.x * kBinsPerThread;
@@ -198,7 +229,7 @@ __global__ void __launch_bounds__(kSelThreads) k_bound2(SelArgs a) {
   uint64_t lc = 0, lm = 0;
 #pragma unroll
   for (int k = 0; k < kBinsPerThread; ++k) {
-    c[k] = hc[k];
+    c[k] = __ldcg(hc + k);
     w[k] = c[k] ? mass(dbase | (uint32_t)(v0 + k), h.kappa) : 0ull;
     lc += c[k];
     lm += c[k] * w[k];
@@ -353,13 +384,23 @@ cudaError_t launch_select(const SelArgs &a, cudaStream_t s) {
   per_cta = (per_cta + 3) / 4 * 4;
   ctas_per_row = (a.n + per_cta - 1) / per_cta;
   dim3 g12((unsigned)ctas_per_row, (unsigned)a.rows);
-  k_hist1<<<g12, kSelThreads, 0, s>>>(a, per_cta);
-  k_bound1<<<a.rows, kSelThreads, 0, s>>>(a);
-  k_hist2<<<g12, kSelThreads, 0, s>>>(a, per_cta);
-  k_bound2<<<a.rows, kSelThreads, 0, s>>>(a);
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_hist1, cudaFuncAttributeMaxDynamicSharedMemorySize, kNB * 12);
+    if (e != cudaSuccess) return e;
+    configured[dev] = 1;
+  }
+  k_hist1<<<g12, kSelThreads, kNB * 12, s>>>(a, per_cta);  // + bound1 in each row's last CTA
+  note_launch();
+  k_hist2<<<g12, kSelThreads, 0, s>>>(a, per_cta);  // + bound2 in each row's last CTA
+  note_launch();
   dim3 g34((unsigned)a.nchunks, (unsigned)a.rows);
   k_count<<<g34, kSelThreads, 0, s>>>(a);
+  note_launch();
   k_write<<<g34, kSelThreads, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -410,6 +451,7 @@ cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t 
                                      int64_t z_stride, HeadState *hs, float kappa0,
                                      cudaStream_t s) {
   k_float_prep<<<(unsigned)rows, kSelThreads, 0, s>>>(scores, n, z, z_stride, hs, kappa0);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -22,8 +22,20 @@ __device__ __forceinline__ void table_entry(const float (&qs)[G][DBAR], const fl
   for (int h = 0; h < G; ++h) t[h] = 0.0f;
   if (m < c) {
     float cm[DBAR];
+    const float *cp = Ci + (int64_t)m * DBAR;
+    if constexpr (DBAR % 4 == 0) {
 #pragma unroll
-    for (int e = 0; e < DBAR; ++e) cm[e] = __ldg(Ci + (int64_t)m * DBAR + e);
+      for (int e = 0; e < DBAR; e += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(cp + e));
+        cm[e] = v.x; cm[e + 1] = v.y; cm[e + 2] = v.z; cm[e + 3] = v.w;
+      }
+    } else if constexpr (DBAR == 2) {
+      const float2 v = __ldg(reinterpret_cast<const float2 *>(cp));
+      cm[0] = v.x; cm[1] = v.y;
+    } else {
+#pragma unroll
+      for (int e = 0; e < DBAR; ++e) cm[e] = __ldg(cp + e);
+    }
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       float acc = __fmul_rn(qs[h][0], cm[0]);
@@ -34,15 +46,21 @@ __device__ __forceinline__ void table_entry(const float (&qs)[G][DBAR], const fl
   }
 }
 
-// PHASE 0: per-head max |t| (atomicMax on non-negative float bits).
-// PHASE 1: quantise with e_h and store the packed G x int16 entries.
+// PHASE 0: per-(unit, group, split) max |t| of each head -> amax_part (plain stores,
+//          no atomics).
+// PHASE 1: every CTA reduces its heads' g*csplit partial maxima -> A_h -> e_h (R2),
+//          recomputes its entries (same FMA chain) and stores the packed G x int16.
+// One CTA = (unit, group i, centroid split); each thread owns kTCPT consecutive
+// centroids (vectorised codebook loads, all issued before use).
 template <int G, int DBAR, int PHASE>
 __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   const int u = blockIdx.z;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int i = blockIdx.y;
-  const int m = blockIdx.x * kTB + threadIdx.x;
+  const int split = blockIdx.x;
   const int hq0 = kv * G;
+  const int per = a.cpow2 / gridDim.x;          // centroids of this CTA
+  const int m0 = split * per;
   float qs[G][DBAR];
 #pragma unroll
   for (int h = 0; h < G; ++h)
@@ -50,14 +68,69 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
     for (int e = 0; e < DBAR; ++e)
       qs[h][e] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + i * DBAR + e));
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
-  float t[G];
-  table_entry<G, DBAR>(qs, Ci, m, a.c, t);
   HeadState *hs = a.hs + (int64_t)b * a.Hq + hq0;
+  float *part = a.amax_part + ((int64_t)u * a.g * gridDim.x) * G;  // [g*csplit][G] of this unit
+  float sc[G];
+  if (PHASE == 1) {
+    // A_h = max over all partial maxima of the head (g * csplit values)
+    __shared__ float sA[G][kTB / 32];
+    const int np = a.g * gridDim.x;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float v = 0.0f;
+      for (int k = threadIdx.x; k < np; k += kTB) v = fmaxf(v, part[(int64_t)k * G + h]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+      if ((threadIdx.x & 31) == 0) sA[h][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float A = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kTB / 32; ++w) A = fmaxf(A, sA[h][w]);
+      const int e = scale_exponent(A);
+      sc[h] = pow2f(e);
+      if (i == 0 && split == 0 && threadIdx.x == 0) {
+        hs[h].e = e;
+        hs[h].kappa = __fmul_rn(a.kappa0, pow2f(-e));
+        hs[h].amax = __float_as_uint(A);
+      }
+    }
+  }
+  float mx[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) mx[h] = 0.0f;
+  for (int m = m0 + threadIdx.x; m < m0 + per; m += kTB) {
+    float t[G];
+    table_entry<G, DBAR>(qs, Ci, m, a.c, t);
+    if (PHASE == 0) {
+#pragma unroll
+      for (int h = 0; h < G; ++h) mx[h] = fmaxf(mx[h], fabsf(t[h]));
+    } else {
+      int16_t packed[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t(t[h], sc[h]);
+      int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
+      if constexpr (G == 4) {
+        uint2 v;
+        v.x = (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
+        v.y = (uint32_t)(uint16_t)packed[2] | ((uint32_t)(uint16_t)packed[3] << 16);
+        *reinterpret_cast<uint2 *>(dst) = v;
+      } else if constexpr (G == 2) {
+        *reinterpret_cast<uint32_t *>(dst) =
+            (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
+      } else {
+#pragma unroll
+        for (int h = 0; h < G; ++h) dst[h] = packed[h];
+      }
+    }
+  }
   if (PHASE == 0) {
     __shared__ float red[G][kTB / 32];
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      float v = fabsf(t[h]);
+      float v = mx[h];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
       if ((threadIdx.x & 31) == 0) red[h][threadIdx.x >> 5] = v;
@@ -67,41 +140,18 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
       float v = 0.0f;
 #pragma unroll
       for (int w = 0; w < kTB / 32; ++w) v = fmaxf(v, red[threadIdx.x][w]);
-      atomicMax(&hs[threadIdx.x].amax, __float_as_uint(v));
-    }
-  } else {
-    int16_t packed[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const int e = scale_exponent(__uint_as_float(hs[h].amax));
-      packed[h] = (int16_t)quant_t(t[h], pow2f(e));
-    }
-    int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
-    if constexpr (G == 4) {
-      uint2 v;
-      v.x = (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
-      v.y = (uint32_t)(uint16_t)packed[2] | ((uint32_t)(uint16_t)packed[3] << 16);
-      *reinterpret_cast<uint2 *>(dst) = v;
-    } else if constexpr (G == 2) {
-      *reinterpret_cast<uint32_t *>(dst) =
-          (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
-    } else {
-#pragma unroll
-      for (int h = 0; h < G; ++h) dst[h] = packed[h];
-    }
-    if (blockIdx.x == 0 && i == 0 && threadIdx.x < G) {
-      const int e = scale_exponent(__uint_as_float(hs[threadIdx.x].amax));
-      hs[threadIdx.x].e = e;
-      hs[threadIdx.x].kappa = __fmul_rn(a.kappa0, pow2f(-e));
+      part[((int64_t)i * gridDim.x + split) * G + threadIdx.x] = v;
     }
   }
 }
 
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
-  dim3 grid((unsigned)(a.cpow2 / kTB), (unsigned)a.g, (unsigned)(a.B * a.Hkv));
+  dim3 grid((unsigned)a.tsplit, (unsigned)a.g, (unsigned)(a.B * a.Hkv));
   k_table<G, DBAR, 0><<<grid, kTB, 0, s>>>(a);
+  note_launch();
   k_table<G, DBAR, 1><<<grid, kTB, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -142,8 +192,7 @@ __global__ void __launch_bounds__(128) k_resident(LayerArgs a) {
   float acc = 0.0f;
   for (int e = 0; e < a.d; ++e) acc = __fmaf_rn(h2f(__ldg(qrow + e)), h2f(__ldg(krow + e)), acc);
   HeadState *hs = a.hs + (int64_t)b * a.Hq + hq;
-  const int ex = scale_exponent(__uint_as_float(hs->amax));
-  const int zq = quant_res(acc, pow2f(ex));
+  const int zq = quant_res(acc, pow2f(hs->e));
   a.z[((int64_t)b * a.Hq + hq) * a.z_stride + a.n_q + r] = (float)zq;
   atomicMax(&hs->M, zq);
   atomicMin(&hs->zmin, zq);
@@ -154,6 +203,7 @@ cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s) {
   const int64_t work = a.n_res * a.G;
   dim3 grid((unsigned)((work + 127) / 128), (unsigned)(a.B * a.Hkv));
   k_resident<<<grid, 128, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
