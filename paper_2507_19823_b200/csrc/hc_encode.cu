@@ -28,80 +28,111 @@ __device__ __forceinline__ void load_centroid(const float *p, float (&c)[DBAR]) 
   }
 }
 
-// One CTA per (key row, group).  Thread t owns the contiguous centroid block
-// [t*per, (t+1)*per) and scans it in ascending m keeping the first strict minimum
-// (loads unrolled by 8 so they are all in flight together); the CTA then reduces
-// (dist, m) lexicographically.  Result: argmin with ties to the lowest index --
-// identical to a sequential scan (R1).
+// One CTA (1024 threads) per (chunk of up to kER key rows, group i): the group's
+// codebook slice is read ONCE per CTA (coalesced: thread t takes centroids
+// t, t+1024, ...; loads unrolled so they are all in flight) and scored against all
+// rows of the chunk.  Each thread keeps, per row, the first strict minimum over its
+// centroids (ascending m); the CTA reduces (dist, m) lexicographically -> argmin
+// with ties to the lowest index, identical to a sequential scan (R1).
+constexpr int kEThreads = 512;
+template <int DBAR> struct EncCfg {
+  static constexpr int kER = DBAR <= 4 ? 8 : (DBAR == 8 ? 4 : 2);  // key rows per CTA
+  static constexpr int kU = DBAR <= 2 ? 8 : (DBAR == 4 ? 4 : 2);   // centroid loads in flight
+};
+
 template <int DBAR>
-__global__ void __launch_bounds__(256) k_encode(EncodeArgs a) {
-  const int64_t r = blockIdx.x;
+__global__ void __launch_bounds__(kEThreads) k_encode(EncodeArgs a) {
+  constexpr int kER = EncCfg<DBAR>::kER;
+  constexpr int kU = EncCfg<DBAR>::kU;
+  const int64_t r0 = (int64_t)blockIdx.x * kER;
+  const int64_t left = a.rows - r0;
+  const int nr = left < kER ? (int)left : kER;
   const int i = blockIdx.y;
-  const uint16_t *krow = a.keys + rowoff(a.kmap, r) + (int64_t)i * DBAR;
-  float kb[DBAR];
+  float kb[kER][DBAR];
 #pragma unroll
-  for (int e = 0; e < DBAR; ++e) kb[e] = h2f(krow[e]);
+  for (int r = 0; r < kER; ++r) {
+    const uint16_t *krow = a.keys + rowoff(a.kmap, r0 + (r < nr ? r : 0)) + (int64_t)i * DBAR;
+#pragma unroll
+    for (int e = 0; e < DBAR; ++e) kb[r][e] = h2f(krow[e]);
+  }
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
-  const int per = (a.c + blockDim.x - 1) / blockDim.x;
-  const int m0 = threadIdx.x * per;
-  const int m1 = min(a.c, m0 + per);
-  float best = INFINITY;
-  int bm = 0x7fffffff;
-  for (int mb = m0; mb < m1; mb += 8) {
-    float cm[8][DBAR];
+  float best[kER];
+  int bm[kER];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (mb + u < m1) load_centroid<DBAR>(Ci + (int64_t)(mb + u) * DBAR, cm[u]);
+  for (int r = 0; r < kER; ++r) { best[r] = INFINITY; bm[r] = 0x7fffffff; }
+  for (int mb = threadIdx.x; mb < a.c; mb += kEThreads * kU) {
+    float cm[kU][DBAR];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (mb + u < m1) {
-        float dist = 0.0f;
+    for (int u = 0; u < kU; ++u) {
+      const int m = mb + u * kEThreads;
+      if (m < a.c) load_centroid<DBAR>(Ci + (int64_t)m * DBAR, cm[u]);
+    }
 #pragma unroll
-        for (int e = 0; e < DBAR; ++e) {
-          const float diff = __fsub_rn(kb[e], cm[u][e]);
-          dist = __fmaf_rn(diff, diff, dist);
+    for (int u = 0; u < kU; ++u) {
+      const int m = mb + u * kEThreads;
+      if (m < a.c) {
+#pragma unroll
+        for (int r = 0; r < kER; ++r) {
+          float dist = 0.0f;
+#pragma unroll
+          for (int e = 0; e < DBAR; ++e) {
+            const float diff = __fsub_rn(kb[r][e], cm[u][e]);
+            dist = __fmaf_rn(diff, diff, dist);
+          }
+          if (dist < best[r]) { best[r] = dist; bm[r] = m; }
         }
-        if (dist < best) { best = dist; bm = mb + u; }
       }
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    float ob = __shfl_xor_sync(0xffffffffu, best, off);
-    int om = __shfl_xor_sync(0xffffffffu, bm, off);
-    if (ob < best || (ob == best && om < bm)) { best = ob; bm = om; }
-  }
-  __shared__ float sb[8];
-  __shared__ int sm[8];
+  __shared__ float sb[kER][kEThreads / 32];
+  __shared__ int sm[kER][kEThreads / 32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) { sb[w] = best; sm[w] = bm; }
-  __syncthreads();
-  if (w == 0) {
-    const int nw = blockDim.x >> 5;
-    best = l < nw ? sb[l] : INFINITY;
-    bm = l < nw ? sm[l] : 0x7fffffff;
+#pragma unroll
+  for (int r = 0; r < kER; ++r) {
+    float b_ = best[r];
+    int m_ = bm[r];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      float ob = __shfl_xor_sync(0xffffffffu, best, off);
-      int om = __shfl_xor_sync(0xffffffffu, bm, off);
-      if (ob < best || (ob == best && om < bm)) { best = ob; bm = om; }
+      const float ob = __shfl_xor_sync(0xffffffffu, b_, off);
+      const int om = __shfl_xor_sync(0xffffffffu, m_, off);
+      if (ob < b_ || (ob == b_ && om < m_)) { b_ = ob; m_ = om; }
     }
-    if (l == 0) a.codes[rowoff(a.omap, r) + (int64_t)i * a.gstride] = (uint16_t)bm;
+    if (l == 0) { sb[r][w] = b_; sm[r][w] = m_; }
+  }
+  __syncthreads();
+  if (w < nr) {  // warp r reduces row r
+    const int r = w;
+    float b_ = l < kEThreads / 32 ? sb[r][l] : INFINITY;
+    int m_ = l < kEThreads / 32 ? sm[r][l] : 0x7fffffff;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, b_, off);
+      const int om = __shfl_xor_sync(0xffffffffu, m_, off);
+      if (ob < b_ || (ob == b_ && om < m_)) { b_ = ob; m_ = om; }
+    }
+    if (l == 0) a.codes[rowoff(a.omap, r0 + r) + (int64_t)i * a.gstride] = (uint16_t)m_;
   }
 }
 
 cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s) {
   if (a.rows <= 0) return cudaSuccess;
-  dim3 grid((unsigned)a.rows, (unsigned)a.g);
   const int dbar = a.d / a.g;
+#define HC_ENC(D)                                                                        \
+  {                                                                                      \
+    dim3 grid((unsigned)((a.rows + EncCfg<D>::kER - 1) / EncCfg<D>::kER), (unsigned)a.g); \
+    k_encode<D><<<grid, kEThreads, 0, s>>>(a);                                           \
+    note_launch();                                                                       \
+    break;                                                                               \
+  }
   switch (dbar) {
-    case 1: k_encode<1><<<grid, 256, 0, s>>>(a); note_launch(); break;
-    case 2: k_encode<2><<<grid, 256, 0, s>>>(a); note_launch(); break;
-    case 4: k_encode<4><<<grid, 256, 0, s>>>(a); note_launch(); break;
-    case 8: k_encode<8><<<grid, 256, 0, s>>>(a); note_launch(); break;
-    case 16: k_encode<16><<<grid, 256, 0, s>>>(a); note_launch(); break;
+    case 1: HC_ENC(1)
+    case 2: HC_ENC(2)
+    case 4: HC_ENC(4)
+    case 8: HC_ENC(8)
+    case 16: HC_ENC(16)
     default: return cudaErrorInvalidValue;
   }
+#undef HC_ENC
   return cudaGetLastError();
 }
 

@@ -98,11 +98,28 @@ __global__ void __launch_bounds__(kGThreads) k_gather(LayerArgs a) {
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // deterministic parallel sum of the chunk partials: thread -> (dim e, part p);
+  // part p sums chunks p, p+np, ... with 4 independent accumulators, then the parts
+  // are added in order.
   const float *p0 = a.partial + (int64_t)row * a.gchunks * a.d;
-  for (int e = threadIdx.x; e < a.d; e += kGThreads) {
+  const int np = kGThreads / a.d;  // >= 1 since d <= 256
+  const int e = threadIdx.x % a.d, pp = threadIdx.x / a.d;
+  float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if (pp < np) {
+    int c = pp;
+    for (; c + 3 * np < a.gchunks; c += 4 * np) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s4[q] += __ldcg(p0 + (int64_t)(c + q * np) * a.d + e);
+    }
+    for (; c < a.gchunks; c += np) s4[0] += __ldcg(p0 + (int64_t)c * a.d + e);
+  }
+  __syncthreads();
+  if (pp < np) sred[pp * a.d + e] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  __syncthreads();
+  if (threadIdx.x < a.d) {
     float s = 0.0f;
-    for (int c = 0; c < a.gchunks; ++c) s += __ldcg(p0 + (int64_t)c * a.d + e);
-    a.out[(int64_t)row * a.d + e] = s;
+    for (int q = 0; q < np; ++q) s += sred[q * a.d + threadIdx.x];
+    a.out[(int64_t)row * a.d + threadIdx.x] = s;
   }
   if (threadIdx.x == 0) hs->gather_done = 0;
 }

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   float mx[G];
 #pragma unroll
   for (int h = 0; h < G; ++h) mx[h] = 0.0f;
+#pragma unroll 4
   for (int m = m0 + threadIdx.x; m < m0 + per; m += kTB) {
     float t[G];
     table_entry<G, DBAR>(qs, Ci, m, a.c, t);
