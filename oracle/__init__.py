@@ -47,6 +47,9 @@ def lib():
             L.or_reconstruct.argtypes = [p, i64, i32, i32, i32, i32, p, p]
             L.or_scale_exponent.argtypes = [f32]; L.or_scale_exponent.restype = i32
             L.or_table.argtypes = [p, i32, i32, i32, i32, i32, p, p, p, p]
+            L.or_codebook_absmax.argtypes = [p, i32, i32, i32, p]
+            L.or_table_bound.argtypes = [p, i32, i32, i32, p]
+            L.or_table_bound.restype = f32
             L.or_scores.argtypes = [p, p, i64, i64, i32, i32, p]
             L.or_resident_scores.argtypes = [p, p, i64, i32, i32, p]
             L.or_kappa.argtypes = [i32, i32]; L.or_kappa.restype = f32
@@ -105,6 +108,21 @@ def table(q, C_, g: int):
     e = np.empty(G, dtype=np.int32)
     lib().or_table(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(T32), _ptr(Tfx), _ptr(e))
     return T32, Tfx, e
+
+
+def codebook_absmax(C_) -> np.ndarray:
+    """Cabs[ci][e] = max_m |C[ci][m][e]| (R2)."""
+    C_ = _c(C_, np.float32)
+    cbg, c, dbar = C_.shape
+    out = np.empty((cbg, dbar), np.float32)
+    lib().or_codebook_absmax(_ptr(C_), cbg, c, dbar, _ptr(out))
+    return out
+
+
+def table_bound(q_head, C_, g: int) -> float:
+    q = _c(q_head, np.float16)
+    Ca = codebook_absmax(C_)
+    return lib().or_table_bound(_ptr(q.view(np.uint16)), q.shape[0], g, C_.shape[0], _ptr(Ca))
 
 
 def scores(Tfx_head, P_groupmajor, n: int) -> np.ndarray:

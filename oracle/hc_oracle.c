@@ -103,7 +103,11 @@ OR_EXPORT void or_reconstruct(const uint16_t *codes, int64_t n, int d, int g, in
 /* ------------------------------------------------------------------------
  * R2 -- query/codebook table.  P:229: "T = q̄·C where T ∈ R^{g×c}".
  *   t = q[i*dbar]*C[i][m][0]; t = fmaf(q[i*dbar+e], C[i][m][e], t), e=1..dbar-1
- * Fixed-point storage (DESIGN R2): A = max |t| over the head's whole table;
+ * Fixed-point storage (DESIGN R2): one power-of-two scale per query head from the
+ * Cauchy-Schwarz-style bound (computable before any table entry exists):
+ *   Cabs[ci][e] = max_m |C[ci][m][e]|
+ *   A_i = |q_0|*Cabs[ci][0]; A_i = fmaf(|q_e|, Cabs[ci][e], A_i)   (same chain as t)
+ *   A   = max_i A_i    (>= |t| for every entry, exactly, by monotone rounding)
  *   e_h = 100 if A < 2^-100 else clamp(14 - floor(log2 A), -100, 100);
  *   T_fx = clamp(rint(t * 2^e_h), -32767, 32767)   (rint = ties-to-even).
  * q [G][d] fp16 -> T32 [G][g][c] fp32 (may be NULL), Tfx [G][g][c] int16, e [G].
@@ -114,6 +118,34 @@ static float or_pow2f(int e) /* exact 2^e for -126 <= e <= 127 */
     float f;
     memcpy(&f, &bits, 4);
     return f;
+}
+
+/* Cabs[ci][e] = max over centroids m of |C[ci][m][e]|  -> out [cbg][dbar] */
+OR_EXPORT void or_codebook_absmax(const float *C, int cbg, int c, int dbar, float *out)
+{
+    for (int ci = 0; ci < cbg; ++ci)
+        for (int e = 0; e < dbar; ++e) {
+            float mx = 0.0f;
+            for (int m = 0; m < c; ++m) {
+                float a = fabsf(C[((size_t)ci * c + m) * dbar + e]);
+                if (a > mx) mx = a;
+            }
+            out[ci * dbar + e] = mx;
+        }
+}
+
+/* A_h of R2 for one query head q [d] */
+OR_EXPORT float or_table_bound(const uint16_t *q, int d, int g, int cbg, const float *Cabs)
+{
+    const int dbar = d / g;
+    float A = 0.0f;
+    for (int i = 0; i < g; ++i) {
+        const float *ca = Cabs + (size_t)(cbg == 1 ? 0 : i) * dbar;
+        float b = fabsf(or_h2f(q[i * dbar])) * ca[0];
+        for (int e = 1; e < dbar; ++e) b = fmaf(fabsf(or_h2f(q[i * dbar + e])), ca[e], b);
+        if (b > A) A = b;
+    }
+    return A;
 }
 
 OR_EXPORT int or_scale_exponent(float A)
@@ -132,8 +164,9 @@ OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, 
 {
     const int dbar = d / g;
     float *t = (float *)malloc(sizeof(float) * (size_t)g * c);
+    float *Cabs = (float *)malloc(sizeof(float) * (size_t)cbg * dbar);
+    or_codebook_absmax(C, cbg, c, dbar, Cabs);
     for (int h = 0; h < G; ++h) {
-        float A = 0.0f;
         for (int i = 0; i < g; ++i) {
             const float *Ci = C + (size_t)(cbg == 1 ? 0 : i) * c * dbar;
             for (int m = 0; m < c; ++m) {
@@ -141,11 +174,9 @@ OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, 
                 for (int e = 1; e < dbar; ++e)
                     acc = fmaf(or_h2f(q[h * d + i * dbar + e]), Ci[(size_t)m * dbar + e], acc);
                 t[(size_t)i * c + m] = acc;
-                float a = fabsf(acc);
-                if (a > A) A = a;
             }
         }
-        int e_h = or_scale_exponent(A);
+        int e_h = or_scale_exponent(or_table_bound(q + (size_t)h * d, d, g, cbg, Cabs));
         float s = or_pow2f(e_h);
         for (size_t k = 0; k < (size_t)g * c; ++k) {
             float v = rintf(t[k] * s);
@@ -156,6 +187,7 @@ OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, 
         }
         e_out[h] = e_h;
     }
+    free(Cabs);
     free(t);
 }
 

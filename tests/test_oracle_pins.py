@@ -115,16 +115,24 @@ def test_table_fp32_within_rounding_bound(orc, G, d, g, c, cbg):
 
 
 def test_table_fixed_point_scale_and_rounding(orc):
-    """R2 fixed point: A·2^e in [2^14, 2^15) (uses the full int16 range) and
-    |T_fx - T32·2^e| <= 1/2 (round to nearest)."""
+    """R2 fixed point: the bound A_h (|q̄_i|·max|C| chain) dominates every entry exactly,
+    A_h·2^e in [2^14, 2^15), |T_fx - T32·2^e| <= 1/2 (round to nearest); A_h is within
+    √dbar·(max over groups of ‖q̄_i‖₁/‖q̄_i‖₂) of the true max (Cauchy-Schwarz)."""
     rng = _rng(11)
     for trial in range(20):
         s = 10.0 ** rng.uniform(-3, 3)
         q = (rng.standard_normal((4, 32)) * s).astype(np.float16)
         C = rng.standard_normal((8, 64, 4)).astype(np.float32)
         T32, Tfx, e = orc.table(q, C, 8)
+        Cabs = np.abs(C).max(1)
+        assert np.array_equal(orc.codebook_absmax(C), Cabs)
         for h in range(4):
-            A = np.abs(T32[h]).max()
+            A = orc.table_bound(q[h], C, 8)
+            amax = np.abs(T32[h]).max()
+            assert amax <= A
+            # independent float64 value of the bound
+            A64 = (np.abs(q[h].astype(np.float64)).reshape(8, 4) * Cabs).sum(1).max()
+            assert abs(A - A64) <= 4 * 2.0 ** -23 * A64
             if A == 0:
                 continue
             scaled = T32[h].astype(np.float64) * 2.0 ** int(e[h])
