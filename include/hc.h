@@ -66,7 +66,8 @@ typedef struct {
 /* Quantized key cache of one model (all layers).  Host struct; device buffers.
  *  codes    [B][L][Hkv][g][n_cap] uint16, GROUP-MAJOR (the index matrix P of P:227,
  *           0-based, one contiguous strip per (b,l,kv,group)); n_cap % 64 == 0.
- *  codebook [L][cbg][c][dbar] fp32 (one codebook set per layer, shared by its KV heads).
+ *  codebook [L][cbg][c][dbar] fp32 (one codebook set per layer, shared by its KV heads);
+ *  cb_absmax [L][cbg][dbar] its per-dimension max |C| (optional, see hc_codebook_absmax).
  *  Recent window (R7, optional, res_cap = W >= 0): the newest n_res[l] <= W tokens keep
  *  exact keys/values resident: res_k/res_v [B][L][Hkv][W][d] fp16, token at global
  *  position p lives in slot p % W.  Candidates of a layer are the quantized tokens
@@ -78,6 +79,8 @@ typedef struct {
     int64_t n_cap;
     uint16_t *codes;
     const float *codebook;
+    const float *cb_absmax; /* optional [L][cbg][dbar]: max_m |C[l][ci][m][e]| (R2's bound;
+                               hc_codebook_absmax fills it once); NULL = recomputed per call */
     int32_t res_cap;
     uint16_t *res_k;
     uint16_t *res_v;
@@ -124,6 +127,12 @@ uint64_t hc_launch_count(void);
  * launched by hc_decode_attention from this thread (one-shot; NULLs disable).  Inside
  * stream capture they become external event-record nodes of the graph. */
 hc_status hc_profile_scan_events(void *begin_event, void *end_event);
+
+/* Codebook constant of R2: out[l][ci][e] = max_m |codebook[l][ci][m][e]| for all L layers.
+ * codebook [L][cbg][c][dbar] fp32, out [L][cbg][dbar] fp32 (device).  Call once per codebook
+ * and store the result in hc_kcache.cb_absmax. */
+hc_status hc_codebook_absmax(const float *codebook, hc_vq vq, int32_t L, float *out,
+                             hc_stream_t stream);
 
 /* Key encoding, R1 ("represented as nearest neighbor of the centroids"):
  *   codes[i*code_stride + r] = argmin_m ||keys[r][i*dbar:(i+1)*dbar] - C[ci][m]||², ties -> lowest m.

@@ -21,7 +21,7 @@ HC_OK, HC_ERR_ARG, HC_ERR_SHAPE, HC_ERR_RANGE, HC_ERR_CAPACITY, HC_ERR_EMPTY, HC
 HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
 
 EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_events",
-           "hc_quantize_keys", "hc_append_kv",
+           "hc_codebook_absmax", "hc_quantize_keys", "hc_append_kv",
            "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
            "hc_select_topk"]
 
@@ -43,7 +43,7 @@ class hc_budget(C.Structure):
 class hc_kcache(C.Structure):
     _fields_ = [("B", C.c_int32), ("L", C.c_int32), ("Hkv", C.c_int32), ("G", C.c_int32),
                 ("vq", hc_vq), ("n_cap", C.c_int64), ("codes", C.c_void_p),
-                ("codebook", C.c_void_p), ("res_cap", C.c_int32), ("res_k", C.c_void_p),
+                ("codebook", C.c_void_p), ("cb_absmax", C.c_void_p), ("res_cap", C.c_int32), ("res_k", C.c_void_p),
                 ("res_v", C.c_void_p), ("n_q", C.c_int64 * MAX_LAYERS),
                 ("n_res", C.c_int32 * MAX_LAYERS)]
 
@@ -74,6 +74,8 @@ def lib():
         L.hc_launch_count.restype = C.c_uint64
         L.hc_profile_scan_events.argtypes = [p, p]
         L.hc_profile_scan_events.restype = i32
+        L.hc_codebook_absmax.argtypes = [p, hc_vq, i32, p, p]
+        L.hc_codebook_absmax.restype = i32
         L.hc_quantize_keys.argtypes = [p, i64, p, hc_vq, p, i64, p]
         L.hc_quantize_keys.restype = i32
         L.hc_append_kv.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, p]
@@ -197,6 +199,11 @@ class KCache:
         s.n_cap = n_cap
         s.codes = self.codes.data_ptr()
         s.codebook = codebook.data_ptr()
+        # R2's codebook constant max_m |C[l][ci][m][e]|, computed once on the device
+        self.cb_absmax = torch.empty((L, cbg, d // g), dtype=torch.float32, device=codebook.device)
+        _check(lib().hc_codebook_absmax(_ptr(codebook), hc_vq(d, g, c, cbg), L,
+                                        _ptr(self.cb_absmax), _stream()))
+        s.cb_absmax = self.cb_absmax.data_ptr()
         s.res_cap = res_cap
         s.res_k = self.res_k.data_ptr() if self.res_k is not None else None
         s.res_v = self.res_v.data_ptr() if self.res_v is not None else None

@@ -96,7 +96,7 @@ struct Layout {
   int nchunks_max;
   int gchunks;
   int64_t k_eff;
-  size_t o_hs, o_T, o_amax, o_z, o_zpart, o_h1c, o_h2c, o_h1m, o_chunk, o_part, o_idx, o_w, total;
+  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_h1c, o_h2c, o_h1m, o_chunk, o_part, o_idx, o_w, total;
   size_t hist_bytes;  // h1c + h2c + h1m (contiguous)
 };
 
@@ -116,7 +116,7 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
   size_t o = 0;
   L.o_hs = o; o += align256((size_t)rows * sizeof(HeadState));
   L.o_T = o; o += align256((size_t)B * Hkv * g * L.cpow2 * G * 2);
-  L.o_amax = o; o += align256((size_t)B * Hkv * g * kMaxTSplit * G * 4);
+  L.o_cbabs = o; o += align256((size_t)kc->vq.cbg * (d / g) * 4);
   L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
   L.o_zpart = o; o += align256((size_t)kMaxScanSplit * rows * L.z_stride * 4);
   L.o_h1c = o; o += (size_t)rows * kNB * 4;
@@ -186,6 +186,16 @@ const char *hc_last_error(void) { return g_err; }
 const char *hc_version(void) { return "hcattn-b200 0.1 (sm_100a)"; }
 
 uint64_t hc_launch_count(void) { return g_launches.load(); }
+
+hc_status hc_codebook_absmax(const float *codebook, hc_vq vq, int32_t L, float *out,
+                             hc_stream_t stream) {
+  hc_status st = check_vq(vq);
+  if (st) return st;
+  if (L <= 0) return fail(HC_ERR_ARG, "L <= 0");
+  if (!codebook || !out) return fail(HC_ERR_ARG, "NULL pointer");
+  return cuda_check(launch_cbabs(codebook, (int64_t)L * vq.cbg, vq.c, vq.d / vq.g, out,
+                                 (cudaStream_t)stream), "hc_codebook_absmax");
+}
 
 hc_status hc_profile_scan_events(void *begin_event, void *end_event) {
   hc::g_scan_ev[0] = (cudaEvent_t)begin_event;
@@ -328,7 +338,14 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   a.kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
   a.hs = (HeadState *)(w8 + Lw.o_hs);
   a.T = (int16_t *)(w8 + Lw.o_T);
-  a.amax_part = (float *)(w8 + Lw.o_amax);
+  if (kc->cb_absmax) {
+    a.cb_absmax = kc->cb_absmax + (int64_t)layer * kc->vq.cbg * (d / g);
+  } else {
+    float *cba = (float *)(w8 + Lw.o_cbabs);
+    cudaError_t e0 = launch_cbabs(a.C, kc->vq.cbg, kc->vq.c, (int)(d / g), cba, s);
+    if (e0 != cudaSuccess) return cuda_check(e0, "codebook absmax");
+    a.cb_absmax = cba;
+  }
   {  // centroid splits: ~2 waves of 256-thread CTAs over units x groups
     const int64_t base = B * H * g;
     int ts = 1;

@@ -64,8 +64,8 @@ struct LayerArgs {
   // workspace
   HeadState *hs;          // [B*Hq]
   int16_t *T;             // [units][g][cpow2][G]
-  float *amax_part;       // [units][g][tsplit][G] partial max |t|
-  int tsplit;             // centroid splits per (unit, group) in the table kernels
+  const float *cb_absmax; // layer [cbg][dbar]: max_m |C[ci][m][e]| (R2 bound)
+  int tsplit;             // centroid splits per (unit, group) in the table kernel
   float *z;               // [B*Hq][z_stride]
   int64_t z_stride;
   uint32_t *h1c;          // [B*Hq][kNB]
@@ -91,6 +91,7 @@ struct LayerArgs {
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);
 cudaError_t launch_table(const LayerArgs &a, cudaStream_t s);
 cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s);
+cudaError_t launch_cbabs(const float *C, int64_t slices, int c, int dbar, float *out, cudaStream_t s);
 cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s);
 cudaError_t launch_gather(const LayerArgs &a, cudaStream_t s);
 

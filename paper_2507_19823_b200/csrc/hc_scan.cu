@@ -143,22 +143,25 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
   static_assert(TPT == 8 || TPT == 16, "TPT");
   constexpr int kChunks = TPT / 8;                     // 8-token chunks per thread
   constexpr int kTile = kScanThreads * TPT;            // tokens per tile
+  constexpr uint32_t kCodeBytes = kTile * 2;           // one group's code strip of a tile
   extern __shared__ __align__(128) uint8_t smem[];
+  // shared memory: T ring [2][slice] | code ring [3][kCodeBytes] | mbarriers tb[2], cb[3]
   const uint32_t slice_bytes = (uint32_t)a.cpow2 * G * 2;
-  uint8_t *buf0 = smem;
-  uint8_t *buf1 = smem + slice_bytes;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 2 * slice_bytes);
+  uint8_t *tbuf = smem;
+  uint8_t *cbuf = smem + 2 * slice_bytes;
+  uint64_t *tb = reinterpret_cast<uint64_t *>(cbuf + 3 * kCodeBytes);
+  uint64_t *cb = tb + 2;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int j = 0; j < 2; ++j) mbar_init(&tb[j], 1);
+    for (int j = 0; j < 3; ++j) mbar_init(&cb[j], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t parity0 = 0, parity1 = 0;
+  uint32_t tph = 0, cph = 0;  // phase bit per barrier
   const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
   const int gper = (a.g + nsplit - 1) / nsplit;
+
   for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
     const int sp = item % nsplit;
     const int tile = item / nsplit;
@@ -168,26 +171,25 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
     const int i1 = min(a.g, i0 + gper);
     const int ng = i1 - i0;
     const int b = u / a.Hkv, kv = u - b * a.Hkv;
-    const int64_t t0 = (int64_t)tk * kTile + (int64_t)warp * (32 * TPT);
-    const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride + (int64_t)kv * a.g * a.n_cap;
+    const int64_t tile0 = (int64_t)tk * kTile;
+    // bytes of this tile's code strip that exist in the [n_cap] strip (multiple of 16)
+    const int64_t avail = a.n_cap - tile0;
+    const uint32_t cbytes = (uint32_t)(avail < kTile ? avail : kTile) * 2;
+    const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride +
+                        ((int64_t)kv * a.g + i0) * a.n_cap + tile0;
     const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
-    P += (int64_t)i0 * a.n_cap;
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bar[0], slice_bytes);
-      bulk_g2s(buf0, Tu, slice_bytes, &bar[0]);
-      if (ng > 1) {
-        mbar_expect_tx(&bar[1], slice_bytes);
-        bulk_g2s(buf1, Tu + slice_bytes, slice_bytes, &bar[1]);
+      for (int j = 0; j < 2 && j < ng; ++j) {
+        mbar_expect_tx(&tb[j], slice_bytes);
+        bulk_g2s(tbuf + j * slice_bytes, Tu + (int64_t)j * slice_bytes, slice_bytes, &tb[j]);
+      }
+      for (int j = 0; j < 3 && j < ng; ++j) {
+        mbar_expect_tx(&cb[j], cbytes);
+        bulk_g2s(cbuf + j * kCodeBytes, P + (int64_t)j * a.n_cap, cbytes, &cb[j]);
       }
     }
-    int64_t tok[kChunks];
-    bool val[kChunks];
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k) {
-      tok[k] = t0 + k * 256 + lane * 8;
-      val[k] = tok[k] < a.n_q;
-    }
+    const int woff = warp * (32 * TPT);  // this warp's first token inside the tile
     int acc[kChunks][8][G];
 #pragma unroll
     for (int k = 0; k < kChunks; ++k)
@@ -195,41 +197,42 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
       for (int u8 = 0; u8 < 8; ++u8)
 #pragma unroll
         for (int h = 0; h < G; ++h) acc[k][u8][h] = 0;
-    uint4 cur[kChunks];
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k) cur[k] = val[k] ? ld_stream(P + tok[k]) : make_uint4(0, 0, 0, 0);
 
+    int ci = 0;  // code ring slot of group i (i % 3)
     for (int i = 0; i < ng; ++i) {
-      uint4 nxt[kChunks];
-      if (i + 1 < ng) {
+      const int ti = i & 1;
+      mbar_wait(&cb[ci], (cph >> ci) & 1u);
+      cph ^= 1u << ci;
+      mbar_wait(&tb[ti], (tph >> ti) & 1u);
+      tph ^= 1u << ti;
+      const uint8_t *sb = tbuf + ti * slice_bytes;
+      const uint8_t *cs = cbuf + ci * kCodeBytes + (size_t)woff * 2;
 #pragma unroll
-        for (int k = 0; k < kChunks; ++k)
-          nxt[k] = val[k] ? ld_stream(P + (int64_t)(i + 1) * a.n_cap + tok[k]) : make_uint4(0, 0, 0, 0);
+      for (int k = 0; k < kChunks; ++k) {
+        const uint4 c = *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
+        lookup8<G>(c, sb, mask, acc[k]);
       }
-      const bool odd = i & 1;
-      if (!odd) { mbar_wait(&bar[0], parity0); parity0 ^= 1u; }
-      else { mbar_wait(&bar[1], parity1); parity1 ^= 1u; }
-      const uint8_t *sb = odd ? buf1 : buf0;
-#pragma unroll
-      for (int k = 0; k < kChunks; ++k) lookup8<G>(cur[k], sb, mask, acc[k]);
       __syncthreads();
-      if (threadIdx.x == 0 && i + 2 < ng) {
+      if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        uint64_t *bb = odd ? &bar[1] : &bar[0];
-        mbar_expect_tx(bb, slice_bytes);
-        bulk_g2s(odd ? buf1 : buf0, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, bb);
+        if (i + 2 < ng) {
+          mbar_expect_tx(&tb[ti], slice_bytes);
+          bulk_g2s(tbuf + ti * slice_bytes, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, &tb[ti]);
+        }
+        if (i + 3 < ng) {
+          mbar_expect_tx(&cb[ci], cbytes);
+          bulk_g2s(cbuf + ci * kCodeBytes, P + (int64_t)(i + 3) * a.n_cap, cbytes, &cb[ci]);
+        }
       }
-      if (i + 1 < ng) {
-#pragma unroll
-        for (int k = 0; k < kChunks; ++k) cur[k] = nxt[k];
-      }
+      ci = ci == 2 ? 0 : ci + 1;
     }
     int mx[G], mn[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
     float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
 #pragma unroll
-    for (int k = 0; k < kChunks; ++k) store_chunk<G>(a, zbase, b, kv, tok[k], acc[k], mx, mn);
+    for (int k = 0; k < kChunks; ++k)
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
     if (nsplit > 1) continue;
 #pragma unroll
     for (int h = 0; h < G; ++h) {
@@ -291,7 +294,7 @@ static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   const int nsplit = a.scan_split;
   const int total = tiles_per_unit * units * nsplit;
   if (total == 0) return cudaSuccess;
-  const size_t smem = (size_t)2 * a.cpow2 * G * 2 + 16;
+  const size_t smem = (size_t)2 * a.cpow2 * G * 2 + 3 * (size_t)kTile * 2 + 5 * 8;
   static int configured[64] = {0};  // per device: opt in to the full 227 KB once
   int dev = 0;
   cudaGetDevice(&dev);

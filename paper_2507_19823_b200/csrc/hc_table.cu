@@ -46,13 +46,12 @@ __device__ __forceinline__ void table_entry(const float (&qs)[G][DBAR], const fl
   }
 }
 
-// PHASE 0: per-(unit, group, split) max |t| of each head -> amax_part (plain stores,
-//          no atomics).
-// PHASE 1: every CTA reduces its heads' g*csplit partial maxima -> A_h -> e_h (R2),
-//          recomputes its entries (same FMA chain) and stores the packed G x int16.
-// One CTA = (unit, group i, centroid split); each thread owns kTCPT consecutive
-// centroids (vectorised codebook loads, all issued before use).
-template <int G, int DBAR, int PHASE>
+// One pass (R2): every CTA = (unit, group i, centroid split) first derives its heads'
+// scale from the bound A_h = max_i fmaf-chain(|q̄_i,e|, Cabs[ci][e]) (threads t < g
+// each evaluate one group's chain; block max), then computes its centroids' entries
+// t (the same FMA chain as the oracle) and stores the packed G x int16
+// clamp(rint(t * 2^e_h)).  Each thread owns centroids m0+tid, m0+tid+256, ...
+template <int G, int DBAR>
 __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   const int u = blockIdx.z;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
@@ -61,24 +60,28 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   const int hq0 = kv * G;
   const int per = a.cpow2 / gridDim.x;          // centroids of this CTA
   const int m0 = split * per;
-  float qs[G][DBAR];
-#pragma unroll
-  for (int h = 0; h < G; ++h)
-#pragma unroll
-    for (int e = 0; e < DBAR; ++e)
-      qs[h][e] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + i * DBAR + e));
-  const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
   HeadState *hs = a.hs + (int64_t)b * a.Hq + hq0;
-  float *part = a.amax_part + ((int64_t)u * a.g * gridDim.x) * G;  // [g*csplit][G] of this unit
+  // --- the per-head scale exponent from the bound
+  __shared__ float sA[G][kTB / 32];
   float sc[G];
-  if (PHASE == 1) {
-    // A_h = max over all partial maxima of the head (g * csplit values)
-    __shared__ float sA[G][kTB / 32];
-    const int np = a.g * gridDim.x;
+  {
+    float bnd[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) bnd[h] = 0.0f;
+    for (int gi = threadIdx.x; gi < a.g; gi += kTB) {
+      const float *ca = a.cb_absmax + (int64_t)(a.cbg == 1 ? 0 : gi) * DBAR;
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const uint16_t *qh = a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + gi * DBAR;
+        float bb = __fmul_rn(fabsf(h2f(__ldg(qh))), __ldg(ca));
+#pragma unroll
+        for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(h2f(__ldg(qh + e))), __ldg(ca + e), bb);
+        bnd[h] = fmaxf(bnd[h], bb);
+      }
+    }
 #pragma unroll
     for (int h = 0; h < G; ++h) {
-      float v = 0.0f;
-      for (int k = threadIdx.x; k < np; k += kTB) v = fmaxf(v, part[(int64_t)k * G + h]);
+      float v = bnd[h];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
       if ((threadIdx.x & 31) == 0) sA[h][threadIdx.x >> 5] = v;
@@ -98,50 +101,32 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
       }
     }
   }
-  float mx[G];
+  float qs[G][DBAR];
 #pragma unroll
-  for (int h = 0; h < G; ++h) mx[h] = 0.0f;
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < DBAR; ++e)
+      qs[h][e] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + i * DBAR + e));
+  const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
 #pragma unroll 4
   for (int m = m0 + threadIdx.x; m < m0 + per; m += kTB) {
     float t[G];
     table_entry<G, DBAR>(qs, Ci, m, a.c, t);
-    if (PHASE == 0) {
+    int16_t packed[G];
 #pragma unroll
-      for (int h = 0; h < G; ++h) mx[h] = fmaxf(mx[h], fabsf(t[h]));
+    for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t(t[h], sc[h]);
+    int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
+    if constexpr (G == 4) {
+      uint2 v;
+      v.x = (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
+      v.y = (uint32_t)(uint16_t)packed[2] | ((uint32_t)(uint16_t)packed[3] << 16);
+      *reinterpret_cast<uint2 *>(dst) = v;
+    } else if constexpr (G == 2) {
+      *reinterpret_cast<uint32_t *>(dst) =
+          (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
     } else {
-      int16_t packed[G];
 #pragma unroll
-      for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t(t[h], sc[h]);
-      int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
-      if constexpr (G == 4) {
-        uint2 v;
-        v.x = (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
-        v.y = (uint32_t)(uint16_t)packed[2] | ((uint32_t)(uint16_t)packed[3] << 16);
-        *reinterpret_cast<uint2 *>(dst) = v;
-      } else if constexpr (G == 2) {
-        *reinterpret_cast<uint32_t *>(dst) =
-            (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
-      } else {
-#pragma unroll
-        for (int h = 0; h < G; ++h) dst[h] = packed[h];
-      }
-    }
-  }
-  if (PHASE == 0) {
-    __shared__ float red[G][kTB / 32];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float v = mx[h];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-      if ((threadIdx.x & 31) == 0) red[h][threadIdx.x >> 5] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < G) {
-      float v = 0.0f;
-#pragma unroll
-      for (int w = 0; w < kTB / 32; ++w) v = fmaxf(v, red[threadIdx.x][w]);
-      part[((int64_t)i * gridDim.x + split) * G + threadIdx.x] = v;
+      for (int h = 0; h < G; ++h) dst[h] = packed[h];
     }
   }
 }
@@ -149,9 +134,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
   dim3 grid((unsigned)a.tsplit, (unsigned)a.g, (unsigned)(a.B * a.Hkv));
-  k_table<G, DBAR, 0><<<grid, kTB, 0, s>>>(a);
-  note_launch();
-  k_table<G, DBAR, 1><<<grid, kTB, 0, s>>>(a);
+  k_table<G, DBAR><<<grid, kTB, 0, s>>>(a);
   note_launch();
   return cudaGetLastError();
 }
@@ -175,6 +158,35 @@ cudaError_t launch_table(const LayerArgs &a, cudaStream_t s) {
     case 4: return table_g<4>(a, s);
   }
   return cudaErrorInvalidValue;
+}
+
+// Cabs[l][ci][e] = max_m |C[l][ci][m][e]| (R2's codebook constant); one CTA per (l, ci)
+__global__ void __launch_bounds__(256) k_cbabs(const float *C, int c, int dbar, float *out) {
+  const int64_t slice = (int64_t)blockIdx.x;  // l * cbg + ci
+  const float *Cs = C + slice * c * dbar;
+  float mx[16];
+  for (int e = 0; e < 16; ++e) mx[e] = 0.0f;
+  for (int m = threadIdx.x; m < c; m += 256)
+    for (int e = 0; e < dbar; ++e) mx[e] = fmaxf(mx[e], fabsf(Cs[(int64_t)m * dbar + e]));
+  __shared__ float red[16][8];
+  for (int e = 0; e < dbar; ++e) {
+    float v = mx[e];
+    for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if ((threadIdx.x & 31) == 0) red[e][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < dbar) {
+    float v = 0.0f;
+    for (int w = 0; w < 8; ++w) v = fmaxf(v, red[threadIdx.x][w]);
+    out[slice * dbar + threadIdx.x] = v;
+  }
+}
+
+cudaError_t launch_cbabs(const float *C, int64_t slices, int c, int dbar, float *out, cudaStream_t s) {
+  if (slices <= 0) return cudaSuccess;
+  k_cbabs<<<(unsigned)slices, 256, 0, s>>>(C, c, dbar, out);
+  note_launch();
+  return cudaGetLastError();
 }
 
 // Resident tokens: one thread per (token, query head); exact fp32 FMA chain over d

@@ -33,10 +33,10 @@ def test_library_exports_every_header_symbol():
 
 def test_struct_layout_matches_header():
     import paper_2507_19823_b200 as hc
-    # hc_kcache: 4 int32 + hc_vq(16) + int64 + 2 ptr + int32(+pad) + 2 ptr + 256 int64 + 256 int32
+    # hc_kcache: 4 int32 + hc_vq(16) + int64 + 3 ptr + int32(+pad) + 2 ptr + 256 int64 + 256 int32
     assert ctypes.sizeof(hc.hc_vq) == 16
     assert ctypes.sizeof(hc.hc_budget) == 24
-    assert ctypes.sizeof(hc.hc_kcache) == 16 + 16 + 8 + 16 + 8 + 16 + 256 * 8 + 256 * 4
+    assert ctypes.sizeof(hc.hc_kcache) == 16 + 16 + 8 + 24 + 8 + 16 + 256 * 8 + 256 * 4
     assert ctypes.sizeof(hc.hc_vstore) == 24
 
 
