@@ -62,7 +62,6 @@ int next_pow2(int c) {
   return p;
 }
 
-constexpr int kGatherRows = 256;
 constexpr int kMaxTSplit = 8;
 constexpr int kMaxScanSplit = 4;
 
@@ -88,16 +87,12 @@ void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int
     }
   }
 }
-constexpr int kChunkTokens = 4096;
 
 struct Layout {
   int cpow2;
   int64_t z_stride;
-  int nchunks_max;
-  int gchunks;
   int64_t k_eff;
-  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_h1c, o_h2c, o_h1m, o_chunk, o_part, o_idx, o_w, total;
-  size_t hist_bytes;  // h1c + h2c + h1m (contiguous)
+  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, total;
 };
 
 Layout make_layout(const hc_kcache *kc, int64_t k_max) {
@@ -109,23 +104,14 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
   if (L.cpow2 < 256) L.cpow2 = 256;
   const int64_t ncand_max = kc->n_cap + kc->res_cap;
   L.z_stride = round_up(ncand_max > 0 ? ncand_max : 1, 64);
-  L.nchunks_max = (int)((L.z_stride + kChunkTokens - 1) / kChunkTokens);
   L.k_eff = k_max < ncand_max ? k_max : ncand_max;
   if (L.k_eff < 1) L.k_eff = 1;
-  L.gchunks = (int)((L.k_eff + kGatherRows - 1) / kGatherRows);
   size_t o = 0;
   L.o_hs = o; o += align256((size_t)rows * sizeof(HeadState));
   L.o_T = o; o += align256((size_t)B * Hkv * g * L.cpow2 * G * 2);
   L.o_cbabs = o; o += align256((size_t)kc->vq.cbg * (d / g) * 4);
   L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
   L.o_zpart = o; o += align256((size_t)kMaxScanSplit * rows * L.z_stride * 4);
-  L.o_h1c = o; o += (size_t)rows * kNB * 4;
-  L.o_h2c = o; o += (size_t)rows * kNB * 4;
-  L.o_h1m = o; o += (size_t)rows * kNB * 8;
-  L.hist_bytes = o - L.o_h1c;
-  o = align256(o);
-  L.o_chunk = o; o += align256((size_t)rows * L.nchunks_max * 2 * 4);
-  L.o_part = o; o += align256((size_t)rows * L.gchunks * d * 4);
   L.o_idx = o; o += align256((size_t)rows * L.k_eff * 4);
   L.o_w = o; o += align256((size_t)rows * L.k_eff * 4);
   L.total = o;
@@ -160,17 +146,6 @@ hc_status check_kcache(const hc_kcache *kc) {
   if (kc->res_cap > 0 && (!kc->res_k || !kc->res_v)) return fail(HC_ERR_ARG, "res_k/res_v NULL");
   if ((int64_t)kc->B * kc->G * kc->Hkv > 65535) return fail(HC_ERR_UNSUPPORTED, "B*Hq > 65535");
   return HC_OK;
-}
-
-__global__ void k_hs_init(HeadState *hs, int rows) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  HeadState h;
-  memset(&h, 0, sizeof(h));
-  h.M = INT_MIN;
-  h.zmin = INT_MAX;
-  h.bstar = kNB;
-  hs[r] = h;
 }
 
 __global__ void k_z_to_int(const float *z, int64_t zs, int32_t *out, int64_t n) {
@@ -354,17 +329,8 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   }
   a.z = (float *)(w8 + Lw.o_z);
   a.z_stride = Lw.z_stride;
-  a.h1c = (uint32_t *)(w8 + Lw.o_h1c);
-  a.h2c = (uint32_t *)(w8 + Lw.o_h2c);
-  a.h1m = (unsigned long long *)(w8 + Lw.o_h1m);
-  a.chunk_cnt = (uint32_t *)(w8 + Lw.o_chunk);
-  a.chunk_tokens = kChunkTokens;
-  a.nchunks = (int)((n_cand + kChunkTokens - 1) / kChunkTokens);
-  a.partial = (float *)(w8 + Lw.o_part);
-  a.grows = kGatherRows;
   const int64_t k_cap = sel_idx ? budget.k_max : Lw.k_eff;  // row stride of idx / w
   a.k_max = k_cap;
-  a.gchunks = (int)(((k_cap < n_cand ? k_cap : n_cand) + kGatherRows - 1) / kGatherRows);
   a.sel_idx = sel_idx ? sel_idx : (int32_t *)(w8 + Lw.o_idx);
   a.sel_w = sel_w ? sel_w : (float *)(w8 + Lw.o_w);
   a.sel_k = sel_k;
@@ -374,21 +340,16 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   a.zpart = (float *)(w8 + Lw.o_zpart);
 
   cudaError_t e;
-  k_hs_init<<<(rows + 127) / 128, 128, 0, s>>>(a.hs, rows);
-  note_launch();
-  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_check(e, "init");
-  if ((e = cudaMemsetAsync(w8 + Lw.o_h1c, 0, Lw.hist_bytes, s)) != cudaSuccess) return cuda_check(e, "memset");
   if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
   if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
   if (n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
   SelArgs sa{};
   sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
   sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
-  sa.h1c = a.h1c; sa.h1m = a.h1m; sa.h2c = a.h2c; sa.chunk_cnt = a.chunk_cnt;
-  sa.nchunks = a.nchunks; sa.chunk_tokens = kChunkTokens;
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
-  if ((e = launch_select(sa, s)) != cudaSuccess) return cuda_check(e, "select");
-  if ((e = launch_gather(a, s)) != cudaSuccess) return cuda_check(e, "gather");
+  if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, 1, a.num_sms, s,
+                               dbg && dbg->z ? 1 : 0)) != cudaSuccess)
+    return cuda_check(e, "select");
   if (dbg) {
     if (dbg->z) {
       dim3 gz((unsigned)((n_cand + 255) / 256), (unsigned)rows);
@@ -412,13 +373,7 @@ size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {
   (void)budget;
   if (rows <= 0 || n <= 0) return 0;
   const int64_t zs = round_up(n, 64);
-  const int64_t nch = (zs + kChunkTokens - 1) / kChunkTokens;
-  size_t o = 0;
-  o += align256((size_t)rows * sizeof(HeadState));
-  o += align256((size_t)rows * zs * 4);
-  o += align256((size_t)rows * kNB * 16);
-  o += align256((size_t)rows * nch * 8);
-  return o;
+  return align256((size_t)rows * sizeof(HeadState)) + align256((size_t)rows * zs * 4);
 }
 
 hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d, hc_budget budget,
@@ -436,16 +391,10 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t *w8 = (uint8_t *)ws;
   const int64_t zs = round_up(n, 64);
-  const int nch = (int)((n + kChunkTokens - 1) / kChunkTokens);
   size_t o = 0;
   HeadState *hs = (HeadState *)(w8 + o); o += align256((size_t)rows * sizeof(HeadState));
-  float *z = (float *)(w8 + o); o += align256((size_t)rows * zs * 4);
-  uint8_t *hist = w8 + o; o += align256((size_t)rows * kNB * 16);
-  uint32_t *chunk = (uint32_t *)(w8 + o);
+  float *z = (float *)(w8 + o);
   cudaError_t e;
-  k_hs_init<<<(int)((rows + 127) / 128), 128, 0, s>>>(hs, (int)rows);
-  note_launch();
-  if ((e = cudaMemsetAsync(hist, 0, (size_t)rows * kNB * 16, s)) != cudaSuccess) return cuda_check(e, "memset");
   const float kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
   if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s)) != cudaSuccess)
     return cuda_check(e, "prep");
@@ -453,12 +402,10 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   sa.hs = hs; sa.z = z; sa.z_stride = zs; sa.rows = (int)rows; sa.n = n;
   sa.tau_q = (uint32_t)rint((double)budget.tau * 16777216.0);
   sa.k_max = budget.k_max; sa.renorm = budget.renorm ? 1 : 0;
-  sa.h1c = (uint32_t *)hist;
-  sa.h2c = (uint32_t *)(hist + (size_t)rows * kNB * 4);
-  sa.h1m = (unsigned long long *)(hist + (size_t)rows * kNB * 8);
-  sa.chunk_cnt = chunk; sa.nchunks = nch; sa.chunk_tokens = kChunkTokens;
   sa.sel_idx = idx; sa.sel_w = w; sa.sel_k = k;
-  return cuda_check(launch_select(sa, s), "hc_select_topk");
+  LayerArgs la{};
+  la.n_q = n; la.z_stride = zs;
+  return cuda_check(launch_select_fused(sa, la, 1, 0, num_sms(), s), "hc_select_topk");
 }
 
 }  // extern "C"

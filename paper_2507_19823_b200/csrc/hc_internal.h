@@ -68,15 +68,6 @@ struct LayerArgs {
   int tsplit;             // centroid splits per (unit, group) in the table kernel
   float *z;               // [B*Hq][z_stride]
   int64_t z_stride;
-  uint32_t *h1c;          // [B*Hq][kNB]
-  unsigned long long *h1m;
-  uint32_t *h2c;          // [B*Hq][kNB]
-  uint32_t *chunk_cnt;    // [B*Hq][nchunks][2]
-  int nchunks;            // chunks per head for count/write
-  int chunk_tokens;
-  float *partial;         // gather partials [B*Hq][gchunks][d]
-  int gchunks;
-  int grows;              // rows per gather CTA
   // outputs
   int32_t *sel_idx;       // [B*Hq][k_max]
   float *sel_w;
@@ -93,7 +84,6 @@ cudaError_t launch_table(const LayerArgs &a, cudaStream_t s);
 cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s);
 cudaError_t launch_cbabs(const float *C, int64_t slices, int c, int dbar, float *out, cudaStream_t s);
 cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s);
-cudaError_t launch_gather(const LayerArgs &a, cudaStream_t s);
 
 // Eq. 4 selection over `rows` independent score rows (query heads):
 // z [rows][z_stride] (exact integers stored as fp32), hs[row].{M,zmin,kappa} set.
@@ -106,17 +96,13 @@ struct SelArgs {
   uint32_t tau_q;
   int64_t k_max;
   int renorm;
-  uint32_t *h1c;
-  unsigned long long *h1m;
-  uint32_t *h2c;
-  uint32_t *chunk_cnt;
-  int nchunks;
-  int chunk_tokens;
   int32_t *sel_idx;       // [rows][k_max]
   float *sel_w;           // [rows][k_max]
   int64_t *sel_k;         // [rows] (may be null)
 };
-cudaError_t launch_select(const SelArgs &a, cudaStream_t s);
+// fused rows a3-a5 (one cluster of CTAs per row); nsplit: scan partial planes in la.zpart
+cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
+                                int num_sms, cudaStream_t st, int zstore = 0);
 
 // standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,

@@ -233,56 +233,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
 #pragma unroll
     for (int k = 0; k < kChunks; ++k)
       store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
-    if (nsplit > 1) continue;
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const int vmx = __reduce_max_sync(0xffffffffu, mx[h]);
-      const int vmn = __reduce_min_sync(0xffffffffu, mn[h]);
-      if (lane == 0 && vmx != INT_MIN) {
-        HeadState *hs = a.hs + (int64_t)b * a.Hq + kv * G + h;
-        atomicMax(&hs->M, vmx);
-        atomicMin(&hs->zmin, vmn);
-      }
-    }
-  }
-}
-
-// exact sum of the split partials -> z, and the per-head max / min
-__global__ void __launch_bounds__(256) k_zreduce(LayerArgs a, int nsplit) {
-  const int row = blockIdx.y;
-  const int64_t j = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
-  int mx = INT_MIN, mn = INT_MAX;
-  if (j < a.n_q) {
-    const int64_t plane = (int64_t)a.B * a.Hq * a.z_stride;
-    const float *src = a.zpart + (int64_t)row * a.z_stride + j;
-    float4 acc = *reinterpret_cast<const float4 *>(src);
-    for (int sp = 1; sp < nsplit; ++sp) {
-      const float4 v = *reinterpret_cast<const float4 *>(src + sp * plane);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
-    float *dst = a.z + (int64_t)row * a.z_stride + j;
-    if (j + 4 <= a.n_q) {
-      *reinterpret_cast<float4 *>(dst) = acc;
-    } else {  // never touch z[n_q..]: the resident tokens' scores live there
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j + u < a.n_q) dst[u] = vv[u];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (j + u < a.n_q) {
-        const int zi = (int)vv[u];
-        mx = max(mx, zi);
-        mn = min(mn, zi);
-      }
-    }
-  }
-  mx = __reduce_max_sync(0xffffffffu, mx);
-  mn = __reduce_min_sync(0xffffffffu, mn);
-  if ((threadIdx.x & 31) == 0 && mx != INT_MIN) {
-    atomicMax(&a.hs[row].M, mx);
-    atomicMin(&a.hs[row].zmin, mn);
   }
 }
 
@@ -313,11 +263,6 @@ static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
   k_scan<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
   note_launch();
-  if (nsplit > 1) {
-    dim3 gr((unsigned)((a.n_q + 1023) / 1024), (unsigned)(a.B * a.Hq));
-    k_zreduce<<<gr, 256, 0, s>>>(a, nsplit);
-    note_launch();
-  }
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
 }

@@ -1,0 +1,482 @@
+// hc_select_fused.cu -- rows a3, a4, a5 in ONE kernel per layer:
+//   normalisation ã = softmax(z̃/√d) as exact fixed-point mass (R4),
+//   Eq. 4 cumulative-mass eviction with the k_max cap (R5),
+//   Eq. 5 weighted sum of the kept value rows (R6).
+//
+// One thread-block CLUSTER of `cs` CTAs per row (= query head).  Each CTA owns a
+// contiguous token range of the row; the row-wide reductions go through distributed
+// shared memory (DSMEM) instead of global atomics and extra launches:
+//   P0  z (sum of the scan's split partials, exact) -> SMEM cache; M, zmin (cluster max/min)
+//   P1  coarse (count, mass) histogram of Δ = M - z >> shift   [SMEM atomics]
+//       cluster reduce: CTA r owns bins [r*NB/cs, (r+1)*NB/cs) and sums them over peers;
+//       bound1: S, Θ = ⌈τ_q·S/2^24⌉, first bucket b* where mass reaches Θ or count k_max
+//   P2  fine count histogram inside b* -> cluster reduce -> bound2: exact Δ*, #ties r
+//   P3  ordered compaction (prefix over cluster ranks, block scan): ascending indices
+//       and weights W_j/S -> sel_idx / sel_w
+//   P4  gather: every CTA sums ã_j·V_j over ITS kept rows (half-warp per 256-B row,
+//       zero-copy when V is host-mapped); rank 0 adds the cs partials in rank order.
+// All sums that decide indices are integers: bit-exact and decomposition-invariant.
+#include <cooperative_groups.h>
+
+#include "hc_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace hc {
+
+constexpr int kFT = 512;                 // threads per CTA
+constexpr int kZCacheMax = 24576;        // tokens whose z a CTA keeps in shared memory
+constexpr int kGU = 8;                   // gathered rows in flight per half-warp
+
+struct Slot {  // per-CTA values published to the cluster through DSMEM
+  int M, zmin;
+  unsigned long long c, m;      // totals of the owned bins
+  int cand;                     // first triggering bin in the owned range (kNB: none)
+  unsigned long long cb, mb;    // count / mass before `cand`
+  unsigned long long ns, nt;    // strict / tie counts of the token range
+  unsigned long long r_tau, r_cap, w;  // bound2 details at the fine candidate
+};
+
+template <typename T>
+__device__ __forceinline__ void bscan2(T &x, T &y, T &tx, T &ty, T *sx, T *sy) {
+  // block-wide exclusive scan of pairs over kFT threads; tx, ty = totals
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T ix = x, iy = y;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const T ox = __shfl_up_sync(0xffffffffu, ix, off);
+    const T oy = __shfl_up_sync(0xffffffffu, iy, off);
+    if (lane >= off) { ix += ox; iy += oy; }
+  }
+  __syncthreads();
+  if (lane == 31) { sx[w] = ix; sy[w] = iy; }
+  __syncthreads();
+  T bx = 0, by = 0;
+  tx = 0; ty = 0;
+#pragma unroll
+  for (int k = 0; k < kFT / 32; ++k) {
+    if (k < w) { bx += sx[k]; by += sy[k]; }
+    tx += sx[k]; ty += sy[k];
+  }
+  x = bx + ix - x;
+  y = by + iy - y;
+}
+
+__device__ __forceinline__ float load_z(const LayerArgs &la, const SelArgs &s, int row, int64_t j,
+                                        int nsplit) {
+  const float *zr = s.z + (int64_t)row * s.z_stride;
+  if (nsplit <= 1 || j >= la.n_q) return zr[j];
+  const int64_t plane = (int64_t)la.B * la.Hq * la.z_stride;
+  const float *p = la.zpart + (int64_t)row * la.z_stride + j;
+  float acc = p[0];
+  for (int sp = 1; sp < nsplit; ++sp) acc += p[sp * plane];  // exact: integers < 2^24
+  return acc;
+}
+
+__device__ __forceinline__ void fma8(float (&acc)[8], float w, const uint4 &v) {
+  const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&u[q]));
+    acc[2 * q] = fmaf(w, f.x, acc[2 * q]);
+    acc[2 * q + 1] = fmaf(w, f.y, acc[2 * q + 1]);
+  }
+}
+
+__device__ __forceinline__ uint4 ld_nc16(const uint16_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(kFT, 1)
+    k_select_fused(SelArgs s, LayerArgs la, int cs, int nsplit, int zcache, int do_gather,
+                   int zstore) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.x / cs;
+  const int tid = threadIdx.x;
+  extern __shared__ __align__(16) uint8_t smem[];
+  unsigned long long *ms = reinterpret_cast<unsigned long long *>(smem);        // [kNB]
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(smem + kNB * 8);                  // [kNB]
+  float *zc = reinterpret_cast<float *>(smem + kNB * 12);                        // token cache
+  __shared__ Slot slot;
+  __shared__ unsigned long long sx[kFT / 32], sy[kFT / 32];
+  __shared__ float s_red[(kFT / 32) * 32 * 8];  // gather partials [nslots][d] (nslots*d == 4096)
+
+  HeadState *hs = s.hs + row;
+  const float kappa = hs->kappa;
+  const int64_t n = s.n;
+  const int64_t per = ((n + cs - 1) / cs + 15) / 16 * 16;
+  const int64_t j0 = (int64_t)rank * per;
+  const int64_t j1 = j0 + per < n ? j0 + per : n;
+  const int64_t nt = j1 > j0 ? j1 - j0 : 0;  // tokens of this CTA
+  auto zat = [&](int64_t j) -> float {      // z of token j in [j0, j1)
+    return zcache ? zc[j - j0] : s.z[(int64_t)row * s.z_stride + j];
+  };
+
+  // ---------------------------------------------------------------- P0: z, M, zmin
+  int mx = INT_MIN, mn = INT_MAX;
+  for (int64_t t = tid; t < nt; t += kFT) {
+    const int64_t j = j0 + t;
+    const float zf = load_z(la, s, row, j, nsplit);
+    if (zcache) zc[t] = zf;
+    if ((!zcache || zstore) && nsplit > 1) const_cast<float *>(s.z)[(int64_t)row * s.z_stride + j] = zf;
+    const int zi = __float2int_rn(zf);
+    mx = max(mx, zi);
+    mn = min(mn, zi);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  {
+    __shared__ int wmx[kFT / 32], wmn[kFT / 32];
+    if ((tid & 31) == 0) { wmx[tid >> 5] = mx; wmn[tid >> 5] = mn; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < kFT / 32; ++w) { mx = max(mx, wmx[w]); mn = min(mn, wmn[w]); }
+      slot.M = mx;
+      slot.zmin = mn;
+    }
+  }
+  cl.sync();
+  int M = INT_MIN, zmin = INT_MAX;
+  for (int r = 0; r < cs; ++r) {
+    const Slot *o = cl.map_shared_rank(&slot, r);
+    M = max(M, o->M);
+    zmin = min(zmin, o->zmin);
+  }
+  const uint32_t dmax = (uint32_t)(M - zmin);
+  const int bits = 32 - __clz(dmax);
+  const int shift = bits > kNBBits ? bits - kNBBits : 0;
+  const int nbo = kNB / cs;                 // owned bins per CTA
+  const int b_lo = rank * nbo;
+
+  // ---------------------------------------------------------------- P1: coarse histogram
+  for (int i = tid; i < kNB; i += kFT) { cnt[i] = 0; ms[i] = 0ull; }
+  __syncthreads();
+  for (int64_t t = tid; t < nt; t += kFT) {
+    const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
+    const uint32_t bk = dl >> shift;
+    atomicAdd(&cnt[bk], 1u);
+    const uint64_t W = mass(dl, kappa);
+    if (W) atomicAdd(&ms[bk], (unsigned long long)W);
+  }
+  cl.sync();
+  for (int i = tid; i < nbo; i += kFT) {  // sum my owned bins over the peers
+    uint32_t c = cnt[b_lo + i];
+    unsigned long long m = ms[b_lo + i];
+    for (int r = 0; r < cs; ++r) {
+      if (r == rank) continue;
+      c += cl.map_shared_rank(cnt, r)[b_lo + i];
+      m += cl.map_shared_rank(ms, r)[b_lo + i];
+    }
+    cnt[b_lo + i] = c;
+    ms[b_lo + i] = m;
+  }
+  cl.sync();
+  // bound1 over the owned bins: thread owns bins [b_lo + tid*bpt, +bpt)
+  const int bpt = (nbo + kFT - 1) / kFT;
+  unsigned long long lc = 0, lm = 0;
+  for (int k = 0; k < bpt; ++k) {
+    const int bi = tid * bpt + k;
+    if (bi < nbo) { lc += cnt[b_lo + bi]; lm += ms[b_lo + bi]; }
+  }
+  unsigned long long pc = lc, pm = lm, tc, tm;
+  bscan2<unsigned long long>(pc, pm, tc, tm, sx, sy);
+  if (tid == 0) { slot.c = tc; slot.m = tm; slot.cand = kNB; }
+  cl.sync();
+  unsigned long long before_c = 0, before_m = 0, S = 0, ntot = 0;
+  for (int r = 0; r < cs; ++r) {
+    const Slot *o = cl.map_shared_rank(&slot, r);
+    if (r < rank) { before_c += o->c; before_m += o->m; }
+    S += o->m;
+    ntot += o->c;
+  }
+  const bool tau_all = s.tau_q >= (1u << 24);
+  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, S);
+  const bool cap_all = (unsigned long long)s.k_max >= ntot;
+  {
+    unsigned long long cc = before_c + pc, cm = before_m + pm;
+    int found = kNB;
+    unsigned long long fcb = 0, fmb = 0;
+    for (int k = 0; k < bpt; ++k) {
+      const int bi = tid * bpt + k;
+      if (bi >= nbo) break;
+      const unsigned long long c = cnt[b_lo + bi], m = ms[b_lo + bi];
+      const bool trig = c && ((!tau_all && cm + m >= theta) || (!cap_all && cc + c >= (unsigned long long)s.k_max));
+      if (trig && found == kNB) { found = b_lo + bi; fcb = cc; fmb = cm; }
+      cc += c;
+      cm += m;
+    }
+    if (found < kNB) atomicMin(&slot.cand, found);
+    __syncthreads();
+    if (found < kNB && found == slot.cand) { slot.cb = fcb; slot.mb = fmb; }
+  }
+  cl.sync();
+  int bstar = kNB, owner = -1;
+  for (int r = 0; r < cs; ++r) {
+    const int c = cl.map_shared_rank(&slot, r)->cand;
+    if (c < bstar) { bstar = c; owner = r; }
+  }
+  unsigned long long cnt_before = 0, mass_before = 0;
+  if (owner >= 0) {
+    cnt_before = cl.map_shared_rank(&slot, owner)->cb;
+    mass_before = cl.map_shared_rank(&slot, owner)->mb;
+  }
+  // ---------------------------------------------------------------- P2: fine histogram
+  uint32_t delta_star = 0xffffffffu;
+  unsigned long long r_ties = 0, ksel = ntot, selmass = S;
+  long long kstar = (long long)ntot;
+  if (bstar < kNB) {
+    cl.sync();  // every peer finished reading my slot / bins
+    for (int i = tid; i < kNB; i += kFT) cnt[i] = 0;
+    __syncthreads();
+    const uint32_t fmask = (1u << shift) - 1u;
+    for (int64_t t = tid; t < nt; t += kFT) {
+      const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
+      if ((int)(dl >> shift) == bstar) atomicAdd(&cnt[dl & fmask], 1u);
+    }
+    cl.sync();
+    for (int i = tid; i < nbo; i += kFT) {
+      uint32_t c = cnt[b_lo + i];
+      for (int r = 0; r < cs; ++r)
+        if (r != rank) c += cl.map_shared_rank(cnt, r)[b_lo + i];
+      cnt[b_lo + i] = c;
+    }
+    cl.sync();
+    const uint32_t dbase = (uint32_t)bstar << shift;
+    lc = 0; lm = 0;
+    for (int k = 0; k < bpt; ++k) {
+      const int bi = tid * bpt + k;
+      if (bi < nbo && cnt[b_lo + bi]) {
+        lc += cnt[b_lo + bi];
+        lm += (unsigned long long)cnt[b_lo + bi] * mass(dbase | (uint32_t)(b_lo + bi), kappa);
+      }
+    }
+    pc = lc; pm = lm;
+    bscan2<unsigned long long>(pc, pm, tc, tm, sx, sy);
+    if (tid == 0) { slot.c = tc; slot.m = tm; slot.cand = kNB; }
+    cl.sync();
+    unsigned long long bc = cnt_before, bm = mass_before;
+    for (int r = 0; r < rank; ++r) {
+      const Slot *o = cl.map_shared_rank(&slot, r);
+      bc += o->c;
+      bm += o->m;
+    }
+    {
+      unsigned long long cc = bc + pc, cm = bm + pm;
+      int found = kNB;
+      unsigned long long f_cc = 0, f_cm = 0, f_w = 0, f_c = 0;
+      for (int k = 0; k < bpt; ++k) {
+        const int bi = tid * bpt + k;
+        if (bi >= nbo) break;
+        const unsigned long long c = cnt[b_lo + bi];
+        if (!c) continue;
+        const unsigned long long w = mass(dbase | (uint32_t)(b_lo + bi), kappa);
+        const bool tt = !tau_all && w && (cm + c * w >= theta);
+        const bool tk = cc + c >= (unsigned long long)s.k_max;
+        if ((tt || tk) && found == kNB) { found = b_lo + bi; f_cc = cc; f_cm = cm; f_w = w; f_c = c; }
+        cc += c;
+        cm += c * w;
+      }
+      if (found < kNB) atomicMin(&slot.cand, found);
+      __syncthreads();
+      if (found < kNB && found == slot.cand) {
+        unsigned long long r_tau = ~0ull, r_cap = ~0ull;
+        if (!tau_all && f_w && f_cm + f_c * f_w >= theta) r_tau = (theta - f_cm + f_w - 1) / f_w;
+        if (f_cc + f_c >= (unsigned long long)s.k_max) r_cap = (unsigned long long)s.k_max - f_cc;
+        if (r_tau == 0) r_tau = 1;
+        slot.cb = f_cc;
+        slot.mb = f_cm;
+        slot.r_tau = r_tau;
+        slot.r_cap = r_cap;
+        slot.w = f_w;
+      }
+    }
+    cl.sync();
+    int fbin = kNB, fown = -1;
+    for (int r = 0; r < cs; ++r) {
+      const int c = cl.map_shared_rank(&slot, r)->cand;
+      if (c < fbin) { fbin = c; fown = r; }
+    }
+    const Slot *o = cl.map_shared_rank(&slot, fown < 0 ? 0 : fown);
+    const unsigned long long r_tau = o->r_tau, r_cap = o->r_cap, f_cc = o->cb, f_cm = o->mb, f_w = o->w;
+    const unsigned long long r = r_tau < r_cap ? r_tau : r_cap;
+    delta_star = dbase | (uint32_t)fbin;
+    r_ties = r;
+    ksel = f_cc + r;
+    kstar = (r_tau <= r_cap) ? (long long)(f_cc + r_tau) : -1;
+    selmass = f_cm + r * f_w;
+  }
+  // ---------------------------------------------------------------- P3: compaction
+  cl.sync();  // peers done with my slot
+  unsigned long long my_s = 0, my_t = 0;
+  for (int64_t t = tid; t < nt; t += kFT) {
+    const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
+    my_s += dl < delta_star;
+    my_t += dl == delta_star;
+  }
+  {
+    unsigned long long a0 = my_s, a1 = my_t, t0_, t1_;
+    bscan2<unsigned long long>(a0, a1, t0_, t1_, sx, sy);
+    if (tid == 0) { slot.ns = t0_; slot.nt = t1_; }
+  }
+  cl.sync();
+  unsigned long long s_before = 0, t_before = 0;
+  for (int r = 0; r < rank; ++r) {
+    const Slot *o = cl.map_shared_rank(&slot, r);
+    s_before += o->ns;
+    t_before += o->nt;
+  }
+  const double denom = s.renorm ? (double)selmass : (double)S;
+  int32_t *oi = s.sel_idx + (int64_t)row * s.k_max;
+  float *ow = s.sel_w + (int64_t)row * s.k_max;
+  const unsigned long long sel_begin = s_before + (t_before < r_ties ? t_before : r_ties);
+  unsigned long long sel_count = 0;
+  {
+    unsigned long long run_s = s_before, run_t = t_before;  // running totals before each round
+    for (int64_t base = 0; base < nt; base += (int64_t)kFT * 16) {
+      const int64_t t = base + (int64_t)tid * 16;
+      uint32_t dl[16];
+      unsigned long long ns = 0, ntie = 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const bool v = t + u < nt;
+        dl[u] = v ? (uint32_t)(M - __float2int_rn(zat(j0 + t + u))) : 0xffffffffu;
+        ns += v && dl[u] < delta_star;
+        ntie += v && dl[u] == delta_star;
+      }
+      unsigned long long ps = ns, pt = ntie, ts, tt;
+      bscan2<unsigned long long>(ps, pt, ts, tt, sx, sy);
+      const unsigned long long rem = r_ties > run_t ? r_ties - run_t : 0;
+      unsigned long long tie_rank = pt;
+      unsigned long long pos = run_s + (run_t < r_ties ? run_t : r_ties) + ps + (rem < pt ? rem : pt);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        bool take = dl[u] < delta_star;
+        if (!take && dl[u] == delta_star && t + u < nt) {
+          take = tie_rank < rem;
+          ++tie_rank;
+        }
+        if (take) {
+          oi[pos] = (int32_t)(j0 + t + u);
+          ow[pos] = (float)((double)mass(dl[u], kappa) / denom);
+          ++pos;
+        }
+      }
+      run_s += ts;
+      run_t += tt;
+    }
+    const unsigned long long end = run_s + (run_t < r_ties ? run_t : r_ties);
+    sel_count = end - sel_begin;
+  }
+  if (rank == 0 && tid == 0) {
+    hs->M = M;
+    hs->zmin = zmin;
+    hs->shift = shift;
+    hs->bstar = bstar;
+    hs->S = S;
+    hs->theta = theta;
+    hs->delta_star = delta_star;
+    hs->r_ties = (uint32_t)r_ties;
+    hs->ksel = (int64_t)ksel;
+    hs->kstar = kstar;
+    hs->sel_mass = selmass;
+    if (s.sel_k) s.sel_k[row] = (int64_t)ksel;
+  }
+  if (!do_gather) return;
+  // ---------------------------------------------------------------- P4: gather (Eq. 5)
+  __syncthreads();  // this CTA's sel_idx / sel_w writes are visible to its own threads
+  const int b = row / la.Hq, hq = row - b * la.Hq, kv = hq / la.G;
+  const int lpr = la.d >> 3;           // lanes per row (16 at d = 128)
+  const int rpw = 32 / lpr;
+  const int nslots = (kFT / 32) * rpw;
+  const int lane = tid & 31;
+  const int gslot = (tid >> 5) * rpw + lane / lpr;
+  const int sub = lane % lpr;
+  const uint16_t *Vb = la.V + (int64_t)b * la.v_b_stride + (int64_t)kv * la.v_kv_stride;
+  const uint16_t *Rb = la.res_v + (int64_t)b * la.res_b_stride + (int64_t)kv * la.res_cap * la.d;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+  const int64_t r0 = (int64_t)sel_begin, r1 = (int64_t)(sel_begin + sel_count);
+  for (int64_t r = r0 + gslot; r < r1; r += (int64_t)nslots * kGU) {
+    uint4 v[kGU];
+    float w[kGU];
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const int64_t rr = r + (int64_t)u * nslots;
+      if (rr < r1) {
+        const int64_t j = oi[rr];
+        w[u] = ow[rr];
+        const uint16_t *src = j < la.n_q ? Vb + j * la.d
+                                         : Rb + ((la.res_slot0 + (j - la.n_q)) % la.res_cap) * la.d;
+        v[u] = ld_nc16(src + sub * 8);
+      } else {
+        w[u] = 0.0f;
+        v[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) fma8(acc, w[u], v[u]);
+  }
+  // CTA partial: slots -> d floats (fixed order), kept in shared memory for the cluster
+  float *part = reinterpret_cast<float *>(cnt);  // reuse the histogram space (>= d floats)
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s_red[gslot * la.d + sub * 8 + e] = acc[e];
+  __syncthreads();
+  for (int e = tid; e < la.d; e += kFT) {
+    float sum = 0.0f;
+    for (int q = 0; q < nslots; ++q) sum += s_red[q * la.d + e];
+    part[e] = sum;
+  }
+  cl.sync();
+  if (rank == 0) {
+    for (int e = tid; e < la.d; e += kFT) {
+      float sum = 0.0f;
+      for (int r = 0; r < cs; ++r) sum += cl.map_shared_rank(part, r)[e];
+      la.out[(int64_t)row * la.d + e] = sum;
+    }
+  }
+  cl.sync();  // keep peers' shared memory alive until rank 0 has read it
+}
+
+cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
+                                int num_sms, cudaStream_t st, int zstore) {
+  int cs = 1;
+  while (cs < 8 && (int64_t)s.rows * cs * 2 <= num_sms && s.n / (cs * 2) >= 1024) cs *= 2;
+  const int64_t per = ((s.n + cs - 1) / cs + 15) / 16 * 16;
+  const int zcache = per <= kZCacheMax ? 1 : 0;
+  const size_t smem = (size_t)kNB * 12 + (zcache ? (size_t)per * 4 : 0);
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kNB * 12 + kZCacheMax * 4));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_select_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    (void)e;
+    configured[dev] = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(s.rows * cs));
+  cfg.blockDim = dim3(kFT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_select_fused, s, la, cs, nsplit, zcache, do_gather, zstore);
+  note_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+}  // namespace hc

@@ -207,8 +207,6 @@ __global__ void __launch_bounds__(128) k_resident(LayerArgs a) {
   HeadState *hs = a.hs + (int64_t)b * a.Hq + hq;
   const int zq = quant_res(acc, pow2f(hs->e));
   a.z[((int64_t)b * a.Hq + hq) * a.z_stride + a.n_q + r] = (float)zq;
-  atomicMax(&hs->M, zq);
-  atomicMin(&hs->zmin, zq);
 }
 
 cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s) {
