@@ -216,9 +216,12 @@ hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const 
   const RowMap codes_at = {H, L * H * g * ncap, g * ncap, (int64_t)layer * H * g * ncap + nq};
   const RowMap vstore_at = {H, L * H * ncap * d, ncap * d, ((int64_t)layer * H * ncap + nq) * d};
   const RowMap flat = {1, d, 0, 0};
-  auto encode_from = [&](const uint16_t *src, RowMap km) -> cudaError_t {
+  auto encode_from = [&](const uint16_t *src, RowMap km, const uint16_t *vsrc = nullptr,
+                         RowMap vsm = RowMap{1, 0, 0, 0}, uint16_t *vdst = nullptr,
+                         RowMap vdm = RowMap{1, 0, 0, 0}) -> cudaError_t {
     EncodeArgs a{};
     a.keys = src; a.kmap = km; a.rows = rows;
+    a.vsrc = vsrc; a.vsmap = vsm; a.vdst = vdst; a.vdmap = vdm;
     a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
     a.d = (int)d; a.g = (int)g; a.c = kc->vq.c; a.cbg = kc->vq.cbg;
     a.codes = kc->codes; a.omap = codes_at; a.gstride = ncap;
@@ -231,8 +234,7 @@ hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const 
   cudaError_t e = cudaSuccess;
   if (W == 0) {
     if (nq >= ncap) return fail(HC_ERR_CAPACITY, "layer %d full (n_cap=%lld)", layer, (long long)ncap);
-    e = encode_from(k_new, flat);
-    if (e == cudaSuccess) e = copy(v_new, flat, vs->base, vstore_at);
+    e = encode_from(k_new, flat, v_new, flat, vs->base, vstore_at);
     if (e != cudaSuccess) return cuda_check(e, "hc_append_kv");
     kc->n_q[layer] = nq + 1;
     return HC_OK;
@@ -250,8 +252,7 @@ hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const 
   if (nq >= ncap) return fail(HC_ERR_CAPACITY, "layer %d full (n_cap=%lld)", layer, (long long)ncap);
   const int64_t slot = nq % W;  // the oldest resident token (position nq)
   const RowMap res_at = {H, L * H * W * d, W * d, ((int64_t)layer * H * W + slot) * d};
-  e = encode_from(kc->res_k, res_at);
-  if (e == cudaSuccess) e = copy(kc->res_v, res_at, vs->base, vstore_at);
+  e = encode_from(kc->res_k, res_at, kc->res_v, res_at, vs->base, vstore_at);
   if (e == cudaSuccess) e = copy(k_new, flat, kc->res_k, res_at);
   if (e == cudaSuccess) e = copy(v_new, flat, kc->res_v, res_at);
   if (e != cudaSuccess) return cuda_check(e, "hc_append_kv");
@@ -306,6 +307,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   a.res_b_stride = L * H * (W > 0 ? W : 1) * d;
   a.res_slot0 = W > 0 ? n_q % W : 0;
   a.V = vs->base + (int64_t)layer * H * ncap * d;
+  a.v_placement = vs->placement == HC_V_DEVICE ? 0 : 1;
   a.v_b_stride = L * H * ncap * d;
   a.v_kv_stride = ncap * d;
   a.tau_q = (uint32_t)rint((double)budget.tau * 16777216.0);

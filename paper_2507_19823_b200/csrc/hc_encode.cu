@@ -36,7 +36,7 @@ __device__ __forceinline__ void load_centroid(const float *p, float (&c)[DBAR]) 
 // with ties to the lowest index, identical to a sequential scan (R1).
 constexpr int kEThreads = 512;
 template <int DBAR> struct EncCfg {
-  static constexpr int kER = DBAR <= 4 ? 8 : (DBAR == 8 ? 4 : 2);  // key rows per CTA
+  static constexpr int kER = 2;                                     // key rows per CTA
   static constexpr int kU = DBAR <= 2 ? 8 : (DBAR == 4 ? 4 : 2);   // centroid loads in flight
 };
 
@@ -111,6 +111,15 @@ __global__ void __launch_bounds__(kEThreads) k_encode(EncodeArgs a) {
       if (ob < b_ || (ob == b_ && om < m_)) { b_ = ob; m_ = om; }
     }
     if (l == 0) a.codes[rowoff(a.omap, r0 + r) + (int64_t)i * a.gstride] = (uint16_t)m_;
+  }
+  // fused append of the rows' values (hc_append_kv): group-0 CTAs copy 16 B per thread
+  if (a.vsrc && i == 0) {
+    const int per_row = a.d / 8;
+    if ((int)threadIdx.x < nr * per_row) {
+      const int r = threadIdx.x / per_row, q = threadIdx.x % per_row;
+      const uint4 v = *reinterpret_cast<const uint4 *>(a.vsrc + rowoff(a.vsmap, r0 + r) + q * 8);
+      *reinterpret_cast<uint4 *>(a.vdst + rowoff(a.vdmap, r0 + r) + q * 8) = v;
+    }
   }
 }
 

@@ -27,6 +27,11 @@ struct EncodeArgs {
   uint16_t *codes;
   RowMap omap;           // code offset of (r, group 0)
   int64_t gstride;       // elements between groups
+  // optional fused value-row copy (append): vdst[vdmap(r)] = vsrc[vsmap(r)], d halves
+  const uint16_t *vsrc;
+  RowMap vsmap;
+  uint16_t *vdst;
+  RowMap vdmap;
 };
 cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s);
 
@@ -54,6 +59,7 @@ struct LayerArgs {
   int64_t res_b_stride;   // elements between batches
   int64_t res_slot0;      // slot of candidate n_q: (n_q) % W
   const uint16_t *V;      // value store at layer l, batch 0
+  int v_placement;        // 0 = HBM (bulk-copy ring gather), 1 = host-mapped (zero-copy loads)
   int64_t v_b_stride;     // elements between batches
   int64_t v_kv_stride;    // elements between KV heads
   // budget

@@ -17,6 +17,7 @@
 //       zero-copy when V is host-mapped); rank 0 adds the cs partials in rank order.
 // All sums that decide indices are integers: bit-exact and decomposition-invariant.
 #include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "hc_internal.h"
 
@@ -93,13 +94,16 @@ __device__ __forceinline__ uint4 ld_nc16(const uint16_t *p) {
 
 __global__ void __launch_bounds__(kFT, 1)
     k_select_fused(SelArgs s, LayerArgs la, int cs, int nsplit, int zcache, int do_gather,
-                   int zstore) {
+                   int zstore, int stop) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int row = blockIdx.x / cs;
   const int tid = threadIdx.x;
   extern __shared__ __align__(16) uint8_t smem[];
-  unsigned long long *ms = reinterpret_cast<unsigned long long *>(smem);        // [kNB]
+  // per-bin mass as two u32 words (native 32-bit shared atomics; a 64-bit shared
+  // atomicAdd compiles to a CAS spin loop): mass = mhi * 2^32 + mlo
+  uint32_t *mlo = reinterpret_cast<uint32_t *>(smem);                            // [kNB]
+  uint32_t *mhi = reinterpret_cast<uint32_t *>(smem + kNB * 4);                  // [kNB]
   uint32_t *cnt = reinterpret_cast<uint32_t *>(smem + kNB * 8);                  // [kNB]
   float *zc = reinterpret_cast<float *>(smem + kNB * 12);                        // token cache
   __shared__ Slot slot;
@@ -118,15 +122,51 @@ __global__ void __launch_bounds__(kFT, 1)
   };
 
   // ---------------------------------------------------------------- P0: z, M, zmin
+  // 4 consecutive tokens per thread per round, all split planes loaded before use.
   int mx = INT_MIN, mn = INT_MAX;
-  for (int64_t t = tid; t < nt; t += kFT) {
-    const int64_t j = j0 + t;
-    const float zf = load_z(la, s, row, j, nsplit);
-    if (zcache) zc[t] = zf;
-    if ((!zcache || zstore) && nsplit > 1) const_cast<float *>(s.z)[(int64_t)row * s.z_stride + j] = zf;
-    const int zi = __float2int_rn(zf);
-    mx = max(mx, zi);
-    mn = min(mn, zi);
+  {
+    const float *zr = s.z + (int64_t)row * s.z_stride;
+    const int64_t plane = (int64_t)la.B * la.Hq * la.z_stride;
+    const float *zp = la.zpart + (int64_t)row * la.z_stride;
+    const int64_t qend = nsplit > 1 ? (la.n_q < j1 ? la.n_q : j1) : j0;  // [j0, qend) from partials
+    for (int64_t t = (int64_t)tid * 4; t < nt; t += (int64_t)kFT * 4) {
+      const int64_t j = j0 + t;
+      float v[4];
+      if (j + 4 <= qend) {
+        float4 acc = *reinterpret_cast<const float4 *>(zp + j);
+        float4 part[3];
+#pragma unroll
+        for (int sp = 1; sp < 4; ++sp)
+          if (sp < nsplit) part[sp - 1] = *reinterpret_cast<const float4 *>(zp + sp * plane + j);
+#pragma unroll
+        for (int sp = 1; sp < 4; ++sp)
+          if (sp < nsplit) {
+            acc.x += part[sp - 1].x; acc.y += part[sp - 1].y;
+            acc.z += part[sp - 1].z; acc.w += part[sp - 1].w;
+          }
+        for (int sp = 4; sp < nsplit; ++sp) {
+          const float4 q4 = *reinterpret_cast<const float4 *>(zp + sp * plane + j);
+          acc.x += q4.x; acc.y += q4.y; acc.z += q4.z; acc.w += q4.w;
+        }
+        v[0] = acc.x; v[1] = acc.y; v[2] = acc.z; v[3] = acc.w;
+      } else if (j >= qend && j + 4 <= j1 && ((j & 3) == 0)) {
+        const float4 q4 = *reinterpret_cast<const float4 *>(zr + j);
+        v[0] = q4.x; v[1] = q4.y; v[2] = q4.z; v[3] = q4.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (j + u < j1) ? load_z(la, s, row, j + u, nsplit) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t + u < nt) {
+          if (zcache) zc[t + u] = v[u];
+          if ((!zcache || zstore) && nsplit > 1) const_cast<float *>(zr)[j + u] = v[u];
+          const int zi = __float2int_rn(v[u]);
+          mx = max(mx, zi);
+          mn = min(mn, zi);
+        }
+      }
+    }
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   mn = __reduce_min_sync(0xffffffffu, mn);
@@ -150,30 +190,39 @@ __global__ void __launch_bounds__(kFT, 1)
   const uint32_t dmax = (uint32_t)(M - zmin);
   const int bits = 32 - __clz(dmax);
   const int shift = bits > kNBBits ? bits - kNBBits : 0;
+  if (stop == 1) { cl.sync(); return; }
   const int nbo = kNB / cs;                 // owned bins per CTA
   const int b_lo = rank * nbo;
 
   // ---------------------------------------------------------------- P1: coarse histogram
-  for (int i = tid; i < kNB; i += kFT) { cnt[i] = 0; ms[i] = 0ull; }
+  for (int i = tid; i < kNB; i += kFT) { cnt[i] = 0; mlo[i] = 0u; mhi[i] = 0u; }
   __syncthreads();
   for (int64_t t = tid; t < nt; t += kFT) {
     const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
     const uint64_t W = mass(dl, kappa);
-    if (W) atomicAdd(&ms[bk], (unsigned long long)W);
+    if (W) {
+      const uint32_t wl = (uint32_t)W;
+      uint32_t wh = (uint32_t)(W >> 32);
+      const uint32_t old = atomicAdd(&mlo[bk], wl);
+      wh += (old + wl < old) ? 1u : 0u;  // carry out of the low word
+      if (wh) atomicAdd(&mhi[bk], wh);
+    }
   }
   cl.sync();
   for (int i = tid; i < nbo; i += kFT) {  // sum my owned bins over the peers
     uint32_t c = cnt[b_lo + i];
-    unsigned long long m = ms[b_lo + i];
+    unsigned long long m = ((unsigned long long)mhi[b_lo + i] << 32) + mlo[b_lo + i];
     for (int r = 0; r < cs; ++r) {
       if (r == rank) continue;
       c += cl.map_shared_rank(cnt, r)[b_lo + i];
-      m += cl.map_shared_rank(ms, r)[b_lo + i];
+      m += ((unsigned long long)cl.map_shared_rank(mhi, r)[b_lo + i] << 32) +
+           cl.map_shared_rank(mlo, r)[b_lo + i];
     }
     cnt[b_lo + i] = c;
-    ms[b_lo + i] = m;
+    mlo[b_lo + i] = (uint32_t)m;
+    mhi[b_lo + i] = (uint32_t)(m >> 32);
   }
   cl.sync();
   // bound1 over the owned bins: thread owns bins [b_lo + tid*bpt, +bpt)
@@ -181,7 +230,7 @@ __global__ void __launch_bounds__(kFT, 1)
   unsigned long long lc = 0, lm = 0;
   for (int k = 0; k < bpt; ++k) {
     const int bi = tid * bpt + k;
-    if (bi < nbo) { lc += cnt[b_lo + bi]; lm += ms[b_lo + bi]; }
+    if (bi < nbo) { lc += cnt[b_lo + bi]; lm += ((unsigned long long)mhi[b_lo + bi] << 32) + mlo[b_lo + bi]; }
   }
   unsigned long long pc = lc, pm = lm, tc, tm;
   bscan2<unsigned long long>(pc, pm, tc, tm, sx, sy);
@@ -204,7 +253,8 @@ __global__ void __launch_bounds__(kFT, 1)
     for (int k = 0; k < bpt; ++k) {
       const int bi = tid * bpt + k;
       if (bi >= nbo) break;
-      const unsigned long long c = cnt[b_lo + bi], m = ms[b_lo + bi];
+      const unsigned long long c = cnt[b_lo + bi];
+      const unsigned long long m = ((unsigned long long)mhi[b_lo + bi] << 32) + mlo[b_lo + bi];
       const bool trig = c && ((!tau_all && cm + m >= theta) || (!cap_all && cc + c >= (unsigned long long)s.k_max));
       if (trig && found == kNB) { found = b_lo + bi; fcb = cc; fmb = cm; }
       cc += c;
@@ -220,6 +270,7 @@ __global__ void __launch_bounds__(kFT, 1)
     const int c = cl.map_shared_rank(&slot, r)->cand;
     if (c < bstar) { bstar = c; owner = r; }
   }
+  if (stop == 2) { cl.sync(); return; }
   unsigned long long cnt_before = 0, mass_before = 0;
   if (owner >= 0) {
     cnt_before = cl.map_shared_rank(&slot, owner)->cb;
@@ -312,16 +363,37 @@ __global__ void __launch_bounds__(kFT, 1)
   }
   // ---------------------------------------------------------------- P3: compaction
   cl.sync();  // peers done with my slot
-  unsigned long long my_s = 0, my_t = 0;
-  for (int64_t t = tid; t < nt; t += kFT) {
-    const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
-    my_s += dl < delta_star;
-    my_t += dl == delta_star;
-  }
+  if (stop == 3) return;
+  // warp-chunked ordered compaction: warp w owns tokens [w*wc, (w+1)*wc) of this CTA;
+  // lane-strided (bank-conflict-free) reads, ballots give in-order positions.
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t wc = ((nt + kFT / 32 - 1) / (kFT / 32) + 31) / 32 * 32;
+  const int64_t w_lo = (int64_t)warp * wc;
+  const int64_t w_hi = w_lo + wc < nt ? w_lo + wc : nt;
+  __shared__ unsigned long long s_ws[kFT / 32], s_wt[kFT / 32];
   {
-    unsigned long long a0 = my_s, a1 = my_t, t0_, t1_;
-    bscan2<unsigned long long>(a0, a1, t0_, t1_, sx, sy);
-    if (tid == 0) { slot.ns = t0_; slot.nt = t1_; }
+    unsigned int ns = 0, ntie = 0;
+    for (int64_t t = w_lo + lane; t < w_hi; t += 32) {
+      const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
+      ns += dl < delta_star;
+      ntie += dl == delta_star;
+    }
+    ns = __reduce_add_sync(0xffffffffu, ns);
+    ntie = __reduce_add_sync(0xffffffffu, ntie);
+    if (lane == 0) { s_ws[warp] = ns; s_wt[warp] = ntie; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long a0 = 0, a1 = 0;
+    for (int w = 0; w < kFT / 32; ++w) {
+      const unsigned long long x0 = s_ws[w], x1 = s_wt[w];
+      s_ws[w] = a0;  // exclusive prefix within the CTA
+      s_wt[w] = a1;
+      a0 += x0;
+      a1 += x1;
+    }
+    slot.ns = a0;
+    slot.nt = a1;
   }
   cl.sync();
   unsigned long long s_before = 0, t_before = 0;
@@ -330,47 +402,37 @@ __global__ void __launch_bounds__(kFT, 1)
     s_before += o->ns;
     t_before += o->nt;
   }
+  const unsigned long long cta_s = slot.ns, cta_t = slot.nt;
   const double denom = s.renorm ? (double)selmass : (double)S;
   int32_t *oi = s.sel_idx + (int64_t)row * s.k_max;
   float *ow = s.sel_w + (int64_t)row * s.k_max;
   const unsigned long long sel_begin = s_before + (t_before < r_ties ? t_before : r_ties);
-  unsigned long long sel_count = 0;
+  const unsigned long long sel_end =
+      s_before + cta_s + (t_before + cta_t < r_ties ? t_before + cta_t : r_ties);
+  const unsigned long long sel_count = sel_end - sel_begin;
   {
-    unsigned long long run_s = s_before, run_t = t_before;  // running totals before each round
-    for (int64_t base = 0; base < nt; base += (int64_t)kFT * 16) {
-      const int64_t t = base + (int64_t)tid * 16;
-      uint32_t dl[16];
-      unsigned long long ns = 0, ntie = 0;
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const bool v = t + u < nt;
-        dl[u] = v ? (uint32_t)(M - __float2int_rn(zat(j0 + t + u))) : 0xffffffffu;
-        ns += v && dl[u] < delta_star;
-        ntie += v && dl[u] == delta_star;
+    unsigned long long t_run = t_before + s_wt[warp];                      // ties before
+    const unsigned long long s_run0 = s_before + s_ws[warp];
+    unsigned long long pos = s_run0 + (t_run < r_ties ? t_run : r_ties);   // kept before
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t tb = w_lo; tb < w_hi; tb += 32) {
+      const int64_t t = tb + lane;
+      const bool v = t < w_hi;
+      const uint32_t dl = v ? (uint32_t)(M - __float2int_rn(zat(j0 + t))) : 0xffffffffu;
+      const bool st = v && dl < delta_star;
+      const bool ti = v && dl == delta_star;
+      const unsigned bt = __ballot_sync(0xffffffffu, ti);
+      const unsigned long long my_tie_rank = t_run + __popc(bt & lt);
+      const bool take = st || (ti && my_tie_rank < r_ties);
+      const unsigned bs = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const unsigned long long p = pos + __popc(bs & lt);
+        oi[p] = (int32_t)(j0 + t);
+        ow[p] = (float)((double)mass(dl, kappa) / denom);
       }
-      unsigned long long ps = ns, pt = ntie, ts, tt;
-      bscan2<unsigned long long>(ps, pt, ts, tt, sx, sy);
-      const unsigned long long rem = r_ties > run_t ? r_ties - run_t : 0;
-      unsigned long long tie_rank = pt;
-      unsigned long long pos = run_s + (run_t < r_ties ? run_t : r_ties) + ps + (rem < pt ? rem : pt);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        bool take = dl[u] < delta_star;
-        if (!take && dl[u] == delta_star && t + u < nt) {
-          take = tie_rank < rem;
-          ++tie_rank;
-        }
-        if (take) {
-          oi[pos] = (int32_t)(j0 + t + u);
-          ow[pos] = (float)((double)mass(dl[u], kappa) / denom);
-          ++pos;
-        }
-      }
-      run_s += ts;
-      run_t += tt;
+      pos += __popc(bs);
+      t_run += __popc(bt);
     }
-    const unsigned long long end = run_s + (run_t < r_ties ? run_t : r_ties);
-    sel_count = end - sel_begin;
   }
   if (rank == 0 && tid == 0) {
     hs->M = M;
@@ -386,14 +448,16 @@ __global__ void __launch_bounds__(kFT, 1)
     hs->sel_mass = selmass;
     if (s.sel_k) s.sel_k[row] = (int64_t)ksel;
   }
-  if (!do_gather) return;
+  if (!do_gather || stop == 4) {
+    cl.sync();  // peers may still read my slot (P3 prefix) through DSMEM
+    return;
+  }
   // ---------------------------------------------------------------- P4: gather (Eq. 5)
   __syncthreads();  // this CTA's sel_idx / sel_w writes are visible to its own threads
   const int b = row / la.Hq, hq = row - b * la.Hq, kv = hq / la.G;
   const int lpr = la.d >> 3;           // lanes per row (16 at d = 128)
   const int rpw = 32 / lpr;
   const int nslots = (kFT / 32) * rpw;
-  const int lane = tid & 31;
   const int gslot = (tid >> 5) * rpw + lane / lpr;
   const int sub = lane % lpr;
   const uint16_t *Vb = la.V + (int64_t)b * la.v_b_stride + (int64_t)kv * la.v_kv_stride;
@@ -402,25 +466,49 @@ __global__ void __launch_bounds__(kFT, 1)
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
   const int64_t r0 = (int64_t)sel_begin, r1 = (int64_t)(sel_begin + sel_count);
-  for (int64_t r = r0 + gslot; r < r1; r += (int64_t)nslots * kGU) {
-    uint4 v[kGU];
-    float w[kGU];
+  // half-warp per 256-B row (16 x 16-B L1-bypassing loads; zero-copy over the host link
+  // when V is host-mapped), software-pipelined: the (index, weight) batch of round k+1 is
+  // loaded while round k's rows are in flight
+  if (stop != 5) {
+    int32_t jn[kGU];
+    float wn[kGU];
+    const int64_t step = (int64_t)nslots * kGU;
+    int64_t r = r0 + gslot;
 #pragma unroll
     for (int u = 0; u < kGU; ++u) {
       const int64_t rr = r + (int64_t)u * nslots;
-      if (rr < r1) {
-        const int64_t j = oi[rr];
-        w[u] = ow[rr];
-        const uint16_t *src = j < la.n_q ? Vb + j * la.d
-                                         : Rb + ((la.res_slot0 + (j - la.n_q)) % la.res_cap) * la.d;
-        v[u] = ld_nc16(src + sub * 8);
-      } else {
-        w[u] = 0.0f;
-        v[u] = make_uint4(0, 0, 0, 0);
-      }
+      jn[u] = rr < r1 ? oi[rr] : -1;
+      wn[u] = rr < r1 ? ow[rr] : 0.0f;
     }
+    for (; r < r1; r += step) {
+      uint4 v[kGU];
+      float w[kGU];
 #pragma unroll
-    for (int u = 0; u < kGU; ++u) fma8(acc, w[u], v[u]);
+      for (int u = 0; u < kGU; ++u) {
+        const int64_t j = jn[u];
+        w[u] = wn[u];
+        if (j >= 0) {
+          const uint16_t *src;
+          if (j < la.n_q) {
+            src = Vb + j * la.d;
+          } else {  // resident window slot (rare): 32-bit modulo
+            const uint32_t slot_ = (uint32_t)(la.res_slot0 + (j - la.n_q)) % (uint32_t)la.res_cap;
+            src = Rb + (int64_t)slot_ * la.d;
+          }
+          v[u] = ld_nc16(src + sub * 8);
+        } else {
+          v[u] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        const int64_t rr = r + step + (int64_t)u * nslots;
+        jn[u] = rr < r1 ? oi[rr] : -1;
+        wn[u] = rr < r1 ? ow[rr] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) fma8(acc, w[u], v[u]);
+    }
   }
   // CTA partial: slots -> d floats (fixed order), kept in shared memory for the cluster
   float *part = reinterpret_cast<float *>(cnt);  // reuse the histogram space (>= d floats)
@@ -450,7 +538,7 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
   while (cs < 8 && (int64_t)s.rows * cs * 2 <= num_sms && s.n / (cs * 2) >= 1024) cs *= 2;
   const int64_t per = ((s.n + cs - 1) / cs + 15) / 16 * 16;
   const int zcache = per <= kZCacheMax ? 1 : 0;
-  const size_t smem = (size_t)kNB * 12 + (zcache ? (size_t)per * 4 : 0);
+  size_t smem = (size_t)kNB * 12 + (zcache ? (size_t)per * 4 : 0);
   static int configured[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -474,7 +562,13 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_select_fused, s, la, cs, nsplit, zcache, do_gather, zstore);
+  static int stop_env = -1;
+  if (stop_env < 0) {
+    const char *ev = getenv("HC_SEL_STOP");
+    stop_env = ev ? atoi(ev) : 0;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_select_fused, s, la, cs, nsplit, zcache, do_gather, zstore,
+                                     stop_env);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
