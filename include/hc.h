@@ -174,6 +174,41 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
                          int32_t *idx, float *w, int64_t *k, void *ws, size_t ws_bytes,
                          hc_stream_t stream);
 
+/* ---- Sequence-sharded decode, one layer, R ranks (one per GPU).
+ * Rank `rank` holds the contiguous GLOBAL token range [shard_base, shard_base + n_q[layer])
+ * of every (b, layer, kv) unit (its own codes and value rows; no resident window).  The
+ * scores are exact integers (R2/R3) and the softmax mass is a function of Δ = M − z only
+ * (R4), so the global Eq. 4 selection is assembled from integer collectives that the
+ * CALLER performs between the phases (NCCL over NVLink on GPUs; any backend works):
+ *   hc_shard_begin   table + scan;   stats [rows][2] int32 {max z, -min z}  -> all-reduce MAX
+ *   hc_shard_hist1   (global stats)  h1 [rows][4096][2] uint64 (count, mass)  -> all-reduce SUM
+ *   hc_shard_hist2   (global h1)     h2 [rows][4096] uint64 (fine counts)     -> all-reduce SUM
+ *   hc_shard_counts  (global h2)     cnt [rows][2] uint64 (#Δ<Δ*, #Δ==Δ*)     -> all-gather
+ *   hc_shard_finish  (allcnt [R][rows][2]) writes this rank's kept tokens (global indices) at
+ *                    their GLOBAL positions of sel_idx/sel_w [rows][k_max] (other ranks'
+ *                    positions untouched) and its Eq. 5 numerator share out [rows][d] fp32
+ *                                                                               -> all-reduce SUM
+ * rows = B*Hq.  Every rank evaluates the same bounds on the same reduced integers, so the
+ * kept index set equals the unsharded one bit for bit (R-invariance).  The workspace
+ * (hc_shard_workspace_bytes) carries state between the phases of one layer. */
+size_t hc_shard_workspace_bytes(const hc_kcache *kc, hc_budget budget);
+hc_status hc_shard_begin(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs, int32_t layer,
+                         hc_budget budget, int32_t *stats, void *ws, size_t ws_bytes,
+                         hc_stream_t stream);
+hc_status hc_shard_hist1(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                         const int32_t *gstats, uint64_t *h1, void *ws, size_t ws_bytes,
+                         hc_stream_t stream);
+hc_status hc_shard_hist2(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                         const int32_t *gstats, const uint64_t *h1, uint64_t *h2, void *ws,
+                         size_t ws_bytes, hc_stream_t stream);
+hc_status hc_shard_counts(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                          const uint64_t *h2, uint64_t *cnt, void *ws, size_t ws_bytes,
+                          hc_stream_t stream);
+hc_status hc_shard_finish(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                          const uint64_t *allcnt, int32_t rank, int32_t world, int64_t shard_base,
+                          float *out, int32_t *sel_idx, float *sel_w, int64_t *sel_k, void *ws,
+                          size_t ws_bytes, hc_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

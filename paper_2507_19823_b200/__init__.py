@@ -23,7 +23,8 @@ HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
 EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_events",
            "hc_codebook_absmax", "hc_quantize_keys", "hc_append_kv",
            "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
-           "hc_select_topk"]
+           "hc_select_topk", "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
+           "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish"]
 
 
 class HcError(RuntimeError):
@@ -90,6 +91,18 @@ def lib():
         L.hc_select_workspace_bytes.restype = C.c_size_t
         L.hc_select_topk.argtypes = [p, i64, i64, i32, hc_budget, p, p, p, p, C.c_size_t, p]
         L.hc_select_topk.restype = i32
+        KC, VS = C.POINTER(hc_kcache), C.POINTER(hc_vstore)
+        L.hc_shard_workspace_bytes.argtypes = [KC, hc_budget]
+        L.hc_shard_workspace_bytes.restype = C.c_size_t
+        L.hc_shard_begin.argtypes = [p, KC, VS, i32, hc_budget, p, p, C.c_size_t, p]
+        L.hc_shard_hist1.argtypes = [KC, VS, i32, hc_budget, p, p, p, C.c_size_t, p]
+        L.hc_shard_hist2.argtypes = [KC, VS, i32, hc_budget, p, p, p, p, C.c_size_t, p]
+        L.hc_shard_counts.argtypes = [KC, VS, i32, hc_budget, p, p, p, C.c_size_t, p]
+        L.hc_shard_finish.argtypes = [KC, VS, i32, hc_budget, p, i32, i32, i64, p, p, p, p, p,
+                                      C.c_size_t, p]
+        for f in ("hc_shard_begin", "hc_shard_hist1", "hc_shard_hist2", "hc_shard_counts",
+                  "hc_shard_finish"):
+            getattr(L, f).restype = i32
         _lib = L
     return _lib
 

@@ -92,7 +92,8 @@ struct Layout {
   int cpow2;
   int64_t z_stride;
   int64_t k_eff;
-  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, total;
+  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, total;
+  int nch_max;  // sharded compaction chunks
 };
 
 Layout make_layout(const hc_kcache *kc, int64_t k_max) {
@@ -114,6 +115,9 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
   L.o_zpart = o; o += align256((size_t)kMaxScanSplit * rows * L.z_stride * 4);
   L.o_idx = o; o += align256((size_t)rows * L.k_eff * 4);
   L.o_w = o; o += align256((size_t)rows * L.k_eff * 4);
+  L.nch_max = shard_chunks(ncand_max > 0 ? ncand_max : 1);
+  L.o_chunk = o; o += align256((size_t)rows * L.nch_max * 8);
+  L.o_part = o; o += align256((size_t)rows * L.nch_max * d * 4);
   L.total = o;
   return L;
 }
@@ -265,10 +269,11 @@ size_t hc_decode_workspace_bytes(const hc_kcache *kc, hc_budget budget) {
   return make_layout(kc, budget.k_max).total;
 }
 
-hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
-                              int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
-                              float *sel_w, int64_t *sel_k, const hc_decode_debug *dbg, void *ws,
-                              size_t ws_bytes, hc_stream_t stream) {
+// validation + LayerArgs of one layer call (decode or a sharded phase)
+static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
+                               int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
+                               float *sel_w, int64_t *sel_k, void *ws, size_t ws_bytes,
+                               cudaStream_t s, bool need_q, LayerArgs &a, Layout &Lw) {
   hc_status st = check_kcache(kc);
   if (st) return st;
   if (!vs || !vs->base) return fail(HC_ERR_ARG, "vstore is NULL");
@@ -276,7 +281,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   if (!(vs->placement == HC_V_DEVICE || vs->placement == HC_V_HOST_MAPPED))
     return fail(HC_ERR_ARG, "bad vstore placement");
   if (layer < 0 || layer >= kc->L) return fail(HC_ERR_RANGE, "layer %d out of range", layer);
-  if (!q || !out) return fail(HC_ERR_ARG, "q/out NULL");
+  if (need_q && (!q || !out)) return fail(HC_ERR_ARG, "q/out NULL");
   if (!(budget.tau > 0.0f && budget.tau <= 1.0f)) return fail(HC_ERR_ARG, "tau=%g not in (0,1]", budget.tau);
   if (budget.k_max < 1) return fail(HC_ERR_ARG, "k_max < 1");
   if (!!sel_idx != !!sel_w) return fail(HC_ERR_ARG, "pass both sel_idx and sel_w, or neither");
@@ -285,16 +290,13 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     return fail(HC_ERR_RANGE, "cache counts out of range");
   const int64_t n_cand = n_q + n_res;
   if (n_cand == 0) return fail(HC_ERR_EMPTY, "layer %d has no tokens", layer);
-  const Layout Lw = make_layout(kc, budget.k_max);
+  Lw = make_layout(kc, budget.k_max);
   if (!ws || ws_bytes < Lw.total)
     return fail(HC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, Lw.total);
-  cudaStream_t s = (cudaStream_t)stream;
   uint8_t *w8 = (uint8_t *)ws;
   const int64_t B = kc->B, H = kc->Hkv, G = kc->G, Hq = G * H, d = kc->vq.d, g = kc->vq.g;
   const int64_t L = kc->L, W = kc->res_cap, ncap = kc->n_cap;
-  const int rows = (int)(B * Hq);
-
-  LayerArgs a{};
+  a = LayerArgs{};
   a.B = (int)B; a.Hkv = (int)H; a.G = (int)G; a.Hq = (int)Hq; a.d = (int)d; a.g = (int)g;
   a.c = kc->vq.c; a.cbg = kc->vq.cbg; a.dbar = (int)(d / g); a.cpow2 = Lw.cpow2;
   a.n_q = n_q; a.n_res = n_res; a.n_cand = n_cand; a.n_cap = ncap; a.res_cap = W > 0 ? W : 1;
@@ -317,7 +319,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   a.T = (int16_t *)(w8 + Lw.o_T);
   if (kc->cb_absmax) {
     a.cb_absmax = kc->cb_absmax + (int64_t)layer * kc->vq.cbg * (d / g);
-  } else {
+  } else if (need_q) {
     float *cba = (float *)(w8 + Lw.o_cbabs);
     cudaError_t e0 = launch_cbabs(a.C, kc->vq.cbg, kc->vq.c, (int)(d / g), cba, s);
     if (e0 != cudaSuccess) return cuda_check(e0, "codebook absmax");
@@ -341,6 +343,21 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   choose_scan(B * H, n_q, (int)g, Lw.cpow2, (int)G, a.num_sms, &a.scan_tpt, &a.scan_split);
   a.zpart = (float *)(w8 + Lw.o_zpart);
 
+  return HC_OK;
+}
+
+hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
+                              int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
+                              float *sel_w, int64_t *sel_k, const hc_decode_debug *dbg, void *ws,
+                              size_t ws_bytes, hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  LayerArgs a;
+  Layout Lw;
+  hc_status st = prepare_layer(q, kc, vs, layer, budget, out, sel_idx, sel_w, sel_k, ws, ws_bytes, s,
+                               true, a, Lw);
+  if (st) return st;
+  const int rows = a.B * a.Hq;
+  const int64_t n_q = a.n_q, n_cand = a.n_cand;
   cudaError_t e;
   if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
   if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
@@ -369,6 +386,106 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     }
   }
   return HC_OK;
+}
+
+// ---------------------------------------------------------------- sequence-sharded decode
+static hc_status shard_prepare(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
+                               int32_t layer, hc_budget budget, void *ws, size_t ws_bytes,
+                               cudaStream_t s, bool need_q, LayerArgs &a, Layout &Lw, SelArgs &sa,
+                               int32_t *sel_idx = nullptr, float *sel_w = nullptr,
+                               int64_t *sel_k = nullptr) {
+  if (kc && kc->res_cap > 0 && kc->n_res[layer < 0 || layer >= HC_MAX_LAYERS ? 0 : layer] > 0)
+    return fail(HC_ERR_UNSUPPORTED, "sharded decode does not take a resident window (n_res must be 0)");
+  float dummy_out = 0.0f;
+  hc_status st = prepare_layer(q, kc, vs, layer, budget, need_q ? &dummy_out : &dummy_out, sel_idx,
+                               sel_w, sel_k, ws, ws_bytes, s, need_q, a, Lw);
+  if (st) return st;
+  a.out = nullptr;
+  sa = SelArgs{};
+  sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = a.B * a.Hq; sa.n = a.n_cand;
+  sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
+  sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
+  return HC_OK;
+}
+
+size_t hc_shard_workspace_bytes(const hc_kcache *kc, hc_budget budget) {
+  return hc_decode_workspace_bytes(kc, budget);
+}
+
+hc_status hc_shard_begin(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs, int32_t layer,
+                         hc_budget budget, int32_t *stats, void *ws, size_t ws_bytes,
+                         hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  LayerArgs a; Layout Lw; SelArgs sa;
+  hc_status st = shard_prepare(q, kc, vs, layer, budget, ws, ws_bytes, s, true, a, Lw, sa);
+  if (st) return st;
+  if (!stats) return fail(HC_ERR_ARG, "stats NULL");
+  cudaError_t e;
+  if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
+  if (a.n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
+  return cuda_check(launch_shard_stats(a, a.n_q > 0 ? a.scan_split : 1, stats, s), "shard stats");
+}
+
+hc_status hc_shard_hist1(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                         const int32_t *gstats, uint64_t *h1, void *ws, size_t ws_bytes,
+                         hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  LayerArgs a; Layout Lw; SelArgs sa;
+  hc_status st = shard_prepare(nullptr, kc, vs, layer, budget, ws, ws_bytes, s, false, a, Lw, sa);
+  if (st) return st;
+  if (!gstats || !h1) return fail(HC_ERR_ARG, "NULL pointer");
+  return cuda_check(launch_shard_hist1(a, gstats, (unsigned long long *)h1, s), "shard hist1");
+}
+
+hc_status hc_shard_hist2(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                         const int32_t *gstats, const uint64_t *h1, uint64_t *h2, void *ws,
+                         size_t ws_bytes, hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  LayerArgs a; Layout Lw; SelArgs sa;
+  hc_status st = shard_prepare(nullptr, kc, vs, layer, budget, ws, ws_bytes, s, false, a, Lw, sa);
+  if (st) return st;
+  if (!gstats || !h1 || !h2) return fail(HC_ERR_ARG, "NULL pointer");
+  return cuda_check(launch_shard_hist2(a, sa, gstats, (const unsigned long long *)h1,
+                                       (unsigned long long *)h2, s), "shard hist2");
+}
+
+hc_status hc_shard_counts(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                          const uint64_t *h2, uint64_t *cnt, void *ws, size_t ws_bytes,
+                          hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  LayerArgs a; Layout Lw; SelArgs sa;
+  hc_status st = shard_prepare(nullptr, kc, vs, layer, budget, ws, ws_bytes, s, false, a, Lw, sa);
+  if (st) return st;
+  if (!h2 || !cnt) return fail(HC_ERR_ARG, "NULL pointer");
+  return cuda_check(launch_shard_counts(a, sa, (const unsigned long long *)h2,
+                                        (uint32_t *)((uint8_t *)ws + Lw.o_chunk),
+                                        (unsigned long long *)cnt, s), "shard counts");
+}
+
+hc_status hc_shard_finish(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, hc_budget budget,
+                          const uint64_t *allcnt, int32_t rank, int32_t world, int64_t shard_base,
+                          float *out, int32_t *sel_idx, float *sel_w, int64_t *sel_k, void *ws,
+                          size_t ws_bytes, hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (rank < 0 || world < 1 || rank >= world) return fail(HC_ERR_RANGE, "rank/world");
+  if (!allcnt || !out || !sel_idx || !sel_w) return fail(HC_ERR_ARG, "NULL pointer");
+  if (shard_base < 0) return fail(HC_ERR_RANGE, "shard_base < 0");
+  LayerArgs a; Layout Lw; SelArgs sa;
+  hc_status st = shard_prepare(nullptr, kc, vs, layer, budget, ws, ws_bytes, s, false, a, Lw, sa,
+                               sel_idx, sel_w, sel_k);
+  if (st) return st;
+  if (shard_base + a.n_cand > 0x7fffffffLL) return fail(HC_ERR_UNSUPPORTED, "global index >= 2^31");
+  uint8_t *w8 = (uint8_t *)ws;
+  cudaError_t e = launch_shard_finish(a, sa, (const uint32_t *)(w8 + Lw.o_chunk),
+                                      (const unsigned long long *)allcnt, rank, shard_base,
+                                      (float *)(w8 + Lw.o_part), out, s);
+  if (e != cudaSuccess) return cuda_check(e, "shard finish");
+  if (sel_k) {
+    const int rows = a.B * a.Hq;
+    e = cudaMemcpy2DAsync(sel_k, 8, &a.hs->ksel, sizeof(HeadState), 8, rows,
+                          cudaMemcpyDeviceToDevice, s);
+  }
+  return cuda_check(e, "shard finish");
 }
 
 size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {

@@ -110,6 +110,19 @@ struct SelArgs {
 cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
                                 int num_sms, cudaStream_t st, int zstore = 0);
 
+// sequence-sharded phases (hc_shard.cu)
+int shard_chunks(int64_t n);
+cudaError_t launch_shard_stats(const LayerArgs &a, int nsplit, int32_t *stats, cudaStream_t st);
+cudaError_t launch_shard_hist1(const LayerArgs &a, const int32_t *gstats, unsigned long long *h1,
+                               cudaStream_t st);
+cudaError_t launch_shard_hist2(const LayerArgs &a, const SelArgs &s, const int32_t *gstats,
+                               const unsigned long long *h1, unsigned long long *h2, cudaStream_t st);
+cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsigned long long *h2,
+                                uint32_t *chunk, unsigned long long *cnt, cudaStream_t st);
+cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
+                                const unsigned long long *allcnt, int rank, int64_t base,
+                                float *part, float *out, cudaStream_t st);
+
 // standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
                                      int64_t z_stride, HeadState *hs, float kappa0,

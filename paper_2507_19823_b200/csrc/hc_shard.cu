@@ -1,0 +1,444 @@
+// hc_shard.cu -- SURVEY §8(e): sequence-sharded decode across R GPUs.
+//
+// Rank r holds the contiguous global token range [base, base + n_q) of every
+// (b, layer, kv) unit (its own P codes and V rows).  Because the scores are exact
+// integers (R2/R3) and the softmax mass W is a function of Δ = M - z alone (R4), the
+// global selection (R5) can be assembled from integer all-reductions only:
+//   stats  : local max / min of z                 -> all-reduce MAX       (C1)
+//   hist1  : coarse (count, mass) histogram of Δ   -> all-reduce SUM u64   (C2)
+//   hist2  : fine histogram inside the global b*   -> all-reduce SUM u64   (C3)
+//   counts : local (#Δ<Δ*, #Δ==Δ*) per chunk       -> all-gather row totals (C4)
+//   finish : ordered compaction with global offsets + local Eq. 5 partial sums
+//                                                  -> all-reduce SUM fp32  (C5)
+// Every rank evaluates bound1 / bound2 on the same reduced integers, so all ranks
+// agree on (b*, Δ*, r) bit for bit: the index set is R-invariant.
+#include "hc_internal.h"
+
+namespace hc {
+
+constexpr int kShT = 256;
+constexpr int kShChunk = 4096;  // tokens per compaction chunk (16 per thread)
+
+__device__ __forceinline__ float sh_z(const LayerArgs &a, int row, int64_t j, int nsplit) {
+  const float *zr = a.z + (int64_t)row * a.z_stride;
+  if (nsplit <= 1 || j >= a.n_q) return zr[j];
+  const int64_t plane = (int64_t)a.B * a.Hq * a.z_stride;
+  const float *p = a.zpart + (int64_t)row * a.z_stride + j;
+  float acc = p[0];
+  for (int sp = 1; sp < nsplit; ++sp) acc += p[sp * plane];
+  return acc;
+}
+
+// z <- sum of split partials; stats[row] = {max z, -min z} (atomic max)
+__global__ void __launch_bounds__(kShT) k_sh_stats(LayerArgs a, int nsplit, int32_t *stats) {
+  const int row = blockIdx.y;
+  int mx = INT_MIN, mn = INT_MAX;
+  for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
+    const float zf = sh_z(a, row, j, nsplit);
+    if (nsplit > 1 && j < a.n_q) a.z[(int64_t)row * a.z_stride + j] = zf;
+    const int zi = __float2int_rn(zf);
+    mx = max(mx, zi);
+    mn = min(mn, zi);
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  if ((threadIdx.x & 31) == 0 && mx != INT_MIN) {
+    atomicMax(&stats[2 * row], mx);
+    atomicMax(&stats[2 * row + 1], -mn);
+  }
+}
+
+__global__ void k_sh_init_stats(int32_t *stats, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) { stats[2 * r] = INT_MIN; stats[2 * r + 1] = INT_MIN; }
+}
+
+__device__ __forceinline__ int sh_shift(int M, int zmin) {
+  const uint32_t dmax = (uint32_t)(M - zmin);
+  const int bits = 32 - __clz(dmax);
+  return bits > kNBBits ? bits - kNBBits : 0;
+}
+
+// coarse histogram (count, mass) of the local tokens with the GLOBAL M, zmin -> h1 (u64 atomics)
+__global__ void __launch_bounds__(kShT) k_sh_hist1(LayerArgs a, const int32_t *gstats,
+                                                   unsigned long long *h1) {
+  __shared__ uint32_t cnt[kNB], mlo[kNB], mhi[kNB];
+  const int row = blockIdx.y;
+  const int M = gstats[2 * row], zmin = -gstats[2 * row + 1];
+  const int shift = sh_shift(M, zmin);
+  const float kappa = a.hs[row].kappa;
+  for (int i = threadIdx.x; i < kNB; i += kShT) { cnt[i] = 0; mlo[i] = 0; mhi[i] = 0; }
+  __syncthreads();
+  for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
+    const uint32_t dl = (uint32_t)(M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    const uint32_t bk = dl >> shift;
+    atomicAdd(&cnt[bk], 1u);
+    const uint64_t W = mass(dl, kappa);
+    if (W) {
+      const uint32_t wl = (uint32_t)W;
+      uint32_t wh = (uint32_t)(W >> 32);
+      const uint32_t old = atomicAdd(&mlo[bk], wl);
+      wh += (old + wl < old) ? 1u : 0u;
+      if (wh) atomicAdd(&mhi[bk], wh);
+    }
+  }
+  __syncthreads();
+  unsigned long long *hr = h1 + (int64_t)row * kNB * 2;
+  for (int i = threadIdx.x; i < kNB; i += kShT) {
+    if (cnt[i]) {
+      atomicAdd(&hr[2 * i], (unsigned long long)cnt[i]);
+      atomicAdd(&hr[2 * i + 1], ((unsigned long long)mhi[i] << 32) + mlo[i]);
+    }
+  }
+}
+
+// block exclusive scan of pairs (kShT threads)
+__device__ __forceinline__ void sh_scan2(unsigned long long &x, unsigned long long &y,
+                                         unsigned long long &tx, unsigned long long &ty) {
+  __shared__ unsigned long long sx[kShT / 32], sy[kShT / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long ix = x, iy = y;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long ox = __shfl_up_sync(0xffffffffu, ix, off);
+    const unsigned long long oy = __shfl_up_sync(0xffffffffu, iy, off);
+    if (lane >= off) { ix += ox; iy += oy; }
+  }
+  __syncthreads();
+  if (lane == 31) { sx[w] = ix; sy[w] = iy; }
+  __syncthreads();
+  unsigned long long bx = 0, by = 0;
+  tx = 0; ty = 0;
+  for (int k = 0; k < kShT / 32; ++k) {
+    if (k < w) { bx += sx[k]; by += sy[k]; }
+    tx += sx[k]; ty += sy[k];
+  }
+  x = bx + ix - x;
+  y = by + iy - y;
+}
+
+// bound1 on the GLOBAL coarse histogram (identical on every rank) -> hs
+__global__ void __launch_bounds__(kShT) k_sh_bound1(SelArgs s, const int32_t *gstats,
+                                                    const unsigned long long *h1) {
+  const int row = blockIdx.x;
+  HeadState *hs = s.hs + row;
+  constexpr int kB = kNB / kShT;
+  const unsigned long long *hr = h1 + (int64_t)row * kNB * 2;
+  unsigned long long c[kB], m[kB], lc = 0, lm = 0;
+#pragma unroll
+  for (int k = 0; k < kB; ++k) {
+    const int bi = threadIdx.x * kB + k;
+    c[k] = hr[2 * bi];
+    m[k] = hr[2 * bi + 1];
+    lc += c[k];
+    lm += m[k];
+  }
+  unsigned long long pc = lc, pm = lm, tc, tm;
+  sh_scan2(pc, pm, tc, tm);
+  const unsigned long long S = tm, ntot = tc;
+  const bool tau_all = s.tau_q >= (1u << 24);
+  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, S);
+  const bool cap_all = (unsigned long long)s.k_max >= ntot;
+  __shared__ int sb;
+  if (threadIdx.x == 0) sb = kNB;
+  __syncthreads();
+  int found = kNB;
+  unsigned long long fcb = 0, fmb = 0, cc = pc, cm = pm;
+#pragma unroll
+  for (int k = 0; k < kB; ++k) {
+    const bool trig = c[k] && ((!tau_all && cm + m[k] >= theta) ||
+                               (!cap_all && cc + c[k] >= (unsigned long long)s.k_max));
+    if (trig && found == kNB) { found = threadIdx.x * kB + k; fcb = cc; fmb = cm; }
+    cc += c[k];
+    cm += m[k];
+  }
+  if (found < kNB) atomicMin(&sb, found);
+  __syncthreads();
+  const int M = gstats[2 * row], zmin = -gstats[2 * row + 1];
+  if (threadIdx.x == 0) {
+    hs->M = M;
+    hs->zmin = zmin;
+    hs->shift = sh_shift(M, zmin);
+    hs->S = S;
+    hs->theta = theta;
+    hs->bstar = sb;
+    hs->ksel = (int64_t)ntot;
+    hs->kstar = (int64_t)ntot;
+    hs->delta_star = 0xffffffffu;
+    hs->r_ties = 0;
+    hs->sel_mass = S;
+  }
+  if (found < kNB && found == sb) { hs->cnt_before = (uint32_t)fcb; hs->mass_before = fmb; }
+}
+
+// fine histogram of local tokens inside the global b*
+__global__ void __launch_bounds__(kShT) k_sh_hist2(LayerArgs a, unsigned long long *h2) {
+  __shared__ uint32_t cnt[kNB];
+  const int row = blockIdx.y;
+  const HeadState h = a.hs[row];
+  if (h.bstar >= kNB) return;
+  for (int i = threadIdx.x; i < kNB; i += kShT) cnt[i] = 0;
+  __syncthreads();
+  const uint32_t fmask = (1u << h.shift) - 1u;
+  for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
+    const uint32_t dl = (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    if ((int)(dl >> h.shift) == h.bstar) atomicAdd(&cnt[dl & fmask], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kNB; i += kShT)
+    if (cnt[i]) atomicAdd(&h2[(int64_t)row * kNB + i], (unsigned long long)cnt[i]);
+}
+
+// bound2 on the GLOBAL fine histogram -> Δ*, r, k_sel (identical on every rank)
+__global__ void __launch_bounds__(kShT) k_sh_bound2(SelArgs s, const unsigned long long *h2) {
+  const int row = blockIdx.x;
+  HeadState *hs = s.hs + row;
+  const HeadState h = *hs;
+  if (h.bstar >= kNB) return;
+  constexpr int kB = kNB / kShT;
+  const uint32_t dbase = (uint32_t)h.bstar << h.shift;
+  const unsigned long long *hr = h2 + (int64_t)row * kNB;
+  unsigned long long c[kB], w[kB], lc = 0, lm = 0;
+#pragma unroll
+  for (int k = 0; k < kB; ++k) {
+    const int bi = threadIdx.x * kB + k;
+    c[k] = hr[bi];
+    w[k] = c[k] ? mass(dbase | (uint32_t)bi, h.kappa) : 0ull;
+    lc += c[k];
+    lm += c[k] * w[k];
+  }
+  unsigned long long pc = lc, pm = lm, tc, tm;
+  sh_scan2(pc, pm, tc, tm);
+  const bool tau_all = s.tau_q >= (1u << 24);
+  __shared__ int sv;
+  if (threadIdx.x == 0) sv = kNB;
+  __syncthreads();
+  unsigned long long cc = h.cnt_before + pc, cm = h.mass_before + pm;
+  int found = kNB;
+  unsigned long long f_cc = 0, f_cm = 0, f_w = 0, f_c = 0;
+#pragma unroll
+  for (int k = 0; k < kB; ++k) {
+    if (c[k] && found == kNB) {
+      const bool tt = !tau_all && w[k] && (cm + c[k] * w[k] >= h.theta);
+      const bool tk = cc + c[k] >= (unsigned long long)s.k_max;
+      if (tt || tk) { found = threadIdx.x * kB + k; f_cc = cc; f_cm = cm; f_w = w[k]; f_c = c[k]; }
+    }
+    cc += c[k];
+    cm += c[k] * w[k];
+  }
+  if (found < kNB) atomicMin(&sv, found);
+  __syncthreads();
+  if (found < kNB && found == sv) {
+    unsigned long long r_tau = ~0ull, r_cap = ~0ull;
+    if (!tau_all && f_w && f_cm + f_c * f_w >= h.theta) r_tau = (h.theta - f_cm + f_w - 1) / f_w;
+    if (f_cc + f_c >= (unsigned long long)s.k_max) r_cap = (unsigned long long)s.k_max - f_cc;
+    if (r_tau == 0) r_tau = 1;
+    const unsigned long long r = r_tau < r_cap ? r_tau : r_cap;
+    hs->delta_star = dbase | (uint32_t)found;
+    hs->r_ties = (uint32_t)r;
+    hs->ksel = (int64_t)(f_cc + r);
+    hs->kstar = (r_tau <= r_cap) ? (int64_t)(f_cc + r_tau) : -1;
+    hs->sel_mass = f_cm + r * f_w;
+  }
+}
+
+// per-chunk local (strict, tie) counts -> chunk [rows][nch][2]; row totals -> cnt [rows][2]
+__global__ void __launch_bounds__(kShT) k_sh_counts(LayerArgs a, int nch, uint32_t *chunk,
+                                                    unsigned long long *cnt) {
+  const int row = blockIdx.y, ch = blockIdx.x;
+  const HeadState h = a.hs[row];
+  const int64_t j0 = (int64_t)ch * kShChunk;
+  unsigned ns = 0, nt = 0;
+  for (int64_t j = j0 + threadIdx.x; j < j0 + kShChunk && j < a.n_cand; j += kShT) {
+    const uint32_t dl = (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    ns += dl < h.delta_star;
+    nt += dl == h.delta_star;
+  }
+  ns = __reduce_add_sync(0xffffffffu, ns);
+  nt = __reduce_add_sync(0xffffffffu, nt);
+  __shared__ unsigned s0[kShT / 32], s1[kShT / 32];
+  if ((threadIdx.x & 31) == 0) { s0[threadIdx.x >> 5] = ns; s1[threadIdx.x >> 5] = nt; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned a0 = 0, a1 = 0;
+    for (int w = 0; w < kShT / 32; ++w) { a0 += s0[w]; a1 += s1[w]; }
+    chunk[((int64_t)row * nch + ch) * 2] = a0;
+    chunk[((int64_t)row * nch + ch) * 2 + 1] = a1;
+    atomicAdd(&cnt[2 * row], (unsigned long long)a0);
+    atomicAdd(&cnt[2 * row + 1], (unsigned long long)a1);
+  }
+}
+
+// ordered compaction with the offsets of lower ranks + local Eq. 5 partial numerators.
+// allcnt [R][rows][2] (all-gathered row totals).  Writes the rank's kept tokens (GLOBAL
+// indices base + j) at their GLOBAL positions of sel_idx / sel_w, and part [rows][nch][d].
+__global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int nch,
+                                                   const uint32_t *chunk,
+                                                   const unsigned long long *allcnt, int rank,
+                                                   int64_t base, float *part) {
+  const int row = blockIdx.y, ch = blockIdx.x;
+  const HeadState h = a.hs[row];
+  __shared__ unsigned long long sp[2];
+  if (threadIdx.x == 0) {
+    unsigned long long ps = 0, pt = 0;
+    for (int r = 0; r < rank; ++r) {
+      ps += allcnt[((int64_t)r * s.rows + row) * 2];
+      pt += allcnt[((int64_t)r * s.rows + row) * 2 + 1];
+    }
+    for (int k = 0; k < ch; ++k) {
+      ps += chunk[((int64_t)row * nch + k) * 2];
+      pt += chunk[((int64_t)row * nch + k) * 2 + 1];
+    }
+    sp[0] = ps;
+    sp[1] = pt;
+  }
+  __syncthreads();
+  const unsigned long long s_before = sp[0], t_before = sp[1], r = h.r_ties;
+  const int64_t j0 = (int64_t)ch * kShChunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // warp w owns tokens [j0 + w*512, +512) of the chunk; ballots keep index order
+  const int64_t w0 = j0 + (int64_t)warp * (kShChunk / (kShT / 32));
+  const int64_t w1 = w0 + kShChunk / (kShT / 32);
+  __shared__ unsigned long long ws_[kShT / 32], wt_[kShT / 32];
+  unsigned ns = 0, nt = 0;
+  for (int64_t j = w0 + lane; j < w1 && j < a.n_cand; j += 32) {
+    const uint32_t dl = (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    ns += dl < h.delta_star;
+    nt += dl == h.delta_star;
+  }
+  ns = __reduce_add_sync(0xffffffffu, ns);
+  nt = __reduce_add_sync(0xffffffffu, nt);
+  if (lane == 0) { ws_[warp] = ns; wt_[warp] = nt; }
+  __syncthreads();
+  unsigned long long s_w = s_before, t_w = t_before;
+  for (int k = 0; k < warp; ++k) { s_w += ws_[k]; t_w += wt_[k]; }
+  const double denom = s.renorm ? (double)h.sel_mass : (double)h.S;
+  int32_t *oi = s.sel_idx + (int64_t)row * s.k_max;
+  float *ow = s.sel_w + (int64_t)row * s.k_max;
+  unsigned long long pos = s_w + (t_w < r ? t_w : r), t_run = t_w;
+  const unsigned lt = (1u << lane) - 1u;
+  // gather: each lane handles 4 dims of d = 128 (dpl = d / 32)
+  const int dpl = a.d >> 5;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+  const int b = row / a.Hq, hq = row - b * a.Hq, kv = hq / a.G;
+  const uint16_t *Vb = a.V + (int64_t)b * a.v_b_stride + (int64_t)kv * a.v_kv_stride;
+  for (int64_t jb = w0; jb < w1 && jb < a.n_cand; jb += 32) {
+    const int64_t j = jb + lane;
+    const bool v = j < w1 && j < a.n_cand;
+    const uint32_t dl = v ? (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j])) : 0xffffffffu;
+    const bool st = v && dl < h.delta_star;
+    const bool ti = v && dl == h.delta_star;
+    const unsigned bt = __ballot_sync(0xffffffffu, ti);
+    const bool take = st || (ti && t_run + __popc(bt & lt) < r);
+    const unsigned bs = __ballot_sync(0xffffffffu, take);
+    float wv = 0.0f;
+    if (take) {
+      const unsigned long long p = pos + __popc(bs & lt);
+      wv = (float)((double)mass(dl, h.kappa) / denom);
+      if ((int64_t)p < s.k_max) {
+        oi[p] = (int32_t)(base + j);
+        ow[p] = wv;
+      }
+    }
+    // Eq. 5 partial: the warp walks its kept rows (lane-order), all lanes read each row
+    unsigned m = bs;
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const float w_ = __shfl_sync(0xffffffffu, wv, src);
+      const int64_t jj = jb + src;
+      const uint16_t *row_p = Vb + jj * a.d + lane * dpl;
+      for (int e = 0; e < dpl; ++e) acc[e] = fmaf(w_, __half2float(__ushort_as_half(row_p[e])), acc[e]);
+    }
+    pos += __popc(bs);
+    t_run += __popc(bt);
+  }
+  __shared__ float red[kShT / 32][256];
+  for (int e = 0; e < dpl; ++e) red[warp][lane * dpl + e] = acc[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.d; e += kShT) {
+    float sum = 0.0f;
+    for (int w = 0; w < kShT / 32; ++w) sum += red[w][e];
+    part[((int64_t)row * nch + ch) * a.d + e] = sum;
+  }
+}
+
+// deterministic sum of the chunk partials -> out [rows][d] (this rank's numerator share)
+__global__ void k_sh_reduce(int rows, int nch, int d, const float *part, float *out) {
+  const int row = blockIdx.x;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float sum = 0.0f;
+    for (int c = 0; c < nch; ++c) sum += part[((int64_t)row * nch + c) * d + e];
+    out[(int64_t)row * d + e] = sum;
+  }
+}
+
+static int sh_grid(int64_t n) {
+  int64_t g = (n + kShT * 16 - 1) / (kShT * 16);
+  return (int)(g < 1 ? 1 : (g > 64 ? 64 : g));
+}
+
+cudaError_t launch_shard_stats(const LayerArgs &a, int nsplit, int32_t *stats, cudaStream_t st) {
+  const int rows = a.B * a.Hq;
+  k_sh_init_stats<<<(rows + 127) / 128, 128, 0, st>>>(stats, rows);
+  note_launch();
+  k_sh_stats<<<dim3(sh_grid(a.n_cand), rows), kShT, 0, st>>>(a, nsplit, stats);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_hist1(const LayerArgs &a, const int32_t *gstats, unsigned long long *h1,
+                               cudaStream_t st) {
+  const int rows = a.B * a.Hq;
+  cudaMemsetAsync(h1, 0, (size_t)rows * kNB * 16, st);
+  k_sh_hist1<<<dim3(sh_grid(a.n_cand), rows), kShT, 0, st>>>(a, gstats, h1);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_hist2(const LayerArgs &a, const SelArgs &s, const int32_t *gstats,
+                               const unsigned long long *h1, unsigned long long *h2, cudaStream_t st) {
+  const int rows = a.B * a.Hq;
+  k_sh_bound1<<<rows, kShT, 0, st>>>(s, gstats, h1);
+  note_launch();
+  cudaMemsetAsync(h2, 0, (size_t)rows * kNB * 8, st);
+  k_sh_hist2<<<dim3(sh_grid(a.n_cand), rows), kShT, 0, st>>>(a, h2);
+  note_launch();
+  return cudaGetLastError();
+}
+
+int shard_chunks(int64_t n) { return (int)((n + kShChunk - 1) / kShChunk); }
+
+cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsigned long long *h2,
+                                uint32_t *chunk, unsigned long long *cnt, cudaStream_t st) {
+  const int rows = a.B * a.Hq;
+  k_sh_bound2<<<rows, kShT, 0, st>>>(s, h2);
+  note_launch();
+  cudaMemsetAsync(cnt, 0, (size_t)rows * 16, st);
+  const int nch = shard_chunks(a.n_cand);
+  if (nch > 0) {
+    k_sh_counts<<<dim3(nch, rows), kShT, 0, st>>>(a, nch, chunk, cnt);
+    note_launch();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
+                                const unsigned long long *allcnt, int rank, int64_t base,
+                                float *part, float *out, cudaStream_t st) {
+  const int rows = a.B * a.Hq;
+  const int nch = shard_chunks(a.n_cand);
+  if (nch > 0) {
+    k_sh_write<<<dim3(nch, rows), kShT, 0, st>>>(a, s, nch, chunk, allcnt, rank, base, part);
+    note_launch();
+    k_sh_reduce<<<rows, 128, 0, st>>>(rows, nch, a.d, part, out);
+    note_launch();
+  } else {
+    cudaMemsetAsync(out, 0, (size_t)rows * a.d * 4, st);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hc

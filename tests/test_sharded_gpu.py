@@ -1,0 +1,64 @@
+"""Sequence-sharded decode kernels on ONE GPU: R shards of the context are
+driven in lock-step in one process (collectives = tensor reductions, no ranks waiting on
+each other).  The kept index set must equal the UNSHARDED oracle's bit for bit
+(R-invariance) and the summed output must be within tolerance."""
+import numpy as np
+import pytest
+
+from harness import TOL_ABS, TOL_REL, Case, oracle_unit
+
+pytestmark = pytest.mark.gpu
+
+
+def _shard_caches(case: Case, R: int, device="cuda"):
+    import torch
+    import paper_2507_19823_b200 as hc
+    import synth.device as sd
+    L = case.L
+    full = hc.KCache(case.B, L, case.Hkv, case.G, case.d, case.g, case.c, case.n_cap,
+                     torch.from_numpy(np.stack([case.codebook(l) for l in range(L)])).to(device),
+                     cbg=case.cbg, device=device)
+    vfull = hc.VStore.allocate(case.B, L, case.Hkv, case.n_cap, case.d, device=device)
+    sd.fill_codes(full.codes, case.seed, case.c, case.n)
+    sd.fill_values(vfull.tensor, case.seed, case.n, device=device)
+    bounds = np.linspace(0, case.n, R + 1).astype(int)
+    shards = []
+    for r in range(R):
+        a, b = int(bounds[r]), int(bounds[r + 1])
+        cap = max(64, (b - a + 63) // 64 * 64)
+        kc = hc.KCache(case.B, L, case.Hkv, case.G, case.d, case.g, case.c, cap, full.codebook,
+                       cbg=case.cbg, device=device)
+        kc.codes[..., : b - a] = full.codes[..., a:b]
+        vs = hc.VStore.allocate(case.B, L, case.Hkv, cap, case.d, device=device)
+        vs.tensor[:, :, :, : b - a] = vfull.tensor[:, :, :, a:b]
+        for l in range(L):
+            kc.set_counts(l, b - a)
+        shards.append((kc, vs, a))
+    return shards
+
+
+@pytest.mark.parametrize("R,n,tau,k_max", [(2, 9000, 0.9, 1500), (3, 7001, 0.7, 50000),
+                                           (4, 12000, 1.0, 3000), (2, 5000, 0.95, 1)])
+def test_virtual_shards_match_unsharded_oracle(R, n, tau, k_max):
+    import torch
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.sharded import GpuShard, decode_layer_virtual
+    case = Case(B=2, Hkv=2, n=n, tau=tau, k_max=k_max, seed=40 + R)
+    parts = _shard_caches(case, R)
+    bud = hc.budget(tau, k_max)
+    shards = [GpuShard(kc, vs, bud) for kc, vs, _ in parts]
+    q = torch.from_numpy(np.stack([case.query(b, 0) for b in range(case.B)])).cuda()
+    out = decode_layer_virtual(shards, q, 0, [a for _, _, a in parts]).cpu().numpy()
+    torch.cuda.synchronize()
+    sel = torch.stack([s.sel_idx for s in shards]).amax(0).cpu().numpy()
+    ksel = shards[0].sel_k.cpu().numpy()
+    for b in range(case.B):
+        for kv in range(case.Hkv):
+            ref = oracle_unit(case, b, 0, kv)
+            for h in range(case.G):
+                row = b * case.Hq + kv * case.G + h
+                k = int(ksel[row])
+                assert k == ref["k_sel"][h]
+                assert np.array_equal(sel[row, :k], ref["idx"][h])
+                err = np.abs(out[row] - ref["out"][h])
+                assert np.all(err <= TOL_ABS + TOL_REL * np.abs(ref["out"][h]))
