@@ -44,6 +44,11 @@ CONFIGS = {
             placement=1,
             workload="config3: Llama-3-8B-shaped, 128K ctx, 12.5% KV budget (g=32, c=8192), "
                      "k_max=16384, tau=0.9, batch 4, V in host pinned memory (zero-copy), 1xB200"),
+    4: dict(B=1, L=32, Hkv=8, G=4, d=128, g=32, c=8192, n=1048576, k_max=131072, tau=0.9,
+            placement=0,
+            workload="config4: Llama-3-8B-shaped, 1M ctx sequence-sharded across the GPUs "
+                     "(contiguous token ranges, NCCL merges), 12.5% KV budget (g=32, c=8192), "
+                     "k_max=131072, tau=0.9, batch 1, V in HBM"),
 }
 Q_SCALE = 2.29  # calibrates tau=0.9 to Table 3's 15.6 % selection ratio
 SEED = 0x48434154
@@ -124,7 +129,11 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workload
 class Workload:
-    def __init__(self, cfg: dict, device: str):
+    """The synthetic decode state of one rank.  With world > 1 (or virtual shards) rank r
+    holds the contiguous global token range [a_r, b_r) of every (b, layer, kv) unit; the
+    newest token (global position n-1) lives on the last rank, which does the append."""
+
+    def __init__(self, cfg: dict, device: str, rank: int = 0, world: int = 1):
         import numpy as np
         import torch
 
@@ -134,15 +143,17 @@ class Workload:
         self.cfg = cfg
         B, L, H, G, d, g, c, n = (cfg[k] for k in ("B", "L", "Hkv", "G", "d", "g", "c", "n"))
         self.Hq = G * H
-        n_cap = (n + 63) // 64 * 64
+        bounds = [int(x) for x in np.linspace(0, n, world + 1)]
+        self.base, self.n_local = bounds[rank], bounds[rank + 1] - bounds[rank]
+        self.is_last = rank == world - 1
+        n_cap = max(64, (self.n_local + 63) // 64 * 64)
         cb = np.stack([synth.gen_codebook(SEED, l, g, c, d // g) for l in range(L)])
         self.codebook = torch.from_numpy(cb).to(device)
         self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device)
         self.vs = hc.VStore.allocate(B, L, H, n_cap, d, placement=cfg["placement"], device=device)
-        sd.fill_codes(self.kc.codes, SEED, c, n)
-        sd.fill_values(self.vs.tensor, SEED, n, device=device)
-        for l in range(L):
-            self.kc.set_counts(l, n - 1)
+        sd.fill_codes(self.kc.codes, SEED, c, self.n_local, start=self.base)
+        sd.fill_values(self.vs.tensor, SEED, self.n_local, device=device, start=self.base)
+        self.reset_counts()
         # per-step inputs: q for every layer, the new token's k and v
         q = np.stack([np.stack([synth.gen_query(SEED + 1, b, l, self.Hq, d, Q_SCALE)
                                 for b in range(B)]) for l in range(L)])
@@ -165,19 +176,34 @@ class Workload:
             b_.record()
             e_.record()
         torch.cuda.synchronize()
+        self.shard = None
+        self.comm = None
+
+    def enable_sharding(self, comm):
+        from paper_2507_19823_b200.sharded import GpuShard
+        self.shard = GpuShard(self.kc, self.vs, self.bud)
+        self.comm = comm
 
     def reset_counts(self):
+        n_here = self.n_local - (1 if self.is_last else 0)  # the step appends position n-1
         for l in range(self.cfg["L"]):
-            self.kc.set_counts(l, self.cfg["n"] - 1)
+            self.kc.set_counts(l, n_here)
 
     def step(self, profile=False):
         import paper_2507_19823_b200 as hc
+        from paper_2507_19823_b200 import sharded
         for l in range(self.cfg["L"]):
-            self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
+            if self.is_last:
+                self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
             if profile:
                 hc.profile_scan_events(*self.ev[l])
-            hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
-                                sel_k=self.sel_k[l], ws=self.ws)
+            if self.shard is None:
+                hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
+                                    sel_k=self.sel_k[l], ws=self.ws)
+            else:
+                o = sharded.decode_layer(self.shard, self.comm, self.q[l], l, self.base)
+                self.out[l].copy_(o.view_as(self.out[l]))
+                self.sel_k[l].copy_(self.shard.sel_k.view_as(self.sel_k[l]))
 
     def step_e2e(self):
         self.q.copy_(self.q_host, non_blocking=True)
@@ -237,6 +263,27 @@ def time_graph(g, K, W, dist=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return ms
+
+
+def hc_lib_check():
+    import paper_2507_19823_b200 as hc
+    hc.lib()  # no CPU fallback: fail loudly if the CUDA library is missing
+
+
+def measure_h2d_gbs() -> float:
+    import torch
+    src = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        dst.copy_(src, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    return 5 * (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9
 
 
 # ----------------------------------------------------------------------------- CPU oracle
@@ -305,18 +352,72 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_virtual(args, cfg, R):
+    """Test mode: the sequence-sharded step of `cfg` as R shards on one GPU, collectives as
+    tensor reductions (paper_2507_19823_b200.sharded.decode_layer_virtual)."""
+    import torch
+
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.sharded import GpuShard, decode_layer_virtual
+    wls = [Workload(cfg, "cuda", r, R) for r in range(R)]
+    shards = [GpuShard(w.kc, w.vs, w.bud) for w in wls]
+    bases = [w.base for w in wls]
+    L = cfg["L"]
+
+    def step():
+        for l in range(L):
+            wls[-1].kc.append(l, wls[-1].k_new[l], wls[-1].v_new[l], wls[-1].vs)
+            o = decode_layer_virtual(shards, wls[0].q[l], l, bases)
+            wls[0].out[l].copy_(o.view_as(wls[0].out[l]))
+
+    for w in wls:
+        w.reset_counts()
+    step()
+    torch.cuda.synchronize()
+    for w in wls:
+        w.reset_counts()
+    g = torch.cuda.CUDAGraph()
+    s_ = torch.cuda.Stream()
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
+        with torch.cuda.graph(g, stream=s_):
+            step()
+    torch.cuda.current_stream().wait_stream(s_)
+    ms = time_graph(g, args.steps, max(args.warmup, 3)) / args.steps
+    ksel = shards[0].sel_k.float().mean().item()
+    print(json.dumps({"metric": METRIC, "value": 1000.0 / ms, "unit": "steps/s", "n_gpus": 1,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                      "config": {"workload": cfg["workload"],
+                                 "parallelism": f"virtual-shards x{R} on one GPU (test mode)"},
+                      "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / cfg["n"]}}), flush=True)
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--steps", type=int, default=None, help="default 500 (config 1/2), 20 (3/4)")
+    ap.add_argument("--warmup", type=int, default=None, help="default 10 (config 1/2), 3 (3/4)")
+    ap.add_argument("--virtual-shards", type=int, default=0,
+                    help="test mode: run config 4's sharded step as R shards on ONE GPU")
+    ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
+                    help="default: 3 at N=1 (128K ctx, the metric's single-GPU config), "
+                         "4 at N>1 (1M ctx sequence-sharded)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        args.config = 3 if world_env == 1 else 4
     cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = 500 if args.config in (1, 2) else 20
+    if args.warmup is None:
+        args.warmup = 10 if args.config in (1, 2) else 3
+    if args.virtual_shards:
+        run_virtual(args, cfg, args.virtual_shards)
+        return
     if args.impl == "reference":
         run_reference(args, cfg)
         return
@@ -333,8 +434,13 @@ def main():
     torch.cuda.set_device(local)
     dev = "cuda"
     args.warmup = max(args.warmup, 3)
+    hc_lib_check()
 
-    wl = Workload(cfg, dev)
+    sharded_mode = world > 1 and args.config == 4
+    wl = Workload(cfg, dev, rank if sharded_mode else 0, world if sharded_mode else 1)
+    if sharded_mode:
+        from paper_2507_19823_b200.sharded import TorchComm
+        wl.enable_sharding(TorchComm())
     torch.cuda.synchronize()
     # eager correctness sanity (one step) then capture the step with scan events
     wl.reset_counts()
@@ -352,7 +458,8 @@ def main():
     ms_e2e = time_graph(g_e2e, K2, args.warmup, dist) / K2
 
     B, L, H, g, n, d = (cfg[k] for k in ("B", "L", "Hkv", "g", "n", "d"))
-    p_bytes_layer = B * H * n * g * 2
+    n_here = wl.n_local
+    p_bytes_layer = B * H * n_here * g * 2
     achieved = p_bytes_layer / (scan_avg_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     traffic = None
@@ -361,15 +468,27 @@ def main():
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     ksel = wl.sel_k.float().mean().item()
-    value = world * 1000.0 / ms_per_step
+    jobs = 1 if sharded_mode else world  # replicas multiply the work, shards split it
+    value = jobs * 1000.0 / ms_per_step
+    # value-gather bytes (all layers, all heads, this rank's share) and the host-link peak
+    v_bytes = ksel * B * wl.Hq * L * d * 2 / (world if sharded_mode else 1)
+    host_link = None
+    if cfg["placement"] == 1:
+        pk = measure_h2d_gbs()
+        host_link = {"bytes_per_step": v_bytes, "achieved_gbs_lower_bound": v_bytes / (ms_per_step * 1e-3) / 1e9,
+                     "peak_gbs": pk, "peak_source": "measured pinned H2D cudaMemcpy 1 GiB",
+                     "frac": v_bytes / (ms_per_step * 1e-3) / 1e9 / pk,
+                     "note": "zero-copy reads of only the selected value rows; whole step time in the denominator"}
     h2d = (wl.q.numel() + wl.k_new.numel() + wl.v_new.numel()) * 2
     d2h = wl.out.numel() * 4
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if sharded_mode else "weak", "vs_baseline": None,
         "dtype": "i16+f32", "data": "synthetic (seeded splitmix64; codes uniform, C,q,V ~ Irwin-Hall normal)",
-        "config": {"workload": cfg["workload"], "parallelism": "replicas" if world > 1 else "single",
+        "config": {"workload": cfg["workload"],
+                   "parallelism": (f"sequence-sharded x{world}" if sharded_mode else
+                                   ("replicas" if world > 1 else "single")),
                    "l2": f"inputs > L2: P = {B * L * H * n * g * 2 / 1e9:.2f} GB/step, V = "
                          f"{B * L * H * n * d * 2 / 1e9:.2f} GB",
                    "graph": "one CUDA graph per step (32 x append + decode)"},
@@ -382,7 +501,8 @@ def main():
                      "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L / ms_per_step,
                      "peak_source": peak_src},
         "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / n},
-        "e2e": {"value": world * 1000.0 / ms_e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+        "host_link": host_link,
+        "e2e": {"value": jobs * 1000.0 / ms_e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,

@@ -31,9 +31,9 @@ def lib():
             build()
         L = C.CDLL(LIB)
         L.synth_codes.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
-                                  C.c_uint32, C.c_void_p]
+                                  C.c_uint32, C.c_int64, C.c_void_p]
         L.synth_values.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
-                                   C.c_int, C.c_void_p]
+                                   C.c_int, C.c_int64, C.c_void_p]
         _lib = L
     return _lib
 
@@ -45,9 +45,9 @@ def _keys(seed, tag, shape_prefix, extra):
     return np.array(ks, dtype=np.uint64)
 
 
-def fill_codes(codes, seed: int, c: int, n: int, layers=None):
-    """codes: torch int16 cuda [B][L][Hkv][g][n_cap]; fill positions [0, n) of the given
-    layers (default all) with synth.gen_codes streams."""
+def fill_codes(codes, seed: int, c: int, n: int, layers=None, start: int = 0):
+    """codes: torch int16 cuda [B][L][Hkv][g][n_cap]; fill local positions [0, n) of the given
+    layers (default all) with synth.gen_codes streams of GLOBAL positions [start, start+n)."""
     import torch
     B, L, H, g, ncap = codes.shape
     layers = range(L) if layers is None else layers
@@ -60,14 +60,15 @@ def fill_codes(codes, seed: int, c: int, n: int, layers=None):
             sub = codes[b, l]  # [H][g][ncap] contiguous
             r = lib().synth_codes(C.c_void_p(sub.data_ptr()),
                                   C.c_void_p(kt.data_ptr() + b * H * g * 8), H * g, ncap, n, c,
-                                  C.c_void_p(s))
+                                  start, C.c_void_p(s))
             if r:
                 raise RuntimeError(f"synth_codes failed: {r}")
         torch.cuda.current_stream().synchronize()
 
 
-def fill_values(vt, seed: int, n: int, layers=None, device="cuda"):
-    """vt: torch fp16 [B][L][Hkv][n_cap][d] (cuda or pinned host, UVA pointer); rows [0, n)."""
+def fill_values(vt, seed: int, n: int, layers=None, device="cuda", start: int = 0):
+    """vt: torch fp16 [B][L][Hkv][n_cap][d] (cuda or pinned host, UVA pointer); local rows
+    [0, n) <- GLOBAL rows [start, start+n)."""
     import torch
     B, L, H, ncap, d = vt.shape
     layers = range(L) if layers is None else layers
@@ -79,7 +80,7 @@ def fill_values(vt, seed: int, n: int, layers=None, device="cuda"):
         for b in range(B):
             sub = vt[b, l]
             r = lib().synth_values(C.c_void_p(sub.data_ptr()), C.c_void_p(kt.data_ptr() + b * H * 8),
-                                   H, ncap * d, n, d, C.c_void_p(s))
+                                   H, ncap * d, n, d, start, C.c_void_p(s))
             if r:
                 raise RuntimeError(f"synth_values failed: {r}")
         torch.cuda.current_stream().synchronize()

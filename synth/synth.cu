@@ -14,13 +14,13 @@ __device__ __forceinline__ uint64_t fin(uint64_t z) {
 
 // out[s * strip_stride + j] = code(keys[s], j, c) for j < n, s < nstrips
 __global__ void k_codes(uint16_t *out, const uint64_t *keys, int64_t nstrips, int64_t strip_stride,
-                        int64_t n, uint32_t c) {
+                        int64_t n, uint32_t c, int64_t start) {
   const int64_t s = blockIdx.y + (int64_t)blockIdx.z * 65535;
   if (s >= nstrips) return;
   const uint64_t key = keys[s];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t u = fin(key + (uint64_t)(j + 1) * GOLDEN);
+    const uint64_t u = fin(key + (uint64_t)(j + start + 1) * GOLDEN);
     out[s * strip_stride + j] = (uint16_t)(((u >> 32) * (uint64_t)c) >> 32);
   }
 }
@@ -34,7 +34,7 @@ __device__ __forceinline__ uint16_t v16(uint64_t u) {
 
 // out[s * strip_stride + j*d + e] = v16(u64(keys[s], j*d + e)), rows [0, n)
 __global__ void k_values(uint16_t *out, const uint64_t *keys, int64_t nstrips, int64_t strip_stride,
-                         int64_t n, int d) {
+                         int64_t n, int d, int64_t start) {
   const int64_t s = blockIdx.y + (int64_t)blockIdx.z * 65535;
   if (s >= nstrips) return;
   const uint64_t key = keys[s];
@@ -43,7 +43,7 @@ __global__ void k_values(uint16_t *out, const uint64_t *keys, int64_t nstrips, i
        t += (int64_t)gridDim.x * blockDim.x * 8) {
     uint16_t h[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) h[q] = v16(fin(key + (uint64_t)(t + q + 1) * GOLDEN));
+    for (int q = 0; q < 8; ++q) h[q] = v16(fin(key + (uint64_t)(t + start * d + q + 1) * GOLDEN));
     uint4 v;
     v.x = h[0] | ((uint32_t)h[1] << 16);
     v.y = h[2] | ((uint32_t)h[3] << 16);
@@ -54,20 +54,20 @@ __global__ void k_values(uint16_t *out, const uint64_t *keys, int64_t nstrips, i
 }
 
 extern "C" int synth_codes(uint16_t *out, const uint64_t *keys, int64_t nstrips,
-                           int64_t strip_stride, int64_t n, uint32_t c, void *stream) {
+                           int64_t strip_stride, int64_t n, uint32_t c, int64_t start, void *stream) {
   if (nstrips <= 0 || n <= 0) return 0;
   dim3 grid((unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64), (unsigned)(nstrips < 65535 ? nstrips : 65535),
             (unsigned)((nstrips + 65534) / 65535));
-  k_codes<<<grid, 256, 0, (cudaStream_t)stream>>>(out, keys, nstrips, strip_stride, n, c);
+  k_codes<<<grid, 256, 0, (cudaStream_t)stream>>>(out, keys, nstrips, strip_stride, n, c, start);
   return (int)cudaGetLastError();
 }
 
 extern "C" int synth_values(uint16_t *out, const uint64_t *keys, int64_t nstrips,
-                            int64_t strip_stride, int64_t n, int d, void *stream) {
+                            int64_t strip_stride, int64_t n, int d, int64_t start, void *stream) {
   if (nstrips <= 0 || n <= 0) return 0;
   const int64_t tot8 = n * d / 8;
   dim3 grid((unsigned)((tot8 + 255) / 256 < 256 ? (tot8 + 255) / 256 : 256), (unsigned)(nstrips < 65535 ? nstrips : 65535),
             (unsigned)((nstrips + 65534) / 65535));
-  k_values<<<grid, 256, 0, (cudaStream_t)stream>>>(out, keys, nstrips, strip_stride, n, d);
+  k_values<<<grid, 256, 0, (cudaStream_t)stream>>>(out, keys, nstrips, strip_stride, n, d, start);
   return (int)cudaGetLastError();
 }
