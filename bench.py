@@ -149,7 +149,8 @@ class Workload:
         n_cap = max(64, (self.n_local + 63) // 64 * 64)
         cb = np.stack([synth.gen_codebook(SEED, l, g, c, d // g) for l in range(L)])
         self.codebook = torch.from_numpy(cb).to(device)
-        self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device)
+        self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device,
+                            lut_bits=cfg.get("lut_bits", 16))
         self.vs = hc.VStore.allocate(B, L, H, n_cap, d, placement=cfg["placement"], device=device)
         sd.fill_codes(self.kc.codes, SEED, c, self.n_local, start=self.base)
         sd.fill_values(self.vs.tensor, SEED, self.n_local, device=device, start=self.base)
@@ -306,7 +307,8 @@ def oracle_wave(cfg, units, threads):
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(max_workers=threads) as ex:
         list(ex.map(lambda a: oracle.decode_unit(a[0], a[1], a[2], n, a[3], cfg["tau"],
-                                                  cfg["k_max"]), inputs))
+                                                  cfg["k_max"], lut_bits=cfg.get("lut_bits", 16)),
+                    inputs))
     return time.perf_counter() - t0
 
 
@@ -398,6 +400,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="default 500 (config 1/2), 20 (3/4)")
     ap.add_argument("--warmup", type=int, default=None, help="default 10 (config 1/2), 3 (3/4)")
+    ap.add_argument("--lut8", action="store_true",
+                    help="8-bit query/codebook table variant (R2b, SURVEY f3)")
     ap.add_argument("--virtual-shards", type=int, default=0,
                     help="test mode: run config 4's sharded step as R shards on ONE GPU")
     ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
@@ -410,7 +414,10 @@ def main():
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.config is None:
         args.config = 3 if world_env == 1 else 4
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    cfg["lut_bits"] = 8 if args.lut8 else 16
+    if args.lut8:
+        cfg["workload"] += "; 8-bit table variant (R2b)"
     if args.steps is None:
         args.steps = 500 if args.config in (1, 2) else 20
     if args.warmup is None:
@@ -485,7 +492,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong" if sharded_mode else "weak", "vs_baseline": None,
-        "dtype": "i16+f32", "data": "synthetic (seeded splitmix64; codes uniform, C,q,V ~ Irwin-Hall normal)",
+        "dtype": "i8+f32" if cfg.get("lut_bits") == 8 else "i16+f32", "data": "synthetic (seeded splitmix64; codes uniform, C,q,V ~ Irwin-Hall normal)",
         "config": {"workload": cfg["workload"],
                    "parallelism": (f"sequence-sharded x{world}" if sharded_mode else
                                    ("replicas" if world > 1 else "single")),

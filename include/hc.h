@@ -47,9 +47,13 @@ typedef void *hc_stream_t; /* cudaStream_t */
  * dbar = d/g dims; c centroids per codebook slice; cbg codebook slices
  * (cbg == g: one codebook per group as C ∈ R^{g×c×dbar}; cbg == 1: one
  * codebook shared by all groups, Table 4b).
+ * lut_bits: precision of the query/codebook table T (R2): 0 or 16 = 16-bit fixed point
+ * (default, >= fp16 precision); 8 = the 8-bit table variant (R2b: ~bf16
+ * worst-case precision, half the shared-memory traffic; requires G == 4).
  * Supported by the kernels: d % g == 0, dbar in {1,2,4,8,16}, 1 <= c <= 8192. */
 typedef struct {
     int32_t d, g, c, cbg;
+    int32_t lut_bits;
 } hc_vq;
 
 /* Budget (R5): tau ∈ (0,1] is Eq. 4's cumulative-mass threshold (τ = 0.9 in

@@ -66,6 +66,9 @@ def lib():
             L.or_decode_unit.argtypes = [p, i32, i32, i32, i32, i32, p, p, i64, i64, p, p, p, i64,
                                          f32, i64, i32, p, p, p, p, p, p, p, p, p]
             L.or_decode_unit.restype = i32
+            L.or_decode_unit_bits.argtypes = L.or_decode_unit.argtypes + [i32]
+            L.or_decode_unit_bits.restype = i32
+            L.or_table_bits.argtypes = [p, i32, i32, i32, i32, i32, p, p, p, p, i32]
             _lib = L
     return _lib
 
@@ -98,15 +101,17 @@ def reconstruct(codes, C_, d: int) -> np.ndarray:
     return out
 
 
-def table(q, C_, g: int):
-    """q fp16 [G][d] -> (T32 fp32 [G][g][c], Tfx int16 [G][g][c], e int32 [G]) (R2)."""
+def table(q, C_, g: int, lut_bits: int = 16):
+    """q fp16 [G][d] -> (T32 fp32 [G][g][c], Tfx int16 [G][g][c], e int32 [G]) (R2, P:229);
+    lut_bits = 8 selects the 8-bit table variant (R2b)."""
     q = _c(q, np.float16); C_ = _c(C_, np.float32)
     G, d = q.shape
     cbg, c, dbar = C_.shape
     T32 = np.empty((G, g, c), dtype=np.float32)
     Tfx = np.empty((G, g, c), dtype=np.int16)
     e = np.empty(G, dtype=np.int32)
-    lib().or_table(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(T32), _ptr(Tfx), _ptr(e))
+    lib().or_table_bits(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(T32), _ptr(Tfx),
+                        _ptr(e), lut_bits)
     return T32, Tfx, e
 
 
@@ -212,7 +217,7 @@ def exact_attention(q_head, K, V) -> np.ndarray:
 
 
 def decode_unit(q, C_, P_groupmajor, nq: int, V, tau: float, k_max: int, renorm: int = 0,
-                rk=None, rv=None):
+                rk=None, rv=None, lut_bits: int = 16):
     """Full decode of one (b, l, kv) unit for its G query heads (R2->R6)."""
     q = _c(q, np.float16); C_ = _c(C_, np.float32); P = _c(P_groupmajor, np.uint16)
     V = _c(V, np.float16)
@@ -230,10 +235,11 @@ def decode_unit(q, C_, P_groupmajor, nq: int, V, tau: float, k_max: int, renorm:
     idx = np.empty((G, km), np.int32); w = np.empty((G, km), np.float64)
     ks = np.empty(G, np.int64); S = np.empty(G, np.uint64); M = np.empty(G, np.int32)
     kst = np.empty(G, np.int64); out = np.empty((G, d), np.float64)
-    rc = lib().or_decode_unit(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(P), nq,
-                              P.shape[1], _ptr(V.view(np.uint16)), _ptr(rk.view(np.uint16)),
-                              _ptr(rv.view(np.uint16)), nres, tau, k_max, renorm, _ptr(z), _ptr(e),
-                              _ptr(idx), _ptr(w), _ptr(ks), _ptr(S), _ptr(M), _ptr(kst), _ptr(out))
+    rc = lib().or_decode_unit_bits(_ptr(q.view(np.uint16)), G, d, g, c, cbg, _ptr(C_), _ptr(P), nq,
+                                   P.shape[1], _ptr(V.view(np.uint16)), _ptr(rk.view(np.uint16)),
+                                   _ptr(rv.view(np.uint16)), nres, tau, k_max, renorm, _ptr(z),
+                                   _ptr(e), _ptr(idx), _ptr(w), _ptr(ks), _ptr(S), _ptr(M),
+                                   _ptr(kst), _ptr(out), lut_bits)
     if rc:
         raise ValueError(f"or_decode_unit rc={rc}")
     return dict(z=z[:, :n], e=e, idx=[idx[h, :ks[h]].copy() for h in range(G)],

@@ -108,8 +108,10 @@ OR_EXPORT void or_reconstruct(const uint16_t *codes, int64_t n, int d, int g, in
  *   Cabs[ci][e] = max_m |C[ci][m][e]|
  *   A_i = |q_0|*Cabs[ci][0]; A_i = fmaf(|q_e|, Cabs[ci][e], A_i)   (same chain as t)
  *   A   = max_i A_i    (>= |t| for every entry, exactly, by monotone rounding)
- *   e_h = 100 if A < 2^-100 else clamp(14 - floor(log2 A), -100, 100);
- *   T_fx = clamp(rint(t * 2^e_h), -32767, 32767)   (rint = ties-to-even).
+ *   e_h = 100 if A < 2^-100 else clamp(top - floor(log2 A), -100, 100);
+ *   T_fx = clamp(rint(t * 2^e_h), -Tmax, Tmax)   (rint = ties-to-even)
+ * with (top, Tmax) = (14, 32767) for the default 16-bit table and (6, 127) for the 8-bit
+ * table variant (DESIGN R2b).
  * q [G][d] fp16 -> T32 [G][g][c] fp32 (may be NULL), Tfx [G][g][c] int16, e [G].
  * ---------------------------------------------------------------------- */
 static float or_pow2f(int e) /* exact 2^e for -126 <= e <= 127 */
@@ -148,21 +150,25 @@ OR_EXPORT float or_table_bound(const uint16_t *q, int d, int g, int cbg, const f
     return A;
 }
 
-OR_EXPORT int or_scale_exponent(float A)
+static int or_scale_exponent_top(float A, int top)
 {
     if (!(A >= 0x1p-100f)) return 100;
     int ex;
     (void)frexpf(A, &ex); /* A = f * 2^ex, f in [0.5, 1) -> floor(log2 A) = ex - 1 */
-    int e = 14 - (ex - 1);
+    int e = top - (ex - 1);
     if (e < -100) e = -100;
     if (e > 100) e = 100;
     return e;
 }
 
-OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
-                        float *T32, int16_t *Tfx, int32_t *e_out)
+OR_EXPORT int or_scale_exponent(float A) { return or_scale_exponent_top(A, 14); }
+
+OR_EXPORT void or_table_bits(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
+                             float *T32, int16_t *Tfx, int32_t *e_out, int lut_bits)
 {
     const int dbar = d / g;
+    const int top = lut_bits == 8 ? 6 : 14;
+    const float tmax = lut_bits == 8 ? 127.0f : 32767.0f;
     float *t = (float *)malloc(sizeof(float) * (size_t)g * c);
     float *Cabs = (float *)malloc(sizeof(float) * (size_t)cbg * dbar);
     or_codebook_absmax(C, cbg, c, dbar, Cabs);
@@ -176,12 +182,12 @@ OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, 
                 t[(size_t)i * c + m] = acc;
             }
         }
-        int e_h = or_scale_exponent(or_table_bound(q + (size_t)h * d, d, g, cbg, Cabs));
+        int e_h = or_scale_exponent_top(or_table_bound(q + (size_t)h * d, d, g, cbg, Cabs), top);
         float s = or_pow2f(e_h);
         for (size_t k = 0; k < (size_t)g * c; ++k) {
             float v = rintf(t[k] * s);
-            if (v > 32767.0f) v = 32767.0f;
-            if (v < -32767.0f) v = -32767.0f;
+            if (v > tmax) v = tmax;
+            if (v < -tmax) v = -tmax;
             Tfx[(size_t)h * g * c + k] = (int16_t)v;
             if (T32) T32[(size_t)h * g * c + k] = t[k];
         }
@@ -189,6 +195,12 @@ OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, 
     }
     free(Cabs);
     free(t);
+}
+
+OR_EXPORT void or_table(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
+                        float *T32, int16_t *Tfx, int32_t *e_out)
+{
+    or_table_bits(q, G, d, g, c, cbg, C, T32, Tfx, e_out, 16);
 }
 
 /* ------------------------------------------------------------------------
@@ -431,17 +443,18 @@ OR_EXPORT void or_exact_attention(const uint16_t *q, const uint16_t *K, const ui
  * Outputs per head h: z [G][nq+nres], e [G], idx [G][k_max], w [G][k_max],
  * k_sel [G], S [G], M [G], kstar [G], out [G][d] (double).
  * ---------------------------------------------------------------------- */
-OR_EXPORT int or_decode_unit(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
-                             const uint16_t *P, int64_t nq, int64_t stride, const uint16_t *V,
-                             const uint16_t *rk, const uint16_t *rv, int64_t nres, float tau,
-                             int64_t k_max, int renorm, int32_t *z, int32_t *e_out,
-                             int32_t *idx, double *w, int64_t *k_sel, uint64_t *S, int32_t *M,
-                             int64_t *kstar, double *out)
+OR_EXPORT int or_decode_unit_bits(const uint16_t *q, int G, int d, int g, int c, int cbg,
+                                  const float *C, const uint16_t *P, int64_t nq, int64_t stride,
+                                  const uint16_t *V, const uint16_t *rk, const uint16_t *rv,
+                                  int64_t nres, float tau, int64_t k_max, int renorm, int32_t *z,
+                                  int32_t *e_out, int32_t *idx, double *w, int64_t *k_sel,
+                                  uint64_t *S, int32_t *M, int64_t *kstar, double *out,
+                                  int lut_bits)
 {
     int64_t n = nq + nres;
     if (n <= 0) return 5;
     int16_t *Tfx = (int16_t *)malloc(sizeof(int16_t) * (size_t)G * g * c);
-    or_table(q, G, d, g, c, cbg, C, NULL, Tfx, e_out);
+    or_table_bits(q, G, d, g, c, cbg, C, NULL, Tfx, e_out, lut_bits);
     for (int h = 0; h < G; ++h) {
         int32_t *zh = z + (size_t)h * n;
         or_scores(Tfx + (size_t)h * g * c, P, nq, stride, g, c, zh);
@@ -463,4 +476,15 @@ OR_EXPORT int or_decode_unit(const uint16_t *q, int G, int d, int g, int c, int 
     }
     free(Tfx);
     return 0;
+}
+
+OR_EXPORT int or_decode_unit(const uint16_t *q, int G, int d, int g, int c, int cbg, const float *C,
+                             const uint16_t *P, int64_t nq, int64_t stride, const uint16_t *V,
+                             const uint16_t *rk, const uint16_t *rv, int64_t nres, float tau,
+                             int64_t k_max, int renorm, int32_t *z, int32_t *e_out,
+                             int32_t *idx, double *w, int64_t *k_sel, uint64_t *S, int32_t *M,
+                             int64_t *kstar, double *out)
+{
+    return or_decode_unit_bits(q, G, d, g, c, cbg, C, P, nq, stride, V, rk, rv, nres, tau, k_max,
+                               renorm, z, e_out, idx, w, k_sel, S, M, kstar, out, 16);
 }

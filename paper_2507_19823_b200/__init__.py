@@ -34,7 +34,8 @@ class HcError(RuntimeError):
 
 
 class hc_vq(C.Structure):
-    _fields_ = [("d", C.c_int32), ("g", C.c_int32), ("c", C.c_int32), ("cbg", C.c_int32)]
+    _fields_ = [("d", C.c_int32), ("g", C.c_int32), ("c", C.c_int32), ("cbg", C.c_int32),
+                ("lut_bits", C.c_int32)]
 
 
 class hc_budget(C.Structure):
@@ -193,7 +194,7 @@ class KCache:
     optional recent window res_k/res_v [B][L][Hkv][W][d] fp16."""
 
     def __init__(self, B, L, Hkv, G, d, g, c, n_cap, codebook, cbg=None, res_cap=0,
-                 codes=None, device="cuda"):
+                 codes=None, device="cuda", lut_bits=16):
         import torch
         cbg = g if cbg is None else cbg
         self.B, self.L, self.Hkv, self.G, self.d, self.g, self.c, self.cbg = B, L, Hkv, G, d, g, c, cbg
@@ -208,7 +209,7 @@ class KCache:
             self.res_k = self.res_v = None
         s = hc_kcache()
         s.B, s.L, s.Hkv, s.G = B, L, Hkv, G
-        s.vq = hc_vq(d, g, c, cbg)
+        s.vq = hc_vq(d, g, c, cbg, lut_bits)
         s.n_cap = n_cap
         s.codes = self.codes.data_ptr()
         s.codebook = codebook.data_ptr()

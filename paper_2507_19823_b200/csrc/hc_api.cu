@@ -68,10 +68,18 @@ constexpr int kMaxScanSplit = 4;
 // Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
 // the group split so the work fills the SMs with the least shared-memory time, modelled
 // per SM as  lookups/5.2 + slice_bytes_streamed/100  cycles (+ partial write/reduce).
-void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int *tpt, int *split) {
+void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int *tpt, int *split,
+                 int lut8) {
+  // per-SM shared-memory cycles: lookups * wavefronts/32 + (table slice + code strip) / 128 B
+  const double wf = lut8 ? 3.53 : 6.15;            // measured wavefronts per warp lookup
+  const double entry = lut8 ? 4.0 : 2.0 * G;       // table entry bytes
   double best = 1e300;
-  *tpt = 16; *split = 1;
-  for (int t : {8, 16}) {
+  *tpt = lut8 ? 32 : 16; *split = 1;
+  const int tpts16[2] = {8, 16}, tpts8[1] = {32};
+  const int *tl = lut8 ? tpts8 : tpts16;
+  const int nt = lut8 ? 1 : 2;
+  for (int ti = 0; ti < nt; ++ti) {
+    const int t = tl[ti];
     const int64_t tile = 512LL * t;
     const int64_t tiles = units * ((n + tile - 1) / tile);
     for (int sp : {1, 2, 4}) {
@@ -79,7 +87,7 @@ void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int
       const int64_t items = tiles * sp;
       const int64_t waves = (items + sms - 1) / sms;
       const double gper = (double)((g + sp - 1) / sp);
-      double item = tile * gper / 5.2 + gper * cpow2 * G * 2 / 100.0;
+      double item = tile * gper * wf / 32.0 + gper * (cpow2 * entry + tile * 4.0) / 128.0;
       if (sp > 1) item += tile * G * 4.0 / 64.0;  // partial stores
       double cost = waves * item;
       if (sp > 1) cost += (double)units * n * G * 4.0 * (sp + 1) / (sms * 64.0);  // reduce pass
@@ -299,6 +307,7 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   a = LayerArgs{};
   a.B = (int)B; a.Hkv = (int)H; a.G = (int)G; a.Hq = (int)Hq; a.d = (int)d; a.g = (int)g;
   a.c = kc->vq.c; a.cbg = kc->vq.cbg; a.dbar = (int)(d / g); a.cpow2 = Lw.cpow2;
+  a.lut8 = kc->vq.lut_bits == 8 ? 1 : 0;
   a.n_q = n_q; a.n_res = n_res; a.n_cand = n_cand; a.n_cap = ncap; a.res_cap = W > 0 ? W : 1;
   a.q = q;
   a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
@@ -340,7 +349,7 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   a.sel_k = sel_k;
   a.out = out;
   a.num_sms = num_sms();
-  choose_scan(B * H, n_q, (int)g, Lw.cpow2, (int)G, a.num_sms, &a.scan_tpt, &a.scan_split);
+  choose_scan(B * H, n_q, (int)g, Lw.cpow2, (int)G, a.num_sms, &a.scan_tpt, &a.scan_split, a.lut8);
   a.zpart = (float *)(w8 + Lw.o_zpart);
 
   return HC_OK;

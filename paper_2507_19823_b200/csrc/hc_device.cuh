@@ -27,6 +27,20 @@ HC_HD int scale_exponent(float A) {
   return e < -100 ? -100 : (e > 100 ? 100 : e);
 }
 
+// R2b (8-bit table): e = clamp(6 - floor(log2 A), -100, 100)
+HC_HD int scale_exponent8(float A) {
+  if (!(A >= 0x1p-100f)) return 100;
+  int ex = ((__float_as_int(A) >> 23) & 0xff) - 127;
+  int e = 6 - ex;
+  return e < -100 ? -100 : (e > 100 ? 100 : e);
+}
+
+HC_HD int quant_t8(float t, float s) {
+  float v = rintf(__fmul_rn(t, s));
+  v = fminf(fmaxf(v, -127.0f), 127.0f);
+  return (int)v;
+}
+
 // R2: T_fx = clamp(rint(t * 2^e), +-32767)
 HC_HD int quant_t(float t, float s) {
   float v = rintf(__fmul_rn(t, s));

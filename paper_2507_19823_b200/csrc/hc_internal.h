@@ -48,6 +48,7 @@ cudaError_t launch_rowcopy(const RowCopyArgs &a, cudaStream_t s);
 struct LayerArgs {
   // shape
   int B, Hkv, G, Hq, d, g, c, cbg, dbar, cpow2;
+  int lut8;               // 1: 8-bit table variant (R2b), entries = 4 x (int8 + 128) in a u32
   int64_t n_q, n_res, n_cand, n_cap, res_cap;
   // inputs
   const uint16_t *q;      // [B][Hq][d]

@@ -208,6 +208,124 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// 8-bit table variant (R2b): one 4-byte LDS per (token, group) -- 3.5 instead of
+// 6.15 shared-memory wavefronts per warp lookup -- and SWAR accumulation: the entry holds
+// the 4 heads as (int8 + 128) bytes; acc_e += w & 0x00FF00FF (heads 0, 2), acc_o +=
+// (w >> 8) & 0x00FF00FF (heads 1, 3), 16-bit fields never overflow for g <= 257, and
+// z_h = field - 128*ng exactly.  Two registers per token let a thread own 32 tokens
+// (tile = 16384 tokens), which halves the table-slice ingress per token.
+template <int TPT>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tiles_per_unit,
+                                                            int total_tiles, int nsplit) {
+  constexpr int G = 4;
+  constexpr int kChunks = TPT / 8;
+  constexpr int kTile = kScanThreads * TPT;
+  constexpr uint32_t kCodeBytes = kTile * 2;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t slice_bytes = (uint32_t)a.cpow2 * 4;
+  uint8_t *tbuf = smem;
+  uint8_t *cbuf = smem + 2 * slice_bytes;
+  uint64_t *tb = reinterpret_cast<uint64_t *>(cbuf + 3 * kCodeBytes);
+  uint64_t *cb = tb + 2;
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 2; ++j) mbar_init(&tb[j], 1);
+    for (int j = 0; j < 3; ++j) mbar_init(&cb[j], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t tph = 0, cph = 0;
+  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gper = (a.g + nsplit - 1) / nsplit;
+
+  for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
+    const int sp = item % nsplit;
+    const int tile = item / nsplit;
+    const int u = tile / tiles_per_unit;
+    const int tk = tile - u * tiles_per_unit;
+    const int i0 = sp * gper;
+    const int i1 = min(a.g, i0 + gper);
+    const int ng = i1 - i0;
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int64_t tile0 = (int64_t)tk * kTile;
+    const int64_t avail = a.n_cap - tile0;
+    const uint32_t cbytes = (uint32_t)(avail < kTile ? avail : kTile) * 2;
+    const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride +
+                        ((int64_t)kv * a.g + i0) * a.n_cap + tile0;
+    const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int j = 0; j < 2 && j < ng; ++j) {
+        mbar_expect_tx(&tb[j], slice_bytes);
+        bulk_g2s(tbuf + j * slice_bytes, Tu + (int64_t)j * slice_bytes, slice_bytes, &tb[j]);
+      }
+      for (int j = 0; j < 3 && j < ng; ++j) {
+        mbar_expect_tx(&cb[j], cbytes);
+        bulk_g2s(cbuf + j * kCodeBytes, P + (int64_t)j * a.n_cap, cbytes, &cb[j]);
+      }
+    }
+    const int woff = warp * (32 * TPT);
+    uint32_t ae[kChunks][8], ao[kChunks][8];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { ae[k][t] = 0u; ao[k][t] = 0u; }
+    int ci = 0;
+    for (int i = 0; i < ng; ++i) {
+      const int ti = i & 1;
+      mbar_wait(&cb[ci], (cph >> ci) & 1u);
+      cph ^= 1u << ci;
+      mbar_wait(&tb[ti], (tph >> ti) & 1u);
+      tph ^= 1u << ti;
+      const uint8_t *sb = tbuf + ti * slice_bytes;
+      const uint8_t *cs = cbuf + ci * kCodeBytes + (size_t)woff * 2;
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const uint4 c = *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
+        const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t e0 = *reinterpret_cast<const uint32_t *>(sb + ((w4[q] << 2) & mask));
+          const uint32_t e1 = *reinterpret_cast<const uint32_t *>(sb + ((w4[q] >> 14) & mask));
+          ae[k][2 * q] += e0 & 0x00FF00FFu;
+          ao[k][2 * q] += (e0 >> 8) & 0x00FF00FFu;
+          ae[k][2 * q + 1] += e1 & 0x00FF00FFu;
+          ao[k][2 * q + 1] += (e1 >> 8) & 0x00FF00FFu;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (i + 2 < ng) {
+          mbar_expect_tx(&tb[ti], slice_bytes);
+          bulk_g2s(tbuf + ti * slice_bytes, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, &tb[ti]);
+        }
+        if (i + 3 < ng) {
+          mbar_expect_tx(&cb[ci], cbytes);
+          bulk_g2s(cbuf + ci * kCodeBytes, P + (int64_t)(i + 3) * a.n_cap, cbytes, &cb[ci]);
+        }
+      }
+      ci = ci == 2 ? 0 : ci + 1;
+    }
+    const int bias = 128 * ng;
+    int mx[G], mn[G];
+    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      int acc[8][G];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        acc[t][0] = (int)(ae[k][t] & 0xffffu) - bias;
+        acc[t][2] = (int)(ae[k][t] >> 16) - bias;
+        acc[t][1] = (int)(ao[k][t] & 0xffffu) - bias;
+        acc[t][3] = (int)(ao[k][t] >> 16) - bias;
+      }
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn);
+    }
+  }
+}
+
 template <int G, int TPT>
 static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   constexpr int kTile = kScanThreads * TPT;
@@ -245,7 +363,39 @@ static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
   return scan_launch<G, 16>(a, s);
 }
 
+static cudaError_t scan8_launch(const LayerArgs &a, cudaStream_t s) {
+  constexpr int TPT = 32;
+  constexpr int kTile = kScanThreads * TPT;
+  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
+  const int units = a.B * a.Hkv;
+  const int nsplit = a.scan_split;
+  const int total = tiles_per_unit * units * nsplit;
+  if (total == 0) return cudaSuccess;
+  const size_t smem = (size_t)2 * a.cpow2 * 4 + 3 * (size_t)kTile * 2 + 5 * 8;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan8<TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured[dev] = 1;
+  }
+  const int grid = total < a.num_sms ? total : a.num_sms;
+  cudaEvent_t eb, ee;
+  scan_events(&eb, &ee);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
+  k_scan8<TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  note_launch();
+  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s) {
+  if (a.lut8) return scan8_launch(a, s);
   switch (a.G) {
     case 1: return scan_g<1>(a, s);
     case 2: return scan_g<2>(a, s);

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
       float A = 0.0f;
 #pragma unroll
       for (int w = 0; w < kTB / 32; ++w) A = fmaxf(A, sA[h][w]);
-      const int e = scale_exponent(A);
+      const int e = a.lut8 ? scale_exponent8(A) : scale_exponent(A);
       sc[h] = pow2f(e);
       if (i == 0 && split == 0 && threadIdx.x == 0) {
         hs[h].e = e;
@@ -112,6 +112,13 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   for (int m = m0 + threadIdx.x; m < m0 + per; m += kTB) {
     float t[G];
     table_entry<G, DBAR>(qs, Ci, m, a.c, t);
+    if (G == 4 && a.lut8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
+      uint32_t wv = 0;
+#pragma unroll
+      for (int h = 0; h < G; ++h) wv |= (uint32_t)(quant_t8(t[h], sc[h]) + 128) << (8 * h);
+      reinterpret_cast<uint32_t *>(a.T)[((int64_t)u * a.g + i) * a.cpow2 + m] = wv;
+      continue;
+    }
     int16_t packed[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t(t[h], sc[h]);

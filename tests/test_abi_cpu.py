@@ -31,28 +31,49 @@ def test_library_exports_every_header_symbol():
     assert "sm_100a" in hc.version()
 
 
-def test_struct_layout_matches_header():
+def test_struct_layout_matches_header(tmp_path):
+    """ctypes mirrors of the C structs agree with the C compiler's layout (gcc, same header)."""
+    import subprocess
     import paper_2507_19823_b200 as hc
-    # hc_kcache: 4 int32 + hc_vq(16) + int64 + 3 ptr + int32(+pad) + 2 ptr + 256 int64 + 256 int32
-    assert ctypes.sizeof(hc.hc_vq) == 16
-    assert ctypes.sizeof(hc.hc_budget) == 24
-    assert ctypes.sizeof(hc.hc_kcache) == 16 + 16 + 8 + 24 + 8 + 16 + 256 * 8 + 256 * 4
-    assert ctypes.sizeof(hc.hc_vstore) == 24
+    fields = {"hc_vq": ["d", "g", "c", "cbg", "lut_bits"],
+              "hc_budget": ["tau", "k_max", "renorm"],
+              "hc_kcache": ["B", "L", "Hkv", "G", "vq", "n_cap", "codes", "codebook", "cb_absmax",
+                            "res_cap", "res_k", "res_v", "n_q", "n_res"],
+              "hc_vstore": ["placement", "base", "n_cap"],
+              "hc_decode_debug": ["z", "e", "S", "M", "kstar"]}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "hc.h"', "int main(void){"]
+    for st, fs in fields.items():
+        src.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f in fs:
+            src.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    src.append("return 0;}")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
+    got = dict(line.split() for line in subprocess.check_output([str(exe)]).decode().splitlines())
+    for st, fs in fields.items():
+        cls = getattr(hc, st)
+        assert int(got[st]) == ctypes.sizeof(cls), st
+        for f in fs:
+            assert int(got[f"{st}.{f}"]) == getattr(cls, f).offset, f"{st}.{f}"
 
 
 def test_validation_without_gpu():
     """Argument validation is synchronous and needs no device."""
     import paper_2507_19823_b200 as hc
     L = hc.lib()
-    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 3, 16, 3), None, 10, None)
+    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 3, 16, 3, 0), None, 10, None)
     assert st == hc.HC_ERR_SHAPE
-    st = L.hc_quantize_keys(None, 0, None, hc.hc_vq(128, 32, 16, 32), None, 0, None)
+    st = L.hc_quantize_keys(None, 0, None, hc.hc_vq(128, 32, 16, 32, 0), None, 0, None)
     assert st == hc.HC_OK
-    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 32, 70000, 32), None, 10, None)
+    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 32, 70000, 32, 0), None, 10, None)
     assert st == hc.HC_ERR_RANGE
+    st = L.hc_quantize_keys(None, 10, None, hc.hc_vq(128, 32, 16, 32, 12), None, 10, None)
+    assert st == hc.HC_ERR_ARG
     kc = hc.hc_kcache()
     kc.B, kc.L, kc.Hkv, kc.G = 1, 1, 1, 4
-    kc.vq = hc.hc_vq(128, 32, 8192, 32)
+    kc.vq = hc.hc_vq(128, 32, 8192, 32, 0)
     kc.n_cap = 100  # not a multiple of 64
     assert L.hc_decode_workspace_bytes(ctypes.byref(kc), hc.budget(0.9, 10)) == 0
     kc.n_cap = 4096

@@ -128,6 +128,21 @@ def test_empty_cache_error(torch_cuda):
     assert ei.value.status == hc.HC_ERR_ARG
 
 
+# ------------------------------------------------------------------ 8-bit table variant (R2b)
+@pytest.mark.parametrize("n,g,tau,k_max,B,Hkv", [(4096, 32, 0.9, 512, 1, 1), (20011, 32, 0.7, 5000, 2, 2),
+                                                 (17000, 64, 0.9, 4250, 1, 2), (40000, 32, 1.0, 9000, 1, 1),
+                                                 (3, 32, 0.9, 2, 1, 1)])
+def test_lut8_variant(torch_cuda, n, g, tau, k_max, B, Hkv):
+    """The 8-bit-table scan (SWAR accumulation, 16K-token tiles) is bit-exact with the oracle's
+    R2b mode on scores, masses and index sets."""
+    _run(Case(B=B, Hkv=Hkv, g=g, n=n, tau=tau, k_max=k_max, lut_bits=8, seed=50 + n % 97))
+
+
+def test_lut8_config3_full_size_sampled(torch_cuda):
+    case = Case(B=4, L=1, Hkv=8, g=32, n=131072, k_max=16384, placement=1, seed=3, lut_bits=8)
+    _run(case, units=[(1, 2), (3, 7)])
+
+
 # ------------------------------------------------------------------ append protocol
 @pytest.mark.parametrize("res_cap", [0, 4])
 def test_append_then_decode(torch_cuda, res_cap):

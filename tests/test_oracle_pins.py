@@ -141,6 +141,24 @@ def test_table_fixed_point_scale_and_rounding(orc):
             assert np.abs(Tfx[h]).max() <= 32767
 
 
+def test_table_8bit_variant_scale_and_bound(orc):
+    """R2b (8-bit table): A·2^e in [2^6, 2^7), |T_fx| <= 127, round to nearest,
+    and the 16-bit table is the same values on a 2^8-finer grid (|T16 - 256·T8| <= 128.5)."""
+    rng = _rng(111)
+    for trial in range(10):
+        q = (rng.standard_normal((4, 128)) * 2.29).astype(np.float16)
+        C = rng.standard_normal((32, 256, 4)).astype(np.float32)
+        T32, T8, e8 = orc.table(q, C, 32, lut_bits=8)
+        _, T16, e16 = orc.table(q, C, 32)
+        assert np.array_equal(e16, e8 + 8)
+        for h in range(4):
+            A = orc.table_bound(q[h], C, 32)
+            assert 2 ** 6 <= A * 2.0 ** int(e8[h]) < 2 ** 7
+            assert np.abs(T8[h]).max() <= 127
+            assert np.all(np.abs(T8[h] - T32[h].astype(np.float64) * 2.0 ** int(e8[h])) <= 0.5)
+            assert np.all(np.abs(T16[h].astype(np.int64) - 256 * T8[h].astype(np.int64)) <= 128.5)
+
+
 def test_table_zero_query(orc):
     """q = 0 -> T = 0 (and the scale falls back to 2^100)."""
     C = _rng(1).standard_normal((4, 16, 2)).astype(np.float32)
