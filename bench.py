@@ -149,11 +149,19 @@ class Workload:
         n_cap = max(64, (self.n_local + 63) // 64 * 64)
         cb = np.stack([synth.gen_codebook(SEED, l, g, c, d // g) for l in range(L)])
         self.codebook = torch.from_numpy(cb).to(device)
-        self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device,
-                            lut_bits=cfg.get("lut_bits", 16))
-        self.vs = hc.VStore.allocate(B, L, H, n_cap, d, placement=cfg["placement"], device=device)
-        sd.fill_codes(self.kc.codes, SEED, c, self.n_local, start=self.base)
-        sd.fill_values(self.vs.tensor, SEED, self.n_local, device=device, start=self.base)
+        self.vo_only = cfg.get("vo_only", False)
+        if self.vo_only:  # every token resident with exact keys: codes / value store unused
+            self.kc = hc.KCache(B, L, H, G, d, g, c, 64, self.codebook, device=device,
+                                res_cap=n_cap)
+            self.vs = hc.VStore.allocate(B, L, H, 64, d, device=device)
+            sd.fill_values(self.kc.res_k, SEED + 7, self.n_local, device=device, start=self.base)
+            sd.fill_values(self.kc.res_v, SEED, self.n_local, device=device, start=self.base)
+        else:
+            self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device,
+                                lut_bits=cfg.get("lut_bits", 16))
+            self.vs = hc.VStore.allocate(B, L, H, n_cap, d, placement=cfg["placement"], device=device)
+            sd.fill_codes(self.kc.codes, SEED, c, self.n_local, start=self.base)
+            sd.fill_values(self.vs.tensor, SEED, self.n_local, device=device, start=self.base)
         self.reset_counts()
         # per-step inputs: q for every layer, the new token's k and v
         q = np.stack([np.stack([synth.gen_query(SEED + 1, b, l, self.Hq, d, Q_SCALE)
@@ -188,7 +196,10 @@ class Workload:
     def reset_counts(self):
         n_here = self.n_local - (1 if self.is_last else 0)  # the step appends position n-1
         for l in range(self.cfg["L"]):
-            self.kc.set_counts(l, n_here)
+            if self.vo_only:
+                self.kc.set_counts(l, 0, n_here)
+            else:
+                self.kc.set_counts(l, n_here)
 
     def step(self, profile=False):
         import paper_2507_19823_b200 as hc
@@ -400,6 +411,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None, help="default 500 (config 1/2), 20 (3/4)")
     ap.add_argument("--warmup", type=int, default=None, help="default 10 (config 1/2), 3 (3/4)")
+    ap.add_argument("--vo-only", action="store_true",
+                    help="value-offload-only mode (SURVEY f2): exact fp16 keys, no quantization")
     ap.add_argument("--lut8", action="store_true",
                     help="8-bit query/codebook table variant (R2b, SURVEY f3)")
     ap.add_argument("--virtual-shards", type=int, default=0,
@@ -416,6 +429,9 @@ def main():
         args.config = 3 if world_env == 1 else 4
     cfg = dict(CONFIGS[args.config])
     cfg["lut_bits"] = 8 if args.lut8 else 16
+    cfg["vo_only"] = bool(args.vo_only)
+    if args.vo_only:
+        cfg["workload"] += "; value-offload-only mode (exact fp16 keys, Table 1a VO row)"
     if args.lut8:
         cfg["workload"] += "; 8-bit table variant (R2b)"
     if args.steps is None:
@@ -466,7 +482,7 @@ def main():
 
     B, L, H, g, n, d = (cfg[k] for k in ("B", "L", "Hkv", "g", "n", "d"))
     n_here = wl.n_local
-    p_bytes_layer = B * H * n_here * g * 2
+    p_bytes_layer = B * H * n_here * (d if wl.vo_only else g) * 2  # exact K rows in VO-only mode
     achieved = p_bytes_layer / (scan_avg_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     traffic = None
@@ -503,7 +519,8 @@ def main():
         "quantized_key_frac_hbm": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_scan (Eq. 3 quantized-key scan)",
+                     "kernel": ("k_resident (exact-key dense scan, VO-only mode)" if wl.vo_only
+                                else "k_scan (Eq. 3 quantized-key scan)"),
                      "algorithmic_bytes_per_launch": p_bytes_layer,
                      "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L / ms_per_step,
                      "peak_source": peak_src},

@@ -196,32 +196,87 @@ cudaError_t launch_cbabs(const float *C, int64_t slices, int c, int dbar, float 
   return cudaGetLastError();
 }
 
-// Resident tokens: one thread per (token, query head); exact fp32 FMA chain over d
-// (R3), mapped onto the head's 2^-e grid; writes z and folds into M / zmin.
-__global__ void __launch_bounds__(128) k_resident(LayerArgs a) {
+// Resident (exact-key) tokens, R3: z = rint(clamp(fmaf-chain_e(q_e * k_e) * 2^e_h)).  Also the
+// dense scan of the value-offload-only mode (every token resident, n_q = 0).
+// CTA = (unit, tile of kRT tokens); the tile's key rows are staged in shared memory with
+// coalesced 16-B loads (row stride padded by 4 B so the 8 tokens of a warp hit 8 banks),
+// then thread (token, head) runs the FMA chain in ascending e over half2 pairs.
+constexpr int kRT = 128;  // tokens per CTA (kRT * G threads for G = 4)
+
+template <int G>
+__global__ void __launch_bounds__(kRT * G) k_resident(LayerArgs a) {
+  extern __shared__ __align__(16) uint8_t rsm[];
   const int u = blockIdx.y;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int h = (int)(idx % a.G);
-  const int64_t r = idx / a.G;
+  const int d = a.d;
+  const int rowb = d * 2 + 4;                   // padded row stride (bytes)
+  float *qs = reinterpret_cast<float *>(rsm);   // [G][d]
+  uint8_t *ks = rsm + G * d * 4;                // [kRT][rowb]
+  const int64_t r0 = (int64_t)blockIdx.x * kRT;
+  const int nthr = kRT * G;
+  for (int i = threadIdx.x; i < G * d; i += nthr)
+    qs[i] = h2f(a.q[((int64_t)b * a.Hq + kv * G + i / d) * d + i % d]);
+  const int per_row = d / 8;  // 16-B pieces per row
+  for (int i = threadIdx.x; i < kRT * per_row; i += nthr) {
+    const int t = i / per_row, pc = i % per_row;
+    const int64_t r = r0 + t;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < a.n_res) {
+      const int64_t slot = (a.res_slot0 + r) % a.res_cap;
+      v = *reinterpret_cast<const uint4 *>(a.res_k + (int64_t)b * a.res_b_stride +
+                                           ((int64_t)kv * a.res_cap + slot) * d + pc * 8);
+    }
+    uint32_t *dst = reinterpret_cast<uint32_t *>(ks + t * rowb + pc * 16);
+    dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;  // 4-B aligned (padded rows)
+  }
+  __syncthreads();
+  const int t = threadIdx.x / G, h = threadIdx.x % G;
+  const int64_t r = r0 + t;
   if (r >= a.n_res) return;
-  const int hq = kv * a.G + h;
-  const int64_t slot = (a.res_slot0 + r) % a.res_cap;
-  const uint16_t *krow = a.res_k + (int64_t)b * a.res_b_stride + ((int64_t)kv * a.res_cap + slot) * a.d;
-  const uint16_t *qrow = a.q + ((int64_t)b * a.Hq + hq) * a.d;
+  const __half2 *krow = reinterpret_cast<const __half2 *>(ks + t * rowb);
+  const float *qh = qs + h * d;
   float acc = 0.0f;
-  for (int e = 0; e < a.d; ++e) acc = __fmaf_rn(h2f(__ldg(qrow + e)), h2f(__ldg(krow + e)), acc);
-  HeadState *hs = a.hs + (int64_t)b * a.Hq + hq;
-  const int zq = quant_res(acc, pow2f(hs->e));
+  for (int e2 = 0; e2 < d / 2; ++e2) {
+    const float2 kf = __half22float2(krow[e2]);
+    acc = __fmaf_rn(qh[2 * e2], kf.x, acc);
+    acc = __fmaf_rn(qh[2 * e2 + 1], kf.y, acc);
+  }
+  const int hq = kv * G + h;
+  const int zq = quant_res(acc, pow2f(a.hs[(int64_t)b * a.Hq + hq].e));
   a.z[((int64_t)b * a.Hq + hq) * a.z_stride + a.n_q + r] = (float)zq;
 }
 
 cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s) {
   if (a.n_res <= 0) return cudaSuccess;
-  const int64_t work = a.n_res * a.G;
-  dim3 grid((unsigned)((work + 127) / 128), (unsigned)(a.B * a.Hkv));
-  k_resident<<<grid, 128, 0, s>>>(a);
+  // with no quantized tokens (value-offload-only mode) this IS the key scan: profile it
+  cudaEvent_t eb = nullptr, ee = nullptr;
+  unsigned evflag = 0;
+  if (a.n_q == 0) {
+    scan_events(&eb, &ee);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+    if (eb) cudaEventRecordWithFlags(eb, s, evflag);
+  }
+  dim3 grid((unsigned)((a.n_res + kRT - 1) / kRT), (unsigned)(a.B * a.Hkv));
+  const size_t smem = (size_t)a.G * a.d * 4 + (size_t)kRT * (a.d * 2 + 4);
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {  // d = 256 needs > 48 KiB
+    cudaFuncSetAttribute(k_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_resident<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_resident<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    configured[dev] = 1;
+  }
+  switch (a.G) {
+    case 1: k_resident<1><<<grid, kRT * 1, smem, s>>>(a); break;
+    case 2: k_resident<2><<<grid, kRT * 2, smem, s>>>(a); break;
+    case 4: k_resident<4><<<grid, kRT * 4, smem, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
   note_launch();
+  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
 }
 

@@ -102,6 +102,14 @@ def test_resident_window(torch_cuda):
     _run(Case(n=0, res_cap=64, n_res=64, k_max=64, tau=1.0, seed=12))
 
 
+@pytest.mark.parametrize("n_res,G", [(19000, 4), (5003, 2), (777, 1)])
+def test_value_offload_only_mode(torch_cuda, n_res, G):
+    """SURVEY f2 / Table 1a's "VO" row: exact fp16 keys for every token (all resident, no
+    quantized codes) -> dense exact scoring kernel + the same selection and gather."""
+    _run(Case(n=0, G=G, Hkv=2, res_cap=n_res + 64, n_res=n_res, k_max=n_res // 5, tau=0.9,
+              seed=60 + G))
+
+
 def test_renorm(torch_cuda):
     _run(Case(n=7000, renorm=1, k_max=300, seed=13))
 
