@@ -176,9 +176,18 @@ class Workload:
         self.v_new = self.v_host.to(device)
         self.out = torch.zeros((L, B, self.Hq, d), dtype=torch.float32, device=device)
         self.out_host = torch.zeros_like(self.out, device="cpu").pin_memory()
-        self.bud = hc.budget(cfg["tau"], cfg["k_max"])
+        self.cpu_gather = cfg.get("cpu_gather", False)
+        self.bud = hc.budget(cfg["tau"], cfg["k_max"], select_only=self.cpu_gather)
         self.ws = hc.Workspace(self.kc.workspace_bytes(self.bud), device=device)
         self.sel_k = torch.zeros((L, B, self.Hq), dtype=torch.int64, device=device)
+        if self.cpu_gather:  # (idx, w) of one layer, device + pinned host; host Eq. 5 output
+            km = cfg["k_max"]
+            self.sel_i_d = torch.empty((B * self.Hq, km), dtype=torch.int32, device=device)
+            self.sel_w_d = torch.empty((B * self.Hq, km), dtype=torch.float32, device=device)
+            self.sel_i_h = torch.empty_like(self.sel_i_d, device="cpu").pin_memory()
+            self.sel_w_h = torch.empty_like(self.sel_w_d, device="cpu").pin_memory()
+            self.sel_k_h = torch.empty((L, B * self.Hq), dtype=torch.int64).pin_memory()
+            self.out_cpu = torch.empty((L, B * self.Hq, d), dtype=torch.float32).pin_memory()
         self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(L)]
         for b_, e_ in self.ev:  # torch creates the CUDA event lazily on first record
@@ -209,13 +218,38 @@ class Workload:
                 self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
             if profile:
                 hc.profile_scan_events(*self.ev[l])
-            if self.shard is None:
+            if self.cpu_gather:
+                self._step_cpu_gather(l)
+            elif self.shard is None:
                 hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
                                     sel_k=self.sel_k[l], ws=self.ws)
             else:
                 o = sharded.decode_layer(self.shard, self.comm, self.q[l], l, self.base)
                 self.out[l].copy_(o.view_as(self.out[l]))
                 self.sel_k[l].copy_(self.shard.sel_k.view_as(self.sel_k[l]))
+
+    def _step_cpu_gather(self, l):
+        """GPU: table, scan, softmax mass, selection; D2H (idx, w, k); host threads: Eq. 5 over
+        the pinned value store; H2D of the layer output (all stream-ordered, graph-capturable)."""
+        import ctypes as C
+
+        import paper_2507_19823_b200 as hc
+        cfg = self.cfg
+        B, L, H, d = cfg["B"], cfg["L"], cfg["Hkv"], cfg["d"]
+        hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
+                            sel_idx=self.sel_i_d, sel_w=self.sel_w_d, sel_k=self.sel_k[l], ws=self.ws)
+        self.sel_i_h.copy_(self.sel_i_d, non_blocking=True)
+        self.sel_w_h.copy_(self.sel_w_d, non_blocking=True)
+        self.sel_k_h[l].copy_(self.sel_k[l].view(-1), non_blocking=True)
+        ncap = self.kc.n_cap
+        V = self.vs.tensor[0, l]
+        st = hc.lib().hc_enqueue_host_weighted_sum(
+            C.c_void_p(self.sel_i_h.data_ptr()), C.c_void_p(self.sel_w_h.data_ptr()),
+            C.c_void_p(self.sel_k_h[l].data_ptr()), B * self.Hq, cfg["k_max"],
+            C.c_void_p(V.data_ptr()), L * H * ncap * d, ncap * d, self.Hq, cfg["G"], d,
+            C.c_void_p(self.out_cpu[l].data_ptr()), 0, hc._stream())
+        hc._check(st)
+        self.out[l].view(-1, d).copy_(self.out_cpu[l], non_blocking=True)
 
     def step_e2e(self):
         self.q.copy_(self.q_host, non_blocking=True)
@@ -413,6 +447,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=None, help="default 10 (config 1/2), 3 (3/4)")
     ap.add_argument("--vo-only", action="store_true",
                     help="value-offload-only mode (SURVEY f2): exact fp16 keys, no quantization")
+    ap.add_argument("--cpu-gather", action="store_true",
+                    help="the paper's split (SURVEY f1): GPU selects, Eq. 5 runs on host threads "
+                         "over the host-resident values (needs a host-V config, e.g. 3)")
     ap.add_argument("--lut8", action="store_true",
                     help="8-bit query/codebook table variant (R2b, SURVEY f3)")
     ap.add_argument("--virtual-shards", type=int, default=0,
@@ -430,6 +467,11 @@ def main():
     cfg = dict(CONFIGS[args.config])
     cfg["lut_bits"] = 8 if args.lut8 else 16
     cfg["vo_only"] = bool(args.vo_only)
+    cfg["cpu_gather"] = bool(args.cpu_gather)
+    if args.cpu_gather:
+        if cfg["placement"] != 1:
+            raise SystemExit("--cpu-gather needs host-resident values (e.g. --config 3)")
+        cfg["workload"] += "; Eq. 5 on host threads from D2H-shipped (idx, w) (paper's CPU part)"
     if args.vo_only:
         cfg["workload"] += "; value-offload-only mode (exact fp16 keys, Table 1a VO row)"
     if args.lut8:

@@ -58,11 +58,15 @@ typedef struct {
 
 /* Budget (R5): tau ∈ (0,1] is Eq. 4's cumulative-mass threshold (τ = 0.9 in
  * §4.1); k_max >= 1 caps the kept set: k_sel = min(k*(τ), k_max);
- * renorm = 0 keeps Eq. 5's unrenormalised ã* (default), 1 divides by the kept mass. */
+ * renorm = 0 keeps Eq. 5's unrenormalised ã* (default), 1 divides by the kept mass;
+ * select_only = 0: the GPU computes Eq. 5 (default); 1: stop after the selection (sel_idx /
+ * sel_w / sel_k must be given, `out` is not written) so Eq. 5 can run on the host over the
+ * offloaded values -- the paper's own split (hc_host_weighted_sum). */
 typedef struct {
     float tau;
     int64_t k_max;
     int32_t renorm;
+    int32_t select_only;
 } hc_budget;
 
 #define HC_MAX_LAYERS 256
@@ -177,6 +181,27 @@ size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget);
 hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d, hc_budget budget,
                          int32_t *idx, float *w, int64_t *k, void *ws, size_t ws_bytes,
                          hc_stream_t stream);
+
+/* ---- Host-side Eq. 5 (the paper's "CPU part").
+ * out[row][e] = Σ_{r<k[row]} w[row][r] · V_row(idx[row][r])[e], fp32 accumulation in index
+ * order, on `threads` host threads (0 = all cores).  All pointers are HOST pointers:
+ *   idx [rows][k_stride] int32, w [rows][k_stride] fp32, k [rows] int64 (e.g. the D2H copies
+ *   of hc_decode_attention's selection with select_only = 1), row = b*Hq + hq;
+ *   V: value store of ONE layer, fp16, row j of (b, kv = hq / G) at
+ *      V + b*v_b_stride + kv*v_kv_stride + j*d  (elements);
+ *   out [rows][d] fp32.
+ * hc_host_weighted_sum runs synchronously; hc_enqueue_host_weighted_sum enqueues the same
+ * work as a host node on `stream` (cudaLaunchHostFunc; graph-capturable), executing after
+ * prior work on the stream (e.g. the D2H copies of idx / w / k). */
+hc_status hc_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
+                               int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
+                               int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d, float *out,
+                               int32_t threads);
+hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k,
+                                       int64_t rows, int64_t k_stride, const uint16_t *V,
+                                       int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
+                                       int32_t G, int32_t d, float *out, int32_t threads,
+                                       hc_stream_t stream);
 
 /* ---- Sequence-sharded decode, one layer, R ranks (one per GPU).
  * Rank `rank` holds the contiguous GLOBAL token range [shard_base, shard_base + n_q[layer])

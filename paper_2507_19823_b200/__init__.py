@@ -23,7 +23,8 @@ HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
 EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_events",
            "hc_codebook_absmax", "hc_quantize_keys", "hc_append_kv",
            "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
-           "hc_select_topk", "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
+           "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
+           "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
            "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish"]
 
 
@@ -39,7 +40,8 @@ class hc_vq(C.Structure):
 
 
 class hc_budget(C.Structure):
-    _fields_ = [("tau", C.c_float), ("k_max", C.c_int64), ("renorm", C.c_int32)]
+    _fields_ = [("tau", C.c_float), ("k_max", C.c_int64), ("renorm", C.c_int32),
+                ("select_only", C.c_int32)]
 
 
 class hc_kcache(C.Structure):
@@ -92,6 +94,11 @@ def lib():
         L.hc_select_workspace_bytes.restype = C.c_size_t
         L.hc_select_topk.argtypes = [p, i64, i64, i32, hc_budget, p, p, p, p, C.c_size_t, p]
         L.hc_select_topk.restype = i32
+        hw = [p, p, p, i64, i64, p, i64, i64, i32, i32, i32, p, i32]
+        L.hc_host_weighted_sum.argtypes = hw
+        L.hc_host_weighted_sum.restype = i32
+        L.hc_enqueue_host_weighted_sum.argtypes = hw + [p]
+        L.hc_enqueue_host_weighted_sum.restype = i32
         KC, VS = C.POINTER(hc_kcache), C.POINTER(hc_vstore)
         L.hc_shard_workspace_bytes.argtypes = [KC, hc_budget]
         L.hc_shard_workspace_bytes.restype = C.c_size_t
@@ -138,8 +145,8 @@ def profile_scan_events(begin, end):
                                         C.c_void_p(end.cuda_event) if end is not None else None))
 
 
-def budget(tau: float, k_max: int, renorm: bool = False) -> hc_budget:
-    return hc_budget(float(tau), int(k_max), int(bool(renorm)))
+def budget(tau: float, k_max: int, renorm: bool = False, select_only: bool = False) -> hc_budget:
+    return hc_budget(float(tau), int(k_max), int(bool(renorm)), int(bool(select_only)))
 
 
 # ----------------------------------------------------------------------------- encode

@@ -15,12 +15,12 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhc.so")
 SOURCES = ["hc_api.cu", "hc_encode.cu", "hc_table.cu", "hc_scan.cu", "hc_select.cu",
-           "hc_select_fused.cu", "hc_shard.cu"]
+           "hc_select_fused.cu", "hc_shard.cu", "hc_host.cu"]
 HEADERS = ["hc_device.cuh", "hc_internal.h"]
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}"]
 
 
@@ -54,7 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose and log:
                 sys.stderr.write(log)
     if force or jobs or _stale(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *objs])
+        run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp",
+             *objs, "-lgomp"])
         os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -289,7 +289,9 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   if (!(vs->placement == HC_V_DEVICE || vs->placement == HC_V_HOST_MAPPED))
     return fail(HC_ERR_ARG, "bad vstore placement");
   if (layer < 0 || layer >= kc->L) return fail(HC_ERR_RANGE, "layer %d out of range", layer);
-  if (need_q && (!q || !out)) return fail(HC_ERR_ARG, "q/out NULL");
+  if (need_q && (!q || (!out && !budget.select_only))) return fail(HC_ERR_ARG, "q/out NULL");
+  if (budget.select_only && (!sel_idx || !sel_w || !sel_k))
+    return fail(HC_ERR_ARG, "select_only needs sel_idx, sel_w and sel_k");
   if (!(budget.tau > 0.0f && budget.tau <= 1.0f)) return fail(HC_ERR_ARG, "tau=%g not in (0,1]", budget.tau);
   if (budget.k_max < 1) return fail(HC_ERR_ARG, "k_max < 1");
   if (!!sel_idx != !!sel_w) return fail(HC_ERR_ARG, "pass both sel_idx and sel_w, or neither");
@@ -375,7 +377,8 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
   sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
-  if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, 1, a.num_sms, s,
+  if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, budget.select_only ? 0 : 1,
+                               a.num_sms, s,
                                dbg && dbg->z ? 1 : 0)) != cudaSuccess)
     return cuda_check(e, "select");
   if (dbg) {

@@ -36,7 +36,7 @@ def test_struct_layout_matches_header(tmp_path):
     import subprocess
     import paper_2507_19823_b200 as hc
     fields = {"hc_vq": ["d", "g", "c", "cbg", "lut_bits"],
-              "hc_budget": ["tau", "k_max", "renorm"],
+              "hc_budget": ["tau", "k_max", "renorm", "select_only"],
               "hc_kcache": ["B", "L", "Hkv", "G", "vq", "n_cap", "codes", "codebook", "cb_absmax",
                             "res_cap", "res_k", "res_v", "n_q", "n_res"],
               "hc_vstore": ["placement", "base", "n_cap"],
@@ -105,3 +105,34 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "hc_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_host_weighted_sum_matches_oracle_gather():
+    """SURVEY f1 (the paper's CPU part of Eq. 2): hc_host_weighted_sum on host
+    memory equals the oracle's Eq. 5 (double) within fp32 accumulation error; runs on CPU."""
+    import numpy as np
+    import oracle
+    import paper_2507_19823_b200 as hc
+    import ctypes as C
+    rng = np.random.default_rng(3)
+    B, Hkv, G, d, n, k_stride = 2, 2, 4, 128, 5000, 1500
+    Hq = Hkv * G
+    V = rng.standard_normal((B, Hkv, n, d)).astype(np.float16)
+    rows = B * Hq
+    idx = np.zeros((rows, k_stride), np.int32)
+    w = np.zeros((rows, k_stride), np.float32)
+    k = rng.integers(1, k_stride, size=rows).astype(np.int64)
+    for r in range(rows):
+        sel = np.sort(rng.choice(n, size=k[r], replace=False))
+        idx[r, :k[r]] = sel
+        ww = rng.random(k[r])
+        w[r, :k[r]] = (ww / ww.sum()).astype(np.float32)
+    out = np.zeros((rows, d), np.float32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    st = hc.lib().hc_host_weighted_sum(p(idx), p(w), p(k), rows, k_stride, p(V.view(np.uint16)),
+                                      Hkv * n * d, n * d, Hq, G, d, p(out), 4)
+    assert st == hc.HC_OK
+    for r in range(rows):
+        b, hq = divmod(r, Hq)
+        ref = oracle.gather(idx[r, :k[r]], w[r, :k[r]].astype(np.float64), V[b, hq // G])
+        assert np.allclose(out[r], ref, rtol=2e-3, atol=1e-3)

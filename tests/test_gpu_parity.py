@@ -247,6 +247,35 @@ def test_host_mapped_values(torch_cuda):
     _run(Case(B=2, Hkv=2, n=6000, k_max=900, placement=1, seed=31))
 
 
+# ------------------------------------------------------------------ the paper's CPU-side Eq. 5 (f1)
+def test_select_only_then_host_weighted_sum(torch_cuda):
+    """the GPU stops after the selection (budget.select_only), the (idx, w, k) go
+    to the host and Eq. 5 runs on host threads over the host-resident values."""
+    import ctypes as C
+    import paper_2507_19823_b200 as hc
+    torch = torch_cuda
+    case = Case(B=2, Hkv=2, n=12000, k_max=2000, placement=1, seed=71)
+    kc, vs, q = build_gpu(case)
+    B, Hq, km = case.B, case.Hq, case.k_max
+    idx = torch.full((B, Hq, km), -1, dtype=torch.int32, device="cuda")
+    w = torch.zeros((B, Hq, km), dtype=torch.float32, device="cuda")
+    k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
+    hc.decode_attention(q[0].contiguous(), kc, vs, 0, hc.budget(case.tau, km, select_only=True),
+                        out=torch.empty(1, device="cuda"), sel_idx=idx, sel_w=w, sel_k=k)
+    hi, hw, hk = idx.cpu(), w.cpu(), k.cpu()
+    out = torch.zeros((B * Hq, case.d), dtype=torch.float32)
+    V = vs.tensor  # pinned host [B][L][Hkv][n_cap][d]
+    st = hc.lib().hc_host_weighted_sum(C.c_void_p(hi.data_ptr()), C.c_void_p(hw.data_ptr()),
+                                       C.c_void_p(hk.data_ptr()), B * Hq, km, C.c_void_p(V.data_ptr()),
+                                       case.L * case.Hkv * case.n_cap * case.d, case.n_cap * case.d,
+                                       Hq, case.G, case.d, C.c_void_p(out.data_ptr()), 0)
+    assert st == hc.HC_OK
+    gpu = dict(out=out.numpy().reshape(B, Hq, case.d), idx=hi.numpy(), w=hw.numpy(), k=hk.numpy())
+    for b in range(B):
+        for kv in range(case.Hkv):
+            compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv, check_z=False)
+
+
 # ------------------------------------------------------------------ full-size sampled parity
 def test_config2_full_size_sampled(torch_cuda):
     """BASELINE config 2 shape (32K ctx, 8 KV heads, g=64, k_max=8192, τ=0.9), in the launch
