@@ -5,6 +5,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <atomic>
 
@@ -100,7 +101,7 @@ struct Layout {
   int cpow2;
   int64_t z_stride;
   int64_t k_eff;
-  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, total;
+  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, total;
   int nch_max;  // sharded compaction chunks
 };
 
@@ -126,6 +127,12 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
   L.nch_max = shard_chunks(ncand_max > 0 ? ncand_max : 1);
   L.o_chunk = o; o += align256((size_t)rows * L.nch_max * 8);
   L.o_part = o; o += align256((size_t)rows * L.nch_max * d * 4);
+  {
+    const int64_t units = B * Hkv;
+    const int64_t nchu = gather_union_chunks(ncand_max > 0 ? ncand_max : 1);
+    L.o_upart = o; o += align256((size_t)units * nchu * G * d * 4);
+    L.o_udone = o; o += align256((size_t)units * 4);
+  }
   L.total = o;
   return L;
 }
@@ -377,10 +384,28 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
   sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
-  if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, budget.select_only ? 0 : 1,
-                               a.num_sms, s,
+  // Eq. 5 placement policy (measured): host-mapped values -> the GQA union
+  // de-duplicated gather kernel (fewer host-link bytes: +18 % steps/s at config 3); HBM
+  // values -> the gather fused into the select kernel (higher memory-level parallelism).
+  // HC_GATHER=fused|union overrides.
+  static int gather_mode = -1;  // 0 fused, 1 union, 2 by placement
+  if (gather_mode < 0) {
+    const char *ev = getenv("HC_GATHER");
+    gather_mode = (ev && !strcmp(ev, "fused")) ? 0 : ((ev && !strcmp(ev, "union")) ? 1 : 2);
+  }
+  const bool want_union = gather_mode == 1 || (gather_mode == 2 && a.v_placement == 1);
+  const bool union_gather = !budget.select_only && want_union && a.G > 1;
+  if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
+                               (budget.select_only || union_gather) ? 0 : 1, a.num_sms, s,
                                dbg && dbg->z ? 1 : 0)) != cudaSuccess)
     return cuda_check(e, "select");
+  if (union_gather) {
+    uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_udone);
+    if ((e = cudaMemsetAsync(done, 0, (size_t)a.B * a.Hkv * 4, s)) != cudaSuccess)
+      return cuda_check(e, "memset");
+    if ((e = launch_gather_union(a, (float *)((uint8_t *)ws + Lw.o_upart), done, s)) != cudaSuccess)
+      return cuda_check(e, "gather");
+  }
   if (dbg) {
     if (dbg->z) {
       dim3 gz((unsigned)((n_cand + 255) / 256), (unsigned)rows);

@@ -124,6 +124,10 @@ cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st);
 
+// Eq. 5 with GQA union de-duplication (hc_gather.cu)
+int gather_union_chunks(int64_t n_cand);
+cudaError_t launch_gather_union(const LayerArgs &a, float *part, uint32_t *done, cudaStream_t s);
+
 // standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
                                      int64_t z_stride, HeadState *hs, float kappa0,
