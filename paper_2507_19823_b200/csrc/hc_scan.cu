@@ -13,6 +13,9 @@
 //  * the P strip of group i (group-major layout, contiguous per group) is read
 //    with 128-bit L1-bypassing loads, one group ahead of use;
 //  * one 8-byte LDS per (token, group) returns the 4 GQA heads' table entries.
+#include <stdlib.h>
+#include <string.h>
+
 #include "hc_internal.h"
 
 namespace hc {
@@ -109,7 +112,10 @@ __device__ __forceinline__ void store_chunk(const LayerArgs &a, float *zbase, in
 // its groups [i0, i1) and writes the exact integer partial to zpart[split]; k_zreduce
 // adds the partials (exact: integers < 2^24 in fp32) -- so small-context configs can
 // spread one unit's tokens AND groups over all SMs without re-streaming every slice.
-template <int G, int TPT>
+// RC = 1: the code strips go straight to registers (16-B L1-bypassing loads, two groups
+// ahead) instead of through a shared-memory ring -- saves 4 of the ~37 shared-memory bytes
+// per (token, group) the scan moves.
+template <int G, int TPT, int RC>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles_per_unit,
                                                            int total_tiles, int nsplit) {
   static_assert(TPT == 8 || TPT == 16, "TPT");
@@ -156,12 +162,26 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
         mbar_expect_tx(&tb[j], slice_bytes);
         bulk_g2s(tbuf + j * slice_bytes, Tu + (int64_t)j * slice_bytes, slice_bytes, &tb[j]);
       }
-      for (int j = 0; j < 3 && j < ng; ++j) {
-        mbar_expect_tx(&cb[j], cbytes);
-        bulk_g2s(cbuf + j * kCodeBytes, P + (int64_t)j * a.n_cap, cbytes, &cb[j]);
+      if (!RC) {
+        for (int j = 0; j < 3 && j < ng; ++j) {
+          mbar_expect_tx(&cb[j], cbytes);
+          bulk_g2s(cbuf + j * kCodeBytes, P + (int64_t)j * a.n_cap, cbytes, &cb[j]);
+        }
       }
     }
     const int woff = warp * (32 * TPT);  // this warp's first token inside the tile
+    // register code ring (RC): group i in rc0, i+1 in rc1
+    uint4 rc0[kChunks], rc1[kChunks];
+    bool cval[kChunks];
+    if (RC) {
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        cval[k] = tile0 + woff + k * 256 + lane * 8 < a.n_q;
+        const uint16_t *pk = P + woff + k * 256 + lane * 8;
+        rc0[k] = cval[k] ? ld_stream(pk) : make_uint4(0, 0, 0, 0);
+        rc1[k] = (cval[k] && ng > 1) ? ld_stream(pk + a.n_cap) : make_uint4(0, 0, 0, 0);
+      }
+    }
     int acc[kChunks][8][G];
 #pragma unroll
     for (int k = 0; k < kChunks; ++k)
@@ -173,15 +193,24 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
     int ci = 0;  // code ring slot of group i (i % 3)
     for (int i = 0; i < ng; ++i) {
       const int ti = i & 1;
-      mbar_wait(&cb[ci], (cph >> ci) & 1u);
-      cph ^= 1u << ci;
+      uint4 rc2[kChunks];
+      if (RC) {  // prefetch group i+2
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k)
+          rc2[k] = (cval[k] && i + 2 < ng)
+                       ? ld_stream(P + (int64_t)(i + 2) * a.n_cap + woff + k * 256 + lane * 8)
+                       : make_uint4(0, 0, 0, 0);
+      } else {
+        mbar_wait(&cb[ci], (cph >> ci) & 1u);
+        cph ^= 1u << ci;
+      }
       mbar_wait(&tb[ti], (tph >> ti) & 1u);
       tph ^= 1u << ti;
       const uint8_t *sb = tbuf + ti * slice_bytes;
       const uint8_t *cs = cbuf + ci * kCodeBytes + (size_t)woff * 2;
 #pragma unroll
       for (int k = 0; k < kChunks; ++k) {
-        const uint4 c = *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
+        const uint4 c = RC ? rc0[k] : *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
         lookup8<G>(c, sb, mask, acc[k]);
       }
       __syncthreads();
@@ -191,10 +220,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
           mbar_expect_tx(&tb[ti], slice_bytes);
           bulk_g2s(tbuf + ti * slice_bytes, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, &tb[ti]);
         }
-        if (i + 3 < ng) {
+        if (!RC && i + 3 < ng) {
           mbar_expect_tx(&cb[ci], cbytes);
           bulk_g2s(cbuf + ci * kCodeBytes, P + (int64_t)(i + 3) * a.n_cap, cbytes, &cb[ci]);
         }
+      }
+      if (RC) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) { rc0[k] = rc1[k]; rc1[k] = rc2[k]; }
       }
       ci = ci == 2 ? 0 : ci + 1;
     }
@@ -326,7 +359,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
   }
 }
 
-template <int G, int TPT>
+template <int G, int TPT, int RC>
 static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   constexpr int kTile = kScanThreads * TPT;
   const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
@@ -339,8 +372,8 @@ static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<G, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_scan<G, TPT, RC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured[dev] = 1;
   }
@@ -351,16 +384,26 @@ static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cap);
   const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  k_scan<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  k_scan<G, TPT, RC><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
 }
 
+static int scan_codes_in_regs() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_SCAN_CODES");
+    v = (ev && !strcmp(ev, "smem")) ? 0 : 1;
+  }
+  return v;
+}
+
 template <int G>
 static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
-  if (a.scan_tpt == 8) return scan_launch<G, 8>(a, s);
-  return scan_launch<G, 16>(a, s);
+  const int rc = scan_codes_in_regs();
+  if (a.scan_tpt == 8) return rc ? scan_launch<G, 8, 1>(a, s) : scan_launch<G, 8, 0>(a, s);
+  return rc ? scan_launch<G, 16, 1>(a, s) : scan_launch<G, 16, 0>(a, s);
 }
 
 static cudaError_t scan8_launch(const LayerArgs &a, cudaStream_t s) {
