@@ -101,7 +101,8 @@ struct Layout {
   int cpow2;
   int64_t z_stride;
   int64_t k_eff;
-  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, total;
+  size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
+      o_rdone, total;
   int nch_max;  // sharded compaction chunks
 };
 
@@ -132,6 +133,9 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
     const int64_t nchu = gather_union_chunks(ncand_max > 0 ? ncand_max : 1);
     L.o_upart = o; o += align256((size_t)units * nchu * G * d * 4);
     L.o_udone = o; o += align256((size_t)units * 4);
+    const int64_t nchr = gather_rows_chunks(L.k_eff);
+    L.o_rpart = o; o += align256((size_t)rows * nchr * 128 * 4);
+    L.o_rdone = o; o += align256((size_t)rows * 4);
   }
   L.total = o;
   return L;
@@ -386,19 +390,32 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
   // Eq. 5 placement policy (measured): host-mapped values -> the GQA union
   // de-duplicated gather kernel (fewer host-link bytes: +18 % steps/s at config 3); HBM
-  // values -> the gather fused into the select kernel (higher memory-level parallelism).
-  // HC_GATHER=fused|union overrides.
-  static int gather_mode = -1;  // 0 fused, 1 union, 2 by placement
+  // values -> the high-occupancy per-head row gather (many rows in flight per SM).
+  // HC_GATHER=fused|union|rows overrides; "fused" runs Eq. 5 inside the select kernel.
+  static int gather_mode = -1;  // 0 fused, 1 union, 3 rows, 2 by placement
   if (gather_mode < 0) {
     const char *ev = getenv("HC_GATHER");
-    gather_mode = (ev && !strcmp(ev, "fused")) ? 0 : ((ev && !strcmp(ev, "union")) ? 1 : 2);
+    gather_mode = (ev && !strcmp(ev, "fused")) ? 0
+                  : (ev && !strcmp(ev, "union")) ? 1
+                  : (ev && !strcmp(ev, "rows")) ? 3 : 2;
   }
   const bool want_union = gather_mode == 1 || (gather_mode == 2 && a.v_placement == 1);
   const bool union_gather = !budget.select_only && want_union && a.G > 1;
+  const bool want_rows = gather_mode == 3 || (gather_mode == 2 && a.v_placement == 0);
+  const bool rows_gather = !budget.select_only && !union_gather && want_rows && a.d == 128;
   if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
-                               (budget.select_only || union_gather) ? 0 : 1, a.num_sms, s,
+                               (budget.select_only || union_gather || rows_gather) ? 0 : 1,
+                               a.num_sms, s,
                                dbg && dbg->z ? 1 : 0)) != cudaSuccess)
     return cuda_check(e, "select");
+  if (rows_gather) {
+    uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);
+    if ((e = cudaMemsetAsync(done, 0, (size_t)rows * 4, s)) != cudaSuccess)
+      return cuda_check(e, "memset");
+    const int64_t kc2 = a.k_max < n_cand ? a.k_max : n_cand;
+    if ((e = launch_gather_rows(a, kc2, (float *)((uint8_t *)ws + Lw.o_rpart), done, s)) != cudaSuccess)
+      return cuda_check(e, "gather");
+  }
   if (union_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_udone);
     if ((e = cudaMemsetAsync(done, 0, (size_t)a.B * a.Hkv * 4, s)) != cudaSuccess)

@@ -190,6 +190,118 @@ __global__ void __launch_bounds__(kGT) k_gather_union(LayerArgs a, int nchunks, 
 
 int gather_union_chunks(int64_t n_cand) { return (int)((n_cand + kGC - 1) / kGC); }
 
+// ---------------------------------------------------------------------------------------
+// High-occupancy per-head gather (HBM values): CTA = (query head, chunk of kRC kept
+// entries).  The chunk's (index, weight) pairs are staged in shared memory; each
+// half-warp owns kRC/16 rows and issues all of their 16-B loads before the first FMA
+// (16 rows x 16 B in flight per thread, ~2 CTAs per SM), which is what a random 256-B
+// row gather needs to approach the HBM rate.  Chunk partials are added in chunk order by
+// the row's last CTA.
+constexpr int kRC = 256;   // kept rows per CTA
+constexpr int kRT = 256;   // threads
+constexpr int kRU = kRC / ((kRT / 32) * 2);  // rows per half-warp (16 at d = 128)
+
+__global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float *part,
+                                                     uint32_t *done) {
+  __shared__ int32_t sj[kRC];
+  __shared__ float sw[kRC];
+  __shared__ float red[(kRT / 32) * 2 * 128];
+  const int row = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
+  const int b = row / a.Hq, hq = row - b * a.Hq, kv = hq / a.G;
+  const int64_t k = a.hs[row].ksel;
+  const int64_t e0 = (int64_t)ch * kRC;
+  if (e0 >= k) return;  // only the ceil(k/kRC) CTAs holding kept rows take part
+  const int32_t *li = a.sel_idx + (int64_t)row * a.k_max;
+  const float *lw = a.sel_w + (int64_t)row * a.k_max;
+  for (int i = tid; i < kRC; i += kRT) {
+    const bool v = e0 + i < k;
+    sj[i] = v ? li[e0 + i] : -1;
+    sw[i] = v ? lw[e0 + i] : 0.0f;
+  }
+  __syncthreads();
+  const int lane = tid & 31, hw = tid >> 4;   // half-warp id (0..15)
+  const int sub = lane & 15;                  // 8-dim slice (d = 128)
+  const uint16_t *Vb = a.V + (int64_t)b * a.v_b_stride + (int64_t)kv * a.v_kv_stride;
+  const uint16_t *Rb = a.res_v + (int64_t)b * a.res_b_stride + (int64_t)kv * a.res_cap * a.d;
+  uint4 v[kRU];
+#pragma unroll
+  for (int q = 0; q < kRU; ++q) {
+    const int j = sj[hw * kRU + q];
+    if (j >= 0) {
+      const uint16_t *src;
+      if (j < a.n_q) {
+        src = Vb + (int64_t)j * a.d;
+      } else {
+        const uint32_t sl = (uint32_t)(a.res_slot0 + (j - a.n_q)) % (uint32_t)a.res_cap;
+        src = Rb + (int64_t)sl * a.d;
+      }
+      v[q] = ldg_nc16(src + sub * 8);
+    } else {
+      v[q] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+#pragma unroll
+  for (int q = 0; q < kRU; ++q) {
+    const float w = sw[hw * kRU + q];
+    const uint32_t uu[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&uu[p]));
+      acc[2 * p] = fmaf(w, f2.x, acc[2 * p]);
+      acc[2 * p + 1] = fmaf(w, f2.y, acc[2 * p + 1]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[hw * 128 + sub * 8 + e] = acc[e];
+  __syncthreads();
+  float *pp = part + ((int64_t)row * nch + ch) * 128;
+  if (tid < 128) {
+    float s = 0.0f;
+    for (int q = 0; q < (kRT / 32) * 2; ++q) s += red[q * 128 + tid];
+    pp[tid] = s;
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int nact = (int)((k + kRC - 1) / kRC);  // CTAs of this row that hold kept rows
+    const unsigned prev = atomicAdd(&done[row], 1u);
+    last = prev == (unsigned)(nact > 0 ? nact : 1) - 1;
+    if (last) done[row] = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nact = (int)((k + kRC - 1) / kRC);
+  if (tid < 128) {
+    const float *p0 = part + (int64_t)row * nch * 128 + tid;
+    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int c = 0;
+    for (; c + 3 < nact; c += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s4[q] += __ldcg(p0 + (int64_t)(c + q) * 128);
+    }
+    for (; c < nact; ++c) s4[0] += __ldcg(p0 + (int64_t)c * 128);
+    a.out[(int64_t)row * 128 + tid] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  }
+}
+
+int gather_rows_chunks(int64_t k_cap) { return (int)((k_cap + kRC - 1) / kRC); }
+
+cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, uint32_t *done,
+                               cudaStream_t s) {
+  const int nch = gather_rows_chunks(k_cap);
+  if (nch == 0) return cudaSuccess;
+  // CTAs beyond a row's k_sel exit at once (they only count if they hold kept rows)
+  dim3 grid((unsigned)nch, (unsigned)(a.B * a.Hq));
+  k_gather_rows<<<grid, kRT, 0, s>>>(a, nch, part, done);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather_union(const LayerArgs &a, float *part, uint32_t *done, cudaStream_t s) {
   const int nch = gather_union_chunks(a.n_cand);
   if (nch == 0) return cudaSuccess;

@@ -127,6 +127,9 @@ cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint
 // Eq. 5 with GQA union de-duplication (hc_gather.cu)
 int gather_union_chunks(int64_t n_cand);
 cudaError_t launch_gather_union(const LayerArgs &a, float *part, uint32_t *done, cudaStream_t s);
+int gather_rows_chunks(int64_t k_cap);
+cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, uint32_t *done,
+                               cudaStream_t s);
 
 // standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,

@@ -74,6 +74,47 @@ __device__ __forceinline__ float load_z(const LayerArgs &la, const SelArgs &s, i
   return acc;
 }
 
+// visit every token t in [0, nt) of the CTA once (any order) with 16 tokens per thread in
+// flight: 4 x 16-B loads issued before use (zsrc is 16-B aligned: the z cache or the z row)
+template <typename F>
+__device__ __forceinline__ void for_tokens_pos(const float *zsrc, int64_t nt, F &&f) {
+  const int64_t nt4 = nt & ~(int64_t)3;
+  for (int64_t base = (int64_t)threadIdx.x * 4; base < nt4; base += (int64_t)kFT * 16) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + (int64_t)u * kFT * 4;
+      v[u] = t < nt4 ? *reinterpret_cast<const float4 *>(zsrc + t) : make_float4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + (int64_t)u * kFT * 4;
+      if (t < nt4) { f(t, v[u].x); f(t + 1, v[u].y); f(t + 2, v[u].z); f(t + 3, v[u].w); }
+    }
+  }
+  for (int64_t t = nt4 + threadIdx.x; t < nt; t += kFT) f(t, zsrc[t]);
+}
+
+template <typename F>
+__device__ __forceinline__ void for_tokens(const float *zsrc, int64_t nt, F &&f) {
+  const int64_t nt4 = nt & ~(int64_t)3;
+  for (int64_t base = (int64_t)threadIdx.x * 4; base < nt4; base += (int64_t)kFT * 16) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = base + (int64_t)u * kFT * 4;
+      v[u] = t < nt4 ? *reinterpret_cast<const float4 *>(zsrc + t) : make_float4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (base + (int64_t)u * kFT * 4 < nt4) {
+        f(v[u].x); f(v[u].y); f(v[u].z); f(v[u].w);
+      }
+    }
+  }
+  for (int64_t t = nt4 + threadIdx.x; t < nt; t += kFT) f(zsrc[t]);
+}
+
 __device__ __forceinline__ void fma8(float (&acc)[8], float w, const uint4 &v) {
   const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -120,11 +161,19 @@ __global__ void __launch_bounds__(kFT, 1)
   auto zat = [&](int64_t j) -> float {      // z of token j in [j0, j1)
     return zcache ? zc[j - j0] : s.z[(int64_t)row * s.z_stride + j];
   };
+  const float *zsrc = zcache ? zc : s.z + (int64_t)row * s.z_stride + j0;  // token t at zsrc[t]
 
   // ---------------------------------------------------------------- P0: z, M, zmin
   // 4 consecutive tokens per thread per round, all split planes loaded before use.
   int mx = INT_MIN, mn = INT_MAX;
-  {
+  if (nsplit <= 1) {  // z is final: stream it once (16 tokens in flight per thread)
+    for_tokens_pos(s.z + (int64_t)row * s.z_stride + j0, nt, [&](int64_t t, float zf) {
+      if (zcache) zc[t] = zf;
+      const int zi = __float2int_rn(zf);
+      mx = max(mx, zi);
+      mn = min(mn, zi);
+    });
+  } else {
     const float *zr = s.z + (int64_t)row * s.z_stride;
     const int64_t plane = (int64_t)la.B * la.Hq * la.z_stride;
     const float *zp = la.zpart + (int64_t)row * la.z_stride;
@@ -197,8 +246,8 @@ __global__ void __launch_bounds__(kFT, 1)
   // ---------------------------------------------------------------- P1: coarse histogram
   for (int i = tid; i < kNB; i += kFT) { cnt[i] = 0; mlo[i] = 0u; mhi[i] = 0u; }
   __syncthreads();
-  for (int64_t t = tid; t < nt; t += kFT) {
-    const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
+  for_tokens(zsrc, nt, [&](float zf) {
+    const uint32_t dl = (uint32_t)(M - __float2int_rn(zf));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
     const uint64_t W = mass(dl, kappa);
@@ -209,7 +258,7 @@ __global__ void __launch_bounds__(kFT, 1)
       wh += (old + wl < old) ? 1u : 0u;  // carry out of the low word
       if (wh) atomicAdd(&mhi[bk], wh);
     }
-  }
+  });
   cl.sync();
   for (int i = tid; i < nbo; i += kFT) {  // sum my owned bins over the peers
     uint32_t c = cnt[b_lo + i];
@@ -285,10 +334,10 @@ __global__ void __launch_bounds__(kFT, 1)
     for (int i = tid; i < kNB; i += kFT) cnt[i] = 0;
     __syncthreads();
     const uint32_t fmask = (1u << shift) - 1u;
-    for (int64_t t = tid; t < nt; t += kFT) {
-      const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
+    for_tokens(zsrc, nt, [&](float zf) {
+      const uint32_t dl = (uint32_t)(M - __float2int_rn(zf));
       if ((int)(dl >> shift) == bstar) atomicAdd(&cnt[dl & fmask], 1u);
-    }
+    });
     cl.sync();
     for (int i = tid; i < nbo; i += kFT) {
       uint32_t c = cnt[b_lo + i];
@@ -373,10 +422,21 @@ __global__ void __launch_bounds__(kFT, 1)
   __shared__ unsigned long long s_ws[kFT / 32], s_wt[kFT / 32];
   {
     unsigned int ns = 0, ntie = 0;
-    for (int64_t t = w_lo + lane; t < w_hi; t += 32) {
-      const uint32_t dl = (uint32_t)(M - __float2int_rn(zat(j0 + t)));
-      ns += dl < delta_star;
-      ntie += dl == delta_star;
+    for (int64_t tb = w_lo; tb < w_hi; tb += 32 * 8) {  // 8 loads in flight per lane
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t t = tb + q * 32 + lane;
+        v[q] = t < w_hi ? zsrc[t] : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (tb + q * 32 + lane < w_hi) {
+          const uint32_t dl = (uint32_t)(M - __float2int_rn(v[q]));
+          ns += dl < delta_star;
+          ntie += dl == delta_star;
+        }
+      }
     }
     ns = __reduce_add_sync(0xffffffffu, ns);
     ntie = __reduce_add_sync(0xffffffffu, ntie);
@@ -415,23 +475,34 @@ __global__ void __launch_bounds__(kFT, 1)
     const unsigned long long s_run0 = s_before + s_ws[warp];
     unsigned long long pos = s_run0 + (t_run < r_ties ? t_run : r_ties);   // kept before
     const unsigned lt = (1u << lane) - 1u;
-    for (int64_t tb = w_lo; tb < w_hi; tb += 32) {
-      const int64_t t = tb + lane;
-      const bool v = t < w_hi;
-      const uint32_t dl = v ? (uint32_t)(M - __float2int_rn(zat(j0 + t))) : 0xffffffffu;
-      const bool st = v && dl < delta_star;
-      const bool ti = v && dl == delta_star;
-      const unsigned bt = __ballot_sync(0xffffffffu, ti);
-      const unsigned long long my_tie_rank = t_run + __popc(bt & lt);
-      const bool take = st || (ti && my_tie_rank < r_ties);
-      const unsigned bs = __ballot_sync(0xffffffffu, take);
-      if (take) {
-        const unsigned long long p = pos + __popc(bs & lt);
-        oi[p] = (int32_t)(j0 + t);
-        ow[p] = (float)((double)mass(dl, kappa) / denom);
+    for (int64_t tb0 = w_lo; tb0 < w_hi; tb0 += 32 * 8) {  // 8 loads in flight per lane
+      float zv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t t = tb0 + q * 32 + lane;
+        zv[q] = t < w_hi ? zsrc[t] : 0.0f;
       }
-      pos += __popc(bs);
-      t_run += __popc(bt);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t tb = tb0 + q * 32;
+        if (tb >= w_hi) break;
+        const int64_t t = tb + lane;
+        const bool v = t < w_hi;
+        const uint32_t dl = v ? (uint32_t)(M - __float2int_rn(zv[q])) : 0xffffffffu;
+        const bool st = v && dl < delta_star;
+        const bool ti = v && dl == delta_star;
+        const unsigned bt = __ballot_sync(0xffffffffu, ti);
+        const unsigned long long my_tie_rank = t_run + __popc(bt & lt);
+        const bool take = st || (ti && my_tie_rank < r_ties);
+        const unsigned bs = __ballot_sync(0xffffffffu, take);
+        if (take) {
+          const unsigned long long p = pos + __popc(bs & lt);
+          oi[p] = (int32_t)(j0 + t);
+          ow[p] = (float)((double)mass(dl, kappa) / denom);
+        }
+        pos += __popc(bs);
+        t_run += __popc(bt);
+      }
     }
   }
   if (rank == 0 && tid == 0) {
@@ -466,10 +537,68 @@ __global__ void __launch_bounds__(kFT, 1)
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
   const int64_t r0 = (int64_t)sel_begin, r1 = (int64_t)(sel_begin + sel_count);
-  // half-warp per 256-B row (16 x 16-B L1-bypassing loads; zero-copy over the host link
-  // when V is host-mapped), software-pipelined: the (index, weight) batch of round k+1 is
+  // HBM values: half-warp per 256-B row, 16-B cp.async (LDGSTS, L1-bypassing) into a
+  // per-thread 2-stage shared-memory ring: stage k+1's kGU rows are in flight while stage k
+  // is consumed (each thread reads back only its own copies: no barrier), doubling the rows
+  // in flight per SM without registers.
+  if (stop != 5 && la.v_placement == 0) {
+    int32_t jn[kGU], jc[kGU];
+    float wn[kGU], wc[kGU];
+    const int64_t step = (int64_t)nslots * kGU;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem);
+    auto src_of = [&](int64_t j) -> const uint16_t * {
+      if (j < la.n_q) return Vb + j * la.d;
+      const uint32_t sl = (uint32_t)(la.res_slot0 + (j - la.n_q)) % (uint32_t)la.res_cap;
+      return Rb + (int64_t)sl * la.d;
+    };
+    auto issue = [&](int stage, const int32_t (&jj)[kGU]) {
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        if (jj[u] >= 0) {
+          const uint32_t dst = ring + (uint32_t)(((stage * kGU + u) * kFT + tid) * 16);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                       "l"(src_of(jj[u]) + sub * 8)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    __syncthreads();  // the ring overwrites the histogram / z-cache space
+    int64_t r = r0 + gslot;
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) {
+      const int64_t rr = r + (int64_t)u * nslots;
+      jc[u] = rr < r1 ? oi[rr] : -1;
+      wc[u] = rr < r1 ? ow[rr] : 0.0f;
+    }
+    issue(0, jc);
+    int stage = 0;
+    for (; r < r1; r += step) {
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        const int64_t rr = r + step + (int64_t)u * nslots;
+        jn[u] = rr < r1 ? oi[rr] : -1;
+        wn[u] = rr < r1 ? ow[rr] : 0.0f;
+      }
+      issue(stage ^ 1, jn);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        if (jc[u] >= 0) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(smem + ((stage * kGU + u) * kFT + tid) * 16);
+          fma8(acc, wc[u], v);
+        }
+        jc[u] = jn[u];
+        wc[u] = wn[u];
+      }
+      stage ^= 1;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  // host-mapped values: half-warp per 256-B row (16 x 16-B L1-bypassing zero-copy loads
+  // over the host link), software-pipelined: the (index, weight) batch of round k+1 is
   // loaded while round k's rows are in flight
-  if (stop != 5) {
+  if (stop != 5 && la.v_placement != 0) {
     int32_t jn[kGU];
     float wn[kGU];
     const int64_t step = (int64_t)nslots * kGU;
@@ -539,6 +668,8 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
   const int64_t per = ((s.n + cs - 1) / cs + 15) / 16 * 16;
   const int zcache = per <= kZCacheMax ? 1 : 0;
   size_t smem = (size_t)kNB * 12 + (zcache ? (size_t)per * 4 : 0);
+  const size_t ring = (size_t)2 * kGU * kFT * 16;  // cp.async gather ring (HBM values)
+  if (do_gather && la.v_placement == 0 && smem < ring) smem = ring;
   static int configured[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
