@@ -112,6 +112,23 @@ __device__ __forceinline__ void store_chunk(const LayerArgs &a, float *zbase, in
 // its groups [i0, i1) and writes the exact integer partial to zpart[split]; k_zreduce
 // adds the partials (exact: integers < 2^24 in fp32) -- so small-context configs can
 // spread one unit's tokens AND groups over all SMs without re-streaming every slice.
+// per-head max / min of the final scores (unsplit scan): warp reduce + one atomic per warp,
+// so the select kernel needs no extra pass over z for them
+template <int G>
+__device__ __forceinline__ void fold_minmax(const LayerArgs &a, int b, int kv, const int (&mx)[G],
+                                            const int (&mn)[G]) {
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const int vmx = __reduce_max_sync(0xffffffffu, mx[h]);
+    const int vmn = __reduce_min_sync(0xffffffffu, mn[h]);
+    if ((threadIdx.x & 31) == 0 && vmx != INT_MIN) {
+      HeadState *hs = a.hs + (int64_t)b * a.Hq + kv * G + h;
+      atomicMax(&hs->M, vmx);
+      atomicMin(&hs->zmin, vmn);
+    }
+  }
+}
+
 // RC = 1: the code strips go straight to registers (16-B L1-bypassing loads, two groups
 // ahead) instead of through a shared-memory ring -- saves 4 of the ~37 shared-memory bytes
 // per (token, group) the scan moves.
@@ -238,6 +255,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
 #pragma unroll
     for (int k = 0; k < kChunks; ++k)
       store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
+    if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
 }
 
@@ -343,6 +361,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
     }
     const int bias = 128 * ng;
     int mx[G], mn[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
     float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) {
@@ -356,6 +376,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
       }
       store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn);
     }
+    if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
 }
 

@@ -166,7 +166,16 @@ __global__ void __launch_bounds__(kFT, 1)
   // ---------------------------------------------------------------- P0: z, M, zmin
   // 4 consecutive tokens per thread per round, all split planes loaded before use.
   int mx = INT_MIN, mn = INT_MAX;
-  if (nsplit <= 1) {  // z is final: stream it once (16 tokens in flight per thread)
+  // z final and not cached: M / zmin were folded into hs by the scan / resident / prep
+  // epilogues -> no pass over z here
+  const bool skip_p0 = nsplit <= 1 && !zcache;
+  if (skip_p0) {
+    if (tid == 0) {
+      const int m0 = hs->M, z0 = hs->zmin;
+      mx = m0;
+      mn = z0;
+    }
+  } else if (nsplit <= 1) {  // z is final: stream it once into the cache
     for_tokens_pos(s.z + (int64_t)row * s.z_stride + j0, nt, [&](int64_t t, float zf) {
       if (zcache) zc[t] = zf;
       const int zi = __float2int_rn(zf);

@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
         hs[h].e = e;
         hs[h].kappa = __fmul_rn(a.kappa0, pow2f(-e));
         hs[h].amax = __float_as_uint(A);
+        hs[h].M = INT_MIN;     // folded by the scan / resident epilogues (atomics)
+        hs[h].zmin = INT_MAX;
       }
     }
   }
@@ -242,8 +244,11 @@ __global__ void __launch_bounds__(kRT * G) k_resident(LayerArgs a) {
     acc = __fmaf_rn(qh[2 * e2 + 1], kf.y, acc);
   }
   const int hq = kv * G + h;
-  const int zq = quant_res(acc, pow2f(a.hs[(int64_t)b * a.Hq + hq].e));
+  HeadState *hsr = a.hs + (int64_t)b * a.Hq + hq;
+  const int zq = quant_res(acc, pow2f(hsr->e));
   a.z[((int64_t)b * a.Hq + hq) * a.z_stride + a.n_q + r] = (float)zq;
+  atomicMax(&hsr->M, zq);
+  atomicMin(&hsr->zmin, zq);
 }
 
 cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s) {
