@@ -422,30 +422,41 @@ __global__ void __launch_bounds__(kFT, 1)
   // ---------------------------------------------------------------- P3: compaction
   cl.sync();  // peers done with my slot
   if (stop == 3) return;
-  // warp-chunked ordered compaction: warp w owns tokens [w*wc, (w+1)*wc) of this CTA;
-  // lane-strided (bank-conflict-free) reads, ballots give in-order positions.
+  // warp-chunked ordered compaction: warp w owns tokens [w*wc, (w+1)*wc) of this CTA and
+  // walks it 256 tokens per step, 8 consecutive tokens per lane (two 16-B loads); warp
+  // scans of the lanes' (tie, kept) counts give in-order positions.
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t wc = ((nt + kFT / 32 - 1) / (kFT / 32) + 31) / 32 * 32;
-  const int64_t w_lo = (int64_t)warp * wc;
+  const int64_t wc = ((nt + kFT / 32 - 1) / (kFT / 32) + 255) / 256 * 256;
+  const int64_t w_lo = (int64_t)warp * wc < nt ? (int64_t)warp * wc : nt;
   const int64_t w_hi = w_lo + wc < nt ? w_lo + wc : nt;
+  auto load8 = [&](int64_t t, float (&v)[8]) {  // tokens t..t+7 (t % 8 == 0), 0 past w_hi
+    if (t + 8 <= w_hi) {
+      const float4 a4 = *reinterpret_cast<const float4 *>(zsrc + t);
+      const float4 b4 = *reinterpret_cast<const float4 *>(zsrc + t + 4);
+      v[0] = a4.x; v[1] = a4.y; v[2] = a4.z; v[3] = a4.w;
+      v[4] = b4.x; v[5] = b4.y; v[6] = b4.z; v[7] = b4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = t + u < w_hi ? zsrc[t + u] : 0.0f;
+    }
+  };
   __shared__ unsigned long long s_ws[kFT / 32], s_wt[kFT / 32];
   {
     unsigned int ns = 0, ntie = 0;
-    for (int64_t tb = w_lo; tb < w_hi; tb += 32 * 8) {  // 8 loads in flight per lane
-      float v[8];
+    for (int64_t tb = w_lo; tb < w_hi; tb += 4 * 256) {  // 4 steps (8 x 16-B loads) in flight
+      float v[4][8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int64_t t = tb + q * 32 + lane;
-        v[q] = t < w_hi ? zsrc[t] : 0.0f;
-      }
+      for (int k = 0; k < 4; ++k) load8(tb + k * 256 + lane * 8, v[k]);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (tb + q * 32 + lane < w_hi) {
-          const uint32_t dl = (uint32_t)(M - __float2int_rn(v[q]));
-          ns += dl < delta_star;
-          ntie += dl == delta_star;
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (tb + k * 256 + lane * 8 + u < w_hi) {
+            const uint32_t dl = (uint32_t)(M - __float2int_rn(v[k][u]));
+            ns += dl < delta_star;
+            ntie += dl == delta_star;
+          }
         }
-      }
     }
     ns = __reduce_add_sync(0xffffffffu, ns);
     ntie = __reduce_add_sync(0xffffffffu, ntie);
@@ -472,7 +483,9 @@ __global__ void __launch_bounds__(kFT, 1)
     t_before += o->nt;
   }
   const unsigned long long cta_s = slot.ns, cta_t = slot.nt;
-  const double denom = s.renorm ? (double)selmass : (double)S;
+  // weight W_j / denom in fp32: W has <= 24 significant bits (exact in fp32), one rounding
+  // of 1/denom -> relative error < 2^-23
+  const float inv_den = (float)(1.0 / (s.renorm ? (double)selmass : (double)S));
   int32_t *oi = s.sel_idx + (int64_t)row * s.k_max;
   float *ow = s.sel_w + (int64_t)row * s.k_max;
   const unsigned long long sel_begin = s_before + (t_before < r_ties ? t_before : r_ties);
@@ -481,37 +494,62 @@ __global__ void __launch_bounds__(kFT, 1)
   const unsigned long long sel_count = sel_end - sel_begin;
   {
     unsigned long long t_run = t_before + s_wt[warp];                      // ties before
-    const unsigned long long s_run0 = s_before + s_ws[warp];
-    unsigned long long pos = s_run0 + (t_run < r_ties ? t_run : r_ties);   // kept before
-    const unsigned lt = (1u << lane) - 1u;
-    for (int64_t tb0 = w_lo; tb0 < w_hi; tb0 += 32 * 8) {  // 8 loads in flight per lane
-      float zv[8];
+    unsigned long long pos = s_before + s_ws[warp] + (t_run < r_ties ? t_run : r_ties);
+    float vn[8], vnn[8];  // two steps prefetched
+    if (w_lo < w_hi) load8(w_lo + lane * 8, vn);
+    if (w_lo + 256 < w_hi) load8(w_lo + 256 + lane * 8, vnn);
+    for (int64_t tb = w_lo; tb < w_hi; tb += 256) {
+      const int64_t t0 = tb + lane * 8;
+      float v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int64_t t = tb0 + q * 32 + lane;
-        zv[q] = t < w_hi ? zsrc[t] : 0.0f;
+      for (int u = 0; u < 8; ++u) { v[u] = vn[u]; vn[u] = vnn[u]; }
+      if (tb + 512 < w_hi) load8(t0 + 512, vnn);
+      uint32_t dl[8];
+      unsigned nst = 0, ntie = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = t0 + u < w_hi;
+        dl[u] = ok ? (uint32_t)(M - __float2int_rn(v[u])) : 0xffffffffu;
+        nst += ok && dl[u] < delta_star;
+        ntie += ok && dl[u] == delta_star;
       }
+      // exclusive warp scans: ties before this lane, then kept before this lane
+      unsigned tie_pre = ntie;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int64_t tb = tb0 + q * 32;
-        if (tb >= w_hi) break;
-        const int64_t t = tb + lane;
-        const bool v = t < w_hi;
-        const uint32_t dl = v ? (uint32_t)(M - __float2int_rn(zv[q])) : 0xffffffffu;
-        const bool st = v && dl < delta_star;
-        const bool ti = v && dl == delta_star;
-        const unsigned bt = __ballot_sync(0xffffffffu, ti);
-        const unsigned long long my_tie_rank = t_run + __popc(bt & lt);
-        const bool take = st || (ti && my_tie_rank < r_ties);
-        const unsigned bs = __ballot_sync(0xffffffffu, take);
-        if (take) {
-          const unsigned long long p = pos + __popc(bs & lt);
-          oi[p] = (int32_t)(j0 + t);
-          ow[p] = (float)((double)mass(dl, kappa) / denom);
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, tie_pre, off);
+        if (lane >= off) tie_pre += o;
+      }
+      const unsigned tie_tot = __shfl_sync(0xffffffffu, tie_pre, 31);
+      tie_pre -= ntie;
+      const unsigned long long my_t0 = t_run + tie_pre;
+      const unsigned taken = my_t0 >= r_ties ? 0u
+                             : (unsigned)((r_ties - my_t0) < ntie ? (r_ties - my_t0) : ntie);
+      unsigned kpre = nst + taken;
+      const unsigned kept = kpre;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, kpre, off);
+        if (lane >= off) kpre += o;
+      }
+      const unsigned kept_tot = __shfl_sync(0xffffffffu, kpre, 31);
+      unsigned long long p = pos + (kpre - kept);
+      unsigned ties_seen = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        bool take = dl[u] < delta_star;
+        if (!take && dl[u] == delta_star && t0 + u < w_hi) {
+          take = ties_seen < taken;
+          ++ties_seen;
         }
-        pos += __popc(bs);
-        t_run += __popc(bt);
+        if (take) {
+          oi[p] = (int32_t)(j0 + t0 + u);
+          ow[p] = __fmul_rn((float)mass(dl[u], kappa), inv_den);
+          ++p;
+        }
       }
+      pos += kept_tot;
+      t_run += tie_tot;
     }
   }
   if (rank == 0 && tid == 0) {
