@@ -149,6 +149,7 @@ hc_status check_vq(const hc_vq &vq) {
     return fail(HC_ERR_UNSUPPORTED, "dbar=%d not in {1,2,4,8,16}", dbar);
   if (vq.c > 65536) return fail(HC_ERR_RANGE, "c=%d exceeds the 16-bit index range", vq.c);
   if (!(vq.cbg == 1 || vq.cbg == vq.g)) return fail(HC_ERR_SHAPE, "cbg must be 1 or g");
+  if (vq.g > 128) return fail(HC_ERR_UNSUPPORTED, "g=%d > 128 (|z~| must stay below 2^22)", vq.g);
   if (vq.d % 8 || vq.d > 256 || (32 % (vq.d / 8)))
     return fail(HC_ERR_UNSUPPORTED, "d=%d not in {64,128,256}", vq.d);
   return HC_OK;

@@ -133,7 +133,10 @@ __device__ __forceinline__ uint4 ld_nc16(const uint16_t *p) {
   return v;
 }
 
-__global__ void __launch_bounds__(kFT, 1)
+// kG = false: selection only (P0-P3; the gather runs as its own kernel or not at all) --
+// lighter on registers, two CTAs per SM
+template <bool kG, int kOcc>
+__global__ void __launch_bounds__(kFT, kOcc)
     k_select_fused(SelArgs s, LayerArgs la, int cs, int nsplit, int zcache, int do_gather,
                    int zstore, int stop) {
   cg::cluster_group cl = cg::this_cluster();
@@ -158,9 +161,6 @@ __global__ void __launch_bounds__(kFT, 1)
   const int64_t j0 = (int64_t)rank * per;
   const int64_t j1 = j0 + per < n ? j0 + per : n;
   const int64_t nt = j1 > j0 ? j1 - j0 : 0;  // tokens of this CTA
-  auto zat = [&](int64_t j) -> float {      // z of token j in [j0, j1)
-    return zcache ? zc[j - j0] : s.z[(int64_t)row * s.z_stride + j];
-  };
   const float *zsrc = zcache ? zc : s.z + (int64_t)row * s.z_stride + j0;  // token t at zsrc[t]
 
   // ---------------------------------------------------------------- P0: z, M, zmin
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kFT, 1)
   } else if (nsplit <= 1) {  // z is final: stream it once into the cache
     for_tokens_pos(s.z + (int64_t)row * s.z_stride + j0, nt, [&](int64_t t, float zf) {
       if (zcache) zc[t] = zf;
-      const int zi = __float2int_rn(zf);
+      const int zi = zint(zf);
       mx = max(mx, zi);
       mn = min(mn, zi);
     });
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (t + u < nt) {
           if (zcache) zc[t + u] = v[u];
           if ((!zcache || zstore) && nsplit > 1) const_cast<float *>(zr)[j + u] = v[u];
-          const int zi = __float2int_rn(v[u]);
+          const int zi = zint(v[u]);
           mx = max(mx, zi);
           mn = min(mn, zi);
         }
@@ -256,10 +256,10 @@ __global__ void __launch_bounds__(kFT, 1)
   for (int i = tid; i < kNB; i += kFT) { cnt[i] = 0; mlo[i] = 0u; mhi[i] = 0u; }
   __syncthreads();
   for_tokens(zsrc, nt, [&](float zf) {
-    const uint32_t dl = (uint32_t)(M - __float2int_rn(zf));
+    const uint32_t dl = (uint32_t)(M - zint(zf));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
-    const uint64_t W = mass(dl, kappa);
+    const uint64_t W = mass_d(dl, kappa);
     if (W) {
       const uint32_t wl = (uint32_t)W;
       uint32_t wh = (uint32_t)(W >> 32);
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kFT, 1)
     __syncthreads();
     const uint32_t fmask = (1u << shift) - 1u;
     for_tokens(zsrc, nt, [&](float zf) {
-      const uint32_t dl = (uint32_t)(M - __float2int_rn(zf));
+      const uint32_t dl = (uint32_t)(M - zint(zf));
       if ((int)(dl >> shift) == bstar) atomicAdd(&cnt[dl & fmask], 1u);
     });
     cl.sync();
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kFT, 1)
       const int bi = tid * bpt + k;
       if (bi < nbo && cnt[b_lo + bi]) {
         lc += cnt[b_lo + bi];
-        lm += (unsigned long long)cnt[b_lo + bi] * mass(dbase | (uint32_t)(b_lo + bi), kappa);
+        lm += (unsigned long long)cnt[b_lo + bi] * mass_d(dbase | (uint32_t)(b_lo + bi), kappa);
       }
     }
     pc = lc; pm = lm;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kFT, 1)
         if (bi >= nbo) break;
         const unsigned long long c = cnt[b_lo + bi];
         if (!c) continue;
-        const unsigned long long w = mass(dbase | (uint32_t)(b_lo + bi), kappa);
+        const unsigned long long w = mass_d(dbase | (uint32_t)(b_lo + bi), kappa);
         const bool tt = !tau_all && w && (cm + c * w >= theta);
         const bool tk = cc + c >= (unsigned long long)s.k_max;
         if ((tt || tk) && found == kNB) { found = b_lo + bi; f_cc = cc; f_cm = cm; f_w = w; f_c = c; }
@@ -443,16 +443,17 @@ __global__ void __launch_bounds__(kFT, 1)
   __shared__ unsigned long long s_ws[kFT / 32], s_wt[kFT / 32];
   {
     unsigned int ns = 0, ntie = 0;
-    for (int64_t tb = w_lo; tb < w_hi; tb += 4 * 256) {  // 4 steps (8 x 16-B loads) in flight
-      float v[4][8];
+    constexpr int kCU = kOcc == 1 ? 4 : 2;  // steps in flight (2 x 16-B loads each)
+    for (int64_t tb = w_lo; tb < w_hi; tb += kCU * 256) {
+      float v[kCU][8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) load8(tb + k * 256 + lane * 8, v[k]);
+      for (int k = 0; k < kCU; ++k) load8(tb + k * 256 + lane * 8, v[k]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kCU; ++k)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (tb + k * 256 + lane * 8 + u < w_hi) {
-            const uint32_t dl = (uint32_t)(M - __float2int_rn(v[k][u]));
+            const uint32_t dl = (uint32_t)(M - zint(v[k][u]));
             ns += dl < delta_star;
             ntie += dl == delta_star;
           }
@@ -495,6 +496,9 @@ __global__ void __launch_bounds__(kFT, 1)
   {
     unsigned long long t_run = t_before + s_wt[warp];                      // ties before
     unsigned long long pos = s_before + s_ws[warp] + (t_run < r_ties ? t_run : r_ties);
+    // staging slice of this warp: 256 x (Δ, token) in the P1 mass bins (free after P2)
+    uint32_t *stg_d = reinterpret_cast<uint32_t *>(smem) + warp * 512;
+    uint32_t *stg_t = stg_d + 256;
     float vn[8], vnn[8];  // two steps prefetched
     if (w_lo < w_hi) load8(w_lo + lane * 8, vn);
     if (w_lo + 256 < w_hi) load8(w_lo + 256 + lane * 8, vnn);
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(kFT, 1)
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const bool ok = t0 + u < w_hi;
-        dl[u] = ok ? (uint32_t)(M - __float2int_rn(v[u])) : 0xffffffffu;
+        dl[u] = ok ? (uint32_t)(M - zint(v[u])) : 0xffffffffu;
         nst += ok && dl[u] < delta_star;
         ntie += ok && dl[u] == delta_star;
       }
@@ -533,7 +537,9 @@ __global__ void __launch_bounds__(kFT, 1)
         if (lane >= off) kpre += o;
       }
       const unsigned kept_tot = __shfl_sync(0xffffffffu, kpre, 31);
-      unsigned long long p = pos + (kpre - kept);
+      // stage the step's kept (Δ, token) in this warp's shared slice, then write them
+      // lane-parallel: one weight per lane instead of 8 divergent ones, coalesced stores
+      unsigned q = kpre - kept;
       unsigned ties_seen = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -543,11 +549,17 @@ __global__ void __launch_bounds__(kFT, 1)
           ++ties_seen;
         }
         if (take) {
-          oi[p] = (int32_t)(j0 + t0 + u);
-          ow[p] = __fmul_rn((float)mass(dl[u], kappa), inv_den);
-          ++p;
+          stg_d[q] = dl[u];
+          stg_t[q] = (uint32_t)(t0 + u);
+          ++q;
         }
       }
+      __syncwarp();
+      for (unsigned i = lane; i < kept_tot; i += 32) {
+        oi[pos + i] = (int32_t)(j0 + stg_t[i]);
+        ow[pos + i] = __fmul_rn((float)mass_d(stg_d[i], kappa), inv_den);
+      }
+      __syncwarp();
       pos += kept_tot;
       t_run += tie_tot;
     }
@@ -566,7 +578,7 @@ __global__ void __launch_bounds__(kFT, 1)
     hs->sel_mass = selmass;
     if (s.sel_k) s.sel_k[row] = (int64_t)ksel;
   }
-  if (!do_gather || stop == 4) {
+  if (!kG || !do_gather || stop == 4) {
     cl.sync();  // peers may still read my slot (P3 prefix) through DSMEM
     return;
   }
@@ -710,23 +722,39 @@ __global__ void __launch_bounds__(kFT, 1)
 
 cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
                                 int num_sms, cudaStream_t st, int zstore) {
-  int cs = 1;
-  while (cs < 8 && (int64_t)s.rows * cs * 2 <= num_sms && s.n / (cs * 2) >= 1024) cs *= 2;
-  const int64_t per = ((s.n + cs - 1) / cs + 15) / 16 * 16;
-  const int zcache = per <= kZCacheMax ? 1 : 0;
-  size_t smem = (size_t)kNB * 12 + (zcache ? (size_t)per * 4 : 0);
   const size_t ring = (size_t)2 * kGU * kFT * 16;  // cp.async gather ring (HBM values)
-  if (do_gather && la.v_placement == 0 && smem < ring) smem = ring;
-  static int configured[64] = {0};
+  auto smem_of = [&](int cs_, int *zc) {
+    const int64_t per = ((s.n + cs_ - 1) / cs_ + 15) / 16 * 16;
+    *zc = per <= kZCacheMax ? 1 : 0;
+    size_t sm = (size_t)kNB * 12 + (*zc ? (size_t)per * 4 : 0);
+    if (do_gather && la.v_placement == 0 && sm < ring) sm = ring;
+    return sm;
+  };
+  // CTAs resident per SM: 1 with the gather (128 registers), else 2 if shared memory allows
+  auto occ_of = [&](size_t sm) { return (!do_gather && sm <= 110 * 1024) ? 2 : 1; };
+  int cs = 1, zcache = 0, occ = 1;
+  while (cs < 8 && s.n / (cs * 2) >= 1024) {
+    int zc2 = 0;
+    const size_t sm2 = smem_of(cs * 2, &zc2);
+    // a second CTA per SM only pays for long rows (latency of the phase barriers otherwise)
+    const int o2 = s.n / (cs * 2) >= 32768 ? occ_of(sm2) : 1;
+    if ((int64_t)s.rows * cs * 2 > (int64_t)num_sms * o2) break;
+    cs *= 2;
+    occ = (int64_t)s.rows * cs > num_sms ? 2 : 1;
+  }
+  const size_t smem = smem_of(cs, &zcache);
+  static int configured[64][3] = {{0}};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_select_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int vi = do_gather ? 0 : occ;  // 0: gather, 1: select 1 CTA/SM, 2: select 2 CTAs/SM
+  auto fn = vi == 0 ? k_select_fused<true, 1> : vi == 1 ? k_select_fused<false, 1> : k_select_fused<false, 2>;
+  if (dev >= 0 && dev < 64 && !configured[dev][vi]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(kNB * 12 + kZCacheMax * 4));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_select_fused, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     (void)e;
-    configured[dev] = 1;
+    configured[dev][vi] = 1;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(s.rows * cs));
@@ -745,8 +773,7 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
     const char *ev = getenv("HC_SEL_STOP");
     stop_env = ev ? atoi(ev) : 0;
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_select_fused, s, la, cs, nsplit, zcache, do_gather, zstore,
-                                     stop_env);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, s, la, cs, nsplit, zcache, do_gather, zstore, stop_env);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kShT) k_sh_stats(LayerArgs a, int nsplit, int3
   for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
     const float zf = sh_z(a, row, j, nsplit);
     if (nsplit > 1 && j < a.n_q) a.z[(int64_t)row * a.z_stride + j] = zf;
-    const int zi = __float2int_rn(zf);
+    const int zi = zint(zf);
     mx = max(mx, zi);
     mn = min(mn, zi);
   }
@@ -70,10 +70,10 @@ __global__ void __launch_bounds__(kShT) k_sh_hist1(LayerArgs a, const int32_t *g
   for (int i = threadIdx.x; i < kNB; i += kShT) { cnt[i] = 0; mlo[i] = 0; mhi[i] = 0; }
   __syncthreads();
   for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
-    const uint32_t dl = (uint32_t)(M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    const uint32_t dl = (uint32_t)(M - zint(a.z[(int64_t)row * a.z_stride + j]));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
-    const uint64_t W = mass(dl, kappa);
+    const uint64_t W = mass_d(dl, kappa);
     if (W) {
       const uint32_t wl = (uint32_t)W;
       uint32_t wh = (uint32_t)(W >> 32);
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kShT) k_sh_hist2(LayerArgs a, unsigned long lo
   __syncthreads();
   const uint32_t fmask = (1u << h.shift) - 1u;
   for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
-    const uint32_t dl = (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    const uint32_t dl = (uint32_t)(h.M - zint(a.z[(int64_t)row * a.z_stride + j]));
     if ((int)(dl >> h.shift) == h.bstar) atomicAdd(&cnt[dl & fmask], 1u);
   }
   __syncthreads();
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kShT) k_sh_bound2(SelArgs s, const unsigned lo
   for (int k = 0; k < kB; ++k) {
     const int bi = threadIdx.x * kB + k;
     c[k] = hr[bi];
-    w[k] = c[k] ? mass(dbase | (uint32_t)bi, h.kappa) : 0ull;
+    w[k] = c[k] ? mass_d(dbase | (uint32_t)bi, h.kappa) : 0ull;
     lc += c[k];
     lm += c[k] * w[k];
   }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kShT) k_sh_counts(LayerArgs a, int nch, uint32
   const int64_t j0 = (int64_t)ch * kShChunk;
   unsigned ns = 0, nt = 0;
   for (int64_t j = j0 + threadIdx.x; j < j0 + kShChunk && j < a.n_cand; j += kShT) {
-    const uint32_t dl = (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    const uint32_t dl = (uint32_t)(h.M - zint(a.z[(int64_t)row * a.z_stride + j]));
     ns += dl < h.delta_star;
     nt += dl == h.delta_star;
   }
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int n
   __shared__ unsigned long long ws_[kShT / 32], wt_[kShT / 32];
   unsigned ns = 0, nt = 0;
   for (int64_t j = w0 + lane; j < w1 && j < a.n_cand; j += 32) {
-    const uint32_t dl = (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j]));
+    const uint32_t dl = (uint32_t)(h.M - zint(a.z[(int64_t)row * a.z_stride + j]));
     ns += dl < h.delta_star;
     nt += dl == h.delta_star;
   }
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int n
   for (int64_t jb = w0; jb < w1 && jb < a.n_cand; jb += 32) {
     const int64_t j = jb + lane;
     const bool v = j < w1 && j < a.n_cand;
-    const uint32_t dl = v ? (uint32_t)(h.M - __float2int_rn(a.z[(int64_t)row * a.z_stride + j])) : 0xffffffffu;
+    const uint32_t dl = v ? (uint32_t)(h.M - zint(a.z[(int64_t)row * a.z_stride + j])) : 0xffffffffu;
     const bool st = v && dl < h.delta_star;
     const bool ti = v && dl == h.delta_star;
     const unsigned bt = __ballot_sync(0xffffffffu, ti);
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int n
     float wv = 0.0f;
     if (take) {
       const unsigned long long p = pos + __popc(bs & lt);
-      wv = (float)((double)mass(dl, h.kappa) / denom);
+      wv = (float)((double)mass_d(dl, h.kappa) / denom);
       if ((int64_t)p < s.k_max) {
         oi[p] = (int32_t)(base + j);
         ow[p] = wv;
