@@ -62,6 +62,7 @@ def lib():
             L.or_select_float.argtypes = [p, i64, i32, f32, i64, i32, p, p, p]
             L.or_select_float.restype = i32
             L.or_gather.argtypes = [p, p, i64, p, i32, p]
+            L.or_select_shared.argtypes = [p, i32, i64, p, i32, f32, i64, p, p, p, p, p, p]
             L.or_exact_attention.argtypes = [p, p, p, i64, i32, p]
             L.or_decode_unit.argtypes = [p, i32, i32, i32, i32, i32, p, p, i64, i64, p, p, p, i64,
                                          f32, i64, i32, p, p, p, p, p, p, p, p, p]
@@ -200,6 +201,25 @@ def select_float(zf, d: int, tau: float, k_max: int, renorm: int = 0):
     return dict(idx=idx[:k].copy(), w=w[:k].copy(), k_sel=k)
 
 
+def select_shared(z, e, d: int, tau: float, k_max: int):
+    """R8 (NEXT f3(iii)): one Eq. 4 selection for the G query heads of a KV head on their
+    head-averaged fixed-point mass.  z [G][n] int32, e [G] -> dict(idx, w [G][k], k_sel,
+    S_A, kstar, A [n])."""
+    z = _c(z, np.int32); e = _c(e, np.int32)
+    G, n = z.shape
+    km = max(k_max, 1)
+    idx = np.empty(km, np.int32); w = np.empty((G, km), np.float64)
+    ks = np.zeros(1, np.int64); SA = np.zeros(1, np.uint64); kst = np.zeros(1, np.int64)
+    A = np.empty(max(n, 1), np.uint64)
+    rc = lib().or_select_shared(_ptr(z), G, n, _ptr(e), d, tau, k_max, _ptr(idx), _ptr(w),
+                                _ptr(ks), _ptr(SA), _ptr(kst), _ptr(A))
+    if rc:
+        raise ValueError(f"or_select_shared rc={rc}")
+    k = int(ks[0])
+    return dict(idx=idx[:k].copy(), w=w[:, :k].copy(), k_sel=k, S_A=int(SA[0]),
+                kstar=int(kst[0]), A=A[:n].copy())
+
+
 def gather(idx, w, V) -> np.ndarray:
     idx = _c(idx, np.int32); w = _c(w, np.float64); V = _c(V, np.float16)
     out = np.empty(V.shape[1], dtype=np.float64)
@@ -217,8 +237,10 @@ def exact_attention(q_head, K, V) -> np.ndarray:
 
 
 def decode_unit(q, C_, P_groupmajor, nq: int, V, tau: float, k_max: int, renorm: int = 0,
-                rk=None, rv=None, lut_bits: int = 16):
-    """Full decode of one (b, l, kv) unit for its G query heads (R2->R6)."""
+                rk=None, rv=None, lut_bits: int = 16, shared: bool = False):
+    """Full decode of one (b, l, kv) unit for its G query heads (R2->R6).  shared=True:
+    R8 -- one selection for the G heads (or_select_shared on the same scores), each head
+    summing its own weights over it (Eq. 5 via or_gather)."""
     q = _c(q, np.float16); C_ = _c(C_, np.float32); P = _c(P_groupmajor, np.uint16)
     V = _c(V, np.float16)
     G, d = q.shape
@@ -242,5 +264,15 @@ def decode_unit(q, C_, P_groupmajor, nq: int, V, tau: float, k_max: int, renorm:
                                    _ptr(kst), _ptr(out), lut_bits)
     if rc:
         raise ValueError(f"or_decode_unit rc={rc}")
+    if shared:
+        if renorm:
+            raise ValueError("shared selection takes renorm=0")
+        sh = select_shared(z[:, :n], e, d, tau, k_max)
+        Vall = np.concatenate([V[:nq], rv[:nres]]) if nres else V[:nq]
+        outs = np.stack([gather(sh["idx"], sh["w"][h], Vall) for h in range(G)])
+        k = sh["k_sel"]
+        return dict(z=z[:, :n], e=e, idx=[sh["idx"]] * G, w=[sh["w"][h] for h in range(G)],
+                    k_sel=np.full(G, k, np.int64), S=S, M=M, kstar=np.full(G, sh["kstar"], np.int64),
+                    out=outs, S_A=sh["S_A"], A=sh["A"])
     return dict(z=z[:, :n], e=e, idx=[idx[h, :ks[h]].copy() for h in range(G)],
                 w=[w[h, :ks[h]].copy() for h in range(G)], k_sel=ks, S=S, M=M, kstar=kst, out=out)

@@ -400,6 +400,98 @@ OR_EXPORT int or_select_float(const float *zf, int64_t n, int d, float tau, int6
 }
 
 /* ------------------------------------------------------------------------
+ * R8 (NEXT f3(iii); SURVEY F8 "per query head or per KV head") -- shared selection
+ * per KV head.  Reading (DESIGN.md §2 R8): the G query heads of one KV head keep ONE
+ * index set, chosen by Eq. 4 applied to their head-averaged attention
+ * distribution ā_j = (1/G) Σ_h ã_{h,j} (ã from Eq. 2's softmax).  Exactly:
+ *   W_{h,j} = R4 mass of head h (own M_h, κ_h);      S_h = Σ_j W_{h,j};
+ *   ρ_h = floor((2^104 - 1) / S_h);                   Â_{h,j} = floor(W_{h,j}·ρ_h / 2^64)
+ *   (≈ 2^40·ã_{h,j});  A_j = Σ_h Â_{h,j} (≈ G·2^40·ā_j);  S_A = Σ_j A_j;
+ *   Θ = ceil(τ_q·S_A / 2^24); order (A desc, j asc); k* = min{k : Σ_{r<k} A_(r) >= Θ};
+ *   τ_q >= 2^24 -> all; k_sel = min(k*, k_max).
+ * Each head h then applies Eq. 5 with its OWN weights W_{h,j} / S_h over the shared set
+ * (w_out[h][k], idx ascending).  z [G][n] int32 fixed-point scores, e [G] their exponents.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+    uint64_t A;
+    int64_t j;
+} or_gitem;
+
+static int or_cmp_g(const void *a, const void *b)
+{
+    const or_gitem *x = (const or_gitem *)a, *y = (const or_gitem *)b;
+    if (x->A != y->A) return x->A > y->A ? -1 : 1; /* A descending */
+    return x->j < y->j ? -1 : (x->j > y->j ? 1 : 0);
+}
+
+OR_EXPORT int or_select_shared(const int32_t *z, int G, int64_t n, const int32_t *e, int d,
+                               float tau, int64_t k_max, int32_t *idx_out, double *w_out,
+                               int64_t *k_sel_out, uint64_t *SA_out, int64_t *kstar_out,
+                               uint64_t *A_out)
+{
+    if (n <= 0) return 5;
+    if (G < 1 || G > 8) return 1;
+    int32_t M[8];
+    float kap[8];
+    uint64_t S[8], rho[8];
+    for (int h = 0; h < G; ++h) {
+        const int32_t *zh = z + (size_t)h * n;
+        M[h] = zh[0];
+        for (int64_t j = 1; j < n; ++j)
+            if (zh[j] > M[h]) M[h] = zh[j];
+        kap[h] = or_kappa(d, e[h]);
+        S[h] = 0;
+        for (int64_t j = 0; j < n; ++j)
+            S[h] += or_mass((uint32_t)((int64_t)M[h] - (int64_t)zh[j]), kap[h]);
+        unsigned __int128 num = ((unsigned __int128)1 << 104) - 1;
+        rho[h] = (uint64_t)(num / S[h]);
+    }
+    or_gitem *it = (or_gitem *)malloc(sizeof(or_gitem) * (size_t)n);
+    uint64_t SA = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        uint64_t A = 0;
+        for (int h = 0; h < G; ++h) {
+            uint64_t W = or_mass((uint32_t)((int64_t)M[h] - (int64_t)z[(size_t)h * n + j]), kap[h]);
+            A += (uint64_t)(((unsigned __int128)W * rho[h]) >> 64);
+        }
+        it[j].A = A;
+        it[j].j = j;
+        if (A_out) A_out[j] = A;
+        SA += A;
+    }
+    qsort(it, (size_t)n, sizeof(or_gitem), or_cmp_g);
+    uint32_t tq = or_tau_q(tau);
+    int64_t kstar = n;
+    if (tq < 16777216u) {
+        uint64_t theta = or_threshold(tq, SA), cum = 0;
+        for (int64_t k = 1; k <= n; ++k) {
+            cum += it[k - 1].A;
+            if (cum >= theta) {
+                kstar = k;
+                break;
+            }
+        }
+    }
+    int64_t ksel = kstar < k_max ? kstar : k_max;
+    int64_t *sel = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ksel > 0 ? ksel : 1));
+    for (int64_t k = 0; k < ksel; ++k) sel[k] = it[k].j;
+    qsort(sel, (size_t)ksel, sizeof(int64_t), or_cmp_i64);
+    for (int64_t k = 0; k < ksel; ++k) {
+        idx_out[k] = (int32_t)sel[k];
+        for (int h = 0; h < G; ++h) {
+            uint64_t W = or_mass((uint32_t)((int64_t)M[h] - (int64_t)z[(size_t)h * n + sel[k]]), kap[h]);
+            w_out[(size_t)h * k_max + k] = (double)W / (double)S[h];
+        }
+    }
+    *k_sel_out = ksel;
+    if (SA_out) *SA_out = SA;
+    if (kstar_out) *kstar_out = kstar;
+    free(sel);
+    free(it);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------
  * R6 -- sparse weighted sum, Eq. 5: ỹ = Σ_{i∈Π_k*} ã*_i V_i,
  * accumulated in double, in ascending-index order.  V rows fp16 [*][d].
  * ---------------------------------------------------------------------- */

@@ -392,6 +392,119 @@ def test_select_float_spec_examples(orc):
     assert r["w"][0] == 1.0 and r["w"][1] == 0.0
 
 
+# ---------------------------------------------------------------- R8 shared selection (f3(iii))
+def _shared_A(orc, z, e, d=128):
+    """Â_{h,j} = floor(W_{h,j}·ρ_h / 2^64), ρ_h = floor((2^104-1)/S_h), A_j = Σ_h Â_{h,j} in
+    Python integers (R8), on the pinned R4 masses."""
+    G, n = z.shape
+    A = [0] * n
+    for h in range(G):
+        kap = orc.kappa(d, int(e[h]))
+        M = int(z[h].max())
+        W = [orc.mass(M - int(v), kap) for v in z[h]]
+        rho = ((1 << 104) - 1) // sum(W)
+        for j in range(n):
+            A[j] += (W[j] * rho) >> 64
+    return A
+
+
+def test_select_shared_brute_force_tiny(orc):
+    """R8 on n <= 8, G in {2, 4}, heavy ties: the kept set is the exhaustive minimal prefix of
+    the head-averaged mass A (brute force over all subsets, C-P5's rule on A)."""
+    rng = _rng(61)
+    for trial in range(80):
+        G = 2 if trial % 2 else 4
+        n = int(rng.integers(1, 9))
+        z = (rng.integers(-3, 3, size=(G, n)) * 700 if trial % 3 == 0
+             else rng.integers(-3000, 3000, size=(G, n))).astype(np.int32)
+        e = rng.integers(9, 12, size=G).astype(np.int32)
+        A = _shared_A(orc, z, e)
+        for tau in (0.3, 0.6, 0.9, 1.0):
+            for k_max in (1, 3, n):
+                r = orc.select_shared(z, e, 128, tau, k_max)
+                assert r["A"].tolist() == A
+                kstar, sel = _brute_select(A, orc.tau_q(tau), k_max)
+                assert r["kstar"] == kstar
+                assert r["idx"].tolist() == sel
+
+
+def test_select_shared_mass_is_mean_softmax(orc):
+    """A_j / (G·2^40) = (1/G) Σ_h softmax_h(z̃/√d)_j within the closed form per head
+    a·(e^{2·EXP2_ERR} - 1) + 1/S_h + 2^-40 + 2^-63 (exp2 error, W truncation, ρ and Â
+    floors); S_A within [G·(2^40 - n - 1), G·(2^40 - 1)]."""
+    rng = _rng(62)
+    G, n = 4, 3000
+    e = np.array([12, 13, 12, 14], np.int32)
+    z = np.stack([(rng.standard_normal(n) * 2.29 * math.sqrt(128) * 2.0 ** int(e[h]))
+                  .clip(-2 ** 22, 2 ** 22) for h in range(G)]).astype(np.int32)
+    r = orc.select_shared(z, e, 128, 1.0, n)
+    assert r["k_sel"] == n
+    SA = r["S_A"]
+    assert G * (2 ** 40 - n - 1) <= SA <= G * (2 ** 40 - 1)
+    assert SA == int(sum(int(a) for a in r["A"]))
+    mean = np.zeros(n)
+    bound = np.zeros(n)
+    for h in range(G):
+        x = z[h].astype(np.float64) * 2.0 ** -int(e[h]) / math.sqrt(128)
+        sm = np.exp(x - x.max())
+        sm /= sm.sum()
+        S_h = sum(orc.mass(int(z[h].max()) - int(v), orc.kappa(128, int(e[h]))) for v in z[h])
+        mean += sm / G
+        bound += (sm * (math.exp(2 * EXP2_ERR) - 1) + 1.0 / S_h + 2.0 ** -40 + 2.0 ** -63) / G
+    got = r["A"].astype(np.float64) / (G * 2.0 ** 40)
+    assert np.all(np.abs(got - mean) <= bound)
+
+
+def test_select_shared_invariants(orc):
+    """R8: threshold met and minimal on A, top-k* by (A desc, index asc), monotone in τ,
+    τ = 1 -> all, the cap keeps the A-order prefix, n = 1 keeps {0} with weight 1."""
+    rng = _rng(63)
+    G, n = 4, 1500
+    e = np.full(G, 12, np.int32)
+    z = (rng.standard_normal((G, n)) * 3000).astype(np.int32)
+    prev = 0
+    order = None
+    for tau in (0.2, 0.5, 0.9, 0.99, 1.0):
+        r = orc.select_shared(z, e, 128, tau, n)
+        A = [int(a) for a in r["A"]]
+        order = sorted(range(n), key=lambda j: (-A[j], j))
+        sel = r["idx"].tolist()
+        assert sel == sorted(order[:r["k_sel"]])
+        tq = orc.tau_q(tau)
+        m = sum(A[j] for j in sel)
+        if tq >= 2 ** 24:
+            assert len(sel) == n
+        else:
+            assert m * 2 ** 24 >= tq * r["S_A"]
+            assert (m - A[order[r["k_sel"] - 1]]) * 2 ** 24 < tq * r["S_A"]
+        assert len(sel) >= prev
+        prev = len(sel)
+    full = orc.select_shared(z, e, 128, 0.9, n)
+    for k_max in (1, 10, full["kstar"] - 1, full["kstar"]):
+        r = orc.select_shared(z, e, 128, 0.9, k_max)
+        assert r["k_sel"] == min(k_max, full["kstar"])
+        assert r["idx"].tolist() == sorted(order[:r["k_sel"]]) or k_max >= full["kstar"]
+    r = orc.select_shared(np.array([[5], [-7]], np.int32), np.array([3, 4], np.int32), 128, 0.9, 4)
+    assert r["idx"].tolist() == [0] and np.all(r["w"] == 1.0)
+
+
+def test_decode_shared_tau1_equals_per_head(orc):
+    """R8 at τ = 1 keeps every token, so each head's Eq. 5 output equals the per-head
+    decode's bit for bit (same weights W/S, same ascending summation)."""
+    rng = _rng(64)
+    G, d, g, c, n = 4, 128, 32, 64, 700
+    q = (rng.standard_normal((G, d)) * 2.0).astype(np.float16)
+    C_ = rng.standard_normal((g, c, d // g)).astype(np.float32)
+    P = rng.integers(0, c, size=(g, n)).astype(np.uint16)
+    V = rng.standard_normal((n, d)).astype(np.float16)
+    a = orc.decode_unit(q, C_, P, n, V, 1.0, n)
+    b = orc.decode_unit(q, C_, P, n, V, 1.0, n, shared=True)
+    assert np.array_equal(a["out"], b["out"])
+    b9 = orc.decode_unit(q, C_, P, n, V, 0.9, n, shared=True)
+    assert all(np.array_equal(b9["idx"][0], b9["idx"][h]) for h in range(G))
+    assert b9["k_sel"][0] < n
+
+
 # ---------------------------------------------------------------- R6 gather (Eq. 5)
 def test_gather_singleton_is_row(orc):
     """singleton selection (index i, weight 1) -> V_i exactly."""
