@@ -177,7 +177,8 @@ class Workload:
         self.out = torch.zeros((L, B, self.Hq, d), dtype=torch.float32, device=device)
         self.out_host = torch.zeros_like(self.out, device="cpu").pin_memory()
         self.cpu_gather = cfg.get("cpu_gather", False)
-        self.bud = hc.budget(cfg["tau"], cfg["k_max"], select_only=self.cpu_gather)
+        self.bud = hc.budget(cfg["tau"], cfg["k_max"], select_only=self.cpu_gather,
+                             shared_kv=cfg.get("shared_kv", False))
         self.ws = hc.Workspace(self.kc.workspace_bytes(self.bud), device=device)
         self.sel_k = torch.zeros((L, B, self.Hq), dtype=torch.int64, device=device)
         if self.cpu_gather:  # (idx, w) of one layer, device + pinned host; host Eq. 5 output
@@ -322,7 +323,7 @@ def union_gather_bytes(wl) -> float:
     idx = torch.full((B, H * G, km), -1, dtype=torch.int32, device="cuda")
     w = torch.zeros((B, H * G, km), dtype=torch.float32, device="cuda")
     k = torch.zeros((B, H * G), dtype=torch.int64, device="cuda")
-    bud = hc.budget(cfg["tau"], km, select_only=True)
+    bud = hc.budget(cfg["tau"], km, select_only=True, shared_kv=cfg.get("shared_kv", False))
     rows = 0
     for l in range(L):
         hc.decode_attention(wl.q[l], wl.kc, wl.vs, l, bud, sel_idx=idx, sel_w=w, sel_k=k, ws=wl.ws,
@@ -475,6 +476,8 @@ def main():
                          "over the host-resident values (needs a host-V config, e.g. 3)")
     ap.add_argument("--lut8", action="store_true",
                     help="8-bit query/codebook table variant (R2b, SURVEY f3)")
+    ap.add_argument("--shared-kv", action="store_true",
+                    help="one selection per KV head shared by its GQA heads (R8, SURVEY f3(iii))")
     ap.add_argument("--virtual-shards", type=int, default=0,
                     help="test mode: run config 4's sharded step as R shards on ONE GPU")
     ap.add_argument("--config", type=int, default=None, choices=sorted(CONFIGS),
@@ -491,6 +494,9 @@ def main():
     cfg["lut_bits"] = 8 if args.lut8 else 16
     cfg["vo_only"] = bool(args.vo_only)
     cfg["cpu_gather"] = bool(args.cpu_gather)
+    cfg["shared_kv"] = bool(args.shared_kv)
+    if args.shared_kv:
+        cfg["workload"] += "; per-KV-head shared selection (R8, f3(iii))"
     if args.cpu_gather:
         if cfg["placement"] != 1:
             raise SystemExit("--cpu-gather needs host-resident values (e.g. --config 3)")

@@ -61,12 +61,18 @@ typedef struct {
  * renorm = 0 keeps Eq. 5's unrenormalised ã* (default), 1 divides by the kept mass;
  * select_only = 0: the GPU computes Eq. 5 (default); 1: stop after the selection (sel_idx /
  * sel_w / sel_k must be given, `out` is not written) so Eq. 5 can run on the host over the
- * offloaded values -- the paper's own split (hc_host_weighted_sum). */
+ * offloaded values -- the paper's own split (hc_host_weighted_sum).
+ * shared_kv = 0: one selection per query head (default, DESIGN R5/R7); 1: ONE selection
+ * per KV head shared by its G query heads, on their head-averaged attention mass (DESIGN
+ * R8); each head keeps its own weights W_h/S_h over the shared
+ * rows, so a value row is read once for G heads.  Takes renorm = 0 (else
+ * HC_ERR_UNSUPPORTED); the G rows of sel_idx / sel_k are identical. */
 typedef struct {
     float tau;
     int64_t k_max;
     int32_t renorm;
     int32_t select_only;
+    int32_t shared_kv;
 } hc_budget;
 
 #define HC_MAX_LAYERS 256

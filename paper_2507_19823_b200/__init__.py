@@ -41,7 +41,7 @@ class hc_vq(C.Structure):
 
 class hc_budget(C.Structure):
     _fields_ = [("tau", C.c_float), ("k_max", C.c_int64), ("renorm", C.c_int32),
-                ("select_only", C.c_int32)]
+                ("select_only", C.c_int32), ("shared_kv", C.c_int32)]
 
 
 class hc_kcache(C.Structure):
@@ -145,8 +145,11 @@ def profile_scan_events(begin, end):
                                         C.c_void_p(end.cuda_event) if end is not None else None))
 
 
-def budget(tau: float, k_max: int, renorm: bool = False, select_only: bool = False) -> hc_budget:
-    return hc_budget(float(tau), int(k_max), int(bool(renorm)), int(bool(select_only)))
+def budget(tau: float, k_max: int, renorm: bool = False, select_only: bool = False,
+           shared_kv: bool = False) -> hc_budget:
+    """R5 budget; shared_kv=True -> one selection per KV head (R8, include/hc.h)."""
+    return hc_budget(float(tau), int(k_max), int(bool(renorm)), int(bool(select_only)),
+                     int(bool(shared_kv)))
 
 
 # ----------------------------------------------------------------------------- encode

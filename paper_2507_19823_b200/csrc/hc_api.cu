@@ -102,11 +102,11 @@ struct Layout {
   int64_t z_stride;
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
-      o_rdone, total;
+      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, total;
   int nch_max;  // sharded compaction chunks
 };
 
-Layout make_layout(const hc_kcache *kc, int64_t k_max) {
+Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
   Layout L{};
   const int64_t B = kc->B, Hkv = kc->Hkv, G = kc->G, Hq = G * Hkv;
   const int64_t rows = B * Hq;
@@ -136,6 +136,12 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max) {
     const int64_t nchr = gather_rows_chunks(L.k_eff);
     L.o_rpart = o; o += align256((size_t)rows * nchr * 128 * 4);
     L.o_rdone = o; o += align256((size_t)rows * 4);
+    if (shared) {  // R8 shared selection state, 4-level histograms, chunk counts
+      L.o_grp = o; o += align256((size_t)units * sizeof(GroupState));
+      L.o_ghist = o; o += align256((size_t)units * 4 * kNB * 16);
+      L.o_gchunk = o; o += align256((size_t)units * grp_chunks(ncand_max > 0 ? ncand_max : 1) * 8);
+      L.o_gkey = o; o += align256((size_t)units * L.z_stride * 8);
+    }
   }
   L.total = o;
   return L;
@@ -286,7 +292,7 @@ hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const 
 
 size_t hc_decode_workspace_bytes(const hc_kcache *kc, hc_budget budget) {
   if (check_kcache(kc) != HC_OK) return 0;
-  return make_layout(kc, budget.k_max).total;
+  return make_layout(kc, budget.k_max, budget.shared_kv).total;
 }
 
 // validation + LayerArgs of one layer call (decode or a sharded phase)
@@ -312,7 +318,9 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
     return fail(HC_ERR_RANGE, "cache counts out of range");
   const int64_t n_cand = n_q + n_res;
   if (n_cand == 0) return fail(HC_ERR_EMPTY, "layer %d has no tokens", layer);
-  Lw = make_layout(kc, budget.k_max);
+  if (budget.shared_kv && budget.renorm)
+    return fail(HC_ERR_UNSUPPORTED, "shared_kv selection takes renorm = 0");
+  Lw = make_layout(kc, budget.k_max, budget.shared_kv);
   if (!ws || ws_bytes < Lw.total)
     return fail(HC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, Lw.total);
   uint8_t *w8 = (uint8_t *)ws;
@@ -365,6 +373,12 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   a.num_sms = num_sms();
   choose_scan(B * H, n_q, (int)g, Lw.cpow2, (int)G, a.num_sms, &a.scan_tpt, &a.scan_split, a.lut8);
   a.zpart = (float *)(w8 + Lw.o_zpart);
+  if (budget.shared_kv) {
+    a.grp = (GroupState *)(w8 + Lw.o_grp);
+    a.grp_hist = (unsigned long long *)(w8 + Lw.o_ghist);
+    a.grp_chunk = (uint32_t *)(w8 + Lw.o_gchunk);
+    a.grp_key = (unsigned long long *)(w8 + Lw.o_gkey);
+  }
 
   return HC_OK;
 }
@@ -401,13 +415,29 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
                   : (ev && !strcmp(ev, "rows")) ? 3 : 2;
   }
   const bool want_union = gather_mode == 1 || (gather_mode == 2 && a.v_placement == 1);
-  const bool union_gather = !budget.select_only && want_union && a.G > 1;
+  // shared per-KV-head selection (R8): the G rows keep one list -> always the union gather
+  const bool shared = budget.shared_kv != 0;
+  const bool union_gather = !budget.select_only && (want_union || shared) && a.G > 1;
   const bool want_rows = gather_mode == 3 || (gather_mode == 2 && a.v_placement == 0);
   const bool rows_gather = !budget.select_only && !union_gather && want_rows && a.d == 128;
-  if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
-                               (budget.select_only || union_gather || rows_gather) ? 0 : 1,
-                               a.num_sms, s,
-                               dbg && dbg->z ? 1 : 0)) != cudaSuccess)
+  if (shared) {
+    if ((e = launch_group_select(a, n_q > 0 ? a.scan_split : 1, s)) != cudaSuccess)
+      return cuda_check(e, "shared select");
+    if (!budget.select_only && !union_gather) {  // G == 1: per-row gather of the lists
+      uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);
+      if ((e = cudaMemsetAsync(done, 0, (size_t)rows * 4, s)) != cudaSuccess) return cuda_check(e, "memset");
+      const int64_t kc2 = a.k_max < n_cand ? a.k_max : n_cand;
+      if (a.d == 128) {
+        if ((e = launch_gather_rows(a, kc2, (float *)((uint8_t *)ws + Lw.o_rpart), done, s)) != cudaSuccess)
+          return cuda_check(e, "gather");
+      } else {
+        return fail(HC_ERR_UNSUPPORTED, "shared_kv with G = 1 needs d = 128");
+      }
+    }
+  } else if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
+                                      (budget.select_only || union_gather || rows_gather) ? 0 : 1,
+                                      a.num_sms, s,
+                                      dbg && dbg->z ? 1 : 0)) != cudaSuccess)
     return cuda_check(e, "select");
   if (rows_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);
@@ -449,6 +479,7 @@ static hc_status shard_prepare(const uint16_t *q, const hc_kcache *kc, const hc_
                                cudaStream_t s, bool need_q, LayerArgs &a, Layout &Lw, SelArgs &sa,
                                int32_t *sel_idx = nullptr, float *sel_w = nullptr,
                                int64_t *sel_k = nullptr) {
+  if (budget.shared_kv) return fail(HC_ERR_UNSUPPORTED, "sharded decode selects per query head (shared_kv = 0)");
   if (kc && kc->res_cap > 0 && kc->n_res[layer < 0 || layer >= HC_MAX_LAYERS ? 0 : layer] > 0)
     return fail(HC_ERR_UNSUPPORTED, "sharded decode does not take a resident window (n_res must be 0)");
   float dummy_out = 0.0f;

@@ -173,4 +173,19 @@ struct alignas(16) HeadState {
 };
 static_assert(sizeof(HeadState) == 128, "HeadState size");
 
+// per-(b, KV head) state of the shared selection (R8, hc_group.cu), in the workspace
+struct alignas(16) GroupState {
+  uint64_t SA;          // Σ_j A_j
+  uint64_t theta;       // Θ = ceil(τ_q·S_A / 2^24)
+  uint64_t ntot;        // candidates
+  uint64_t cb, mb;      // count / mass of the keys below the current prefix bucket
+  uint64_t prefix;      // fixed high bits of the boundary key D*
+  uint64_t dstar;       // exact boundary key (2^48 = keep all)
+  uint64_t r_ties;      // ties at D* kept (lowest indices)
+  int64_t ksel, kstar;
+  uint64_t rho[4];      // ρ_h = floor((2^104 - 1) / S_h)
+  int32_t done;         // boundary resolved
+  int32_t pad[3];
+};
+
 }  // namespace hc

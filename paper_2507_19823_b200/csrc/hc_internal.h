@@ -84,6 +84,11 @@ struct LayerArgs {
   int scan_tpt;           // tokens per thread in the scan (8 or 16)
   int scan_split;         // group splits per token tile (1 = write z directly)
   float *zpart;           // [scan_split][B*Hq][z_stride] partial sums when scan_split > 1
+  // shared per-KV-head selection (R8, hc_group.cu)
+  GroupState *grp;                 // [B*Hkv]
+  unsigned long long *grp_hist;    // [B*Hkv][4 levels][kNB][count, mass]
+  uint32_t *grp_chunk;             // [B*Hkv][chunks][strict, ties]
+  unsigned long long *grp_key;     // [B*Hkv][z_stride] order key D of every candidate
 };
 
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);
@@ -123,6 +128,10 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st);
+
+// R8 shared per-KV-head selection (hc_group.cu): sel_idx / sel_w / hs.ksel of the G rows
+int grp_chunks(int64_t n);
+cudaError_t launch_group_select(const LayerArgs &a, int nsplit, cudaStream_t st);
 
 // Eq. 5 with GQA union de-duplication (hc_gather.cu)
 int gather_union_chunks(int64_t n_cand);

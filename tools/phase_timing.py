@@ -7,6 +7,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     import torch
     import bench
     cfg = dict(bench.CONFIGS[CFG]); cfg["L"] = 2
+    cfg["shared_kv"] = os.environ.get("PT_SHARED", "0") == "1"
+    reps = int(os.environ.get("PT_REPS", "200" if CFG == 2 else "20"))
     wl = bench.Workload(cfg, "cuda")
     import paper_2507_19823_b200 as hc
     for _ in range(5):
@@ -14,7 +16,6 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    reps = 200 if CFG == 2 else 20
     for _ in range(reps):
         hc.decode_attention(wl.q[1], wl.kc, wl.vs, 1, wl.bud, out=wl.out[1], ws=wl.ws)
     e1.record(); torch.cuda.synchronize()
