@@ -62,6 +62,7 @@ def lib():
             L.or_select_float.argtypes = [p, i64, i32, f32, i64, i32, p, p, p]
             L.or_select_float.restype = i32
             L.or_gather.argtypes = [p, p, i64, p, i32, p]
+            L.or_kmeans_step.argtypes = [p, i64, i32, i32, i32, i32, p, i64, p, p, p]
             L.or_select_shared.argtypes = [p, i32, i64, p, i32, f32, i64, p, p, p, p, p, p]
             L.or_exact_attention.argtypes = [p, p, p, i64, i32, p]
             L.or_decode_unit.argtypes = [p, i32, i32, i32, i32, i32, p, p, i64, i64, p, p, p, i64,
@@ -91,6 +92,23 @@ def encode(keys, C_, g: int) -> np.ndarray:
     out = np.empty((rows, g), dtype=np.uint16)
     lib().or_encode(_ptr(keys.view(np.uint16)), rows, d, g, c, cbg, _ptr(C_), _ptr(out))
     return out
+
+
+def kmeans_step(keys, C_, counts, sample, g: int):
+    """f4: one MiniBatchKMeans step -> (new C [cbg][c][dbar] fp32, new counts
+    [cbg][c] int64, labels [b][g] u16).  Inputs are not modified."""
+    keys = _c(keys, np.float16)
+    C2 = np.array(C_, dtype=np.float32, order="C", copy=True)
+    v2 = np.array(counts, dtype=np.int64, order="C", copy=True)
+    sample = _c(sample, np.int64)
+    n_keys, d = keys.shape
+    cbg, c, dbar = C2.shape
+    lab = np.zeros((max(sample.shape[0], 1), g), np.uint16)
+    rc = lib().or_kmeans_step(_ptr(keys.view(np.uint16)), n_keys, d, g, c, cbg, _ptr(sample),
+                              sample.shape[0], _ptr(C2), _ptr(v2), _ptr(lab))
+    if rc:
+        raise ValueError(f"or_kmeans_step rc={rc}")
+    return C2, v2, lab[: sample.shape[0]]
 
 
 def reconstruct(codes, C_, d: int) -> np.ndarray:

@@ -87,6 +87,60 @@ OR_EXPORT void or_encode(const uint16_t *keys, int64_t rows, int d, int g, int c
     }
 }
 
+/* ------------------------------------------------------------------------
+ * f4 -- one MiniBatchKMeans step ("MiniBatchKMeans [Sculley 2010] implemented in
+ * Scikit-learn ... batch size of 10,000"; codebooks per group, §3.1).  Sculley's
+ * Alg. 1 with the per-centre learning rate 1/v, in its batched (scikit-learn) form:
+ *   1. labels: every sampled key's sub-vectors are assigned with the centres as they are
+ *      at the start of the step -- R1's nearest-centroid rule (or_encode);
+ *   2. per centre m of codebook slice ci: n_m = #assigned, s_m = Σ assigned sub-vectors;
+ *      if n_m > 0:  C_m <- (C_m·v_m + s_m) / (v_m + n_m),  v_m <- v_m + n_m
+ *      (= Alg. 1's sequential updates c <- (1-1/v)c + x/v over the batch).
+ * Arithmetic (DESIGN F4): s_m exact in int64 units of 2^-24 (every fp16 value is an
+ * integer multiple of 2^-24 below 2^16); the update in double, written as
+ *   q = ((double)C·(double)v + (double)s·2^-24) / (double)(v + n),  C = (float)q (RN).
+ * sample [b] = key row indices (the caller draws them); labels [b][g] (optional).
+ * ---------------------------------------------------------------------- */
+OR_EXPORT int or_kmeans_step(const uint16_t *keys, int64_t n_keys, int d, int g, int c, int cbg,
+                             const int64_t *sample, int64_t b, float *C, int64_t *counts,
+                             uint16_t *labels)
+{
+    const int dbar = d / g;
+    if (b <= 0) return 0;
+    uint16_t *batch = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)b * d);
+    uint16_t *lab = labels ? labels : (uint16_t *)malloc(sizeof(uint16_t) * (size_t)b * g);
+    for (int64_t s = 0; s < b; ++s) {
+        if (sample[s] < 0 || sample[s] >= n_keys) return 3;
+        memcpy(batch + s * d, keys + sample[s] * d, sizeof(uint16_t) * (size_t)d);
+    }
+    or_encode(batch, b, d, g, c, cbg, C, lab);
+    int64_t *S = (int64_t *)calloc((size_t)cbg * c * dbar, sizeof(int64_t));
+    int64_t *n = (int64_t *)calloc((size_t)cbg * c, sizeof(int64_t));
+    for (int64_t s = 0; s < b; ++s)
+        for (int i = 0; i < g; ++i) {
+            const int ci = cbg == 1 ? 0 : i;
+            const int m = lab[s * g + i];
+            n[(size_t)ci * c + m] += 1;
+            for (int e = 0; e < dbar; ++e)
+                S[((size_t)ci * c + m) * dbar + e] +=
+                    (int64_t)ldexp((double)or_h2f(batch[s * d + i * dbar + e]), 24);
+        }
+    for (int64_t cm = 0; cm < (int64_t)cbg * c; ++cm) {
+        if (!n[cm]) continue;
+        const int64_t v = counts[cm];
+        for (int e = 0; e < dbar; ++e) {
+            const double num = (double)C[cm * dbar + e] * (double)v + (double)S[cm * dbar + e] * 0x1p-24;
+            C[cm * dbar + e] = (float)(num / (double)(v + n[cm]));
+        }
+        counts[cm] = v + n[cm];
+    }
+    free(S);
+    free(n);
+    free(batch);
+    if (!labels) free(lab);
+    return 0;
+}
+
 /* Eq. 2 Q(K): row j = concat_i C[i][P[j][i]]. codes [n][g] row-major. */
 OR_EXPORT void or_reconstruct(const uint16_t *codes, int64_t n, int d, int g, int c, int cbg,
                               const float *C, float *out)

@@ -392,6 +392,84 @@ def test_select_float_spec_examples(orc):
     assert r["w"][0] == 1.0 and r["w"][1] == 0.0
 
 
+# ---------------------------------------------------------------- f4 MiniBatchKMeans step
+def test_kmeans_first_step_is_cluster_mean_and_matches_sklearn(orc):
+    """With v = 0 the step is one Lloyd iteration: every assigned centre becomes the mean of
+    its sub-vectors (float64 mean -> fp32, bit for bit) -- and matches scikit-learn's KMeans
+    (max_iter=1, the library P:356 uses) within fp32 rounding; unassigned centres stay."""
+    from sklearn.cluster import KMeans
+    rng = _rng(71)
+    d, g, c = 16, 4, 6
+    dbar = d // g
+    planted = rng.standard_normal((c, dbar)) * 4
+    X = (planted[rng.integers(0, c, 3000)] + rng.standard_normal((3000, dbar)) * 0.3)
+    keys = X.reshape(750, d).astype(np.float16)  # 750 keys x 4 groups, one shared codebook
+    C0 = (planted + rng.standard_normal((c, dbar)) * 0.5).astype(np.float32)[None]
+    C1, v1, lab = orc.kmeans_step(keys, C0, np.zeros((1, c), np.int64), np.arange(750), g)
+    sub = keys.astype(np.float64).reshape(-1, dbar)
+    labs = lab.reshape(-1)
+    for m in range(c):
+        pts = sub[labs == m]
+        assert v1[0, m] == len(pts)
+        if len(pts):
+            assert np.array_equal(C1[0, m], pts.mean(0).astype(np.float32))
+        else:
+            assert np.array_equal(C1[0, m], C0[0, m])
+    km = KMeans(n_clusters=c, init=C0[0].astype(np.float64), n_init=1, max_iter=1,
+                algorithm="lloyd").fit(sub)
+    # sklearn reports the centres after its iteration
+    assert np.allclose(km.cluster_centers_, C1[0], rtol=1e-5, atol=1e-5)
+
+
+def test_kmeans_equals_sequential_sculley(orc):
+    """The batched update equals Sculley's Alg. 1 (per-sample c <- (1 - 1/v)c + x/v with
+    assignments cached at the start of the batch) within fp32 rounding, per-group codebooks,
+    non-zero prior counts, repeated sample indices."""
+    rng = _rng(72)
+    d, g, c = 32, 8, 5
+    dbar = d // g
+    keys = rng.standard_normal((400, d)).astype(np.float16)
+    C0 = rng.standard_normal((g, c, dbar)).astype(np.float32)
+    v0 = rng.integers(0, 50, size=(g, c)).astype(np.int64)
+    sample = rng.integers(0, 400, size=300)
+    C1, v1, lab = orc.kmeans_step(keys, C0, v0, sample, g)
+    assert np.array_equal(lab, orc.encode(keys[sample], C0, g))
+    C = C0.astype(np.float64).copy()
+    v = v0.copy()
+    for s_, j in enumerate(sample):
+        for i in range(g):
+            m = int(lab[s_, i])
+            x = keys[j, i * dbar:(i + 1) * dbar].astype(np.float64)
+            v[i, m] += 1
+            eta = 1.0 / v[i, m]
+            C[i, m] = (1 - eta) * C[i, m] + eta * x
+    assert np.array_equal(v, v1)
+    assert np.allclose(C1, C, rtol=1e-6, atol=1e-6)
+    assert v1.sum() - v0.sum() == 300 * g
+
+
+def test_kmeans_converges_on_planted_clusters(orc):
+    """Repeated steps on keys drawn around planted centres recover them (MiniBatchKMeans
+    converges; the step is deterministic)."""
+    rng = _rng(73)
+    d, g, c = 8, 2, 4
+    dbar = d // g
+    planted = rng.standard_normal((g, c, dbar)) * 5
+    lab = rng.integers(0, c, size=(5000, g))
+    keys = np.concatenate([planted[i][lab[:, i]] for i in range(g)], 1)
+    keys = (keys + rng.standard_normal(keys.shape) * 0.05).astype(np.float16)
+    C = (planted + rng.standard_normal(planted.shape) * 1.0).astype(np.float32)
+    v = np.zeros((g, c), np.int64)
+    for it in range(20):
+        C, v, _ = orc.kmeans_step(keys, C, v, rng.integers(0, 5000, size=500), g)
+    for i in range(g):
+        err = np.linalg.norm(np.sort(C[i], 0) - np.sort(planted[i], 0))
+        assert err < 0.1
+    a = orc.kmeans_step(keys, C, v, np.arange(100), g)
+    b = orc.kmeans_step(keys, C, v, np.arange(100), g)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
 # ---------------------------------------------------------------- R8 shared selection (f3(iii))
 def _shared_A(orc, z, e, d=128):
     """Â_{h,j} = floor(W_{h,j}·ρ_h / 2^64), ρ_h = floor((2^104-1)/S_h), A_j = Σ_h Â_{h,j} in
