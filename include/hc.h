@@ -155,6 +155,23 @@ hc_status hc_codebook_absmax(const float *codebook, hc_vq vq, int32_t L, float *
 hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *codebook, hc_vq vq,
                            uint16_t *codes, int64_t code_stride, hc_stream_t stream);
 
+/* NEXT f4 -- codebook training: ONE MiniBatchKMeans step ("MiniBatchKMeans ...
+ * batch size of 10,000"; Sculley 2010 Alg. 1 in its batched scikit-learn form, DESIGN F4):
+ *   labels[i*b + s] = R1 nearest centroid of keys[sample[s]]'s group-i sub-vector under the
+ *   codebook as it is at the start of the step; then for every centroid m of slice ci with
+ *   n_m > 0 assigned sub-vectors summing to s_m:
+ *     C_m <- (C_m·v_m + s_m) / (v_m + n_m)   (double, then fp32 round-to-nearest),
+ *     v_m <- v_m + n_m.
+ * keys [n_keys][d] fp16 (device); sample [b] int64 key-row indices (device; rows outside
+ * [0, n_keys) are skipped, label 0xFFFF); codebook [cbg][c][dbar] fp32 and counts [cbg][c]
+ * int64 (device, updated in place; counts start at 0 for a fresh codebook); labels [g][b]
+ * u16 (device, optional).  s_m is summed exactly (int64 units of 2^-24), so the result
+ * is independent of thread order.  ws >= hc_kmeans_workspace_bytes(vq, b). */
+size_t hc_kmeans_workspace_bytes(hc_vq vq, int64_t b);
+hc_status hc_kmeans_step(const uint16_t *keys, int64_t n_keys, const int64_t *sample, int64_t b,
+                         hc_vq vq, float *codebook, int64_t *counts, uint16_t *labels, void *ws,
+                         size_t ws_bytes, hc_stream_t stream);
+
 /* Append one decode token for layer `layer` (all B sequences, all Hkv heads).
  * k_new, v_new [B][Hkv][d] fp16.  With res_cap == 0 the key is encoded (R1) into
  * codes at position n_q[layer] and v is written to the value store there.  With a

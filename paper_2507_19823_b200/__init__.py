@@ -25,7 +25,8 @@ EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_ev
            "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
            "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
            "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
-           "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish"]
+           "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish", "hc_kmeans_workspace_bytes",
+           "hc_kmeans_step"]
 
 
 class HcError(RuntimeError):
@@ -99,6 +100,10 @@ def lib():
         L.hc_host_weighted_sum.restype = i32
         L.hc_enqueue_host_weighted_sum.argtypes = hw + [p]
         L.hc_enqueue_host_weighted_sum.restype = i32
+        L.hc_kmeans_workspace_bytes.argtypes = [hc_vq, i64]
+        L.hc_kmeans_workspace_bytes.restype = C.c_size_t
+        L.hc_kmeans_step.argtypes = [p, i64, p, i64, hc_vq, p, p, p, p, C.c_size_t, p]
+        L.hc_kmeans_step.restype = i32
         KC, VS = C.POINTER(hc_kcache), C.POINTER(hc_vstore)
         L.hc_shard_workspace_bytes.argtypes = [KC, hc_budget]
         L.hc_shard_workspace_bytes.restype = C.c_size_t
@@ -165,6 +170,49 @@ def quantize_keys(keys, codebook, g: int, codes=None, stream=None):
                                 codes.shape[1], _stream(stream))
     _check(st)
     return codes
+
+
+def kmeans_step(keys, sample, codebook, counts, g: int, labels=None, ws=None, stream=None):
+    """f4: one MiniBatchKMeans step on the GPU (include/hc.h hc_kmeans_step).
+    keys fp16 [n_keys][d], sample int64 [b] (cuda), codebook fp32 [cbg][c][d/g] and counts
+    int64 [cbg][c] updated in place; labels int16-view-of-u16 [g][b] (optional)."""
+    import torch
+    n_keys, d = keys.shape
+    cbg, c, dbar = codebook.shape
+    b = sample.shape[0]
+    vq = hc_vq(d, g, c, cbg)
+    if ws is None:
+        ws = Workspace(int(lib().hc_kmeans_workspace_bytes(vq, b)), keys.device)
+    st = lib().hc_kmeans_step(_ptr(keys), n_keys, _ptr(sample), b, vq, _ptr(codebook),
+                              _ptr(counts), _ptr(labels) if labels is not None else None,
+                              _ptr(ws.t), ws.nbytes, _stream(stream))
+    _check(st)
+    return codebook, counts
+
+
+def train_codebook(keys, g: int, c: int, iters: int = 200, batch: int = 10000, seed: int = 0,
+                   cbg=None, init=None):
+    """MiniBatchKMeans codebook training (max 200 iterations, batch 10,000) from the
+    key matrix keys fp16 [N][d] (cuda).  init: fp32 [cbg][c][d/g] (default: the sub-vectors
+    of c seeded distinct key rows).  Batches are seeded splitmix64 draws (synth)."""
+    import numpy as np
+    import torch
+
+    import synth
+    N, d = keys.shape
+    cbg = g if cbg is None else cbg
+    dbar = d // g
+    if init is None:
+        rows = synth.sample_rows(seed, 0, N, c)
+        k0 = keys[torch.from_numpy(rows).to(keys.device)].float().view(c, g, dbar)
+        init = (k0.permute(1, 0, 2).contiguous() if cbg == g else k0[:, 0, :].unsqueeze(0).contiguous())
+    C_ = init.clone().float().contiguous()
+    counts = torch.zeros((cbg, c), dtype=torch.int64, device=keys.device)
+    ws = Workspace(int(lib().hc_kmeans_workspace_bytes(hc_vq(d, g, c, cbg), batch)), keys.device)
+    for it in range(iters):
+        sample = torch.from_numpy(synth.sample_rows(seed, 1 + it, N, batch).astype(np.int64)).to(keys.device)
+        kmeans_step(keys, sample, C_, counts, g, ws=ws)
+    return C_, counts
 
 
 # ----------------------------------------------------------------------------- caches

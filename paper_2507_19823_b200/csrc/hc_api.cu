@@ -226,7 +226,47 @@ hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *code
   a.codes = codes;
   a.omap = RowMap{1, 1, 0, 0};
   a.gstride = code_stride;
-  return cuda_check(launch_encode(a, (cudaStream_t)stream), "hc_quantize_keys");
+  // many rows (prefill): shared-memory-staged bulk kernel; few rows (decode): k_encode
+  return cuda_check(rows >= 1024 ? launch_encode_bulk(a, (cudaStream_t)stream)
+                                 : launch_encode(a, (cudaStream_t)stream),
+                    "hc_quantize_keys");
+}
+
+size_t hc_kmeans_workspace_bytes(hc_vq vq, int64_t b) {
+  if (check_vq(vq) != HC_OK || b < 0) return 0;
+  const size_t cc = (size_t)vq.cbg * vq.c, dbar = (size_t)(vq.d / vq.g);
+  return align256(cc * 8) + align256(cc * dbar * 8) + align256((size_t)vq.g * (size_t)(b > 0 ? b : 1) * 2);
+}
+
+hc_status hc_kmeans_step(const uint16_t *keys, int64_t n_keys, const int64_t *sample, int64_t b,
+                         hc_vq vq, float *codebook, int64_t *counts, uint16_t *labels, void *ws,
+                         size_t ws_bytes, hc_stream_t stream) {
+  hc_status st = check_vq(vq);
+  if (st) return st;
+  if (b < 0 || n_keys < 0) return fail(HC_ERR_ARG, "b < 0 or n_keys < 0");
+  if (b == 0) return HC_OK;
+  if (!keys || !sample || !codebook || !counts) return fail(HC_ERR_ARG, "NULL pointer");
+  if (b > 0x7fffffff) return fail(HC_ERR_UNSUPPORTED, "b > 2^31-1");
+  const size_t need = hc_kmeans_workspace_bytes(vq, b);
+  if (!ws || ws_bytes < need) return fail(HC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+  const size_t cc = (size_t)vq.cbg * vq.c, dbar = (size_t)(vq.d / vq.g);
+  uint8_t *w8 = (uint8_t *)ws;
+  unsigned long long *n = (unsigned long long *)w8;
+  unsigned long long *S = (unsigned long long *)(w8 + align256(cc * 8));
+  uint16_t *lab = labels ? labels : (uint16_t *)(w8 + align256(cc * 8) + align256(cc * dbar * 8));
+  EncodeArgs a{};
+  a.keys = keys;
+  a.kmap = RowMap{1, vq.d, 0, 0};
+  a.rows = b;
+  a.C = codebook;
+  a.d = vq.d; a.g = vq.g; a.c = vq.c; a.cbg = vq.cbg;
+  a.codes = lab;
+  a.omap = RowMap{1, 1, 0, 0};
+  a.gstride = b;
+  a.kidx = sample;
+  a.n_keys = n_keys;
+  return cuda_check(launch_kmeans_step(a, sample, b, codebook, counts, n, S, (cudaStream_t)stream),
+                    "hc_kmeans_step");
 }
 
 hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const uint16_t *k_new,

@@ -32,8 +32,17 @@ struct EncodeArgs {
   RowMap vsmap;
   uint16_t *vdst;
   RowMap vdmap;
+  // bulk encode only: optional row gather (key row of r = kidx[r], valid if < n_keys)
+  const int64_t *kidx;
+  int64_t n_keys;
 };
 cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s);
+// many rows: codebook slice staged in shared memory, rows per thread (hc_kmeans.cu)
+cudaError_t launch_encode_bulk(const EncodeArgs &a, cudaStream_t s);
+// f4: one MiniBatchKMeans step; enc.codes = labels [g][b], enc.kidx = sample
+cudaError_t launch_kmeans_step(const EncodeArgs &enc, const int64_t *sample, int64_t b, float *C,
+                               int64_t *counts, unsigned long long *n, unsigned long long *S,
+                               cudaStream_t st);
 
 struct RowCopyArgs {
   const uint16_t *src;

@@ -32,7 +32,7 @@ _C2 = np.uint64(0x94D049BB133111EB)
 IH4_STD = 37837.22652  # sqrt((2**32 - 1) / 3)
 
 # stream tags (tensor kinds)
-TAG_P, TAG_V, TAG_Q, TAG_C, TAG_K, TAG_RK, TAG_RV = 1, 2, 3, 4, 5, 6, 7
+TAG_P, TAG_V, TAG_Q, TAG_C, TAG_K, TAG_RK, TAG_RV, TAG_S = 1, 2, 3, 4, 5, 6, 7, 8
 
 BASE_SEED = 0x48434154  # "HCAT"
 
@@ -137,3 +137,10 @@ def planted_keys(seed: int, rows: int, d: int, g: int, clusters: int, cbg_c: int
     for i in range(g):
         keys[:, i * dbar:(i + 1) * dbar] = centres[i][a[:, i]].astype(np.float16)
     return keys, cb, a
+
+
+def sample_rows(seed: int, it: int, N: int, count: int) -> np.ndarray:
+    """Row indices in [0, N) for k-means batch `it` (with replacement) -> int64 [count]."""
+    u = u64(stream_key(seed, TAG_S, it), 0, count)
+    with np.errstate(over="ignore"):
+        return (((u >> np.uint64(32)) * np.uint64(N)) >> np.uint64(32)).astype(np.int64)
