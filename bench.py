@@ -277,6 +277,18 @@ class Workload:
         return g, launches
 
 
+class EagerStep:
+    """Stand-in for a captured graph (replay = run the step eagerly); counts are reset so
+    every replay appends at the same position, like the graph."""
+
+    def __init__(self, wl, fn):
+        self.wl, self.fn = wl, fn
+
+    def replay(self):
+        self.wl.reset_counts()
+        self.fn()
+
+
 def event_ms(b, e) -> float:
     """cudaEventElapsedTime for events recorded by the library inside the graph (torch's
     Event object does not know they were recorded, so ask the driver directly)."""
@@ -540,8 +552,22 @@ def main():
     wl.reset_counts()
     wl.step()
     torch.cuda.synchronize()
-    g_step, launches_per_step = wl.capture(lambda: wl.step(profile=True))
-    g_e2e, _ = wl.capture(wl.step_e2e)
+    graph_mode = "one CUDA graph per step (32 x append + decode)"
+    try:
+        g_step, launches_per_step = wl.capture(lambda: wl.step(profile=True))
+        g_e2e, _ = wl.capture(wl.step_e2e)
+    except Exception as ex:  # e.g. a collective backend that refuses graph capture
+        if not sharded_mode:
+            raise
+        torch.cuda.synchronize()
+        graph_mode = f"eager steps (graph capture failed: {type(ex).__name__})"
+        g_step, launches_per_step = EagerStep(wl, lambda: wl.step(profile=True)), None
+        g_e2e = EagerStep(wl, wl.step_e2e)
+        import paper_2507_19823_b200 as hc
+        before = hc.launch_count()
+        g_step.replay()
+        torch.cuda.synchronize()
+        launches_per_step = hc.launch_count() - before
 
     with ClockSampler(local) as clk:
         ms = time_graph(g_step, args.steps, args.warmup, dist)
@@ -588,7 +614,7 @@ def main():
                                    ("replicas" if world > 1 else "single")),
                    "l2": f"inputs > L2: P = {B * L * H * n * g * 2 / 1e9:.2f} GB/step, V = "
                          f"{B * L * H * n * d * 2 / 1e9:.2f} GB",
-                   "graph": "one CUDA graph per step (32 x append + decode)"},
+                   "graph": graph_mode},
         "quantized_key_gbs": achieved,
         "quantized_key_frac_hbm": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -260,6 +260,146 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
 }
 
 // ---------------------------------------------------------------------------------------
+// Cross-tile pipelined variant of k_scan<G, TPT, RC = 1> (the default).  The CTA's work is
+// one stream of (item, group) steps:
+//  * table slices live in a 3-slot ring filled by bulk copies (TMA engine) on "full"
+//    mbarriers; there is NO CTA-wide barrier per group: each warp, after its lookups in
+//    slot s%3, bumps a shared counter, and the LAST warp to finish the slot refills it
+//    with step s+3's slice -- warps drift up to two steps apart instead of draining at a
+//    __syncthreads every group;
+//  * each thread prefetches its code registers two steps ahead;
+//  * both prefetchers run across item boundaries, so the next tile's slices and codes are
+//    in flight while this tile's scores are stored.
+// Same arithmetic, same z.
+struct ScanCursor {
+  int item, i, ng;
+  const uint16_t *P;  // this thread's code pointer at group i0 of `item`
+  const uint8_t *T;   // table slice of group i0 of `item`
+  int64_t tile0;
+};
+
+template <int G, int TPT>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int tiles_per_unit,
+                                                                int total_tiles, int nsplit) {
+  constexpr int kChunks = TPT / 8;
+  constexpr int kTile = kScanThreads * TPT;
+  constexpr int kSlots = 3;
+  constexpr uint32_t kWarps = kScanThreads / 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t slice_bytes = (uint32_t)a.cpow2 * G * 2;
+  uint8_t *tbuf = smem;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSlots * slice_bytes);
+  __shared__ uint32_t s_done[kSlots];
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < kSlots; ++j) { mbar_init(&full[j], 1); s_done[j] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if ((int)blockIdx.x >= total_tiles) return;
+  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int woff = warp * (32 * TPT);  // this warp's first token inside a tile
+  const int gper = (a.g + nsplit - 1) / nsplit;
+
+  auto cset = [&](ScanCursor &c, int item) {
+    c.item = item;
+    c.i = 0;
+    if (item < total_tiles) {
+      const int sp = item % nsplit, tile = item / nsplit;
+      const int u = tile / tiles_per_unit, tk = tile - u * tiles_per_unit;
+      const int i0 = sp * gper;
+      c.ng = min(a.g, i0 + gper) - i0;
+      const int b = u / a.Hkv, kv = u - b * a.Hkv;
+      c.tile0 = (int64_t)tk * kTile;
+      c.P = a.codes + (int64_t)b * a.code_b_stride + ((int64_t)kv * a.g + i0) * a.n_cap + c.tile0 +
+            woff + lane * 8;
+      c.T = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
+    }
+  };
+  auto cadv = [&](ScanCursor &c) {
+    if (++c.i >= c.ng) cset(c, c.item + gridDim.x);
+  };
+  auto ccodes = [&](const ScanCursor &c, uint4 (&r)[kChunks]) {
+    const bool live = c.item < total_tiles;
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      const bool v = live && c.tile0 + woff + k * 256 + lane * 8 < a.n_q;
+      r[k] = v ? ld_stream(c.P + (int64_t)c.i * a.n_cap + k * 256) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto cslice = [&](const ScanCursor &c, int slot) {  // one thread: bulk-copy c's slice
+    if (c.item < total_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&full[slot], slice_bytes);
+      bulk_g2s(tbuf + slot * slice_bytes, c.T + (int64_t)c.i * slice_bytes, slice_bytes, &full[slot]);
+    }
+  };
+  ScanCursor lc, lt;  // code cursor: step + 2; table cursor: step + 3
+  cset(lc, blockIdx.x);
+  cset(lt, blockIdx.x);
+  uint4 rc0[kChunks], rc1[kChunks];
+  ccodes(lc, rc0);
+  cadv(lc);
+  ccodes(lc, rc1);
+  cadv(lc);
+  for (int j = 0; j < kSlots; ++j) {
+    if (threadIdx.x == 0) cslice(lt, j);
+    cadv(lt);
+  }
+
+  uint32_t ph = 0;  // phase bit per slot
+  int slot = 0;
+  for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
+    const int sp = item % nsplit, tile = item / nsplit;
+    const int u = tile / tiles_per_unit, tk = tile - u * tiles_per_unit;
+    const int i0 = sp * gper;
+    const int ng = min(a.g, i0 + gper) - i0;
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int64_t tile0 = (int64_t)tk * kTile;
+    int acc[kChunks][8][G];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+      for (int u8 = 0; u8 < 8; ++u8)
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[k][u8][h] = 0;
+    for (int i = 0; i < ng; ++i) {
+      uint4 rc2[kChunks];
+      ccodes(lc, rc2);  // step + 2 (possibly the next item's)
+      cadv(lc);
+      mbar_wait(&full[slot], (ph >> slot) & 1u);
+      ph ^= 1u << slot;
+      const uint8_t *sb = tbuf + slot * slice_bytes;
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) lookup8<G>(rc0[k], sb, mask, acc[k]);
+      // release the slot: the last warp out refills it with step + 3
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        const uint32_t old = atomicAdd(&s_done[slot], 1u);
+        if (old == kWarps - 1) {
+          s_done[slot] = 0;
+          __threadfence_block();
+          cslice(lt, slot);
+        }
+      }
+      cadv(lt);
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) { rc0[k] = rc1[k]; rc1[k] = rc2[k]; }
+      slot = slot == kSlots - 1 ? 0 : slot + 1;
+    }
+    int mx[G], mn[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
+    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k)
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
+    if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // 8-bit table variant (R2b): one 4-byte LDS per (token, group) -- 3.5 instead of
 // 6.15 shared-memory wavefronts per warp lookup -- and SWAR accumulation: the entry holds
 // the 4 heads as (int8 + 128) bytes; acc_e += w & 0x00FF00FF (heads 0, 2), acc_o +=
@@ -381,6 +521,49 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
 }
 
 template <int G, int TPT, int RC>
+static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s);
+
+static int scan_pipelined() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_SCAN_PIPE");
+    v = (ev && !strcmp(ev, "0")) ? 0 : 1;
+  }
+  return v;
+}
+
+template <int G, int TPT>
+static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
+  constexpr int kTile = kScanThreads * TPT;
+  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
+  const int units = a.B * a.Hkv;
+  const int nsplit = a.scan_split;
+  const int total = tiles_per_unit * units * nsplit;
+  if (total == 0) return cudaSuccess;
+  const size_t smem = (size_t)3 * a.cpow2 * G * 2 + 3 * 8;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan_pipe<G, TPT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+    if (e != cudaSuccess) return e;
+    configured[dev] = 1;
+  }
+  const int grid = total < a.num_sms ? total : a.num_sms;
+  cudaEvent_t eb, ee;
+  scan_events(&eb, &ee);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
+  k_scan_pipe<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  note_launch();
+  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
+  return cudaGetLastError();
+}
+
+template <int G, int TPT, int RC>
 static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   constexpr int kTile = kScanThreads * TPT;
   const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
@@ -423,6 +606,8 @@ static int scan_codes_in_regs() {
 template <int G>
 static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
   const int rc = scan_codes_in_regs();
+  if (rc && scan_pipelined())
+    return a.scan_tpt == 8 ? scan_pipe_launch<G, 8>(a, s) : scan_pipe_launch<G, 16>(a, s);
   if (a.scan_tpt == 8) return rc ? scan_launch<G, 8, 1>(a, s) : scan_launch<G, 8, 0>(a, s);
   return rc ? scan_launch<G, 16, 1>(a, s) : scan_launch<G, 16, 0>(a, s);
 }
