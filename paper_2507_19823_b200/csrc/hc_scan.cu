@@ -327,9 +327,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
       r[k] = v ? ld_stream(c.P + (int64_t)c.i * a.n_cap + k * 256) : make_uint4(0, 0, 0, 0);
     }
   };
-  auto cslice = [&](const ScanCursor &c, int slot) {  // one thread: bulk-copy c's slice
+  // one thread: bulk-copy c's slice into `slot`.  No proxy fence: every generic read of the
+  // slot has returned its data before the refilling warp observes the last release (see
+  // below), and a fence.proxy.async would also stall on this thread's in-flight loads.
+  auto cslice = [&](const ScanCursor &c, int slot) {
     if (c.item < total_tiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&full[slot], slice_bytes);
       bulk_g2s(tbuf + slot * slice_bytes, c.T + (int64_t)c.i * slice_bytes, slice_bytes, &full[slot]);
     }
@@ -372,14 +374,32 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
       const uint8_t *sb = tbuf + slot * slice_bytes;
 #pragma unroll
       for (int k = 0; k < kChunks; ++k) lookup8<G>(rc0[k], sb, mask, acc[k]);
-      // release the slot: the last warp out refills it with step + 3
+      // Release the slot; the last warp out refills it with step + 3.  Every lookup result
+      // has been consumed (the empty asm statements take all accumulators as inputs), so
+      // this warp's reads of the slot are complete before its counter increment issues.
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+        for (int u8 = 0; u8 < 8; u8 += 2) {
+          if constexpr (G == 4)
+            asm volatile("" ::"r"(acc[k][u8][0]), "r"(acc[k][u8][1]), "r"(acc[k][u8][2]), "r"(acc[k][u8][3]),
+                         "r"(acc[k][u8 + 1][0]), "r"(acc[k][u8 + 1][1]), "r"(acc[k][u8 + 1][2]),
+                         "r"(acc[k][u8 + 1][3]));
+          else if constexpr (G == 2)
+            asm volatile("" ::"r"(acc[k][u8][0]), "r"(acc[k][u8][1]), "r"(acc[k][u8 + 1][0]),
+                         "r"(acc[k][u8 + 1][1]));
+          else
+            asm volatile("" ::"r"(acc[k][u8][0]), "r"(acc[k][u8 + 1][0]));
+        }
       __syncwarp();
       if (lane == 0) {
-        __threadfence_block();
-        const uint32_t old = atomicAdd(&s_done[slot], 1u);
+        uint32_t old;
+        asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "r"(smem_u32(&s_done[slot]))
+                     : "memory");
         if (old == kWarps - 1) {
-          s_done[slot] = 0;
-          __threadfence_block();
+          asm volatile("st.relaxed.cta.shared::cta.u32 [%0], 0;" ::"r"(smem_u32(&s_done[slot])) : "memory");
           cslice(lt, slot);
         }
       }
