@@ -21,6 +21,10 @@
 namespace hc {
 
 constexpr int kScanThreads = 512;
+#ifndef HC_LOOKUP_BATCH
+#define HC_LOOKUP_BATCH 1
+#endif
+constexpr bool kLookupBatch = HC_LOOKUP_BATCH;
 
 __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
   uint4 v;
@@ -32,14 +36,19 @@ __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
 
 template <int G>
 struct Lut;
+// Head pairs share a 32-bit word w = (odd head, signed) << 16 | (even head + 32768) (k_table).
+// The even accumulator sums whole words (mod 2^32), the odd one w >> 16 (= the odd head,
+// exactly, since the biased low field is in [1, 65535]); unbias() recovers
+// Σ even = Σ w - 2^16·Σ odd - 32768·ng -- two integer adds per pair instead of three.
+__device__ __forceinline__ int wadd(int acc, uint32_t w) { return (int)((uint32_t)acc + w); }
 template <>
 struct Lut<4> {  // 8-byte entries: 4 x int16
   static constexpr int kShift = 3;
   __device__ __forceinline__ static void add(const uint8_t *sb, uint32_t off, int (&acc)[4]) {
     const uint2 v = *reinterpret_cast<const uint2 *>(sb + off);
-    acc[0] += (int)(int16_t)(v.x & 0xffffu);
+    acc[0] = wadd(acc[0], v.x);
     acc[1] += ((int)v.x) >> 16;
-    acc[2] += (int)(int16_t)(v.y & 0xffffu);
+    acc[2] = wadd(acc[2], v.y);
     acc[3] += ((int)v.y) >> 16;
   }
 };
@@ -48,10 +57,20 @@ struct Lut<2> {
   static constexpr int kShift = 2;
   __device__ __forceinline__ static void add(const uint8_t *sb, uint32_t off, int (&acc)[2]) {
     const uint32_t v = *reinterpret_cast<const uint32_t *>(sb + off);
-    acc[0] += (int)(int16_t)(v & 0xffffu);
+    acc[0] = wadd(acc[0], v);
     acc[1] += ((int)v) >> 16;
   }
 };
+template <int G>
+__device__ __forceinline__ void unbias(int (&acc)[8][G], int ng) {
+  if constexpr (G >= 2) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+#pragma unroll
+      for (int h = 0; h < G; h += 2)
+        acc[t][h] = (int)((uint32_t)acc[t][h] - ((uint32_t)acc[t][h + 1] << 16) - 32768u * (uint32_t)ng);
+  }
+}
 template <>
 struct Lut<1> {
   static constexpr int kShift = 1;
@@ -62,9 +81,31 @@ struct Lut<1> {
 
 // 8 codes (one uint4) -> 8 tokens' accumulators.  Codes are masked to cpow2-1, so
 // any 16-bit pattern stays inside the slice (valid codes are < c <= cpow2).
+// all 8 table words of a chunk loaded before any is consumed (8 LDS in flight per warp)
+__device__ __forceinline__ void lookup8_g4(const uint4 &c, const uint8_t *sb, uint32_t mask,
+                                           int (&acc)[8][4]) {
+  const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+  uint2 v[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[2 * q] = *reinterpret_cast<const uint2 *>(sb + ((w[q] << 3) & mask));
+    v[2 * q + 1] = *reinterpret_cast<const uint2 *>(sb + ((w[q] >> 13) & mask));
+  }
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    acc[t][0] = wadd(acc[t][0], v[t].x);
+    acc[t][1] += ((int)v[t].x) >> 16;
+    acc[t][2] = wadd(acc[t][2], v[t].y);
+    acc[t][3] += ((int)v[t].y) >> 16;
+  }
+}
+
 template <int G>
 __device__ __forceinline__ void lookup8(const uint4 &c, const uint8_t *sb, uint32_t mask,
                                         int (&acc)[8][G]) {
+  if constexpr (G == 4) {
+    if (kLookupBatch) { lookup8_g4(c, sb, mask, acc); return; }
+  }
   const uint32_t w[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -253,8 +294,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
     float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
 #pragma unroll
-    for (int k = 0; k < kChunks; ++k)
+    for (int k = 0; k < kChunks; ++k) {
+      unbias<G>(acc[k], ng);
       store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
+    }
     if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
 }
@@ -413,8 +456,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
     float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
 #pragma unroll
-    for (int k = 0; k < kChunks; ++k)
+    for (int k = 0; k < kChunks; ++k) {
+      unbias<G>(acc[k], ng);
       store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
+    }
     if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
 }
@@ -518,6 +563,145 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
         }
       }
       ci = ci == 2 ? 0 : ci + 1;
+    }
+    const int bias = 128 * ng;
+    int mx[G], mn[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
+    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      int acc[8][G];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        acc[t][0] = (int)(ae[k][t] & 0xffffu) - bias;
+        acc[t][2] = (int)(ae[k][t] >> 16) - bias;
+        acc[t][1] = (int)(ao[k][t] & 0xffffu) - bias;
+        acc[t][3] = (int)(ao[k][t] >> 16) - bias;
+      }
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn);
+    }
+    if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
+  }
+}
+
+// Pipelined 8-bit variant (same scheme as k_scan_pipe): a 3-slot ring of (table slice,
+// code strip) pairs filled by bulk copies on one "full" mbarrier per slot, released by the
+// last warp out, prefetch across item boundaries.
+template <int TPT>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan8_pipe(LayerArgs a, int tiles_per_unit,
+                                                                 int total_tiles, int nsplit) {
+  constexpr int G = 4;
+  constexpr int kChunks = TPT / 8;
+  constexpr int kTile = kScanThreads * TPT;
+  constexpr uint32_t kCodeBytes = kTile * 2;
+  constexpr int kSlots = 3;
+  constexpr uint32_t kWarps = kScanThreads / 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t slice_bytes = (uint32_t)a.cpow2 * 4;
+  uint8_t *tbuf = smem;
+  uint8_t *cbuf = smem + kSlots * slice_bytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(cbuf + kSlots * kCodeBytes);
+  __shared__ uint32_t s_done[kSlots];
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < kSlots; ++j) { mbar_init(&full[j], 1); s_done[j] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if ((int)blockIdx.x >= total_tiles) return;
+  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int woff = warp * (32 * TPT);
+  const int gper = (a.g + nsplit - 1) / nsplit;
+  int lt_item = blockIdx.x, lt_i = 0, lt_ng = 0;
+  const uint16_t *lt_P = nullptr;
+  const uint8_t *lt_T = nullptr;
+  uint32_t lt_cbytes = 0;
+  auto lset = [&](int item) {
+    lt_item = item;
+    lt_i = 0;
+    if (item < total_tiles) {
+      const int sp = item % nsplit, tile = item / nsplit;
+      const int u = tile / tiles_per_unit, tk = tile - u * tiles_per_unit;
+      const int i0 = sp * gper;
+      lt_ng = min(a.g, i0 + gper) - i0;
+      const int b = u / a.Hkv, kv = u - b * a.Hkv;
+      const int64_t tile0 = (int64_t)tk * kTile;
+      const int64_t avail = a.n_cap - tile0;
+      lt_cbytes = (uint32_t)(avail < kTile ? avail : kTile) * 2;
+      lt_P = a.codes + (int64_t)b * a.code_b_stride + ((int64_t)kv * a.g + i0) * a.n_cap + tile0;
+      lt_T = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
+    }
+  };
+  auto ladv = [&]() {
+    if (++lt_i >= lt_ng) lset(lt_item + gridDim.x);
+  };
+  auto lfill = [&](int slot) {  // one thread: table slice + code strip of the lookahead step
+    if (lt_item < total_tiles) {
+      mbar_expect_tx(&full[slot], slice_bytes + lt_cbytes);
+      bulk_g2s(tbuf + slot * slice_bytes, lt_T + (int64_t)lt_i * slice_bytes, slice_bytes, &full[slot]);
+      bulk_g2s(cbuf + slot * kCodeBytes, lt_P + (int64_t)lt_i * a.n_cap, lt_cbytes, &full[slot]);
+    }
+  };
+  lset(blockIdx.x);
+  for (int j = 0; j < kSlots; ++j) {
+    if (threadIdx.x == 0) lfill(j);
+    ladv();
+  }
+  uint32_t ph = 0;
+  int slot = 0;
+  for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
+    const int sp = item % nsplit, tile = item / nsplit;
+    const int u = tile / tiles_per_unit, tk = tile - u * tiles_per_unit;
+    const int i0 = sp * gper;
+    const int ng = min(a.g, i0 + gper) - i0;
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int64_t tile0 = (int64_t)tk * kTile;
+    uint32_t ae[kChunks][8], ao[kChunks][8];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { ae[k][t] = 0u; ao[k][t] = 0u; }
+    for (int i = 0; i < ng; ++i) {
+      mbar_wait(&full[slot], (ph >> slot) & 1u);
+      ph ^= 1u << slot;
+      const uint8_t *sb = tbuf + slot * slice_bytes;
+      const uint8_t *cs = cbuf + slot * kCodeBytes + (size_t)woff * 2;
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const uint4 c = *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
+        const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t e0 = *reinterpret_cast<const uint32_t *>(sb + ((w4[q] << 2) & mask));
+          const uint32_t e1 = *reinterpret_cast<const uint32_t *>(sb + ((w4[q] >> 14) & mask));
+          ae[k][2 * q] += e0 & 0x00FF00FFu;
+          ao[k][2 * q] += (e0 >> 8) & 0x00FF00FFu;
+          ae[k][2 * q + 1] += e1 & 0x00FF00FFu;
+          ao[k][2 * q + 1] += (e1 >> 8) & 0x00FF00FFu;
+        }
+      }
+      // every read of the slot (codes and table) has been consumed by the adds above
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k)
+        asm volatile("" ::"r"(ae[k][0]), "r"(ae[k][1]), "r"(ae[k][2]), "r"(ae[k][3]), "r"(ae[k][4]),
+                     "r"(ae[k][5]), "r"(ae[k][6]), "r"(ae[k][7]), "r"(ao[k][0]), "r"(ao[k][1]),
+                     "r"(ao[k][2]), "r"(ao[k][3]), "r"(ao[k][4]), "r"(ao[k][5]), "r"(ao[k][6]),
+                     "r"(ao[k][7]));
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t old;
+        asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "r"(smem_u32(&s_done[slot]))
+                     : "memory");
+        if (old == kWarps - 1) {
+          asm volatile("st.relaxed.cta.shared::cta.u32 [%0], 0;" ::"r"(smem_u32(&s_done[slot])) : "memory");
+          lfill(slot);
+        }
+      }
+      ladv();
+      slot = slot == kSlots - 1 ? 0 : slot + 1;
     }
     const int bias = 128 * ng;
     int mx[G], mn[G];
@@ -663,8 +847,39 @@ static cudaError_t scan8_launch(const LayerArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+static cudaError_t scan8_pipe_launch(const LayerArgs &a, cudaStream_t s) {
+  constexpr int TPT = 32;
+  constexpr int kTile = kScanThreads * TPT;
+  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
+  const int units = a.B * a.Hkv;
+  const int nsplit = a.scan_split;
+  const int total = tiles_per_unit * units * nsplit;
+  if (total == 0) return cudaSuccess;
+  const size_t smem = (size_t)3 * a.cpow2 * 4 + 3 * (size_t)kTile * 2 + 3 * 8;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan8_pipe<TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         226 * 1024);
+    if (e != cudaSuccess) return e;
+    configured[dev] = 1;
+  }
+  const int grid = total < a.num_sms ? total : a.num_sms;
+  cudaEvent_t eb, ee;
+  scan_events(&eb, &ee);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
+  k_scan8_pipe<TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  note_launch();
+  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s) {
-  if (a.lut8) return scan8_launch(a, s);
+  if (a.lut8) return scan_pipelined() ? scan8_pipe_launch(a, s) : scan8_launch(a, s);
   switch (a.G) {
     case 1: return scan_g<1>(a, s);
     case 2: return scan_g<2>(a, s);

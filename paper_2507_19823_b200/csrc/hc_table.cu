@@ -125,14 +125,16 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
 #pragma unroll
     for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t(t[h], sc[h]);
     int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
+    // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd head's
+    // signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
     if constexpr (G == 4) {
       uint2 v;
-      v.x = (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
-      v.y = (uint32_t)(uint16_t)packed[2] | ((uint32_t)(uint16_t)packed[3] << 16);
+      v.x = (uint32_t)(packed[0] + 32768) | ((uint32_t)(uint16_t)packed[1] << 16);
+      v.y = (uint32_t)(packed[2] + 32768) | ((uint32_t)(uint16_t)packed[3] << 16);
       *reinterpret_cast<uint2 *>(dst) = v;
     } else if constexpr (G == 2) {
       *reinterpret_cast<uint32_t *>(dst) =
-          (uint32_t)(uint16_t)packed[0] | ((uint32_t)(uint16_t)packed[1] << 16);
+          (uint32_t)(packed[0] + 32768) | ((uint32_t)(uint16_t)packed[1] << 16);
     } else {
 #pragma unroll
       for (int h = 0; h < G; ++h) dst[h] = packed[h];
