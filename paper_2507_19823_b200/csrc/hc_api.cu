@@ -17,6 +17,15 @@ using namespace hc;
 namespace hc {
 static std::atomic<unsigned long long> g_launches{0};
 static thread_local cudaEvent_t g_scan_ev[2] = {nullptr, nullptr};
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_PDL");
+    v = (ev && !strcmp(ev, "0")) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 void scan_events(cudaEvent_t *begin, cudaEvent_t *end) {
   *begin = g_scan_ev[0];
@@ -436,13 +445,6 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   const int rows = a.B * a.Hq;
   const int64_t n_q = a.n_q, n_cand = a.n_cand;
   cudaError_t e;
-  if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
-  if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
-  if (n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
-  SelArgs sa{};
-  sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
-  sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
-  sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
   // Eq. 5 placement policy (measured): host-mapped values -> the GQA union
   // de-duplicated gather kernel (fewer host-link bytes: +18 % steps/s at config 3); HBM
   // values -> the high-occupancy per-head row gather (many rows in flight per SM).
@@ -459,21 +461,22 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   const bool shared = budget.shared_kv != 0;
   const bool union_gather = !budget.select_only && (want_union || shared) && a.G > 1;
   const bool want_rows = gather_mode == 3 || (gather_mode == 2 && a.v_placement == 0);
-  const bool rows_gather = !budget.select_only && !union_gather && want_rows && a.d == 128;
+  const bool rows_gather = !budget.select_only && !union_gather && (want_rows || shared) && a.d == 128;
+  if (shared && !budget.select_only && !union_gather && !rows_gather)
+    return fail(HC_ERR_UNSUPPORTED, "shared_kv with G = 1 needs d = 128");
+  // the gather's completion counters are zeroed by k_table (no memset between chain kernels)
+  if (union_gather) { a.gdone = (uint32_t *)((uint8_t *)ws + Lw.o_udone); a.gdone_n = a.B * a.Hkv; }
+  if (rows_gather) { a.gdone = (uint32_t *)((uint8_t *)ws + Lw.o_rdone); a.gdone_n = rows; }
+  if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
+  if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
+  if (n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
+  SelArgs sa{};
+  sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
+  sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
+  sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
   if (shared) {
     if ((e = launch_group_select(a, n_q > 0 ? a.scan_split : 1, s)) != cudaSuccess)
       return cuda_check(e, "shared select");
-    if (!budget.select_only && !union_gather) {  // G == 1: per-row gather of the lists
-      uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);
-      if ((e = cudaMemsetAsync(done, 0, (size_t)rows * 4, s)) != cudaSuccess) return cuda_check(e, "memset");
-      const int64_t kc2 = a.k_max < n_cand ? a.k_max : n_cand;
-      if (a.d == 128) {
-        if ((e = launch_gather_rows(a, kc2, (float *)((uint8_t *)ws + Lw.o_rpart), done, s)) != cudaSuccess)
-          return cuda_check(e, "gather");
-      } else {
-        return fail(HC_ERR_UNSUPPORTED, "shared_kv with G = 1 needs d = 128");
-      }
-    }
   } else if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
                                       (budget.select_only || union_gather || rows_gather) ? 0 : 1,
                                       a.num_sms, s,
@@ -481,16 +484,12 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     return cuda_check(e, "select");
   if (rows_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);
-    if ((e = cudaMemsetAsync(done, 0, (size_t)rows * 4, s)) != cudaSuccess)
-      return cuda_check(e, "memset");
     const int64_t kc2 = a.k_max < n_cand ? a.k_max : n_cand;
     if ((e = launch_gather_rows(a, kc2, (float *)((uint8_t *)ws + Lw.o_rpart), done, s)) != cudaSuccess)
       return cuda_check(e, "gather");
   }
   if (union_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_udone);
-    if ((e = cudaMemsetAsync(done, 0, (size_t)a.B * a.Hkv * 4, s)) != cudaSuccess)
-      return cuda_check(e, "memset");
     if ((e = launch_gather_union(a, (float *)((uint8_t *)ws + Lw.o_upart), done, s)) != cudaSuccess)
       return cuda_check(e, "gather");
   }

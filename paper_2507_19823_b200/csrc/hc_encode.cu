@@ -44,6 +44,8 @@ template <int DBAR>
 __global__ void __launch_bounds__(kEThreads) k_encode(EncodeArgs a) {
   constexpr int kER = EncCfg<DBAR>::kER;
   constexpr int kU = EncCfg<DBAR>::kU;
+  pdl_trigger();
+  pdl_wait();
   const int64_t r0 = (int64_t)blockIdx.x * kER;
   const int64_t left = a.rows - r0;
   const int nr = left < kER ? (int)left : kER;
@@ -129,7 +131,7 @@ cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s) {
 #define HC_ENC(D)                                                                        \
   {                                                                                      \
     dim3 grid((unsigned)((a.rows + EncCfg<D>::kER - 1) / EncCfg<D>::kER), (unsigned)a.g); \
-    k_encode<D><<<grid, kEThreads, 0, s>>>(a);                                           \
+    launch_chain(k_encode<D>, grid, dim3(kEThreads), 0, s, a);                           \
     note_launch();                                                                       \
     break;                                                                               \
   }
@@ -147,6 +149,8 @@ cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s) {
 
 // copy `rows` fp16 rows of d elements; one warp per row, 16 B per lane
 __global__ void __launch_bounds__(256) k_rowcopy(RowCopyArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (r >= a.rows) return;
   const int l = threadIdx.x & 31;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(256) k_rowcopy(RowCopyArgs a) {
 
 cudaError_t launch_rowcopy(const RowCopyArgs &a, cudaStream_t s) {
   if (a.rows <= 0) return cudaSuccess;
-  k_rowcopy<<<(unsigned)((a.rows + 7) / 8), 256, 0, s>>>(a);
+  launch_chain(k_rowcopy, dim3((unsigned)((a.rows + 7) / 8)), dim3(256), 0, s, a);
   note_launch();
   return cudaGetLastError();
 }

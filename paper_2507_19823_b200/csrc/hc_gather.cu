@@ -43,6 +43,8 @@ __global__ void __launch_bounds__(kGT) k_gather_union(LayerArgs a, int nchunks, 
   __shared__ uint16_t ulist[kGC];
   __shared__ int s_lo[G], s_hi[G], s_cnt;
   __shared__ int s_wc[kGT / 32];
+  pdl_trigger();
+  pdl_wait();
   const int ch = blockIdx.x, u = blockIdx.y;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int64_t j0 = (int64_t)ch * kGC;
@@ -206,6 +208,8 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   __shared__ int32_t sj[kRC];
   __shared__ float sw[kRC];
   __shared__ float red[(kRT / 32) * 2 * 128];
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
   const int b = row / a.Hq, hq = row - b * a.Hq, kv = hq / a.G;
   const int64_t k = a.hs[row].ksel;
@@ -297,7 +301,7 @@ cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, u
   if (nch == 0) return cudaSuccess;
   // CTAs beyond a row's k_sel exit at once (they only count if they hold kept rows)
   dim3 grid((unsigned)nch, (unsigned)(a.B * a.Hq));
-  k_gather_rows<<<grid, kRT, 0, s>>>(a, nch, part, done);
+  launch_chain(k_gather_rows, grid, dim3(kRT), 0, s, a, nch, part, done);
   note_launch();
   return cudaGetLastError();
 }
@@ -307,9 +311,9 @@ cudaError_t launch_gather_union(const LayerArgs &a, float *part, uint32_t *done,
   if (nch == 0) return cudaSuccess;
   dim3 grid((unsigned)nch, (unsigned)(a.B * a.Hkv));
   switch (a.G) {
-    case 1: k_gather_union<1><<<grid, kGT, 0, s>>>(a, nch, part, done); break;
-    case 2: k_gather_union<2><<<grid, kGT, 0, s>>>(a, nch, part, done); break;
-    case 4: k_gather_union<4><<<grid, kGT, 0, s>>>(a, nch, part, done); break;
+    case 1: launch_chain(k_gather_union<1>, grid, dim3(kGT), 0, s, a, nch, part, done); break;
+    case 2: launch_chain(k_gather_union<2>, grid, dim3(kGT), 0, s, a, nch, part, done); break;
+    case 4: launch_chain(k_gather_union<4>, grid, dim3(kGT), 0, s, a, nch, part, done); break;
     default: return cudaErrorInvalidValue;
   }
   note_launch();

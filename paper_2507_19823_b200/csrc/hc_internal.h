@@ -10,6 +10,30 @@ namespace hc {
 
 // number of kernels this library has enqueued (or captured into a graph)
 void note_launch(int n = 1);
+
+// Programmatic dependent launch (PDL) along the decode chain (encode -> table -> [resident]
+// -> scan -> select -> gather -> next layer's encode): each chain kernel triggers its
+// dependents at entry and waits (griddepcontrol.wait) before touching memory written by
+// its predecessors, so the next kernel's launch and prologue overlap this kernel's tail.
+// HC_PDL=0 disables the attribute (plain stream order).
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                         Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 // profiling hook: events recorded around the next scan launch (may be null)
 void scan_events(cudaEvent_t *begin, cudaEvent_t *end);
 
@@ -98,6 +122,10 @@ struct LayerArgs {
   unsigned long long *grp_hist;    // [B*Hkv][4 levels][kNB][count, mass]
   uint32_t *grp_chunk;             // [B*Hkv][chunks][strict, ties]
   unsigned long long *grp_key;     // [B*Hkv][z_stride] order key D of every candidate
+  // completion counters of this layer's gather kernel, zeroed by k_table (no memset node
+  // between the chain kernels)
+  uint32_t *gdone;
+  int gdone_n;
 };
 
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);

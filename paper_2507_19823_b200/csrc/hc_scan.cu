@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
     for (int j = 0; j < 3; ++j) mbar_init(&cb[j], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();
   uint32_t tph = 0, cph = 0;  // phase bit per barrier
   const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -340,7 +342,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
     for (int j = 0; j < kSlots; ++j) { mbar_init(&full[j], 1); s_done[j] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();
   if ((int)blockIdx.x >= total_tiles) return;
   const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -492,7 +496,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
     for (int j = 0; j < 3; ++j) mbar_init(&cb[j], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();
   uint32_t tph = 0, cph = 0;
   const uint32_t mask = (uint32_t)(a.cpow2 - 1) << 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -610,7 +616,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8_pipe(LayerArgs a, int
     for (int j = 0; j < kSlots; ++j) { mbar_init(&full[j], 1); s_done[j] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();
   if ((int)blockIdx.x >= total_tiles) return;
   const uint32_t mask = (uint32_t)(a.cpow2 - 1) << 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -764,7 +772,7 @@ static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cap);
   const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  k_scan_pipe<G, TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  launch_chain(k_scan_pipe<G, TPT>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
@@ -795,7 +803,7 @@ static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cap);
   const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  k_scan<G, TPT, RC><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  launch_chain(k_scan<G, TPT, RC>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
@@ -844,7 +852,7 @@ static cudaError_t scan8_launch(const LayerArgs &a, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cap);
   const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  k_scan8<TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  launch_chain(k_scan8<TPT>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
@@ -875,7 +883,7 @@ static cudaError_t scan8_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cap);
   const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  k_scan8_pipe<TPT><<<grid, kScanThreads, smem, s>>>(a, tiles_per_unit, total, nsplit);
+  launch_chain(k_scan8_pipe<TPT>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();

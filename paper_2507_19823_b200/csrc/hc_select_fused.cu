@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(kFT, kOcc)
   __shared__ unsigned long long sx[kFT / 32], sy[kFT / 32];
   __shared__ float s_red[(kFT / 32) * 32 * 8];  // gather partials [nslots][d] (nslots*d == 4096)
 
+  pdl_trigger();
+  pdl_wait();
   HeadState *hs = s.hs + row;
   const float kappa = hs->kappa;
   const int64_t n = s.n;
@@ -761,13 +763,15 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
   cfg.blockDim = dim3(kFT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   static int stop_env = -1;
   if (stop_env < 0) {
     const char *ev = getenv("HC_SEL_STOP");

@@ -53,6 +53,10 @@ __device__ __forceinline__ void table_entry(const float (&qs)[G][DBAR], const fl
 // clamp(rint(t * 2^e_h)).  Each thread owns centroids m0+tid, m0+tid+256, ...
 template <int G, int DBAR>
 __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  if (a.gdone && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+    for (int t = threadIdx.x; t < a.gdone_n; t += blockDim.x) a.gdone[t] = 0u;
   const int u = blockIdx.z;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int i = blockIdx.y;
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
   dim3 grid((unsigned)a.tsplit, (unsigned)a.g, (unsigned)(a.B * a.Hkv));
-  k_table<G, DBAR><<<grid, kTB, 0, s>>>(a);
+  launch_chain(k_table<G, DBAR>, grid, dim3(kTB), 0, s, a);
   note_launch();
   return cudaGetLastError();
 }
@@ -210,6 +214,8 @@ constexpr int kRT = 128;  // tokens per CTA (kRT * G threads for G = 4)
 template <int G>
 __global__ void __launch_bounds__(kRT * G) k_resident(LayerArgs a) {
   extern __shared__ __align__(16) uint8_t rsm[];
+  pdl_trigger();
+  pdl_wait();
   const int u = blockIdx.y;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int d = a.d;
@@ -277,9 +283,9 @@ cudaError_t launch_resident(const LayerArgs &a, cudaStream_t s) {
     configured[dev] = 1;
   }
   switch (a.G) {
-    case 1: k_resident<1><<<grid, kRT * 1, smem, s>>>(a); break;
-    case 2: k_resident<2><<<grid, kRT * 2, smem, s>>>(a); break;
-    case 4: k_resident<4><<<grid, kRT * 4, smem, s>>>(a); break;
+    case 1: launch_chain(k_resident<1>, grid, dim3(kRT * 1), smem, s, a); break;
+    case 2: launch_chain(k_resident<2>, grid, dim3(kRT * 2), smem, s, a); break;
+    case 4: launch_chain(k_resident<4>, grid, dim3(kRT * 4), smem, s, a); break;
     default: return cudaErrorInvalidValue;
   }
   note_launch();
