@@ -73,7 +73,6 @@ int next_pow2(int c) {
 }
 
 constexpr int kMaxTSplit = 8;
-constexpr int kMaxScanSplit = 4;
 
 // Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
 // the group split so the work fills the SMs with the least shared-memory time, modelled
@@ -131,7 +130,7 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
   L.o_T = o; o += align256((size_t)B * Hkv * g * L.cpow2 * G * 2);
   L.o_cbabs = o; o += align256((size_t)kc->vq.cbg * (d / g) * 4);
   L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
-  L.o_zpart = o; o += align256((size_t)kMaxScanSplit * rows * L.z_stride * 4);
+  L.o_zpart = o;  // (no partial planes: split scans accumulate exactly into z)
   L.o_idx = o; o += align256((size_t)rows * L.k_eff * 4);
   L.o_w = o; o += align256((size_t)rows * L.k_eff * 4);
   L.nch_max = shard_chunks(ncand_max > 0 ? ncand_max : 1);

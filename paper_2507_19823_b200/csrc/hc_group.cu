@@ -61,31 +61,18 @@ __device__ __forceinline__ void grp_ctx(const LayerArgs &a, int u, GrpCtx &c) {
   }
 }
 
-// z <- Σ split partials (exact integers) for the quantized tokens, M folded by atomicMax;
-// 4 consecutive tokens per thread (16-B loads; rows are 64-float aligned)
-__global__ void __launch_bounds__(kGrT) k_grp_fin(LayerArgs a, int nsplit) {
+// split scans leave M unfolded: M = max z over the quantized tokens (atomicMax), z final
+__global__ void __launch_bounds__(kGrT) k_grp_fin(LayerArgs a, int) {
   const int row = blockIdx.y;
-  float *zr = a.z + (int64_t)row * a.z_stride;
-  const int64_t plane = (int64_t)a.B * a.Hq * a.z_stride;
-  const float *zp = a.zpart + (int64_t)row * a.z_stride;
+  const float *zr = a.z + (int64_t)row * a.z_stride;
   const int64_t nq = a.n_q;
   int mx = INT_MIN;
   for (int64_t t = ((int64_t)blockIdx.x * kGrT + threadIdx.x) * 4; t < nq; t += (int64_t)gridDim.x * kGrT * 4) {
-    float4 acc = *reinterpret_cast<const float4 *>(zp + t);
-    for (int sp = 1; sp < nsplit; ++sp) {
-      const float4 v = *reinterpret_cast<const float4 *>(zp + sp * plane + t);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-    const float f[4] = {acc.x, acc.y, acc.z, acc.w};
     if (t + 4 <= nq) {
-      *reinterpret_cast<float4 *>(zr + t) = acc;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) mx = max(mx, zint(f[u]));
-    } else {  // ragged tail: positions >= n_q hold resident scores
-      for (int u = 0; u < 4 && t + u < nq; ++u) {
-        zr[t + u] = f[u];
-        mx = max(mx, zint(f[u]));
-      }
+      const float4 v = *reinterpret_cast<const float4 *>(zr + t);
+      mx = max(max(mx, zint(v.x)), max(zint(v.y), max(zint(v.z), zint(v.w))));
+    } else {
+      for (int u = 0; u < 4 && t + u < nq; ++u) mx = max(mx, zint(zr[t + u]));
     }
   }
   mx = __reduce_max_sync(0xffffffffu, mx);

@@ -119,10 +119,40 @@ __device__ __forceinline__ void lookup8(const uint4 &c, const uint8_t *sb, uint3
   }
 }
 
+// group-split items add their exact integer partial sums into z (zeroed by k_table) with
+// float atomics: every partial and every prefix is an integer below 2^23, so the fp32 sum
+// is exact in any order and z is final after the scan (no partial planes, no reduce pass)
+__device__ __forceinline__ void red_add4(float *p, float a0, float a1, float a2, float a3) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a0), "f"(a1), "f"(a2),
+               "f"(a3)
+               : "memory");
+}
+
+template <int G>
+__device__ __forceinline__ void store_chunk_add(const LayerArgs &a, int b, int kv, int64_t tok,
+                                                const int (&acc)[8][G]) {
+  if (tok >= a.n_q) return;
+  const int64_t rem_ = a.n_q - tok;
+  const int nval = rem_ < 8 ? (int)rem_ : 8;
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    float *zp = a.z + ((int64_t)b * a.Hq + kv * G + h) * a.z_stride + tok;
+    if (nval == 8) {
+      red_add4(zp, (float)acc[0][h], (float)acc[1][h], (float)acc[2][h], (float)acc[3][h]);
+      red_add4(zp + 4, (float)acc[4][h], (float)acc[5][h], (float)acc[6][h], (float)acc[7][h]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u < nval) atomicAdd(zp + u, (float)acc[u][h]);
+    }
+  }
+}
+
 template <int G>
 __device__ __forceinline__ void store_chunk(const LayerArgs &a, float *zbase, int b, int kv,
                                             int64_t tok, const int (&acc)[8][G], int (&mx)[G],
-                                            int (&mn)[G]) {
+                                            int (&mn)[G], bool add = false) {
+  if (add) { store_chunk_add<G>(a, b, kv, tok, acc); return; }
   if (tok >= a.n_q) return;
   const int64_t rem_ = a.n_q - tok;
   const int nval = rem_ < 8 ? (int)rem_ : 8;
@@ -153,9 +183,9 @@ __device__ __forceinline__ void store_chunk(const LayerArgs &a, float *zbase, in
 }
 
 // Work item = (unit, token tile, group split).  With nsplit > 1 each item sums only
-// its groups [i0, i1) and writes the exact integer partial to zpart[split]; k_zreduce
-// adds the partials (exact: integers < 2^24 in fp32) -- so small-context configs can
-// spread one unit's tokens AND groups over all SMs without re-streaming every slice.
+// its groups [i0, i1) and adds the exact integer partial into z (store_chunk_add) -- so
+// small-context configs can spread one unit's tokens AND groups over all SMs without
+// re-streaming every slice.
 // per-head max / min of the final scores (unsplit scan): warp reduce + one atomic per warp,
 // so the select kernel needs no extra pass over z for them
 template <int G>
@@ -297,11 +327,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
     int mx[G], mn[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
-    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+    float *zbase = a.z;
+    const bool zadd = nsplit > 1;
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) {
       unbias<G>(acc[k], ng);
-      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn, zadd);
     }
     if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
@@ -461,11 +492,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
     int mx[G], mn[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
-    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+    float *zbase = a.z;
+    const bool zadd = nsplit > 1;
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) {
       unbias<G>(acc[k], ng);
-      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn);
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn, zadd);
     }
     if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
@@ -577,7 +609,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
     int mx[G], mn[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
-    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+    float *zbase = a.z;
+    const bool zadd = nsplit > 1;
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) {
       int acc[8][G];
@@ -588,7 +621,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tile
         acc[t][1] = (int)(ao[k][t] & 0xffffu) - bias;
         acc[t][3] = (int)(ao[k][t] >> 16) - bias;
       }
-      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn);
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn, zadd);
     }
     if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }
@@ -718,7 +751,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8_pipe(LayerArgs a, int
     int mx[G], mn[G];
 #pragma unroll
     for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
-    float *zbase = nsplit == 1 ? a.z : a.zpart + (int64_t)sp * a.B * a.Hq * a.z_stride;
+    float *zbase = a.z;
+    const bool zadd = nsplit > 1;
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) {
       int acc[8][G];
@@ -729,7 +763,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8_pipe(LayerArgs a, int
         acc[t][1] = (int)(ao[k][t] & 0xffffu) - bias;
         acc[t][3] = (int)(ao[k][t] >> 16) - bias;
       }
-      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn);
+      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn, zadd);
     }
     if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
   }

@@ -6,7 +6,7 @@
 // One thread-block CLUSTER of `cs` CTAs per row (= query head).  Each CTA owns a
 // contiguous token range of the row; the row-wide reductions go through distributed
 // shared memory (DSMEM) instead of global atomics and extra launches:
-//   P0  z (sum of the scan's split partials, exact) -> SMEM cache; M, zmin (cluster max/min)
+//   P0  z (final after the scan) -> SMEM cache; M, zmin (cluster max/min) unless folded
 //   P1  coarse (count, mass) histogram of Δ = M - z >> shift   [SMEM atomics]
 //       cluster reduce: CTA r owns bins [r*NB/cs, (r+1)*NB/cs) and sums them over peers;
 //       bound1: S, Θ = ⌈τ_q·S/2^24⌉, first bucket b* where mass reaches Θ or count k_max
@@ -63,16 +63,6 @@ __device__ __forceinline__ void bscan2(T &x, T &y, T &tx, T &ty, T *sx, T *sy) {
   y = by + iy - y;
 }
 
-__device__ __forceinline__ float load_z(const LayerArgs &la, const SelArgs &s, int row, int64_t j,
-                                        int nsplit) {
-  const float *zr = s.z + (int64_t)row * s.z_stride;
-  if (nsplit <= 1 || j >= la.n_q) return zr[j];
-  const int64_t plane = (int64_t)la.B * la.Hq * la.z_stride;
-  const float *p = la.zpart + (int64_t)row * la.z_stride + j;
-  float acc = p[0];
-  for (int sp = 1; sp < nsplit; ++sp) acc += p[sp * plane];  // exact: integers < 2^24
-  return acc;
-}
 
 // visit every token t in [0, nt) of the CTA once (any order) with 16 tokens per thread in
 // flight: 4 x 16-B loads issued before use (zsrc is 16-B aligned: the z cache or the z row)
@@ -177,56 +167,13 @@ __global__ void __launch_bounds__(kFT, kOcc)
       mx = m0;
       mn = z0;
     }
-  } else if (nsplit <= 1) {  // z is final: stream it once into the cache
+  } else {  // stream z once (final after the scan: split scans accumulate exactly into z)
     for_tokens_pos(s.z + (int64_t)row * s.z_stride + j0, nt, [&](int64_t t, float zf) {
       if (zcache) zc[t] = zf;
       const int zi = zint(zf);
       mx = max(mx, zi);
       mn = min(mn, zi);
     });
-  } else {
-    const float *zr = s.z + (int64_t)row * s.z_stride;
-    const int64_t plane = (int64_t)la.B * la.Hq * la.z_stride;
-    const float *zp = la.zpart + (int64_t)row * la.z_stride;
-    const int64_t qend = nsplit > 1 ? (la.n_q < j1 ? la.n_q : j1) : j0;  // [j0, qend) from partials
-    for (int64_t t = (int64_t)tid * 4; t < nt; t += (int64_t)kFT * 4) {
-      const int64_t j = j0 + t;
-      float v[4];
-      if (j + 4 <= qend) {
-        float4 acc = *reinterpret_cast<const float4 *>(zp + j);
-        float4 part[3];
-#pragma unroll
-        for (int sp = 1; sp < 4; ++sp)
-          if (sp < nsplit) part[sp - 1] = *reinterpret_cast<const float4 *>(zp + sp * plane + j);
-#pragma unroll
-        for (int sp = 1; sp < 4; ++sp)
-          if (sp < nsplit) {
-            acc.x += part[sp - 1].x; acc.y += part[sp - 1].y;
-            acc.z += part[sp - 1].z; acc.w += part[sp - 1].w;
-          }
-        for (int sp = 4; sp < nsplit; ++sp) {
-          const float4 q4 = *reinterpret_cast<const float4 *>(zp + sp * plane + j);
-          acc.x += q4.x; acc.y += q4.y; acc.z += q4.z; acc.w += q4.w;
-        }
-        v[0] = acc.x; v[1] = acc.y; v[2] = acc.z; v[3] = acc.w;
-      } else if (j >= qend && j + 4 <= j1 && ((j & 3) == 0)) {
-        const float4 q4 = *reinterpret_cast<const float4 *>(zr + j);
-        v[0] = q4.x; v[1] = q4.y; v[2] = q4.z; v[3] = q4.w;
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = (j + u < j1) ? load_z(la, s, row, j + u, nsplit) : 0.0f;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (t + u < nt) {
-          if (zcache) zc[t + u] = v[u];
-          if ((!zcache || zstore) && nsplit > 1) const_cast<float *>(zr)[j + u] = v[u];
-          const int zi = zint(v[u]);
-          mx = max(mx, zi);
-          mn = min(mn, zi);
-        }
-      }
-    }
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   mn = __reduce_min_sync(0xffffffffu, mn);

@@ -19,14 +19,8 @@ namespace hc {
 constexpr int kShT = 256;
 constexpr int kShChunk = 4096;  // tokens per compaction chunk (16 per thread)
 
-__device__ __forceinline__ float sh_z(const LayerArgs &a, int row, int64_t j, int nsplit) {
-  const float *zr = a.z + (int64_t)row * a.z_stride;
-  if (nsplit <= 1 || j >= a.n_q) return zr[j];
-  const int64_t plane = (int64_t)a.B * a.Hq * a.z_stride;
-  const float *p = a.zpart + (int64_t)row * a.z_stride + j;
-  float acc = p[0];
-  for (int sp = 1; sp < nsplit; ++sp) acc += p[sp * plane];
-  return acc;
+__device__ __forceinline__ float sh_z(const LayerArgs &a, int row, int64_t j, int) {
+  return a.z[(int64_t)row * a.z_stride + j];  // final after the scan (split scans add into z)
 }
 
 // z <- sum of split partials; stats[row] = {max z, -min z} (atomic max)
@@ -35,7 +29,6 @@ __global__ void __launch_bounds__(kShT) k_sh_stats(LayerArgs a, int nsplit, int3
   int mx = INT_MIN, mn = INT_MAX;
   for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
     const float zf = sh_z(a, row, j, nsplit);
-    if (nsplit > 1 && j < a.n_q) a.z[(int64_t)row * a.z_stride + j] = zf;
     const int zi = zint(zf);
     mx = max(mx, zi);
     mn = min(mn, zi);

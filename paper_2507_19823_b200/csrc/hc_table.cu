@@ -57,6 +57,16 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   pdl_wait();
   if (a.gdone && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
     for (int t = threadIdx.x; t < a.gdone_n; t += blockDim.x) a.gdone[t] = 0u;
+  if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
+    const int uu = blockIdx.z, bb = uu / a.Hkv, kk = uu - bb * a.Hkv;
+    const int64_t nz4 = (a.n_q + 3) / 4;  // float4s per row (rows are 64-float aligned)
+    const int64_t part = (int64_t)blockIdx.y * gridDim.x + blockIdx.x, parts = (int64_t)gridDim.x * gridDim.y;
+    for (int h = 0; h < G; ++h) {
+      float4 *zr = reinterpret_cast<float4 *>(a.z + ((int64_t)bb * a.Hq + kk * G + h) * a.z_stride);
+      for (int64_t q = part * blockDim.x + threadIdx.x; q < nz4; q += parts * blockDim.x)
+        zr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
   const int u = blockIdx.z;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int i = blockIdx.y;
