@@ -15,7 +15,8 @@ void note_launch(int n = 1);
 // -> scan -> select -> gather -> next layer's encode): each chain kernel triggers its
 // dependents at entry and waits (griddepcontrol.wait) before touching memory written by
 // its predecessors, so the next kernel's launch and prologue overlap this kernel's tail.
-// HC_PDL=0 disables the attribute (plain stream order).
+// Opt-in (HC_PDL=1): measured neutral in the graph-captured step and slower for eager
+// calls, so plain stream order is the default; the kernels are PDL-safe either way.
 bool pdl_enabled();
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
