@@ -158,9 +158,17 @@ class Workload:
             sd.fill_values(self.kc.res_v, SEED, self.n_local, device=device, start=self.base)
         else:
             self.kc = hc.KCache(B, L, H, G, d, g, c, n_cap, self.codebook, device=device,
-                                lut_bits=cfg.get("lut_bits", 16))
+                                lut_bits=cfg.get("lut_bits", 16), code_bits=cfg.get("code_bits", 16))
             self.vs = hc.VStore.allocate(B, L, H, n_cap, d, placement=cfg["placement"], device=device)
-            sd.fill_codes(self.kc.codes, SEED, c, self.n_local, start=self.base)
+            if cfg.get("code_bits", 16) == 13:  # fill u16 layer by layer, pack into strips
+                c16 = torch.zeros((B, 1, H, g, n_cap), dtype=torch.int16, device=device)
+                for l in range(L):
+                    sd.fill_codes(c16, SEED, c, self.n_local, start=self.base, layers=[0], layer_ids=[l])
+                    for b_ in range(B):  # codes[b, l] is one contiguous run of strips
+                        hc.pack_codes13(c16[b_:b_ + 1], n_cap, n_cap, out=self.kc.codes[b_:b_ + 1, l:l + 1])
+                del c16
+            else:
+                sd.fill_codes(self.kc.codes, SEED, c, self.n_local, start=self.base)
             sd.fill_values(self.vs.tensor, SEED, self.n_local, device=device, start=self.base)
         self.reset_counts()
         # per-step inputs: q for every layer, the new token's k and v
@@ -488,6 +496,8 @@ def main():
                          "over the host-resident values (needs a host-V config, e.g. 3)")
     ap.add_argument("--lut8", action="store_true",
                     help="8-bit query/codebook table variant (R2b, SURVEY f3)")
+    ap.add_argument("--code-bits", type=int, default=16, choices=[16, 13],
+                    help="13: packed 13-bit code strips (SURVEY f3(ii), 19%% fewer code bytes)")
     ap.add_argument("--shared-kv", action="store_true",
                     help="one selection per KV head shared by its GQA heads (R8, SURVEY f3(iii))")
     ap.add_argument("--virtual-shards", type=int, default=0,
@@ -507,6 +517,9 @@ def main():
     cfg["vo_only"] = bool(args.vo_only)
     cfg["cpu_gather"] = bool(args.cpu_gather)
     cfg["shared_kv"] = bool(args.shared_kv)
+    cfg["code_bits"] = args.code_bits
+    if args.code_bits == 13:
+        cfg["workload"] += "; packed 13-bit codes (f3(ii))"
     if args.shared_kv:
         cfg["workload"] += "; per-KV-head shared selection (R8, f3(iii))"
     if args.cpu_gather:
@@ -580,6 +593,8 @@ def main():
     B, L, H, g, n, d = (cfg[k] for k in ("B", "L", "Hkv", "g", "n", "d"))
     n_here = wl.n_local
     p_bytes_layer = B * H * n_here * (d if wl.vo_only else g) * 2  # exact K rows in VO-only mode
+    if cfg.get("code_bits", 16) == 13 and not wl.vo_only:
+        p_bytes_layer = B * H * n_here * g * 13 // 8  # packed code strips
     achieved = p_bytes_layer / (scan_avg_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     traffic = None

@@ -54,7 +54,16 @@ typedef void *hc_stream_t; /* cudaStream_t */
 typedef struct {
     int32_t d, g, c, cbg;
     int32_t lut_bits;
+    int32_t code_bits; /* 0 or 16: u16 codes; 13: packed codes (NEXT f3(ii), see below) */
 } hc_vq;
+
+/* Packed 13-bit code layout (code_bits = 13, requires c <= 8192 and lut_bits = 16): every
+ * (b, l, kv, group) strip of n_cap tokens is HC_STRIP13_BYTES(n_cap) = 13*n_cap/8 bytes:
+ *   [lo: n_cap bytes, code & 0xff][nib: n_cap/2 bytes, (code >> 8) & 15, token t in byte
+ *   t/2, low nibble for even t][bit: n_cap/8 bytes, code >> 12, token t at bit t%8 of byte t/8]
+ * and hc_kcache.codes points at B*L*Hkv*g such strips (same order as the u16 layout).
+ * 19 % fewer code bytes than u16 at g = 32 (52 vs 64 B per token and KV head). */
+#define HC_STRIP13_BYTES(n_cap) ((int64_t)(n_cap) * 13 / 8)
 
 /* Budget (R5): tau ∈ (0,1] is Eq. 4's cumulative-mass threshold (τ = 0.9 in
  * §4.1); k_max >= 1 caps the kept set: k_sel = min(k*(τ), k_max);
@@ -168,6 +177,14 @@ hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *code
  * u16 (device, optional).  s_m is summed exactly (int64 units of 2^-24), so the result
  * is independent of thread order.  ws >= hc_kmeans_workspace_bytes(vq, b). */
 size_t hc_kmeans_workspace_bytes(hc_vq vq, int64_t b);
+
+/* Pack u16 codes into the 13-bit strip layout (code_bits = 13, above): for s < strips,
+ * t < n: strip s of dst (HC_STRIP13_BYTES(n_cap) bytes each) gets src[s*src_stride + t].
+ * Codes must be < 8192 (HC_ERR_RANGE is not checked on the device: higher bits are
+ * dropped).  n <= n_cap, n_cap % 64 == 0; tokens >= n of each strip are left unchanged.
+ * Device pointers; asynchronous on `stream`. */
+hc_status hc_pack_codes13(const uint16_t *src, int64_t strips, int64_t n, int64_t src_stride,
+                          uint8_t *dst, int64_t n_cap, hc_stream_t stream);
 hc_status hc_kmeans_step(const uint16_t *keys, int64_t n_keys, const int64_t *sample, int64_t b,
                          hc_vq vq, float *codebook, int64_t *counts, uint16_t *labels, void *ws,
                          size_t ws_bytes, hc_stream_t stream);

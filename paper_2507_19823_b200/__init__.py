@@ -26,7 +26,7 @@ EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_ev
            "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
            "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
            "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish", "hc_kmeans_workspace_bytes",
-           "hc_kmeans_step"]
+           "hc_kmeans_step", "hc_pack_codes13"]
 
 
 class HcError(RuntimeError):
@@ -37,7 +37,7 @@ class HcError(RuntimeError):
 
 class hc_vq(C.Structure):
     _fields_ = [("d", C.c_int32), ("g", C.c_int32), ("c", C.c_int32), ("cbg", C.c_int32),
-                ("lut_bits", C.c_int32)]
+                ("lut_bits", C.c_int32), ("code_bits", C.c_int32)]
 
 
 class hc_budget(C.Structure):
@@ -100,6 +100,8 @@ def lib():
         L.hc_host_weighted_sum.restype = i32
         L.hc_enqueue_host_weighted_sum.argtypes = hw + [p]
         L.hc_enqueue_host_weighted_sum.restype = i32
+        L.hc_pack_codes13.argtypes = [p, i64, i64, i64, p, i64, p]
+        L.hc_pack_codes13.restype = i32
         L.hc_kmeans_workspace_bytes.argtypes = [hc_vq, i64]
         L.hc_kmeans_workspace_bytes.restype = C.c_size_t
         L.hc_kmeans_step.argtypes = [p, i64, p, i64, hc_vq, p, p, p, p, C.c_size_t, p]
@@ -190,6 +192,22 @@ def kmeans_step(keys, sample, codebook, counts, g: int, labels=None, ws=None, st
     return codebook, counts
 
 
+def pack_codes13(codes16, n: int, n_cap: int, out=None, stream=None):
+    """f3(ii): u16 codes [..., >= n] (int16 view, cuda) -> packed strips [..., 13 n_cap / 8] u8."""
+    import torch
+    lead = codes16.shape[:-1]
+    strips = 1
+    for x in lead:
+        strips *= x
+    if out is None:
+        out = torch.zeros(tuple(lead) + (n_cap * 13 // 8,), dtype=torch.uint8, device=codes16.device)
+    if not (out.is_contiguous() and codes16.is_contiguous()):
+        raise ValueError("pack_codes13 needs contiguous tensors (strips back to back)")
+    _check(lib().hc_pack_codes13(_ptr(codes16), strips, n, codes16.shape[-1], _ptr(out), n_cap,
+                                 _stream(stream)))
+    return out
+
+
 def train_codebook(keys, g: int, c: int, iters: int = 200, batch: int = 10000, seed: int = 0,
                    cbg=None, init=None):
     """MiniBatchKMeans codebook training (max 200 iterations, batch 10,000) from the
@@ -252,14 +270,19 @@ class KCache:
     optional recent window res_k/res_v [B][L][Hkv][W][d] fp16."""
 
     def __init__(self, B, L, Hkv, G, d, g, c, n_cap, codebook, cbg=None, res_cap=0,
-                 codes=None, device="cuda", lut_bits=16):
+                 codes=None, device="cuda", lut_bits=16, code_bits=16):
         import torch
         cbg = g if cbg is None else cbg
         self.B, self.L, self.Hkv, self.G, self.d, self.g, self.c, self.cbg = B, L, Hkv, G, d, g, c, cbg
         self.n_cap, self.res_cap = n_cap, res_cap
+        self.code_bits = code_bits
         self.codebook = codebook
-        self.codes = codes if codes is not None else torch.zeros(
-            (B, L, Hkv, g, n_cap), dtype=torch.int16, device=device)
+        if code_bits == 13:  # packed strips (include/hc.h HC_STRIP13_BYTES)
+            self.codes = codes if codes is not None else torch.zeros(
+                (B, L, Hkv, g, n_cap * 13 // 8), dtype=torch.uint8, device=device)
+        else:
+            self.codes = codes if codes is not None else torch.zeros(
+                (B, L, Hkv, g, n_cap), dtype=torch.int16, device=device)
         if res_cap > 0:
             self.res_k = torch.zeros((B, L, Hkv, res_cap, d), dtype=torch.float16, device=device)
             self.res_v = torch.zeros((B, L, Hkv, res_cap, d), dtype=torch.float16, device=device)
@@ -267,7 +290,7 @@ class KCache:
             self.res_k = self.res_v = None
         s = hc_kcache()
         s.B, s.L, s.Hkv, s.G = B, L, Hkv, G
-        s.vq = hc_vq(d, g, c, cbg, lut_bits)
+        s.vq = hc_vq(d, g, c, cbg, lut_bits, code_bits)
         s.n_cap = n_cap
         s.codes = self.codes.data_ptr()
         s.codebook = codebook.data_ptr()
@@ -290,6 +313,16 @@ class KCache:
 
     def n_res(self, layer):
         return self.s.n_res[layer]
+
+    def load_codes16(self, codes16, n: int, stream=None):
+        """Fill the cache's codes from u16 codes [B][L][Hkv][g][>= n] (int16 view, cuda): a
+        copy for 16-bit caches, hc_pack_codes13 for packed ones."""
+        if self.code_bits != 13:
+            self.codes[..., :n] = codes16[..., :n]
+            return
+        strips = self.B * self.L * self.Hkv * self.g
+        _check(lib().hc_pack_codes13(_ptr(codes16), strips, n, codes16.shape[-1], _ptr(self.codes),
+                                     self.n_cap, _stream(stream)))
 
     def set_counts(self, layer, n_q, n_res=0):
         self.s.n_q[layer] = n_q

@@ -165,6 +165,10 @@ hc_status check_vq(const hc_vq &vq) {
     return fail(HC_ERR_UNSUPPORTED, "dbar=%d not in {1,2,4,8,16}", dbar);
   if (vq.c > 65536) return fail(HC_ERR_RANGE, "c=%d exceeds the 16-bit index range", vq.c);
   if (!(vq.cbg == 1 || vq.cbg == vq.g)) return fail(HC_ERR_SHAPE, "cbg must be 1 or g");
+  if (!(vq.code_bits == 0 || vq.code_bits == 16 || vq.code_bits == 13))
+    return fail(HC_ERR_UNSUPPORTED, "code_bits=%d not in {16, 13}", vq.code_bits);
+  if (vq.code_bits == 13 && (vq.c > 8192 || vq.lut_bits == 8))
+    return fail(HC_ERR_UNSUPPORTED, "13-bit codes need c <= 8192 and the 16-bit table");
   if (vq.g > 128) return fail(HC_ERR_UNSUPPORTED, "g=%d > 128 (|z~| must stay below 2^22)", vq.g);
   if (vq.d % 8 || vq.d > 256 || (32 % (vq.d / 8)))
     return fail(HC_ERR_UNSUPPORTED, "d=%d not in {64,128,256}", vq.d);
@@ -242,6 +246,17 @@ hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *code
                     "hc_quantize_keys");
 }
 
+hc_status hc_pack_codes13(const uint16_t *src, int64_t strips, int64_t n, int64_t src_stride,
+                          uint8_t *dst, int64_t n_cap, hc_stream_t stream) {
+  if (strips < 0 || n < 0) return fail(HC_ERR_ARG, "strips/n < 0");
+  if (n_cap % 64 || n > n_cap) return fail(HC_ERR_SHAPE, "need n <= n_cap and n_cap %% 64 == 0");
+  if (src_stride < n) return fail(HC_ERR_SHAPE, "src_stride < n");
+  if (strips == 0 || n == 0) return HC_OK;
+  if (!src || !dst) return fail(HC_ERR_ARG, "NULL pointer");
+  return cuda_check(launch_pack13(src, strips, n, src_stride, dst, n_cap, (cudaStream_t)stream),
+                    "hc_pack_codes13");
+}
+
 size_t hc_kmeans_workspace_bytes(hc_vq vq, int64_t b) {
   if (check_vq(vq) != HC_OK || b < 0) return 0;
   const size_t cc = (size_t)vq.cbg * vq.c, dbar = (size_t)(vq.d / vq.g);
@@ -305,6 +320,13 @@ hc_status hc_append_kv(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const 
     a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
     a.d = (int)d; a.g = (int)g; a.c = kc->vq.c; a.cbg = kc->vq.cbg;
     a.codes = kc->codes; a.omap = codes_at; a.gstride = ncap;
+    if (kc->vq.code_bits == 13) {  // packed strips: strip of (b, layer, kv, group 0)
+      a.pcodes = reinterpret_cast<uint8_t *>(kc->codes);
+      a.psmap = RowMap{H, L * H * g, g, (int64_t)layer * H * g};
+      a.strip_bytes = HC_STRIP13_BYTES(ncap);
+      a.pn_cap = ncap;
+      a.ptok = nq;
+    }
     return launch_encode(a, s);
   };
   auto copy = [&](const uint16_t *src, RowMap sm, uint16_t *dst, RowMap dm) -> cudaError_t {
@@ -385,6 +407,11 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
   a.codes = kc->codes + (int64_t)layer * H * g * ncap;
   a.code_b_stride = L * H * g * ncap;
+  if (kc->vq.code_bits == 13) {
+    a.strip_bytes = HC_STRIP13_BYTES(ncap);
+    a.pcodes = reinterpret_cast<const uint8_t *>(kc->codes) + (int64_t)layer * H * g * a.strip_bytes;
+    a.pc_b_stride = L * H * g * a.strip_bytes;
+  }
   a.res_k = W > 0 ? kc->res_k + (int64_t)layer * H * W * d : nullptr;
   a.res_v = W > 0 ? kc->res_v + (int64_t)layer * H * W * d : nullptr;
   a.res_b_stride = L * H * (W > 0 ? W : 1) * d;

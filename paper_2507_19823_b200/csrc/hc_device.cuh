@@ -108,6 +108,37 @@ __device__ __forceinline__ uint64_t mass_d(uint32_t delta, float kappa) {
 }
 #endif
 
+#ifdef __CUDACC__
+// ---- packed 13-bit codes (f3(ii), include/hc.h): strip = [lo n_cap B][nib n_cap/2 B][bit n_cap/8 B]
+__device__ __forceinline__ void rmw_bits(uint8_t *byte_addr, int bit_in_byte, uint32_t width,
+                                         uint32_t val) {
+  const uintptr_t ad = reinterpret_cast<uintptr_t>(byte_addr);
+  uint32_t *w = reinterpret_cast<uint32_t *>(ad & ~(uintptr_t)3);
+  const int sh = (int)(ad & 3) * 8 + bit_in_byte;
+  const uint32_t m = ((1u << width) - 1u) << sh;
+  atomicAnd(w, ~m);
+  atomicOr(w, (val << sh) & m);
+}
+__device__ __forceinline__ void put_code13(uint8_t *strip, int64_t n_cap, int64_t t, uint32_t code) {
+  rmw_bits(strip + t, 0, 8, code & 0xffu);
+  rmw_bits(strip + n_cap + t / 2, (int)(t & 1) * 4, 4, (code >> 8) & 15u);
+  rmw_bits(strip + n_cap + n_cap / 2 + t / 8, (int)(t & 7), 1, (code >> 12) & 1u);
+}
+// raw = {lo bytes 0-3, lo bytes 4-7, 8 nibbles, 8 bits (low byte)} of 8 consecutive tokens ->
+// the u16-layout uint4 (token 2q in the low half of word q)
+__device__ __forceinline__ uint4 unpack13(const uint4 &raw) {
+  uint32_t o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t lo = __byte_perm(q < 2 ? raw.x : raw.y, 0u, (q & 1) ? 0x4342u : 0x4140u);
+    const uint32_t n2 = (raw.z >> (8 * q)) & 0xffu;
+    const uint32_t b2 = (raw.w >> (2 * q)) & 3u;
+    o[q] = lo | ((n2 & 0xfu) << 8) | ((n2 & 0xf0u) << 20) | ((b2 & 1u) << 12) | ((b2 & 2u) << 27);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+#endif
+
 // R5: Θ = ceil(τ_q · S / 2^24)  (τ_q <= 2^24, S < 2^63)
 HC_HD uint64_t threshold(uint32_t tau_q, uint64_t S) {
   uint64_t lo = (uint64_t)tau_q * S;

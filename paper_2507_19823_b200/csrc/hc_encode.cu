@@ -112,7 +112,12 @@ __global__ void __launch_bounds__(kEThreads) k_encode(EncodeArgs a) {
       const int om = __shfl_xor_sync(0xffffffffu, m_, off);
       if (ob < b_ || (ob == b_ && om < m_)) { b_ = ob; m_ = om; }
     }
-    if (l == 0) a.codes[rowoff(a.omap, r0 + r) + (int64_t)i * a.gstride] = (uint16_t)m_;
+    if (l == 0) {
+      if (a.pcodes)  // packed 13-bit strip (f3(ii))
+        put_code13(a.pcodes + (rowoff(a.psmap, r0 + r) + i) * a.strip_bytes, a.pn_cap, a.ptok, (uint32_t)m_);
+      else
+        a.codes[rowoff(a.omap, r0 + r) + (int64_t)i * a.gstride] = (uint16_t)m_;
+    }
   }
   // fused append of the rows' values (hc_append_kv): group-0 CTAs copy 16 B per thread
   if (a.vsrc && i == 0) {
@@ -164,6 +169,43 @@ __global__ void __launch_bounds__(256) k_rowcopy(RowCopyArgs a) {
 cudaError_t launch_rowcopy(const RowCopyArgs &a, cudaStream_t s) {
   if (a.rows <= 0) return cudaSuccess;
   launch_chain(k_rowcopy, dim3((unsigned)((a.rows + 7) / 8)), dim3(256), 0, s, a);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// u16 strips -> packed 13-bit strips: one thread per (strip, 8 consecutive tokens); full
+// groups are plain stores (8 B lo, 4 B nibbles, 1 B bits), a ragged last group read-
+// modify-writes only its tokens
+__global__ void __launch_bounds__(256) k_pack13(const uint16_t *src, int64_t strips, int64_t n,
+                                                int64_t src_stride, uint8_t *dst, int64_t n_cap) {
+  const int64_t groups = (n + 7) / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= strips * groups) return;
+  const int64_t s = idx / groups, t0 = (idx - s * groups) * 8;
+  const uint16_t *sp = src + s * src_stride + t0;
+  uint8_t *strip = dst + s * (n_cap * 13 / 8);
+  if (t0 + 8 <= n) {
+    uint32_t lo0 = 0, lo1 = 0, nib = 0, bit = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t c = sp[u];
+      if (u < 4) lo0 |= (c & 0xffu) << (8 * u); else lo1 |= (c & 0xffu) << (8 * (u - 4));
+      nib |= ((c >> 8) & 15u) << (4 * u);
+      bit |= ((c >> 12) & 1u) << u;
+    }
+    *reinterpret_cast<uint2 *>(strip + t0) = make_uint2(lo0, lo1);
+    *reinterpret_cast<uint32_t *>(strip + n_cap + t0 / 2) = nib;
+    strip[n_cap + n_cap / 2 + t0 / 8] = (uint8_t)bit;
+  } else {
+    for (int64_t t = t0; t < n; ++t) put_code13(strip, n_cap, t, sp[t - t0]);
+  }
+}
+
+cudaError_t launch_pack13(const uint16_t *src, int64_t strips, int64_t n, int64_t src_stride,
+                          uint8_t *dst, int64_t n_cap, cudaStream_t s) {
+  const int64_t tot = strips * ((n + 7) / 8);
+  if (tot <= 0) return cudaSuccess;
+  k_pack13<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(src, strips, n, src_stride, dst, n_cap);
   note_launch();
   return cudaGetLastError();
 }

@@ -60,6 +60,11 @@ struct EncodeArgs {
   // bulk encode only: optional row gather (key row of r = kidx[r], valid if < n_keys)
   const int64_t *kidx;
   int64_t n_keys;
+  // packed 13-bit codes (f3(ii)): if pcodes, row r's group-i code goes to token ptok of
+  // strip psmap(r) + i (strip_bytes each, n_cap tokens) instead of codes/omap
+  uint8_t *pcodes;
+  RowMap psmap;
+  int64_t strip_bytes, pn_cap, ptok;
 };
 cudaError_t launch_encode(const EncodeArgs &a, cudaStream_t s);
 // many rows: codebook slice staged in shared memory, rows per thread (hc_kmeans.cu)
@@ -89,6 +94,9 @@ struct LayerArgs {
   const float *C;         // layer codebook [cbg][c][dbar]
   const uint16_t *codes;  // layer 0 of batch 0 base + l*Hkv*g*n_cap ; batch stride below
   int64_t code_b_stride;  // elements between batches
+  const uint8_t *pcodes;  // packed 13-bit codes (f3(ii)) at layer l, batch 0; null = u16 codes
+  int64_t pc_b_stride;    // bytes between batches
+  int64_t strip_bytes;    // bytes per (b, l, kv, group) strip = 13 n_cap / 8
   const uint16_t *res_k;  // [B][L][Hkv][W][d] at layer l (batch stride below)
   const uint16_t *res_v;
   int64_t res_b_stride;   // elements between batches
@@ -166,6 +174,10 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st);
+
+// f3(ii) packed codes (hc_encode.cu)
+cudaError_t launch_pack13(const uint16_t *src, int64_t strips, int64_t n, int64_t src_stride,
+                          uint8_t *dst, int64_t n_cap, cudaStream_t s);
 
 // R8 shared per-KV-head selection (hc_group.cu): sel_idx / sel_w / hs.ksel of the G rows
 int grp_chunks(int64_t n);

@@ -37,6 +37,21 @@ __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
   return v;
 }
 
+// packed 13-bit code planes (f3(ii)): 8 tokens = 8 B lo + 4 B nibbles + 1 B bits
+__device__ __forceinline__ uint4 ld_raw13(const uint8_t *strip, int64_t n_cap, int64_t tok) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint32_t lo0, lo1, nib;
+  uint16_t bit;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+               : "=r"(lo0), "=r"(lo1) : "l"(strip + tok), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(nib) : "l"(strip + n_cap + tok / 2), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+               : "=h"(bit) : "l"(strip + n_cap + n_cap / 2 + tok / 8), "l"(pol));
+  return make_uint4(lo0, lo1, nib, (uint32_t)bit);
+}
+
 template <int G>
 struct Lut;
 // Head pairs share a 32-bit word w = (odd head, signed) << 16 | (even head + 32768) (k_table).
@@ -353,11 +368,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles
 struct ScanCursor {
   int item, i, ng;
   const uint16_t *P;  // this thread's code pointer at group i0 of `item`
+  const uint8_t *Pb;  // packed codes: the strip of group i0 of `item`
   const uint8_t *T;   // table slice of group i0 of `item`
   int64_t tile0;
 };
 
-template <int G, int TPT>
+template <int G, int TPT, bool P13>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int tiles_per_unit,
                                                                 int total_tiles, int nsplit) {
   constexpr int kChunks = TPT / 8;
@@ -394,6 +410,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
       c.tile0 = (int64_t)tk * kTile;
       c.P = a.codes + (int64_t)b * a.code_b_stride + ((int64_t)kv * a.g + i0) * a.n_cap + c.tile0 +
             woff + lane * 8;
+      if (P13) c.Pb = a.pcodes + (int64_t)b * a.pc_b_stride + ((int64_t)kv * a.g + i0) * a.strip_bytes;
       c.T = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
     }
   };
@@ -404,8 +421,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
     const bool live = c.item < total_tiles;
 #pragma unroll
     for (int k = 0; k < kChunks; ++k) {
-      const bool v = live && c.tile0 + woff + k * 256 + lane * 8 < a.n_q;
-      r[k] = v ? ld_stream(c.P + (int64_t)c.i * a.n_cap + k * 256) : make_uint4(0, 0, 0, 0);
+      const int64_t tok = c.tile0 + woff + k * 256 + lane * 8;
+      const bool v = live && tok < a.n_q;
+      if (P13)
+        r[k] = v ? ld_raw13(c.Pb + (int64_t)c.i * a.strip_bytes, a.n_cap, tok) : make_uint4(0, 0, 0, 0);
+      else
+        r[k] = v ? ld_stream(c.P + (int64_t)c.i * a.n_cap + k * 256) : make_uint4(0, 0, 0, 0);
     }
   };
   // one thread: bulk-copy c's slice into `slot`.  No proxy fence: every generic read of the
@@ -454,7 +475,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
       ph ^= 1u << slot;
       const uint8_t *sb = tbuf + slot * slice_bytes;
 #pragma unroll
-      for (int k = 0; k < kChunks; ++k) lookup8<G>(rc0[k], sb, mask, acc[k]);
+      for (int k = 0; k < kChunks; ++k) lookup8<G>(P13 ? unpack13(rc0[k]) : rc0[k], sb, mask, acc[k]);
       // Release the slot; the last warp out refills it with step + 3.  Every lookup result
       // has been consumed (the empty asm statements take all accumulators as inputs), so
       // this warp's reads of the slot are complete before its counter increment issues.
@@ -781,7 +802,7 @@ static int scan_pipelined() {
   return v;
 }
 
-template <int G, int TPT>
+template <int G, int TPT, bool P13>
 static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   constexpr int kTile = kScanThreads * TPT;
   const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
@@ -794,7 +815,7 @@ static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan_pipe<G, TPT>,
+    cudaError_t e = cudaFuncSetAttribute(k_scan_pipe<G, TPT, P13>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     if (e != cudaSuccess) return e;
     configured[dev] = 1;
@@ -806,7 +827,7 @@ static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cap);
   const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  launch_chain(k_scan_pipe<G, TPT>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
+  launch_chain(k_scan_pipe<G, TPT, P13>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
@@ -855,8 +876,10 @@ static int scan_codes_in_regs() {
 template <int G>
 static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
   const int rc = scan_codes_in_regs();
+  if (a.pcodes)  // packed 13-bit codes: pipelined kernel only
+    return a.scan_tpt == 8 ? scan_pipe_launch<G, 8, true>(a, s) : scan_pipe_launch<G, 16, true>(a, s);
   if (rc && scan_pipelined())
-    return a.scan_tpt == 8 ? scan_pipe_launch<G, 8>(a, s) : scan_pipe_launch<G, 16>(a, s);
+    return a.scan_tpt == 8 ? scan_pipe_launch<G, 8, false>(a, s) : scan_pipe_launch<G, 16, false>(a, s);
   if (a.scan_tpt == 8) return rc ? scan_launch<G, 8, 1>(a, s) : scan_launch<G, 8, 0>(a, s);
   return rc ? scan_launch<G, 16, 1>(a, s) : scan_launch<G, 16, 0>(a, s);
 }

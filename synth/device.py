@@ -45,15 +45,17 @@ def _keys(seed, tag, shape_prefix, extra):
     return np.array(ks, dtype=np.uint64)
 
 
-def fill_codes(codes, seed: int, c: int, n: int, layers=None, start: int = 0):
+def fill_codes(codes, seed: int, c: int, n: int, layers=None, start: int = 0, layer_ids=None):
     """codes: torch int16 cuda [B][L][Hkv][g][n_cap]; fill local positions [0, n) of the given
-    layers (default all) with synth.gen_codes streams of GLOBAL positions [start, start+n)."""
+    layers (default all) with synth.gen_codes streams of GLOBAL positions [start, start+n).
+    layer_ids: the stream's layer index per filled slot (default: the slot index)."""
     import torch
     B, L, H, g, ncap = codes.shape
-    layers = range(L) if layers is None else layers
+    layers = list(range(L) if layers is None else layers)
+    ids = layers if layer_ids is None else list(layer_ids)
     s = torch.cuda.current_stream().cuda_stream
-    for l in layers:
-        keys = np.array([stream_key(seed, TAG_P, b, l, kv, i)
+    for l, lid in zip(layers, ids):
+        keys = np.array([stream_key(seed, TAG_P, b, lid, kv, i)
                          for b in range(B) for kv in range(H) for i in range(g)], dtype=np.uint64)
         kt = torch.from_numpy(keys.view(np.int64)).to(codes.device)
         for b in range(B):

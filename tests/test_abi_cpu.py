@@ -35,7 +35,7 @@ def test_struct_layout_matches_header(tmp_path):
     """ctypes mirrors of the C structs agree with the C compiler's layout (gcc, same header)."""
     import subprocess
     import paper_2507_19823_b200 as hc
-    fields = {"hc_vq": ["d", "g", "c", "cbg", "lut_bits"],
+    fields = {"hc_vq": ["d", "g", "c", "cbg", "lut_bits", "code_bits"],
               "hc_budget": ["tau", "k_max", "renorm", "select_only"],
               "hc_kcache": ["B", "L", "Hkv", "G", "vq", "n_cap", "codes", "codebook", "cb_absmax",
                             "res_cap", "res_k", "res_v", "n_q", "n_res"],
