@@ -62,6 +62,7 @@ def lib():
             L.or_select_float.argtypes = [p, i64, i32, f32, i64, i32, p, p, p]
             L.or_select_float.restype = i32
             L.or_gather.argtypes = [p, p, i64, p, i32, p]
+            L.or_blockwise_attention.argtypes = [p, p, p, i64, i32, i32, i32, i64, p]
             L.or_kmeans_step.argtypes = [p, i64, i32, i32, i32, i32, p, i64, p, p, p]
             L.or_select_shared.argtypes = [p, i32, i64, p, i32, f32, i64, p, p, p, p, p, p]
             L.or_exact_attention.argtypes = [p, p, p, i64, i32, p]
@@ -242,6 +243,18 @@ def gather(idx, w, V) -> np.ndarray:
     idx = _c(idx, np.int32); w = _c(w, np.float64); V = _c(V, np.float16)
     out = np.empty(V.shape[1], dtype=np.float64)
     lib().or_gather(_ptr(idx), _ptr(w), idx.shape[0], _ptr(V.view(np.uint16)), V.shape[1], _ptr(out))
+    return out
+
+
+def blockwise_attention(q, k, v, bs: int) -> np.ndarray:
+    """f4 (iii), App. B: anchor-block + causal local-block prefill attention.
+    q [n][Hq][d], k, v [n][Hkv][d] fp16 -> out [n][Hq][d] double."""
+    q = _c(q, np.float16); k = _c(k, np.float16); v = _c(v, np.float16)
+    n, Hq, d = q.shape
+    Hkv = k.shape[1]
+    out = np.empty((n, Hq, d), dtype=np.float64)
+    lib().or_blockwise_attention(_ptr(q.view(np.uint16)), _ptr(k.view(np.uint16)), _ptr(v.view(np.uint16)),
+                                 n, Hq, Hkv, d, bs, _ptr(out))
     return out
 
 

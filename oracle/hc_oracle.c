@@ -581,6 +581,53 @@ OR_EXPORT void or_exact_attention(const uint16_t *q, const uint16_t *K, const ui
 }
 
 /* ------------------------------------------------------------------------
+ * f4 (iii) -- App. B "Enhanced prefilling with block-wise attention": the
+ * prompt is cut into blocks of bs tokens; "attention is computed exclusively between a
+ * designated anchor block and the current processing block".  Reading (DESIGN F5): the
+ * anchor is block 0; query i of block kb = i / bs attends to the keys j with
+ *   j <= i                      if kb == 0 (causal inside the anchor block),
+ *   j < bs  or  kb*bs <= j <= i otherwise (the whole anchor + causal inside its block),
+ * with softmax(q·k/√d) in double (Eq. 1 restricted to that key set).  q [n][Hq][d],
+ * k, v [n][Hkv][d] fp16, query head h uses KV head h / (Hq/Hkv); out [n][Hq][d] double.
+ * ---------------------------------------------------------------------- */
+OR_EXPORT void or_blockwise_attention(const uint16_t *q, const uint16_t *k, const uint16_t *v,
+                                      int64_t n, int Hq, int Hkv, int d, int64_t bs, double *out)
+{
+    const int G = Hq / Hkv;
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+    for (int64_t i = 0; i < n; ++i)
+        for (int h = 0; h < Hq; ++h) {
+            const int kv = h / G;
+            const int64_t kb = i / bs;
+            double *z = (double *)malloc(sizeof(double) * (size_t)(i + 1));
+            char *ok = (char *)malloc((size_t)(i + 1));
+            double M = -INFINITY;
+            for (int64_t j = 0; j <= i; ++j) {
+                ok[j] = (char)(kb == 0 || j < bs || j >= kb * bs);
+                if (!ok[j]) continue;
+                double acc = 0.0;
+                for (int e = 0; e < d; ++e)
+                    acc += (double)or_h2f(q[(i * Hq + h) * d + e]) * (double)or_h2f(k[(j * Hkv + kv) * d + e]);
+                z[j] = acc / sqrt((double)d);
+                if (z[j] > M) M = z[j];
+            }
+            double S = 0.0;
+            for (int64_t j = 0; j <= i; ++j)
+                if (ok[j]) {
+                    z[j] = exp(z[j] - M);
+                    S += z[j];
+                }
+            double *o = out + (i * Hq + h) * d;
+            for (int e = 0; e < d; ++e) o[e] = 0.0;
+            for (int64_t j = 0; j <= i; ++j)
+                if (ok[j])
+                    for (int e = 0; e < d; ++e) o[e] += (z[j] / S) * (double)or_h2f(v[(j * Hkv + kv) * d + e]);
+            free(z);
+            free(ok);
+        }
+}
+
+/* ------------------------------------------------------------------------
  * One decode unit (batch b, layer l, KV head kv) for its G GQA query heads
  * (head h of the unit uses KV head kv, DESIGN R7), steps R2 -> R6 in the
  * paper's order.  Candidates j in [0, nq) are quantized (codes P, group-major,

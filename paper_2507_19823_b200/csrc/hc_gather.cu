@@ -210,8 +210,11 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   __shared__ float red[(kRT / 32) * 2 * 128];
   pdl_trigger();
   pdl_wait();
-  const int row = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
-  const int b = row / a.Hq, hq = row - b * a.Hq, kv = hq / a.G;
+  // grid (G, chunk, unit): the G heads of a KV head read their c-th kept chunks back to back
+  // -- those cover about the same token range, so rows kept by several heads hit in L2
+  const int u = blockIdx.z, ch = blockIdx.y, tid = threadIdx.x;
+  const int b = u / a.Hkv, kv = u - b * a.Hkv;
+  const int row = b * a.Hq + kv * a.G + blockIdx.x;
   const int64_t k = a.hs[row].ksel;
   const int64_t e0 = (int64_t)ch * kRC;
   if (e0 >= k) return;  // only the ceil(k/kRC) CTAs holding kept rows take part
@@ -300,7 +303,7 @@ cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, u
   const int nch = gather_rows_chunks(k_cap);
   if (nch == 0) return cudaSuccess;
   // CTAs beyond a row's k_sel exit at once (they only count if they hold kept rows)
-  dim3 grid((unsigned)nch, (unsigned)(a.B * a.Hq));
+  dim3 grid((unsigned)a.G, (unsigned)nch, (unsigned)(a.B * a.Hkv));
   launch_chain(k_gather_rows, grid, dim3(kRT), 0, s, a, nch, part, done);
   note_launch();
   return cudaGetLastError();

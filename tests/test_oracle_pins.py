@@ -392,6 +392,46 @@ def test_select_float_spec_examples(orc):
     assert r["w"][0] == 1.0 and r["w"][1] == 0.0
 
 
+# ---------------------------------------------------------------- f4 block-wise prefill (App. B)
+def test_blockwise_one_block_is_causal_attention(orc):
+    """bs >= n: the anchor block is the whole prompt -> plain causal attention, i.e. Eq. 1
+    over the prefix (or_exact_attention, pinned above), per query and head (GQA 2)."""
+    rng = _rng(81)
+    n, Hq, Hkv, d = 40, 4, 2, 32
+    q = rng.standard_normal((n, Hq, d)).astype(np.float16)
+    k = rng.standard_normal((n, Hkv, d)).astype(np.float16)
+    v = rng.standard_normal((n, Hkv, d)).astype(np.float16)
+    out = orc.blockwise_attention(q, k, v, 64)
+    for i in (0, 1, 17, 39):
+        for h in range(Hq):
+            ref = orc.exact_attention(q[i, h], k[: i + 1, h // 2], v[: i + 1, h // 2])
+            assert np.allclose(out[i, h], ref, rtol=1e-12, atol=1e-12)
+
+
+def test_blockwise_anchor_plus_local_keys(orc):
+    """Query i of block kb >= 1 sees exactly the anchor block and its own block's prefix:
+    equal to Eq. 1 over that gathered key list, and blind to every other key (perturbing
+    them leaves the output bit-identical)."""
+    rng = _rng(82)
+    n, Hq, Hkv, d, bs = 50, 2, 1, 16, 12
+    q = rng.standard_normal((n, Hq, d)).astype(np.float16)
+    k = rng.standard_normal((n, Hkv, d)).astype(np.float16)
+    v = rng.standard_normal((n, Hkv, d)).astype(np.float16)
+    out = orc.blockwise_attention(q, k, v, bs)
+    for i in (12, 13, 30, 49):
+        kb = i // bs
+        keys = list(range(bs)) + list(range(kb * bs, i + 1))
+        for h in range(Hq):
+            ref = orc.exact_attention(q[i, h], k[keys, 0], v[keys, 0])
+            assert np.allclose(out[i, h], ref, rtol=1e-12, atol=1e-12)
+    k2, v2 = k.copy(), v.copy()
+    k2[bs:2 * bs] = rng.standard_normal((bs, Hkv, d))  # block 1: invisible to blocks >= 2
+    v2[bs:2 * bs] = rng.standard_normal((bs, Hkv, d))
+    out2 = orc.blockwise_attention(q, k2, v2, bs)
+    assert np.array_equal(out[2 * bs:], out2[2 * bs:])
+    assert not np.array_equal(out[bs:2 * bs], out2[bs:2 * bs])
+
+
 # ---------------------------------------------------------------- f4 MiniBatchKMeans step (P:356)
 def test_kmeans_first_step_is_cluster_mean_and_matches_sklearn(orc):
     """With v = 0 the step is one Lloyd iteration: every assigned centre becomes the mean of
