@@ -178,6 +178,23 @@ hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *code
  * is independent of thread order.  ws >= hc_kmeans_workspace_bytes(vq, b). */
 size_t hc_kmeans_workspace_bytes(hc_vq vq, int64_t b);
 
+/* NEXT f4 (iii) -- App. B block-wise prefill attention (DESIGN F5): query i of
+ * block kb = i / bs attends to the anchor block (keys j < bs) and causally to its own block
+ * (kb*bs <= j <= i); block 0 is causal.  out[i][h] = softmax over that key set of
+ * q[i][h]·k[j][h/(Hq/Hkv)] / sqrt(d), applied to v.  q [n][Hq][d], k, v [n][Hkv][d] fp16,
+ * out [n][Hq][d] fp32 (device).  d = 128, bs % 64 == 0, Hq % Hkv == 0. */
+hc_status hc_blockwise_attention(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,
+                                 int32_t Hq, int32_t Hkv, int32_t d, int64_t bs, float *out,
+                                 hc_stream_t stream);
+
+/* Prefill append: "when a block operation concludes, the quantization of the key cache"
+ * -- encode n new keys per sequence (R1, bulk encoder) into codes positions
+ * [n_q, n_q + n) of `layer` and copy their values into the value store; n_q += n.
+ * k, v [B][n][Hkv][d] fp16 (device).  16-bit codes, no resident window in use
+ * (n_res == 0), else HC_ERR_UNSUPPORTED; HC_ERR_CAPACITY if n_q + n > n_cap. */
+hc_status hc_prefill_append(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const uint16_t *k,
+                            const uint16_t *v, int64_t n, hc_stream_t stream);
+
 /* Pack u16 codes into the 13-bit strip layout (code_bits = 13, above): for s < strips,
  * t < n: strip s of dst (HC_STRIP13_BYTES(n_cap) bytes each) gets src[s*src_stride + t].
  * Codes must be < 8192 (HC_ERR_RANGE is not checked on the device: higher bits are

@@ -26,7 +26,7 @@ EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_ev
            "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
            "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
            "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish", "hc_kmeans_workspace_bytes",
-           "hc_kmeans_step", "hc_pack_codes13"]
+           "hc_kmeans_step", "hc_pack_codes13", "hc_blockwise_attention", "hc_prefill_append"]
 
 
 class HcError(RuntimeError):
@@ -100,6 +100,10 @@ def lib():
         L.hc_host_weighted_sum.restype = i32
         L.hc_enqueue_host_weighted_sum.argtypes = hw + [p]
         L.hc_enqueue_host_weighted_sum.restype = i32
+        L.hc_blockwise_attention.argtypes = [p, p, p, i64, i32, i32, i32, i64, p, p]
+        L.hc_blockwise_attention.restype = i32
+        L.hc_prefill_append.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, i64, p]
+        L.hc_prefill_append.restype = i32
         L.hc_pack_codes13.argtypes = [p, i64, i64, i64, p, i64, p]
         L.hc_pack_codes13.restype = i32
         L.hc_kmeans_workspace_bytes.argtypes = [hc_vq, i64]
@@ -190,6 +194,18 @@ def kmeans_step(keys, sample, codebook, counts, g: int, labels=None, ws=None, st
                               _ptr(ws.t), ws.nbytes, _stream(stream))
     _check(st)
     return codebook, counts
+
+
+def blockwise_attention(q, k, v, bs: int, out=None, stream=None):
+    """f4 (iii), App. B: q [n][Hq][d], k, v [n][Hkv][d] fp16 (cuda) -> out [n][Hq][d] fp32."""
+    import torch
+    n, Hq, d = q.shape
+    Hkv = k.shape[1]
+    if out is None:
+        out = torch.empty((n, Hq, d), dtype=torch.float32, device=q.device)
+    _check(lib().hc_blockwise_attention(_ptr(q), _ptr(k), _ptr(v), n, Hq, Hkv, d, bs, _ptr(out),
+                                        _stream(stream)))
+    return out
 
 
 def pack_codes13(codes16, n: int, n_cap: int, out=None, stream=None):
@@ -323,6 +339,13 @@ class KCache:
         strips = self.B * self.L * self.Hkv * self.g
         _check(lib().hc_pack_codes13(_ptr(codes16), strips, n, codes16.shape[-1], _ptr(self.codes),
                                      self.n_cap, _stream(stream)))
+
+    def prefill_append(self, layer, k, v, vstore, stream=None):
+        """hc_prefill_append: k, v [B][n][Hkv][d] fp16 (cuda) -> codes / values at
+        positions [n_q, n_q + n) of `layer` (bulk R1 encode)."""
+        vs = vstore.struct()
+        _check(lib().hc_prefill_append(C.byref(self.s), C.byref(vs), layer, _ptr(k), _ptr(v),
+                                       k.shape[1], _stream(stream)))
 
     def set_counts(self, layer, n_q, n_res=0):
         self.s.n_q[layer] = n_q

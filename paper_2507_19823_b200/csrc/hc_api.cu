@@ -246,6 +246,55 @@ hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *code
                     "hc_quantize_keys");
 }
 
+hc_status hc_blockwise_attention(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,
+                                 int32_t Hq, int32_t Hkv, int32_t d, int64_t bs, float *out,
+                                 hc_stream_t stream) {
+  if (n < 0 || bs <= 0 || Hq <= 0 || Hkv <= 0) return fail(HC_ERR_ARG, "bad n / bs / heads");
+  if (d != 128) return fail(HC_ERR_UNSUPPORTED, "blockwise attention is built for d = 128");
+  if (bs % 64) return fail(HC_ERR_SHAPE, "bs must be a multiple of 64");
+  if (Hq % Hkv) return fail(HC_ERR_SHAPE, "Hq %% Hkv != 0");
+  if (n == 0) return HC_OK;
+  if (!q || !k || !v || !out) return fail(HC_ERR_ARG, "NULL pointer");
+  return cuda_check(launch_blockwise_attn(q, k, v, n, Hq, Hkv, bs, out, (cudaStream_t)stream),
+                    "hc_blockwise_attention");
+}
+
+hc_status hc_prefill_append(hc_kcache *kc, const hc_vstore *vs, int32_t layer, const uint16_t *k,
+                            const uint16_t *v, int64_t n, hc_stream_t stream) {
+  hc_status st = check_kcache(kc);
+  if (st) return st;
+  if (!vs || !vs->base) return fail(HC_ERR_ARG, "vstore is NULL");
+  if (vs->n_cap != kc->n_cap) return fail(HC_ERR_SHAPE, "vstore.n_cap != kcache.n_cap");
+  if (layer < 0 || layer >= kc->L) return fail(HC_ERR_RANGE, "layer %d out of range", layer);
+  if (n < 0) return fail(HC_ERR_ARG, "n < 0");
+  if (n == 0) return HC_OK;
+  if (!k || !v) return fail(HC_ERR_ARG, "k/v NULL");
+  if (kc->vq.code_bits == 13) return fail(HC_ERR_UNSUPPORTED, "prefill append writes 16-bit codes");
+  if (kc->n_res[layer] != 0) return fail(HC_ERR_UNSUPPORTED, "prefill append with a non-empty window");
+  const int64_t B = kc->B, L = kc->L, H = kc->Hkv, d = kc->vq.d, g = kc->vq.g, ncap = kc->n_cap;
+  const int64_t nq = kc->n_q[layer];
+  if (nq + n > ncap) return fail(HC_ERR_CAPACITY, "layer %d: %lld + %lld > n_cap", layer, (long long)nq, (long long)n);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t b = 0; b < B; ++b) {  // rows r = t * Hkv + kv of sequence b
+    EncodeArgs a{};
+    a.keys = k;
+    a.kmap = RowMap{1, d, 0, b * n * H * d};
+    a.rows = n * H;
+    a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
+    a.d = (int)d; a.g = (int)g; a.c = kc->vq.c; a.cbg = kc->vq.cbg;
+    a.codes = kc->codes;
+    a.omap = RowMap{H, 1, g * ncap, ((b * L + layer) * H) * g * ncap + nq};
+    a.gstride = ncap;
+    cudaError_t e = a.rows >= 1024 ? launch_encode_bulk(a, s) : launch_encode(a, s);
+    if (e != cudaSuccess) return cuda_check(e, "hc_prefill_append encode");
+    RowCopyArgs c{v, RowMap{1, d, 0, b * n * H * d}, vs->base,
+                  RowMap{H, d, ncap * d, ((b * L + layer) * H * ncap + nq) * d}, n * H, (int)d};
+    if ((e = launch_rowcopy(c, s)) != cudaSuccess) return cuda_check(e, "hc_prefill_append values");
+  }
+  kc->n_q[layer] = nq + n;
+  return HC_OK;
+}
+
 hc_status hc_pack_codes13(const uint16_t *src, int64_t strips, int64_t n, int64_t src_stride,
                           uint8_t *dst, int64_t n_cap, hc_stream_t stream) {
   if (strips < 0 || n < 0) return fail(HC_ERR_ARG, "strips/n < 0");

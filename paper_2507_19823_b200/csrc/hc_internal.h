@@ -175,6 +175,10 @@ cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st);
 
+// f4 (iii) App. B block-wise prefill attention (hc_prefill.cu), d = 128
+cudaError_t launch_blockwise_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,
+                                  int Hq, int Hkv, int64_t bs, float *out, cudaStream_t s);
+
 // f3(ii) packed codes (hc_encode.cu)
 cudaError_t launch_pack13(const uint16_t *src, int64_t strips, int64_t n, int64_t src_stride,
                           uint8_t *dst, int64_t n_cap, cudaStream_t s);

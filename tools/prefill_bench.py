@@ -50,8 +50,31 @@ def main():
     torch.cuda.synchronize()
     km = {"what": "kmeans step", "batch": b, "ms": e0.elapsed_time(e1) / reps,
           "iters_200_s": e0.elapsed_time(e1) / reps * 200 / 1e3}
+    # App. B block-wise prefill attention, one Llama-3-8B layer (32 q heads, 8 KV heads)
+    n, Hq, Hkv, bs = int(os.environ.get("PF_N", 131072)), 32, 8, int(os.environ.get("PF_BS", 4096))
+    q = torch.randn((n, Hq, d), device="cuda").half() * 0.5
+    k = torch.randn((n, Hkv, d), device="cuda").half() * 0.5
+    v = torch.randn((n, Hkv, d), device="cuda").half()
+    out = torch.empty((n, Hq, d), device="cuda")
+    for _ in range(2):
+        hc.blockwise_attention(q, k, v, bs, out=out)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        hc.blockwise_attention(q, k, v, bs, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    keys = 0  # visited (query, key) pairs of one head, causal within blocks
+    for i0 in range(0, n, 64):
+        kb = i0 // bs
+        keys += 64 * ((bs if kb else 0) + (i0 + 64 - kb * bs))
+    flops = 4.0 * d * keys * Hq  # QK^T and PV, 2 flops per MAC
+    att = {"what": "blockwise attention (App. B)", "n": n, "bs": bs, "Hq": Hq, "Hkv": Hkv, "ms": ms,
+           "tflops": flops / ms / 1e9, "frac_of_dense_bf16_2250": flops / ms / 1e9 / 2250.0}
     print(json.dumps(enc))
     print(json.dumps(km))
+    print(json.dumps(att))
 
 
 if __name__ == "__main__":
