@@ -137,6 +137,28 @@ __device__ __forceinline__ uint4 unpack13(const uint4 &raw) {
   }
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
+
+// mass_d() as two 32-bit words, branch-free (the P1 histogram's hot loop): every step is
+// the same exact operation as in mass_d; delta <= 2^23 (|z̃| <= 2^22, g <= 128).
+__device__ __forceinline__ void mass_parts(uint32_t delta, float kappa, uint32_t &lo, uint32_t &hi) {
+  const float df = __fsub_rn(__int_as_float(0x4B000000 + (int)delta), 8388608.0f);
+  const float x0 = -__fmul_rn(df, kappa);
+  const float x = fmaxf(x0, -64.0f);  // keeps 2^(40+n) normal; x0 < -40 -> 0 below
+  const float r = __fadd_rn(x, 12582912.0f);
+  float nf = __fsub_rn(r, 12582912.0f);
+  const bool adj = nf > x;
+  nf = adj ? __fsub_rn(nf, 1.0f) : nf;
+  const int ni = __float_as_int(r) - 0x4B400000 - (adj ? 1 : 0);
+  const float v = __fmul_rn(exp2_poly(__fsub_rn(x, nf)), pow2f(40 + ni));
+  const uint32_t b = __float_as_uint(v);
+  const int sh = (int)(b >> 23) - 150;  // v = m * 2^sh, m in [2^23, 2^24)
+  const uint32_t m = (b & 0x7FFFFFu) | 0x800000u;
+  uint32_t l = sh >= 0 ? (m << sh) : (sh > -32 ? (m >> -sh) : 0u);
+  uint32_t h = sh > 8 ? (m >> (32 - sh)) : 0u;
+  const bool zero = x0 < -40.0f;
+  lo = zero ? 0u : l;
+  hi = zero ? 0u : h;
+}
 #endif
 
 // R5: Θ = ceil(τ_q · S / 2^24)  (τ_q <= 2^24, S < 2^63)

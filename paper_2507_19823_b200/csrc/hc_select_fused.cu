@@ -208,14 +208,11 @@ __global__ void __launch_bounds__(kFT, kOcc)
     const uint32_t dl = (uint32_t)(M - zint(zf));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
-    const uint64_t W = mass_d(dl, kappa);
-    if (W) {
-      const uint32_t wl = (uint32_t)W;
-      uint32_t wh = (uint32_t)(W >> 32);
-      const uint32_t old = atomicAdd(&mlo[bk], wl);
-      wh += (old + wl < old) ? 1u : 0u;  // carry out of the low word
-      if (wh) atomicAdd(&mhi[bk], wh);
-    }
+    uint32_t wl, wh;
+    mass_parts(dl, kappa, wl, wh);
+    const uint32_t old = atomicAdd(&mlo[bk], wl);
+    wh += (old + wl < old) ? 1u : 0u;  // carry out of the low word
+    if (wh) atomicAdd(&mhi[bk], wh);
   });
   cl.sync();
   for (int i = tid; i < nbo; i += kFT) {  // sum my owned bins over the peers
