@@ -112,7 +112,7 @@ struct Layout {
   int64_t z_stride;
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
-      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, total;
+      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, total;
   int nch_max;  // sharded compaction chunks
 };
 
@@ -146,6 +146,7 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
     const int64_t nchr = gather_rows_chunks(L.k_eff);
     L.o_rpart = o; o += align256((size_t)rows * nchr * 128 * 4);
     L.o_rdone = o; o += align256((size_t)rows * 4);
+    L.o_grange = o; o += align256((size_t)rows * 16);  // sharded finish: list slice per row
     if (shared) {  // R8 shared selection state, 4-level histograms, chunk counts
       L.o_grp = o; o += align256((size_t)units * sizeof(GroupState));
       L.o_ghist = o; o += align256((size_t)units * 4 * kNB * 16);
@@ -680,7 +681,8 @@ hc_status hc_shard_finish(const hc_kcache *kc, const hc_vstore *vs, int32_t laye
   uint8_t *w8 = (uint8_t *)ws;
   cudaError_t e = launch_shard_finish(a, sa, (const uint32_t *)(w8 + Lw.o_chunk),
                                       (const unsigned long long *)allcnt, rank, shard_base,
-                                      (float *)(w8 + Lw.o_part), out, s);
+                                      (float *)(w8 + Lw.o_part), out, s, (int64_t *)(w8 + Lw.o_grange),
+                                      (float *)(w8 + Lw.o_rpart), (uint32_t *)(w8 + Lw.o_rdone));
   if (e != cudaSuccess) return cuda_check(e, "shard finish");
   if (sel_k) {
     const int rows = a.B * a.Hq;

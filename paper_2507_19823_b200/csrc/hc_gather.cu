@@ -215,14 +215,15 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   const int u = blockIdx.z, ch = blockIdx.y, tid = threadIdx.x;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int row = b * a.Hq + kv * a.G + blockIdx.x;
-  const int64_t k = a.hs[row].ksel;
+  const int64_t k = a.g_cnt ? a.g_cnt[row] : a.hs[row].ksel;
   const int64_t e0 = (int64_t)ch * kRC;
   if (e0 >= k) return;  // only the ceil(k/kRC) CTAs holding kept rows take part
-  const int32_t *li = a.sel_idx + (int64_t)row * a.k_max;
-  const float *lw = a.sel_w + (int64_t)row * a.k_max;
+  const int64_t off = a.g_cnt ? a.g_off[row] : 0;
+  const int32_t *li = a.sel_idx + (int64_t)row * a.k_max + off;
+  const float *lw = a.sel_w + (int64_t)row * a.k_max + off;
   for (int i = tid; i < kRC; i += kRT) {
     const bool v = e0 + i < k;
-    sj[i] = v ? li[e0 + i] : -1;
+    sj[i] = v ? (int32_t)(li[e0 + i] - a.g_base) : -1;
     sw[i] = v ? lw[e0 + i] : 0.0f;
   }
   __syncthreads();

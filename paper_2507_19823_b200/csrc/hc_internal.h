@@ -135,6 +135,10 @@ struct LayerArgs {
   // between the chain kernels)
   uint32_t *gdone;
   int gdone_n;
+  // k_gather_rows on a sub-range of each row's list (sequence-sharded finish): entries
+  // [g_off[row], g_off[row] + g_cnt[row]) with local token index = sel_idx - g_base
+  const int64_t *g_off, *g_cnt;
+  int64_t g_base;
 };
 
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);
@@ -173,7 +177,8 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
                                 uint32_t *chunk, unsigned long long *cnt, cudaStream_t st);
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
-                                float *part, float *out, cudaStream_t st);
+                                float *part, float *out, cudaStream_t st, int64_t *grange = nullptr,
+                                float *rpart = nullptr, uint32_t *rdone = nullptr);
 
 // f4 (iii) App. B block-wise prefill attention (hc_prefill.cu), d = 128
 cudaError_t launch_blockwise_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,

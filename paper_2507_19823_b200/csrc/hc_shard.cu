@@ -23,22 +23,40 @@ __device__ __forceinline__ float sh_z(const LayerArgs &a, int row, int64_t j, in
   return a.z[(int64_t)row * a.z_stride + j];  // final after the scan (split scans add into z)
 }
 
+// visit tokens j of a row with 4 consecutive tokens per thread per round (16-B loads; z rows
+// are 64-float aligned), grid-stride over the row's CTAs
+template <typename F>
+__device__ __forceinline__ void sh_tokens(const float *zr, int64_t n, F &&f) {
+  const int64_t n4 = n & ~(int64_t)3;
+  for (int64_t t = ((int64_t)blockIdx.x * kShT + threadIdx.x) * 4; t < n4; t += (int64_t)gridDim.x * kShT * 4) {
+    const float4 v = *reinterpret_cast<const float4 *>(zr + t);
+    f(t, v.x); f(t + 1, v.y); f(t + 2, v.z); f(t + 3, v.w);
+  }
+  if (blockIdx.x == 0)
+    for (int64_t t = n4 + threadIdx.x; t < n; t += kShT) f(t, zr[t]);
+}
+
 // z <- sum of split partials; stats[row] = {max z, -min z} (atomic max)
 __global__ void __launch_bounds__(kShT) k_sh_stats(LayerArgs a, int nsplit, int32_t *stats) {
   const int row = blockIdx.y;
   int mx = INT_MIN, mn = INT_MAX;
-  for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
-    const float zf = sh_z(a, row, j, nsplit);
+  sh_tokens(a.z + (int64_t)row * a.z_stride, a.n_cand, [&](int64_t, float zf) {
     const int zi = zint(zf);
     mx = max(mx, zi);
     mn = min(mn, zi);
-  }
+  });
   mx = __reduce_max_sync(0xffffffffu, mx);
   mn = __reduce_min_sync(0xffffffffu, mn);
   if ((threadIdx.x & 31) == 0 && mx != INT_MIN) {
     atomicMax(&stats[2 * row], mx);
     atomicMax(&stats[2 * row + 1], -mn);
   }
+}
+
+// unsplit scan: the scan epilogue already folded max / min into hs -> no pass over z
+__global__ void k_sh_stats_folded(const HeadState *hs, int32_t *stats, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) { stats[2 * r] = hs[r].M; stats[2 * r + 1] = -hs[r].zmin; }
 }
 
 __global__ void k_sh_init_stats(int32_t *stats, int rows) {
@@ -62,19 +80,16 @@ __global__ void __launch_bounds__(kShT) k_sh_hist1(LayerArgs a, const int32_t *g
   const float kappa = a.hs[row].kappa;
   for (int i = threadIdx.x; i < kNB; i += kShT) { cnt[i] = 0; mlo[i] = 0; mhi[i] = 0; }
   __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
-    const uint32_t dl = (uint32_t)(M - zint(a.z[(int64_t)row * a.z_stride + j]));
+  sh_tokens(a.z + (int64_t)row * a.z_stride, a.n_cand, [&](int64_t, float zf) {
+    const uint32_t dl = (uint32_t)(M - zint(zf));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
-    const uint64_t W = mass_d(dl, kappa);
-    if (W) {
-      const uint32_t wl = (uint32_t)W;
-      uint32_t wh = (uint32_t)(W >> 32);
-      const uint32_t old = atomicAdd(&mlo[bk], wl);
-      wh += (old + wl < old) ? 1u : 0u;
-      if (wh) atomicAdd(&mhi[bk], wh);
-    }
-  }
+    uint32_t wl, wh;
+    mass_parts(dl, kappa, wl, wh);
+    const uint32_t old = atomicAdd(&mlo[bk], wl);
+    wh += (old + wl < old) ? 1u : 0u;
+    if (wh) atomicAdd(&mhi[bk], wh);
+  });
   __syncthreads();
   unsigned long long *hr = h1 + (int64_t)row * kNB * 2;
   for (int i = threadIdx.x; i < kNB; i += kShT) {
@@ -173,10 +188,10 @@ __global__ void __launch_bounds__(kShT) k_sh_hist2(LayerArgs a, unsigned long lo
   for (int i = threadIdx.x; i < kNB; i += kShT) cnt[i] = 0;
   __syncthreads();
   const uint32_t fmask = (1u << h.shift) - 1u;
-  for (int64_t j = (int64_t)blockIdx.x * kShT + threadIdx.x; j < a.n_cand; j += (int64_t)gridDim.x * kShT) {
-    const uint32_t dl = (uint32_t)(h.M - zint(a.z[(int64_t)row * a.z_stride + j]));
+  sh_tokens(a.z + (int64_t)row * a.z_stride, a.n_cand, [&](int64_t, float zf) {
+    const uint32_t dl = (uint32_t)(h.M - zint(zf));
     if ((int)(dl >> h.shift) == h.bstar) atomicAdd(&cnt[dl & fmask], 1u);
-  }
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < kNB; i += kShT)
     if (cnt[i]) atomicAdd(&h2[(int64_t)row * kNB + i], (unsigned long long)cnt[i]);
@@ -242,10 +257,26 @@ __global__ void __launch_bounds__(kShT) k_sh_counts(LayerArgs a, int nch, uint32
   const HeadState h = a.hs[row];
   const int64_t j0 = (int64_t)ch * kShChunk;
   unsigned ns = 0, nt = 0;
-  for (int64_t j = j0 + threadIdx.x; j < j0 + kShChunk && j < a.n_cand; j += kShT) {
-    const uint32_t dl = (uint32_t)(h.M - zint(a.z[(int64_t)row * a.z_stride + j]));
-    ns += dl < h.delta_star;
-    nt += dl == h.delta_star;
+  const float *zr = a.z + (int64_t)row * a.z_stride;
+#pragma unroll
+  for (int k = 0; k < kShChunk / (kShT * 4); ++k) {  // 4 x 16-B loads per thread
+    const int64_t t = j0 + ((int64_t)k * kShT + threadIdx.x) * 4;
+    if (t + 4 <= a.n_cand) {
+      const float4 v = *reinterpret_cast<const float4 *>(zr + t);
+      const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t dl = (uint32_t)(h.M - zint(f[u]));
+        ns += dl < h.delta_star;
+        nt += dl == h.delta_star;
+      }
+    } else {
+      for (int64_t j = t; j < t + 4 && j < a.n_cand; ++j) {
+        const uint32_t dl = (uint32_t)(h.M - zint(zr[j]));
+        ns += dl < h.delta_star;
+        nt += dl == h.delta_star;
+      }
+    }
   }
   ns = __reduce_add_sync(0xffffffffu, ns);
   nt = __reduce_add_sync(0xffffffffu, nt);
@@ -268,9 +299,22 @@ __global__ void __launch_bounds__(kShT) k_sh_counts(LayerArgs a, int nch, uint32
 __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int nch,
                                                    const uint32_t *chunk,
                                                    const unsigned long long *allcnt, int rank,
-                                                   int64_t base, float *part) {
+                                                   int64_t base, float *part, int64_t *grange) {
   const int row = blockIdx.y, ch = blockIdx.x;
   const HeadState h = a.hs[row];
+  if (grange && ch == 0 && threadIdx.x == 0) {  // this rank's slice of the row's kept list
+    unsigned long long sb = 0, tb = 0;
+    for (int r = 0; r < rank; ++r) {
+      sb += allcnt[((int64_t)r * s.rows + row) * 2];
+      tb += allcnt[((int64_t)r * s.rows + row) * 2 + 1];
+    }
+    const unsigned long long sr = allcnt[((int64_t)rank * s.rows + row) * 2];
+    const unsigned long long tr = allcnt[((int64_t)rank * s.rows + row) * 2 + 1];
+    const unsigned long long rt = h.r_ties;
+    const unsigned long long tk = tb >= rt ? 0ull : (rt - tb < tr ? rt - tb : tr);
+    grange[row] = (int64_t)(sb + (tb < rt ? tb : rt));  // [2][rows]: offsets, then counts
+    grange[s.rows + row] = (int64_t)(sr + tk);
+  }
   __shared__ unsigned long long sp[2];
   if (threadIdx.x == 0) {
     unsigned long long ps = 0, pt = 0;
@@ -336,7 +380,7 @@ __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int n
       }
     }
     // Eq. 5 partial: the warp walks its kept rows (lane-order), all lanes read each row
-    unsigned m = bs;
+    unsigned m = grange ? 0u : bs;  // grange: k_gather_rows does Eq. 5 afterwards
     while (m) {
       const int src = __ffs(m) - 1;
       m &= m - 1;
@@ -348,6 +392,7 @@ __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int n
     pos += __popc(bs);
     t_run += __popc(bt);
   }
+  if (grange) return;
   __shared__ float red[kShT / 32][256];
   for (int e = 0; e < dpl; ++e) red[warp][lane * dpl + e] = acc[e];
   __syncthreads();
@@ -355,6 +400,126 @@ __global__ void __launch_bounds__(kShT) k_sh_write(LayerArgs a, SelArgs s, int n
     float sum = 0.0f;
     for (int w = 0; w < kShT / 32; ++w) sum += red[w][e];
     part[((int64_t)row * nch + ch) * a.d + e] = sum;
+  }
+}
+
+// Ordered compaction only (Eq. 5 follows in k_gather_rows over the rank's list slice):
+// warp w of the CTA owns tokens [j0 + 512 w, +512), walked 256 per step (8 per lane, two
+// 16-B loads), warp scans of the lanes' (tie, kept) counts give in-order positions, kept
+// (Δ, token) pairs are staged in shared memory and written lane-parallel.  Also records
+// this rank's slice [off, off + cnt) of every row's kept list (grange [2][rows]).
+constexpr int kShWT = kShChunk / (kShT / 32);  // tokens per warp (512)
+__global__ void __launch_bounds__(kShT) k_sh_compact(LayerArgs a, SelArgs s, int nch,
+                                                     const uint32_t *chunk,
+                                                     const unsigned long long *allcnt, int rank,
+                                                     int64_t base, int64_t *grange) {
+  const int row = blockIdx.y, ch = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const HeadState h = a.hs[row];
+  __shared__ unsigned long long sp[2];
+  __shared__ unsigned s_ws[kShT / 32], s_wt[kShT / 32];
+  __shared__ uint32_t stg_d[kShT / 32][256], stg_t[kShT / 32][256];
+  if (tid == 0) {
+    unsigned long long ps = 0, pt = 0;
+    for (int r = 0; r < rank; ++r) {
+      ps += allcnt[((int64_t)r * s.rows + row) * 2];
+      pt += allcnt[((int64_t)r * s.rows + row) * 2 + 1];
+    }
+    if (ch == 0) {
+      const unsigned long long sr = allcnt[((int64_t)rank * s.rows + row) * 2];
+      const unsigned long long tr = allcnt[((int64_t)rank * s.rows + row) * 2 + 1];
+      const unsigned long long rt = h.r_ties;
+      const unsigned long long tk = pt >= rt ? 0ull : (rt - pt < tr ? rt - pt : tr);
+      grange[row] = (int64_t)(ps + (pt < rt ? pt : rt));
+      grange[s.rows + row] = (int64_t)(sr + tk);
+    }
+    for (int k = 0; k < ch; ++k) {
+      ps += chunk[((int64_t)row * nch + k) * 2];
+      pt += chunk[((int64_t)row * nch + k) * 2 + 1];
+    }
+    sp[0] = ps;
+    sp[1] = pt;
+  }
+  const float *zr = a.z + (int64_t)row * a.z_stride;
+  const int64_t w_lo = (int64_t)ch * kShChunk + (int64_t)warp * kShWT;
+  const int64_t w_hi = w_lo + kShWT < a.n_cand ? w_lo + kShWT : a.n_cand;
+  auto load8 = [&](int64_t t, uint32_t (&dl)[8]) {
+    float v[8];
+    if (t + 8 <= w_hi) {
+      const float4 a4 = *reinterpret_cast<const float4 *>(zr + t);
+      const float4 b4 = *reinterpret_cast<const float4 *>(zr + t + 4);
+      v[0] = a4.x; v[1] = a4.y; v[2] = a4.z; v[3] = a4.w; v[4] = b4.x; v[5] = b4.y; v[6] = b4.z; v[7] = b4.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = t + u < w_hi ? zr[t + u] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dl[u] = t + u < w_hi ? (uint32_t)(h.M - zint(v[u])) : 0xffffffffu;
+  };
+  {  // per-warp totals
+    unsigned ns = 0, nt = 0;
+    for (int64_t tb = w_lo; tb < w_hi; tb += 256) {
+      uint32_t dl[8];
+      load8(tb + lane * 8, dl);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { ns += dl[u] < h.delta_star; nt += dl[u] == h.delta_star; }
+    }
+    ns = __reduce_add_sync(0xffffffffu, ns);
+    nt = __reduce_add_sync(0xffffffffu, nt);
+    if (lane == 0) { s_ws[warp] = ns; s_wt[warp] = nt; }
+  }
+  __syncthreads();
+  unsigned long long s_w = sp[0], t_run = sp[1];
+  for (int k = 0; k < warp; ++k) { s_w += s_ws[k]; t_run += s_wt[k]; }
+  const unsigned long long r_ties = h.r_ties;
+  unsigned long long pos = s_w + (t_run < r_ties ? t_run : r_ties);
+  const double den_d = s.renorm ? (double)h.sel_mass : (double)h.S;
+  const float inv_den = (float)(1.0 / den_d);
+  int32_t *oi = s.sel_idx + (int64_t)row * s.k_max;
+  float *ow = s.sel_w + (int64_t)row * s.k_max;
+  for (int64_t tb = w_lo; tb < w_hi; tb += 256) {
+    const int64_t t0 = tb + lane * 8;
+    uint32_t dl[8];
+    load8(t0, dl);
+    unsigned nst = 0, ntie = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { nst += dl[u] < h.delta_star; ntie += dl[u] == h.delta_star; }
+    unsigned tie_pre = ntie;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, tie_pre, off);
+      if (lane >= off) tie_pre += o;
+    }
+    const unsigned tie_tot = __shfl_sync(0xffffffffu, tie_pre, 31);
+    tie_pre -= ntie;
+    const unsigned long long my_t0 = t_run + tie_pre;
+    const unsigned taken = my_t0 >= r_ties ? 0u : (unsigned)((r_ties - my_t0) < ntie ? (r_ties - my_t0) : ntie);
+    unsigned kpre = nst + taken;
+    const unsigned kept = kpre;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, kpre, off);
+      if (lane >= off) kpre += o;
+    }
+    const unsigned kept_tot = __shfl_sync(0xffffffffu, kpre, 31);
+    unsigned q = kpre - kept, seen = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      bool take = dl[u] < h.delta_star;
+      if (dl[u] == h.delta_star) { take = seen < taken; ++seen; }
+      if (take) { stg_d[warp][q] = dl[u]; stg_t[warp][q] = (uint32_t)(t0 + u - w_lo); ++q; }
+    }
+    __syncwarp();
+    for (unsigned i = lane; i < kept_tot; i += 32) {
+      const unsigned long long p = pos + i;
+      if ((int64_t)p < s.k_max) {
+        oi[p] = (int32_t)(base + w_lo + stg_t[warp][i]);
+        ow[p] = __fmul_rn((float)mass_d(stg_d[warp][i], h.kappa), inv_den);
+      }
+    }
+    __syncwarp();
+    pos += kept_tot;
+    t_run += tie_tot;
   }
 }
 
@@ -375,6 +540,11 @@ static int sh_grid(int64_t n) {
 
 cudaError_t launch_shard_stats(const LayerArgs &a, int nsplit, int32_t *stats, cudaStream_t st) {
   const int rows = a.B * a.Hq;
+  if (nsplit <= 1 && a.n_res == 0 && a.n_q > 0) {
+    k_sh_stats_folded<<<(rows + 127) / 128, 128, 0, st>>>(a.hs, stats, rows);
+    note_launch();
+    return cudaGetLastError();
+  }
   k_sh_init_stats<<<(rows + 127) / 128, 128, 0, st>>>(stats, rows);
   note_launch();
   k_sh_stats<<<dim3(sh_grid(a.n_cand), rows), kShT, 0, st>>>(a, nsplit, stats);
@@ -420,11 +590,25 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
 
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
-                                float *part, float *out, cudaStream_t st) {
+                                float *part, float *out, cudaStream_t st, int64_t *grange,
+                                float *rpart, uint32_t *rdone) {
   const int rows = a.B * a.Hq;
   const int nch = shard_chunks(a.n_cand);
-  if (nch > 0) {
-    k_sh_write<<<dim3(nch, rows), kShT, 0, st>>>(a, s, nch, chunk, allcnt, rank, base, part);
+  if (nch > 0 && grange && a.d == 128) {
+    // compaction only, then the many-rows-in-flight gather over this rank's list slice
+    k_sh_compact<<<dim3(nch, rows), kShT, 0, st>>>(a, s, nch, chunk, allcnt, rank, base, grange);
+    note_launch();
+    cudaError_t e = cudaMemsetAsync(rdone, 0, (size_t)rows * 4, st);
+    if (e != cudaSuccess) return e;
+    LayerArgs g = a;
+    g.g_off = grange;
+    g.g_cnt = grange + rows;
+    g.g_base = base;
+    g.out = out;
+    const int64_t kc2 = a.k_max < a.n_cand ? a.k_max : a.n_cand;
+    return launch_gather_rows(g, kc2, rpart, rdone, st);
+  } else if (nch > 0) {
+    k_sh_write<<<dim3(nch, rows), kShT, 0, st>>>(a, s, nch, chunk, allcnt, rank, base, part, nullptr);
     note_launch();
     k_sh_reduce<<<rows, 128, 0, st>>>(rows, nch, a.d, part, out);
     note_launch();
