@@ -9,8 +9,12 @@
 // product.  Only the anchor tiles and the own-block tiles up to the diagonal are visited,
 // so the work is O(n * 2 bs) instead of O(n^2).  d = 128.
 //
-// This is the prefill side (not the decode hot path); mma.sync keeps it simple -- a
-// tcgen05 / TMEM version is the next step if prefill throughput matters.
+// Two kernels: k_blockwise_attn_tc (default, bs % 128 == 0): tcgen05.mma with operands in
+// 128B-swizzled shared memory (UMMA descriptors), S and O accumulators in TMEM, lazy softmax
+// rescaling; k_blockwise_attn (mma.sync m16n8k16) for bs % 128 != 0 or HC_PREFILL_TC=0.
+#include <stdlib.h>
+#include <string.h>
+
 #include "hc_internal.h"
 
 namespace hc {
@@ -211,10 +215,286 @@ __global__ void __launch_bounds__(kPT) k_blockwise_attn(PrefillArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// tcgen05 version: CTA = 128 queries of one head (4 warps, thread t owns query row t), key
+// tiles of 128.  Per tile: S = Q K^T (tcgen05.mma kind::f16, M = N = 128, K = 16 x 8,
+// fp32 accumulator in TMEM columns [0, 128)), each thread reads its S row from TMEM
+// (tcgen05.ld 32x32b), does the online-softmax update for its own row (no shuffles), writes
+// P (fp16) into shared memory, then O_tile = P V (second MMA into TMEM columns [128, 256))
+// and O_reg = O_reg * corr + O_tile in registers.  Operands live in shared memory in the
+// 128-byte-swizzled K-major layout the UMMA descriptors describe (8-row x 128-B atoms,
+// 16-B chunk c of row r at c ^ (r & 7)); V is stored transposed (d-major) so both MMAs use
+// K-major B operands.
+constexpr int kTM = 128;  // queries per CTA / keys per tile
+constexpr int kTThreads = 128;
+
+__device__ __forceinline__ uint32_t sw128_off(int r, int cg) {  // 16-B chunk cg (0..15) of row r
+  const int kc = cg >> 3, c = cg & 7;
+  return (uint32_t)(kc * (kTM * 128) + r * 128 + ((c ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;            // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;  // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1u << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ uint64_t umma_desc_k(uint32_t tile_saddr, int ks) {  // K step of 16
+  return umma_desc(tile_saddr + (uint32_t)((ks >> 2) * (kTM * 128) + (ks & 3) * 32));
+}
+// MN-major B (V as stored: key rows, dv contiguous): atoms of 8 keys x 64 dv (1024 B),
+// 8-key groups at SBO = 1024 B, the two 64-dv halves at LBO = 16 KiB; K step (16 keys) = 2 KiB
+__device__ __forceinline__ uint64_t umma_desc_mn(uint32_t tile_saddr, int ks) {
+  uint64_t d = (uint64_t)(((tile_saddr + (uint32_t)ks * 2048u) >> 4) & 0x3FFFu);
+  d |= (uint64_t)((kTM * 128) >> 4) << 16;  // leading byte offset: next 64-wide MN half
+  d |= (uint64_t)(1024u >> 4) << 32;         // stride byte offset: next 8 K-rows
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// f16 x f16 -> f32, M = N = 128, A K-major; B K-major (S = Q K^T) or MN-major (O = P V)
+constexpr uint32_t kIdescF16 = (1u << 4) | ((uint32_t)(kTM >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+constexpr uint32_t kIdescF16BMN = kIdescF16 | (1u << 16);
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t acc,
+                                         uint32_t idesc = kIdescF16) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+#define HC_TLD32(addr, r)                                                                          \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"\
+               "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"     \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),  \
+                 "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),           \
+                 "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),        \
+                 "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),        \
+                 "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),        \
+                 "=r"(r[31])                                                                        \
+               : "r"(addr))
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kTThreads, 2) k_blockwise_attn_tc(PrefillArgs a) {
+  extern __shared__ __align__(1024) uint8_t tsm_raw[];
+  uint8_t *tsm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *sQ = tsm;                   // [128 q][128 d]      K-major (A of S)
+  uint8_t *sK = sQ + kTM * 256;        // [128 keys][128 d]   K-major (B of S)
+  uint8_t *sVt = sK + kTM * 256;       // [128 keys][128 d]   MN-major (B of O), same layout as sK
+  uint8_t *sP = sK;                    // [128 q][128 keys]   K-major (A of O): reuses sK once S is done
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int h = blockIdx.y, kvh = h / (a.Hq / a.Hkv);
+  const int64_t i0 = (int64_t)blockIdx.x * kTM;
+  const int64_t kb = i0 / a.bs;
+  const int64_t qs = (int64_t)a.Hq * kPD, ks_ = (int64_t)a.Hkv * kPD;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // Q tile -> swizzled smem (thread t: row t, 16 chunks of 16 B)
+  {
+    const int64_t i = i0 + tid;
+    const uint16_t *src = a.q + (i < a.n ? i : 0) * qs + (int64_t)h * kPD;
+#pragma unroll
+    for (int cg = 0; cg < 16; ++cg) {
+      uint4 v = i < a.n ? *reinterpret_cast<const uint4 *>(src + cg * 8) : make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4 *>(sQ + sw128_off(tid, cg)) = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const uint32_t tS = tmem, tO = tmem + 128;
+  const uint32_t lane_sel = (uint32_t)(warp * 32) << 16;
+  const uint32_t aQ = (uint32_t)__cvta_generic_to_shared(sQ), aK = (uint32_t)__cvta_generic_to_shared(sK);
+  const uint32_t aVt = (uint32_t)__cvta_generic_to_shared(sVt), aP = (uint32_t)__cvta_generic_to_shared(sP);
+
+  const int64_t last = i0 + kTM < a.n ? i0 + kTM : a.n;
+  const int n_anchor = kb == 0 ? 0 : (int)(a.bs / kTM);
+  const int64_t own0 = kb * a.bs;
+  const int n_own = (int)((last - own0 + kTM - 1) / kTM);
+  const int ntiles = n_anchor + n_own;
+  const int64_t qi = i0 + tid;  // this thread's query
+  // O accumulates in TMEM across tiles (PV MMAs with accumulate); the softmax reference
+  // max m_ref is only raised when a tile's max exceeds it by more than 2^8 (then O and l are
+  // rescaled in place), so P = 2^(s - m_ref) <= 2^8 stays well inside fp16
+  float mref = -INFINITY, lrow = 0.0f;
+  uint32_t phase = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    const int64_t k0 = t < n_anchor ? (int64_t)t * kTM : own0 + (int64_t)(t - n_anchor) * kTM;
+    // K and V tiles (key rows), coalesced: 16 consecutive threads read one 256-B row
+#pragma unroll 1
+    for (int it0 = 0; it0 < 16; it0 += 4) {
+      uint4 kv4[4], vv4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = (it0 + q) * kTThreads + tid, r = idx >> 4, cg = idx & 15;
+        const int64_t j = k0 + r;
+        const bool ok = j < a.n;
+        const int64_t off = (ok ? j : 0) * ks_ + (int64_t)kvh * kPD + cg * 8;
+        kv4[q] = ok ? *reinterpret_cast<const uint4 *>(a.k + off) : make_uint4(0, 0, 0, 0);
+        vv4[q] = ok ? *reinterpret_cast<const uint4 *>(a.v + off) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int idx = (it0 + q) * kTThreads + tid, r = idx >> 4, cg = idx & 15;
+        *reinterpret_cast<uint4 *>(sK + sw128_off(r, cg)) = kv4[q];
+        *reinterpret_cast<uint4 *>(sVt + sw128_off(r, cg)) = vv4[q];
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < kPD / 16; ++kk) umma_f16(tS, umma_desc_k(aQ, kk), umma_desc_k(aK, kk), kk > 0);
+      umma_commit(&mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    // this thread's S row (TMEM lane = row): scaled, masked
+    const bool diag = k0 + kTM > i0 && (kb == 0 || k0 >= own0);
+    float sv[kTM];
+    float mt = -INFINITY;
+    {
+      uint32_t r[32];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        HC_TLD32(tS + lane_sel + c4 * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int64_t j = k0 + c4 * 32 + u;
+          float x = __uint_as_float(r[u]) * a.scale_log2;
+          if (j >= a.n || (diag && j > qi)) x = -INFINITY;
+          sv[c4 * 32 + u] = x;
+          mt = fmaxf(mt, x);
+        }
+      }
+    }
+    const bool raise = mt > mref + 8.0f;  // also true for the first finite max
+    float corr = 1.0f;
+    if (raise) {
+      corr = mref == -INFINITY ? 0.0f : exp2f(mref - mt);
+      mref = mt;
+      lrow *= corr;
+    }
+    if (t > 0 && __any_sync(0xffffffffu, raise)) {  // rescale this warp's O rows in TMEM
+      uint32_t r[32];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        HC_TLD32(tO + lane_sel + c4 * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) r[u] = __float_as_uint(__uint_as_float(r[u]) * corr);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"
+                     "%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31};"
+                     ::"r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+                     "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+                     "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+                     "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+                     "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(tO + lane_sel + c4 * 32)
+                     : "memory");
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    float rs = 0.0f;
+#pragma unroll
+    for (int cg = 0; cg < 16; ++cg) {  // P row (fp16, <= 2^8) -> swizzled smem (reuses sK)
+      uint32_t w4[4];
+#pragma unroll
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float p0 = mref == -INFINITY ? 0.0f : exp2f(sv[cg * 8 + 2 * e2] - mref);
+        const float p1 = mref == -INFINITY ? 0.0f : exp2f(sv[cg * 8 + 2 * e2 + 1] - mref);
+        rs += p0 + p1;
+        w4[e2] = pack_h2(p0, p1);
+      }
+      *reinterpret_cast<uint4 *>(sP + sw128_off(tid, cg)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    lrow += rs;
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < kTM / 16; ++kk)
+        umma_f16(tO, umma_desc_k(aP, kk), umma_desc_mn(aVt, kk), (t > 0 || kk > 0) ? 1u : 0u, kIdescF16BMN);
+      umma_commit(&mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+  }
+  {  // out = O / l
+    const float inv = lrow > 0.0f ? 1.0f / lrow : 0.0f;
+    float *op = a.out + qi * qs + (int64_t)h * kPD;
+    uint32_t r[32];
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      HC_TLD32(tO + lane_sel + c4 * 32, r);
+      tmem_wait_ld();
+      if (qi < a.n) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          *reinterpret_cast<float4 *>(op + c4 * 32 + e) =
+              make_float4(__uint_as_float(r[e]) * inv, __uint_as_float(r[e + 1]) * inv,
+                          __uint_as_float(r[e + 2]) * inv, __uint_as_float(r[e + 3]) * inv);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+static int prefill_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_PREFILL_TC");
+    v = (ev && !strcmp(ev, "0")) ? 0 : 1;
+  }
+  return v;
+}
+
 cudaError_t launch_blockwise_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,
                                   int Hq, int Hkv, int64_t bs, float *out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   PrefillArgs a{q, k, v, out, n, bs, Hq, Hkv, (float)(1.4426950408889634 / sqrt((double)kPD))};
+  if (prefill_tc() && bs % kTM == 0) {
+    const size_t smem = (size_t)3 * kTM * 256 + 1024;
+    static int configured_tc[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !configured_tc[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(k_blockwise_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured_tc[dev] = 1;
+    }
+    dim3 grid((unsigned)((n + kTM - 1) / kTM), (unsigned)Hq);
+    k_blockwise_attn_tc<<<grid, kTThreads, smem, s>>>(a);
+    note_launch();
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)(kPBM + 4 * kPBN) * kPRow * 2;
   static int configured[64] = {0};
   int dev = 0;
