@@ -487,6 +487,9 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
     const int64_t base = B * H * g;
     int ts = 1;
     while (ts < kMaxTSplit && base * ts * 2 <= 2 * 148 * 8 && Lw.cpow2 / (ts * 2) >= 256) ts *= 2;
+    static int ts_env = -1;  // dev override (HC_TSPLIT)
+    if (ts_env < 0) { const char *ev = getenv("HC_TSPLIT"); ts_env = ev ? atoi(ev) : 0; }
+    if (ts_env > 0 && Lw.cpow2 / ts_env >= 256) ts = ts_env;
     a.tsplit = ts;
   }
   a.z = (float *)(w8 + Lw.o_z);

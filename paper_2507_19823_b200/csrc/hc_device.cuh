@@ -48,6 +48,23 @@ HC_HD int quant_t(float t, float s) {
   return (int)v;
 }
 
+#ifdef __CUDACC__
+// Device versions of quant_t / quant_t8 without conversion instructions (FRND and F2I issue
+// at 1/8 rate): pre-clamping to +-2^16 does not change clamp(rint(x)), and for |x| <= 2^22
+// adding 1.5*2^23 rounds to the nearest integer, ties to even, exactly like rintf.
+__device__ __forceinline__ int rint_small(float x) {  // |x| <= 2^22
+  return __float_as_int(__fadd_rn(x, 12582912.0f)) - 0x4B400000;
+}
+__device__ __forceinline__ int quant_t_d(float t, float s) {
+  const int r = rint_small(fminf(fmaxf(__fmul_rn(t, s), -65536.0f), 65536.0f));
+  return min(max(r, -32767), 32767);
+}
+__device__ __forceinline__ int quant_t8_d(float t, float s) {
+  const int r = rint_small(fminf(fmaxf(__fmul_rn(t, s), -65536.0f), 65536.0f));
+  return min(max(r, -127), 127);
+}
+#endif
+
 // R3 resident: rint(clamp(acc * 2^e, +-2^22))
 HC_HD int quant_res(float acc, float s) {
   float v = __fmul_rn(acc, s);

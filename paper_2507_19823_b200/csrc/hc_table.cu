@@ -124,20 +124,43 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
     for (int e = 0; e < DBAR; ++e)
       qs[h][e] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + i * DBAR + e));
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
-#pragma unroll 4
-  for (int m = m0 + threadIdx.x; m < m0 + per; m += kTB) {
+  // batches of kTBatch centroids per thread: all their codebook loads issued before use
+  constexpr int kTBatch = DBAR <= 4 ? 8 : 4;
+  for (int mb = m0 + threadIdx.x; mb < m0 + per; mb += kTB * kTBatch) {
+  float cmb[kTBatch][DBAR];
+#pragma unroll
+  for (int ub = 0; ub < kTBatch; ++ub) {
+    const int m = mb + ub * kTB;
+    if (m < m0 + per && m < a.c) {
+#pragma unroll
+      for (int e = 0; e < DBAR; ++e) cmb[ub][e] = __ldg(Ci + (int64_t)m * DBAR + e);
+    } else {
+#pragma unroll
+      for (int e = 0; e < DBAR; ++e) cmb[ub][e] = 0.0f;
+    }
+  }
+#pragma unroll
+  for (int ub = 0; ub < kTBatch; ++ub) {
+    const int m = mb + ub * kTB;
+    if (m >= m0 + per) break;
     float t[G];
-    table_entry<G, DBAR>(qs, Ci, m, a.c, t);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {  // the R2 FMA chain (table_entry), entries m >= c are 0
+      float acc = __fmul_rn(qs[h][0], cmb[ub][0]);
+#pragma unroll
+      for (int e = 1; e < DBAR; ++e) acc = __fmaf_rn(qs[h][e], cmb[ub][e], acc);
+      t[h] = m < a.c ? acc : 0.0f;
+    }
     if (G == 4 && a.lut8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
       uint32_t wv = 0;
 #pragma unroll
-      for (int h = 0; h < G; ++h) wv |= (uint32_t)(quant_t8(t[h], sc[h]) + 128) << (8 * h);
+      for (int h = 0; h < G; ++h) wv |= (uint32_t)(quant_t8_d(t[h], sc[h]) + 128) << (8 * h);
       reinterpret_cast<uint32_t *>(a.T)[((int64_t)u * a.g + i) * a.cpow2 + m] = wv;
       continue;
     }
     int16_t packed[G];
 #pragma unroll
-    for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t(t[h], sc[h]);
+    for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t_d(t[h], sc[h]);
     int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
     // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd head's
     // signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
@@ -153,6 +176,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
 #pragma unroll
       for (int h = 0; h < G; ++h) dst[h] = packed[h];
     }
+  }
   }
 }
 
