@@ -638,7 +638,11 @@ def main():
                                 else "k_scan (Eq. 3 quantized-key scan)"),
                      "algorithmic_bytes_per_launch": p_bytes_layer,
                      "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L / ms_per_step,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src,
+                     "dominant_kernel": ("k_gather_union (zero-copy value gather, bound by the host link: see "
+                                         "host_link; profiles/r01_launches_config3_summary.md)"
+                                         if host_link is not None else
+                                         "scan / select / gather share the step (see DESIGN.md §5)")},
         "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / n},
         "host_link": host_link,
         "e2e": {"value": jobs * 1000.0 / ms_e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d,
