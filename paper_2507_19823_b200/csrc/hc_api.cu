@@ -502,6 +502,13 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   a.out = out;
   a.num_sms = num_sms();
   choose_scan(B * H, n_q, (int)g, Lw.cpow2, (int)G, a.num_sms, &a.scan_tpt, &a.scan_split, a.lut8);
+  {  // dev overrides (HC_SCAN_SPLIT, HC_SCAN_TPT) for cost-model checks
+    static int sp_env = -1, tpt_env = -1;
+    if (sp_env < 0) { const char *ev = getenv("HC_SCAN_SPLIT"); sp_env = ev ? atoi(ev) : 0; }
+    if (tpt_env < 0) { const char *ev = getenv("HC_SCAN_TPT"); tpt_env = ev ? atoi(ev) : 0; }
+    if (sp_env > 0 && sp_env <= g) a.scan_split = sp_env;
+    if ((tpt_env == 8 || tpt_env == 16) && !a.lut8) a.scan_tpt = tpt_env;
+  }
   a.zpart = (float *)(w8 + Lw.o_zpart);
   if (budget.shared_kv) {
     a.grp = (GroupState *)(w8 + Lw.o_grp);
