@@ -49,6 +49,11 @@ CONFIGS = {
             workload="config4: Llama-3-8B-shaped, 1M ctx sequence-sharded across the GPUs "
                      "(contiguous token ranges, NCCL merges), 12.5% KV budget (g=32, c=8192), "
                      "k_max=131072, tau=0.9, batch 1, V in HBM"),
+    5: dict(B=1, L=32, Hkv=8, G=4, d=128, g=32, c=8192, n=4194304, k_max=524288, tau=0.9,
+            placement=1,
+            workload="config5: Llama-3-8B-shaped, 4M ctx sequence-sharded across the GPUs, 12.5% KV "
+                     "budget (g=32, c=8192), k_max=524288, tau=0.9, batch 1, V in host pinned memory "
+                     "(32 GiB per rank at N=8)"),
 }
 Q_SCALE = 2.29  # calibrates tau=0.9 to Table 3's 15.6 % selection ratio
 SEED = 0x48434154
@@ -530,6 +535,9 @@ def main():
         cfg["workload"] += "; value-offload-only mode (exact fp16 keys, Table 1a VO row)"
     if args.lut8:
         cfg["workload"] += "; 8-bit table variant (R2b)"
+    if args.config == 5 and world_env < 4 and not args.impl == "reference":
+        raise SystemExit("config 5 (4M ctx, 275 GB of host-resident values) needs >= 4 ranks "
+                         "(python -m torch.distributed.run --nproc-per-node N bench.py --config 5)")
     if args.steps is None:
         args.steps = 500 if args.config in (1, 2) else 20
     if args.warmup is None:
@@ -555,7 +563,7 @@ def main():
     args.warmup = max(args.warmup, 3)
     hc_lib_check()
 
-    sharded_mode = world > 1 and args.config == 4
+    sharded_mode = world > 1 and args.config in (4, 5)
     wl = Workload(cfg, dev, rank if sharded_mode else 0, world if sharded_mode else 1)
     if sharded_mode:
         from paper_2507_19823_b200.sharded import TorchComm

@@ -289,3 +289,10 @@ def test_config3_full_size_sampled(torch_cuda):
     sampled units."""
     case = Case(B=4, L=1, Hkv=8, g=32, n=131072, k_max=16384, placement=1, seed=3)
     _run(case, units=[(0, 0), (3, 7)])
+
+
+def test_config4_full_size_sampled(torch_cuda):
+    """BASELINE config 4 shape on one GPU (1M ctx, g=32, k_max=131072, V in HBM), one layer,
+    two sampled units: index sets bit-exact and outputs within tolerance at the full size."""
+    case = Case(B=1, L=1, Hkv=8, g=32, n=1048576, k_max=131072, seed=4)
+    _run(case, units=[(0, 0), (0, 6)])
