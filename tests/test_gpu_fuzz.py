@@ -1,0 +1,57 @@
+"""Randomised GPU-vs-oracle sweep over the decode path's shape space (seeded, reproducible):
+batch, KV heads, GQA group, d, g (dbar 1..16), c, n (ragged, across tiles and splits),
+tau, k_max (binding or not), resident window, shared codebooks, 16/13-bit codes and per-head /
+shared selection.  Every case: bit-exact z, S, M, k_sel and index sets; outputs within the
+north_star tolerance (harness.compare_unit)."""
+import numpy as np
+import pytest
+
+from harness import Case, build_gpu, compare_unit, oracle_unit, run_gpu_layer
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2507_19823_b200 as hc
+    hc.lib()
+    return torch
+
+
+def _cases(k=48, seed=2026):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(k):
+        d = int(rng.choice([64, 128, 128, 256]))
+        dbar = int(rng.choice([d_ for d_ in (1, 2, 4, 8, 16) if d // d_ <= 128]))
+        g = d // dbar
+        G = int(rng.choice([1, 2, 4]))
+        c = int(rng.choice([2, 37, 256, 1000, 8192]))
+        n = int(rng.integers(1, 40000))
+        res = int(rng.choice([0, 0, 0, 17, 64]))
+        n_res = min(res, int(rng.integers(0, res + 1))) if res else 0
+        tau = float(rng.choice([0.3, 0.7, 0.9, 0.99, 1.0]))
+        k_max = int(rng.choice([1, 50, max(1, n // 8), n + n_res + 5]))
+        code_bits = 13 if (c <= 8192 and rng.random() < 0.25) else 16
+        shared = bool(G > 1 and rng.random() < 0.2)
+        cbg = 1 if rng.random() < 0.25 else g
+        B = int(rng.integers(1, 3))
+        Hkv = int(rng.integers(1, 3))
+        out.append(dict(B=B, Hkv=Hkv, G=G, d=d, g=g, c=c, cbg=cbg, n=n, res_cap=res, n_res=n_res,
+                        tau=tau, k_max=k_max, code_bits=code_bits, shared=shared, seed=1000 + i))
+    return out
+
+
+@pytest.mark.parametrize("kw", _cases(), ids=lambda kw: "-".join(f"{k}{v}" for k, v in kw.items()
+                                                                if k in ("d", "g", "G", "c", "n", "tau")))
+def test_fuzz_decode_parity(torch_cuda, kw):
+    case = Case(**kw)
+    if case.n == 0 and case.n_res == 0:
+        pytest.skip("empty")
+    kc, vs, q = build_gpu(case)
+    gpu = run_gpu_layer(case, kc, vs, q, 0)
+    for b in range(case.B):
+        for kv in range(case.Hkv):
+            compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv)
