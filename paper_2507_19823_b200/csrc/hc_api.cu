@@ -616,7 +616,10 @@ static hc_status shard_prepare(const uint16_t *q, const hc_kcache *kc, const hc_
   a.out = nullptr;
   sa = SelArgs{};
   sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = a.B * a.Hq; sa.n = a.n_cand;
-  sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
+  // the cap is GLOBAL: a shard's own candidate count may be below k_max (k_eff clamps only
+  // the workspace list stride of the unsharded path); the kept lists are written with the
+  // caller's stride budget.k_max in the finish phase
+  sa.tau_q = a.tau_q; sa.k_max = budget.k_max; sa.renorm = a.renorm;
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
   return HC_OK;
 }

@@ -217,6 +217,10 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   const int row = b * a.Hq + kv * a.G + blockIdx.x;
   const int64_t k = a.g_cnt ? a.g_cnt[row] : a.hs[row].ksel;
   const int64_t e0 = (int64_t)ch * kRC;
+  if (k == 0) {  // nothing kept (a shard's slice can be empty): the row's share is zero
+    if (ch == 0 && tid < 128) a.out[(int64_t)row * 128 + tid] = 0.0f;
+    return;
+  }
   if (e0 >= k) return;  // only the ceil(k/kRC) CTAs holding kept rows take part
   const int64_t off = a.g_cnt ? a.g_off[row] : 0;
   const int32_t *li = a.sel_idx + (int64_t)row * a.k_max + off;

@@ -38,7 +38,9 @@ def _shard_caches(case: Case, R: int, device="cuda"):
 
 
 @pytest.mark.parametrize("R,n,tau,k_max", [(2, 9000, 0.9, 1500), (3, 7001, 0.7, 50000),
-                                           (4, 12000, 1.0, 3000), (2, 5000, 0.95, 1)])
+                                           (4, 12000, 1.0, 3000), (2, 5000, 0.95, 1),
+                                           (5, 33333, 0.9, 4000), (8, 70000, 0.99, 9000),
+                                           (3, 150, 0.5, 20), (6, 20000, 0.3, 100000)])
 def test_virtual_shards_match_unsharded_oracle(R, n, tau, k_max):
     import torch
     import paper_2507_19823_b200 as hc
