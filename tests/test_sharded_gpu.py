@@ -64,3 +64,40 @@ def test_virtual_shards_match_unsharded_oracle(R, n, tau, k_max):
                 assert np.array_equal(sel[row, :k], ref["idx"][h])
                 err = np.abs(out[row] - ref["out"][h])
                 assert np.all(err <= TOL_ABS + TOL_REL * np.abs(ref["out"][h]))
+
+
+def _fuzz(k=12, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(k):
+        R = int(rng.integers(2, 9))
+        n = int(rng.integers(R * 3, 60000))
+        tau = float(rng.choice([0.2, 0.6, 0.9, 0.99, 1.0]))
+        k_max = int(rng.choice([1, 7, max(1, n // 10), n // R + 1, n + 3]))
+        out.append((R, n, tau, k_max, 500 + i))
+    return out
+
+
+@pytest.mark.parametrize("R,n,tau,k_max,seed", _fuzz())
+def test_virtual_shards_fuzz(R, n, tau, k_max, seed):
+    """Seeded sweep: R shards (ragged splits of n), caps below / above a shard's size."""
+    import torch
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.sharded import GpuShard, decode_layer_virtual
+    case = Case(B=1, Hkv=2, n=n, tau=tau, k_max=k_max, seed=seed)
+    parts = _shard_caches(case, R)
+    bud = hc.budget(tau, k_max)
+    shards = [GpuShard(kc, vs, bud) for kc, vs, _ in parts]
+    q = torch.from_numpy(np.stack([case.query(b, 0) for b in range(case.B)])).cuda()
+    out = decode_layer_virtual(shards, q, 0, [a for _, _, a in parts]).cpu().numpy()
+    sel = torch.stack([s.sel_idx for s in shards]).amax(0).cpu().numpy()
+    ksel = shards[0].sel_k.cpu().numpy()
+    for kv in range(case.Hkv):
+        ref = oracle_unit(case, 0, 0, kv)
+        for h in range(case.G):
+            row = kv * case.G + h
+            k = int(ksel[row])
+            assert k == ref["k_sel"][h]
+            assert np.array_equal(sel[row, :k], ref["idx"][h])
+            err = np.abs(out[row] - ref["out"][h])
+            assert np.all(err <= TOL_ABS + TOL_REL * np.abs(ref["out"][h]))
