@@ -55,3 +55,39 @@ def test_fuzz_decode_parity(torch_cuda, kw):
     for b in range(case.B):
         for kv in range(case.Hkv):
             compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv)
+
+
+def _sel_cases(k=16, seed=31):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(k):
+        n = int(rng.integers(1, 300000))
+        scale = float(rng.choice([1e-30, 1e-3, 1.0, 30.0, 1e4, 1e30]))
+        tau = float(rng.choice([0.1, 0.5, 0.9, 0.999, 1.0]))
+        k_max = int(rng.choice([1, 100, max(1, n // 3), n + 1]))
+        rows = int(rng.integers(1, 6))
+        d = int(rng.choice([1, 64, 128]))
+        out.append((n, scale, tau, k_max, rows, d, 300 + i))
+    return out
+
+
+@pytest.mark.parametrize("n,scale,tau,k_max,rows,d,seed", _sel_cases())
+def test_fuzz_select_topk(torch_cuda, n, scale, tau, k_max, rows, d, seed):
+    """hc_select_topk on real scores (R5b) over extreme scales, heavy ties, constant rows."""
+    import oracle
+    import paper_2507_19823_b200 as hc
+    torch = torch_cuda
+    rng = np.random.default_rng(seed)
+    sc = (rng.standard_normal((rows, n)) * scale).astype(np.float32)
+    if rows > 1:
+        sc[1] = np.round(sc[1] / max(scale, 1e-30) * 4) * max(scale, 1e-30) / 4  # ties
+    if rows > 2:
+        sc[2] = np.float32(scale)  # constant row
+    idx, w, k = hc.select_topk(torch.from_numpy(sc).cuda(), d, hc.budget(tau, k_max))
+    torch.cuda.synchronize()
+    for r in range(rows):
+        ref = oracle.select_float(sc[r], d, tau, k_max)
+        kk = int(k[r])
+        assert kk == ref["k_sel"]
+        assert np.array_equal(idx[r, :kk].cpu().numpy(), ref["idx"])
+        assert np.allclose(w[r, :kk].cpu().numpy(), ref["w"], rtol=1e-6, atol=1e-12)
