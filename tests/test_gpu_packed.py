@@ -110,3 +110,41 @@ def test_packed_config3_full_size_sampled(torch_cuda):
     """BASELINE config 3 shape with packed codes (bench.py --code-bits 13), sampled units."""
     case = Case(B=4, L=1, Hkv=8, g=32, n=131072, k_max=16384, placement=1, seed=3, code_bits=13)
     _run(case, units=[(0, 0), (3, 7)])
+
+
+def test_packed_append_with_window_eviction(torch_cuda):
+    """Packed codes + a 5-token recent window: every append past the window encodes the
+    evicted oldest token into the packed planes; decode over the cache matches the oracle."""
+    import oracle
+    import paper_2507_19823_b200 as hc
+    import synth
+    torch = torch_cuda
+    B, L, Hkv, G, d, g, c, n_cap, W = 2, 1, 2, 4, 128, 32, 512, 128, 5
+    case = Case(B=B, L=L, Hkv=Hkv, G=G, g=g, c=c, n=0, n_cap=n_cap, seed=23, code_bits=13)
+    cb = case.codebook(0)[None]
+    kc = hc.KCache(B, L, Hkv, G, d, g, c, n_cap, torch.from_numpy(cb).cuda(), res_cap=W, code_bits=13)
+    vs = hc.VStore.allocate(B, L, Hkv, n_cap, d)
+    steps = 45
+    K = synth.gen_keys(23, 1, steps * B * Hkv, d).reshape(steps, B, Hkv, d)
+    Vv = synth.gen_keys(23, 2, steps * B * Hkv, d).reshape(steps, B, Hkv, d)
+    for t in range(steps):
+        kc.append(0, torch.from_numpy(K[t]).cuda(), torch.from_numpy(Vv[t]).cuda(), vs)
+    torch.cuda.synchronize()
+    nq = steps - W
+    assert kc.n_q(0) == nq and kc.n_res(0) == W
+    q = torch.from_numpy(np.stack([synth.gen_query(23, b, 0, Hkv * G, d, 2.29) for b in range(B)])).cuda()
+    bud = hc.budget(0.9, 16)
+    idx = torch.full((B, Hkv * G, 16), -1, dtype=torch.int32, device="cuda")
+    w = torch.zeros((B, Hkv * G, 16), dtype=torch.float32, device="cuda")
+    k = torch.zeros((B, Hkv * G), dtype=torch.int64, device="cuda")
+    out = hc.decode_attention(q, kc, vs, 0, bud, sel_idx=idx, sel_w=w, sel_k=k).cpu().numpy()
+    for b in range(B):
+        for kv in range(Hkv):
+            P = oracle.encode(K[:nq, b, kv], cb[0], g).T
+            ref = oracle.decode_unit(q[b, kv * G:(kv + 1) * G].cpu().numpy(), cb[0], P, nq,
+                                     Vv[:nq, b, kv], 0.9, 16, rk=K[nq:, b, kv], rv=Vv[nq:, b, kv])
+            for h in range(G):
+                kk = int(k[b, kv * G + h])
+                assert kk == ref["k_sel"][h]
+                assert np.array_equal(idx[b, kv * G + h, :kk].cpu().numpy(), ref["idx"][h])
+                assert np.all(np.abs(out[b, kv * G + h] - ref["out"][h]) <= 1e-3 + 2e-3 * np.abs(ref["out"][h]))
