@@ -199,9 +199,10 @@ int gather_union_chunks(int64_t n_cand) { return (int)((n_cand + kGC - 1) / kGC)
 // (16 rows x 16 B in flight per thread, ~2 CTAs per SM), which is what a random 256-B
 // row gather needs to approach the HBM rate.  Chunk partials are added in chunk order by
 // the row's last CTA.
-constexpr int kRC = 256;   // kept rows per CTA
 constexpr int kRT = 256;   // threads
-constexpr int kRU = kRC / ((kRT / 32) * 2);  // rows per half-warp (16 at d = 128)
+constexpr int kRU = 16;    // rows in flight per half-warp per round
+constexpr int kRR = 4;     // rounds per CTA (fewer CTAs -> fewer partials / fences)
+constexpr int kRC = kRU * (kRT / 16) * kRR;  // kept rows per CTA (1024)
 
 __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float *part,
                                                      uint32_t *done) {
@@ -235,35 +236,39 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   const int sub = lane & 15;                  // 8-dim slice (d = 128)
   const uint16_t *Vb = a.V + (int64_t)b * a.v_b_stride + (int64_t)kv * a.v_kv_stride;
   const uint16_t *Rb = a.res_v + (int64_t)b * a.res_b_stride + (int64_t)kv * a.res_cap * a.d;
-  uint4 v[kRU];
-#pragma unroll
-  for (int q = 0; q < kRU; ++q) {
-    const int j = sj[hw * kRU + q];
-    if (j >= 0) {
-      const uint16_t *src;
-      if (j < a.n_q) {
-        src = Vb + (int64_t)j * a.d;
-      } else {
-        const uint32_t sl = (uint32_t)(a.res_slot0 + (j - a.n_q)) % (uint32_t)a.res_cap;
-        src = Rb + (int64_t)sl * a.d;
-      }
-      v[q] = ldg_nc16(src + sub * 8);
-    } else {
-      v[q] = make_uint4(0, 0, 0, 0);
-    }
-  }
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+  const int nround = (int)((k - e0 + kRU * (kRT / 16) - 1) / (kRU * (kRT / 16)));
+  for (int rd = 0; rd < kRR && rd < nround; ++rd) {
+    const int base = rd * (kRU * (kRT / 16)) + hw * kRU;
+    uint4 v[kRU];
 #pragma unroll
-  for (int q = 0; q < kRU; ++q) {
-    const float w = sw[hw * kRU + q];
-    const uint32_t uu[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+    for (int q = 0; q < kRU; ++q) {
+      const int j = sj[base + q];
+      if (j >= 0) {
+        const uint16_t *src;
+        if (j < a.n_q) {
+          src = Vb + (int64_t)j * a.d;
+        } else {
+          const uint32_t sl = (uint32_t)(a.res_slot0 + (j - a.n_q)) % (uint32_t)a.res_cap;
+          src = Rb + (int64_t)sl * a.d;
+        }
+        v[q] = ldg_nc16(src + sub * 8);
+      } else {
+        v[q] = make_uint4(0, 0, 0, 0);
+      }
+    }
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&uu[p]));
-      acc[2 * p] = fmaf(w, f2.x, acc[2 * p]);
-      acc[2 * p + 1] = fmaf(w, f2.y, acc[2 * p + 1]);
+    for (int q = 0; q < kRU; ++q) {
+      const float w = sw[base + q];
+      const uint32_t uu[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&uu[p]));
+        acc[2 * p] = fmaf(w, f2.x, acc[2 * p]);
+        acc[2 * p + 1] = fmaf(w, f2.y, acc[2 * p + 1]);
+      }
     }
   }
 #pragma unroll
@@ -274,9 +279,9 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
     float s = 0.0f;
     for (int q = 0; q < (kRT / 32) * 2; ++q) s += red[q * 128 + tid];
     pp[tid] = s;
+    __threadfence();  // only the writers of the partial publish it
   }
   __shared__ bool last;
-  __threadfence();
   __syncthreads();
   if (tid == 0) {
     const int nact = (int)((k + kRC - 1) / kRC);  // CTAs of this row that hold kept rows
