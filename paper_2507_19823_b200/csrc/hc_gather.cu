@@ -201,11 +201,12 @@ int gather_union_chunks(int64_t n_cand) { return (int)((n_cand + kGC - 1) / kGC)
 // the row's last CTA.
 constexpr int kRT = 256;   // threads
 constexpr int kRU = 16;    // rows in flight per half-warp per round
-constexpr int kRR = 4;     // rounds per CTA (fewer CTAs -> fewer partials / fences)
-constexpr int kRC = kRU * (kRT / 16) * kRR;  // kept rows per CTA (1024)
+constexpr int kRR = 8;     // max rounds per CTA (fewer CTAs -> fewer partials / fences)
+constexpr int kRS = kRU * (kRT / 16);        // kept rows per round (256)
+constexpr int kRC = kRS * kRR;               // max kept rows per CTA
 
 __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float *part,
-                                                     uint32_t *done) {
+                                                     uint32_t *done, int rounds) {
   __shared__ int32_t sj[kRC];
   __shared__ float sw[kRC];
   __shared__ float red[(kRT / 32) * 2 * 128];
@@ -217,16 +218,17 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
   const int row = b * a.Hq + kv * a.G + blockIdx.x;
   const int64_t k = a.g_cnt ? a.g_cnt[row] : a.hs[row].ksel;
-  const int64_t e0 = (int64_t)ch * kRC;
+  const int64_t per = (int64_t)kRS * rounds;  // kept rows of this CTA
+  const int64_t e0 = (int64_t)ch * per;
   if (k == 0) {  // nothing kept (a shard's slice can be empty): the row's share is zero
     if (ch == 0 && tid < 128) a.out[(int64_t)row * 128 + tid] = 0.0f;
     return;
   }
-  if (e0 >= k) return;  // only the ceil(k/kRC) CTAs holding kept rows take part
+  if (e0 >= k) return;  // only the ceil(k/per) CTAs holding kept rows take part
   const int64_t off = a.g_cnt ? a.g_off[row] : 0;
   const int32_t *li = a.sel_idx + (int64_t)row * a.k_max + off;
   const float *lw = a.sel_w + (int64_t)row * a.k_max + off;
-  for (int i = tid; i < kRC; i += kRT) {
+  for (int i = tid; i < per; i += kRT) {
     const bool v = e0 + i < k;
     sj[i] = v ? (int32_t)(li[e0 + i] - a.g_base) : -1;
     sw[i] = v ? lw[e0 + i] : 0.0f;
@@ -239,9 +241,9 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
-  const int nround = (int)((k - e0 + kRU * (kRT / 16) - 1) / (kRU * (kRT / 16)));
-  for (int rd = 0; rd < kRR && rd < nround; ++rd) {
-    const int base = rd * (kRU * (kRT / 16)) + hw * kRU;
+  const int nround = (int)((k - e0 + kRS - 1) / kRS);
+  for (int rd = 0; rd < rounds && rd < nround; ++rd) {
+    const int base = rd * kRS + hw * kRU;
     uint4 v[kRU];
 #pragma unroll
     for (int q = 0; q < kRU; ++q) {
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   __shared__ bool last;
   __syncthreads();
   if (tid == 0) {
-    const int nact = (int)((k + kRC - 1) / kRC);  // CTAs of this row that hold kept rows
+    const int nact = (int)((k + per - 1) / per);  // CTAs of this row that hold kept rows
     const unsigned prev = atomicAdd(&done[row], 1u);
     last = prev == (unsigned)(nact > 0 ? nact : 1) - 1;
     if (last) done[row] = 0;
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const int nact = (int)((k + kRC - 1) / kRC);
+  const int nact = (int)((k + per - 1) / per);
   if (tid < 128) {
     const float *p0 = part + (int64_t)row * nch * 128 + tid;
     float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -306,15 +308,21 @@ __global__ void __launch_bounds__(kRT) k_gather_rows(LayerArgs a, int nch, float
   }
 }
 
-int gather_rows_chunks(int64_t k_cap) { return (int)((k_cap + kRC - 1) / kRC); }
+int gather_rows_chunks(int64_t k_cap) { return (int)((k_cap + kRS - 1) / kRS); }  // rounds = 1
 
 cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, uint32_t *done,
                                cudaStream_t s) {
-  const int nch = gather_rows_chunks(k_cap);
+  // rounds per CTA: as many as keep >= 4 CTAs per SM (fewer partials and fences per row)
+  const int rows = a.B * a.Hq;
+  int rounds = 1;
+  while (rounds < kRR && (int64_t)rows * ((k_cap + (int64_t)kRS * rounds * 2 - 1) / ((int64_t)kRS * rounds * 2)) >=
+                             (int64_t)a.num_sms * 4)
+    rounds *= 2;
+  const int nch = (int)((k_cap + (int64_t)kRS * rounds - 1) / ((int64_t)kRS * rounds));
   if (nch == 0) return cudaSuccess;
   // CTAs beyond a row's k_sel exit at once (they only count if they hold kept rows)
   dim3 grid((unsigned)a.G, (unsigned)nch, (unsigned)(a.B * a.Hkv));
-  launch_chain(k_gather_rows, grid, dim3(kRT), 0, s, a, nch, part, done);
+  launch_chain(k_gather_rows, grid, dim3(kRT), 0, s, a, nch, part, done, rounds);
   note_launch();
   return cudaGetLastError();
 }
