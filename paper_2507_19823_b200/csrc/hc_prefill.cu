@@ -49,6 +49,11 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
                : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2 (2^-inf = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   const __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t *>(&h);
@@ -371,10 +376,11 @@ __global__ void __launch_bounds__(kTThreads, 2) k_blockwise_attn_tc(PrefillArgs 
     mbar_wait(&mbar, phase);
     phase ^= 1u;
     tc_fence_after();
-    // this thread's S row (TMEM lane = row): scaled, masked
-    const bool diag = k0 + kTM > i0 && (kb == 0 || k0 >= own0);
+    // this thread's S row (TMEM lane = row), raw scores; the log2(e)/sqrt(d) scale is folded
+    // into the exponent's FMA.  Masking only on the diagonal / ragged tiles (CTA-uniform).
+    const bool masked = (k0 + kTM > i0 && (kb == 0 || k0 >= own0)) || k0 + kTM > a.n;
     float sv[kTM];
-    float mt = -INFINITY;
+    float mraw = -INFINITY;
     {
       uint32_t r[32];
 #pragma unroll
@@ -382,15 +388,18 @@ __global__ void __launch_bounds__(kTThreads, 2) k_blockwise_attn_tc(PrefillArgs 
         HC_TLD32(tS + lane_sel + c4 * 32, r);
         tmem_wait_ld();
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const int64_t j = k0 + c4 * 32 + u;
-          float x = __uint_as_float(r[u]) * a.scale_log2;
-          if (j >= a.n || (diag && j > qi)) x = -INFINITY;
-          sv[c4 * 32 + u] = x;
-          mt = fmaxf(mt, x);
-        }
+        for (int u = 0; u < 32; ++u) sv[c4 * 32 + u] = __uint_as_float(r[u]);
       }
     }
+    if (masked) {
+      const int lim = (int)min((int64_t)kTM, min(a.n, qi + 1) - k0);  // keys < k0 + lim are visible
+#pragma unroll
+      for (int u = 0; u < kTM; ++u)
+        if (u >= lim) sv[u] = -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < kTM; ++u) mraw = fmaxf(mraw, sv[u]);
+    const float mt = mraw * a.scale_log2;
     const bool raise = mt > mref + 8.0f;  // also true for the first finite max
     float corr = 1.0f;
     if (raise) {
@@ -418,13 +427,14 @@ __global__ void __launch_bounds__(kTThreads, 2) k_blockwise_attn_tc(PrefillArgs 
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     float rs = 0.0f;
+    const float nm = mref == -INFINITY ? 0.0f : -mref;  // all-masked rows: sv = -inf -> p = 0
 #pragma unroll
     for (int cg = 0; cg < 16; ++cg) {  // P row (fp16, <= 2^8) -> swizzled smem (reuses sK)
       uint32_t w4[4];
 #pragma unroll
       for (int e2 = 0; e2 < 4; ++e2) {
-        const float p0 = mref == -INFINITY ? 0.0f : exp2f(sv[cg * 8 + 2 * e2] - mref);
-        const float p1 = mref == -INFINITY ? 0.0f : exp2f(sv[cg * 8 + 2 * e2 + 1] - mref);
+        const float p0 = ex2_approx(fmaf(sv[cg * 8 + 2 * e2], a.scale_log2, nm));
+        const float p1 = ex2_approx(fmaf(sv[cg * 8 + 2 * e2 + 1], a.scale_log2, nm));
         rs += p0 + p1;
         w4[e2] = pack_h2(p0, p1);
       }
