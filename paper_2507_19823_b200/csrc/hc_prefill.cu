@@ -344,26 +344,19 @@ __global__ void __launch_bounds__(kTThreads, 2) k_blockwise_attn_tc(PrefillArgs 
   uint32_t phase = 0;
   for (int t = 0; t < ntiles; ++t) {
     const int64_t k0 = t < n_anchor ? (int64_t)t * kTM : own0 + (int64_t)(t - n_anchor) * kTM;
-    // K and V tiles (key rows), coalesced: 16 consecutive threads read one 256-B row
-#pragma unroll 1
-    for (int it0 = 0; it0 < 16; it0 += 4) {
-      uint4 kv4[4], vv4[4];
+    // K and V tiles (key rows), coalesced (16 consecutive threads per 256-B row), all 32
+    // 16-B copies per thread in flight at once (cp.async, zero-fill past n)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int idx = (it0 + q) * kTThreads + tid, r = idx >> 4, cg = idx & 15;
-        const int64_t j = k0 + r;
-        const bool ok = j < a.n;
-        const int64_t off = (ok ? j : 0) * ks_ + (int64_t)kvh * kPD + cg * 8;
-        kv4[q] = ok ? *reinterpret_cast<const uint4 *>(a.k + off) : make_uint4(0, 0, 0, 0);
-        vv4[q] = ok ? *reinterpret_cast<const uint4 *>(a.v + off) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int idx = (it0 + q) * kTThreads + tid, r = idx >> 4, cg = idx & 15;
-        *reinterpret_cast<uint4 *>(sK + sw128_off(r, cg)) = kv4[q];
-        *reinterpret_cast<uint4 *>(sVt + sw128_off(r, cg)) = vv4[q];
-      }
+    for (int it = 0; it < 16; ++it) {
+      const int idx = it * kTThreads + tid, r = idx >> 4, cg = idx & 15;
+      const int64_t j = k0 + r;
+      const bool ok = j < a.n;
+      const int64_t off = (ok ? j : 0) * ks_ + (int64_t)kvh * kPD + cg * 8;
+      cp_async16(sK + sw128_off(r, cg), a.k + off, ok);
+      cp_async16(sVt + sw128_off(r, cg), a.v + off, ok);
     }
+    cp_async_commit();
+    cp_async_wait_all();
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
