@@ -11,10 +11,14 @@
 //       cluster reduce: CTA r owns bins [r*NB/cs, (r+1)*NB/cs) and sums them over peers;
 //       bound1: S, Θ = ⌈τ_q·S/2^24⌉, first bucket b* where mass reaches Θ or count k_max
 //   P2  fine count histogram inside b* -> cluster reduce -> bound2: exact Δ*, #ties r
-//   P3  ordered compaction (prefix over cluster ranks, block scan): ascending indices
-//       and weights W_j/S -> sel_idx / sel_w
-//   P4  gather: every CTA sums ã_j·V_j over ITS kept rows (half-warp per 256-B row,
-//       zero-copy when V is host-mapped); rank 0 adds the cs partials in rank order.
+//   P3  ordered compaction: per-warp (strict, tie) counts -> prefixes over warps and
+//       cluster ranks; each warp walks its chunk 256 tokens per step (8 per lane), warp
+//       scans give in-order positions, kept (Δ, token) are staged in shared memory and
+//       written lane-parallel: ascending indices and weights W_j/S -> sel_idx / sel_w
+//   P4  (HC_GATHER=fused only) gather: every CTA sums ã_j·V_j over ITS kept rows; the
+//       default path runs Eq. 5 in hc_gather.cu (k_gather_rows / k_gather_union).
+// Two instantiations: with P4 (1 CTA/SM) and selection-only (64 registers, 2 CTAs/SM
+// for long rows).
 // All sums that decide indices are integers: bit-exact and decomposition-invariant.
 #include <cooperative_groups.h>
 #include <stdlib.h>
