@@ -446,9 +446,10 @@ __global__ void __launch_bounds__(kFT, kOcc)
   {
     unsigned long long t_run = t_before + s_wt[warp];                      // ties before
     unsigned long long pos = s_before + s_ws[warp] + (t_run < r_ties ? t_run : r_ties);
-    // staging slice of this warp: 256 x (Δ, token) in the P1 mass bins (free after P2)
-    uint32_t *stg_d = reinterpret_cast<uint32_t *>(smem) + warp * 512;
-    uint32_t *stg_t = stg_d + 256;
+    // staging slice of this warp (in the P1 mass bins, free after P2): 256 x (Δ, offset in
+    // the step) + one dump slot that absorbs the stores of tokens not kept (branch-free)
+    uint32_t *stg_d = reinterpret_cast<uint32_t *>(smem) + warp * 257;
+    uint16_t *stg_o = reinterpret_cast<uint16_t *>(reinterpret_cast<uint32_t *>(smem) + (kFT / 32) * 257) + warp * 257;
     float vn[8], vnn[8];  // two steps prefetched
     if (w_lo < w_hi) load8(w_lo + lane * 8, vn);
     if (w_lo + 256 < w_hi) load8(w_lo + 256 + lane * 8, vnn);
@@ -493,20 +494,17 @@ __global__ void __launch_bounds__(kFT, kOcc)
       unsigned ties_seen = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        bool take = dl[u] < delta_star;
-        if (!take && dl[u] == delta_star && t0 + u < w_hi) {
-          take = ties_seen < taken;
-          ++ties_seen;
-        }
-        if (take) {
-          stg_d[q] = dl[u];
-          stg_t[q] = (uint32_t)(t0 + u);
-          ++q;
-        }
+        const bool is_tie = dl[u] == delta_star && t0 + u < w_hi;
+        const bool take = dl[u] < delta_star || (is_tie && ties_seen < taken);
+        ties_seen += is_tie ? 1u : 0u;
+        const unsigned slot = take ? q : 256u;
+        stg_d[slot] = dl[u];
+        stg_o[slot] = (uint16_t)(lane * 8 + u);
+        q += take ? 1u : 0u;
       }
       __syncwarp();
       for (unsigned i = lane; i < kept_tot; i += 32) {
-        oi[pos + i] = (int32_t)(j0 + stg_t[i]);
+        oi[pos + i] = (int32_t)(j0 + tb + stg_o[i]);
         ow[pos + i] = __fmul_rn((float)mass_d(stg_d[i], kappa), inv_den);
       }
       __syncwarp();
