@@ -190,6 +190,10 @@ class Workload:
         self.out = torch.zeros((L, B, self.Hq, d), dtype=torch.float32, device=device)
         self.out_host = torch.zeros_like(self.out, device="cpu").pin_memory()
         self.cpu_gather = cfg.get("cpu_gather", False)
+        self.hetero = None
+        if cfg.get("host_frac", 0.0) > 0.0:  # heterogeneous Eq. 5 (GPU pull + host threads)
+            from paper_2507_19823_b200.hetero import HeteroEq5
+            self.hetero = HeteroEq5(self.kc, self.vs, cfg["k_max"], cfg["host_frac"], device=device)
         self.bud = hc.budget(cfg["tau"], cfg["k_max"], select_only=self.cpu_gather,
                              shared_kv=cfg.get("shared_kv", False))
         self.ws = hc.Workspace(self.kc.workspace_bytes(self.bud), device=device)
@@ -234,6 +238,8 @@ class Workload:
                 hc.profile_scan_events(*self.ev[l])
             if self.cpu_gather:
                 self._step_cpu_gather(l)
+            elif self.hetero is not None:
+                self.hetero(self.q[l], l, self.bud, self.out[l], self.sel_k[l], self.ws)
             elif self.shard is None:
                 hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
                                     sel_k=self.sel_k[l], ws=self.ws)
@@ -337,9 +343,11 @@ def time_graph(g, K, W, dist=None):
     return ms
 
 
-def union_gather_bytes(wl) -> float:
+def union_gather_bytes(wl, host_frac: float = 0.0):
     """Value bytes the union gather reads per step: re-run the step's selections (eager, after
-    the timed region) and count, per (b, layer, kv), the union of the G heads' kept rows."""
+    the timed region) and count, per (b, layer, kv), the union of the G heads' kept rows.
+    With a heterogeneous split returns (GPU-pulled bytes, host-summed bytes): rows with index
+    >= t_split = round(host_frac * n_q) go over the host link, the rest stay in host DRAM."""
     import torch
 
     import paper_2507_19823_b200 as hc
@@ -349,14 +357,20 @@ def union_gather_bytes(wl) -> float:
     w = torch.zeros((B, H * G, km), dtype=torch.float32, device="cuda")
     k = torch.zeros((B, H * G), dtype=torch.int64, device="cuda")
     bud = hc.budget(cfg["tau"], km, select_only=True, shared_kv=cfg.get("shared_kv", False))
-    rows = 0
+    rows = rows_h = 0
     for l in range(L):
         hc.decode_attention(wl.q[l], wl.kc, wl.vs, l, bud, sel_idx=idx, sel_w=w, sel_k=k, ws=wl.ws,
                             out=wl.out[l])
+        t_split = int(round(host_frac * wl.kc.n_q(l)))
         for b in range(B):
             for kv in range(H):
                 sets = [idx[b, kv * G + h, : int(k[b, kv * G + h])] for h in range(G)]
-                rows += int(torch.unique(torch.cat(sets)).numel())
+                u = torch.unique(torch.cat(sets))
+                nh = int((u < t_split).sum())
+                rows_h += nh
+                rows += int(u.numel()) - nh
+    if host_frac > 0.0:
+        return rows * d * 2.0, rows_h * d * 2.0
     return rows * d * 2.0
 
 
@@ -489,6 +503,9 @@ def run_virtual(args, cfg, R):
 
 
 # ----------------------------------------------------------------------------- main
+HOST_FRAC_DEFAULT = 0.6  # measured optimum on the B200 box (DESIGN §8b f1, tools/hetero_sweep.py)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -499,6 +516,10 @@ def main():
     ap.add_argument("--cpu-gather", action="store_true",
                     help="the paper's split (SURVEY f1): GPU selects, Eq. 5 runs on host threads "
                          "over the host-resident values (needs a host-V config, e.g. 3)")
+    ap.add_argument("--host-frac", type=float, default=None,
+                    help="heterogeneous Eq. 5 for host-resident values: host threads sum the kept "
+                         "rows of this share of the token range while the GPU pulls the rest "
+                         "(default for host-V configs: %s; 0 = GPU only)" % HOST_FRAC_DEFAULT)
     ap.add_argument("--lut8", action="store_true",
                     help="8-bit query/codebook table variant (R2b, SURVEY f3)")
     ap.add_argument("--code-bits", type=int, default=16, choices=[16, 13],
@@ -523,6 +544,14 @@ def main():
     cfg["cpu_gather"] = bool(args.cpu_gather)
     cfg["shared_kv"] = bool(args.shared_kv)
     cfg["code_bits"] = args.code_bits
+    hf = args.host_frac if args.host_frac is not None else (
+        HOST_FRAC_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather else 0.0)
+    cfg["host_frac"] = hf
+    if hf > 0.0:
+        if cfg["placement"] != 1 or args.cpu_gather:
+            raise SystemExit("--host-frac needs host-resident values (e.g. --config 3) and no --cpu-gather")
+        cfg["workload"] += (f"; heterogeneous Eq. 5: host threads sum the kept rows of the first "
+                            f"{hf:.2f} of the tokens over host DRAM, the GPU pulls the rest zero-copy")
     if args.code_bits == 13:
         cfg["workload"] += "; packed 13-bit codes (f3(ii))"
     if args.shared_kv:
@@ -616,9 +645,16 @@ def main():
     # value-gather bytes (all layers, all heads, this rank's share) and the host-link peak
     v_bytes = ksel * B * wl.Hq * L * d * 2 / (world if sharded_mode else 1)
     host_link = None
+    host_dram = None
     if cfg["placement"] == 1:
         if not wl.cpu_gather and world == 1:
-            v_bytes = union_gather_bytes(wl)  # rows actually read: union over the GQA heads
+            if wl.hetero is not None:  # the host's share of the rows stays in host DRAM
+                v_bytes, h_bytes = union_gather_bytes(wl, cfg["host_frac"])
+                host_dram = {"bytes_per_step": h_bytes, "rows": "union of the GQA heads' kept rows, "
+                             "index < t_split", "achieved_gbs_lower_bound": h_bytes / (ms_per_step * 1e-3) / 1e9,
+                             "host_frac": cfg["host_frac"], "threads": os.cpu_count()}
+            else:
+                v_bytes = union_gather_bytes(wl)  # rows actually read: union over the GQA heads
         pk = measure_h2d_gbs()
         host_link = {"bytes_per_step": v_bytes, "rows": "union of the GQA heads' kept rows",
                      "achieved_gbs_lower_bound": v_bytes / (ms_per_step * 1e-3) / 1e9,
@@ -653,6 +689,7 @@ def main():
                                          "scan / select / gather share the step (see DESIGN.md §5)")},
         "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / n},
         "host_link": host_link,
+        "host_dram": host_dram,
         "e2e": {"value": jobs * 1000.0 / ms_e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "gpu_launches": launches_per_step * args.steps,

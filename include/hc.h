@@ -151,6 +151,14 @@ uint64_t hc_launch_count(void);
  * stream capture they become external event-record nodes of the graph. */
 hc_status hc_profile_scan_events(void *begin_event, void *end_event);
 
+/* Host value-store memory (A8): page-lock caller-allocated host memory (e.g. an
+ * anonymous mapping advised for 2 MiB transparent huge pages, so random row reads by host
+ * threads and by the GPU do not miss the TLB on every row) and map it into the device
+ * address space (cudaHostRegister Portable | Mapped).  *dev_ptr = the device-accessible
+ * address to put in hc_vstore.base (HC_V_HOST_MAPPED).  Synchronous; not for the hot path. */
+hc_status hc_host_register(void *host, size_t bytes, void **dev_ptr);
+hc_status hc_host_unregister(void *host);
+
 /* Codebook constant of R2: out[l][ci][e] = max_m |codebook[l][ci][m][e]| for all L layers.
  * codebook [L][cbg][c][dbar] fp32, out [L][cbg][dbar] fp32 (device).  Call once per codebook
  * and store the result in hc_kcache.cb_absmax. */
@@ -259,6 +267,46 @@ hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const
                                        int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
                                        int32_t G, int32_t d, float *out, int32_t threads,
                                        hc_stream_t stream);
+
+/* ---- Heterogeneous Eq. 5 (§3.2 "Heterogeneous Attention Computation"): the
+ * kept value rows are summed partly on the GPU (zero-copy pull over the host link) and
+ * partly by host threads over host DRAM (the paper's CPU part), concurrently, split
+ * by token index at t_split <= n_q (DESIGN §8b f1; paper_2507_19823_b200/hetero.py):
+ *   out = Σ_{j∈sel, j<t_split} ã_j V_j   (hc_*host_weighted_sum_range, host; value store only)
+ *       + Σ_{j∈sel, j>=t_split} ã_j V_j  (hc_gather_values, GPU; incl. the resident window)
+ *   joined by hc_add_partial.
+ *
+ * hc_host_weighted_sum_range: as hc_host_weighted_sum restricted to kept tokens
+ *   tok_begin <= j < tok_end (rows with no kept token in range get 0).  Work items are
+ *   (KV unit, 4096-token chunk); the G heads of a unit run back to back over a chunk so
+ *   shared rows come from the core's cache; chunk partials are added in chunk order (the
+ *   result does not depend on `threads`).  F16C/AVX-512 or AVX2 when the CPU has them.
+ *   HC_ERR_RANGE if tok_begin < 0 or tok_end < tok_begin. */
+hc_status hc_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
+                                     int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
+                                     int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
+                                     int64_t tok_begin, int64_t tok_end, float *out, int32_t threads);
+hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k,
+                                             int64_t rows, int64_t k_stride, const uint16_t *V,
+                                             int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
+                                             int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end,
+                                             float *out, int32_t threads, hc_stream_t stream);
+
+/* GPU Eq. 5 over a GIVEN selection, restricted to kept tokens tok_begin <= j < tok_end:
+ *   out[b][h] = Σ_{r<sel_k[row], tok_begin<=sel_idx[row][r]<tok_end} sel_w[row][r] · V_j
+ * with row = b*Hq + h.  sel_idx/sel_w [B*Hq][k_stride] (ascending indices per row) and
+ * sel_k [B*Hq] are DEVICE arrays as hc_decode_attention writes them; V is the layer's value
+ * store (HBM or host-mapped: only kept rows in range are read; rows kept by several GQA
+ * heads once).  ws: hc_decode_workspace_bytes(kc, budget with k_max = k_stride); its
+ * gather region is used (the selection arrays are the caller's).  An empty range writes 0.
+ * HC_ERR_RANGE for tok_begin < 0 or tok_end < tok_begin. */
+hc_status hc_gather_values(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, const int32_t *sel_idx,
+                           const float *sel_w, const int64_t *sel_k, int64_t k_stride, int64_t tok_begin,
+                           int64_t tok_end, float *out, void *ws, size_t ws_bytes, hc_stream_t stream);
+
+/* out[i] += part[i] for i < n (fp32).  part may be host-mapped pinned memory (the host
+ * share of the heterogeneous split, read zero-copy after the host node finished). */
+hc_status hc_add_partial(float *out, const float *part, int64_t n, hc_stream_t stream);
 
 /* ---- Sequence-sharded decode, one layer, R ranks (one per GPU).
  * Rank `rank` holds the contiguous GLOBAL token range [shard_base, shard_base + n_q[layer])

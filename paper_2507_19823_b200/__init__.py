@@ -26,7 +26,9 @@ EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_ev
            "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
            "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
            "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish", "hc_kmeans_workspace_bytes",
-           "hc_kmeans_step", "hc_pack_codes13", "hc_blockwise_attention", "hc_prefill_append"]
+           "hc_kmeans_step", "hc_pack_codes13", "hc_blockwise_attention", "hc_prefill_append",
+           "hc_host_weighted_sum_range", "hc_enqueue_host_weighted_sum_range", "hc_gather_values",
+           "hc_add_partial", "hc_host_register", "hc_host_unregister"]
 
 
 class HcError(RuntimeError):
@@ -100,6 +102,20 @@ def lib():
         L.hc_host_weighted_sum.restype = i32
         L.hc_enqueue_host_weighted_sum.argtypes = hw + [p]
         L.hc_enqueue_host_weighted_sum.restype = i32
+        hr = [p, p, p, i64, i64, p, i64, i64, i32, i32, i32, i64, i64, p, i32]
+        L.hc_host_weighted_sum_range.argtypes = hr
+        L.hc_host_weighted_sum_range.restype = i32
+        L.hc_enqueue_host_weighted_sum_range.argtypes = hr + [p]
+        L.hc_enqueue_host_weighted_sum_range.restype = i32
+        L.hc_gather_values.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, p, i64,
+                                       i64, i64, p, p, C.c_size_t, p]
+        L.hc_gather_values.restype = i32
+        L.hc_add_partial.argtypes = [p, p, i64, p]
+        L.hc_add_partial.restype = i32
+        L.hc_host_register.argtypes = [p, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.hc_host_register.restype = i32
+        L.hc_host_unregister.argtypes = [p]
+        L.hc_host_unregister.restype = i32
         L.hc_blockwise_attention.argtypes = [p, p, p, i64, i32, i32, i32, i64, p, p]
         L.hc_blockwise_attention.restype = i32
         L.hc_prefill_append.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, i64, p]
@@ -250,26 +266,92 @@ def train_codebook(keys, g: int, c: int, iters: int = 200, batch: int = 10000, s
 
 
 # ----------------------------------------------------------------------------- caches
+class HostBuffer:
+    """Page-locked, device-mapped host memory for the offloaded value store (A8):
+    an anonymous mapping aligned to and advised for 2 MiB transparent huge pages
+    (madvise MADV_HUGEPAGE), first-touched by parallel threads, then registered with
+    hc_host_register.  Random 256-byte row reads by host threads and by the GPU then walk
+    one page-table entry per 2 MiB instead of per 4 KiB (a 34 GB store has 8.4 M 4-KiB PTEs,
+    67 MB of page tables -- a DRAM miss per row on top of the row itself)."""
+
+    HUGE = 2 << 20
+
+    def __init__(self, nbytes: int, huge: bool = True, threads: int = 16):
+        import concurrent.futures as cf
+        import mmap
+        HP = self.HUGE
+        self.size = max(HP, (int(nbytes) + HP - 1) // HP * HP)
+        self.mm = mmap.mmap(-1, self.size + HP, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        self._anchor = C.c_char.from_buffer(self.mm)
+        base = C.addressof(self._anchor)
+        self.offset = (base + HP - 1) // HP * HP - base
+        self.addr = base + self.offset
+        self.huge = False
+        if huge:
+            libc = C.CDLL(None, use_errno=True)
+            libc.madvise.argtypes = [C.c_void_p, C.c_size_t, C.c_int]
+            self.huge = libc.madvise(self.addr, self.size, 14) == 0  # MADV_HUGEPAGE
+        step = max(HP, (self.size // max(1, threads)) // HP * HP)
+        with cf.ThreadPoolExecutor(max_workers=threads) as ex:  # first touch (ctypes drops the GIL)
+            list(ex.map(lambda o: C.memset(self.addr + o, 0, min(step, self.size - o)),
+                        range(0, self.size, step)))
+        dev = C.c_void_p()
+        _check(lib().hc_host_register(self.addr, self.size, C.byref(dev)))
+        self.dev = int(dev.value)
+        self.registered = True
+
+    def tensor(self, shape, dtype):
+        import torch
+        n = 1
+        for x in shape:
+            n *= int(x)
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        mv = memoryview(self.mm)[self.offset:self.offset + nbytes]
+        return torch.frombuffer(mv, dtype=dtype).view(*shape)
+
+    def device_pointer(self, host_ptr: int) -> int:
+        return self.dev + (int(host_ptr) - self.addr)
+
+    def close(self):
+        if getattr(self, "registered", False):
+            lib().hc_host_unregister(self.addr)
+            self.registered = False
+
+    def __del__(self):  # unregister before the mapping goes (its addresses get reused)
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class VStore:
     """Value store [B][L][Hkv][n_cap][d] fp16, in HBM or host-pinned mapped memory."""
     tensor: object           # torch fp16 tensor (cuda, or pinned cpu)
     placement: int
     n_cap: int
+    host: HostBuffer | None = None
 
     @staticmethod
-    def allocate(B, L, Hkv, n_cap, d, placement=HC_V_DEVICE, device="cuda"):
+    def allocate(B, L, Hkv, n_cap, d, placement=HC_V_DEVICE, device="cuda", huge=True):
+        """placement HC_V_HOST_MAPPED: a HostBuffer (2 MiB THP-advised, registered) unless
+        huge=False (torch pinned memory, 4 KiB pages)."""
         import torch
         if placement == HC_V_DEVICE:
             t = torch.empty((B, L, Hkv, n_cap, d), dtype=torch.float16, device=device)
-        else:
-            t = torch.empty((B, L, Hkv, n_cap, d), dtype=torch.float16, pin_memory=True)
+            return VStore(t, placement, n_cap)
+        if huge:
+            hb = HostBuffer(B * L * Hkv * n_cap * d * 2)
+            if hb.dev == hb.addr:  # UVA: host and device addresses coincide (callers rely on it)
+                return VStore(hb.tensor((B, L, Hkv, n_cap, d), torch.float16), placement, n_cap, hb)
+            hb.close()
+        t = torch.empty((B, L, Hkv, n_cap, d), dtype=torch.float16, pin_memory=True)
         return VStore(t, placement, n_cap)
 
     def struct(self) -> hc_vstore:
         ptr = self.tensor.data_ptr()
         if self.placement == HC_V_HOST_MAPPED:
-            ptr = host_device_pointer(ptr)
+            ptr = self.host.device_pointer(ptr) if self.host is not None else host_device_pointer(ptr)
         return hc_vstore(self.placement, ptr, self.n_cap)
 
 
@@ -409,3 +491,38 @@ def select_topk(scores, d: int, bud: hc_budget, idx=None, w=None, k=None, ws=Non
     _check(lib().hc_select_topk(_ptr(scores), rows, n, d, bud, _ptr(idx), _ptr(w), _ptr(k),
                                 _ptr(ws.t), ws.nbytes, _stream(stream)))
     return idx, w, k
+
+
+# ----------------------------------------------------------------------------- heterogeneous Eq. 5
+def gather_values(kc: KCache, vstore: VStore, layer: int, sel_idx, sel_w, sel_k, tok_begin: int,
+                  tok_end: int, out, ws: Workspace, stream=None):
+    """hc_gather_values: GPU Eq. 5 over a given selection, kept tokens in [tok_begin, tok_end)."""
+    vs = vstore.struct()
+    _check(lib().hc_gather_values(C.byref(kc.s), C.byref(vs), layer, _ptr(sel_idx), _ptr(sel_w),
+                                  _ptr(sel_k), sel_idx.shape[-1], int(tok_begin), int(tok_end), _ptr(out),
+                                  _ptr(ws.t), ws.nbytes, _stream(stream)))
+    return out
+
+
+def add_partial(out, part, stream=None):
+    """hc_add_partial: out += part (fp32; part may be pinned host memory, read zero-copy)."""
+    _check(lib().hc_add_partial(_ptr(out), C.c_void_p(host_device_pointer(part.data_ptr()))
+                                if not part.is_cuda else _ptr(part), out.numel(), _stream(stream)))
+    return out
+
+
+def host_weighted_sum_range(idx, w, k, vstore: VStore, layer: int, G: int, tok_begin: int, tok_end: int,
+                            out, threads: int = 0, stream=None):
+    """hc_(enqueue_)host_weighted_sum_range on HOST tensors: idx/w [rows][k_stride], k [rows],
+    out [rows][d]; V = the pinned value store's layer.  stream=None runs synchronously, else
+    the work is enqueued as a host node on `stream` (graph-capturable)."""
+    B, L, Hkv, n_cap, d = vstore.tensor.shape
+    V = vstore.tensor[0, layer]
+    rows, ks = idx.shape
+    args = [_ptr(idx), _ptr(w), _ptr(k), rows, ks, _ptr(V), L * Hkv * n_cap * d, n_cap * d, Hkv * G, G, d,
+            int(tok_begin), int(tok_end), _ptr(out), int(threads)]
+    if stream is None:
+        _check(lib().hc_host_weighted_sum_range(*args))
+    else:
+        _check(lib().hc_enqueue_host_weighted_sum_range(*args, _stream(stream)))
+    return out

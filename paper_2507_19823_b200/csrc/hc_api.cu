@@ -223,6 +223,19 @@ hc_status hc_profile_scan_events(void *begin_event, void *end_event) {
   return HC_OK;
 }
 
+hc_status hc_host_register(void *host, size_t bytes, void **dev_ptr) {
+  if (!host || !bytes || !dev_ptr) return fail(HC_ERR_ARG, "host/bytes/dev_ptr");
+  cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) return cuda_check(e, "cudaHostRegister");
+  e = cudaHostGetDevicePointer(dev_ptr, host, 0);
+  return e != cudaSuccess ? cuda_check(e, "cudaHostGetDevicePointer") : HC_OK;
+}
+
+hc_status hc_host_unregister(void *host) {
+  cudaError_t e = cudaHostUnregister(host);
+  return e != cudaSuccess ? cuda_check(e, "cudaHostUnregister") : HC_OK;
+}
+
 hc_status hc_quantize_keys(const uint16_t *keys, int64_t rows, const float *codebook, hc_vq vq,
                            uint16_t *codes, int64_t code_stride, hc_stream_t stream) {
   hc_status st = check_vq(vq);
@@ -453,6 +466,7 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   a.c = kc->vq.c; a.cbg = kc->vq.cbg; a.dbar = (int)(d / g); a.cpow2 = Lw.cpow2;
   a.lut8 = kc->vq.lut_bits == 8 ? 1 : 0;
   a.n_q = n_q; a.n_res = n_res; a.n_cand = n_cand; a.n_cap = ncap; a.res_cap = W > 0 ? W : 1;
+  a.gtok_lo = 0; a.gtok_hi = n_cand;
   a.q = q;
   a.C = kc->codebook + (int64_t)layer * kc->vq.cbg * kc->vq.c * (d / g);
   a.codes = kc->codes + (int64_t)layer * H * g * ncap;
@@ -598,6 +612,43 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     }
   }
   return HC_OK;
+}
+
+hc_status hc_gather_values(const hc_kcache *kc, const hc_vstore *vs, int32_t layer, const int32_t *sel_idx,
+                           const float *sel_w, const int64_t *sel_k, int64_t k_stride, int64_t tok_begin,
+                           int64_t tok_end, float *out, void *ws, size_t ws_bytes, hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!sel_idx || !sel_w || !sel_k || !out) return fail(HC_ERR_ARG, "sel_idx/sel_w/sel_k/out NULL");
+  if (k_stride < 1) return fail(HC_ERR_ARG, "k_stride < 1");
+  if (tok_begin < 0 || tok_end < tok_begin) return fail(HC_ERR_RANGE, "bad token range [%lld, %lld)",
+                                                        (long long)tok_begin, (long long)tok_end);
+  LayerArgs a;
+  Layout Lw;
+  hc_budget bud{1.0f, k_stride, 0, 0, 0};
+  hc_status st = prepare_layer(nullptr, kc, vs, layer, bud, out, const_cast<int32_t *>(sel_idx),
+                               const_cast<float *>(sel_w), const_cast<int64_t *>(sel_k), ws, ws_bytes, s,
+                               false, a, Lw);
+  if (st) return st;
+  a.k_in = sel_k;
+  a.gtok_lo = tok_begin < a.n_cand ? tok_begin : a.n_cand;
+  a.gtok_hi = tok_end < a.n_cand ? tok_end : a.n_cand;
+  uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_udone);
+  cudaError_t e = cudaMemsetAsync(done, 0, (size_t)a.B * a.Hkv * 4, s);
+  if (e != cudaSuccess) return cuda_check(e, "gather counters");
+  if (a.gtok_hi <= a.gtok_lo) {  // nothing in range: the GPU share is zero
+    e = cudaMemsetAsync(out, 0, (size_t)a.B * a.Hq * a.d * 4, s);
+    return e != cudaSuccess ? cuda_check(e, "gather zero") : HC_OK;
+  }
+  if ((e = launch_gather_union(a, (float *)((uint8_t *)ws + Lw.o_upart), done, s)) != cudaSuccess)
+    return cuda_check(e, "gather");
+  return HC_OK;
+}
+
+hc_status hc_add_partial(float *out, const float *part, int64_t n, hc_stream_t stream) {
+  if (!out || !part) return fail(HC_ERR_ARG, "out/part NULL");
+  if (n < 0) return fail(HC_ERR_ARG, "n < 0");
+  cudaError_t e = launch_add_partial(out, part, n, (cudaStream_t)stream);
+  return e != cudaSuccess ? cuda_check(e, "add partial") : HC_OK;
 }
 
 // ---------------------------------------------------------------- sequence-sharded decode

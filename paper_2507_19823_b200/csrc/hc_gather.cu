@@ -47,16 +47,19 @@ __global__ void __launch_bounds__(kGT) k_gather_union(LayerArgs a, int nchunks, 
   pdl_wait();
   const int ch = blockIdx.x, u = blockIdx.y;
   const int b = u / a.Hkv, kv = u - b * a.Hkv;
-  const int64_t j0 = (int64_t)ch * kGC;
-  const int64_t j1 = j0 + kGC < a.n_cand ? j0 + kGC : a.n_cand;
+  // chunk ch covers [cb + ch*kGC, +kGC) ∩ [gtok_lo, gtok_hi), cb = gtok_lo rounded down
+  const int64_t cb = a.gtok_lo / kGC * kGC;
+  const int64_t j0 = cb + (int64_t)ch * kGC;  // slot t of wtab / ulist = token j0 + t
+  const int64_t jlo = j0 > a.gtok_lo ? j0 : a.gtok_lo;
+  const int64_t j1 = j0 + kGC < a.gtok_hi ? j0 + kGC : a.gtok_hi;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < G * kGC; i += kGT) (&wtab[0][0])[i] = 0.0f;
   if (tid < G) {
     const int row = b * a.Hq + kv * G + tid;
-    const int64_t k = a.hs[row].ksel;
+    const int64_t k = a.k_in ? a.k_in[row] : a.hs[row].ksel;
     const int32_t *li = a.sel_idx + (int64_t)row * a.k_max;
-    s_lo[tid] = (int)lower_bound_i32(li, k, j0);
-    s_hi[tid] = (int)lower_bound_i32(li, k, j1);
+    s_lo[tid] = (int)lower_bound_i32(li, k, jlo);
+    s_hi[tid] = (int)lower_bound_i32(li, k, j1 > jlo ? j1 : jlo);
   }
   __syncthreads();
 #pragma unroll
@@ -191,6 +194,20 @@ __global__ void __launch_bounds__(kGT) k_gather_union(LayerArgs a, int nchunks, 
 }
 
 int gather_union_chunks(int64_t n_cand) { return (int)((n_cand + kGC - 1) / kGC); }
+
+__global__ void k_add_partial(float *out, const float *part, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += part[i];
+}
+
+cudaError_t launch_add_partial(float *out, const float *part, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  launch_chain(k_add_partial, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, out, part, n);
+  note_launch();
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------------------------------
 // High-occupancy per-head gather (HBM values): CTA = (query head, chunk of kRC kept
@@ -328,7 +345,8 @@ cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, u
 }
 
 cudaError_t launch_gather_union(const LayerArgs &a, float *part, uint32_t *done, cudaStream_t s) {
-  const int nch = gather_union_chunks(a.n_cand);
+  const int64_t cb = a.gtok_lo / kGC * kGC;
+  const int nch = a.gtok_hi > a.gtok_lo ? gather_union_chunks(a.gtok_hi - cb) : 0;
   if (nch == 0) return cudaSuccess;
   dim3 grid((unsigned)nch, (unsigned)(a.B * a.Hkv));
   switch (a.G) {

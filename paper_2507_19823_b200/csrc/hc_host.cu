@@ -1,17 +1,34 @@
 // hc_host.cu -- the paper's "CPU part" of Eq. 2 (§3.2):
 // Eq. 5's sparse weighted sum over the offloaded values, executed on host threads from
-// the selection the GPU produced.  fp16 -> fp32 through a 64K-entry table; each thread
-// owns whole rows (query heads), accumulates in fp32 in index order.
+// the selection the GPU produced -- for the whole token range, or for the token range
+// [tok_begin, tok_end) the host owns in the heterogeneous split (the GPU pulls the rest
+// over the host link, hc_gather_values; DESIGN §8b f1).
+//
+// Work item = (KV unit u = (b, kv), token chunk of kHostChunk tokens).  For each of the
+// unit's G query heads the item cuts the head's ascending kept list to the chunk (binary
+// search) and accumulates w_j·V_j in fp32; heads run back to back over the same chunk, so
+// a row kept by several heads is read from DRAM once and from the core's L2 afterwards
+// (the GQA union, as in k_gather_union).  Chunk partials are added in chunk order:
+// results do not depend on the thread count or schedule.
+// fp16 -> fp32 with F16C (AVX-512 or AVX2, runtime-dispatched), rows prefetched
+// g_pf entries ahead; scalar table fallback on CPUs without F16C.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 #include <omp.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
+#include <vector>
 
 #include "../../include/hc.h"
 
 namespace {
+
+constexpr int64_t kHostChunk = 4096;  // tokens per work item
+int g_pf = 16;                        // kept rows prefetched ahead (HC_HOST_PF)
+int g_hint = 0;                       // 0: T0, 1: T1, 2: T2 (HC_HOST_HINT)
 
 float g_h2f[65536];
 std::atomic<int> g_h2f_ready{0};
@@ -43,6 +60,21 @@ void init_table() {
   g_h2f_ready.store(1, std::memory_order_release);
 }
 
+enum Isa { kScalar = 0, kAvx2 = 1, kAvx512 = 2 };
+Isa detect_isa() {
+  static int isa = -1;
+  if (isa < 0) {
+    __builtin_cpu_init();
+    if (__builtin_cpu_supports("avx512f") && __builtin_cpu_supports("f16c") && __builtin_cpu_supports("fma"))
+      isa = kAvx512;
+    else if (__builtin_cpu_supports("avx2") && __builtin_cpu_supports("f16c") && __builtin_cpu_supports("fma"))
+      isa = kAvx2;
+    else
+      isa = kScalar;
+  }
+  return (Isa)isa;
+}
+
 struct HostArgs {
   const int32_t *idx;
   const float *w;
@@ -53,28 +85,131 @@ struct HostArgs {
   int32_t Hq, G, d;
   float *out;
   int32_t threads;
+  int64_t tok_begin, tok_end;  // host-owned token range (global indices)
   bool owned_once;
 };
 
-void run(const HostArgs &a) {
-  init_table();
-  const int nt = a.threads > 0 ? a.threads : omp_get_max_threads();
-#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
-  for (int64_t row = 0; row < a.rows; ++row) {
-    const int64_t b = row / a.Hq, hq = row % a.Hq, kv = hq / a.G;
-    const uint16_t *Vb = a.V + b * a.v_b_stride + kv * a.v_kv_stride;
-    float acc[256];
-    for (int e = 0; e < a.d; ++e) acc[e] = 0.0f;
-    const int64_t kk = a.k[row];
-    const int32_t *ix = a.idx + row * a.k_stride;
-    const float *wt = a.w + row * a.k_stride;
-    for (int64_t r = 0; r < kk; ++r) {
-      const uint16_t *vr = Vb + (int64_t)ix[r] * a.d;
-      const float wr = wt[r];
-      if (r + 4 < kk) __builtin_prefetch(Vb + (int64_t)ix[r + 4] * a.d, 0, 0);
-      for (int e = 0; e < a.d; ++e) acc[e] += wr * g_h2f[vr[e]];
+inline void prefetch_row(const uint16_t *p, int d) {
+  const char *c = reinterpret_cast<const char *>(p);
+  if (g_hint == 0) for (int o = 0; o < d * 2; o += 64) _mm_prefetch(c + o, _MM_HINT_T0);
+  else if (g_hint == 1) for (int o = 0; o < d * 2; o += 64) _mm_prefetch(c + o, _MM_HINT_T1);
+  else for (int o = 0; o < d * 2; o += 64) _mm_prefetch(c + o, _MM_HINT_T2);
+}
+
+// acc[0..d) += Σ_{r in [lo, hi)} w[r] · V[ix[r]]
+__attribute__((target("avx512f,f16c,fma"))) void accum_avx512(const uint16_t *Vb, const int32_t *ix,
+                                                              const float *wt, int64_t lo, int64_t hi,
+                                                              int d, float *acc) {
+  if (d == 128) {
+    __m512 a[8];
+    for (int q = 0; q < 8; ++q) a[q] = _mm512_loadu_ps(acc + 16 * q);
+    for (int64_t r = lo; r < hi; ++r) {
+      if (r + g_pf < hi) prefetch_row(Vb + (int64_t)ix[r + g_pf] * 128, 128);
+      const uint16_t *v = Vb + (int64_t)ix[r] * 128;
+      const __m512 w = _mm512_set1_ps(wt[r]);
+      for (int q = 0; q < 8; ++q)
+        a[q] = _mm512_fmadd_ps(w, _mm512_cvtph_ps(_mm256_loadu_si256((const __m256i *)(v + 16 * q))), a[q]);
     }
-    for (int e = 0; e < a.d; ++e) a.out[row * a.d + e] = acc[e];
+    for (int q = 0; q < 8; ++q) _mm512_storeu_ps(acc + 16 * q, a[q]);
+    return;
+  }
+  for (int64_t r = lo; r < hi; ++r) {
+    if (r + g_pf < hi) prefetch_row(Vb + (int64_t)ix[r + g_pf] * d, d);
+    const uint16_t *v = Vb + (int64_t)ix[r] * d;
+    const __m512 w = _mm512_set1_ps(wt[r]);
+    for (int e = 0; e < d; e += 16)
+      _mm512_storeu_ps(acc + e, _mm512_fmadd_ps(w, _mm512_cvtph_ps(_mm256_loadu_si256((const __m256i *)(v + e))),
+                                                _mm512_loadu_ps(acc + e)));
+  }
+}
+
+__attribute__((target("avx2,f16c,fma"))) void accum_avx2(const uint16_t *Vb, const int32_t *ix,
+                                                         const float *wt, int64_t lo, int64_t hi, int d,
+                                                         float *acc) {
+  for (int64_t r = lo; r < hi; ++r) {
+    if (r + g_pf < hi) prefetch_row(Vb + (int64_t)ix[r + g_pf] * d, d);
+    const uint16_t *v = Vb + (int64_t)ix[r] * d;
+    const __m256 w = _mm256_set1_ps(wt[r]);
+    for (int e = 0; e < d; e += 8)
+      _mm256_storeu_ps(acc + e, _mm256_fmadd_ps(w, _mm256_cvtph_ps(_mm_loadu_si128((const __m128i *)(v + e))),
+                                                _mm256_loadu_ps(acc + e)));
+  }
+}
+
+void accum_scalar(const uint16_t *Vb, const int32_t *ix, const float *wt, int64_t lo, int64_t hi, int d,
+                  float *acc) {
+  for (int64_t r = lo; r < hi; ++r) {
+    if (r + g_pf < hi) __builtin_prefetch(Vb + (int64_t)ix[r + g_pf] * d, 0, 0);
+    const uint16_t *v = Vb + (int64_t)ix[r] * d;
+    const float wr = wt[r];
+    for (int e = 0; e < d; ++e) acc[e] += wr * g_h2f[v[e]];
+  }
+}
+
+int64_t lower_bound_i32(const int32_t *a, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+void run(const HostArgs &a) {
+  const Isa isa = detect_isa();
+  if (const char *ev = getenv("HC_HOST_PF")) g_pf = atoi(ev);
+  if (const char *ev = getenv("HC_HOST_HINT")) g_hint = atoi(ev);
+  if (isa == kScalar) init_table();
+  const int nt = a.threads > 0 ? a.threads : omp_get_max_threads();
+  const int G = a.G, d = a.d;
+  const int64_t units = a.rows / G;
+  // clamp the range to the tokens actually kept (lists are ascending)
+  int64_t last = -1;
+  for (int64_t row = 0; row < a.rows; ++row)
+    if (a.k[row] > 0 && a.idx[row * a.k_stride + a.k[row] - 1] > last) last = a.idx[row * a.k_stride + a.k[row] - 1];
+  const int64_t t0 = a.tok_begin, t1 = a.tok_end < last + 1 ? a.tok_end : last + 1;
+  const int64_t nch = t1 > t0 ? (t1 - t0 + kHostChunk - 1) / kHostChunk : 0;
+  if (nch == 0) {
+    memset(a.out, 0, sizeof(float) * (size_t)a.rows * d);
+    return;
+  }
+  // chunk partials [units][nch][G][d], reused across calls by the calling thread
+  thread_local std::vector<float> part;
+  const size_t need = (size_t)units * nch * G * d;
+  if (part.size() < need) part.resize(need);
+  float *P = part.data();
+  const int64_t items = units * nch;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
+  for (int64_t it = 0; it < items; ++it) {
+    const int64_t u = it / nch, c = it - u * nch;
+    const int64_t j0 = t0 + c * kHostChunk, j1 = j0 + kHostChunk < t1 ? j0 + kHostChunk : t1;
+    const int64_t b = (u * G) / a.Hq, kv = ((u * G) % a.Hq) / G;
+    const uint16_t *Vb = a.V + b * a.v_b_stride + kv * a.v_kv_stride;
+    float *pp = P + (size_t)it * G * d;
+    memset(pp, 0, sizeof(float) * (size_t)G * d);
+    for (int h = 0; h < G; ++h) {
+      const int64_t row = u * G + h;
+      const int32_t *ix = a.idx + row * a.k_stride;
+      const float *wt = a.w + row * a.k_stride;
+      const int64_t kk = a.k[row];
+      const int64_t lo = lower_bound_i32(ix, kk, j0), hi = lower_bound_i32(ix, kk, j1);
+      if (lo >= hi) continue;
+      float *acc = pp + (size_t)h * d;
+      if (isa == kAvx512 && d % 16 == 0) accum_avx512(Vb, ix, wt, lo, hi, d, acc);
+      else if (isa != kScalar && d % 8 == 0) accum_avx2(Vb, ix, wt, lo, hi, d, acc);
+      else { init_table(); accum_scalar(Vb, ix, wt, lo, hi, d, acc); }
+    }
+  }
+  // out[row] = Σ_c partial[u][c][h] in chunk order
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t row = 0; row < a.rows; ++row) {
+    const int64_t u = row / G, h = row - u * G;
+    float *o = a.out + row * d;
+    for (int e = 0; e < d; ++e) o[e] = 0.0f;
+    for (int64_t c = 0; c < nch; ++c) {
+      const float *pp = P + ((size_t)(u * nch + c) * G + h) * d;
+      for (int e = 0; e < d; ++e) o[e] += pp[e];
+    }
   }
 }
 
@@ -84,19 +219,62 @@ void CUDART_CB host_cb(void *p) {
   if (a->owned_once) delete a;
 }
 
+hc_status check(const int32_t *idx, const float *w, const int64_t *k, const uint16_t *V, float *out,
+                int64_t rows, int32_t Hq, int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end) {
+  if (!idx || !w || !k || !V || !out) return HC_ERR_ARG;
+  if (rows < 0 || Hq <= 0 || G <= 0 || d <= 0 || d > 256 || Hq % G || rows % G) return HC_ERR_SHAPE;
+  if (tok_begin < 0 || tok_end < tok_begin) return HC_ERR_RANGE;
+  return HC_OK;
+}
+
+hc_status enqueue(const HostArgs &proto, hc_stream_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  // a captured host node may run many times: its argument block lives as long as the library
+  HostArgs *a = new HostArgs(proto);
+  a->owned_once = cap != cudaStreamCaptureStatusActive;
+  if (cudaLaunchHostFunc(s, host_cb, a) != cudaSuccess) {
+    delete a;
+    return HC_ERR_CUDA;
+  }
+  return HC_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+hc_status hc_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
+                                     int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
+                                     int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
+                                     int64_t tok_begin, int64_t tok_end, float *out, int32_t threads) {
+  hc_status st = check(idx, w, k, V, out, rows, Hq, G, d, tok_begin, tok_end);
+  if (st) return st;
+  HostArgs a{idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, out, threads,
+             tok_begin, tok_end, false};
+  run(a);
+  return HC_OK;
+}
+
+hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k,
+                                             int64_t rows, int64_t k_stride, const uint16_t *V,
+                                             int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
+                                             int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end,
+                                             float *out, int32_t threads, hc_stream_t stream) {
+  hc_status st = check(idx, w, k, V, out, rows, Hq, G, d, tok_begin, tok_end);
+  if (st) return st;
+  return enqueue(HostArgs{idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, out, threads,
+                          tok_begin, tok_end, false},
+                 stream);
+}
 
 hc_status hc_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
                                int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
                                int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d, float *out,
                                int32_t threads) {
-  if (!idx || !w || !k || !V || !out) return HC_ERR_ARG;
-  if (rows < 0 || Hq <= 0 || G <= 0 || d <= 0 || d > 256 || Hq % G) return HC_ERR_SHAPE;
-  HostArgs a{idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, out, threads, false};
-  run(a);
-  return HC_OK;
+  return hc_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, 0,
+                                    (int64_t)INT32_MAX + 1, out, threads);
 }
 
 hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k,
@@ -104,19 +282,8 @@ hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const
                                        int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
                                        int32_t G, int32_t d, float *out, int32_t threads,
                                        hc_stream_t stream) {
-  if (!idx || !w || !k || !V || !out) return HC_ERR_ARG;
-  if (rows < 0 || Hq <= 0 || G <= 0 || d <= 0 || d > 256 || Hq % G) return HC_ERR_SHAPE;
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cap);
-  // a captured host node may run many times: its argument block lives as long as the library
-  HostArgs *a = new HostArgs{idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d,
-                             out, threads, cap != cudaStreamCaptureStatusActive};
-  if (cudaLaunchHostFunc(s, host_cb, a) != cudaSuccess) {
-    delete a;
-    return HC_ERR_CUDA;
-  }
-  return HC_OK;
+  return hc_enqueue_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G,
+                                            d, 0, (int64_t)INT32_MAX + 1, out, threads, stream);
 }
 
 }  // extern "C"

@@ -139,6 +139,11 @@ struct LayerArgs {
   // [g_off[row], g_off[row] + g_cnt[row]) with local token index = sel_idx - g_base
   const int64_t *g_off, *g_cnt;
   int64_t g_base;
+  // k_gather_union: kept counts per row from this array instead of hs[row].ksel (standalone
+  // hc_gather_values), and the token range [gtok_lo, gtok_hi) the GPU sums (heterogeneous
+  // split: the host owns the rest; decode: [0, n_cand))
+  const int64_t *k_in;
+  int64_t gtok_lo, gtok_hi;
 };
 
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);
@@ -195,6 +200,7 @@ cudaError_t launch_group_select(const LayerArgs &a, int nsplit, cudaStream_t st)
 // Eq. 5 with GQA union de-duplication (hc_gather.cu)
 int gather_union_chunks(int64_t n_cand);
 cudaError_t launch_gather_union(const LayerArgs &a, float *part, uint32_t *done, cudaStream_t s);
+cudaError_t launch_add_partial(float *out, const float *part, int64_t n, cudaStream_t s);
 int gather_rows_chunks(int64_t k_cap);
 cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, uint32_t *done,
                                cudaStream_t s);

@@ -136,3 +136,54 @@ def test_host_weighted_sum_matches_oracle_gather():
         b, hq = divmod(r, Hq)
         ref = oracle.gather(idx[r, :k[r]], w[r, :k[r]].astype(np.float64), V[b, hq // G])
         assert np.allclose(out[r], ref, rtol=2e-3, atol=1e-3)
+
+
+def test_host_weighted_sum_range_split_matches_oracle():
+    """Heterogeneous Eq. 5 (include/hc.h hc_host_weighted_sum_range): the host share over
+    kept tokens in [t0, t1) equals the oracle's Eq. 5 over exactly those kept tokens, and
+    the shares of a split [0, t) + [t, n) add up to the whole sum; independent of the
+    thread count (chunk partials in order)."""
+    import numpy as np
+    import oracle
+    import paper_2507_19823_b200 as hc
+    import ctypes as C
+    rng = np.random.default_rng(5)
+    B, Hkv, G, d, n, k_stride = 2, 2, 4, 128, 20011, 3000
+    Hq = Hkv * G
+    V = rng.standard_normal((B, Hkv, n, d)).astype(np.float16)
+    rows = B * Hq
+    idx = np.zeros((rows, k_stride), np.int32)
+    w = np.zeros((rows, k_stride), np.float32)
+    k = rng.integers(0, k_stride, size=rows).astype(np.int64)
+    k[3] = 0  # a row with nothing kept
+    for r in range(rows):
+        sel = np.sort(rng.choice(n, size=k[r], replace=False))
+        idx[r, :k[r]] = sel
+        ww = rng.random(k[r])
+        w[r, :k[r]] = (ww / max(ww.sum(), 1e-30)).astype(np.float32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+
+    def host(t0, t1, threads):
+        out = np.full((rows, d), np.nan, np.float32)
+        st = hc.lib().hc_host_weighted_sum_range(p(idx), p(w), p(k), rows, k_stride,
+                                                p(V.view(np.uint16)), Hkv * n * d, n * d, Hq, G, d,
+                                                t0, t1, p(out), threads)
+        assert st == hc.HC_OK
+        return out
+
+    for t0, t1 in [(0, n), (0, 4096), (5000, 13333), (13333, n), (n, n), (7, 8)]:
+        out = host(t0, t1, 3)
+        for r in range(rows):
+            b, hq = divmod(r, Hq)
+            s = idx[r, :k[r]]
+            m = (s >= t0) & (s < t1)
+            ref = oracle.gather(s[m], w[r, :k[r]][m].astype(np.float64), V[b, hq // G]) if m.any() \
+                else np.zeros(d)
+            assert np.allclose(out[r], ref, rtol=2e-3, atol=1e-3), (t0, t1, r)
+    t = 9001
+    whole = host(0, n, 1)
+    assert np.allclose(host(0, t, 2) + host(t, n, 5), whole, rtol=1e-5, atol=1e-6)
+    assert np.array_equal(host(0, n, 7), whole)  # thread-count independent
+    st = hc.lib().hc_host_weighted_sum_range(p(idx), p(w), p(k), rows, k_stride, p(V.view(np.uint16)),
+                                            Hkv * n * d, n * d, Hq, G, d, 10, 5, p(whole), 1)
+    assert st == hc.HC_ERR_RANGE

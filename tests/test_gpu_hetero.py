@@ -1,0 +1,95 @@
+"""Heterogeneous Eq. 5 (DESIGN §8b f1, include/hc.h hc_gather_values / hc_host_weighted_sum_range
+/ hc_add_partial; §3.2): GPU pulls the kept rows with index < t_split, host
+threads sum the rest over host DRAM, concurrently; the joined output equals the oracle's Eq. 5
+within the north_star tolerance and the selection is the oracle's bit for bit."""
+import numpy as np
+import pytest
+
+from harness import Case, build_gpu, compare_unit, oracle_unit
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2507_19823_b200 as hc
+    hc.lib()
+    return torch
+
+
+def _run(case, host_frac, graph=False):
+    import torch
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.hetero import HeteroEq5
+    kc, vs, q = build_gpu(case)
+    B, Hq, d, km = case.B, case.Hq, case.d, case.k_max
+    bud = hc.budget(case.tau, km, case.renorm)
+    ws = hc.Workspace(kc.workspace_bytes(bud))
+    het = HeteroEq5(kc, vs, km, host_frac, threads=4)
+    out = torch.full((B, Hq, d), float("nan"), dtype=torch.float32, device="cuda")
+    sel_k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
+    qq = q[0].contiguous()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                het(qq, 0, bud, out, sel_k, ws)
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(2):  # replays re-run the host node and the joins
+            out.fill_(float("nan"))
+            g.replay()
+    else:
+        het(qq, 0, bud, out, sel_k, ws)
+    torch.cuda.synchronize()
+    gpu = dict(out=out.cpu().numpy(), idx=het.idx_d.view(B, Hq, km).cpu().numpy(),
+               w=het.w_d.view(B, Hq, km).cpu().numpy(), k=sel_k.cpu().numpy())
+    for b in range(B):
+        for kv in range(case.Hkv):
+            compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv, check_z=False)
+    return het
+
+
+@pytest.mark.parametrize("host_frac", [0.0, 0.37, 1.0])
+def test_hetero_split_matches_oracle(torch_cuda, host_frac):
+    _run(Case(B=2, Hkv=2, n=12011, k_max=1500, placement=1, seed=81), host_frac)
+
+
+def test_hetero_split_graph_replay(torch_cuda):
+    _run(Case(B=1, Hkv=2, n=20000, k_max=3000, placement=1, seed=82), 0.5, graph=True)
+
+
+def test_hetero_split_window_and_renorm(torch_cuda):
+    """resident window tokens (global indices n_q..) land on the host side of the split."""
+    _run(Case(B=1, Hkv=2, n=9000, res_cap=64, n_res=40, k_max=700, renorm=1, placement=1, seed=83), 0.25)
+
+
+def test_gather_values_range(torch_cuda):
+    """hc_gather_values over [t0, t1) equals the oracle's Eq. 5 over the kept tokens in range."""
+    import torch
+    import oracle
+    import paper_2507_19823_b200 as hc
+    case = Case(B=1, Hkv=2, n=10000, k_max=1200, placement=1, seed=84)
+    kc, vs, q = build_gpu(case)
+    B, Hq, d, km = case.B, case.Hq, case.d, case.k_max
+    bud = hc.budget(case.tau, km, select_only=True)
+    ws = hc.Workspace(kc.workspace_bytes(bud))
+    idx = torch.full((B * Hq, km), -1, dtype=torch.int32, device="cuda")
+    w = torch.zeros((B * Hq, km), dtype=torch.float32, device="cuda")
+    k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
+    hc.decode_attention(q[0].contiguous(), kc, vs, 0, bud, out=torch.empty(1, device="cuda"),
+                        sel_idx=idx, sel_w=w, sel_k=k, ws=ws)
+    for t0, t1 in [(0, 10000), (2047, 2049), (1000, 7777), (5000, 5000), (9990, 20000)]:
+        out = torch.full((B, Hq, d), float("nan"), device="cuda")
+        hc.gather_values(kc, vs, 0, idx, w, k, t0, t1, out, ws)
+        torch.cuda.synchronize()
+        ii, ww, kk, oo = idx.cpu().numpy(), w.cpu().numpy(), k.view(-1).cpu().numpy(), out.view(B * Hq, d).cpu().numpy()
+        for r in range(B * Hq):
+            s = ii[r, :kk[r]]
+            m = (s >= t0) & (s < t1)
+            V = case.values(0, 0, (r % Hq) // case.G)
+            ref = oracle.gather(s[m], ww[r, :kk[r]][m].astype(np.float64), V) if m.any() else np.zeros(d)
+            assert np.all(np.abs(oo[r] - ref) <= 1e-3 + 2e-3 * np.abs(ref)), (t0, t1, r)
