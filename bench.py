@@ -194,9 +194,27 @@ class Workload:
         if cfg.get("host_frac", 0.0) > 0.0:  # heterogeneous Eq. 5 (GPU pull + host threads)
             from paper_2507_19823_b200.hetero import HeteroEq5
             self.hetero = HeteroEq5(self.kc, self.vs, cfg["k_max"], cfg["host_frac"], device=device)
+        # micro-batch pipelining (--pipeline P): P independent chains of B/P sequences on their
+        # own streams, so one chain's GPU selection overlaps another's Eq. 5 (host + link)
+        self.parts = []
+        P = cfg.get("pipeline", 1)
+        if P > 1:
+            from paper_2507_19823_b200.hetero import HeteroEq5
+            if B % P:
+                raise SystemExit(f"--pipeline {P} must divide the batch B={B}")
+            nb = B // P
+            for i in range(P):
+                kv_ = self.kc.batch_view(i * nb, nb)
+                vs_ = self.vs.batch_view(i * nb, nb)
+                het = (HeteroEq5(kv_, vs_, cfg["k_max"], cfg["host_frac"], device=device)
+                       if cfg.get("host_frac", 0.0) > 0.0 else None)
+                self.parts.append(dict(b0=i * nb, b1=(i + 1) * nb, kc=kv_, vs=vs_, het=het,
+                                       stream=torch.cuda.Stream(device=device)))
         self.bud = hc.budget(cfg["tau"], cfg["k_max"], select_only=self.cpu_gather,
                              shared_kv=cfg.get("shared_kv", False))
         self.ws = hc.Workspace(self.kc.workspace_bytes(self.bud), device=device)
+        for part in self.parts:
+            part["ws"] = hc.Workspace(part["kc"].workspace_bytes(self.bud), device=device)
         self.sel_k = torch.zeros((L, B, self.Hq), dtype=torch.int64, device=device)
         if self.cpu_gather:  # (idx, w) of one layer, device + pinned host; host Eq. 5 output
             km = cfg["k_max"]
@@ -222,15 +240,43 @@ class Workload:
 
     def reset_counts(self):
         n_here = self.n_local - (1 if self.is_last else 0)  # the step appends position n-1
-        for l in range(self.cfg["L"]):
-            if self.vo_only:
-                self.kc.set_counts(l, 0, n_here)
-            else:
-                self.kc.set_counts(l, n_here)
+        for kc in [self.kc] + [p["kc"] for p in getattr(self, "parts", [])]:
+            for l in range(self.cfg["L"]):
+                if self.vo_only:
+                    kc.set_counts(l, 0, n_here)
+                else:
+                    kc.set_counts(l, n_here)
+
+    def step_pipelined(self, profile=False):
+        import torch
+
+        import paper_2507_19823_b200 as hc
+        main = torch.cuda.current_stream()
+        for part in self.parts:
+            part["stream"].wait_stream(main)
+        for i, part in enumerate(self.parts):
+            b0, b1 = part["b0"], part["b1"]
+            with torch.cuda.stream(part["stream"]):
+                for l in range(self.cfg["L"]):
+                    if self.is_last:
+                        part["kc"].append(l, self.k_new[l][b0:b1], self.v_new[l][b0:b1], part["vs"])
+                    if profile and i == 0:
+                        hc.profile_scan_events(*self.ev[l])
+                    if part["het"] is not None:
+                        part["het"](self.q[l][b0:b1], l, self.bud, self.out[l][b0:b1],
+                                    self.sel_k[l][b0:b1], part["ws"])
+                    else:
+                        hc.decode_attention(self.q[l][b0:b1], part["kc"], part["vs"], l, self.bud,
+                                            out=self.out[l][b0:b1], sel_k=self.sel_k[l][b0:b1],
+                                            ws=part["ws"])
+        for part in self.parts:
+            main.wait_stream(part["stream"])
 
     def step(self, profile=False):
         import paper_2507_19823_b200 as hc
         from paper_2507_19823_b200 import sharded
+        if self.parts:
+            return self.step_pipelined(profile)
         for l in range(self.cfg["L"]):
             if self.is_last:
                 self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
@@ -503,6 +549,7 @@ def run_virtual(args, cfg, R):
 
 
 # ----------------------------------------------------------------------------- main
+PIPELINE_DEFAULT = 1  # set from measurement
 HOST_FRAC_DEFAULT = 0.6  # measured optimum on the B200 box (DESIGN §8b f1, tools/hetero_sweep.py)
 
 
@@ -520,6 +567,9 @@ def main():
                     help="heterogeneous Eq. 5 for host-resident values: host threads sum the kept "
                          "rows of this share of the token range while the GPU pulls the rest "
                          "(default for host-V configs: %s; 0 = GPU only)" % HOST_FRAC_DEFAULT)
+    ap.add_argument("--pipeline", type=int, default=None,
+                    help="micro-batch pipelining: P chains of B/P sequences on their own streams "
+                         "(default for host-V configs: %d)" % PIPELINE_DEFAULT)
     ap.add_argument("--lut8", action="store_true",
                     help="8-bit query/codebook table variant (R2b, SURVEY f3)")
     ap.add_argument("--code-bits", type=int, default=16, choices=[16, 13],
@@ -547,6 +597,11 @@ def main():
     hf = args.host_frac if args.host_frac is not None else (
         HOST_FRAC_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather else 0.0)
     cfg["host_frac"] = hf
+    pp = args.pipeline if args.pipeline is not None else (
+        PIPELINE_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather and cfg["B"] % PIPELINE_DEFAULT == 0 else 1)
+    cfg["pipeline"] = pp
+    if pp > 1:
+        cfg["workload"] += f"; micro-batch pipeline x{pp} (B/{pp} sequences per chain, own stream)"
     if hf > 0.0:
         if cfg["placement"] != 1 or args.cpu_gather:
             raise SystemExit("--host-frac needs host-resident values (e.g. --config 3) and no --cpu-gather")
@@ -629,9 +684,10 @@ def main():
 
     B, L, H, g, n, d = (cfg[k] for k in ("B", "L", "Hkv", "g", "n", "d"))
     n_here = wl.n_local
-    p_bytes_layer = B * H * n_here * (d if wl.vo_only else g) * 2  # exact K rows in VO-only mode
+    Bs = B // cfg.get("pipeline", 1)  # the profiled scan covers one micro-batch
+    p_bytes_layer = Bs * H * n_here * (d if wl.vo_only else g) * 2  # exact K rows in VO-only mode
     if cfg.get("code_bits", 16) == 13 and not wl.vo_only:
-        p_bytes_layer = B * H * n_here * g * 13 // 8  # packed code strips
+        p_bytes_layer = Bs * H * n_here * g * 13 // 8  # packed code strips
     achieved = p_bytes_layer / (scan_avg_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     traffic = None
@@ -681,7 +737,7 @@ def main():
                      "kernel": ("k_resident (exact-key dense scan, VO-only mode)" if wl.vo_only
                                 else "k_scan (Eq. 3 quantized-key scan)"),
                      "algorithmic_bytes_per_launch": p_bytes_layer,
-                     "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L / ms_per_step,
+                     "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L * cfg.get("pipeline", 1) / ms_per_step,
                      "peak_source": peak_src,
                      "dominant_kernel": ("k_gather_union (zero-copy value gather, bound by the host link: see "
                                          "host_link; profiles/r01_launches_config3_summary.md)"

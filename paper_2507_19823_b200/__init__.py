@@ -348,6 +348,10 @@ class VStore:
         t = torch.empty((B, L, Hkv, n_cap, d), dtype=torch.float16, pin_memory=True)
         return VStore(t, placement, n_cap)
 
+    def batch_view(self, b0: int, nb: int) -> "VStore":
+        """Sequences [b0, b0+nb) of the store (same memory)."""
+        return VStore(self.tensor[b0:b0 + nb], self.placement, self.n_cap, self.host)
+
     def struct(self) -> hc_vstore:
         ptr = self.tensor.data_ptr()
         if self.placement == HC_V_HOST_MAPPED:
@@ -441,6 +445,27 @@ class KCache:
 
     def workspace_bytes(self, bud: hc_budget) -> int:
         return int(lib().hc_decode_workspace_bytes(C.byref(self.s), bud))
+
+    def batch_view(self, b0: int, nb: int) -> "KCache":
+        """The sequences [b0, b0+nb) as a cache of their own (same memory; pointers offset
+        along the batch-major layouts).  Token counts are copied and advance separately, so
+        every view of a batch must see the same appends (e.g. micro-batch pipelining)."""
+        if not (0 <= b0 and nb >= 1 and b0 + nb <= self.B):
+            raise ValueError("batch view out of range")
+        v = object.__new__(KCache)
+        v.__dict__.update(self.__dict__)
+        v.B = nb
+        v.codes = self.codes[b0:b0 + nb]
+        v.res_k = self.res_k[b0:b0 + nb] if self.res_k is not None else None
+        v.res_v = self.res_v[b0:b0 + nb] if self.res_v is not None else None
+        s = hc_kcache()
+        C.memmove(C.addressof(s), C.addressof(self.s), C.sizeof(hc_kcache))
+        s.B = nb
+        s.codes = v.codes.data_ptr()
+        s.res_k = v.res_k.data_ptr() if v.res_k is not None else None
+        s.res_v = v.res_v.data_ptr() if v.res_v is not None else None
+        v.s = s
+        return v
 
 
 class Workspace:

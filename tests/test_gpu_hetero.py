@@ -93,3 +93,36 @@ def test_gather_values_range(torch_cuda):
             V = case.values(0, 0, (r % Hq) // case.G)
             ref = oracle.gather(s[m], ww[r, :kk[r]][m].astype(np.float64), V) if m.any() else np.zeros(d)
             assert np.all(np.abs(oo[r] - ref) <= 1e-3 + 2e-3 * np.abs(ref)), (t0, t1, r)
+
+
+def test_batch_views_pipelined(torch_cuda):
+    """Micro-batch pipelining (bench.py --pipeline): KCache/VStore.batch_view chains of one
+    sequence each, on their own streams, concurrently; results equal the oracle per sequence."""
+    import torch
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.hetero import HeteroEq5
+    case = Case(B=2, Hkv=2, n=15000, k_max=2000, placement=1, seed=85)
+    kc, vs, q = build_gpu(case)
+    B, Hq, d, km = case.B, case.Hq, case.d, case.k_max
+    bud = hc.budget(case.tau, km)
+    out = torch.full((B, Hq, d), float("nan"), device="cuda")
+    sel_k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
+    main = torch.cuda.current_stream()
+    parts = []
+    for b in range(B):
+        kv_, vs_ = kc.batch_view(b, 1), vs.batch_view(b, 1)
+        parts.append((b, HeteroEq5(kv_, vs_, km, 0.5 if b == 0 else 0.0 + 0.3, threads=4),
+                      hc.Workspace(kv_.workspace_bytes(bud)), torch.cuda.Stream()))
+    for b, het, ws, st in parts:
+        st.wait_stream(main)
+        with torch.cuda.stream(st):
+            het(q[0][b:b + 1].contiguous(), 0, bud, out[b:b + 1], sel_k[b:b + 1], ws)
+    for _, _, _, st in parts:
+        main.wait_stream(st)
+    torch.cuda.synchronize()
+    for b, het, _, _ in parts:
+        gpu = dict(out=out[b:b + 1].cpu().numpy(), idx=het.idx_d.view(1, Hq, km).cpu().numpy(),
+                   w=het.w_d.view(1, Hq, km).cpu().numpy(), k=sel_k[b:b + 1].cpu().numpy())
+        for kv in range(case.Hkv):
+            ref = oracle_unit(case, b, 0, kv)
+            compare_unit(case, gpu, ref, 0, kv, check_z=False)

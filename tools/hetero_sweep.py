@@ -1,7 +1,7 @@
 """Sweep the heterogeneous Eq. 5 split on the config-3 workload (128K ctx, B=4, host V):
-steps/s of the captured 32-layer step for each (host_frac, host threads), plus the host-only
-engine in situ.  Usage: python tools/hetero_sweep.py [fracs] [threads]
-e.g. python tools/hetero_sweep.py 0.5,0.6,0.7,0.8 15,16"""
+steps/s of the captured 32-layer step for each (micro-batch pipeline depth, host_frac).
+Usage: python tools/hetero_sweep.py [fracs] [pipelines]
+e.g. python tools/hetero_sweep.py 0.5,0.6,0.7 1,2,4"""
 import os
 import sys
 
@@ -16,21 +16,28 @@ def main():
 
     from paper_2507_19823_b200.hetero import HeteroEq5
     fracs = [float(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0.6,0.7,0.8").split(",")]
-    threads = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "16").split(",")]
-    cfg = dict(bench.CONFIGS[3])
-    cfg.update(lut_bits=16, vo_only=False, cpu_gather=False, shared_kv=False, code_bits=16, host_frac=0.0)
+    pipes = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1").split(",")]
     torch.cuda.set_device(0)
-    wl = bench.Workload(cfg, "cuda", 0, 1)
-    for t in threads:
+    for P in pipes:
+        cfg = dict(bench.CONFIGS[3])
+        cfg.update(lut_bits=16, vo_only=False, cpu_gather=False, shared_kv=False, code_bits=16,
+                   host_frac=0.5, pipeline=P)
+        wl = bench.Workload(cfg, "cuda", 0, 1)
         for f in fracs:
-            wl.hetero = HeteroEq5(wl.kc, wl.vs, cfg["k_max"], f, threads=t) if f > 0 else None
+            if P == 1:
+                wl.hetero = HeteroEq5(wl.kc, wl.vs, cfg["k_max"], f) if f > 0 else None
+            for part in wl.parts:
+                part["het"] = HeteroEq5(part["kc"], part["vs"], cfg["k_max"], f) if f > 0 else None
             wl.reset_counts()
             wl.step()
             torch.cuda.synchronize()
             g, _ = wl.capture(wl.step)
             ms = bench.time_graph(g, 5, 2) / 5
-            print(f"host_frac={f:.2f} threads={t}: {ms:.1f} ms/step = {1000 / ms:.2f} steps/s", flush=True)
+            print(f"pipeline={P} host_frac={f:.2f}: {ms:.1f} ms/step = {1000 / ms:.2f} steps/s", flush=True)
             del g
+        del wl
+        import gc
+        gc.collect()
 
 
 if __name__ == "__main__":
