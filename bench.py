@@ -77,7 +77,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, dev_index: int, period_s: float = 0.005):
+    def __init__(self, dev_index: int, period_s: float = 0.01):
         self.samples, self.reason_bits = [], 0
         self.period = period_s
         self._stop = threading.Event()
@@ -375,11 +375,15 @@ def time_graph(g, K, W, dist=None):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # blocking-sync events: the waiting thread sleeps instead of spinning on a core that the
+    # host share of the heterogeneous Eq. 5 needs
+    e0 = torch.cuda.Event(enable_timing=True, blocking=True)
+    e1 = torch.cuda.Event(enable_timing=True, blocking=True)
     e0.record()
     for _ in range(K):
         g.replay()
     e1.record()
+    e1.synchronize()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if dist is not None:

@@ -32,9 +32,9 @@ class HeteroEq5:
         if not (0.0 <= host_frac <= 1.0):
             raise ValueError("host_frac must be in [0, 1]")
         self.kc, self.vs, self.k_max = kc, vstore, int(k_max)
-        # default: all cores but one (the thread driving the GPU spin-waits on one)
+        # default: all cores (the driving thread should wait on blocking-sync events, not spin)
         self.host_frac = float(host_frac)
-        self.threads = int(threads) if threads > 0 else max(1, (os.cpu_count() or 2) - 1)
+        self.threads = int(threads) if threads > 0 else (os.cpu_count() or 1)
         rows = kc.B * kc.Hq
         self.idx_d = torch.empty((rows, self.k_max), dtype=torch.int32, device=device)
         self.w_d = torch.empty((rows, self.k_max), dtype=torch.float32, device=device)
