@@ -554,6 +554,16 @@ def run_virtual(args, cfg, R):
 
 # ----------------------------------------------------------------------------- main
 PIPELINE_DEFAULT = 1  # set from measurement
+
+# tools/smem_gather_micro.cu on a B200 (profiles/r01_smem_gather_micro.log): one 512-thread CTA
+# per SM doing random lookups into a 64 KiB (8-byte entries) / 32 KiB (4-byte) table slice,
+# nothing else -- the fastest the scan could consume u16 codes (2 B of P per lookup)
+SMEM_CEILING = {
+    8: {"entry_bytes": 8, "code_GBps": 3017.5, "frac_of_hbm": 3017.5 / 6549.4,
+        "wavefronts_per_warp_lookup": 6.15, "source": "profiles/r01_smem_gather_micro.log"},
+    4: {"entry_bytes": 4, "code_GBps": 4778.9, "frac_of_hbm": 4778.9 / 6549.4,
+        "wavefronts_per_warp_lookup": 3.89, "source": "profiles/r01_smem_gather_micro.log"},
+}
 HOST_FRAC_DEFAULT = 0.6  # measured optimum on the B200 box (DESIGN §8b f1, tools/hetero_sweep.py)
 
 
@@ -743,6 +753,9 @@ def main():
                      "algorithmic_bytes_per_launch": p_bytes_layer,
                      "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L * cfg.get("pipeline", 1) / ms_per_step,
                      "peak_source": peak_src,
+                     # the binding on-chip resource: random table lookups in shared
+                     # memory, measured alone by tools/smem_gather_micro.cu on a B200
+                     "smem_gather_ceiling": SMEM_CEILING.get(8 if cfg.get("lut_bits", 16) == 16 else 4),
                      "dominant_kernel": ("k_gather_union (zero-copy value gather, bound by the host link: see "
                                          "host_link; profiles/r01_launches_config3_summary.md)"
                                          if host_link is not None else
