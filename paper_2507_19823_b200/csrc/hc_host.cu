@@ -63,6 +63,12 @@ void init_table() {
 enum Isa { kScalar = 0, kAvx2 = 1, kAvx512 = 2 };
 Isa detect_isa() {
   static int isa = -1;
+  if (const char *ev = getenv("HC_HOST_ISA")) {  // test override: scalar | avx2 | avx512
+    if (!strcmp(ev, "scalar")) return kScalar;
+    if (!strcmp(ev, "avx2") && __builtin_cpu_supports("avx2") && __builtin_cpu_supports("f16c") &&
+        __builtin_cpu_supports("fma"))
+      return kAvx2;
+  }
   if (isa < 0) {
     __builtin_cpu_init();
     if (__builtin_cpu_supports("avx512f") && __builtin_cpu_supports("f16c") && __builtin_cpu_supports("fma"))

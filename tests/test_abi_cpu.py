@@ -138,7 +138,8 @@ def test_host_weighted_sum_matches_oracle_gather():
         assert np.allclose(out[r], ref, rtol=2e-3, atol=1e-3)
 
 
-def test_host_weighted_sum_range_split_matches_oracle():
+@pytest.mark.parametrize("isa", ["", "avx2", "scalar"])
+def test_host_weighted_sum_range_split_matches_oracle(isa, monkeypatch):
     """Heterogeneous Eq. 5 (include/hc.h hc_host_weighted_sum_range): the host share over
     kept tokens in [t0, t1) equals the oracle's Eq. 5 over exactly those kept tokens, and
     the shares of a split [0, t) + [t, n) add up to the whole sum; independent of the
