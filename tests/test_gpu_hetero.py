@@ -126,3 +126,26 @@ def test_batch_views_pipelined(torch_cuda):
         for kv in range(case.Hkv):
             ref = oracle_unit(case, b, 0, kv)
             compare_unit(case, gpu, ref, 0, kv, check_z=False)
+
+
+def test_hetero_config3_full_size_sampled(torch_cuda):
+    """BASELINE config 3 shape (128K ctx, B=4, g=32, k_max=16384, V host-resident) in the
+    launch configuration bench.py times (heterogeneous Eq. 5, host_frac 0.6): one layer,
+    sampled units vs the oracle."""
+    import torch
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.hetero import HeteroEq5
+    case = Case(B=4, L=1, Hkv=8, g=32, n=131072, k_max=16384, placement=1, seed=3)
+    kc, vs, q = build_gpu(case)
+    B, Hq, d, km = case.B, case.Hq, case.d, case.k_max
+    bud = hc.budget(case.tau, km)
+    ws = hc.Workspace(kc.workspace_bytes(bud))
+    het = HeteroEq5(kc, vs, km, 0.6)
+    out = torch.full((B, Hq, d), float("nan"), device="cuda")
+    sel_k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
+    het(q[0].contiguous(), 0, bud, out, sel_k, ws)
+    torch.cuda.synchronize()
+    gpu = dict(out=out.cpu().numpy(), idx=het.idx_d.view(B, Hq, km).cpu().numpy(),
+               w=het.w_d.view(B, Hq, km).cpu().numpy(), k=sel_k.cpu().numpy())
+    for b, kv in [(0, 0), (3, 7)]:
+        compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv, check_z=False)
