@@ -21,7 +21,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     e1.record(); torch.cuda.synchronize()
     print(json.dumps({"stop": os.environ.get("HC_SEL_STOP", "0"), "us_per_layer": e0.elapsed_time(e1) / reps * 1000}))
 else:
-    for st in ["1", "2", "3", "4", "5", "0"]:
+    for st in os.environ.get("PT_STOPS", "1,2,3,4,5,0").split(","):
         env = dict(os.environ, HC_SEL_STOP=st)
         out = subprocess.run([sys.executable, __file__, "child"], env=env, capture_output=True, text=True)
         print(out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-2000:])
