@@ -193,7 +193,10 @@ class Workload:
         self.hetero = None
         if cfg.get("host_frac", 0.0) > 0.0:  # heterogeneous Eq. 5 (GPU pull + host threads)
             from paper_2507_19823_b200.hetero import HeteroEq5
-            self.hetero = HeteroEq5(self.kc, self.vs, cfg["k_max"], cfg["host_frac"], device=device)
+            # replicas (N > 1 processes on one host) split the host cores
+            nthr = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+            self.hetero = HeteroEq5(self.kc, self.vs, cfg["k_max"], cfg["host_frac"], threads=nthr,
+                                    device=device)
         # micro-batch pipelining (--pipeline P): P independent chains of B/P sequences on their
         # own streams, so one chain's GPU selection overlaps another's Eq. 5 (host + link)
         self.parts = []
@@ -608,11 +611,15 @@ def main():
     cfg["cpu_gather"] = bool(args.cpu_gather)
     cfg["shared_kv"] = bool(args.shared_kv)
     cfg["code_bits"] = args.code_bits
+    sharded_run = world_env > 1 and args.config in (4, 5)  # Eq. 5 inside hc_shard_finish
     hf = args.host_frac if args.host_frac is not None else (
-        HOST_FRAC_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather else 0.0)
+        HOST_FRAC_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather and not sharded_run else 0.0)
+    if hf > 0.0 and sharded_run:
+        raise SystemExit("--host-frac is for single-GPU host-V runs (the sharded path gathers in hc_shard_finish)")
     cfg["host_frac"] = hf
     pp = args.pipeline if args.pipeline is not None else (
-        PIPELINE_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather and cfg["B"] % PIPELINE_DEFAULT == 0 else 1)
+        PIPELINE_DEFAULT if cfg["placement"] == 1 and not args.cpu_gather and not sharded_run
+        and cfg["B"] % PIPELINE_DEFAULT == 0 else 1)
     cfg["pipeline"] = pp
     if pp > 1:
         cfg["workload"] += f"; micro-batch pipeline x{pp} (B/{pp} sequences per chain, own stream)"
@@ -652,9 +659,15 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    backend = os.environ.get("HC_BENCH_BACKEND", "nccl")  # gloo: code-path smoke on one GPU
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     if world > 1:
         import torch.distributed as td
-        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            td.init_process_group(backend)
         dist = td
     torch.cuda.set_device(local)
     dev = "cuda"
