@@ -427,6 +427,38 @@ def union_gather_bytes(wl, host_frac: float = 0.0):
     return rows * d * 2.0
 
 
+def measure_host_rows_gbs(wl, reps: int = 3) -> float:
+    """Host DRAM random-row rate: the host Eq. 5 engine alone (all the split's threads) over
+    layer 0's full selection; GB/s of union rows (rows kept by several GQA heads counted once,
+    as the engine reads them once)."""
+    import time
+
+    import torch
+
+    import paper_2507_19823_b200 as hc
+    het, cfg = wl.hetero, wl.cfg
+    G = cfg["G"]
+    bud = hc.budget(cfg["tau"], cfg["k_max"], select_only=True)
+    sel_k = torch.zeros((cfg["B"], wl.Hq), dtype=torch.int64, device="cuda")
+    hc.decode_attention(wl.q[0], wl.kc, wl.vs, 0, bud, out=wl.out[0], sel_idx=het.idx_d, sel_w=het.w_d,
+                        sel_k=sel_k, ws=wl.ws)
+    torch.cuda.synchronize()
+    het.idx_h.copy_(het.idx_d)
+    het.w_h.copy_(het.w_d)
+    het.k_h.copy_(sel_k.view(-1))
+    rows = 0
+    for u in range(het.idx_h.shape[0] // G):
+        sets = [het.idx_h[u * G + h, : int(het.k_h[u * G + h])] for h in range(G)]
+        rows += int(torch.unique(torch.cat(sets)).numel())
+    n = wl.kc.n_q(0)
+    ts = []
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        hc.host_weighted_sum_range(het.idx_h, het.w_h, het.k_h, wl.vs, 0, G, 0, n, het.part_h, het.threads)
+        ts.append(time.perf_counter() - t0)
+    return rows * cfg["d"] * 2 / min(ts[1:]) / 1e9
+
+
 def hc_lib_check():
     import paper_2507_19823_b200 as hc
     hc.lib()  # no CPU fallback: fail loudly if the CUDA library is missing
@@ -733,9 +765,17 @@ def main():
         if not wl.cpu_gather and world == 1:
             if wl.hetero is not None:  # the host's share of the rows stays in host DRAM
                 v_bytes, h_bytes = union_gather_bytes(wl, cfg["host_frac"])
+                pk_mem = measure_host_rows_gbs(wl)
+                both = (h_bytes + v_bytes) / (ms_per_step * 1e-3) / 1e9
                 host_dram = {"bytes_per_step": h_bytes, "rows": "union of the GQA heads' kept rows, "
                              "index < t_split", "achieved_gbs_lower_bound": h_bytes / (ms_per_step * 1e-3) / 1e9,
-                             "host_frac": cfg["host_frac"], "threads": os.cpu_count()}
+                             "host_frac": cfg["host_frac"], "threads": wl.hetero.threads,
+                             # both consumers (host threads + the GPU's zero-copy pulls) read the
+                             # same host DRAM: their sum against its measured random-row rate
+                             "all_row_bytes_gbs": both, "peak_gbs": pk_mem,
+                             "peak_source": "host engine alone, all cores, one layer's full selection "
+                                            "(union rows / time), measured live",
+                             "frac": both / pk_mem if pk_mem else None}
             else:
                 v_bytes = union_gather_bytes(wl)  # rows actually read: union over the GQA heads
         pk = measure_h2d_gbs()
