@@ -292,6 +292,36 @@ hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w,
                                              int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end,
                                              float *out, int32_t threads, hc_stream_t stream);
 
+/* Doorbell host worker: the host share of the split without graph host nodes (a
+ * cudaLaunchHostFunc node costs ~250 us round trip; this path ~10 us).  A persistent host
+ * thread (with its own OpenMP team of `threads`) polls per-job mailboxes in pinned mapped
+ * memory.  A job = one host share of Eq. 5 for `rows` = B*Hq query heads over a host value
+ * store V (HOST pointer of layer 0, strides in elements as hc_host_weighted_sum) into out
+ * [rows][d] fp32 (HOST memory, e.g. pinned); its staging for the selection is owned by the
+ * worker.  On `stream` (kernels only, graph-capturable):
+ *   hc_host_worker_submit: copies each row's kept entries with index < t_split from the
+ *     DEVICE selection (sel_idx/sel_w [rows][k_stride] ascending, sel_k [rows]) into the
+ *     job's staging, then rings the job's doorbell with {t_split, v_off}; the worker then
+ *     computes out = Σ_{kept j < t_split} w_j V[v_off + ...]_j (v_off = element offset of
+ *     the layer in V) exactly as hc_host_weighted_sum_range(tok 0..t_split);
+ *   hc_host_worker_wait: a one-thread kernel that returns once the job's last submission is
+ *     done (so later work on the stream sees out), or after timeout_s seconds, when the
+ *     job is marked failed: hc_host_worker_status then returns HC_ERR_CUDA.
+ * Submissions of one job must not overlap (wait before the next submit).  add_job returns
+ * HC_ERR_CAPACITY beyond max_jobs.  destroy stops the thread (no wait may be pending). */
+typedef struct hc_host_worker hc_host_worker;
+hc_status hc_host_worker_create(int32_t threads, int32_t max_jobs, double timeout_s, hc_host_worker **out);
+hc_status hc_host_worker_destroy(hc_host_worker *w);
+hc_status hc_host_worker_add_job(hc_host_worker *w, int64_t rows, int64_t k_stride, const uint16_t *V,
+                                 int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
+                                 float *out, int32_t *job);
+hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *sel_idx, const float *sel_w,
+                                const int64_t *sel_k, int64_t t_split, int64_t v_off, hc_stream_t stream);
+hc_status hc_host_worker_wait(hc_host_worker *w, int32_t job, hc_stream_t stream);
+hc_status hc_host_worker_status(hc_host_worker *w);
+/* Maintenance / test hook: paused != 0 stops serving doorbells (pending waits then time out). */
+hc_status hc_host_worker_pause(hc_host_worker *w, int32_t paused);
+
 /* GPU Eq. 5 over a GIVEN selection, restricted to kept tokens tok_begin <= j < tok_end:
  *   out[b][h] = Σ_{r<sel_k[row], tok_begin<=sel_idx[row][r]<tok_end} sel_w[row][r] · V_j
  * with row = b*Hq + h.  sel_idx/sel_w [B*Hq][k_stride] (ascending indices per row) and

@@ -28,7 +28,9 @@ EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_ev
            "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish", "hc_kmeans_workspace_bytes",
            "hc_kmeans_step", "hc_pack_codes13", "hc_blockwise_attention", "hc_prefill_append",
            "hc_host_weighted_sum_range", "hc_enqueue_host_weighted_sum_range", "hc_gather_values",
-           "hc_add_partial", "hc_host_register", "hc_host_unregister"]
+           "hc_add_partial", "hc_host_register", "hc_host_unregister", "hc_host_worker_create",
+           "hc_host_worker_destroy", "hc_host_worker_add_job", "hc_host_worker_submit",
+           "hc_host_worker_wait", "hc_host_worker_status", "hc_host_worker_pause"]
 
 
 class HcError(RuntimeError):
@@ -116,6 +118,17 @@ def lib():
         L.hc_host_register.restype = i32
         L.hc_host_unregister.argtypes = [p]
         L.hc_host_unregister.restype = i32
+        L.hc_host_worker_create.argtypes = [i32, i32, C.c_double, C.POINTER(C.c_void_p)]
+        L.hc_host_worker_destroy.argtypes = [p]
+        L.hc_host_worker_add_job.argtypes = [p, i64, i64, p, i64, i64, i32, i32, i32, p, C.POINTER(i32)]
+        L.hc_host_worker_submit.argtypes = [p, i32, p, p, p, i64, i64, p]
+        L.hc_host_worker_wait.argtypes = [p, i32, p]
+        L.hc_host_worker_status.argtypes = [p]
+        L.hc_host_worker_pause.argtypes = [p, i32]
+        for f in ("hc_host_worker_create", "hc_host_worker_destroy", "hc_host_worker_add_job",
+                  "hc_host_worker_submit", "hc_host_worker_wait", "hc_host_worker_status",
+                  "hc_host_worker_pause"):
+            getattr(L, f).restype = i32
         L.hc_blockwise_attention.argtypes = [p, p, p, i64, i32, i32, i32, i64, p, p]
         L.hc_blockwise_attention.restype = i32
         L.hc_prefill_append.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, i64, p]
@@ -551,3 +564,45 @@ def host_weighted_sum_range(idx, w, k, vstore: VStore, layer: int, G: int, tok_b
     else:
         _check(lib().hc_enqueue_host_weighted_sum_range(*args, _stream(stream)))
     return out
+
+
+class HostWorker:
+    """hc_host_worker_*: persistent host thread running host shares of Eq. 5 on doorbells
+    rung by GPU kernels (no graph host nodes).  See include/hc.h."""
+
+    def __init__(self, threads: int = 0, max_jobs: int = 64, timeout_s: float = 30.0):
+        h = C.c_void_p()
+        _check(lib().hc_host_worker_create(int(threads), int(max_jobs), float(timeout_s), C.byref(h)))
+        self.h = h
+
+    def add_job(self, rows: int, k_stride: int, vstore: "VStore", G: int, out) -> int:
+        B, L, Hkv, n_cap, d = vstore.tensor.shape
+        j = C.c_int32()
+        _check(lib().hc_host_worker_add_job(self.h, rows, k_stride, C.c_void_p(vstore.tensor.data_ptr()),
+                                            L * Hkv * n_cap * d, n_cap * d, Hkv * G, G, d,
+                                            _ptr(out), C.byref(j)))
+        return int(j.value)
+
+    def submit(self, job: int, sel_idx, sel_w, sel_k, t_split: int, v_off: int, stream=None):
+        _check(lib().hc_host_worker_submit(self.h, job, _ptr(sel_idx), _ptr(sel_w), _ptr(sel_k),
+                                           int(t_split), int(v_off), _stream(stream)))
+
+    def wait(self, job: int, stream=None):
+        _check(lib().hc_host_worker_wait(self.h, job, _stream(stream)))
+
+    def status(self) -> int:
+        return int(lib().hc_host_worker_status(self.h))
+
+    def pause(self, paused: bool = True):
+        _check(lib().hc_host_worker_pause(self.h, int(bool(paused))))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().hc_host_worker_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -20,9 +20,12 @@
 #include <string.h>
 
 #include <atomic>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "../../include/hc.h"
+#include "hc_internal.h"
 
 namespace {
 
@@ -247,6 +250,146 @@ hc_status enqueue(const HostArgs &proto, hc_stream_t stream) {
   return HC_OK;
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Doorbell host worker: the heterogeneous split without graph host nodes (a host node costs
+// ~250 us round trip on the B200 box, tools/hostnode_latency.py).  A persistent host thread
+// polls per-job mailboxes in pinned mapped memory:
+//   GPU  k_submit: every row copies its kept entries with index < t_split (binary search in
+//        the ascending list) into the job's host staging, writes k_host[row]; the last CTA
+//        (device completion counter, system-scope fences) writes the descriptor
+//        {t_split, V offset} and bumps req[job];
+//   host worker: sees req != seen, runs the engine (OpenMP, its own team), writes out_host,
+//        then done[job] = req (release);
+//   GPU  k_wait: one thread spins (globaltimer-bounded, __nanosleep) until done == req, so
+//        the consumer kernels (hc_add_partial) see out_host.
+// Everything the GPU does is kernels: graph-capturable; replays re-ring the same mailbox.
+struct Mailbox {      // pinned, mapped; one per job
+  volatile uint32_t req, done;
+  volatile int64_t t_split, v_off;
+  volatile uint32_t err;
+};
+
+struct Job {
+  int64_t rows, k_stride;
+  const uint16_t *V;   // host pointer of the store's layer 0 (offset per submit)
+  int64_t v_b_stride, v_kv_stride;
+  int32_t Hq, G, d;
+  float *out;          // host
+  int32_t *idx_h;      // staging (pinned mapped) [rows][k_stride]
+  float *w_h;
+  int64_t *k_h;        // [rows]
+  int32_t *idx_d;      // device aliases of the staging
+  float *w_d;
+  int64_t *k_d;
+  Mailbox *mb_h, *mb_d;
+  uint32_t *ctr;       // device completion counter of k_submit
+  uint32_t seen;
+};
+
+__global__ void k_submit(const int32_t *sel_idx, const float *sel_w, const int64_t *sel_k, int64_t k_stride,
+                         int64_t t_split, int64_t v_off, int32_t *idx_h, float *w_h, int64_t *k_h,
+                         Mailbox *mb, uint32_t *ctr) {
+  const int row = blockIdx.x;
+  __shared__ int64_t s_p;
+  if (threadIdx.x == 0) {
+    const int32_t *li = sel_idx + (int64_t)row * k_stride;
+    int64_t lo = 0, hi = sel_k[row];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)li[mid] < t_split) lo = mid + 1; else hi = mid;
+    }
+    s_p = lo;
+    k_h[row] = lo;
+  }
+  __syncthreads();
+  const int64_t p = s_p;
+  const int32_t *si = sel_idx + (int64_t)row * k_stride;
+  const float *sw = sel_w + (int64_t)row * k_stride;
+  int32_t *di = idx_h + (int64_t)row * k_stride;
+  float *dw = w_h + (int64_t)row * k_stride;
+  const int64_t p4 = p & ~(int64_t)3;  // rows are 16-B aligned when k_stride % 4 == 0
+  if ((k_stride & 3) == 0) {
+    for (int64_t e = (int64_t)threadIdx.x * 4; e < p4; e += (int64_t)blockDim.x * 4) {
+      *reinterpret_cast<int4 *>(di + e) = *reinterpret_cast<const int4 *>(si + e);
+      *reinterpret_cast<float4 *>(dw + e) = *reinterpret_cast<const float4 *>(sw + e);
+    }
+    for (int64_t e = p4 + threadIdx.x; e < p; e += blockDim.x) { di[e] = si[e]; dw[e] = sw[e]; }
+  } else {
+    for (int64_t e = threadIdx.x; e < p; e += blockDim.x) { di[e] = si[e]; dw[e] = sw[e]; }
+  }
+  __threadfence_system();  // this thread's staging writes before the completion count
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(ctr, 1u);
+    if (prev == gridDim.x - 1) {  // last row: every row's writes are fenced
+      *ctr = 0u;
+      __threadfence_system();
+      mb->t_split = t_split;
+      mb->v_off = v_off;
+      __threadfence_system();
+      mb->req = mb->req + 1u;
+      __threadfence_system();
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_wait(Mailbox *mb, uint64_t timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const uint32_t want = mb->req;
+  const uint64_t t0 = gtimer();
+  while (mb->done != want) {
+    __nanosleep(1000);
+    if (gtimer() - t0 > timeout_ns) { mb->err = 1u; break; }
+  }
+  __threadfence_system();
+}
+
+}  // namespace
+
+struct hc_host_worker {
+  std::vector<Job> jobs;
+  std::atomic<int> njobs{0};
+  std::atomic<bool> stop{false};
+  std::atomic<bool> paused{false};
+  std::thread th;
+  int threads;
+  uint64_t timeout_ns;
+  int max_jobs;
+};
+
+namespace {
+
+void worker_loop(hc_host_worker *w) {
+  int idle = 0;
+  while (!w->stop.load(std::memory_order_acquire)) {
+    bool did = false;
+    const int nj = w->paused.load(std::memory_order_acquire) ? 0 : w->njobs.load(std::memory_order_acquire);
+    for (int j = 0; j < nj; ++j) {
+      Job &jb = w->jobs[j];
+      const uint32_t r = jb.mb_h->req;
+      if (r == jb.seen) continue;
+      std::atomic_thread_fence(std::memory_order_acquire);
+      HostArgs a{jb.idx_h, jb.w_h, jb.k_h, jb.rows, jb.k_stride, jb.V + jb.mb_h->v_off, jb.v_b_stride,
+                 jb.v_kv_stride, jb.Hq, jb.G, jb.d, jb.out, w->threads, 0, jb.mb_h->t_split, false};
+      run(a);
+      jb.seen = r;
+      std::atomic_thread_fence(std::memory_order_release);
+      jb.mb_h->done = r;
+      did = true;
+    }
+    if (did) { idle = 0; continue; }
+    if (++idle < 200000) _mm_pause();
+    else std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -290,6 +433,99 @@ hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const
                                        hc_stream_t stream) {
   return hc_enqueue_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G,
                                             d, 0, (int64_t)INT32_MAX + 1, out, threads, stream);
+}
+
+hc_status hc_host_worker_create(int32_t threads, int32_t max_jobs, double timeout_s, hc_host_worker **out) {
+  if (!out || max_jobs < 1 || timeout_s <= 0) return HC_ERR_ARG;
+  hc_host_worker *w = new hc_host_worker();
+  w->threads = threads > 0 ? threads : omp_get_max_threads();
+  w->timeout_ns = (uint64_t)(timeout_s * 1e9);
+  w->max_jobs = max_jobs;
+  w->jobs.resize(max_jobs);  // fixed storage: the worker reads entries while jobs are added
+  w->th = std::thread(worker_loop, w);
+  *out = w;
+  return HC_OK;
+}
+
+hc_status hc_host_worker_destroy(hc_host_worker *w) {
+  if (!w) return HC_ERR_ARG;
+  w->stop.store(true, std::memory_order_release);
+  if (w->th.joinable()) w->th.join();
+  for (int j = 0; j < w->njobs.load(); ++j) {
+    Job &jb = w->jobs[j];
+    cudaFreeHost(jb.idx_h);
+    cudaFreeHost(jb.w_h);
+    cudaFreeHost(jb.k_h);
+    cudaFreeHost((void *)jb.mb_h);
+    cudaFree(jb.ctr);
+  }
+  delete w;
+  return HC_OK;
+}
+
+hc_status hc_host_worker_add_job(hc_host_worker *w, int64_t rows, int64_t k_stride, const uint16_t *V,
+                                 int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
+                                 float *out, int32_t *job) {
+  if (!w || !V || !out || !job) return HC_ERR_ARG;
+  if (rows <= 0 || k_stride < 1 || Hq <= 0 || G <= 0 || d <= 0 || d > 256 || Hq % G || rows % G)
+    return HC_ERR_SHAPE;
+  const int j = w->njobs.load();
+  if (j >= w->max_jobs) return HC_ERR_CAPACITY;
+  Job jb{};
+  jb.rows = rows; jb.k_stride = k_stride; jb.V = V; jb.v_b_stride = v_b_stride; jb.v_kv_stride = v_kv_stride;
+  jb.Hq = Hq; jb.G = G; jb.d = d; jb.out = out;
+  const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
+  bool ok = cudaHostAlloc((void **)&jb.idx_h, (size_t)rows * k_stride * 4, fl) == cudaSuccess &&
+            cudaHostAlloc((void **)&jb.w_h, (size_t)rows * k_stride * 4, fl) == cudaSuccess &&
+            cudaHostAlloc((void **)&jb.k_h, (size_t)rows * 8, fl) == cudaSuccess &&
+            cudaHostAlloc((void **)&jb.mb_h, sizeof(Mailbox), fl) == cudaSuccess &&
+            cudaMalloc((void **)&jb.ctr, 4) == cudaSuccess && cudaMemset(jb.ctr, 0, 4) == cudaSuccess;
+  if (ok) {
+    memset((void *)jb.mb_h, 0, sizeof(Mailbox));
+    ok = cudaHostGetDevicePointer((void **)&jb.idx_d, jb.idx_h, 0) == cudaSuccess &&
+         cudaHostGetDevicePointer((void **)&jb.w_d, jb.w_h, 0) == cudaSuccess &&
+         cudaHostGetDevicePointer((void **)&jb.k_d, jb.k_h, 0) == cudaSuccess &&
+         cudaHostGetDevicePointer((void **)&jb.mb_d, (void *)jb.mb_h, 0) == cudaSuccess;
+  }
+  if (!ok) return HC_ERR_CUDA;
+  jb.seen = 0;
+  w->jobs[j] = jb;
+  w->njobs.store(j + 1, std::memory_order_release);
+  *job = j;
+  return HC_OK;
+}
+
+hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *sel_idx, const float *sel_w,
+                                const int64_t *sel_k, int64_t t_split, int64_t v_off, hc_stream_t stream) {
+  if (!w || !sel_idx || !sel_w || !sel_k) return HC_ERR_ARG;
+  if (job < 0 || job >= w->njobs.load()) return HC_ERR_RANGE;
+  if (t_split < 0 || v_off < 0) return HC_ERR_RANGE;
+  Job &jb = w->jobs[job];
+  k_submit<<<(unsigned)jb.rows, 256, 0, (cudaStream_t)stream>>>(sel_idx, sel_w, sel_k, jb.k_stride, t_split, v_off,
+                                                               jb.idx_d, jb.w_d, jb.k_d, jb.mb_d, jb.ctr);
+  hc::note_launch();
+  return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+hc_status hc_host_worker_wait(hc_host_worker *w, int32_t job, hc_stream_t stream) {
+  if (!w) return HC_ERR_ARG;
+  if (job < 0 || job >= w->njobs.load()) return HC_ERR_RANGE;
+  k_wait<<<1, 32, 0, (cudaStream_t)stream>>>(w->jobs[job].mb_d, w->timeout_ns);
+  hc::note_launch();
+  return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
+}
+
+hc_status hc_host_worker_pause(hc_host_worker *w, int32_t paused) {
+  if (!w) return HC_ERR_ARG;
+  w->paused.store(paused != 0, std::memory_order_release);
+  return HC_OK;
+}
+
+hc_status hc_host_worker_status(hc_host_worker *w) {
+  if (!w) return HC_ERR_ARG;
+  for (int j = 0; j < w->njobs.load(); ++j)
+    if (w->jobs[j].mb_h->err) return HC_ERR_CUDA;
+  return HC_OK;
 }
 
 }  // extern "C"

@@ -25,7 +25,7 @@ import paper_2507_19823_b200 as hc
 
 class HeteroEq5:
     def __init__(self, kc: "hc.KCache", vstore: "hc.VStore", k_max: int, host_frac: float,
-                 threads: int = 0, device="cuda"):
+                 threads: int = 0, device="cuda", mode: str = "doorbell"):
         import torch
         if vstore.placement != hc.HC_V_HOST_MAPPED:
             raise ValueError("the heterogeneous split needs host-resident values (HC_V_HOST_MAPPED)")
@@ -43,6 +43,15 @@ class HeteroEq5:
         self.k_h = torch.empty((rows,), dtype=torch.int64).pin_memory()
         self.part_h = torch.zeros((rows, kc.d), dtype=torch.float32).pin_memory()
         self.side = torch.cuda.Stream(device=device)
+        # "doorbell": a persistent host worker polls a mailbox rung by a GPU kernel (the
+        # selection is copied by that kernel, only the host's share); "hostnode": D2H copies
+        # + a graph host node (cudaLaunchHostFunc, ~250 us round trip per layer)
+        if mode not in ("doorbell", "hostnode"):
+            raise ValueError("mode must be doorbell or hostnode")
+        self.mode = mode
+        if mode == "doorbell":
+            self.worker = hc.HostWorker(threads=self.threads)
+            self.job = self.worker.add_job(rows, self.k_max, vstore, kc.G, self.part_h)
         self.ev_sel = torch.cuda.Event()
         self.ev_host = torch.cuda.Event()
 
@@ -64,11 +73,17 @@ class HeteroEq5:
             self.ev_sel.record(main)
             self.side.wait_event(self.ev_sel)
             with torch.cuda.stream(self.side):
-                self.idx_h.copy_(self.idx_d, non_blocking=True)
-                self.w_h.copy_(self.w_d, non_blocking=True)
-                self.k_h.copy_(sel_k.view(-1), non_blocking=True)
-                hc.host_weighted_sum_range(self.idx_h, self.w_h, self.k_h, self.vs, layer, self.kc.G,
-                                           0, t_split, self.part_h, self.threads, stream=self.side)
+                if self.mode == "doorbell":
+                    B_, L_, Hkv_, ncap_, d_ = self.vs.tensor.shape
+                    self.worker.submit(self.job, self.idx_d, self.w_d, sel_k, t_split,
+                                       layer * Hkv_ * ncap_ * d_, stream=self.side)
+                    self.worker.wait(self.job, stream=self.side)
+                else:
+                    self.idx_h.copy_(self.idx_d, non_blocking=True)
+                    self.w_h.copy_(self.w_d, non_blocking=True)
+                    self.k_h.copy_(sel_k.view(-1), non_blocking=True)
+                    hc.host_weighted_sum_range(self.idx_h, self.w_h, self.k_h, self.vs, layer, self.kc.G,
+                                               0, t_split, self.part_h, self.threads, stream=self.side)
                 self.ev_host.record(self.side)
         hc.gather_values(self.kc, self.vs, layer, self.idx_d, self.w_d, sel_k, t_split, n_cand, out, ws)
         if host:

@@ -19,7 +19,7 @@ def torch_cuda():
     return torch
 
 
-def _run(case, host_frac, graph=False):
+def _run(case, host_frac, graph=False, mode="doorbell"):
     import torch
     import paper_2507_19823_b200 as hc
     from paper_2507_19823_b200.hetero import HeteroEq5
@@ -27,7 +27,7 @@ def _run(case, host_frac, graph=False):
     B, Hq, d, km = case.B, case.Hq, case.d, case.k_max
     bud = hc.budget(case.tau, km, case.renorm)
     ws = hc.Workspace(kc.workspace_bytes(bud))
-    het = HeteroEq5(kc, vs, km, host_frac, threads=4)
+    het = HeteroEq5(kc, vs, km, host_frac, threads=4, mode=mode)
     out = torch.full((B, Hq, d), float("nan"), dtype=torch.float32, device="cuda")
     sel_k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
     qq = q[0].contiguous()
@@ -53,13 +53,15 @@ def _run(case, host_frac, graph=False):
     return het
 
 
+@pytest.mark.parametrize("mode", ["doorbell", "hostnode"])
 @pytest.mark.parametrize("host_frac", [0.0, 0.37, 1.0])
-def test_hetero_split_matches_oracle(torch_cuda, host_frac):
-    _run(Case(B=2, Hkv=2, n=12011, k_max=1500, placement=1, seed=81), host_frac)
+def test_hetero_split_matches_oracle(torch_cuda, host_frac, mode):
+    _run(Case(B=2, Hkv=2, n=12011, k_max=1500, placement=1, seed=81), host_frac, mode=mode)
 
 
-def test_hetero_split_graph_replay(torch_cuda):
-    _run(Case(B=1, Hkv=2, n=20000, k_max=3000, placement=1, seed=82), 0.5, graph=True)
+@pytest.mark.parametrize("mode", ["doorbell", "hostnode"])
+def test_hetero_split_graph_replay(torch_cuda, mode):
+    _run(Case(B=1, Hkv=2, n=20000, k_max=3000, placement=1, seed=82), 0.5, graph=True, mode=mode)
 
 
 def test_hetero_split_window_and_renorm(torch_cuda):
@@ -149,3 +151,31 @@ def test_hetero_config3_full_size_sampled(torch_cuda):
                w=het.w_d.view(B, Hq, km).cpu().numpy(), k=sel_k.cpu().numpy())
     for b, kv in [(0, 0), (3, 7)]:
         compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv, check_z=False)
+
+
+def test_host_worker_timeout_reports(torch_cuda):
+    """hc_host_worker_wait never hangs: with the worker paused the wait kernel gives up after
+    timeout_s and hc_host_worker_status reports HC_ERR_CUDA; a served job reports HC_OK."""
+    import time
+    import torch
+    import paper_2507_19823_b200 as hc
+    vs = hc.VStore.allocate(1, 1, 1, 64, 128, placement=hc.HC_V_HOST_MAPPED)
+    out = torch.zeros((4, 128), dtype=torch.float32).pin_memory()
+    idx = torch.zeros((4, 16), dtype=torch.int32, device="cuda")
+    wt = torch.zeros((4, 16), dtype=torch.float32, device="cuda")
+    k = torch.zeros((4,), dtype=torch.int64, device="cuda")
+    w = hc.HostWorker(threads=1, max_jobs=2, timeout_s=0.2)
+    j = w.add_job(4, 16, vs, 4, out)
+    w.submit(j, idx, wt, k, 64, 0)
+    w.wait(j)
+    torch.cuda.synchronize()
+    assert w.status() == hc.HC_OK
+    w.pause(True)
+    t0 = time.time()
+    w.submit(j, idx, wt, k, 64, 0)
+    w.wait(j)
+    torch.cuda.synchronize()
+    assert time.time() - t0 < 5.0
+    assert w.status() == hc.HC_ERR_CUDA
+    w.pause(False)
+    w.close()
