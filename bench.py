@@ -809,7 +809,11 @@ def main():
                      # the binding on-chip resource: random table lookups in shared
                      # memory, measured alone by tools/smem_gather_micro.cu on a B200
                      "smem_gather_ceiling": SMEM_CEILING.get(8 if cfg.get("lut_bits", 16) == 16 else 4),
-                     "dominant_kernel": ("k_gather_union (zero-copy value gather, bound by the host link: see "
+                     "dominant_kernel": (("Eq. 5 over host-resident values: host worker threads + "
+                                          "k_gather_union, bound by host DRAM's random-row rate (see host_dram; "
+                                          "profiles/r01_launches_config3_hetero_summary.md)")
+                                         if host_dram is not None else
+                                         "k_gather_union (zero-copy value gather, bound by the host link: see "
                                          "host_link; profiles/r01_launches_config3_summary.md)"
                                          if host_link is not None else
                                          "scan / select / gather share the step (see DESIGN.md §5)")},
