@@ -497,10 +497,12 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
     if (e0 != cudaSuccess) return cuda_check(e0, "codebook absmax");
     a.cb_absmax = cba;
   }
-  {  // centroid splits: ~2 waves of 256-thread CTAs over units x groups
+  {  // centroid splits only while units x groups leave SMs idle: every split repeats the
+     // CTA's scale-bound prologue (measured: 1 split per (unit, group) is fastest once the
+     // grid covers the SMs -- config 2 94.8 vs 98.4 us per layer with 4)
     const int64_t base = B * H * g;
     int ts = 1;
-    while (ts < kMaxTSplit && base * ts * 2 <= 2 * 148 * 8 && Lw.cpow2 / (ts * 2) >= 256) ts *= 2;
+    while (ts < kMaxTSplit && base * ts < 148 && Lw.cpow2 / (ts * 2) >= 256) ts *= 2;
     static int ts_env = -1;  // dev override (HC_TSPLIT)
     if (ts_env < 0) { const char *ev = getenv("HC_TSPLIT"); ts_env = ev ? atoi(ev) : 0; }
     if (ts_env > 0 && Lw.cpow2 / ts_env >= 256) ts = ts_env;
