@@ -112,7 +112,8 @@ struct Layout {
   int64_t z_stride;
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
-      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, total;
+      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, total;
+  int skctr_n;
   int nch_max;  // sharded compaction chunks
 };
 
@@ -147,6 +148,10 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
     L.o_rpart = o; o += align256((size_t)rows * nchr * 128 * 4);
     L.o_rdone = o; o += align256((size_t)rows * 4);
     L.o_grange = o; o += align256((size_t)rows * 16);  // sharded finish: list slice per row
+    // stream-K scan: 2 partial tiles (8192 tokens x G int32) per CTA, one counter per tile
+    L.o_skpart = o; o += align256((size_t)kSkMaxCtas * 2 * 8192 * G * 4);
+    L.skctr_n = (int)(units * ((ncand_max + 4095) / 4096));
+    L.o_skctr = o; o += align256((size_t)L.skctr_n * 4);
     if (shared) {  // R8 shared selection state, 4-level histograms, chunk counts
       L.o_grp = o; o += align256((size_t)units * sizeof(GroupState));
       L.o_ghist = o; o += align256((size_t)units * 4 * kNB * 16);
@@ -526,6 +531,9 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
     if ((tpt_env == 8 || tpt_env == 16) && !a.lut8) a.scan_tpt = tpt_env;
   }
   a.zpart = (float *)(w8 + Lw.o_zpart);
+  a.skpart = (int *)(w8 + Lw.o_skpart);
+  a.skctr = (uint32_t *)(w8 + Lw.o_skctr);
+  a.skctr_n = Lw.skctr_n;
   if (budget.shared_kv) {
     a.grp = (GroupState *)(w8 + Lw.o_grp);
     a.grp_hist = (unsigned long long *)(w8 + Lw.o_ghist);

@@ -8,6 +8,8 @@
 
 namespace hc {
 
+constexpr int kSkMaxCtas = 160;  // stream-K scan: max persistent CTAs (partial slots in the workspace)
+
 // number of kernels this library has enqueued (or captured into a graph)
 void note_launch(int n = 1);
 
@@ -144,6 +146,11 @@ struct LayerArgs {
   // split: the host owns the rest; decode: [0, n_cand))
   const int64_t *k_in;
   int64_t gtok_lo, gtok_hi;
+  // stream-K scan (k_scan_sk): per-CTA partial slots [sms][2][tile][G] int32 and per-tile
+  // arrival counters (zeroed by k_table)
+  int *skpart;
+  uint32_t *skctr;
+  int skctr_n;
 };
 
 cudaError_t launch_init(const LayerArgs &a, cudaStream_t s);

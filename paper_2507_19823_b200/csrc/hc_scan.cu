@@ -525,6 +525,215 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
 }
 
 // ---------------------------------------------------------------------------------------
+// Stream-K variant of k_scan_pipe: the (tile, group) steps of the launch are cut into
+// `grid` EQUAL contiguous ranges, one per persistent CTA, so no SM idles in a last partial
+// wave (config 3: 512 tiles on 148 SMs = 3.46 waves, 13 % of the scan lost to the tail).
+// A tile whose groups straddle two CTAs is finished by the second to arrive: each writes
+// its exact int32 partial (own groups, unbiased) to its slot, fences, bumps the tile's
+// counter; the finisher adds the other's partial to its registers, stores z and folds
+// max / min (the sums are exact integers, so the result equals the unsplit scan's).
+// Needs steps per CTA >= 2 g (every tile straddles at most two CTAs; the launcher checks).
+template <int G, int TPT>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan_sk(LayerArgs a, int tiles_per_unit,
+                                                              int total_tiles, int *skpart,
+                                                              uint32_t *skctr) {
+  constexpr int kChunks = TPT / 8;
+  constexpr int kTile = kScanThreads * TPT;
+  constexpr int kSlots = 3;
+  constexpr uint32_t kWarps = kScanThreads / 32;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t slice_bytes = (uint32_t)a.cpow2 * G * 2;
+  uint8_t *tbuf = smem;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSlots * slice_bytes);
+  __shared__ uint32_t s_done[kSlots];
+  __shared__ int s_fin;
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < kSlots; ++j) { mbar_init(&full[j], 1); s_done[j] = 0; }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_trigger();
+  __syncthreads();
+  pdl_wait();
+  const int g = a.g;
+  const int64_t S = (int64_t)total_tiles * g;
+  const int64_t s0 = S * blockIdx.x / gridDim.x, s1 = S * (blockIdx.x + 1) / gridDim.x;
+  if (s0 >= s1) return;
+  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int woff = warp * (32 * TPT);
+
+  // step cursor: s = global step, i = its group, tok0 = its tile's first token (divisions
+  // only when a tile starts)
+  struct Cur { int64_t s; int i; int64_t tok0; const uint16_t *P; const uint8_t *T; };
+  auto cpos = [&](Cur &c, int64_t st) {  // pointers of step st (tile st / g, group st % g)
+    c.s = st;
+    if (st >= s1) return;
+    const int tile = (int)(st / g), i = (int)(st - (int64_t)tile * g);
+    const int u = tile / tiles_per_unit, tk = tile - u * tiles_per_unit;
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    c.i = i;
+    c.tok0 = (int64_t)tk * kTile;
+    c.P = a.codes + (int64_t)b * a.code_b_stride + ((int64_t)kv * g + i) * a.n_cap + c.tok0 + woff + lane * 8;
+    c.T = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * g + i) * slice_bytes;
+  };
+  auto cadv = [&](Cur &c) {
+    if (c.s + 1 < s1 && c.i + 1 < g) {  // same tile: next group's strip and slice
+      ++c.s;
+      ++c.i;
+      c.P += a.n_cap;
+      c.T += slice_bytes;
+    } else {
+      cpos(c, c.s + 1);
+    }
+  };
+  auto ccodes = [&](const Cur &c, uint4 (&r)[kChunks]) {
+    const bool live = c.s < s1;
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      const int64_t tok = c.tok0 + woff + k * 256 + lane * 8;
+      r[k] = (live && tok < a.n_q) ? ld_stream(c.P + k * 256) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto cslice = [&](const Cur &c, int slot) {
+    if (c.s < s1) {
+      mbar_expect_tx(&full[slot], slice_bytes);
+      bulk_g2s(tbuf + slot * slice_bytes, c.T, slice_bytes, &full[slot]);
+    }
+  };
+  Cur lc, lt;
+  cpos(lc, s0);
+  cpos(lt, s0);
+  uint4 rc0[kChunks], rc1[kChunks];
+  ccodes(lc, rc0);
+  cadv(lc);
+  ccodes(lc, rc1);
+  cadv(lc);
+  for (int j = 0; j < kSlots; ++j) {
+    if (threadIdx.x == 0) cslice(lt, j);
+    cadv(lt);
+  }
+  uint32_t ph = 0;
+  int slot = 0;
+  int64_t st = s0;
+  while (st < s1) {
+    const int tile = (int)(st / g);
+    const int64_t t_lo = (int64_t)tile * g, t_hi = t_lo + g;
+    const int64_t e = t_hi < s1 ? t_hi : s1;  // steps of this tile done by this CTA: [st, e)
+    const int ng = (int)(e - st);
+    const bool whole = st == t_lo && e == t_hi;
+    const int u = tile / tiles_per_unit, tk = tile - u * tiles_per_unit;
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int64_t tile0 = (int64_t)tk * kTile;
+    int acc[kChunks][8][G];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+      for (int u8 = 0; u8 < 8; ++u8)
+#pragma unroll
+        for (int h = 0; h < G; ++h) acc[k][u8][h] = 0;
+    for (int i = 0; i < ng; ++i) {
+      uint4 rc2[kChunks];
+      ccodes(lc, rc2);
+      cadv(lc);
+      mbar_wait(&full[slot], (ph >> slot) & 1u);
+      ph ^= 1u << slot;
+      const uint8_t *sb = tbuf + slot * slice_bytes;
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) lookup8<G>(rc0[k], sb, mask, acc[k]);
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+        for (int u8 = 0; u8 < 8; u8 += 2) {
+          if constexpr (G == 4)
+            asm volatile("" ::"r"(acc[k][u8][0]), "r"(acc[k][u8][1]), "r"(acc[k][u8][2]), "r"(acc[k][u8][3]),
+                         "r"(acc[k][u8 + 1][0]), "r"(acc[k][u8 + 1][1]), "r"(acc[k][u8 + 1][2]),
+                         "r"(acc[k][u8 + 1][3]));
+          else if constexpr (G == 2)
+            asm volatile("" ::"r"(acc[k][u8][0]), "r"(acc[k][u8][1]), "r"(acc[k][u8 + 1][0]),
+                         "r"(acc[k][u8 + 1][1]));
+          else
+            asm volatile("" ::"r"(acc[k][u8][0]), "r"(acc[k][u8 + 1][0]));
+        }
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t old;
+        asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "r"(smem_u32(&s_done[slot]))
+                     : "memory");
+        if (old == kWarps - 1) {
+          asm volatile("st.relaxed.cta.shared::cta.u32 [%0], 0;" ::"r"(smem_u32(&s_done[slot])) : "memory");
+          cslice(lt, slot);
+        }
+      }
+      cadv(lt);
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) { rc0[k] = rc1[k]; rc1[k] = rc2[k]; }
+      slot = slot == kSlots - 1 ? 0 : slot + 1;
+    }
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) unbias<G>(acc[k], ng);
+    bool finish = whole;
+    if (!whole) {
+      // my partial -> my slot (0: this tile is my first, 1: my last); the second to arrive
+      // adds the other CTA's slot and finishes the tile
+      const int myslot = st == s0 ? 0 : 1;
+      int *mine = skpart + ((int64_t)blockIdx.x * 2 + myslot) * (kTile * G);
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) {
+          int *dst = mine + ((int64_t)(woff + k * 256 + lane * 8 + u8)) * G;
+          if constexpr (G == 4)
+            *reinterpret_cast<int4 *>(dst) = make_int4(acc[k][u8][0], acc[k][u8][1], acc[k][u8][2], acc[k][u8][3]);
+          else
+#pragma unroll
+            for (int h = 0; h < G; ++h) dst[h] = acc[k][u8][h];
+        }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint32_t prev = atomicAdd(&skctr[tile], 1u);
+        s_fin = prev == 1u;
+        if (prev == 1u) skctr[tile] = 0u;
+      }
+      __syncthreads();
+      finish = s_fin != 0;
+      if (finish) {
+        __threadfence();
+        // the other contributor: the previous CTA (tile = its last) or the next (its first)
+        const int oc = myslot == 0 ? (int)blockIdx.x - 1 : (int)blockIdx.x + 1;
+        const int os = myslot == 0 ? 1 : 0;
+        const int *other = skpart + ((int64_t)oc * 2 + os) * (kTile * G);
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k)
+#pragma unroll
+          for (int u8 = 0; u8 < 8; ++u8) {
+            const int *src = other + ((int64_t)(woff + k * 256 + lane * 8 + u8)) * G;
+            if constexpr (G == 4) {
+              const int4 v = __ldcg(reinterpret_cast<const int4 *>(src));
+              acc[k][u8][0] += v.x; acc[k][u8][1] += v.y; acc[k][u8][2] += v.z; acc[k][u8][3] += v.w;
+            } else {
+#pragma unroll
+              for (int h = 0; h < G; ++h) acc[k][u8][h] += __ldcg(src + h);
+            }
+          }
+      }
+    }
+    if (finish) {
+      int mx[G], mn[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k)
+        store_chunk<G>(a, a.z, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn, false);
+      fold_minmax<G>(a, b, kv, mx, mn);
+    }
+    st = e;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // 8-bit table variant (R2b): one 4-byte LDS per (token, group) -- 3.5 instead of
 // 6.15 shared-memory wavefronts per warp lookup -- and SWAR accumulation: the entry holds
 // the 4 heads as (int8 + 128) bytes; acc_e += w & 0x00FF00FF (heads 0, 2), acc_o +=
@@ -873,9 +1082,54 @@ static int scan_codes_in_regs() {
   return v;
 }
 
+static int scan_streamk() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_SCAN_SK");
+    v = (ev && !strcmp(ev, "0")) ? 0 : 1;
+  }
+  return v;
+}
+
+// stream-K launch when every CTA gets >= 2 tiles of steps (else false: use the pipe kernel)
+template <int G, int TPT>
+static bool scan_sk_launch(const LayerArgs &a, cudaStream_t s, cudaError_t *err) {
+  constexpr int kTile = kScanThreads * TPT;
+  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
+  const int total = tiles_per_unit * a.B * a.Hkv;
+  const int grid = a.num_sms < kSkMaxCtas ? a.num_sms : kSkMaxCtas;
+  if (!a.skpart || !a.skctr || total < 2 * grid || total > a.skctr_n || total == 0) return false;
+  const size_t smem = (size_t)3 * a.cpow2 * G * 2 + 3 * 8;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan_sk<G, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         226 * 1024);
+    if (e != cudaSuccess) { *err = e; return true; }
+    configured[dev] = 1;
+  }
+  cudaEvent_t eb, ee;
+  scan_events(&eb, &ee);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
+  launch_chain(k_scan_sk<G, TPT>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, a.skpart,
+               a.skctr);
+  note_launch();
+  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
+  *err = cudaGetLastError();
+  return true;
+}
+
 template <int G>
 static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
   const int rc = scan_codes_in_regs();
+  if (!a.pcodes && rc && scan_pipelined() && scan_streamk() && a.scan_split == 1) {
+    cudaError_t e = cudaSuccess;
+    if (a.scan_tpt == 8 ? scan_sk_launch<G, 8>(a, s, &e) : scan_sk_launch<G, 16>(a, s, &e)) return e;
+  }
   if (a.pcodes)  // packed 13-bit codes: pipelined kernel only
     return a.scan_tpt == 8 ? scan_pipe_launch<G, 8, true>(a, s) : scan_pipe_launch<G, 16, true>(a, s);
   if (rc && scan_pipelined())

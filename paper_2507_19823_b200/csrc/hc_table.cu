@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   pdl_wait();
   if (a.gdone && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
     for (int t = threadIdx.x; t < a.gdone_n; t += blockDim.x) a.gdone[t] = 0u;
+  if (a.skctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 1 % gridDim.z)
+    for (int t = threadIdx.x; t < a.skctr_n; t += blockDim.x) a.skctr[t] = 0u;
   if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
     const int uu = blockIdx.z, bb = uu / a.Hkv, kk = uu - bb * a.Hkv;
     const int64_t nz4 = (a.n_q + 3) / 4;  // float4s per row (rows are 64-float aligned)
