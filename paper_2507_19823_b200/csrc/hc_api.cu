@@ -79,6 +79,15 @@ constexpr int kMaxTSplit = 8;
 // Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
 // the group split so the work fills the SMs with the least shared-memory time, modelled
 // per SM as  lookups/5.2 + slice_bytes_streamed/100  cycles (+ partial write/reduce).
+bool scan_sk_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_SCAN_SK");
+    v = (ev && !strcmp(ev, "0")) ? 0 : 1;
+  }
+  return v != 0;
+}
+
 void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int *tpt, int *split,
                  int lut8) {
   // per-SM shared-memory cycles: lookups * wavefronts/32 + (table slice + code strip) / 128 B
@@ -96,7 +105,10 @@ void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int
     for (int sp : {1, 2, 4}) {
       if (sp > g) continue;
       const int64_t items = tiles * sp;
-      const int64_t waves = (items + sms - 1) / sms;
+      // unsplit + >= 2 tiles per CTA: the stream-K scan balances steps exactly (k_scan_sk)
+      const bool sk = sp == 1 && !lut8 && tiles >= 2 * (int64_t)(sms < kSkMaxCtas ? sms : kSkMaxCtas) &&
+                      scan_sk_enabled();
+      const double waves = sk ? (double)items / sms : (double)((items + sms - 1) / sms);
       const double gper = (double)((g + sp - 1) / sp);
       double item = tile * gper * wf / 32.0 + gper * (cpow2 * entry + tile * 4.0) / 128.0;
       if (sp > 1) item += tile * G * 4.0 / 64.0;  // partial stores
