@@ -179,3 +179,26 @@ def test_host_worker_timeout_reports(torch_cuda):
     assert w.status() == hc.HC_ERR_CUDA
     w.pause(False)
     w.close()
+
+
+def test_hetero_shared_kv_selection(torch_cuda):
+    """Heterogeneous Eq. 5 over the per-KV-head shared selection (R8): the G rows of a KV head
+    carry one index set, each head sums its own weights on both sides of the split."""
+    import torch
+    import paper_2507_19823_b200 as hc
+    from paper_2507_19823_b200.hetero import HeteroEq5
+    case = Case(B=2, Hkv=2, n=14000, k_max=2000, placement=1, seed=86, shared=True)
+    kc, vs, q = build_gpu(case)
+    B, Hq, d, km = case.B, case.Hq, case.d, case.k_max
+    bud = hc.budget(case.tau, km, shared_kv=True)
+    ws = hc.Workspace(kc.workspace_bytes(bud))
+    het = HeteroEq5(kc, vs, km, 0.5, threads=4)
+    out = torch.full((B, Hq, d), float("nan"), device="cuda")
+    sel_k = torch.zeros((B, Hq), dtype=torch.int64, device="cuda")
+    het(q[0].contiguous(), 0, bud, out, sel_k, ws)
+    torch.cuda.synchronize()
+    gpu = dict(out=out.cpu().numpy(), idx=het.idx_d.view(B, Hq, km).cpu().numpy(),
+               w=het.w_d.view(B, Hq, km).cpu().numpy(), k=sel_k.cpu().numpy())
+    for b in range(B):
+        for kv in range(case.Hkv):
+            compare_unit(case, gpu, oracle_unit(case, b, 0, kv), b, kv, check_z=False)
