@@ -308,7 +308,9 @@ hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w,
  *     done (so later work on the stream sees out), or after timeout_s seconds, when the
  *     job is marked failed: hc_host_worker_status then returns HC_ERR_CUDA.
  * Submissions of one job must not overlap (wait before the next submit).  add_job returns
- * HC_ERR_CAPACITY beyond max_jobs.  destroy stops the thread (no wait may be pending). */
+ * HC_ERR_CAPACITY beyond max_jobs; create / add_job / destroy are setup calls for one
+ * thread (the worker itself only reads jobs that add_job has published).  destroy stops the
+ * thread (no wait may be pending). */
 typedef struct hc_host_worker hc_host_worker;
 hc_status hc_host_worker_create(int32_t threads, int32_t max_jobs, double timeout_s, hc_host_worker **out);
 hc_status hc_host_worker_destroy(hc_host_worker *w);

@@ -570,7 +570,7 @@ class HostWorker:
     """hc_host_worker_*: persistent host thread running host shares of Eq. 5 on doorbells
     rung by GPU kernels (no graph host nodes).  See include/hc.h."""
 
-    def __init__(self, threads: int = 0, max_jobs: int = 64, timeout_s: float = 30.0):
+    def __init__(self, threads: int = 0, max_jobs: int = 64, timeout_s: float = 10.0):
         h = C.c_void_p()
         _check(lib().hc_host_worker_create(int(threads), int(max_jobs), float(timeout_s), C.byref(h)))
         self.h = h
