@@ -96,6 +96,10 @@ struct HostArgs {
   int32_t threads;
   int64_t tok_begin, tok_end;  // host-owned token range (global indices)
   bool owned_once;
+  // streaming input (doorbell worker): unit u's rows are valid once ready[u] == epoch;
+  // the range is then used as given (no clamp pass over the rows)
+  const volatile uint32_t *ready = nullptr;
+  uint32_t epoch = 0;
 };
 
 inline void prefetch_row(const uint16_t *p, int d) {
@@ -173,9 +177,12 @@ void run(const HostArgs &a) {
   const int G = a.G, d = a.d;
   const int64_t units = a.rows / G;
   // clamp the range to the tokens actually kept (lists are ascending)
-  int64_t last = -1;
-  for (int64_t row = 0; row < a.rows; ++row)
-    if (a.k[row] > 0 && a.idx[row * a.k_stride + a.k[row] - 1] > last) last = a.idx[row * a.k_stride + a.k[row] - 1];
+  int64_t last = a.tok_end - 1;
+  if (!a.ready) {
+    last = -1;
+    for (int64_t row = 0; row < a.rows; ++row)
+      if (a.k[row] > 0 && a.idx[row * a.k_stride + a.k[row] - 1] > last) last = a.idx[row * a.k_stride + a.k[row] - 1];
+  }
   const int64_t t0 = a.tok_begin, t1 = a.tok_end < last + 1 ? a.tok_end : last + 1;
   const int64_t nch = t1 > t0 ? (t1 - t0 + kHostChunk - 1) / kHostChunk : 0;
   if (nch == 0) {
@@ -191,6 +198,10 @@ void run(const HostArgs &a) {
 #pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
   for (int64_t it = 0; it < items; ++it) {
     const int64_t u = it / nch, c = it - u * nch;
+    if (a.ready) {  // wait for this unit's staged lists (units arrive in order)
+      while (a.ready[u] != a.epoch) _mm_pause();
+      std::atomic_thread_fence(std::memory_order_acquire);
+    }
     const int64_t j0 = t0 + c * kHostChunk, j1 = j0 + kHostChunk < t1 ? j0 + kHostChunk : t1;
     const int64_t b = (u * G) / a.Hq, kv = ((u * G) % a.Hq) / G;
     const uint16_t *Vb = a.V + b * a.v_b_stride + kv * a.v_kv_stride;
@@ -283,53 +294,75 @@ struct Job {
   float *w_d;
   int64_t *k_d;
   Mailbox *mb_h, *mb_d;
-  uint32_t *ctr;       // device completion counter of k_submit
+  uint32_t *ctr;       // device: [0] completion counter of k_submit, [1] epoch, [2..] per-unit rows staged
+  uint32_t *ready_h, *ready_d;  // pinned mapped [units]: epoch of the unit's last staging
   uint32_t seen;
 };
 
 __global__ void k_submit(const int32_t *sel_idx, const float *sel_w, const int64_t *sel_k, int64_t k_stride,
-                         int64_t t_split, int64_t v_off, int32_t *idx_h, float *w_h, int64_t *k_h,
-                         Mailbox *mb, uint32_t *ctr) {
-  const int row = blockIdx.x;
+                         int64_t rows, int G, int64_t t_split, int64_t v_off, int32_t *idx_h, float *w_h,
+                         int64_t *k_h, Mailbox *mb, uint32_t *ctr, volatile uint32_t *ready) {
+  // the epoch of this submission: the device counter is only advanced by the last CTA to
+  // finish, after every CTA has read it here
+  __shared__ uint32_t s_epoch;
   __shared__ int64_t s_p;
-  if (threadIdx.x == 0) {
-    const int32_t *li = sel_idx + (int64_t)row * k_stride;
-    int64_t lo = 0, hi = sel_k[row];
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)li[mid] < t_split) lo = mid + 1; else hi = mid;
-    }
-    s_p = lo;
-    k_h[row] = lo;
-  }
+  if (threadIdx.x == 0) s_epoch = *(volatile uint32_t *)&ctr[1] + 1u;
   __syncthreads();
-  const int64_t p = s_p;
-  const int32_t *si = sel_idx + (int64_t)row * k_stride;
-  const float *sw = sel_w + (int64_t)row * k_stride;
-  int32_t *di = idx_h + (int64_t)row * k_stride;
-  float *dw = w_h + (int64_t)row * k_stride;
-  const int64_t p4 = p & ~(int64_t)3;  // rows are 16-B aligned when k_stride % 4 == 0
-  if ((k_stride & 3) == 0) {
-    for (int64_t e = (int64_t)threadIdx.x * 4; e < p4; e += (int64_t)blockDim.x * 4) {
-      *reinterpret_cast<int4 *>(di + e) = *reinterpret_cast<const int4 *>(si + e);
-      *reinterpret_cast<float4 *>(dw + e) = *reinterpret_cast<const float4 *>(sw + e);
-    }
-    for (int64_t e = p4 + threadIdx.x; e < p; e += blockDim.x) { di[e] = si[e]; dw[e] = sw[e]; }
-  } else {
-    for (int64_t e = threadIdx.x; e < p; e += blockDim.x) { di[e] = si[e]; dw[e] = sw[e]; }
+  const uint32_t epoch = s_epoch;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // ring first: the worker starts at once and
+    mb->t_split = t_split;                    // consumes units as their ready flags flip
+    mb->v_off = v_off;
+    __threadfence_system();
+    mb->req = epoch;
+    __threadfence_system();
   }
-  __threadfence_system();  // this thread's staging writes before the completion count
-  __syncthreads();
+  // rows in unit-major order, gridDim.x rows in flight: early units become ready early
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const int32_t *li = sel_idx + row * k_stride;
+      int64_t lo = 0, hi = sel_k[row];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)li[mid] < t_split) lo = mid + 1; else hi = mid;
+      }
+      s_p = lo;
+      k_h[row] = lo;
+    }
+    __syncthreads();
+    const int64_t p = s_p;
+    const int32_t *si = sel_idx + row * k_stride;
+    const float *sw = sel_w + row * k_stride;
+    int32_t *di = idx_h + row * k_stride;
+    float *dw = w_h + row * k_stride;
+    if ((k_stride & 3) == 0) {
+      const int64_t p4 = p & ~(int64_t)3;
+      for (int64_t e = (int64_t)threadIdx.x * 4; e < p4; e += (int64_t)blockDim.x * 4) {
+        *reinterpret_cast<int4 *>(di + e) = *reinterpret_cast<const int4 *>(si + e);
+        *reinterpret_cast<float4 *>(dw + e) = *reinterpret_cast<const float4 *>(sw + e);
+      }
+      for (int64_t e = p4 + threadIdx.x; e < p; e += blockDim.x) { di[e] = si[e]; dw[e] = sw[e]; }
+    } else {
+      for (int64_t e = threadIdx.x; e < p; e += blockDim.x) { di[e] = si[e]; dw[e] = sw[e]; }
+    }
+    __threadfence_system();  // this thread's staging writes before the unit's count
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t u = row / G;
+      const uint32_t prev = atomicAdd(&ctr[2 + u], 1u);
+      if (prev == (uint32_t)G - 1u) {  // the unit's last row: publish it
+        ctr[2 + u] = 0u;
+        __threadfence_system();
+        ready[u] = epoch;
+        __threadfence_system();
+      }
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(ctr, 1u);
-    if (prev == gridDim.x - 1) {  // last row: every row's writes are fenced
-      *ctr = 0u;
-      __threadfence_system();
-      mb->t_split = t_split;
-      mb->v_off = v_off;
-      __threadfence_system();
-      mb->req = mb->req + 1u;
-      __threadfence_system();
+    const uint32_t prev = atomicAdd(&ctr[0], 1u);
+    if (prev == gridDim.x - 1) {  // every CTA has read the epoch: advance it
+      ctr[0] = 0u;
+      *(volatile uint32_t *)&ctr[1] = epoch;
     }
   }
 }
@@ -378,6 +411,8 @@ void worker_loop(hc_host_worker *w) {
       std::atomic_thread_fence(std::memory_order_acquire);
       HostArgs a{jb.idx_h, jb.w_h, jb.k_h, jb.rows, jb.k_stride, jb.V + jb.mb_h->v_off, jb.v_b_stride,
                  jb.v_kv_stride, jb.Hq, jb.G, jb.d, jb.out, w->threads, 0, jb.mb_h->t_split, false};
+      a.ready = jb.ready_h;
+      a.epoch = r;
       run(a);
       jb.seen = r;
       std::atomic_thread_fence(std::memory_order_release);
@@ -457,6 +492,7 @@ hc_status hc_host_worker_destroy(hc_host_worker *w) {
     cudaFreeHost(jb.w_h);
     cudaFreeHost(jb.k_h);
     cudaFreeHost((void *)jb.mb_h);
+    cudaFreeHost(jb.ready_h);
     cudaFree(jb.ctr);
   }
   delete w;
@@ -479,13 +515,17 @@ hc_status hc_host_worker_add_job(hc_host_worker *w, int64_t rows, int64_t k_stri
             cudaHostAlloc((void **)&jb.w_h, (size_t)rows * k_stride * 4, fl) == cudaSuccess &&
             cudaHostAlloc((void **)&jb.k_h, (size_t)rows * 8, fl) == cudaSuccess &&
             cudaHostAlloc((void **)&jb.mb_h, sizeof(Mailbox), fl) == cudaSuccess &&
-            cudaMalloc((void **)&jb.ctr, 4) == cudaSuccess && cudaMemset(jb.ctr, 0, 4) == cudaSuccess;
+            cudaHostAlloc((void **)&jb.ready_h, (size_t)(rows / G) * 4, fl) == cudaSuccess &&
+            cudaMalloc((void **)&jb.ctr, (size_t)(2 + rows / G) * 4) == cudaSuccess &&
+            cudaMemset(jb.ctr, 0, (size_t)(2 + rows / G) * 4) == cudaSuccess;
   if (ok) {
     memset((void *)jb.mb_h, 0, sizeof(Mailbox));
+    memset(jb.ready_h, 0, (size_t)(rows / G) * 4);
     ok = cudaHostGetDevicePointer((void **)&jb.idx_d, jb.idx_h, 0) == cudaSuccess &&
          cudaHostGetDevicePointer((void **)&jb.w_d, jb.w_h, 0) == cudaSuccess &&
          cudaHostGetDevicePointer((void **)&jb.k_d, jb.k_h, 0) == cudaSuccess &&
-         cudaHostGetDevicePointer((void **)&jb.mb_d, (void *)jb.mb_h, 0) == cudaSuccess;
+         cudaHostGetDevicePointer((void **)&jb.mb_d, (void *)jb.mb_h, 0) == cudaSuccess &&
+         cudaHostGetDevicePointer((void **)&jb.ready_d, jb.ready_h, 0) == cudaSuccess;
   }
   if (!ok) return HC_ERR_CUDA;
   jb.seen = 0;
@@ -501,8 +541,9 @@ hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *s
   if (job < 0 || job >= w->njobs.load()) return HC_ERR_RANGE;
   if (t_split < 0 || v_off < 0) return HC_ERR_RANGE;
   Job &jb = w->jobs[job];
-  k_submit<<<(unsigned)jb.rows, 256, 0, (cudaStream_t)stream>>>(sel_idx, sel_w, sel_k, jb.k_stride, t_split, v_off,
-                                                               jb.idx_d, jb.w_d, jb.k_d, jb.mb_d, jb.ctr);
+  const unsigned grid = (unsigned)(jb.rows < 32 ? jb.rows : 32);  // rows in flight (unit-major order)
+  k_submit<<<grid, 256, 0, (cudaStream_t)stream>>>(sel_idx, sel_w, sel_k, jb.k_stride, jb.rows, jb.G, t_split,
+                                                   v_off, jb.idx_d, jb.w_d, jb.k_d, jb.mb_d, jb.ctr, jb.ready_d);
   hc::note_launch();
   return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }
