@@ -206,10 +206,12 @@ class Workload:
             if B % P:
                 raise SystemExit(f"--pipeline {P} must divide the batch B={B}")
             nb = B // P
+            shared_worker = hc.HostWorker(threads=os.cpu_count() or 1) if cfg.get("host_frac", 0.0) > 0.0 else None
             for i in range(P):
                 kv_ = self.kc.batch_view(i * nb, nb)
                 vs_ = self.vs.batch_view(i * nb, nb)
-                het = (HeteroEq5(kv_, vs_, cfg["k_max"], cfg["host_frac"], device=device)
+                het = (HeteroEq5(kv_, vs_, cfg["k_max"], cfg["host_frac"], device=device,
+                                 worker=shared_worker)
                        if cfg.get("host_frac", 0.0) > 0.0 else None)
                 self.parts.append(dict(b0=i * nb, b1=(i + 1) * nb, kc=kv_, vs=vs_, het=het,
                                        stream=torch.cuda.Stream(device=device)))

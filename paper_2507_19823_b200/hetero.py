@@ -25,7 +25,7 @@ import paper_2507_19823_b200 as hc
 
 class HeteroEq5:
     def __init__(self, kc: "hc.KCache", vstore: "hc.VStore", k_max: int, host_frac: float,
-                 threads: int = 0, device="cuda", mode: str = "doorbell"):
+                 threads: int = 0, device="cuda", mode: str = "doorbell", worker=None):
         import torch
         if vstore.placement != hc.HC_V_HOST_MAPPED:
             raise ValueError("the heterogeneous split needs host-resident values (HC_V_HOST_MAPPED)")
@@ -50,7 +50,9 @@ class HeteroEq5:
             raise ValueError("mode must be doorbell or hostnode")
         self.mode = mode
         if mode == "doorbell":
-            self.worker = hc.HostWorker(threads=self.threads)
+            # several instances (e.g. micro-batch chains) may share one worker: its jobs then
+            # run one after another with the whole host team
+            self.worker = worker if worker is not None else hc.HostWorker(threads=self.threads)
             self.job = self.worker.add_job(rows, self.k_max, vstore, kc.G, self.part_h)
         self.ev_sel = torch.cuda.Event()
         self.ev_host = torch.cuda.Event()

@@ -26,8 +26,10 @@ def main():
         for f in fracs:
             if P == 1:
                 wl.hetero = HeteroEq5(wl.kc, wl.vs, cfg["k_max"], f) if f > 0 else None
+            import paper_2507_19823_b200 as hc
+            shw = hc.HostWorker(threads=os.cpu_count() or 1) if (f > 0 and wl.parts) else None
             for part in wl.parts:
-                part["het"] = HeteroEq5(part["kc"], part["vs"], cfg["k_max"], f) if f > 0 else None
+                part["het"] = HeteroEq5(part["kc"], part["vs"], cfg["k_max"], f, worker=shw) if f > 0 else None
             wl.reset_counts()
             wl.step()
             torch.cuda.synchronize()
