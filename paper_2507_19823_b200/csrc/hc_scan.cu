@@ -546,7 +546,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_sk(LayerArgs a, int ti
   uint8_t *tbuf = smem;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSlots * slice_bytes);
   __shared__ uint32_t s_done[kSlots];
-  __shared__ int s_fin;
   if (threadIdx.x == 0) {
     for (int j = 0; j < kSlots; ++j) { mbar_init(&full[j], 1); s_done[j] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -675,8 +674,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_sk(LayerArgs a, int ti
     for (int k = 0; k < kChunks; ++k) unbias<G>(acc[k], ng);
     bool finish = whole;
     if (!whole) {
-      // my partial -> my slot (0: this tile is my first, 1: my last); the second to arrive
-      // adds the other CTA's slot and finishes the tile
+      // my partial -> my slot (0: this tile is my first, 1: my last).  Per WARP (each warp owns
+      // a disjoint token range of the tile): the warp's second arrival (over the two CTAs)
+      // adds the other CTA's partial for its tokens and finishes them -- no CTA barrier, one
+      // fence per warp (release / acquire around the counter by lane 0, ordered for the
+      // other lanes by __syncwarp)
       const int myslot = st == s0 ? 0 : 1;
       int *mine = skpart + ((int64_t)blockIdx.x * 2 + myslot) * (kTile * G);
 #pragma unroll
@@ -690,17 +692,17 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_sk(LayerArgs a, int ti
 #pragma unroll
             for (int h = 0; h < G; ++h) dst[h] = acc[k][u8][h];
         }
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const uint32_t prev = atomicAdd(&skctr[tile], 1u);
-        s_fin = prev == 1u;
-        if (prev == 1u) skctr[tile] = 0u;
-      }
-      __syncthreads();
-      finish = s_fin != 0;
-      if (finish) {
+      __syncwarp();
+      uint32_t prev = 0;
+      if (lane == 0) {
         __threadfence();
+        prev = atomicAdd(&skctr[(int64_t)tile * kWarps + warp], 1u);
+        if (prev == 1u) skctr[(int64_t)tile * kWarps + warp] = 0u;
+        __threadfence();
+      }
+      finish = __shfl_sync(0xffffffffu, prev, 0) == 1u;
+      __syncwarp();
+      if (finish) {
         // the other contributor: the previous CTA (tile = its last) or the next (its first)
         const int oc = myslot == 0 ? (int)blockIdx.x - 1 : (int)blockIdx.x + 1;
         const int os = myslot == 0 ? 1 : 0;
@@ -1098,7 +1100,8 @@ static bool scan_sk_launch(const LayerArgs &a, cudaStream_t s, cudaError_t *err)
   const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
   const int total = tiles_per_unit * a.B * a.Hkv;
   const int grid = a.num_sms < kSkMaxCtas ? a.num_sms : kSkMaxCtas;
-  if (!a.skpart || !a.skctr || total < 2 * grid || total > a.skctr_n || total == 0) return false;
+  if (!a.skpart || !a.skctr || total < 2 * grid || (int64_t)total * (kScanThreads / 32) > a.skctr_n || total == 0)
+    return false;
   const size_t smem = (size_t)3 * a.cpow2 * G * 2 + 3 * 8;
   static int configured[64] = {0};
   int dev = 0;
