@@ -160,7 +160,8 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
     L.o_rpart = o; o += align256((size_t)rows * nchr * 128 * 4);
     L.o_rdone = o; o += align256((size_t)rows * 4);
     L.o_grange = o; o += align256((size_t)rows * 16);  // sharded finish: list slice per row
-    // stream-K scan: 2 partial tiles (8192 tokens x G int32) per CTA, one counter per tile
+    // stream-K scan (16-bit table): 2 partial tiles (8192 tokens x G int32) per CTA, one
+    // counter per (tile, warp)
     L.o_skpart = o; o += align256((size_t)kSkMaxCtas * 2 * 8192 * G * 4);
     L.skctr_n = (int)(units * ((ncand_max + 4095) / 4096) * 16);  // per (tile, warp)
     L.o_skctr = o; o += align256((size_t)L.skctr_n * 4);

@@ -296,3 +296,10 @@ def test_config4_full_size_sampled(torch_cuda):
     two sampled units: index sets bit-exact and outputs within tolerance at the full size."""
     case = Case(B=1, L=1, Hkv=8, g=32, n=1048576, k_max=131072, seed=4)
     _run(case, units=[(0, 0), (0, 6)])
+
+
+def test_stream_k_scan_ragged_sampled(torch_cuda):
+    """The 16-bit stream-K scan (k_scan_sk) on a ragged multi-tile shape: 8 units x 37 tiles of
+    8192 tokens (>= 2 tiles per CTA), z bit-exact on sampled units."""
+    case = Case(B=1, L=1, Hkv=8, g=32, n=300007, k_max=30000, seed=58)
+    _run(case, units=[(0, 1), (0, 7)])
