@@ -804,7 +804,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": ("k_resident (exact-key dense scan, VO-only mode)" if wl.vo_only
-                                else "k_scan (Eq. 3 quantized-key scan)"),
+                                else "Eq. 3 quantized-key scan: k_scan_sk (stream-K) when every CTA gets "
+                                     ">= 2 tiles, else k_scan_pipe / k_scan8_pipe (hc_scan.cu)"),
                      "algorithmic_bytes_per_launch": p_bytes_layer,
                      "avg_launch_ms": scan_avg_ms, "share_of_step": scan_avg_ms * L * cfg.get("pipeline", 1) / ms_per_step,
                      "peak_source": peak_src,

@@ -299,6 +299,10 @@ struct Job {
   uint32_t seen;
 };
 
+}  // namespace
+
+namespace hc {  // the worker's kernels (named for launch lists)
+
 __global__ void k_submit(const int32_t *sel_idx, const float *sel_w, const int64_t *sel_k, int64_t k_stride,
                          int64_t rows, int G, int64_t t_split, int64_t v_off, int32_t *idx_h, float *w_h,
                          int64_t *k_h, Mailbox *mb, uint32_t *ctr, volatile uint32_t *ready) {
@@ -384,7 +388,7 @@ __global__ void k_wait(Mailbox *mb, uint64_t timeout_ns) {
   __threadfence_system();
 }
 
-}  // namespace
+}  // namespace hc
 
 struct hc_host_worker {
   std::vector<Job> jobs;
@@ -542,7 +546,7 @@ hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *s
   if (t_split < 0 || v_off < 0) return HC_ERR_RANGE;
   Job &jb = w->jobs[job];
   const unsigned grid = (unsigned)(jb.rows < 32 ? jb.rows : 32);  // rows in flight (unit-major order)
-  k_submit<<<grid, 256, 0, (cudaStream_t)stream>>>(sel_idx, sel_w, sel_k, jb.k_stride, jb.rows, jb.G, t_split,
+  hc::k_submit<<<grid, 256, 0, (cudaStream_t)stream>>>(sel_idx, sel_w, sel_k, jb.k_stride, jb.rows, jb.G, t_split,
                                                    v_off, jb.idx_d, jb.w_d, jb.k_d, jb.mb_d, jb.ctr, jb.ready_d);
   hc::note_launch();
   return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
@@ -551,7 +555,7 @@ hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *s
 hc_status hc_host_worker_wait(hc_host_worker *w, int32_t job, hc_stream_t stream) {
   if (!w) return HC_ERR_ARG;
   if (job < 0 || job >= w->njobs.load()) return HC_ERR_RANGE;
-  k_wait<<<1, 32, 0, (cudaStream_t)stream>>>(w->jobs[job].mb_d, w->timeout_ns);
+  hc::k_wait<<<1, 32, 0, (cudaStream_t)stream>>>(w->jobs[job].mb_d, w->timeout_ns);
   hc::note_launch();
   return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }

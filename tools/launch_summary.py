@@ -19,7 +19,8 @@ def main():
         short = name.split("(")[0].replace("void ", "")
         agg[short][0] += 1
         agg[short][1] += float(r[vi]) / 1e6  # ns -> ms
-    ours = {k: v for k, v in agg.items() if k.startswith("hc::")}
+    ours = {k: v for k, v in agg.items()
+            if k.startswith("hc::") or k in ("<unnamed>::k_submit", "<unnamed>::k_wait")}  # (older builds)
     tot = sum(v[1] for v in ours.values())
     print(f"# {sys.argv[2] if len(sys.argv) > 2 else path}\n")
     print("| kernel | launches | total ms | share | avg us |\n|---|---|---|---|---|")
