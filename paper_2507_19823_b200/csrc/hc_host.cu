@@ -16,6 +16,7 @@
 #include <immintrin.h>
 #include <omp.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -396,6 +397,10 @@ struct hc_host_worker {
   std::atomic<bool> stop{false};
   std::atomic<bool> paused{false};
   std::thread th;
+  // HC_WORKER_STATS=1: time in the engine and idle time between jobs, printed by destroy
+  bool stats = false;
+  double busy_s = 0, idle_s = 0;
+  long jobs_run = 0;
   int threads;
   uint64_t timeout_ns;
   int max_jobs;
@@ -405,6 +410,7 @@ namespace {
 
 void worker_loop(hc_host_worker *w) {
   int idle = 0;
+  auto last_done = std::chrono::steady_clock::now();
   while (!w->stop.load(std::memory_order_acquire)) {
     bool did = false;
     const int nj = w->paused.load(std::memory_order_acquire) ? 0 : w->njobs.load(std::memory_order_acquire);
@@ -417,10 +423,18 @@ void worker_loop(hc_host_worker *w) {
                  jb.v_kv_stride, jb.Hq, jb.G, jb.d, jb.out, w->threads, 0, jb.mb_h->t_split, false};
       a.ready = jb.ready_h;
       a.epoch = r;
+      const auto t0 = std::chrono::steady_clock::now();
       run(a);
       jb.seen = r;
       std::atomic_thread_fence(std::memory_order_release);
       jb.mb_h->done = r;
+      if (w->stats) {
+        const auto t1 = std::chrono::steady_clock::now();
+        w->busy_s += std::chrono::duration<double>(t1 - t0).count();
+        w->idle_s += std::chrono::duration<double>(t0 - last_done).count();
+        ++w->jobs_run;
+        last_done = t1;
+      }
       did = true;
     }
     if (did) { idle = 0; continue; }
@@ -480,6 +494,7 @@ hc_status hc_host_worker_create(int32_t threads, int32_t max_jobs, double timeou
   w->threads = threads > 0 ? threads : omp_get_max_threads();
   w->timeout_ns = (uint64_t)(timeout_s * 1e9);
   w->max_jobs = max_jobs;
+  if (const char *ev = getenv("HC_WORKER_STATS")) w->stats = atoi(ev) != 0;
   w->jobs.resize(max_jobs);  // fixed storage: the worker reads entries while jobs are added
   w->th = std::thread(worker_loop, w);
   *out = w;
@@ -490,6 +505,9 @@ hc_status hc_host_worker_destroy(hc_host_worker *w) {
   if (!w) return HC_ERR_ARG;
   w->stop.store(true, std::memory_order_release);
   if (w->th.joinable()) w->th.join();
+  if (w->stats && w->jobs_run > 1)
+    fprintf(stderr, "[hc_host_worker] %ld jobs: engine %.1f us/job, idle between jobs %.1f us/job\n",
+            w->jobs_run, 1e6 * w->busy_s / w->jobs_run, 1e6 * w->idle_s / (w->jobs_run - 1));
   for (int j = 0; j < w->njobs.load(); ++j) {
     Job &jb = w->jobs[j];
     cudaFreeHost(jb.idx_h);

@@ -37,6 +37,8 @@ def main():
             ms = bench.time_graph(g, 5, 2) / 5
             print(f"pipeline={P} host_frac={f:.2f}: {ms:.1f} ms/step = {1000 / ms:.2f} steps/s", flush=True)
             del g
+            if wl.hetero is not None and getattr(wl.hetero, "worker", None) is not None:
+                wl.hetero.worker.close()  # prints HC_WORKER_STATS
         del wl
         import gc
         gc.collect()
