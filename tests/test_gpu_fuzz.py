@@ -3,6 +3,8 @@ batch, KV heads, GQA group, d, g (dbar 1..16), c, n (ragged, across tiles and sp
 tau, k_max (binding or not), resident window, shared codebooks, 16/13-bit codes and per-head /
 shared selection.  Every case: bit-exact z, S, M, k_sel and index sets; outputs within the
 north_star tolerance (harness.compare_unit)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -20,7 +22,10 @@ def torch_cuda():
     return torch
 
 
-def _cases(k=48, seed=2026):
+def _cases(k=None, seed=None):
+    # HC_FUZZ_N / HC_FUZZ_SEED widen the sweep (e.g. 300 cases for a soak run)
+    k = int(os.environ.get("HC_FUZZ_N", "48")) if k is None else k
+    seed = int(os.environ.get("HC_FUZZ_SEED", "2026")) if seed is None else seed
     rng = np.random.default_rng(seed)
     out = []
     for i in range(k):
@@ -39,8 +44,11 @@ def _cases(k=48, seed=2026):
         cbg = 1 if rng.random() < 0.25 else g
         B = int(rng.integers(1, 3))
         Hkv = int(rng.integers(1, 3))
-        out.append(dict(B=B, Hkv=Hkv, G=G, d=d, g=g, c=c, cbg=cbg, n=n, res_cap=res, n_res=n_res,
-                        tau=tau, k_max=k_max, code_bits=code_bits, shared=shared, seed=1000 + i))
+        kw = dict(B=B, Hkv=Hkv, G=G, d=d, g=g, c=c, cbg=cbg, n=n, res_cap=res, n_res=n_res,
+                  tau=tau, k_max=k_max, code_bits=code_bits, shared=shared, seed=1000 + i)
+        if i >= 48 and rng.random() < 0.3:  # wider sweeps also cover host-mapped values
+            kw["placement"] = 1
+        out.append(kw)
     return out
 
 
