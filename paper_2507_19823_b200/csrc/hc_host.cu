@@ -4,7 +4,7 @@
 // [tok_begin, tok_end) the host owns in the heterogeneous split (the GPU pulls the rest
 // over the host link, hc_gather_values; DESIGN §8b f1).
 //
-// Work item = (KV unit u = (b, kv), token chunk of kHostChunk tokens).  For each of the
+// Work item = (KV unit u = (b, kv), token chunk of g_chunk tokens).  For each of the
 // unit's G query heads the item cuts the head's ascending kept list to the chunk (binary
 // search) and accumulates w_j·V_j in fp32; heads run back to back over the same chunk, so
 // a row kept by several heads is read from DRAM once and from the core's L2 afterwards
@@ -30,7 +30,7 @@
 
 namespace {
 
-constexpr int64_t kHostChunk = 4096;  // tokens per work item
+int64_t g_chunk = 4096;                // tokens per work item (HC_HOST_CHUNK)
 int g_pf = 16;                        // kept rows prefetched ahead (HC_HOST_PF)
 int g_hint = 0;                       // 0: T0, 1: T1, 2: T2 (HC_HOST_HINT)
 
@@ -173,6 +173,7 @@ void run(const HostArgs &a) {
   const Isa isa = detect_isa();
   if (const char *ev = getenv("HC_HOST_PF")) g_pf = atoi(ev);
   if (const char *ev = getenv("HC_HOST_HINT")) g_hint = atoi(ev);
+  if (const char *ev = getenv("HC_HOST_CHUNK")) { const long v = atol(ev); if (v >= 256) g_chunk = v; }
   if (isa == kScalar) init_table();
   const int nt = a.threads > 0 ? a.threads : omp_get_max_threads();
   const int G = a.G, d = a.d;
@@ -185,7 +186,7 @@ void run(const HostArgs &a) {
       if (a.k[row] > 0 && a.idx[row * a.k_stride + a.k[row] - 1] > last) last = a.idx[row * a.k_stride + a.k[row] - 1];
   }
   const int64_t t0 = a.tok_begin, t1 = a.tok_end < last + 1 ? a.tok_end : last + 1;
-  const int64_t nch = t1 > t0 ? (t1 - t0 + kHostChunk - 1) / kHostChunk : 0;
+  const int64_t nch = t1 > t0 ? (t1 - t0 + g_chunk - 1) / g_chunk : 0;
   if (nch == 0) {
     memset(a.out, 0, sizeof(float) * (size_t)a.rows * d);
     return;
@@ -203,7 +204,7 @@ void run(const HostArgs &a) {
       while (a.ready[u] != a.epoch) _mm_pause();
       std::atomic_thread_fence(std::memory_order_acquire);
     }
-    const int64_t j0 = t0 + c * kHostChunk, j1 = j0 + kHostChunk < t1 ? j0 + kHostChunk : t1;
+    const int64_t j0 = t0 + c * g_chunk, j1 = j0 + g_chunk < t1 ? j0 + g_chunk : t1;
     const int64_t b = (u * G) / a.Hq, kv = ((u * G) % a.Hq) / G;
     const uint16_t *Vb = a.V + b * a.v_b_stride + kv * a.v_kv_stride;
     float *pp = P + (size_t)it * G * d;
