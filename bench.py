@@ -490,7 +490,7 @@ def measure_host_rows_gbs(wl, reps: int = 3) -> dict:
             "combined": nbytes / min(tc[1:]) / 1e9, "combined_host_share": split / n}
 
 
-HOST_FRAC_CANDIDATES = (0.6, 0.65, 0.7)
+HOST_FRAC_CANDIDATES = (0.65, 0.7, 0.75)
 
 
 def calibrate_host_frac(wl, cfg):
@@ -659,7 +659,7 @@ SMEM_CEILING = {
     4: {"entry_bytes": 4, "code_GBps": 4778.9, "frac_of_hbm": 4778.9 / 6549.4,
         "wavefronts_per_warp_lookup": 3.89, "source": "profiles/r01_smem_gather_micro.log"},
 }
-HOST_FRAC_DEFAULT = 0.65  # measured optimum on the B200 box (DESIGN §8b f1, tools/hetero_sweep.py)
+HOST_FRAC_DEFAULT = 0.7  # measured optimum on the B200 box (DESIGN §8b f1, tools/hetero_sweep.py)
 
 
 def main():

@@ -31,6 +31,7 @@
 namespace {
 
 int64_t g_chunk = 4096;                // tokens per work item (HC_HOST_CHUNK)
+std::atomic<uint64_t> g_ready_wait_ns{0};  // HC_WORKER_STATS: thread-time spent waiting on staging
 int g_pf = 16;                        // kept rows prefetched ahead (HC_HOST_PF)
 int g_hint = 0;                       // 0: T0, 1: T1, 2: T2 (HC_HOST_HINT)
 
@@ -201,7 +202,13 @@ void run(const HostArgs &a) {
   for (int64_t it = 0; it < items; ++it) {
     const int64_t u = it / nch, c = it - u * nch;
     if (a.ready) {  // wait for this unit's staged lists (units arrive in order)
-      while (a.ready[u] != a.epoch) _mm_pause();
+      if (a.ready[u] != a.epoch) {
+        const auto w0 = std::chrono::steady_clock::now();
+        while (a.ready[u] != a.epoch) _mm_pause();
+        g_ready_wait_ns.fetch_add((uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                      std::chrono::steady_clock::now() - w0).count(),
+                                  std::memory_order_relaxed);
+      }
       std::atomic_thread_fence(std::memory_order_acquire);
     }
     const int64_t j0 = t0 + c * g_chunk, j1 = j0 + g_chunk < t1 ? j0 + g_chunk : t1;
@@ -496,6 +503,7 @@ hc_status hc_host_worker_create(int32_t threads, int32_t max_jobs, double timeou
   w->timeout_ns = (uint64_t)(timeout_s * 1e9);
   w->max_jobs = max_jobs;
   if (const char *ev = getenv("HC_WORKER_STATS")) w->stats = atoi(ev) != 0;
+  g_ready_wait_ns.store(0);
   w->jobs.resize(max_jobs);  // fixed storage: the worker reads entries while jobs are added
   w->th = std::thread(worker_loop, w);
   *out = w;
@@ -507,8 +515,11 @@ hc_status hc_host_worker_destroy(hc_host_worker *w) {
   w->stop.store(true, std::memory_order_release);
   if (w->th.joinable()) w->th.join();
   if (w->stats && w->jobs_run > 1)
-    fprintf(stderr, "[hc_host_worker] %ld jobs: engine %.1f us/job, idle between jobs %.1f us/job\n",
-            w->jobs_run, 1e6 * w->busy_s / w->jobs_run, 1e6 * w->idle_s / (w->jobs_run - 1));
+    fprintf(stderr,
+            "[hc_host_worker] %ld jobs: engine %.1f us/job, idle between jobs %.1f us/job, "
+            "staging waits %.1f thread-us/job\n",
+            w->jobs_run, 1e6 * w->busy_s / w->jobs_run, 1e6 * w->idle_s / (w->jobs_run - 1),
+            1e-3 * (double)g_ready_wait_ns.load() / w->jobs_run);
   for (int j = 0; j < w->njobs.load(); ++j) {
     Job &jb = w->jobs[j];
     cudaFreeHost(jb.idx_h);

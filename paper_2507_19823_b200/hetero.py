@@ -42,7 +42,8 @@ class HeteroEq5:
         self.w_h = torch.empty((rows, self.k_max), dtype=torch.float32).pin_memory()
         self.k_h = torch.empty((rows,), dtype=torch.int64).pin_memory()
         self.part_h = torch.zeros((rows, kc.d), dtype=torch.float32).pin_memory()
-        self.side = torch.cuda.Stream(device=device)
+        # high priority: the staging kernel must not queue behind the GPU share's gather grid
+        self.side = torch.cuda.Stream(device=device, priority=-1)
         # "doorbell": a persistent host worker polls a mailbox rung by a GPU kernel (the
         # selection is copied by that kernel, only the host's share); "hostnode": D2H copies
         # + a graph host node (cudaLaunchHostFunc, ~250 us round trip per layer)
@@ -56,6 +57,8 @@ class HeteroEq5:
             self.job = self.worker.add_job(rows, self.k_max, vstore, kc.G, self.part_h)
         self.ev_sel = torch.cuda.Event()
         self.ev_host = torch.cuda.Event()
+        self.ev_staged = torch.cuda.Event()
+        self.stage_first = os.environ.get("HC_STAGE_FIRST", "1") != "0"
 
     def split_point(self, layer: int) -> int:
         return int(round(self.host_frac * self.kc.n_q(layer)))
@@ -79,6 +82,7 @@ class HeteroEq5:
                     B_, L_, Hkv_, ncap_, d_ = self.vs.tensor.shape
                     self.worker.submit(self.job, self.idx_d, self.w_d, sel_k, t_split,
                                        layer * Hkv_ * ncap_ * d_, stream=self.side)
+                    self.ev_staged.record(self.side)
                     self.worker.wait(self.job, stream=self.side)
                 else:
                     self.idx_h.copy_(self.idx_d, non_blocking=True)
@@ -87,6 +91,10 @@ class HeteroEq5:
                     hc.host_weighted_sum_range(self.idx_h, self.w_h, self.k_h, self.vs, layer, self.kc.G,
                                                0, t_split, self.part_h, self.threads, stream=self.side)
                 self.ev_host.record(self.side)
+        if host and self.mode == "doorbell" and self.stage_first:
+            # the GPU's pull starts once the host's lists are staged: side by side, the gather's
+            # grid and PCIe reads starve the staging kernel (0.26 -> 2.8 ms, tools/staging_timing.py)
+            main.wait_event(self.ev_staged)
         hc.gather_values(self.kc, self.vs, layer, self.idx_d, self.w_d, sel_k, t_split, n_cand, out, ws)
         if host:
             main.wait_event(self.ev_host)
