@@ -576,7 +576,7 @@ hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *s
   if (t_split < 0 || v_off < 0) return HC_ERR_RANGE;
   Job &jb = w->jobs[job];
   static int ctas = -1;  // rows in flight (unit-major order); HC_SUBMIT_CTAS dev override
-  if (ctas < 0) { const char *ev = getenv("HC_SUBMIT_CTAS"); ctas = ev ? atoi(ev) : 32; if (ctas < 1) ctas = 32; }
+  if (ctas < 0) { const char *ev = getenv("HC_SUBMIT_CTAS"); ctas = ev ? atoi(ev) : 64; if (ctas < 1) ctas = 64; }
   const unsigned grid = (unsigned)(jb.rows < ctas ? jb.rows : ctas);
   hc::k_submit<<<grid, 256, 0, (cudaStream_t)stream>>>(sel_idx, sel_w, sel_k, jb.k_stride, jb.rows, jb.G, t_split,
                                                    v_off, jb.idx_d, jb.w_d, jb.k_d, jb.mb_d, jb.ctr, jb.ready_d);
