@@ -172,9 +172,14 @@ int64_t lower_bound_i32(const int32_t *a, int64_t n, int64_t x) {
 
 void run(const HostArgs &a) {
   const Isa isa = detect_isa();
-  if (const char *ev = getenv("HC_HOST_PF")) g_pf = atoi(ev);
-  if (const char *ev = getenv("HC_HOST_HINT")) g_hint = atoi(ev);
-  if (const char *ev = getenv("HC_HOST_CHUNK")) { const long v = atol(ev); if (v >= 256) g_chunk = v; }
+  // dev overrides, read once (thread-safe static init; run() is called from several threads)
+  static const bool env_read = [] {
+    if (const char *ev = getenv("HC_HOST_PF")) g_pf = atoi(ev);
+    if (const char *ev = getenv("HC_HOST_HINT")) g_hint = atoi(ev);
+    if (const char *ev = getenv("HC_HOST_CHUNK")) { const long v = atol(ev); if (v >= 256) g_chunk = v; }
+    return true;
+  }();
+  (void)env_read;
   if (isa == kScalar) init_table();
   const int nt = a.threads > 0 ? a.threads : omp_get_max_threads();
   const int G = a.G, d = a.d;
