@@ -34,7 +34,7 @@ class HeteroEq5:
         self.kc, self.vs, self.k_max = kc, vstore, int(k_max)
         # default: all cores (the driving thread should wait on blocking-sync events, not spin)
         self.host_frac = float(host_frac)
-        self.threads = int(threads) if threads > 0 else (os.cpu_count() or 1)
+        self.threads = int(threads) if threads > 0 else int(os.environ.get("HC_HOST_THREADS", os.cpu_count() or 1))
         rows = kc.B * kc.Hq
         self.idx_d = torch.empty((rows, self.k_max), dtype=torch.int32, device=device)
         self.w_d = torch.empty((rows, self.k_max), dtype=torch.float32, device=device)
