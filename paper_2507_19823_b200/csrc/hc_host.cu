@@ -32,7 +32,7 @@ namespace {
 
 int64_t g_chunk = 4096;                // tokens per work item (HC_HOST_CHUNK)
 std::atomic<uint64_t> g_ready_wait_ns{0};  // HC_WORKER_STATS: thread-time spent waiting on staging
-int g_pf = 16;                        // kept rows prefetched ahead (HC_HOST_PF)
+int g_pf = 32;                        // kept rows prefetched ahead (HC_HOST_PF)
 int g_hint = 0;                       // 0: T0, 1: T1, 2: T2 (HC_HOST_HINT)
 
 float g_h2f[65536];
