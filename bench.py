@@ -719,7 +719,7 @@ def main():
         if cfg["placement"] != 1 or args.cpu_gather:
             raise SystemExit("--host-frac needs host-resident values (e.g. --config 3) and no --cpu-gather")
         cfg["workload"] += ("; heterogeneous Eq. 5: host threads sum the kept rows of the first "
-                            "{HOST_FRAC} of the tokens over host DRAM, the GPU pulls the rest zero-copy")
+                            "host_frac of the tokens over host DRAM, the GPU pulls the rest zero-copy")
         cfg["host_frac_auto"] = args.host_frac is None
     if args.code_bits == 13:
         cfg["workload"] += "; packed 13-bit codes (f3(ii))"
@@ -771,9 +771,6 @@ def main():
     wl = Workload(cfg, dev, rank if sharded_mode else 0, world if sharded_mode else 1)
     if cfg.get("host_frac_auto") and wl.hetero is not None and not wl.parts:
         calibrate_host_frac(wl, cfg)
-    if "{HOST_FRAC}" in cfg["workload"]:
-        cfg["workload"] = cfg["workload"].replace(
-            "{HOST_FRAC}", f"{cfg['host_frac']:.2f}" + (" (calibrated at start-up)" if cfg.get("host_frac_auto") else ""))
     if sharded_mode:
         from paper_2507_19823_b200.sharded import TorchComm
         wl.enable_sharding(TorchComm())
@@ -872,7 +869,10 @@ def main():
                                    ("replicas" if world > 1 else "single")),
                    "l2": f"inputs > L2: P = {B * L * H * n * g * 2 / 1e9:.2f} GB/step, V = "
                          f"{B * L * H * n * d * 2 / 1e9:.2f} GB",
-                   "graph": graph_mode},
+                   "graph": graph_mode,
+                   **({"host_frac": round(cfg["host_frac"], 2),
+                       "host_frac_from": "calibrated at start-up" if cfg.get("host_frac_auto") else "--host-frac"}
+                      if cfg["host_frac"] > 0.0 else {})},
         "quantized_key_gbs": achieved,
         "quantized_key_frac_hbm": achieved / peak,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
