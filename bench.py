@@ -597,7 +597,7 @@ def run_reference(args, cfg):
     v = 1.0 / step_s
     line = {"metric": METRIC, "value": v, "unit": "steps/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": ("strong" if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.config in (4, 5) else "weak"),
             "vs_baseline": None, "dtype": "i16+f32", "data": "synthetic",
             "config": {"workload": cfg["workload"], "reference": "CPU oracle (oracle/hc_oracle.c)"},
             "cpu_baseline": {"value": v, "unit": "steps/s", "cores": wave, "kind": "oracle",
