@@ -8,13 +8,17 @@ scan, softmax mass, Eq. 4 selection, Eq. 5 gather) for all B x 32 query heads.
 The step is captured once in a CUDA graph and replayed (steady state: the append
 rewrites position n-1, the decode covers n tokens).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|3|1] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
 
-N = 1 default workload: BASELINE config 2 (configs[1]): 32 layers, 8 KV heads x GQA 4,
-d = 128, 32K context, g = 64 (the 25 % budget), c = 8192, k_max = 8192, tau = 0.9,
-batch 1, values in HBM.  N > 1 (torchrun): independent replicas of the same step
-on each GPU (weak scaling) -- the sequence-sharded path is not built yet.
---impl reference times the CPU oracle (oracle/, plain C) as it stands.
+N = 1 default workload: BASELINE config 3 (configs[2], the metric's single-GPU "128K-4M ctx"
+configuration): 32 layers, 8 KV heads x GQA 4, d = 128, 128K context, g = 32 (the 12.5 %
+budget), c = 8192, k_max = 16384, tau = 0.9, batch 4, values in host pinned memory; Eq. 5
+runs heterogeneously (host threads + the GPU's zero-copy pull, share calibrated at start-up;
+--host-frac 0 = GPU only) and a `gpu_only` sub-record times the GPU-only pull too.
+N > 1 (torchrun): config 4 (1M context) sequence-sharded over the N ranks through the
+C-ABI sharded decode (NCCL collectives between the phase kernels), strong scaling;
+--config 5 (4M, host-resident values) needs >= 4 ranks, --config5-layers times one layer of
+it on one GPU.  --impl reference times the CPU oracle (oracle/, plain C) as it stands.
 """
 from __future__ import annotations
 
@@ -317,7 +321,7 @@ class Workload:
         st = hc.lib().hc_enqueue_host_weighted_sum(
             C.c_void_p(self.sel_i_h.data_ptr()), C.c_void_p(self.sel_w_h.data_ptr()),
             C.c_void_p(self.sel_k_h[l].data_ptr()), B * self.Hq, cfg["k_max"],
-            C.c_void_p(V.data_ptr()), L * H * ncap * d, ncap * d, self.Hq, cfg["G"], d,
+            C.c_void_p(V.data_ptr()), L * H * ncap * d, ncap * d, self.kc.n_q(l), self.Hq, cfg["G"], d,
             C.c_void_p(self.out_cpu[l].data_ptr()), 0, hc._stream())
         hc._check(st)
         self.out[l].view(-1, d).copy_(self.out_cpu[l], non_blocking=True)
@@ -461,7 +465,8 @@ def measure_host_rows_gbs(wl, reps: int = 3) -> dict:
     out = torch.empty_like(wl.out[0])
 
     def host(t0_, t1_):
-        hc.host_weighted_sum_range(het.idx_h, het.w_h, het.k_h, wl.vs, 0, G, t0_, t1_, het.part_h, het.threads)
+        hc.host_weighted_sum_range(het.idx_h, het.w_h, het.k_h, wl.vs, 0, G, t0_, t1_, het.part_h, het.threads,
+                                   n_valid=n)
 
     def gpu(t0_, t1_):
         hc.gather_values(wl.kc, wl.vs, 0, het.idx_d, het.w_d, sel_k, t0_, t1_, out, wl.ws)
@@ -803,6 +808,8 @@ def main():
     with ClockSampler(local) as clk:
         ms = time_graph(g_step, args.steps, args.warmup, dist)
     ms_per_step = ms / args.steps
+    if wl.hetero is not None:
+        wl.hetero.check()  # a timed-out host share would have poisoned the outputs: refuse the number
     for _ in range(3):  # the profiled twin of the timed graph; events of its last replay
         g_prof.replay()
     torch.cuda.synchronize()

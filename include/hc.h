@@ -254,18 +254,21 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
  *   of hc_decode_attention's selection with select_only = 1), row = b*Hq + hq;
  *   V: value store of ONE layer, fp16, row j of (b, kv = hq / G) at
  *      V + b*v_b_stride + kv*v_kv_stride + j*d  (elements);
+ *   n_valid: rows 0..n_valid-1 of every (b, kv) hold values (the layer's n_q); only kept
+ *      tokens j < n_valid are summed (resident-window tokens j >= n_q live in HBM: add them
+ *      with hc_gather_values(tok_begin = n_q));
  *   out [rows][d] fp32.
  * hc_host_weighted_sum runs synchronously; hc_enqueue_host_weighted_sum enqueues the same
  * work as a host node on `stream` (cudaLaunchHostFunc; graph-capturable), executing after
  * prior work on the stream (e.g. the D2H copies of idx / w / k). */
 hc_status hc_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
                                int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
-                               int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d, float *out,
-                               int32_t threads);
+                               int64_t v_kv_stride, int64_t n_valid, int32_t Hq, int32_t G, int32_t d,
+                               float *out, int32_t threads);
 hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k,
                                        int64_t rows, int64_t k_stride, const uint16_t *V,
-                                       int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
-                                       int32_t G, int32_t d, float *out, int32_t threads,
+                                       int64_t v_b_stride, int64_t v_kv_stride, int64_t n_valid,
+                                       int32_t Hq, int32_t G, int32_t d, float *out, int32_t threads,
                                        hc_stream_t stream);
 
 /* ---- Heterogeneous Eq. 5 (§3.2 "Heterogeneous Attention Computation"): the
@@ -281,16 +284,17 @@ hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const
  *   (KV unit, 4096-token chunk); the G heads of a unit run back to back over a chunk so
  *   shared rows come from the core's cache; chunk partials are added in chunk order (the
  *   result does not depend on `threads`).  F16C/AVX-512 or AVX2 when the CPU has them.
- *   HC_ERR_RANGE if tok_begin < 0 or tok_end < tok_begin. */
+ *   HC_ERR_RANGE if tok_begin < 0, tok_end < tok_begin or tok_end > n_valid. */
 hc_status hc_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
                                      int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
-                                     int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
+                                     int64_t v_kv_stride, int64_t n_valid, int32_t Hq, int32_t G, int32_t d,
                                      int64_t tok_begin, int64_t tok_end, float *out, int32_t threads);
 hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k,
                                              int64_t rows, int64_t k_stride, const uint16_t *V,
-                                             int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
-                                             int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end,
-                                             float *out, int32_t threads, hc_stream_t stream);
+                                             int64_t v_b_stride, int64_t v_kv_stride, int64_t n_valid,
+                                             int32_t Hq, int32_t G, int32_t d, int64_t tok_begin,
+                                             int64_t tok_end, float *out, int32_t threads,
+                                             hc_stream_t stream);
 
 /* Doorbell host worker: the host share of the split without graph host nodes (a
  * cudaLaunchHostFunc node costs ~250 us round trip; this path ~10 us).  A persistent host
@@ -303,10 +307,13 @@ hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w,
  *     DEVICE selection (sel_idx/sel_w [rows][k_stride] ascending, sel_k [rows]) into the
  *     job's staging, then rings the job's doorbell with {t_split, v_off}; the worker then
  *     computes out = Σ_{kept j < t_split} w_j V[v_off + ...]_j (v_off = element offset of
- *     the layer in V) exactly as hc_host_weighted_sum_range(tok 0..t_split);
- *   hc_host_worker_wait: a one-thread kernel that returns once the job's last submission is
- *     done (so later work on the stream sees out), or after timeout_s seconds, when the
- *     job is marked failed: hc_host_worker_status then returns HC_ERR_CUDA.
+ *     the layer in V) exactly as hc_host_weighted_sum_range(tok 0..t_split); n_valid = the
+ *     layer's n_q (HC_ERR_RANGE if t_split > n_valid: window tokens are not in the host store);
+ *   hc_host_worker_wait: a kernel that returns once the job's last submission is done (so
+ *     later work on the stream sees out), or after timeout_s seconds, when the job is marked
+ *     failed (hc_host_worker_status then returns HC_ERR_CUDA) and `out` is filled with NaN
+ *     (if it is mapped pinned memory) so no consumer can take a stale share for a result;
+ *     a result the worker finishes after a newer submission arrived is discarded.
  * Submissions of one job must not overlap (wait before the next submit).  add_job returns
  * HC_ERR_CAPACITY beyond max_jobs; create / add_job / destroy are setup calls for one
  * thread (the worker itself only reads jobs that add_job has published).  destroy stops the
@@ -318,7 +325,8 @@ hc_status hc_host_worker_add_job(hc_host_worker *w, int64_t rows, int64_t k_stri
                                  int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
                                  float *out, int32_t *job);
 hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *sel_idx, const float *sel_w,
-                                const int64_t *sel_k, int64_t t_split, int64_t v_off, hc_stream_t stream);
+                                const int64_t *sel_k, int64_t t_split, int64_t n_valid, int64_t v_off,
+                                hc_stream_t stream);
 hc_status hc_host_worker_wait(hc_host_worker *w, int32_t job, hc_stream_t stream);
 hc_status hc_host_worker_status(hc_host_worker *w);
 /* Maintenance / test hook: paused != 0 stops serving doorbells (pending waits then time out). */

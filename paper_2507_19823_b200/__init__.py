@@ -99,12 +99,12 @@ def lib():
         L.hc_select_workspace_bytes.restype = C.c_size_t
         L.hc_select_topk.argtypes = [p, i64, i64, i32, hc_budget, p, p, p, p, C.c_size_t, p]
         L.hc_select_topk.restype = i32
-        hw = [p, p, p, i64, i64, p, i64, i64, i32, i32, i32, p, i32]
+        hw = [p, p, p, i64, i64, p, i64, i64, i64, i32, i32, i32, p, i32]
         L.hc_host_weighted_sum.argtypes = hw
         L.hc_host_weighted_sum.restype = i32
         L.hc_enqueue_host_weighted_sum.argtypes = hw + [p]
         L.hc_enqueue_host_weighted_sum.restype = i32
-        hr = [p, p, p, i64, i64, p, i64, i64, i32, i32, i32, i64, i64, p, i32]
+        hr = [p, p, p, i64, i64, p, i64, i64, i64, i32, i32, i32, i64, i64, p, i32]
         L.hc_host_weighted_sum_range.argtypes = hr
         L.hc_host_weighted_sum_range.restype = i32
         L.hc_enqueue_host_weighted_sum_range.argtypes = hr + [p]
@@ -121,7 +121,7 @@ def lib():
         L.hc_host_worker_create.argtypes = [i32, i32, C.c_double, C.POINTER(C.c_void_p)]
         L.hc_host_worker_destroy.argtypes = [p]
         L.hc_host_worker_add_job.argtypes = [p, i64, i64, p, i64, i64, i32, i32, i32, p, C.POINTER(i32)]
-        L.hc_host_worker_submit.argtypes = [p, i32, p, p, p, i64, i64, p]
+        L.hc_host_worker_submit.argtypes = [p, i32, p, p, p, i64, i64, i64, p]
         L.hc_host_worker_wait.argtypes = [p, i32, p]
         L.hc_host_worker_status.argtypes = [p]
         L.hc_host_worker_pause.argtypes = [p, i32]
@@ -550,15 +550,16 @@ def add_partial(out, part, stream=None):
 
 
 def host_weighted_sum_range(idx, w, k, vstore: VStore, layer: int, G: int, tok_begin: int, tok_end: int,
-                            out, threads: int = 0, stream=None):
+                            out, threads: int = 0, stream=None, *, n_valid: int):
     """hc_(enqueue_)host_weighted_sum_range on HOST tensors: idx/w [rows][k_stride], k [rows],
-    out [rows][d]; V = the pinned value store's layer.  stream=None runs synchronously, else
-    the work is enqueued as a host node on `stream` (graph-capturable)."""
+    out [rows][d]; V = the pinned value store's layer, rows [0, n_valid) valid (the layer's
+    n_q; tok_end > n_valid raises HC_ERR_RANGE).  stream=None runs synchronously, else the work
+    is enqueued as a host node on `stream` (graph-capturable)."""
     B, L, Hkv, n_cap, d = vstore.tensor.shape
     V = vstore.tensor[0, layer]
     rows, ks = idx.shape
-    args = [_ptr(idx), _ptr(w), _ptr(k), rows, ks, _ptr(V), L * Hkv * n_cap * d, n_cap * d, Hkv * G, G, d,
-            int(tok_begin), int(tok_end), _ptr(out), int(threads)]
+    args = [_ptr(idx), _ptr(w), _ptr(k), rows, ks, _ptr(V), L * Hkv * n_cap * d, n_cap * d, int(n_valid),
+            Hkv * G, G, d, int(tok_begin), int(tok_end), _ptr(out), int(threads)]
     if stream is None:
         _check(lib().hc_host_weighted_sum_range(*args))
     else:
@@ -583,9 +584,11 @@ class HostWorker:
                                             _ptr(out), C.byref(j)))
         return int(j.value)
 
-    def submit(self, job: int, sel_idx, sel_w, sel_k, t_split: int, v_off: int, stream=None):
+    def submit(self, job: int, sel_idx, sel_w, sel_k, t_split: int, v_off: int, stream=None, *,
+               n_valid: int):
+        """n_valid = the layer's n_q (t_split > n_valid raises HC_ERR_RANGE)."""
         _check(lib().hc_host_worker_submit(self.h, job, _ptr(sel_idx), _ptr(sel_w), _ptr(sel_k),
-                                           int(t_split), int(v_off), _stream(stream)))
+                                           int(t_split), int(n_valid), int(v_off), _stream(stream)))
 
     def wait(self, job: int, stream=None):
         _check(lib().hc_host_worker_wait(self.h, job, _stream(stream)))

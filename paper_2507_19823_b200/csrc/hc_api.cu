@@ -604,8 +604,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
       return cuda_check(e, "shared select");
   } else if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
                                       (budget.select_only || union_gather || rows_gather) ? 0 : 1,
-                                      a.num_sms, s,
-                                      dbg && dbg->z ? 1 : 0)) != cudaSuccess)
+                                      a.num_sms, s)) != cudaSuccess)
     return cuda_check(e, "select");
   if (rows_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);

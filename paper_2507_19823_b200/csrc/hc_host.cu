@@ -254,10 +254,13 @@ void CUDART_CB host_cb(void *p) {
 }
 
 hc_status check(const int32_t *idx, const float *w, const int64_t *k, const uint16_t *V, float *out,
-                int64_t rows, int32_t Hq, int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end) {
+                int64_t rows, int32_t Hq, int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end,
+                int64_t n_valid) {
   if (!idx || !w || !k || !V || !out) return HC_ERR_ARG;
   if (rows < 0 || Hq <= 0 || G <= 0 || d <= 0 || d > 256 || Hq % G || rows % G) return HC_ERR_SHAPE;
-  if (tok_begin < 0 || tok_end < tok_begin) return HC_ERR_RANGE;
+  // only rows [0, n_valid) of each (b, kv) exist in the host store: a range past it would
+  // read beyond the layer's values (or the resident window's tokens, which live in HBM)
+  if (tok_begin < 0 || tok_end < tok_begin || n_valid < 0 || tok_end > n_valid) return HC_ERR_RANGE;
   return HC_OK;
 }
 
@@ -301,6 +304,7 @@ struct Job {
   int64_t v_b_stride, v_kv_stride;
   int32_t Hq, G, d;
   float *out;          // host
+  float *out_d;        // device alias of out (pinned mapped), or null: poisoned by k_wait on timeout
   int32_t *idx_h;      // staging (pinned mapped) [rows][k_stride]
   float *w_h;
   int64_t *k_h;        // [rows]
@@ -391,15 +395,26 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
-__global__ void k_wait(Mailbox *mb, uint64_t timeout_ns) {
-  if (threadIdx.x != 0) return;
-  const uint32_t want = mb->req;
-  const uint64_t t0 = gtimer();
-  while (mb->done != want) {
-    __nanosleep(1000);
-    if (gtimer() - t0 > timeout_ns) { mb->err = 1u; break; }
+// On timeout the job is marked failed (hc_host_worker_status -> HC_ERR_CUDA) AND its output
+// is poisoned with NaN, so a consumer that runs anyway (hc_add_partial) cannot pass a stale
+// or half-written host share off as a result.
+__global__ void k_wait(Mailbox *mb, uint64_t timeout_ns, float *out, int64_t n_out) {
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) {
+    const uint32_t want = mb->req;
+    const uint64_t t0 = gtimer();
+    s_fail = 0;
+    while (mb->done != want) {
+      __nanosleep(1000);
+      if (gtimer() - t0 > timeout_ns) { mb->err = 1u; s_fail = 1; break; }
+    }
+    __threadfence_system();
   }
-  __threadfence_system();
+  __syncthreads();
+  if (s_fail && out) {
+    for (int64_t i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = __int_as_float(0x7fc00000);
+    __threadfence_system();
+  }
 }
 
 }  // namespace hc
@@ -439,6 +454,12 @@ void worker_loop(hc_host_worker *w) {
       const auto t0 = std::chrono::steady_clock::now();
       run(a);
       jb.seen = r;
+      // a submission that arrived while this one ran can only follow a timed-out wait (the
+      // stream waits for `done` before the next submit): its staging was overwritten under
+      // the engine, so this result is stale -- do not publish it; the next poll serves the
+      // new request (the timed-out wait already marked the job failed and poisoned `out`)
+      std::atomic_thread_fence(std::memory_order_acquire);
+      if (jb.mb_h->req != r) continue;
       std::atomic_thread_fence(std::memory_order_release);
       jb.mb_h->done = r;
       if (w->stats) {
@@ -462,9 +483,9 @@ extern "C" {
 
 hc_status hc_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
                                      int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
-                                     int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d,
+                                     int64_t v_kv_stride, int64_t n_valid, int32_t Hq, int32_t G, int32_t d,
                                      int64_t tok_begin, int64_t tok_end, float *out, int32_t threads) {
-  hc_status st = check(idx, w, k, V, out, rows, Hq, G, d, tok_begin, tok_end);
+  hc_status st = check(idx, w, k, V, out, rows, Hq, G, d, tok_begin, tok_end, n_valid);
   if (st) return st;
   HostArgs a{idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, out, threads,
              tok_begin, tok_end, false};
@@ -474,10 +495,11 @@ hc_status hc_host_weighted_sum_range(const int32_t *idx, const float *w, const i
 
 hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w, const int64_t *k,
                                              int64_t rows, int64_t k_stride, const uint16_t *V,
-                                             int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
-                                             int32_t G, int32_t d, int64_t tok_begin, int64_t tok_end,
-                                             float *out, int32_t threads, hc_stream_t stream) {
-  hc_status st = check(idx, w, k, V, out, rows, Hq, G, d, tok_begin, tok_end);
+                                             int64_t v_b_stride, int64_t v_kv_stride, int64_t n_valid,
+                                             int32_t Hq, int32_t G, int32_t d, int64_t tok_begin,
+                                             int64_t tok_end, float *out, int32_t threads,
+                                             hc_stream_t stream) {
+  hc_status st = check(idx, w, k, V, out, rows, Hq, G, d, tok_begin, tok_end, n_valid);
   if (st) return st;
   return enqueue(HostArgs{idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, out, threads,
                           tok_begin, tok_end, false},
@@ -486,19 +508,19 @@ hc_status hc_enqueue_host_weighted_sum_range(const int32_t *idx, const float *w,
 
 hc_status hc_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k, int64_t rows,
                                int64_t k_stride, const uint16_t *V, int64_t v_b_stride,
-                               int64_t v_kv_stride, int32_t Hq, int32_t G, int32_t d, float *out,
-                               int32_t threads) {
-  return hc_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G, d, 0,
-                                    (int64_t)INT32_MAX + 1, out, threads);
+                               int64_t v_kv_stride, int64_t n_valid, int32_t Hq, int32_t G, int32_t d,
+                               float *out, int32_t threads) {
+  return hc_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, n_valid, Hq, G,
+                                    d, 0, n_valid, out, threads);
 }
 
 hc_status hc_enqueue_host_weighted_sum(const int32_t *idx, const float *w, const int64_t *k,
                                        int64_t rows, int64_t k_stride, const uint16_t *V,
-                                       int64_t v_b_stride, int64_t v_kv_stride, int32_t Hq,
-                                       int32_t G, int32_t d, float *out, int32_t threads,
+                                       int64_t v_b_stride, int64_t v_kv_stride, int64_t n_valid,
+                                       int32_t Hq, int32_t G, int32_t d, float *out, int32_t threads,
                                        hc_stream_t stream) {
-  return hc_enqueue_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, Hq, G,
-                                            d, 0, (int64_t)INT32_MAX + 1, out, threads, stream);
+  return hc_enqueue_host_weighted_sum_range(idx, w, k, rows, k_stride, V, v_b_stride, v_kv_stride, n_valid,
+                                            Hq, G, d, 0, n_valid, out, threads, stream);
 }
 
 hc_status hc_host_worker_create(int32_t threads, int32_t max_jobs, double timeout_s, hc_host_worker **out) {
@@ -567,6 +589,10 @@ hc_status hc_host_worker_add_job(hc_host_worker *w, int64_t rows, int64_t k_stri
          cudaHostGetDevicePointer((void **)&jb.ready_d, jb.ready_h, 0) == cudaSuccess;
   }
   if (!ok) return HC_ERR_CUDA;
+  if (cudaHostGetDevicePointer((void **)&jb.out_d, out, 0) != cudaSuccess) {
+    jb.out_d = nullptr;  // out not mapped: the timeout still sets the error flag
+    cudaGetLastError();
+  }
   jb.seen = 0;
   w->jobs[j] = jb;
   w->njobs.store(j + 1, std::memory_order_release);
@@ -575,10 +601,11 @@ hc_status hc_host_worker_add_job(hc_host_worker *w, int64_t rows, int64_t k_stri
 }
 
 hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *sel_idx, const float *sel_w,
-                                const int64_t *sel_k, int64_t t_split, int64_t v_off, hc_stream_t stream) {
+                                const int64_t *sel_k, int64_t t_split, int64_t n_valid, int64_t v_off,
+                                hc_stream_t stream) {
   if (!w || !sel_idx || !sel_w || !sel_k) return HC_ERR_ARG;
   if (job < 0 || job >= w->njobs.load()) return HC_ERR_RANGE;
-  if (t_split < 0 || v_off < 0) return HC_ERR_RANGE;
+  if (t_split < 0 || v_off < 0 || n_valid < 0 || t_split > n_valid) return HC_ERR_RANGE;
   Job &jb = w->jobs[job];
   static int ctas = -1;  // rows in flight (unit-major order); HC_SUBMIT_CTAS dev override
   if (ctas < 0) { const char *ev = getenv("HC_SUBMIT_CTAS"); ctas = ev ? atoi(ev) : 64; if (ctas < 1) ctas = 64; }
@@ -592,7 +619,8 @@ hc_status hc_host_worker_submit(hc_host_worker *w, int32_t job, const int32_t *s
 hc_status hc_host_worker_wait(hc_host_worker *w, int32_t job, hc_stream_t stream) {
   if (!w) return HC_ERR_ARG;
   if (job < 0 || job >= w->njobs.load()) return HC_ERR_RANGE;
-  hc::k_wait<<<1, 32, 0, (cudaStream_t)stream>>>(w->jobs[job].mb_d, w->timeout_ns);
+  const Job &jb = w->jobs[job];
+  hc::k_wait<<<1, 256, 0, (cudaStream_t)stream>>>(jb.mb_d, w->timeout_ns, jb.out_d, jb.rows * jb.d);
   hc::note_launch();
   return cudaGetLastError() == cudaSuccess ? HC_OK : HC_ERR_CUDA;
 }

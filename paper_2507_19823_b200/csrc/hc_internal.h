@@ -176,7 +176,7 @@ struct SelArgs {
 };
 // fused rows a3-a5 (one cluster of CTAs per row); nsplit: scan partial planes in la.zpart
 cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
-                                int num_sms, cudaStream_t st, int zstore = 0);
+                                int num_sms, cudaStream_t st);
 
 // sequence-sharded phases (hc_shard.cu)
 int shard_chunks(int64_t n);

@@ -218,144 +218,9 @@ __device__ __forceinline__ void fold_minmax(const LayerArgs &a, int b, int kv, c
   }
 }
 
-// RC = 1: the code strips go straight to registers (16-B L1-bypassing loads, two groups
-// ahead) instead of through a shared-memory ring -- saves 4 of the ~37 shared-memory bytes
-// per (token, group) the scan moves.
-template <int G, int TPT, int RC>
-__global__ void __launch_bounds__(kScanThreads, 1) k_scan(LayerArgs a, int tiles_per_unit,
-                                                           int total_tiles, int nsplit) {
-  static_assert(TPT == 8 || TPT == 16, "TPT");
-  constexpr int kChunks = TPT / 8;                     // 8-token chunks per thread
-  constexpr int kTile = kScanThreads * TPT;            // tokens per tile
-  constexpr uint32_t kCodeBytes = kTile * 2;           // one group's code strip of a tile
-  extern __shared__ __align__(128) uint8_t smem[];
-  // shared memory: T ring [2][slice] | code ring [3][kCodeBytes] | mbarriers tb[2], cb[3]
-  const uint32_t slice_bytes = (uint32_t)a.cpow2 * G * 2;
-  uint8_t *tbuf = smem;
-  uint8_t *cbuf = smem + 2 * slice_bytes;
-  uint64_t *tb = reinterpret_cast<uint64_t *>(cbuf + 3 * kCodeBytes);
-  uint64_t *cb = tb + 2;
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < 2; ++j) mbar_init(&tb[j], 1);
-    for (int j = 0; j < 3; ++j) mbar_init(&cb[j], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_trigger();
-  __syncthreads();
-  pdl_wait();
-  uint32_t tph = 0, cph = 0;  // phase bit per barrier
-  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << Lut<G>::kShift;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gper = (a.g + nsplit - 1) / nsplit;
-
-  for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
-    const int sp = item % nsplit;
-    const int tile = item / nsplit;
-    const int u = tile / tiles_per_unit;
-    const int tk = tile - u * tiles_per_unit;
-    const int i0 = sp * gper;
-    const int i1 = min(a.g, i0 + gper);
-    const int ng = i1 - i0;
-    const int b = u / a.Hkv, kv = u - b * a.Hkv;
-    const int64_t tile0 = (int64_t)tk * kTile;
-    // bytes of this tile's code strip that exist in the [n_cap] strip (multiple of 16)
-    const int64_t avail = a.n_cap - tile0;
-    const uint32_t cbytes = (uint32_t)(avail < kTile ? avail : kTile) * 2;
-    const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride +
-                        ((int64_t)kv * a.g + i0) * a.n_cap + tile0;
-    const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      for (int j = 0; j < 2 && j < ng; ++j) {
-        mbar_expect_tx(&tb[j], slice_bytes);
-        bulk_g2s(tbuf + j * slice_bytes, Tu + (int64_t)j * slice_bytes, slice_bytes, &tb[j]);
-      }
-      if (!RC) {
-        for (int j = 0; j < 3 && j < ng; ++j) {
-          mbar_expect_tx(&cb[j], cbytes);
-          bulk_g2s(cbuf + j * kCodeBytes, P + (int64_t)j * a.n_cap, cbytes, &cb[j]);
-        }
-      }
-    }
-    const int woff = warp * (32 * TPT);  // this warp's first token inside the tile
-    // register code ring (RC): group i in rc0, i+1 in rc1
-    uint4 rc0[kChunks], rc1[kChunks];
-    bool cval[kChunks];
-    if (RC) {
-#pragma unroll
-      for (int k = 0; k < kChunks; ++k) {
-        cval[k] = tile0 + woff + k * 256 + lane * 8 < a.n_q;
-        const uint16_t *pk = P + woff + k * 256 + lane * 8;
-        rc0[k] = cval[k] ? ld_stream(pk) : make_uint4(0, 0, 0, 0);
-        rc1[k] = (cval[k] && ng > 1) ? ld_stream(pk + a.n_cap) : make_uint4(0, 0, 0, 0);
-      }
-    }
-    int acc[kChunks][8][G];
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k)
-#pragma unroll
-      for (int u8 = 0; u8 < 8; ++u8)
-#pragma unroll
-        for (int h = 0; h < G; ++h) acc[k][u8][h] = 0;
-
-    int ci = 0;  // code ring slot of group i (i % 3)
-    for (int i = 0; i < ng; ++i) {
-      const int ti = i & 1;
-      uint4 rc2[kChunks];
-      if (RC) {  // prefetch group i+2
-#pragma unroll
-        for (int k = 0; k < kChunks; ++k)
-          rc2[k] = (cval[k] && i + 2 < ng)
-                       ? ld_stream(P + (int64_t)(i + 2) * a.n_cap + woff + k * 256 + lane * 8)
-                       : make_uint4(0, 0, 0, 0);
-      } else {
-        mbar_wait(&cb[ci], (cph >> ci) & 1u);
-        cph ^= 1u << ci;
-      }
-      mbar_wait(&tb[ti], (tph >> ti) & 1u);
-      tph ^= 1u << ti;
-      const uint8_t *sb = tbuf + ti * slice_bytes;
-      const uint8_t *cs = cbuf + ci * kCodeBytes + (size_t)woff * 2;
-#pragma unroll
-      for (int k = 0; k < kChunks; ++k) {
-        const uint4 c = RC ? rc0[k] : *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
-        lookup8<G>(c, sb, mask, acc[k]);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (i + 2 < ng) {
-          mbar_expect_tx(&tb[ti], slice_bytes);
-          bulk_g2s(tbuf + ti * slice_bytes, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, &tb[ti]);
-        }
-        if (!RC && i + 3 < ng) {
-          mbar_expect_tx(&cb[ci], cbytes);
-          bulk_g2s(cbuf + ci * kCodeBytes, P + (int64_t)(i + 3) * a.n_cap, cbytes, &cb[ci]);
-        }
-      }
-      if (RC) {
-#pragma unroll
-        for (int k = 0; k < kChunks; ++k) { rc0[k] = rc1[k]; rc1[k] = rc2[k]; }
-      }
-      ci = ci == 2 ? 0 : ci + 1;
-    }
-    int mx[G], mn[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
-    float *zbase = a.z;
-    const bool zadd = nsplit > 1;
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k) {
-      unbias<G>(acc[k], ng);
-      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc[k], mx, mn, zadd);
-    }
-    if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
-  }
-}
-
 // ---------------------------------------------------------------------------------------
-// Cross-tile pipelined variant of k_scan<G, TPT, RC = 1> (the default).  The CTA's work is
-// one stream of (item, group) steps:
+// Pipelined scan (used when the stream-K split does not apply: short rows, group splits,
+// packed codes).  The CTA's work is one stream of (item, group) steps:
 //  * table slices live in a 3-slot ring filled by bulk copies (TMA engine) on "full"
 //    mbarriers; there is NO CTA-wide barrier per group: each warp, after its lookups in
 //    slot s%3, bumps a shared counter, and the LAST warp to finish the slot refills it
@@ -742,124 +607,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_sk(LayerArgs a, int ti
 // (w >> 8) & 0x00FF00FF (heads 1, 3), 16-bit fields never overflow for g <= 257, and
 // z_h = field - 128*ng exactly.  Two registers per token let a thread own 32 tokens
 // (tile = 16384 tokens), which halves the table-slice ingress per token.
-template <int TPT>
-__global__ void __launch_bounds__(kScanThreads, 1) k_scan8(LayerArgs a, int tiles_per_unit,
-                                                            int total_tiles, int nsplit) {
-  constexpr int G = 4;
-  constexpr int kChunks = TPT / 8;
-  constexpr int kTile = kScanThreads * TPT;
-  constexpr uint32_t kCodeBytes = kTile * 2;
-  extern __shared__ __align__(128) uint8_t smem[];
-  const uint32_t slice_bytes = (uint32_t)a.cpow2 * 4;
-  uint8_t *tbuf = smem;
-  uint8_t *cbuf = smem + 2 * slice_bytes;
-  uint64_t *tb = reinterpret_cast<uint64_t *>(cbuf + 3 * kCodeBytes);
-  uint64_t *cb = tb + 2;
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < 2; ++j) mbar_init(&tb[j], 1);
-    for (int j = 0; j < 3; ++j) mbar_init(&cb[j], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_trigger();
-  __syncthreads();
-  pdl_wait();
-  uint32_t tph = 0, cph = 0;
-  const uint32_t mask = (uint32_t)(a.cpow2 - 1) << 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gper = (a.g + nsplit - 1) / nsplit;
-
-  for (int item = blockIdx.x; item < total_tiles; item += gridDim.x) {
-    const int sp = item % nsplit;
-    const int tile = item / nsplit;
-    const int u = tile / tiles_per_unit;
-    const int tk = tile - u * tiles_per_unit;
-    const int i0 = sp * gper;
-    const int i1 = min(a.g, i0 + gper);
-    const int ng = i1 - i0;
-    const int b = u / a.Hkv, kv = u - b * a.Hkv;
-    const int64_t tile0 = (int64_t)tk * kTile;
-    const int64_t avail = a.n_cap - tile0;
-    const uint32_t cbytes = (uint32_t)(avail < kTile ? avail : kTile) * 2;
-    const uint16_t *P = a.codes + (int64_t)b * a.code_b_stride +
-                        ((int64_t)kv * a.g + i0) * a.n_cap + tile0;
-    const uint8_t *Tu = reinterpret_cast<const uint8_t *>(a.T) + ((int64_t)u * a.g + i0) * slice_bytes;
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      for (int j = 0; j < 2 && j < ng; ++j) {
-        mbar_expect_tx(&tb[j], slice_bytes);
-        bulk_g2s(tbuf + j * slice_bytes, Tu + (int64_t)j * slice_bytes, slice_bytes, &tb[j]);
-      }
-      for (int j = 0; j < 3 && j < ng; ++j) {
-        mbar_expect_tx(&cb[j], cbytes);
-        bulk_g2s(cbuf + j * kCodeBytes, P + (int64_t)j * a.n_cap, cbytes, &cb[j]);
-      }
-    }
-    const int woff = warp * (32 * TPT);
-    uint32_t ae[kChunks][8], ao[kChunks][8];
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k)
-#pragma unroll
-      for (int t = 0; t < 8; ++t) { ae[k][t] = 0u; ao[k][t] = 0u; }
-    int ci = 0;
-    for (int i = 0; i < ng; ++i) {
-      const int ti = i & 1;
-      mbar_wait(&cb[ci], (cph >> ci) & 1u);
-      cph ^= 1u << ci;
-      mbar_wait(&tb[ti], (tph >> ti) & 1u);
-      tph ^= 1u << ti;
-      const uint8_t *sb = tbuf + ti * slice_bytes;
-      const uint8_t *cs = cbuf + ci * kCodeBytes + (size_t)woff * 2;
-#pragma unroll
-      for (int k = 0; k < kChunks; ++k) {
-        const uint4 c = *reinterpret_cast<const uint4 *>(cs + (k * 256 + lane * 8) * 2);
-        const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t e0 = *reinterpret_cast<const uint32_t *>(sb + ((w4[q] << 2) & mask));
-          const uint32_t e1 = *reinterpret_cast<const uint32_t *>(sb + ((w4[q] >> 14) & mask));
-          ae[k][2 * q] += e0 & 0x00FF00FFu;
-          ao[k][2 * q] += (e0 >> 8) & 0x00FF00FFu;
-          ae[k][2 * q + 1] += e1 & 0x00FF00FFu;
-          ao[k][2 * q + 1] += (e1 >> 8) & 0x00FF00FFu;
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (i + 2 < ng) {
-          mbar_expect_tx(&tb[ti], slice_bytes);
-          bulk_g2s(tbuf + ti * slice_bytes, Tu + (int64_t)(i + 2) * slice_bytes, slice_bytes, &tb[ti]);
-        }
-        if (i + 3 < ng) {
-          mbar_expect_tx(&cb[ci], cbytes);
-          bulk_g2s(cbuf + ci * kCodeBytes, P + (int64_t)(i + 3) * a.n_cap, cbytes, &cb[ci]);
-        }
-      }
-      ci = ci == 2 ? 0 : ci + 1;
-    }
-    const int bias = 128 * ng;
-    int mx[G], mn[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) { mx[h] = INT_MIN; mn[h] = INT_MAX; }
-    float *zbase = a.z;
-    const bool zadd = nsplit > 1;
-#pragma unroll
-    for (int k = 0; k < kChunks; ++k) {
-      int acc[8][G];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        acc[t][0] = (int)(ae[k][t] & 0xffffu) - bias;
-        acc[t][2] = (int)(ae[k][t] >> 16) - bias;
-        acc[t][1] = (int)(ao[k][t] & 0xffffu) - bias;
-        acc[t][3] = (int)(ao[k][t] >> 16) - bias;
-      }
-      store_chunk<G>(a, zbase, b, kv, tile0 + woff + k * 256 + lane * 8, acc, mx, mn, zadd);
-    }
-    if (nsplit == 1) fold_minmax<G>(a, b, kv, mx, mn);
-  }
-}
-
-// Pipelined 8-bit variant (same scheme as k_scan_pipe): a 3-slot ring of (table slice,
+// Same pipeline as k_scan_pipe: a 3-slot ring of (table slice,
 // code strip) pairs filled by bulk copies on one "full" mbarrier per slot, released by the
 // last warp out, prefetch across item boundaries.
 template <int TPT>
@@ -1001,18 +749,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan8_pipe(LayerArgs a, int
   }
 }
 
-template <int G, int TPT, int RC>
-static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s);
-
-static int scan_pipelined() {
-  static int v = -1;
-  if (v < 0) {
-    const char *ev = getenv("HC_SCAN_PIPE");
-    v = (ev && !strcmp(ev, "0")) ? 0 : 1;
-  }
-  return v;
-}
-
 template <int G, int TPT, bool P13>
 static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   constexpr int kTile = kScanThreads * TPT;
@@ -1042,46 +778,6 @@ static cudaError_t scan_pipe_launch(const LayerArgs &a, cudaStream_t s) {
   note_launch();
   if (ee) cudaEventRecordWithFlags(ee, s, evflag);
   return cudaGetLastError();
-}
-
-template <int G, int TPT, int RC>
-static cudaError_t scan_launch(const LayerArgs &a, cudaStream_t s) {
-  constexpr int kTile = kScanThreads * TPT;
-  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
-  const int units = a.B * a.Hkv;
-  const int nsplit = a.scan_split;
-  const int total = tiles_per_unit * units * nsplit;
-  if (total == 0) return cudaSuccess;
-  const size_t smem = (size_t)2 * a.cpow2 * G * 2 + 3 * (size_t)kTile * 2 + 5 * 8;
-  static int configured[64] = {0};  // per device: opt in to the full 227 KB once
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<G, TPT, RC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured[dev] = 1;
-  }
-  const int grid = total < a.num_sms ? total : a.num_sms;
-  cudaEvent_t eb, ee;
-  scan_events(&eb, &ee);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cap);
-  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
-  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  launch_chain(k_scan<G, TPT, RC>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
-  note_launch();
-  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
-  return cudaGetLastError();
-}
-
-static int scan_codes_in_regs() {
-  static int v = -1;
-  if (v < 0) {
-    const char *ev = getenv("HC_SCAN_CODES");
-    v = (ev && !strcmp(ev, "smem")) ? 0 : 1;
-  }
-  return v;
 }
 
 static int scan_streamk() {
@@ -1128,48 +824,13 @@ static bool scan_sk_launch(const LayerArgs &a, cudaStream_t s, cudaError_t *err)
 
 template <int G>
 static cudaError_t scan_g(const LayerArgs &a, cudaStream_t s) {
-  const int rc = scan_codes_in_regs();
-  if (!a.pcodes && rc && scan_pipelined() && scan_streamk() && a.scan_split == 1) {
+  if (!a.pcodes && scan_streamk() && a.scan_split == 1) {
     cudaError_t e = cudaSuccess;
     if (a.scan_tpt == 8 ? scan_sk_launch<G, 8>(a, s, &e) : scan_sk_launch<G, 16>(a, s, &e)) return e;
   }
-  if (a.pcodes)  // packed 13-bit codes: pipelined kernel only
+  if (a.pcodes)  // packed 13-bit codes
     return a.scan_tpt == 8 ? scan_pipe_launch<G, 8, true>(a, s) : scan_pipe_launch<G, 16, true>(a, s);
-  if (rc && scan_pipelined())
-    return a.scan_tpt == 8 ? scan_pipe_launch<G, 8, false>(a, s) : scan_pipe_launch<G, 16, false>(a, s);
-  if (a.scan_tpt == 8) return rc ? scan_launch<G, 8, 1>(a, s) : scan_launch<G, 8, 0>(a, s);
-  return rc ? scan_launch<G, 16, 1>(a, s) : scan_launch<G, 16, 0>(a, s);
-}
-
-static cudaError_t scan8_launch(const LayerArgs &a, cudaStream_t s) {
-  constexpr int TPT = 32;
-  constexpr int kTile = kScanThreads * TPT;
-  const int tiles_per_unit = (int)((a.n_q + kTile - 1) / kTile);
-  const int units = a.B * a.Hkv;
-  const int nsplit = a.scan_split;
-  const int total = tiles_per_unit * units * nsplit;
-  if (total == 0) return cudaSuccess;
-  const size_t smem = (size_t)2 * a.cpow2 * 4 + 3 * (size_t)kTile * 2 + 5 * 8;
-  static int configured[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan8<TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured[dev] = 1;
-  }
-  const int grid = total < a.num_sms ? total : a.num_sms;
-  cudaEvent_t eb, ee;
-  scan_events(&eb, &ee);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cap);
-  const unsigned evflag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
-  if (eb) cudaEventRecordWithFlags(eb, s, evflag);
-  launch_chain(k_scan8<TPT>, dim3(grid), dim3(kScanThreads), smem, s, a, tiles_per_unit, total, nsplit);
-  note_launch();
-  if (ee) cudaEventRecordWithFlags(ee, s, evflag);
-  return cudaGetLastError();
+  return a.scan_tpt == 8 ? scan_pipe_launch<G, 8, false>(a, s) : scan_pipe_launch<G, 16, false>(a, s);
 }
 
 static cudaError_t scan8_pipe_launch(const LayerArgs &a, cudaStream_t s) {
@@ -1204,7 +865,7 @@ static cudaError_t scan8_pipe_launch(const LayerArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_scan(const LayerArgs &a, cudaStream_t s) {
-  if (a.lut8) return scan_pipelined() ? scan8_pipe_launch(a, s) : scan8_launch(a, s);
+  if (a.lut8) return scan8_pipe_launch(a, s);
   switch (a.G) {
     case 1: return scan_g<1>(a, s);
     case 2: return scan_g<2>(a, s);

@@ -132,7 +132,7 @@ __device__ __forceinline__ uint4 ld_nc16(const uint16_t *p) {
 template <bool kG, int kOcc>
 __global__ void __launch_bounds__(kFT, kOcc)
     k_select_fused(SelArgs s, LayerArgs la, int cs, int nsplit, int zcache, int do_gather,
-                   int zstore, int stop) {
+                   int stop) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int row = blockIdx.x / cs;
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kFT, kOcc)
 }
 
 cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
-                                int num_sms, cudaStream_t st, int zstore) {
+                                int num_sms, cudaStream_t st) {
   const size_t ring = (size_t)2 * kGU * kFT * 16;  // cp.async gather ring (HBM values)
   auto smem_of = [&](int cs_, int *zc) {
     const int64_t per = ((s.n + cs_ - 1) / cs_ + 15) / 16 * 16;
@@ -723,7 +723,7 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
     const char *ev = getenv("HC_SEL_STOP");
     stop_env = ev ? atoi(ev) : 0;
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, s, la, cs, nsplit, zcache, do_gather, zstore, stop_env);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, fn, s, la, cs, nsplit, zcache, do_gather, stop_env);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

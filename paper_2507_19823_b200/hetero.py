@@ -60,6 +60,14 @@ class HeteroEq5:
         self.ev_staged = torch.cuda.Event()
         self.stage_first = os.environ.get("HC_STAGE_FIRST", "1") != "0"
 
+    def check(self):
+        """Raise if a host share timed out (its output was poisoned with NaN by the wait
+        kernel); call after synchronizing."""
+        if self.mode == "doorbell":
+            st = self.worker.status()
+            if st != hc.HC_OK:
+                raise hc.HcError(st, "host worker: a host share of Eq. 5 timed out (output poisoned)")
+
     def split_point(self, layer: int) -> int:
         return int(round(self.host_frac * self.kc.n_q(layer)))
 
@@ -81,7 +89,8 @@ class HeteroEq5:
                 if self.mode == "doorbell":
                     B_, L_, Hkv_, ncap_, d_ = self.vs.tensor.shape
                     self.worker.submit(self.job, self.idx_d, self.w_d, sel_k, t_split,
-                                       layer * Hkv_ * ncap_ * d_, stream=self.side)
+                                       layer * Hkv_ * ncap_ * d_, stream=self.side,
+                                       n_valid=self.kc.n_q(layer))
                     self.ev_staged.record(self.side)
                     self.worker.wait(self.job, stream=self.side)
                 else:
@@ -89,7 +98,8 @@ class HeteroEq5:
                     self.w_h.copy_(self.w_d, non_blocking=True)
                     self.k_h.copy_(sel_k.view(-1), non_blocking=True)
                     hc.host_weighted_sum_range(self.idx_h, self.w_h, self.k_h, self.vs, layer, self.kc.G,
-                                               0, t_split, self.part_h, self.threads, stream=self.side)
+                                               0, t_split, self.part_h, self.threads, stream=self.side,
+                                               n_valid=self.kc.n_q(layer))
                 self.ev_host.record(self.side)
         if host and self.mode == "doorbell" and self.stage_first:
             # the GPU's pull starts once the host's lists are staged: side by side, the gather's

@@ -130,7 +130,7 @@ def test_host_weighted_sum_matches_oracle_gather():
     out = np.zeros((rows, d), np.float32)
     p = lambda a: a.ctypes.data_as(C.c_void_p)
     st = hc.lib().hc_host_weighted_sum(p(idx), p(w), p(k), rows, k_stride, p(V.view(np.uint16)),
-                                      Hkv * n * d, n * d, Hq, G, d, p(out), 4)
+                                      Hkv * n * d, n * d, n, Hq, G, d, p(out), 4)
     assert st == hc.HC_OK
     for r in range(rows):
         b, hq = divmod(r, Hq)
@@ -167,7 +167,7 @@ def test_host_weighted_sum_range_split_matches_oracle(isa, monkeypatch):
     def host(t0, t1, threads):
         out = np.full((rows, d), np.nan, np.float32)
         st = hc.lib().hc_host_weighted_sum_range(p(idx), p(w), p(k), rows, k_stride,
-                                                p(V.view(np.uint16)), Hkv * n * d, n * d, Hq, G, d,
+                                                p(V.view(np.uint16)), Hkv * n * d, n * d, n, Hq, G, d,
                                                 t0, t1, p(out), threads)
         assert st == hc.HC_OK
         return out
@@ -186,5 +186,15 @@ def test_host_weighted_sum_range_split_matches_oracle(isa, monkeypatch):
     assert np.allclose(host(0, t, 2) + host(t, n, 5), whole, rtol=1e-5, atol=1e-6)
     assert np.array_equal(host(0, n, 7), whole)  # thread-count independent
     st = hc.lib().hc_host_weighted_sum_range(p(idx), p(w), p(k), rows, k_stride, p(V.view(np.uint16)),
-                                            Hkv * n * d, n * d, Hq, G, d, 10, 5, p(whole), 1)
+                                            Hkv * n * d, n * d, n, Hq, G, d, 10, 5, p(whole), 1)
     assert st == hc.HC_ERR_RANGE
+    # a range past the layer's stored rows (e.g. t_split > n_q: resident-window tokens, whose
+    # values live in HBM) is refused instead of reading beyond the store
+    st = hc.lib().hc_host_weighted_sum_range(p(idx), p(w), p(k), rows, k_stride, p(V.view(np.uint16)),
+                                            Hkv * n * d, n * d, n - 1, Hq, G, d, 0, n, p(whole), 1)
+    assert st == hc.HC_ERR_RANGE
+    # the unranged entry sums only the stored rows [0, n_valid): here every kept index < n
+    out_all = np.zeros_like(whole)
+    st = hc.lib().hc_host_weighted_sum(p(idx), p(w), p(k), rows, k_stride, p(V.view(np.uint16)),
+                                      Hkv * n * d, n * d, n, Hq, G, d, p(out_all), 2)
+    assert st == hc.HC_OK and np.array_equal(out_all, whole)

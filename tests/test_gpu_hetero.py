@@ -45,6 +45,7 @@ def _run(case, host_frac, graph=False, mode="doorbell"):
     else:
         het(qq, 0, bud, out, sel_k, ws)
     torch.cuda.synchronize()
+    het.check()
     gpu = dict(out=out.cpu().numpy(), idx=het.idx_d.view(B, Hq, km).cpu().numpy(),
                w=het.w_d.view(B, Hq, km).cpu().numpy(), k=sel_k.cpu().numpy())
     for b in range(B):
@@ -65,7 +66,8 @@ def test_hetero_split_graph_replay(torch_cuda, mode):
 
 
 def test_hetero_split_window_and_renorm(torch_cuda):
-    """resident window tokens (global indices n_q..) land on the host side of the split."""
+    """resident window tokens (global indices n_q.., exact values in HBM) are summed by the GPU
+    side (t_split <= n_q: the host store holds only the quantized tokens' values)."""
     _run(Case(B=1, Hkv=2, n=9000, res_cap=64, n_res=40, k_max=700, renorm=1, placement=1, seed=83), 0.25)
 
 
@@ -166,17 +168,19 @@ def test_host_worker_timeout_reports(torch_cuda):
     k = torch.zeros((4,), dtype=torch.int64, device="cuda")
     w = hc.HostWorker(threads=1, max_jobs=2, timeout_s=0.2)
     j = w.add_job(4, 16, vs, 4, out)
-    w.submit(j, idx, wt, k, 64, 0)
+    w.submit(j, idx, wt, k, 64, 0, n_valid=64)
     w.wait(j)
     torch.cuda.synchronize()
     assert w.status() == hc.HC_OK
     w.pause(True)
     t0 = time.time()
-    w.submit(j, idx, wt, k, 64, 0)
+    w.submit(j, idx, wt, k, 64, 0, n_valid=64)
     w.wait(j)
     torch.cuda.synchronize()
     assert time.time() - t0 < 5.0
     assert w.status() == hc.HC_ERR_CUDA
+    # the timed-out share is poisoned, never passed off as a result
+    assert torch.isnan(out).all()
     w.pause(False)
     w.close()
 

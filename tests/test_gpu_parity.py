@@ -268,7 +268,7 @@ def test_select_only_then_host_weighted_sum(torch_cuda):
     st = hc.lib().hc_host_weighted_sum(C.c_void_p(hi.data_ptr()), C.c_void_p(hw.data_ptr()),
                                        C.c_void_p(hk.data_ptr()), B * Hq, km, C.c_void_p(V.data_ptr()),
                                        case.L * case.Hkv * case.n_cap * case.d, case.n_cap * case.d,
-                                       Hq, case.G, case.d, C.c_void_p(out.data_ptr()), 0)
+                                       case.n, Hq, case.G, case.d, C.c_void_p(out.data_ptr()), 0)
     assert st == hc.HC_OK
     gpu = dict(out=out.numpy().reshape(B, Hq, case.d), idx=hi.numpy(), w=hw.numpy(), k=hk.numpy())
     for b in range(B):

@@ -727,7 +727,7 @@ def test_decode_deterministic_and_weights_sum(orc):
 
 # ---------------------------------------------------------------- paper closed forms
 def test_table1a_memory_budget():
-    from paper_2507_19823_b200.accounting import memory_budget
+    from accounting import memory_budget
     g = GOLD["table1a_memory_budget"]
     for row in g["rows"]:
         if not row["value_offloaded"] and row["g"] is None:
@@ -738,14 +738,14 @@ def test_table1a_memory_budget():
 
 
 def test_comm_overhead_102_4_MB():
-    from paper_2507_19823_b200.accounting import comm_overhead
+    from accounting import comm_overhead
     c = GOLD["comm_overhead"]
     b = comm_overhead(c["n"], c["L"], c["H"], c["retain_fraction"], c["bytes_per_score"])
     assert b == c["bytes"] and b / 1e6 == c["MB"]
 
 
 def test_cost_per_query_table1b():
-    from paper_2507_19823_b200.accounting import cost_per_query
+    from accounting import cost_per_query
     for case in GOLD["table1b_cost_per_query"]["cases"]:
         r = cost_per_query(case["n"], case["d"], case["c"], case["g"])
         assert r == dict(exact_mults=case["exact_mults"], approx_mults=case["approx_mults"],

@@ -50,7 +50,7 @@ def main():
         for it in range(6):
             a = time.perf_counter()
             st = hc.lib().hc_host_weighted_sum_range(p(idx), p(w), p(k), rows, km, p(V.view(np.uint16)),
-                                                    Lv * Hkv * n * d, n * d, Hq, G, d, t0, n, p(out), threads)
+                                                    Lv * Hkv * n * d, n * d, n, Hq, G, d, t0, n, p(out), threads)
             ts.append(time.perf_counter() - a)
             assert st == 0
         t = float(np.median(ts[1:]))

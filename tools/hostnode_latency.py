@@ -22,7 +22,7 @@ def main():
         for _ in range(32):
             x.add_(1.0)
             if with_host:
-                hc.host_weighted_sum_range(idx, w, k, vs, 0, 4, 0, 0, part, 1,
+                hc.host_weighted_sum_range(idx, w, k, vs, 0, 4, 0, 0, part, 1, n_valid=0,
                                            stream=torch.cuda.current_stream())
             x.add_(1.0)
 

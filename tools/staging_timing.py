@@ -36,7 +36,7 @@ def main():
             torch.cuda.synchronize()
             with torch.cuda.stream(s1):
                 e[0].record()
-                het.worker.submit(het.job, het.idx_d, het.w_d, sel_k, t_split, 0)
+                het.worker.submit(het.job, het.idx_d, het.w_d, sel_k, t_split, 0, n_valid=het.kc.n_q(0))
                 e[1].record()
             if mode == "with_gather":
                 with torch.cuda.stream(s2):
