@@ -61,6 +61,8 @@ def lib():
             L.or_select.restype = i32
             L.or_select_float.argtypes = [p, i64, i32, f32, i64, i32, p, p, p]
             L.or_select_float.restype = i32
+            L.or_float_grid.argtypes = [p, i64, p]
+            L.or_float_grid.restype = i32
             L.or_gather.argtypes = [p, p, i64, p, i32, p]
             L.or_blockwise_attention.argtypes = [p, p, p, i64, i32, i32, i32, i64, p]
             L.or_kmeans_step.argtypes = [p, i64, i32, i32, i32, i32, p, i64, p, p, p]
@@ -218,6 +220,14 @@ def select_float(zf, d: int, tau: float, k_max: int, renorm: int = 0):
         raise ValueError(f"or_select_float rc={rc}")
     k = int(ks[0])
     return dict(idx=idx[:k].copy(), w=w[:k].copy(), k_sel=k)
+
+
+def float_grid(zf):
+    """R5b step 1 (hc_select_topk's input grid): -> (e, z_fx int32 [n])."""
+    zf = _c(zf, np.float32)
+    z = np.empty(max(zf.shape[0], 1), np.int32)
+    e = lib().or_float_grid(_ptr(zf), zf.shape[0], _ptr(z))
+    return int(e), z[:zf.shape[0]].copy()
 
 
 def select_shared(z, e, d: int, tau: float, k_max: int):

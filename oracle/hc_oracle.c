@@ -425,10 +425,9 @@ OR_EXPORT int or_select(const int32_t *z, int64_t n, int e_h, int d, float tau, 
 /* Standalone selection on real-valued scores (hc_select_topk's input), DESIGN
  * R5b: A = max|z|; e = 100 if A < 2^-100 else clamp(22 - floor(log2 A) - 1, -100,
  * 100) so |z·2^e| < 2^22; z_fx = rint(clamp(z·2^e, ±2^22)); then or_select. */
-OR_EXPORT int or_select_float(const float *zf, int64_t n, int d, float tau, int64_t k_max,
-                              int renorm, int32_t *idx_out, double *w_out, int64_t *k_sel_out)
+/* The R5b grid alone: returns e and writes z_fx [n] (step 1 of or_select_float). */
+OR_EXPORT int or_float_grid(const float *zf, int64_t n, int32_t *z)
 {
-    if (n <= 0) return 5;
     float A = 0.0f;
     for (int64_t j = 0; j < n; ++j)
         if (fabsf(zf[j]) > A) A = fabsf(zf[j]);
@@ -441,13 +440,21 @@ OR_EXPORT int or_select_float(const float *zf, int64_t n, int d, float tau, int6
         if (e > 100) e = 100;
     }
     float s = or_pow2f(e);
-    int32_t *z = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     for (int64_t j = 0; j < n; ++j) {
         float v = zf[j] * s;
         if (v > 4194304.0f) v = 4194304.0f;
         if (v < -4194304.0f) v = -4194304.0f;
         z[j] = (int32_t)rintf(v);
     }
+    return e;
+}
+
+OR_EXPORT int or_select_float(const float *zf, int64_t n, int d, float tau, int64_t k_max,
+                              int renorm, int32_t *idx_out, double *w_out, int64_t *k_sel_out)
+{
+    if (n <= 0) return 5;
+    int32_t *z = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int e = or_float_grid(zf, n, z);
     int rc = or_select(z, n, e, d, tau, k_max, renorm, idx_out, w_out, k_sel_out, 0, 0, 0);
     free(z);
     return rc;

@@ -263,8 +263,69 @@ def test_threshold_exact_ceiling(orc):
         tq = int(rng.integers(0, 2 ** 24 + 1))
         S = int(rng.integers(1, 2 ** 62))
         assert orc.threshold(tq, S) == -((-tq * S) // 2 ** 24)
-    assert orc.tau_q(0.9) == round(0.9 * 2 ** 24) or orc.tau_q(0.9) == int(np.float32(0.9) * 2 ** 24 + 0.5)
+
+def test_tau_q_single_valued(orc):
+    """R5: τ_q = rint(τ·2^24) of the fp32 τ, round-half-even -- one value per τ, worked by
+    hand from the fp32 bit patterns (not by re-evaluating the formula)."""
+    # fp32(0.9) = 15099494 * 2^-24 exactly (0x3F666666: mantissa 0x666666 | 1<<23 = 15099494,
+    # exponent -1 -> 15099494 * 2^-24) -> τ·2^24 is an integer: 15099494
+    assert orc.tau_q(0.9) == 15099494
+    # fp32(0.3) = 0x3E99999A = 10066330 * 2^-25 -> τ·2^24 = 5033165.0
+    assert orc.tau_q(0.3) == 5033165
+    # exact half-way points round to even: (2^23 + 1) * 2^-25 -> 2^22 + 0.5 -> 2^22 (even);
+    # (2^23 + 3) * 2^-25 -> 2^22 + 1.5 -> 2^22 + 2
+    assert orc.tau_q(float(np.float32((2 ** 23 + 1) * 2.0 ** -25))) == 2 ** 22
+    assert orc.tau_q(float(np.float32((2 ** 23 + 3) * 2.0 ** -25))) == 2 ** 22 + 2
     assert orc.tau_q(1.0) == 2 ** 24
+    assert orc.tau_q(2.0 ** -24) == 1 and orc.tau_q(2.0 ** -26) == 0
+
+
+def test_select_float_grid_worked_values(orc):
+    """R5b grid: e = clamp(21 - floor(log2 max|z|), -100, 100) (100 if max|z| <
+    2^-100), z_fx = rint(clamp(z·2^e, ±2^22)); every expected value worked by hand."""
+    e, z = orc.float_grid(np.array([1.0], np.float32))            # floor(log2 1) = 0
+    assert e == 21 and z.tolist() == [2 ** 21]
+    e, z = orc.float_grid(np.array([3.0, -1.5], np.float32))      # floor(log2 3) = 1
+    assert e == 20 and z.tolist() == [3 * 2 ** 20, -3 * 2 ** 19]
+    e, z = orc.float_grid(np.array([0.75, 0.5], np.float32))      # floor(log2 0.75) = -1
+    assert e == 22 and z.tolist() == [3 * 2 ** 20, 2 ** 21]
+    # ties to even on the grid: max|z| = 1 -> e = 21; 2.5 and 3.5 grid units -> 2 and 4
+    e, z = orc.float_grid(np.array([1.0, 2.5 * 2.0 ** -21, 3.5 * 2.0 ** -21, -2.5 * 2.0 ** -21], np.float32))
+    assert e == 21 and z.tolist() == [2 ** 21, 2, 4, -2]
+    # 0.1 (fp32 0x3DCCCCCD = 13421773 * 2^-27): e = 21 - (-4) = 25 -> 13421773 / 4 = 3355443.25 -> 3355443
+    e, z = orc.float_grid(np.array([0.1], np.float32))
+    assert e == 25 and z.tolist() == [3355443]
+    # huge scores: floor(log2 3e38) = 127 -> e = -106 clamps to -100; 3e38 * 2^-100 > 2^22 clamps
+    e, z = orc.float_grid(np.array([3e38, -3e38, 1.0], np.float32))
+    assert e == -100 and z.tolist() == [2 ** 22, -(2 ** 22), 0]
+    # tiny scores: max|z| < 2^-100 -> e = 100
+    e, z = orc.float_grid(np.array([2.0 ** -110, 0.0], np.float32))  # 2^-110 * 2^100 = 2^-10 -> 0
+    assert e == 100 and z.tolist() == [0, 0]
+    e, z = orc.float_grid(np.zeros(3, np.float32))
+    assert e == 100 and z.tolist() == [0, 0, 0]
+
+
+def test_select_float_grid_properties(orc):
+    """R5b: the largest |z| lands in [2^21, 2^22); every z_fx is within half a grid step of
+    z·2^e (no clamping below the 2^22 bound); the grid is monotone (a mis-rounding, a wrong
+    exponent or a dropped clamp fails one of these)."""
+    rng = _rng(31)
+    for trial in range(200):
+        scale = float(2.0 ** rng.integers(-60, 60))
+        zf = (rng.standard_normal(int(rng.integers(1, 400))) * scale).astype(np.float32)
+        e, z = orc.float_grid(zf)
+        A = float(np.max(np.abs(zf)))
+        if A == 0.0:
+            continue
+        assert 2 ** 21 <= int(np.max(np.abs(z))) <= 2 ** 22
+        exact = zf.astype(np.float64) * 2.0 ** e
+        assert np.all(np.abs(z - exact) <= 0.5)
+        o = np.argsort(zf, kind="stable")
+        assert np.all(np.diff(z[o]) >= 0)
+        # selection on the grid is the integer selection at scale e
+        r = orc.select_float(zf, 128, 0.9, 1 + trial % 50)
+        ri = orc.select(z, e, 128, 0.9, 1 + trial % 50)
+        assert r["idx"].tolist() == ri["idx"].tolist() and np.array_equal(r["w"], ri["w"])
 
 
 # ---------------------------------------------------------------- R5 selection (Eq. 4)
