@@ -54,20 +54,25 @@ __global__ void __launch_bounds__(kGT) k_gather_union(LayerArgs a, int nchunks, 
   const int64_t j1 = j0 + kGC < a.gtok_hi ? j0 + kGC : a.gtok_hi;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < G * kGC; i += kGT) (&wtab[0][0])[i] = 0.0f;
+  // a row's list: its whole kept list (decode), or this rank's slice of it (sequence-sharded
+  // finish: entries [g_off, g_off + g_cnt) hold GLOBAL indices, local token = index - g_base)
   if (tid < G) {
     const int row = b * a.Hq + kv * G + tid;
-    const int64_t k = a.k_in ? a.k_in[row] : a.hs[row].ksel;
-    const int32_t *li = a.sel_idx + (int64_t)row * a.k_max;
-    s_lo[tid] = (int)lower_bound_i32(li, k, jlo);
-    s_hi[tid] = (int)lower_bound_i32(li, k, j1 > jlo ? j1 : jlo);
+    const int64_t off = a.g_cnt ? a.g_off[row] : 0;
+    const int64_t k = a.g_cnt ? a.g_cnt[row] : (a.k_in ? a.k_in[row] : a.hs[row].ksel);
+    const int32_t *li = a.sel_idx + (int64_t)row * a.k_max + off;
+    s_lo[tid] = (int)lower_bound_i32(li, k, jlo + a.g_base);
+    s_hi[tid] = (int)lower_bound_i32(li, k, (j1 > jlo ? j1 : jlo) + a.g_base);
   }
   __syncthreads();
 #pragma unroll
   for (int h = 0; h < G; ++h) {
     const int row = b * a.Hq + kv * G + h;
-    const int32_t *li = a.sel_idx + (int64_t)row * a.k_max;
-    const float *lw = a.sel_w + (int64_t)row * a.k_max;
-    for (int e = s_lo[h] + tid; e < s_hi[h]; e += kGT) wtab[h][li[e] - j0] = lw[e];
+    const int64_t off = a.g_cnt ? a.g_off[row] : 0;
+    const int32_t *li = a.sel_idx + (int64_t)row * a.k_max + off;
+    const float *lw = a.sel_w + (int64_t)row * a.k_max + off;
+    const int64_t jb = j0 + a.g_base;
+    for (int e = s_lo[h] + tid; e < s_hi[h]; e += kGT) wtab[h][li[e] - jb] = lw[e];
   }
   __syncthreads();
   // ordered compaction of the union (a token is kept by some head iff a weight slot is set;

@@ -190,7 +190,8 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st, int64_t *grange = nullptr,
-                                float *rpart = nullptr, uint32_t *rdone = nullptr);
+                                float *rpart = nullptr, uint32_t *rdone = nullptr,
+                                float *upart = nullptr, uint32_t *udone = nullptr);
 
 // f4 (iii) App. B block-wise prefill attention (hc_prefill.cu), d = 128
 cudaError_t launch_blockwise_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,

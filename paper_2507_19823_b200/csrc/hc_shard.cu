@@ -591,9 +591,25 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st, int64_t *grange,
-                                float *rpart, uint32_t *rdone) {
+                                float *rpart, uint32_t *rdone, float *upart, uint32_t *udone) {
   const int rows = a.B * a.Hq;
   const int nch = shard_chunks(a.n_cand);
+  if (nch > 0 && grange && a.v_placement == 1 && a.G > 1 && upart && udone) {
+    // host-resident values (config 5): the GQA union of this rank's kept rows is read once
+    // over the host link (as in the unsharded decode), not once per head
+    k_sh_compact<<<dim3(nch, rows), kShT, 0, st>>>(a, s, nch, chunk, allcnt, rank, base, grange);
+    note_launch();
+    cudaError_t e = cudaMemsetAsync(udone, 0, (size_t)a.B * a.Hkv * 4, st);
+    if (e != cudaSuccess) return e;
+    LayerArgs g = a;
+    g.g_off = grange;
+    g.g_cnt = grange + rows;
+    g.g_base = base;
+    g.out = out;
+    g.gtok_lo = 0;
+    g.gtok_hi = a.n_cand;
+    return launch_gather_union(g, upart, udone, st);
+  }
   if (nch > 0 && grange && a.d == 128) {
     // compaction only, then the many-rows-in-flight gather over this rank's list slice
     k_sh_compact<<<dim3(nch, rows), kShT, 0, st>>>(a, s, nch, chunk, allcnt, rank, base, grange);

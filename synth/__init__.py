@@ -94,6 +94,18 @@ def gen_values(seed: int, b: int, l: int, kv: int, d: int, start: int, count: in
     return v16(u).reshape(count, d)
 
 
+def gen_value_rows(seed: int, b: int, l: int, kv: int, d: int, rows) -> np.ndarray:
+    """Rows `rows` (int array of token positions) of V[b][l][kv] -> fp16 [len(rows)][d]; the
+    same counters as gen_values (row j = counters j*d .. j*d+d-1), for huge stores of which
+    only a few rows are needed."""
+    rows = np.asarray(rows, dtype=np.uint64)
+    key = np.uint64(stream_key(seed, TAG_V, b, l, kv))
+    j = (rows[:, None] * np.uint64(d) + np.arange(d, dtype=np.uint64)[None, :]).reshape(-1)
+    with np.errstate(over="ignore"):
+        u = _fin(key + (j + np.uint64(1)) * GOLDEN)
+    return v16(u).reshape(len(rows), d)
+
+
 def gen_query(seed: int, b: int, l: int, hq: int, d: int, s: float) -> np.ndarray:
     """q[b][l] -> fp16 [hq][d], approx N(0, s^2) (Irwin-Hall(4), rescaled)."""
     u = u64(stream_key(seed, TAG_Q, b, l), 0, hq * d)

@@ -834,3 +834,30 @@ def test_synth_codes_in_range_and_uniform():
     assert x.max() < c
     h = np.bincount(x[0].astype(np.int64) // 1024, minlength=8)
     assert np.all(np.abs(h / h.sum() - 1 / 8) < 0.01)
+
+
+def test_synth_value_rows_match_gen_values():
+    """synth.gen_value_rows (kept rows only, for huge stores) draws the same counters as
+    gen_values row for row."""
+    import synth
+    full = synth.gen_values(77, 1, 2, 3, 128, 0, 3000)
+    rows = np.array([0, 1, 2999, 1234, 17, 17], np.int64)
+    assert np.array_equal(synth.gen_value_rows(77, 1, 2, 3, 128, rows).view(np.uint16),
+                          full[rows].view(np.uint16))
+    part = synth.gen_values(77, 1, 2, 3, 128, 1000, 500)
+    assert np.array_equal(synth.gen_value_rows(77, 1, 2, 3, 128, np.arange(1000, 1500)).view(np.uint16),
+                          part.view(np.uint16))
+
+
+def test_oracle_unit_rows_equals_decode_unit():
+    """The composed full-size oracle (harness.oracle_unit_rows: kept value rows generated on
+    demand) is the oracle's decode_unit, stage for stage."""
+    from harness import Case, oracle_unit, oracle_unit_rows
+    case = Case(B=1, Hkv=2, n=20011, k_max=1500, tau=0.9, seed=5)
+    for kv in range(2):
+        a, b = oracle_unit(case, 0, 0, kv), oracle_unit_rows(case, 0, 0, kv, chunk=700)
+        assert np.array_equal(a["z"], b["z"]) and np.array_equal(a["S"], b["S"])
+        for h in range(case.G):
+            assert np.array_equal(a["idx"][h], b["idx"][h]) and np.array_equal(a["w"][h], b["w"][h])
+            assert int(a["k_sel"][h]) == int(b["k_sel"][h]) and int(a["kstar"][h]) == int(b["kstar"][h])
+        assert np.allclose(a["out"], b["out"], rtol=1e-12, atol=1e-13)
