@@ -235,7 +235,10 @@ class Workload:
             self.out_cpu = torch.empty((L, B * self.Hq, d), dtype=torch.float32).pin_memory()
         self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                    for _ in range(L)]
-        for b_, e_ in self.ev:  # torch creates the CUDA event lazily on first record
+        # the whole Eq. 3 stage (table + scan) per layer, for the eq3_stage record
+        self.ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(L)]
+        for b_, e_ in self.ev + self.ev3:  # torch creates the CUDA event lazily on first record
             b_.record()
             e_.record()
         torch.cuda.synchronize()
@@ -291,6 +294,7 @@ class Workload:
                 self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
             if profile:
                 hc.profile_scan_events(*self.ev[l])
+                hc.profile_eq3_events(*self.ev3[l])
             if self.cpu_gather:
                 self._step_cpu_gather(l)
             elif self.hetero is not None:
@@ -493,6 +497,94 @@ def measure_host_rows_gbs(wl, reps: int = 3) -> dict:
         tc.append(time.perf_counter() - a)
     return {"host_alone": nbytes / t_h / 1e9, "gpu_alone": nbytes / t_g / 1e9,
             "combined": nbytes / min(tc[1:]) / 1e9, "combined_host_share": split / n}
+
+
+def measure_host_dram_hw(wl) -> dict:
+    """Engine-free host DRAM read rates over the value store's own pinned memory (tools/
+    membench.c: random 256-B rows and a sequential pass, all host cores; CPU model and NUMA
+    layout recorded) -- the hardware ceiling the host share of Eq. 5 is judged against."""
+    from tools import membench
+    t = wl.vs.tensor
+    return membench.measure(t.data_ptr(), t.numel() * t.element_size())
+
+
+def measure_gpu_only(wl, args, dev_index, h2d_peak):
+    """The north_star's stage 4 alone: Eq. 5 entirely on the GPU (host_frac 0, the zero-copy
+    GQA-union pull of every kept row over the host link) on the same workload, timed the same
+    way (CUDA graph, events, K replays after W warm-ups)."""
+    import torch
+    het = wl.hetero
+    wl.hetero = None
+    try:
+        wl.reset_counts()
+        wl.step()
+        torch.cuda.synchronize()
+        g, launches = wl.capture(wl.step)
+        K = max(3, args.steps // 2)
+        with ClockSampler(dev_index) as clk:
+            ms = time_graph(g, K, max(args.warmup, 3)) / K
+        del g
+        v_bytes = union_gather_bytes(wl)
+    finally:
+        wl.hetero = het
+        wl.reset_counts()
+    gbs = v_bytes / (ms * 1e-3) / 1e9
+    return {"value": 1000.0 / ms, "unit": "steps/s", "ms_per_step": ms, "steps": K,
+            "gpu_launches_per_step": launches,
+            "eq5": "GPU only: k_gather_union pulls the union of the GQA heads' kept rows zero-copy",
+            "host_link": {"bytes_per_step": v_bytes, "achieved_gbs_lower_bound": gbs, "peak_gbs": h2d_peak,
+                          "peak_source": "measured pinned H2D cudaMemcpy 1 GiB", "frac": gbs / h2d_peak,
+                          "note": "whole step time in the denominator (scan + selection included)"},
+            "clocks": clk.summary()}
+
+
+def measure_config5_layers(args, layers: int, dev_index: int, h2d_peak: float) -> dict:
+    """BASELINE config 5 (4M-token context, g = 32, k_max = 524,288, values in host pinned
+    memory) on ONE GPU with the layer count reduced to `layers` (the full 32-layer store, 275
+    GB of host values, needs >= 4 ranks): per-layer time of the unsharded decode with the
+    GPU-only Eq. 5 pull, and its Eq. 3 stage."""
+    import torch
+    cfg = dict(CONFIGS[5])
+    cfg.update(L=layers, lut_bits=16, vo_only=False, cpu_gather=False, shared_kv=False, code_bits=16,
+               host_frac=0.0, pipeline=1)
+    wl = Workload(cfg, "cuda")
+    wl.reset_counts()
+    wl.step()
+    torch.cuda.synchronize()
+    g, launches = wl.capture(wl.step)
+    gp, _ = wl.capture(lambda: wl.step(profile=True))
+    K = 10
+    with ClockSampler(dev_index) as clk:
+        ms = time_graph(g, K, 3) / K
+    for _ in range(2):
+        gp.replay()
+    torch.cuda.synchronize()
+    scan = statistics.mean(event_ms(b, e) for (b, e) in wl.ev)
+    eq3 = statistics.mean(event_ms(b, e) for (b, e) in wl.ev3)
+    del g, gp
+    v_bytes = union_gather_bytes(wl)
+    ksel = wl.sel_k.float().mean().item()
+    p_bytes = cfg["B"] * cfg["Hkv"] * wl.n_local * cfg["g"] * 2
+    peak, _ = measured_peaks()
+    res = {"workload": f"config5 on ONE B200, L = {layers} of 32 layers (stated: the 32-layer host "
+                       f"store needs >= 4 ranks), unsharded, GPU-only Eq. 5 (zero-copy union pull), "
+                       f"n = {cfg['n']}, g = 32, k_max = {cfg['k_max']}, tau = 0.9, batch 1",
+           "layers": layers, "ms_per_layer": ms / layers,
+           "steps_per_s_at_32_layers_extrapolated": 1000.0 / (32 * ms / layers),
+           "scan": {"avg_ms": scan, "achieved_gbs": p_bytes / (scan * 1e-3) / 1e9,
+                    "frac_hbm": p_bytes / (scan * 1e-3) / 1e9 / peak},
+           "eq3_stage": {"avg_ms": eq3, "achieved_gbs": p_bytes / (eq3 * 1e-3) / 1e9,
+                         "frac_hbm": p_bytes / (eq3 * 1e-3) / 1e9 / peak},
+           "host_link": {"bytes_per_layer": v_bytes / layers,
+                         "achieved_gbs_lower_bound": v_bytes / (ms * 1e-3) / 1e9,
+                         "peak_gbs": h2d_peak, "frac": v_bytes / (ms * 1e-3) / 1e9 / h2d_peak},
+           "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / cfg["n"]},
+           "gpu_launches_per_step": launches, "clocks": clk.summary()}
+    if wl.vs.host is not None:
+        wl.vs.host.close()
+    del wl
+    torch.cuda.empty_cache()
+    return res
 
 
 HOST_FRAC_CANDIDATES = (0.65, 0.7, 0.75)
@@ -698,6 +790,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None,
+                    help="reduce the layer count L (stated in the workload); config 5 at N=1 needs <= 4")
+    ap.add_argument("--no-config5", action="store_true",
+                    help="skip the config5_layer sub-record of the default (config 3) run")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if args.config is None:
@@ -738,7 +834,13 @@ def main():
         cfg["workload"] += "; value-offload-only mode (exact fp16 keys, Table 1a VO row)"
     if args.lut8:
         cfg["workload"] += "; 8-bit table variant (R2b)"
-    if args.config == 5 and world_env < 4 and not args.impl == "reference":
+    if args.layers is not None:
+        if not 1 <= args.layers <= cfg["L"]:
+            raise SystemExit(f"--layers must be in [1, {cfg['L']}]")
+        cfg["L"] = args.layers
+        cfg["workload"] += f"; L REDUCED to {args.layers} of 32 layers"
+    if args.config == 5 and world_env < 4 and not args.impl == "reference" and not (
+            args.layers is not None and args.layers <= 4):
         raise SystemExit("config 5 (4M ctx, 275 GB of host-resident values) needs >= 4 ranks "
                          "(python -m torch.distributed.run --nproc-per-node N bench.py --config 5)")
     if args.steps is None:
@@ -815,6 +917,7 @@ def main():
     torch.cuda.synchronize()
     scan_ms = [event_ms(b, e) for (b, e) in wl.ev]
     scan_avg_ms = statistics.mean(scan_ms)
+    eq3_avg_ms = statistics.mean(event_ms(b, e) for (b, e) in wl.ev3)
     K2 = args.e2e_steps or max(args.steps // 2, 3)
     ms_e2e = time_graph(g_e2e, K2, args.warmup, dist) / K2
 
@@ -838,27 +941,33 @@ def main():
     v_bytes = ksel * B * wl.Hq * L * d * 2 / (world if sharded_mode else 1)
     host_link = None
     host_dram = None
+    pk = measure_h2d_gbs() if cfg["placement"] == 1 else None
+    gpu_only = None
     if cfg["placement"] == 1:
         if not wl.cpu_gather and world == 1:
             if wl.hetero is not None:  # the host's share of the rows stays in host DRAM
                 v_bytes, h_bytes = union_gather_bytes(wl, cfg["host_frac"])
                 mem = measure_host_rows_gbs(wl)
-                pk_mem = max(mem["combined"], mem["host_alone"], mem["gpu_alone"])
+                hw = measure_host_dram_hw(wl)
+                pk_eng = max(mem["combined"], mem["host_alone"], mem["gpu_alone"])
+                pk_mem = hw["random_rows_gbs"]
                 both = (h_bytes + v_bytes) / (ms_per_step * 1e-3) / 1e9
                 host_dram = {"bytes_per_step": h_bytes, "rows": "union of the GQA heads' kept rows, "
                              "index < t_split", "achieved_gbs_lower_bound": h_bytes / (ms_per_step * 1e-3) / 1e9,
                              "host_frac": cfg["host_frac"], "threads": wl.hetero.threads,
                              # both consumers (host threads + the GPU's zero-copy pulls) read the
-                             # same host DRAM: their sum against its measured random-row rate
+                             # same host DRAM: their sum against the hardware's random-row rate
                              "all_row_bytes_gbs": both, "peak_gbs": pk_mem,
-                             "peak_source": "Eq. 5 alone on one layer's full selection, host engine "
-                                            "and GPU pull concurrently on a time-balanced split "
-                                            "(union rows / time), measured live; see peak_parts",
-                             "peak_parts": mem,
-                             "frac": both / pk_mem if pk_mem else None}
+                             "peak_source": "engine-free all-core random 256-B row reads of the value "
+                                            "store's pinned memory (tools/membench.c); see hw",
+                             "frac": both / pk_mem if pk_mem else None,
+                             "hw": hw,
+                             # what Eq. 5 itself reaches alone on this box (our engines), kept apart
+                             "engine_capability_gbs": pk_eng, "engine_parts": mem,
+                             "frac_of_engine_capability": both / pk_eng if pk_eng else None}
+                gpu_only = measure_gpu_only(wl, args, local, pk)
             else:
                 v_bytes = union_gather_bytes(wl)  # rows actually read: union over the GQA heads
-        pk = measure_h2d_gbs()
         host_link = {"bytes_per_step": v_bytes, "rows": "union of the GQA heads' kept rows",
                      "achieved_gbs_lower_bound": v_bytes / (ms_per_step * 1e-3) / 1e9,
                      "peak_gbs": pk, "peak_source": "measured pinned H2D cudaMemcpy 1 GiB",
@@ -882,6 +991,12 @@ def main():
                       if cfg["host_frac"] > 0.0 else {})},
         "quantized_key_gbs": achieved,
         "quantized_key_frac_hbm": achieved / peak,
+        # the whole Eq. 3 stage the scan needs: table build (row a1) + scan, same bytes
+        "eq3_stage": {"kernels": "k_table + k_scan_sk (hc_table.cu, hc_scan.cu)",
+                      "avg_ms_per_layer": eq3_avg_ms, "scan_ms": scan_avg_ms,
+                      "table_and_launch_gap_ms": eq3_avg_ms - scan_avg_ms,
+                      "achieved_gbs": p_bytes_layer / (eq3_avg_ms * 1e-3) / 1e9,
+                      "frac_hbm": p_bytes_layer / (eq3_avg_ms * 1e-3) / 1e9 / peak},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": ("k_resident (exact-key dense scan, VO-only mode)" if wl.vo_only
@@ -904,6 +1019,7 @@ def main():
         "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / n},
         "host_link": host_link,
         "host_dram": host_dram,
+        "gpu_only": gpu_only,
         "e2e": {"value": jobs * 1000.0 / ms_e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
         "gpu_launches": launches_per_step * args.steps,
@@ -912,6 +1028,22 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
+    if world == 1 and args.config == 3 and not args.no_config5 and args.layers is None:
+        # one-GPU timing of the paper's 4M-token headline configuration: the
+        # config-3 state is released first (its 34 GB of pinned values)
+        import gc
+        g_step = g_prof = g_e2e = None
+        if wl.hetero is not None and wl.hetero.mode == "doorbell":
+            wl.hetero.worker.close()
+        if wl.vs.host is not None:
+            wl.vs.host.close()
+        del wl
+        gc.collect()
+        torch.cuda.empty_cache()
+        try:
+            line["config5_layer"] = measure_config5_layers(args, 1, local, pk or measure_h2d_gbs())
+        except Exception as ex:  # report, never silently drop
+            line["config5_layer"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

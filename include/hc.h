@@ -150,6 +150,9 @@ uint64_t hc_launch_count(void);
  * launched by hc_decode_attention from this thread (one-shot; NULLs disable).  Inside
  * stream capture they become external event-record nodes of the graph. */
 hc_status hc_profile_scan_events(void *begin_event, void *end_event);
+/* Same, around the whole Eq. 3 stage of the NEXT hc_decode_attention call from this thread:
+ * the table build (row a1) + the resident-token scorer + the quantized-key scan (row a2). */
+hc_status hc_profile_eq3_events(void *begin_event, void *end_event);
 
 /* Host value-store memory (A8): page-lock caller-allocated host memory (e.g. an
  * anonymous mapping advised for 2 MiB transparent huge pages, so random row reads by host

@@ -21,6 +21,7 @@ HC_OK, HC_ERR_ARG, HC_ERR_SHAPE, HC_ERR_RANGE, HC_ERR_CAPACITY, HC_ERR_EMPTY, HC
 HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
 
 EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_events",
+           "hc_profile_eq3_events",
            "hc_codebook_absmax", "hc_quantize_keys", "hc_append_kv",
            "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
            "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
@@ -83,6 +84,8 @@ def lib():
         L.hc_launch_count.restype = C.c_uint64
         L.hc_profile_scan_events.argtypes = [p, p]
         L.hc_profile_scan_events.restype = i32
+        L.hc_profile_eq3_events.argtypes = [p, p]
+        L.hc_profile_eq3_events.restype = i32
         L.hc_codebook_absmax.argtypes = [p, hc_vq, i32, p, p]
         L.hc_codebook_absmax.restype = i32
         L.hc_quantize_keys.argtypes = [p, i64, p, hc_vq, p, i64, p]
@@ -183,6 +186,12 @@ def profile_scan_events(begin, end):
     """Record torch.cuda.Event's around the next scan launch (one-shot)."""
     _check(lib().hc_profile_scan_events(C.c_void_p(begin.cuda_event) if begin is not None else None,
                                         C.c_void_p(end.cuda_event) if end is not None else None))
+
+
+def profile_eq3_events(begin, end):
+    """Record torch.cuda.Event's around the next decode call's Eq. 3 stage (table + scan)."""
+    _check(lib().hc_profile_eq3_events(C.c_void_p(begin.cuda_event) if begin is not None else None,
+                                       C.c_void_p(end.cuda_event) if end is not None else None))
 
 
 def budget(tau: float, k_max: int, renorm: bool = False, select_only: bool = False,

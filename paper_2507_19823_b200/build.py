@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhc.so")
 SOURCES = ["hc_api.cu", "hc_encode.cu", "hc_table.cu", "hc_scan.cu", "hc_select.cu",
-           "hc_select_fused.cu", "hc_shard.cu", "hc_host.cu", "hc_gather.cu", "hc_group.cu", "hc_kmeans.cu",
+           "hc_select_fused.cu", "hc_select_pass.cu", "hc_shard.cu", "hc_host.cu", "hc_gather.cu", "hc_group.cu", "hc_kmeans.cu",
            "hc_prefill.cu"]
 HEADERS = ["hc_device.cuh", "hc_internal.h"]
 

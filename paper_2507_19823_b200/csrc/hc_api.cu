@@ -17,6 +17,7 @@ using namespace hc;
 namespace hc {
 static std::atomic<unsigned long long> g_launches{0};
 static thread_local cudaEvent_t g_scan_ev[2] = {nullptr, nullptr};
+static thread_local cudaEvent_t g_eq3_ev[2] = {nullptr, nullptr};
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -124,7 +125,9 @@ struct Layout {
   int64_t z_stride;
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
-      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, total;
+      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, o_sgh, o_sfc, o_sfm,
+      o_slb, total;
+  int64_t slb_n;
   int skctr_n;
   int nch_max;  // sharded compaction chunks
 };
@@ -146,6 +149,12 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
   L.o_cbabs = o; o += align256((size_t)kc->vq.cbg * (d / g) * 4);
   L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
   L.o_zpart = o;  // (no partial planes: split scans accumulate exactly into z)
+  // selection passes (hc_select_pass.cu): coarse / fine histograms, look-back words
+  L.slb_n = select_lb_chunks(ncand_max > 0 ? ncand_max : 1);
+  L.o_sgh = o; o += align256((size_t)rows * kNB * 4);
+  L.o_sfc = o; o += align256((size_t)rows * kNB * 4);
+  L.o_sfm = o; o += align256((size_t)rows * kNB * 8);
+  L.o_slb = o; o += align256((size_t)rows * L.slb_n * 8);
   L.o_idx = o; o += align256((size_t)rows * L.k_eff * 4);
   L.o_w = o; o += align256((size_t)rows * L.k_eff * 4);
   L.nch_max = shard_chunks(ncand_max > 0 ? ncand_max : 1);
@@ -238,6 +247,12 @@ hc_status hc_codebook_absmax(const float *codebook, hc_vq vq, int32_t L, float *
 hc_status hc_profile_scan_events(void *begin_event, void *end_event) {
   hc::g_scan_ev[0] = (cudaEvent_t)begin_event;
   hc::g_scan_ev[1] = (cudaEvent_t)end_event;
+  return HC_OK;
+}
+
+hc_status hc_profile_eq3_events(void *begin_event, void *end_event) {
+  hc::g_eq3_ev[0] = (cudaEvent_t)begin_event;
+  hc::g_eq3_ev[1] = (cudaEvent_t)end_event;
   return HC_OK;
 }
 
@@ -528,6 +543,7 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   }
   a.z = (float *)(w8 + Lw.o_z);
   a.z_stride = Lw.z_stride;
+  a.sel_ghist = (uint32_t *)(w8 + Lw.o_sgh);
   const int64_t k_cap = sel_idx ? budget.k_max : Lw.k_eff;  // row stride of idx / w
   a.k_max = k_cap;
   a.sel_idx = sel_idx ? sel_idx : (int32_t *)(w8 + Lw.o_idx);
@@ -592,20 +608,44 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   // the gather's completion counters are zeroed by k_table (no memset between chain kernels)
   if (union_gather) { a.gdone = (uint32_t *)((uint8_t *)ws + Lw.o_udone); a.gdone_n = a.B * a.Hkv; }
   if (rows_gather) { a.gdone = (uint32_t *)((uint8_t *)ws + Lw.o_rdone); a.gdone_n = rows; }
+  // Eq. 3 stage profiling hook (one-shot): events around table + resident + scan
+  cudaEvent_t e3b = g_eq3_ev[0], e3e = g_eq3_ev[1];
+  g_eq3_ev[0] = g_eq3_ev[1] = nullptr;
+  unsigned e3flag = 0u;
+  if (e3b || e3e) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    e3flag = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  }
+  if (e3b) cudaEventRecordWithFlags(e3b, s, e3flag);
   if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
   if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
   if (n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
+  if (e3e) cudaEventRecordWithFlags(e3e, s, e3flag);
   SelArgs sa{};
   sa.hs = a.hs; sa.z = a.z; sa.z_stride = a.z_stride; sa.rows = rows; sa.n = n_cand;
   sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
+  sa.ghist = (uint32_t *)((uint8_t *)ws + Lw.o_sgh);
+  sa.fcnt = (uint32_t *)((uint8_t *)ws + Lw.o_sfc);
+  sa.fmass = (unsigned long long *)((uint8_t *)ws + Lw.o_sfm);
+  sa.lb = (unsigned long long *)((uint8_t *)ws + Lw.o_slb);
+  sa.lb_n = Lw.slb_n;
+  // the round-1 fused select kernel stays reachable for A/B measurements (HC_SELECT=fused) and
+  // for Eq. 5 inside the select kernel (HC_GATHER=fused)
+  static int sel_old = -1;
+  if (sel_old < 0) { const char *ev = getenv("HC_SELECT"); sel_old = (ev && !strcmp(ev, "fused")) ? 1 : 0; }
+  const bool fused_gather = !(budget.select_only || union_gather || rows_gather);
   if (shared) {
     if ((e = launch_group_select(a, n_q > 0 ? a.scan_split : 1, s)) != cudaSuccess)
       return cuda_check(e, "shared select");
-  } else if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1,
-                                      (budget.select_only || union_gather || rows_gather) ? 0 : 1,
-                                      a.num_sms, s)) != cudaSuccess)
+  } else if (sel_old || fused_gather) {
+    if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, fused_gather ? 1 : 0, a.num_sms, s)) !=
+        cudaSuccess)
+      return cuda_check(e, "select");
+  } else if ((e = launch_select(sa, n_q > 0 ? a.scan_split : 1, a.num_sms, s)) != cudaSuccess) {
     return cuda_check(e, "select");
+  }
   if (rows_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);
     const int64_t kc2 = a.k_max < n_cand ? a.k_max : n_cand;
@@ -783,7 +823,9 @@ size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {
   (void)budget;
   if (rows <= 0 || n <= 0) return 0;
   const int64_t zs = round_up(n, 64);
-  return align256((size_t)rows * sizeof(HeadState)) + align256((size_t)rows * zs * 4);
+  return align256((size_t)rows * sizeof(HeadState)) + align256((size_t)rows * zs * 4) +
+         align256((size_t)rows * kNB * 4) * 2 + align256((size_t)rows * kNB * 8) +
+         align256((size_t)rows * select_lb_chunks(n) * 8);
 }
 
 hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d, hc_budget budget,
@@ -803,19 +845,22 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   const int64_t zs = round_up(n, 64);
   size_t o = 0;
   HeadState *hs = (HeadState *)(w8 + o); o += align256((size_t)rows * sizeof(HeadState));
-  float *z = (float *)(w8 + o);
+  float *z = (float *)(w8 + o); o += align256((size_t)rows * zs * 4);
+  SelArgs sa{};
+  sa.ghist = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
+  sa.fcnt = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
+  sa.fmass = (unsigned long long *)(w8 + o); o += align256((size_t)rows * kNB * 8);
+  sa.lb = (unsigned long long *)(w8 + o);
+  sa.lb_n = select_lb_chunks(n);
   cudaError_t e;
   const float kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
-  if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s)) != cudaSuccess)
+  if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s, sa.ghist)) != cudaSuccess)
     return cuda_check(e, "prep");
-  SelArgs sa{};
   sa.hs = hs; sa.z = z; sa.z_stride = zs; sa.rows = (int)rows; sa.n = n;
   sa.tau_q = (uint32_t)rint((double)budget.tau * 16777216.0);
   sa.k_max = budget.k_max; sa.renorm = budget.renorm ? 1 : 0;
   sa.sel_idx = idx; sa.sel_w = w; sa.sel_k = k;
-  LayerArgs la{};
-  la.n_q = n; la.z_stride = zs;
-  return cuda_check(launch_select_fused(sa, la, 1, 0, num_sms(), s), "hc_select_topk");
+  return cuda_check(launch_select(sa, 1, num_sms(), s), "hc_select_topk");
 }
 
 }  // extern "C"

@@ -239,7 +239,13 @@ struct alignas(16) HeadState {
   uint32_t gather_done; // completion counter of the gather's last-block reduction
   uint32_t h1_done;     // completion counter of hist1 (last CTA runs bound1)
   uint32_t h2_done;     // completion counter of hist2 (last CTA runs bound2)
-  uint32_t pad[7];
+  // hc_select_pass.cu (K1 / K2 / K3 of the decode selection); zeroed by k_table / the prep
+  uint32_t c1_done;     // K1 completion counter (the row's last CTA bounds the cut)
+  uint32_t c2_done;     // K2 completion counter (the last CTA resolves the cut)
+  uint32_t ticket;      // K3 chunk tickets (decoupled look-back order)
+  uint32_t r_lo, r_hi;  // refine range of Δ (inclusive)
+  int32_t fshift;       // refine bin width 2^fshift
+  uint32_t state;       // 1 / 2: refine pass 1 / 2 pending, 3: resolved, 4: error
 };
 static_assert(sizeof(HeadState) == 128, "HeadState size");
 

@@ -137,6 +137,8 @@ struct LayerArgs {
   // between the chain kernels)
   uint32_t *gdone;
   int gdone_n;
+  // the selection's coarse count histograms [B*Hq][kNB], zeroed by k_table (or null)
+  uint32_t *sel_ghist;
   // k_gather_rows on a sub-range of each row's list (sequence-sharded finish): entries
   // [g_off[row], g_off[row] + g_cnt[row]) with local token index = sel_idx - g_base
   const int64_t *g_off, *g_cnt;
@@ -173,10 +175,21 @@ struct SelArgs {
   int32_t *sel_idx;       // [rows][k_max]
   float *sel_w;           // [rows][k_max]
   int64_t *sel_k;         // [rows] (may be null)
+  // hc_select_pass.cu state (workspace): coarse count histograms (zeroed before K1 by k_table
+  // / the float prep), refine histograms and look-back words (zeroed by K1)
+  uint32_t *ghist;             // [rows][kNB]
+  uint32_t *fcnt;              // [rows][kNB]
+  unsigned long long *fmass;   // [rows][kNB]
+  unsigned long long *lb;      // [rows][lb_n]
+  int64_t lb_n;
 };
-// fused rows a3-a5 (one cluster of CTAs per row); nsplit: scan partial planes in la.zpart
+// fused rows a3-a5 (one cluster of CTAs per row; round 1, HC_SELECT=fused); nsplit: scan
+// partial planes in la.zpart
 cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
                                 int num_sms, cudaStream_t st);
+// rows a3-a4 as three passes (hc_select_pass.cu, the default); nsplit > 1 adds a max/min pass
+cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st);
+int select_lb_chunks(int64_t n);
 
 // sequence-sharded phases (hc_shard.cu)
 int shard_chunks(int64_t n);
@@ -216,6 +229,6 @@ cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, u
 // standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
                                      int64_t z_stride, HeadState *hs, float kappa0,
-                                     cudaStream_t s);
+                                     cudaStream_t s, uint32_t *ghist = nullptr);
 
 }  // namespace hc

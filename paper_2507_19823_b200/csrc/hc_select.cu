@@ -1,6 +1,6 @@
 // hc_select.cu -- standalone hc_select_topk front end (R5b): real-valued scores are
-// mapped onto a per-row 2^-e fixed-point grid (|z| < 2^22), then the fused Eq. 4
-// selection kernel (hc_select_fused.cu) runs on them.
+// mapped onto a per-row 2^-e fixed-point grid (|z| < 2^22), then the Eq. 4 selection
+// passes (hc_select_pass.cu) run on them.
 #include <float.h>
 
 #include "hc_internal.h"
@@ -12,7 +12,7 @@ constexpr int kSelThreads = 256;
 // ---------------------------------------------------------------- standalone prep (R5b)
 __global__ void __launch_bounds__(kSelThreads) k_float_prep(const float *sc, int64_t n, float *z,
                                                              int64_t zs, HeadState *hs,
-                                                             float kappa0) {
+                                                             float kappa0, uint32_t *ghist) {
   const int row = blockIdx.x;
   const float *src = sc + (int64_t)row * n;
   float A = 0.0f;
@@ -49,13 +49,21 @@ __global__ void __launch_bounds__(kSelThreads) k_float_prep(const float *sc, int
     hs[row].zmin = mn;
     hs[row].e = e;
     hs[row].kappa = __fmul_rn(kappa0, pow2f(-e));
+    hs[row].S = 0ull;
+    hs[row].mass_before = 0ull;
+    hs[row].c1_done = 0u;
+    hs[row].c2_done = 0u;
+    hs[row].ticket = 0u;
+    hs[row].state = 0u;
   }
+  if (ghist)
+    for (int i = threadIdx.x; i < kNB; i += kSelThreads) ghist[(int64_t)row * kNB + i] = 0u;
 }
 
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
                                      int64_t z_stride, HeadState *hs, float kappa0,
-                                     cudaStream_t s) {
-  k_float_prep<<<(unsigned)rows, kSelThreads, 0, s>>>(scores, n, z, z_stride, hs, kappa0);
+                                     cudaStream_t s, uint32_t *ghist) {
+  k_float_prep<<<(unsigned)rows, kSelThreads, 0, s>>>(scores, n, z, z_stride, hs, kappa0, ghist);
   note_launch();
   return cudaGetLastError();
 }

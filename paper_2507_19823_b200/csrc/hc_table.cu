@@ -59,6 +59,14 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
     for (int t = threadIdx.x; t < a.gdone_n; t += blockDim.x) a.gdone[t] = 0u;
   if (a.skctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 1 % gridDim.z)
     for (int t = threadIdx.x; t < a.skctr_n; t += blockDim.x) a.skctr[t] = 0u;
+  if (a.sel_ghist) {  // the selection's coarse histograms: every CTA clears its slice
+    const int64_t nw = (int64_t)a.B * a.Hq * kNB / 4;  // uint4 words
+    const int64_t cta = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const int64_t nct = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+    uint4 *gh = reinterpret_cast<uint4 *>(a.sel_ghist);
+    for (int64_t t = nw * cta / nct + threadIdx.x; t < nw * (cta + 1) / nct; t += blockDim.x)
+      gh[t] = make_uint4(0u, 0u, 0u, 0u);
+  }
   if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
     const int uu = blockIdx.z, bb = uu / a.Hkv, kk = uu - bb * a.Hkv;
     const int64_t nz4 = (a.n_q + 3) / 4;  // float4s per row (rows are 64-float aligned)
@@ -116,6 +124,12 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
         hs[h].amax = __float_as_uint(A);
         hs[h].M = INT_MIN;     // folded by the scan / resident epilogues (atomics)
         hs[h].zmin = INT_MAX;
+        hs[h].S = 0ull;        // the selection's accumulators and counters (hc_select_pass.cu)
+        hs[h].mass_before = 0ull;
+        hs[h].c1_done = 0u;
+        hs[h].c2_done = 0u;
+        hs[h].ticket = 0u;
+        hs[h].state = 0u;
       }
     }
   }
