@@ -245,9 +245,11 @@ class Workload:
         self.shard = None
         self.comm = None
 
-    def enable_sharding(self, comm):
-        from paper_2507_19823_b200.sharded import GpuShard
-        self.shard = GpuShard(self.kc, self.vs, self.bud)
+    def enable_sharding(self, comm, rank: int, world: int):
+        """The product path: one hc_decode_attention_sharded call per layer, the library
+        issuing the NCCL exchanges on the stream (comm: hc.NcclComm)."""
+        from paper_2507_19823_b200.sharded import CAbiShard
+        self.shard = CAbiShard(self.kc, self.vs, self.bud, rank, world, self.base, comm)
         self.comm = comm
 
     def reset_counts(self):
@@ -286,7 +288,6 @@ class Workload:
 
     def step(self, profile=False):
         import paper_2507_19823_b200 as hc
-        from paper_2507_19823_b200 import sharded
         if self.parts:
             return self.step_pipelined(profile)
         for l in range(self.cfg["L"]):
@@ -303,7 +304,7 @@ class Workload:
                 hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
                                     sel_k=self.sel_k[l], ws=self.ws)
             else:
-                o = sharded.decode_layer(self.shard, self.comm, self.q[l], l, self.base)
+                o = self.shard.decode_layer(self.q[l], l)
                 self.out[l].copy_(o.view_as(self.out[l]))
                 self.sel_k[l].copy_(self.shard.sel_k.view_as(self.sel_k[l]))
 
@@ -879,8 +880,20 @@ def main():
     if cfg.get("host_frac_auto") and wl.hetero is not None and not wl.parts:
         calibrate_host_frac(wl, cfg)
     if sharded_mode:
-        from paper_2507_19823_b200.sharded import TorchComm
-        wl.enable_sharding(TorchComm())
+        import paper_2507_19823_b200 as hc
+        if backend == "nccl":
+            wl.enable_sharding(hc.NcclComm.from_process_group(), rank, world)
+        else:  # HC_BENCH_BACKEND=gloo code-path smoke on one GPU: the phases with gloo collectives
+            from paper_2507_19823_b200.sharded import GpuShard, TorchComm, decode_layer
+
+            class _PhaseShard:
+                def __init__(self, wl_):
+                    self.g, self.c, self.wl = GpuShard(wl_.kc, wl_.vs, wl_.bud), TorchComm(), wl_
+                    self.sel_k = self.g.sel_k
+
+                def decode_layer(self, q, l):
+                    return decode_layer(self.g, self.c, q, l, self.wl.base)
+            wl.shard = _PhaseShard(wl)
     torch.cuda.synchronize()
     # eager correctness sanity (one step) then capture the step with scan events
     wl.reset_counts()

@@ -36,7 +36,7 @@ typedef enum {
     HC_ERR_CAPACITY = 4,    /* append beyond n_cap */
     HC_ERR_EMPTY = 5,       /* no candidates (n_q + n_res == 0) */
     HC_ERR_CUDA = 6,        /* a CUDA runtime error (launch or earlier async fault) */
-    HC_ERR_NCCL = 7,        /* reserved for the sequence-sharded path */
+    HC_ERR_NCCL = 7,        /* an NCCL call of the sequence-sharded path failed */
     HC_ERR_UNSUPPORTED = 8, /* valid but not built for (e.g. c > 8192, G not in {1,2,4}) */
     HC_ERR_WORKSPACE = 9    /* workspace NULL or smaller than *_workspace_bytes() */
 } hc_status;
@@ -369,6 +369,32 @@ hc_status hc_add_partial(float *out, const float *part, int64_t n, hc_stream_t s
  * kept index set equals the unsharded one bit for bit (R-invariance).  The workspace
  * (hc_shard_workspace_bytes) carries state between the phases of one layer. */
 size_t hc_shard_workspace_bytes(const hc_kcache *kc, hc_budget budget);
+
+/* ---- The sequence-sharded decode in ONE call: the five phases below
+ * with the four exchanges between them issued by the library as NCCL collectives on `stream`
+ * (all-reduce MAX of the score range, all-reduce SUM of the two integer histograms,
+ * all-gather of the per-rank (strict, tie) counts, all-reduce SUM of the Eq. 5 numerators):
+ * one layer, this rank's shard [shard_base, shard_base + n_q[layer]) of every unit, the
+ * global Eq. 4 selection and the full output out [B][Hq][d] fp32 on every rank.
+ *   sel_idx / sel_w [B*Hq][k_max] (required): this rank's kept tokens (GLOBAL indices,
+ *     ascending) at their GLOBAL positions of each row's list; other ranks' slots untouched;
+ *   sel_k [B*Hq] (optional): the global k_sel.
+ * comm: an NCCL communicator of the `world` ranks (hc_nccl_comm_init, or any ncclComm_t of
+ * the process's libnccl.so.2); NULL only with world == 1.  ws >= hc_decode_sharded_workspace_
+ * bytes(kc, budget, world) (phase state + exchange buffers).  Graph-capturable (NCCL
+ * collectives are).  NCCL is loaded at run time (dlopen libnccl.so.2, HC_NCCL_LIB overrides);
+ * NCCL failures return HC_ERR_NCCL. */
+typedef struct ncclComm *ncclComm_t; /* NCCL's opaque communicator (nccl.h) */
+#define HC_NCCL_UNIQUE_ID_BYTES 128
+hc_status hc_nccl_get_unique_id(void *id /* HC_NCCL_UNIQUE_ID_BYTES bytes, host */);
+hc_status hc_nccl_comm_init(ncclComm_t *comm, int32_t world, const void *id, int32_t rank);
+hc_status hc_nccl_comm_destroy(ncclComm_t comm);
+size_t hc_decode_sharded_workspace_bytes(const hc_kcache *kc, hc_budget budget, int32_t world);
+hc_status hc_decode_attention_sharded(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
+                                      int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
+                                      float *sel_w, int64_t *sel_k, int32_t rank, int32_t world,
+                                      int64_t shard_base, ncclComm_t comm, void *ws, size_t ws_bytes,
+                                      hc_stream_t stream);
 hc_status hc_shard_begin(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs, int32_t layer,
                          hc_budget budget, int32_t *stats, void *ws, size_t ws_bytes,
                          hc_stream_t stream);

@@ -31,7 +31,9 @@ EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_ev
            "hc_host_weighted_sum_range", "hc_enqueue_host_weighted_sum_range", "hc_gather_values",
            "hc_add_partial", "hc_host_register", "hc_host_unregister", "hc_host_worker_create",
            "hc_host_worker_destroy", "hc_host_worker_add_job", "hc_host_worker_submit",
-           "hc_host_worker_wait", "hc_host_worker_status", "hc_host_worker_pause"]
+           "hc_host_worker_wait", "hc_host_worker_status", "hc_host_worker_pause",
+           "hc_nccl_get_unique_id", "hc_nccl_comm_init", "hc_nccl_comm_destroy",
+           "hc_decode_sharded_workspace_bytes", "hc_decode_attention_sharded"]
 
 
 class HcError(RuntimeError):
@@ -132,6 +134,18 @@ def lib():
                   "hc_host_worker_submit", "hc_host_worker_wait", "hc_host_worker_status",
                   "hc_host_worker_pause"):
             getattr(L, f).restype = i32
+        L.hc_nccl_get_unique_id.argtypes = [p]
+        L.hc_nccl_get_unique_id.restype = i32
+        L.hc_nccl_comm_init.argtypes = [C.POINTER(C.c_void_p), i32, p, i32]
+        L.hc_nccl_comm_init.restype = i32
+        L.hc_nccl_comm_destroy.argtypes = [p]
+        L.hc_nccl_comm_destroy.restype = i32
+        L.hc_decode_sharded_workspace_bytes.argtypes = [C.POINTER(hc_kcache), hc_budget, i32]
+        L.hc_decode_sharded_workspace_bytes.restype = C.c_size_t
+        L.hc_decode_attention_sharded.argtypes = [p, C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32,
+                                                  hc_budget, p, p, p, p, i32, i32, i64, p, p,
+                                                  C.c_size_t, p]
+        L.hc_decode_attention_sharded.restype = i32
         L.hc_blockwise_attention.argtypes = [p, p, p, i64, i32, i32, i32, i64, p, p]
         L.hc_blockwise_attention.restype = i32
         L.hc_prefill_append.argtypes = [C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p, i64, p]
@@ -618,3 +632,41 @@ class HostWorker:
             self.close()
         except Exception:
             pass
+
+
+# ----------------------------------------------------------------------------- NCCL (sharded decode)
+NCCL_UNIQUE_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """hc_nccl_get_unique_id: a fresh NCCL unique id (rank 0 makes it, the others receive it)."""
+    buf = (C.c_char * NCCL_UNIQUE_ID_BYTES)()
+    _check(lib().hc_nccl_get_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """An NCCL communicator of `world` ranks made by hc_nccl_comm_init (the library's
+    libnccl.so.2 -- inside a PyTorch process, the one torch loaded)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes):
+        if len(uid) != NCCL_UNIQUE_ID_BYTES:
+            raise ValueError("uid must be NCCL_UNIQUE_ID_BYTES long")
+        h = C.c_void_p()
+        buf = (C.c_char * NCCL_UNIQUE_ID_BYTES).from_buffer_copy(uid)
+        _check(lib().hc_nccl_comm_init(C.byref(h), int(world), buf, int(rank)))
+        self.h, self.world, self.rank = h, int(world), int(rank)
+
+    @staticmethod
+    def from_process_group(group=None) -> "NcclComm":
+        """Rank 0 makes the unique id; torch.distributed broadcasts it (plumbing only)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return NcclComm(world, rank, obj[0])
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib().hc_nccl_comm_destroy(self.h)
+            self.h = None

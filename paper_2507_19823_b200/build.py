@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhc.so")
 SOURCES = ["hc_api.cu", "hc_encode.cu", "hc_table.cu", "hc_scan.cu", "hc_select.cu",
            "hc_select_fused.cu", "hc_select_pass.cu", "hc_shard.cu", "hc_host.cu", "hc_gather.cu", "hc_group.cu", "hc_kmeans.cu",
-           "hc_prefill.cu"]
+           "hc_prefill.cu", "hc_nccl.cu"]
 HEADERS = ["hc_device.cuh", "hc_internal.h"]
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(log)
     if force or jobs or _stale(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp",
-             *objs, "-lgomp"])
+             *objs, "-lgomp", "-ldl"])
         os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -49,6 +49,15 @@ hc_status fail(hc_status st, const char *fmt, ...) {
   return st;
 }
 
+}  // namespace
+
+int hc::set_error(int st, const char *msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return st;
+}
+
+namespace {
+
 hc_status cuda_check(cudaError_t e, const char *what) {
   if (e != cudaSuccess) return fail(HC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return HC_OK;

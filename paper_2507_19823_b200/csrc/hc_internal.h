@@ -12,6 +12,8 @@ constexpr int kSkMaxCtas = 160;  // stream-K scan: max persistent CTAs (partial 
 
 // number of kernels this library has enqueued (or captured into a graph)
 void note_launch(int n = 1);
+// set the thread's hc_last_error() message; returns st
+int set_error(int st, const char *msg);
 
 // Programmatic dependent launch (PDL) along the decode chain (encode -> table -> [resident]
 // -> scan -> select -> gather -> next layer's encode): each chain kernel triggers its

@@ -8,6 +8,8 @@
 // the scan does ONE shared-memory lookup per (token, group) for all G heads.
 // Entries m >= c are zero (the scan masks codes to cpow2-1).
 #include <float.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "hc_internal.h"
 
@@ -196,8 +198,161 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Codebook-stationary table build (default): CTA = (centroid chunk, group i).  The chunk's
+// codebook rows are loaded ONCE into registers and the CTA loops over every (b, kv) unit,
+// writing that unit's T entries for the chunk -- the codebook is read from L2 once per layer
+// instead of once per unit (config 3: 4 MiB instead of 128 MiB), and every store instruction
+// writes 256 consecutive 8-byte entries.  The per-head scale exponents (R2's bound, which
+// needs every group of q) are computed first by each CTA into shared memory: one warp per
+// head, lanes over groups.  Same arithmetic as k_table (the oracle's or_table_bits).
+constexpr int kT2Threads = 256;
+// query heads B*Hq whose scales and q̄_i a CTA stages (shared memory)
+template <int DBAR>
+constexpr int t2_max_rows() { return DBAR <= 8 ? 1024 : 512; }
+
+template <int G, int DBAR>
+__global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
+  constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;  // centroids per thread
+  constexpr int kTC = kT2Threads * CPT;           // centroids per CTA
+  constexpr int kRows = t2_max_rows<DBAR>();
+  __shared__ float s_sc[kRows];           // 2^e per query head
+  __shared__ float s_q[kRows * DBAR];     // q̄_i (group i of this CTA) per query head
+  pdl_trigger();
+  pdl_wait();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int i = blockIdx.y;
+  const int m0 = blockIdx.x * kTC;
+  const int rows = a.B * a.Hq, units = a.B * a.Hkv;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x, nct = (int64_t)gridDim.x * gridDim.y;
+  // ---- housekeeping of this layer's later kernels, spread over the CTAs
+  if (a.gdone && cta == 0)
+    for (int k = t; k < a.gdone_n; k += kT2Threads) a.gdone[k] = 0u;
+  if (a.skctr && cta == 1 % nct)
+    for (int k = t; k < a.skctr_n; k += kT2Threads) a.skctr[k] = 0u;
+  if (a.sel_ghist) {
+    const int64_t nw = (int64_t)rows * kNB / 4;
+    uint4 *gh = reinterpret_cast<uint4 *>(a.sel_ghist);
+    for (int64_t k = nw * cta / nct + t; k < nw * (cta + 1) / nct; k += kT2Threads) gh[k] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
+    const int64_t nz4 = (a.n_q + 3) / 4, tot = (int64_t)rows * nz4;
+    for (int64_t k = tot * cta / nct + t; k < tot * (cta + 1) / nct; k += kT2Threads) {
+      const int64_t r = k / nz4, q4 = k - r * nz4;
+      reinterpret_cast<float4 *>(a.z + r * a.z_stride)[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  // ---- R2 scales: A_h = max_i fmaf-chain_e(|q_h[i*dbar+e]|, Cabs[ci][e]); one warp per head
+  for (int r = warp; r < rows; r += kT2Threads / 32) {
+    const uint16_t *qh = a.q + (int64_t)r * a.d;
+    float bnd = 0.0f;
+    for (int gi = lane; gi < a.g; gi += 32) {
+      const float *ca = a.cb_absmax + (int64_t)(a.cbg == 1 ? 0 : gi) * DBAR;
+      float bb = __fmul_rn(fabsf(h2f(__ldg(qh + gi * DBAR))), __ldg(ca));
+#pragma unroll
+      for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(h2f(__ldg(qh + gi * DBAR + e))), __ldg(ca + e), bb);
+      bnd = fmaxf(bnd, bb);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) bnd = fmaxf(bnd, __shfl_xor_sync(0xffffffffu, bnd, off));
+    const int e = a.lut8 ? scale_exponent8(bnd) : scale_exponent(bnd);
+    if (lane == 0) {
+      s_sc[r] = pow2f(e);
+      if (cta == 0) {  // the heads' selection state for this layer
+        HeadState *hs = a.hs + r;
+        hs->e = e;
+        hs->kappa = __fmul_rn(a.kappa0, pow2f(-e));
+        hs->amax = __float_as_uint(bnd);
+        hs->M = INT_MIN;  // folded by the scan / resident epilogues (atomics)
+        hs->zmin = INT_MAX;
+        hs->S = 0ull;     // the selection's accumulators and counters (hc_select_pass.cu)
+        hs->mass_before = 0ull;
+        hs->c1_done = 0u;
+        hs->c2_done = 0u;
+        hs->ticket = 0u;
+        hs->state = 0u;
+      }
+    }
+    if (lane < DBAR) s_q[r * DBAR + lane] = h2f(__ldg(qh + i * DBAR + lane));
+  }
+  __syncthreads();
+  // ---- this CTA's codebook rows, once
+  const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
+  float cm[CPT][DBAR];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int m = m0 + t + k * kT2Threads;
+#pragma unroll
+    for (int e = 0; e < DBAR; ++e) cm[k][e] = m < a.c ? __ldg(Ci + (int64_t)m * DBAR + e) : 0.0f;
+  }
+  // ---- every unit's entries for these centroids (entries m >= c are 0)
+  for (int u = 0; u < units; ++u) {
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int r0 = b * a.Hq + kv * G;
+    float qs[G][DBAR], sc[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      sc[h] = s_sc[r0 + h];
+#pragma unroll
+      for (int e = 0; e < DBAR; ++e) qs[h][e] = s_q[(r0 + h) * DBAR + e];
+    }
+    int16_t *Tu = a.T + ((int64_t)u * a.g + i) * a.cpow2 * G;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int m = m0 + t + k * kT2Threads;
+      if (m >= a.cpow2) break;
+      float tv[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) {  // the R2 FMA chain (or_table_bits)
+        float acc = __fmul_rn(qs[h][0], cm[k][0]);
+#pragma unroll
+        for (int e = 1; e < DBAR; ++e) acc = __fmaf_rn(qs[h][e], cm[k][e], acc);
+        tv[h] = m < a.c ? acc : 0.0f;
+      }
+      if (G == 4 && a.lut8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
+        uint32_t wv = 0;
+#pragma unroll
+        for (int h = 0; h < G; ++h) wv |= (uint32_t)(quant_t8_d(tv[h], sc[h]) + 128) << (8 * h);
+        reinterpret_cast<uint32_t *>(a.T)[((int64_t)u * a.g + i) * a.cpow2 + m] = wv;
+        continue;
+      }
+      int16_t pk[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) pk[h] = (int16_t)quant_t_d(tv[h], sc[h]);
+      int16_t *dst = Tu + (int64_t)m * G;
+      if constexpr (G == 4) {  // even heads +32768-biased (hc_scan.cu Lut)
+        uint2 v;
+        v.x = (uint32_t)(pk[0] + 32768) | ((uint32_t)(uint16_t)pk[1] << 16);
+        v.y = (uint32_t)(pk[2] + 32768) | ((uint32_t)(uint16_t)pk[3] << 16);
+        *reinterpret_cast<uint2 *>(dst) = v;
+      } else if constexpr (G == 2) {
+        *reinterpret_cast<uint32_t *>(dst) = (uint32_t)(pk[0] + 32768) | ((uint32_t)(uint16_t)pk[1] << 16);
+      } else {
+        dst[0] = pk[0];
+      }
+    }
+  }
+}
+
+static bool table2_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *ev = getenv("HC_TABLE");
+    v = (ev && !strcmp(ev, "old")) ? 0 : 1;
+  }
+  return v != 0;
+}
+
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
+  if (table2_enabled() && a.B * a.Hq <= t2_max_rows<DBAR>()) {
+    constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;
+    constexpr int kTC = kT2Threads * CPT;
+    dim3 grid((unsigned)((a.cpow2 + kTC - 1) / kTC), (unsigned)a.g);
+    launch_chain(k_table2<G, DBAR>, grid, dim3(kT2Threads), 0, s, a);
+    note_launch();
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)a.tsplit, (unsigned)a.g, (unsigned)(a.B * a.Hkv));
   launch_chain(k_table<G, DBAR>, grid, dim3(kTB), 0, s, a);
   note_launch();

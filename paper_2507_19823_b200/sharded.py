@@ -12,11 +12,16 @@ Rank r of R holds the contiguous global token range [base_r, base_r + n_r) of ev
 
 Everything that decides the kept set is an exact integer, and every rank evaluates the
 same bounds on the same reduced integers, so the selection is identical to the
-unsharded one (R-invariance).  ``decode_layer`` runs one layer with any
-``comm`` that provides the four collectives: ``TorchComm`` (torch.distributed: NCCL over
-NVLink on B200s, gloo on CPU) or ``VirtualComm`` (R shards driven in lock-step in one
-process, collectives as tensor reductions -- used to test the sharded kernels on one GPU
-without ranks that wait on each other).
+unsharded one (R-invariance).
+
+Two drivers of the same phases:
+  ``CAbiShard`` -- the product path: ONE C-ABI call per layer (hc_decode_attention_sharded),
+      the library issues the collectives itself as NCCL calls on the stream (``hc.NcclComm``,
+      graph-capturable); Python only builds the communicator.
+  ``decode_layer`` -- the phases one by one with any ``comm`` providing the four collectives:
+      ``TorchComm`` (torch.distributed, e.g. gloo on CPU for the protocol tests) or the
+      lock-step ``decode_layer_virtual`` (R shards in one process, collectives as tensor
+      reductions -- tests the sharded kernels on one GPU without ranks that wait on each other).
 """
 from __future__ import annotations
 
@@ -137,4 +142,37 @@ class GpuShard:
                                     hc._ptr(self.out), hc._ptr(self.sel_idx), hc._ptr(self.sel_w),
                                     hc._ptr(self.sel_k), hc._ptr(self.ws.t), self.ws.nbytes,
                                     hc._stream()))
+        return self.out
+
+
+class CAbiShard:
+    """This rank's shard driven through hc_decode_attention_sharded (include/hc.h): the five
+    phases and the four NCCL exchanges in one library call per layer."""
+
+    def __init__(self, kc, vs, bud, rank: int, world: int, base: int, comm=None, device="cuda"):
+        import torch
+
+        import paper_2507_19823_b200 as hc
+        if world > 1 and comm is None:
+            raise ValueError("world > 1 needs an hc.NcclComm")
+        self.hc, self.kc, self.vs, self.bud = hc, kc, vs, bud
+        self.rank, self.world, self.base, self.comm = int(rank), int(world), int(base), comm
+        rows = kc.B * kc.Hq
+        nb = int(hc.lib().hc_decode_sharded_workspace_bytes(C.byref(kc.s), bud, self.world))
+        self.ws = hc.Workspace(nb, device)
+        km = int(bud.k_max)
+        self.out = torch.empty((rows, kc.d), dtype=torch.float32, device=device)
+        self.sel_idx = torch.full((rows, km), -1, dtype=torch.int32, device=device)
+        self.sel_w = torch.zeros((rows, km), dtype=torch.float32, device=device)
+        self.sel_k = torch.zeros((rows,), dtype=torch.int64, device=device)
+
+    def decode_layer(self, q, layer: int):
+        """q [B][Hq][d] fp16 -> out [B*Hq][d] fp32 (the full Eq. 5 output, on every rank)."""
+        hc, L = self.hc, self.hc.lib()
+        vs = self.vs.struct()
+        hc._check(L.hc_decode_attention_sharded(
+            hc._ptr(q), C.byref(self.kc.s), C.byref(vs), layer, self.bud, hc._ptr(self.out),
+            hc._ptr(self.sel_idx), hc._ptr(self.sel_w), hc._ptr(self.sel_k), self.rank, self.world,
+            self.base, self.comm.h if self.comm is not None else None, hc._ptr(self.ws.t),
+            self.ws.nbytes, hc._stream()))
         return self.out

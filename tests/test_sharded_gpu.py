@@ -101,3 +101,62 @@ def test_virtual_shards_fuzz(R, n, tau, k_max, seed):
             assert np.array_equal(sel[row, :k], ref["idx"][h])
             err = np.abs(out[row] - ref["out"][h])
             assert np.all(err <= TOL_ABS + TOL_REL * np.abs(ref["out"][h]))
+
+
+@pytest.mark.parametrize("use_nccl", [True, False])
+def test_cabi_sharded_entry_world1(use_nccl):
+    """hc_decode_attention_sharded (the phases + NCCL exchanges in one C-ABI call) on a
+    1-rank NCCL communicator (the only world one GPU can host): equals the unsharded oracle
+    bit for bit on index sets; eager and CUDA-graph replay."""
+    import torch
+    import paper_2507_19823_b200 as hc
+    from harness import shard_caches
+    from paper_2507_19823_b200.sharded import CAbiShard
+    case = Case(B=2, Hkv=2, n=20011, tau=0.9, k_max=2500, seed=71)
+    (kc, vs, base), = shard_caches(case, 1)
+    comm = hc.NcclComm(1, 0, hc.nccl_unique_id()) if use_nccl else None
+    sh = CAbiShard(kc, vs, hc.budget(case.tau, case.k_max), 0, 1, base, comm)
+    q = torch.from_numpy(np.stack([case.query(b, 0) for b in range(case.B)])).cuda()
+
+    def check(out):
+        o = out.view(case.B, case.Hq, -1).cpu().numpy()
+        sel = sh.sel_idx.view(case.B, case.Hq, -1).cpu().numpy()
+        ks = sh.sel_k.view(case.B, case.Hq).cpu().numpy()
+        for b in range(case.B):
+            for kv in range(case.Hkv):
+                ref = oracle_unit(case, b, 0, kv)
+                for h in range(case.G):
+                    hq = kv * case.G + h
+                    k = int(ks[b, hq])
+                    assert k == ref["k_sel"][h]
+                    assert np.array_equal(sel[b, hq, :k], ref["idx"][h])
+                    err = np.abs(o[b, hq] - ref["out"][h])
+                    assert np.all(err <= TOL_ABS + TOL_REL * np.abs(ref["out"][h]))
+
+    out = sh.decode_layer(q, 0)
+    torch.cuda.synchronize()
+    check(out)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            sh.decode_layer(q, 0)
+    torch.cuda.current_stream().wait_stream(s)
+    sh.out.fill_(float("nan"))
+    sh.sel_idx.fill_(-1)
+    g.replay()
+    torch.cuda.synchronize()
+    check(sh.out)
+    if comm is not None:
+        comm.close()
+
+
+def test_cabi_sharded_entry_rejects_missing_comm():
+    import paper_2507_19823_b200 as hc
+    from harness import shard_caches
+    from paper_2507_19823_b200.sharded import CAbiShard
+    case = Case(B=1, Hkv=1, n=1000, k_max=100, seed=3)
+    (kc, vs, base), = shard_caches(case, 1)
+    with pytest.raises(ValueError):
+        CAbiShard(kc, vs, hc.budget(0.9, 100), 0, 2, base, None)
