@@ -963,7 +963,7 @@ def main():
                 mem = measure_host_rows_gbs(wl)
                 hw = measure_host_dram_hw(wl)
                 pk_eng = max(mem["combined"], mem["host_alone"], mem["gpu_alone"])
-                pk_mem = hw["random_rows_gbs"]
+                pk_mem = hw["peak_gbs"]
                 both = (h_bytes + v_bytes) / (ms_per_step * 1e-3) / 1e9
                 host_dram = {"bytes_per_step": h_bytes, "rows": "union of the GQA heads' kept rows, "
                              "index < t_split", "achieved_gbs_lower_bound": h_bytes / (ms_per_step * 1e-3) / 1e9,

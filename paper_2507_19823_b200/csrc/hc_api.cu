@@ -135,8 +135,8 @@ struct Layout {
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
       o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, o_sgh, o_sfc, o_sfm,
-      o_slb, total;
-  int64_t slb_n;
+      o_scl, o_spre, o_slist, total;
+  int64_t snch, scap;
   int skctr_n;
   int nch_max;  // sharded compaction chunks
 };
@@ -158,12 +158,16 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
   L.o_cbabs = o; o += align256((size_t)kc->vq.cbg * (d / g) * 4);
   L.o_z = o; o += align256((size_t)rows * L.z_stride * 4);
   L.o_zpart = o;  // (no partial planes: split scans accumulate exactly into z)
-  // selection passes (hc_select_pass.cu): coarse / fine histograms, look-back words
-  L.slb_n = select_lb_chunks(ncand_max > 0 ? ncand_max : 1);
+  // selection passes (hc_select_pass.cu): coarse / fine histograms, per-chunk counters and
+  // prefixes, the in-range token lists
+  L.snch = select_chunks(ncand_max > 0 ? ncand_max : 1);
+  L.scap = select_list_cap(ncand_max > 0 ? ncand_max : 1);
   L.o_sgh = o; o += align256((size_t)rows * kNB * 4);
   L.o_sfc = o; o += align256((size_t)rows * kNB * 4);
   L.o_sfm = o; o += align256((size_t)rows * kNB * 8);
-  L.o_slb = o; o += align256((size_t)rows * L.slb_n * 8);
+  L.o_scl = o; o += align256((size_t)rows * L.snch * 4);
+  L.o_spre = o; o += align256((size_t)rows * L.snch * 8);
+  L.o_slist = o; o += align256((size_t)rows * L.scap * 8);
   L.o_idx = o; o += align256((size_t)rows * L.k_eff * 4);
   L.o_w = o; o += align256((size_t)rows * L.k_eff * 4);
   L.nch_max = shard_chunks(ncand_max > 0 ? ncand_max : 1);
@@ -638,8 +642,11 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.ghist = (uint32_t *)((uint8_t *)ws + Lw.o_sgh);
   sa.fcnt = (uint32_t *)((uint8_t *)ws + Lw.o_sfc);
   sa.fmass = (unsigned long long *)((uint8_t *)ws + Lw.o_sfm);
-  sa.lb = (unsigned long long *)((uint8_t *)ws + Lw.o_slb);
-  sa.lb_n = Lw.slb_n;
+  sa.cntlo = (uint32_t *)((uint8_t *)ws + Lw.o_scl);
+  sa.pre = (unsigned long long *)((uint8_t *)ws + Lw.o_spre);
+  sa.list = (unsigned long long *)((uint8_t *)ws + Lw.o_slist);
+  sa.nch = select_chunks(n_cand);
+  sa.cap = Lw.scap;
   // the round-1 fused select kernel stays reachable for A/B measurements (HC_SELECT=fused) and
   // for Eq. 5 inside the select kernel (HC_GATHER=fused)
   static int sel_old = -1;
@@ -834,7 +841,8 @@ size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {
   const int64_t zs = round_up(n, 64);
   return align256((size_t)rows * sizeof(HeadState)) + align256((size_t)rows * zs * 4) +
          align256((size_t)rows * kNB * 4) * 2 + align256((size_t)rows * kNB * 8) +
-         align256((size_t)rows * select_lb_chunks(n) * 8);
+         align256((size_t)rows * select_chunks(n) * 4) + align256((size_t)rows * select_chunks(n) * 8) +
+         align256((size_t)rows * select_list_cap(n) * 8);
 }
 
 hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d, hc_budget budget,
@@ -842,7 +850,7 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
                          hc_stream_t stream) {
   if (rows <= 0 || rows > 65535) return fail(HC_ERR_ARG, "rows must be in [1, 65535]");
   if (n <= 0) return fail(HC_ERR_EMPTY, "n == 0");
-  if (n >= (1ll << 31)) return fail(HC_ERR_UNSUPPORTED, "n >= 2^31");
+  if (n > (1ll << 27)) return fail(HC_ERR_UNSUPPORTED, "n > 2^27 (per-chunk selection state)");
   if (d <= 0) return fail(HC_ERR_ARG, "d <= 0");
   if (!scores || !idx || !w) return fail(HC_ERR_ARG, "NULL pointer");
   if (!(budget.tau > 0.0f && budget.tau <= 1.0f)) return fail(HC_ERR_ARG, "tau=%g not in (0,1]", budget.tau);
@@ -859,8 +867,11 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   sa.ghist = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
   sa.fcnt = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
   sa.fmass = (unsigned long long *)(w8 + o); o += align256((size_t)rows * kNB * 8);
-  sa.lb = (unsigned long long *)(w8 + o);
-  sa.lb_n = select_lb_chunks(n);
+  sa.cntlo = (uint32_t *)(w8 + o); o += align256((size_t)rows * select_chunks(n) * 4);
+  sa.pre = (unsigned long long *)(w8 + o); o += align256((size_t)rows * select_chunks(n) * 8);
+  sa.list = (unsigned long long *)(w8 + o);
+  sa.nch = select_chunks(n);
+  sa.cap = select_list_cap(n);
   cudaError_t e;
   const float kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
   if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s, sa.ghist)) != cudaSuccess)

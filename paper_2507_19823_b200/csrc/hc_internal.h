@@ -182,8 +182,10 @@ struct SelArgs {
   uint32_t *ghist;             // [rows][kNB]
   uint32_t *fcnt;              // [rows][kNB]
   unsigned long long *fmass;   // [rows][kNB]
-  unsigned long long *lb;      // [rows][lb_n]
-  int64_t lb_n;
+  uint32_t *cntlo;             // [rows][nch] per chunk: tokens above the refine range
+  unsigned long long *pre;     // [rows][nch] per chunk: exclusive (strict << 32 | ties) prefix
+  unsigned long long *list;    // [rows][cap] in-range tokens (index << 32 | Δ)
+  int64_t nch, cap;            // chunks per row (kSelChunk tokens each), list capacity per row
 };
 // fused rows a3-a5 (one cluster of CTAs per row; round 1, HC_SELECT=fused); nsplit: scan
 // partial planes in la.zpart
@@ -191,7 +193,9 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
                                 int num_sms, cudaStream_t st);
 // rows a3-a4 as three passes (hc_select_pass.cu, the default); nsplit > 1 adds a max/min pass
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st);
-int select_lb_chunks(int64_t n);
+constexpr int kSelChunk = 8192;  // tokens per write chunk
+inline int64_t select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChunk; }
+inline int64_t select_list_cap(int64_t n) { int64_t c = n / 16; return c < 4096 ? 4096 : c; }
 
 // sequence-sharded phases (hc_shard.cu)
 int shard_chunks(int64_t n);

@@ -11,17 +11,22 @@
 //                    by a slack that covers the exp2 polynomial's rounding), and keeps the
 //                    range of bins the exact cut can fall in (plus the k_max cap's bin, from
 //                    exact counts).  shift == 0 (bins = exact Δ values) resolves right there.
-//   K2 k_sel_refine  the exact mass of every token above that range (P_above) and exact
-//                    counts (exact masses too if the range spans more than kNB values) of
-//                    the tokens inside it; the last CTA walks them to the exact Δ*, the
-//                    number r of Δ* ties kept (lowest indices), k_sel, k*, the kept mass --
-//                    or, for a wide range, narrows it to one fine bin for a second K2
-//                    launch (a no-op when the first resolved).
-//   K3 k_sel_compact single-pass ordered compaction: CTAs take per-row chunk tickets in
-//                    order and chain (strict, tie) counts by decoupled look-back, so every
-//                    kept token's output position (ascending index) is known in one pass;
-//                    the kept (index, W/S) pairs are staged in shared memory and written
-//                    coalesced.
+//   K2 k_sel_refine  the exact mass of every token above that range (P_above; the W of
+//                    those ~15 % of the tokens computed 32 at a time from a warp queue, not
+//                    under divergence), exact counts (and exact masses if the range spans
+//                    more than kNB values) of the tokens inside it, per K3-chunk counts of the
+//                    tokens above the range, and the in-range tokens themselves (index, Δ) on
+//                    a per-row list; the last CTA walks the fine bins to the exact Δ*, the
+//                    number r of Δ* ties kept (lowest indices), k_sel, k*, the kept mass -- or,
+//                    for a wide range, narrows it to one fine bin.
+//   K4 k_sel_prefix  one CTA per row: (if narrowed) the second refine from the in-range list;
+//                    then every chunk's (strict, tie) counts -- the count above the range plus
+//                    its in-range tokens classified against Δ* -- and their exclusive prefix.
+//   K3 k_sel_write   independent CTAs per (row, chunk): the chunk's kept tokens at their
+//                    global positions (prefix + in-chunk scan), staged in shared memory and
+//                    written coalesced as (index, W/S).
+// A row whose in-range list overflowed its capacity (degenerate score distributions: heavy
+// ties) is finished by K4 from a pass over its z instead -- slower, equally exact.
 //
 // Every decision is integer arithmetic on exact quantities (counts, u64 masses, the
 // 128-bit threshold Θ), so the kept set equals the oracle's bit for bit (or_select: sort by
@@ -221,7 +226,6 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   __shared__ uint32_t hist[kNB];
   __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
-  __shared__ int s_found;
   pdl_trigger();
   pdl_wait();
   const int row = blockIdx.y, t = threadIdx.x;
@@ -231,15 +235,15 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   const int shift = sel_shift(M, zmin);
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
   for (int i = t; i < kNB; i += kST) hist[i] = 0u;
-  {  // this CTA's share of the row's refine histograms and look-back words (used by K2 / K3)
-    const int64_t nf = (int64_t)kNB, nl = s.lb_n;
+  {  // this CTA's share of the row's refine histograms and chunk counters (used by K2 / K4)
+    const int64_t nf = (int64_t)kNB, nl = s.nch;
     const int64_t f0 = nf * blockIdx.x / gridDim.x, f1 = nf * (blockIdx.x + 1) / gridDim.x;
     for (int64_t i = f0 + t; i < f1; i += kST) {
       s.fcnt[(int64_t)row * kNB + i] = 0u;
       s.fmass[(int64_t)row * kNB + i] = 0ull;
     }
     const int64_t l0 = nl * blockIdx.x / gridDim.x, l1 = nl * (blockIdx.x + 1) / gridDim.x;
-    for (int64_t i = l0 + t; i < l1; i += kST) s.lb[(int64_t)row * nl + i] = 0ull;
+    for (int64_t i = l0 + t; i < l1; i += kST) s.cntlo[(int64_t)row * nl + i] = 0u;
   }
   __syncthreads();
   unsigned long long S = 0;
@@ -296,12 +300,6 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
       __threadfence();
       hs->state = kStDone;
     }
-    return;
-  }
-  if (shift == 0) {  // coarse bins are exact Δ values: exact masses from the counts
-    if (t == 0) hs->mass_before = 0ull;
-    resolve_bins(hist, nullptr, 0, 0u, dmax, 0ull, 0ull, s, hs, row, kappa, theta, tau_all, cap_all, Sx,
-                 &s_found);
     return;
   }
   __shared__ unsigned long long sw[3][kST / 32];
@@ -389,51 +387,103 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
 }
 
 // ---------------------------------------------------------------------------- K2
-__global__ void __launch_bounds__(kST) k_sel_refine(SelArgs s, int64_t per, int pass) {
+// The CTA's token range is whole chunks; per chunk every thread holds 16 consecutive tokens.
+__global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   extern __shared__ __align__(16) uint8_t sm2[];
   uint32_t *fc = reinterpret_cast<uint32_t *>(sm2);                 // [kNB] fine counts
   uint32_t *fml = reinterpret_cast<uint32_t *>(sm2 + kNB * 4);      // [kNB] fine mass, low word
   uint32_t *fmh = reinterpret_cast<uint32_t *>(sm2 + kNB * 8);      // [kNB] high word
   unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(sm2 + kNB * 4);  // resolve: over fml/fmh
+  uint32_t *wq = reinterpret_cast<uint32_t *>(sm2 + kNB * 12);      // [kST/32][64] per-warp Δ queues
   __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
   __shared__ int s_found;
   pdl_trigger();
   pdl_wait();
-  const int row = blockIdx.y, t = threadIdx.x;
+  const int row = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   HeadState *hs = s.hs + row;
-  if (hs->state != (pass == 0 ? kStRefine1 : kStRefine2)) return;
+  if (hs->state != kStRefine1) return;
   const int M = hs->M;
   const float kappa = hs->kappa;
   const uint32_t lo = hs->r_lo, hi = hs->r_hi;
   const int f = hs->fshift;
-  const bool first = pass == 0;
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
   for (int i = t; i < kNB; i += kST) { fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u; }
   __syncthreads();
-  unsigned long long P = 0;
-  sel_tokens(s.z + (int64_t)row * s.z_stride, j0, j1, [&](float zf) {
-    const uint32_t dl = (uint32_t)(M - zint(zf));
-    if (dl < lo) {
-      if (first) P += wmass(dl, kappa);
-    } else if (dl <= hi) {
-      const uint32_t fb = (dl - lo) >> f;
-      atomicAdd(&fc[fb], 1u);
-      if (f > 0) {  // fine bins of several Δ values: their exact mass too
-        uint32_t wl, wh;
-        mass_parts(dl, kappa, wl, wh);
-        const uint32_t old = atomicAdd(&fml[fb], wl);
-        wh += (old + wl < old) ? 1u : 0u;
-        if (wh) atomicAdd(&fmh[fb], wh);
+  const float *zr = s.z + (int64_t)row * s.z_stride;
+  uint32_t *q = wq + warp * 64;
+  int qn = 0;                 // warp-uniform queue length
+  unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
+  unsigned long long *lst = s.list + (int64_t)row * s.cap;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t cb = j0; cb < j1; cb += kSelChunk) {
+    const int64_t tb = cb + (int64_t)t * 16;
+    const int64_t ce = min(j1, cb + (int64_t)kSelChunk);
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = tb + 4 * k;
+      if (p + 4 <= ce) {
+        const float4 x = *reinterpret_cast<const float4 *>(zr + p);
+        v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[4 * k + u] = p + u < ce ? zr[p + u] : 0.0f;
       }
     }
-  });
-  if (first) {
-    P = warp_sum_u64(P);
-    if ((t & 31) == 0) s_red[t >> 5] = P;
+    uint32_t nlo = 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const bool valid = tb + u < ce;
+      const uint32_t dl = (uint32_t)(M - zint(v[u]));
+      const bool above = valid && dl < lo;
+      const bool inr = valid && dl >= lo && dl <= hi;
+      nlo += above ? 1u : 0u;
+      // the exact W of the tokens above the range, 32 at a time from the warp's queue
+      const unsigned ma = __ballot_sync(0xffffffffu, above);
+      if (ma) {
+        if (above) q[qn + __popc(ma & lt)] = dl;
+        qn += __popc(ma);
+        if (qn >= 32) {
+          __syncwarp();
+          P += wmass(q[lane], kappa);
+          const uint32_t rest = lane + 32 < qn ? q[lane + 32] : 0u;
+          __syncwarp();
+          if (lane + 32 < qn) q[lane] = rest;
+          qn -= 32;
+          __syncwarp();
+        }
+      }
+      const unsigned mr = __ballot_sync(0xffffffffu, inr);
+      if (mr) {  // in-range: fine histogram + the row's in-range list (warp-aggregated append)
+        unsigned base = 0;
+        if (lane == __ffs(mr) - 1) base = atomicAdd(&hs->ticket, (unsigned)__popc(mr));
+        base = __shfl_sync(0xffffffffu, base, __ffs(mr) - 1);
+        if (inr) {
+          const uint32_t fb = (dl - lo) >> f;
+          atomicAdd(&fc[fb], 1u);
+          if (f > 0) {  // fine bins of several Δ values: their exact mass too
+            uint32_t wl, wh;
+            mass_parts(dl, kappa, wl, wh);
+            const uint32_t old = atomicAdd(&fml[fb], wl);
+            wh += (old + wl < old) ? 1u : 0u;
+            if (wh) atomicAdd(&fmh[fb], wh);
+          }
+          const unsigned pos = base + __popc(mr & lt);
+          if (pos < (unsigned)s.cap) lst[pos] = ((unsigned long long)(tb + u) << 32) | dl;
+        }
+      }
+    }
+    // the chunk's count of tokens above the range (K4 adds its in-range tokens below Δ*)
+    nlo = __reduce_add_sync(0xffffffffu, nlo);
+    if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + cb / kSelChunk], nlo);
   }
+  __syncwarp();
+  if (lane < qn) P += wmass(q[lane], kappa);
+  P = warp_sum_u64(P);
+  if (lane == 0) s_red[warp] = P;
   __syncthreads();
-  if (first && t == 0) {
+  if (t == 0) {
     unsigned long long tot = 0;
     for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
     if (tot) atomicAdd((unsigned long long *)&hs->mass_before, tot);
@@ -464,8 +514,6 @@ __global__ void __launch_bounds__(kST) k_sel_refine(SelArgs s, int64_t per, int 
   }
   if (t == 0) hs->c2_done = 0u;
   __syncthreads();
-  // the histograms are read: clear them for a second pass / the next call
-  for (int i = t; i < kNB; i += kST) { gc[i] = 0u; gm[i] = 0ull; }
   const unsigned long long Sx = hs->S, theta = hs->theta;
   const bool tau_all = s.tau_q >= (1u << 24);
   const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
@@ -474,117 +522,167 @@ __global__ void __launch_bounds__(kST) k_sel_refine(SelArgs s, int64_t per, int 
                cap_all, Sx, &s_found);
 }
 
-// ---------------------------------------------------------------------------- K3
-// look-back word: [flag 2 bits (1 aggregate, 2 inclusive prefix)][strict 31][ties 31]
-__device__ __forceinline__ unsigned long long lb_pack(uint32_t flag, uint32_t ns, uint32_t nt) {
-  return ((unsigned long long)flag << 62) | ((unsigned long long)ns << 31) | nt;
-}
-
-template <int TPT>
-__global__ void __launch_bounds__(kST) k_sel_compact(SelArgs s) {
-  constexpr int kChunk = kST * TPT;
-  extern __shared__ __align__(16) uint8_t sm[];
-  uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm);                // [kChunk] Δ of kept tokens
-  uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm + kChunk * 4);   // [kChunk] offset in chunk
+// ---------------------------------------------------------------------------- K4
+// One CTA per row.  Dynamic shared memory: strict / tie counts per chunk [2][nch] (+ the
+// second refine's fine counts [kNB]).
+__global__ void __launch_bounds__(kST) k_sel_prefix(SelArgs s) {
+  extern __shared__ __align__(16) uint8_t sm4[];
+  uint32_t *cs = reinterpret_cast<uint32_t *>(sm4);       // [nch] strict
+  uint32_t *ct = cs + s.nch;                               // [nch] ties
+  uint32_t *fc = ct + s.nch;                               // [kNB] second-refine counts
   __shared__ unsigned long long sw[2][kST / 32];
-  __shared__ int s_ticket;
-  __shared__ unsigned long long s_pre;
+  __shared__ int s_found;
   pdl_trigger();
   pdl_wait();
-  const int row = blockIdx.y, t = threadIdx.x, lane = t & 31;
+  const int row = blockIdx.x, t = threadIdx.x;
   HeadState *hs = s.hs + row;
-  if (t == 0) s_ticket = (int)atomicAdd(&hs->ticket, 1u);
+  const float *zr = s.z + (int64_t)row * s.z_stride;
+  const unsigned long long *lst = s.list + (int64_t)row * s.cap;
+  const unsigned long long nl = hs->ticket;               // in-range tokens of K2 (may exceed cap)
+  const bool complete = nl <= (unsigned long long)s.cap;
+  const int M = hs->M;
+  const float kappa = hs->kappa;
+  if (hs->state == kStRefine2) {  // the boundary fine bin [r_lo, r_hi]: exact counts per Δ
+    const uint32_t lo = hs->r_lo, hi = hs->r_hi;
+    for (int i = t; i < kNB; i += kST) fc[i] = 0u;
+    __syncthreads();
+    if (complete) {
+      for (unsigned long long e = t; e < nl; e += kST) {
+        const uint32_t dl = (uint32_t)lst[e];
+        if (dl >= lo && dl <= hi) atomicAdd(&fc[dl - lo], 1u);
+      }
+    } else {
+      for (int64_t j = t; j < s.n; j += kST) {
+        const uint32_t dl = (uint32_t)(M - zint(zr[j]));
+        if (dl >= lo && dl <= hi) atomicAdd(&fc[dl - lo], 1u);
+      }
+    }
+    __syncthreads();
+    const bool tau_all = s.tau_q >= (1u << 24);
+    const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
+    resolve_bins(fc, nullptr, 0, lo, hi, hs->cnt_before, hs->mass_before, s, hs, row, kappa, hs->theta,
+                 tau_all, cap_all, hs->S, &s_found);
+    __syncthreads();
+  }
+  if (hs->state != kStDone) return;
+  const uint32_t dstar = hs->delta_star;
+  const int64_t nch = s.nch;
+  if (dstar == 0xffffffffu) {  // everything kept: the chunks' sizes
+    for (int64_t c = t; c < nch; c += kST) {
+      cs[c] = (uint32_t)(min(s.n, (c + 1) * kSelChunk) - c * kSelChunk);
+      ct[c] = 0u;
+    }
+  } else if (complete) {  // above the range + the in-range tokens below / at Δ*
+    for (int64_t c = t; c < nch; c += kST) { cs[c] = s.cntlo[(int64_t)row * nch + c]; ct[c] = 0u; }
+    __syncthreads();
+    for (unsigned long long e = t; e < nl; e += kST) {
+      const unsigned long long w = lst[e];
+      const uint32_t dl = (uint32_t)w;
+      const int64_t c = (int64_t)(w >> 32) / kSelChunk;
+      if (dl < dstar) atomicAdd(&cs[c], 1u);
+      else if (dl == dstar) atomicAdd(&ct[c], 1u);
+    }
+  } else {  // the list overflowed: count from z (slow path, exact)
+    for (int64_t c = t; c < nch; c += kST) { cs[c] = 0u; ct[c] = 0u; }
+    __syncthreads();
+    for (int64_t j = t; j < s.n; j += kST) {
+      const uint32_t dl = (uint32_t)(M - zint(zr[j]));
+      if (dl < dstar) atomicAdd(&cs[j / kSelChunk], 1u);
+      else if (dl == dstar) atomicAdd(&ct[j / kSelChunk], 1u);
+    }
+  }
   __syncthreads();
-  const int c = s_ticket;
+  // exclusive prefix over the chunks (thread-contiguous runs, then a block scan)
+  const int64_t per = (nch + kST - 1) / kST;
+  const int64_t c0 = min(nch, (int64_t)t * per), c1 = min(nch, c0 + per);
+  unsigned long long x[2] = {0, 0}, tot[2];
+  for (int64_t c = c0; c < c1; ++c) { x[0] += cs[c]; x[1] += ct[c]; }
+  bscan<2>(x, tot, sw);
+  unsigned long long ps = x[0], pt = x[1];
+  unsigned long long *pre = s.pre + (int64_t)row * nch;
+  for (int64_t c = c0; c < c1; ++c) {
+    pre[c] = (ps << 32) | pt;
+    ps += cs[c];
+    pt += ct[c];
+  }
+}
+
+// ---------------------------------------------------------------------------- K3
+// CTA = (chunk, row); 16 consecutive tokens per thread.
+__global__ void __launch_bounds__(kST) k_sel_write(SelArgs s) {
+  extern __shared__ __align__(16) uint8_t sm3[];
+  uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3);                  // [kSelChunk] Δ of kept tokens
+  uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm3 + kSelChunk * 4);  // [kSelChunk] offsets
+  __shared__ uint32_t sw[kST / 32];
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t c = blockIdx.x;
+  HeadState *hs = s.hs + row;
   if (hs->state != kStDone) return;  // (an error state writes nothing: sel_k stays unset)
   const int M = hs->M;
   const float kappa = hs->kappa;
   const uint32_t dstar = hs->delta_star;
   const unsigned long long r = hs->r_ties;
-  const int64_t j0 = (int64_t)c * kChunk, j1 = min(s.n, j0 + kChunk);
+  const unsigned long long pw = s.pre[(int64_t)row * s.nch + c];
+  const unsigned long long Sb = pw >> 32, Tb = pw & 0xffffffffull;
+  const int64_t j0 = c * kSelChunk, j1 = min(s.n, j0 + kSelChunk);
   const float *zr = s.z + (int64_t)row * s.z_stride;
-  // my TPT consecutive tokens
-  uint32_t dl[TPT];
-  const int64_t tb = j0 + (int64_t)t * TPT;
+  const int64_t tb = j0 + (int64_t)t * 16;
+  uint32_t dl[16];
 #pragma unroll
-  for (int q = 0; q < TPT; q += 4) {
-    float4 v = make_float4(0, 0, 0, 0);
-    if (tb + q + 4 <= j1) {
-      v = __ldcs(reinterpret_cast<const float4 *>(zr + tb + q));
+  for (int k = 0; k < 4; ++k) {
+    const int64_t p = tb + 4 * k;
+    float v[4];
+    if (p + 4 <= j1) {
+      const float4 x = *reinterpret_cast<const float4 *>(zr + p);
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
     } else {
-      if (tb + q < j1) v.x = zr[tb + q];
-      if (tb + q + 1 < j1) v.y = zr[tb + q + 1];
-      if (tb + q + 2 < j1) v.z = zr[tb + q + 2];
-    }
-    const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      dl[q + u] = tb + q + u < j1 ? (uint32_t)(M - zint(vv[u])) : 0xffffffffu;
-  }
-  unsigned long long x[2] = {0, 0}, tot[2];
+      for (int u = 0; u < 4; ++u) v[u] = p + u < j1 ? zr[p + u] : 0.0f;
+    }
 #pragma unroll
-  for (int q = 0; q < TPT; ++q) {
-    x[0] += dl[q] < dstar;
-    x[1] += (dl[q] == dstar && dstar != 0xffffffffu) ? 1u : 0u;
+    for (int u = 0; u < 4; ++u) dl[4 * k + u] = p + u < j1 ? (uint32_t)(M - zint(v[u])) : 0xffffffffu;
   }
-  const unsigned long long my_s = x[0], my_t = x[1];
-  bscan<2>(x, tot, sw);
-  // decoupled look-back: publish the aggregate, sum predecessors back to an inclusive prefix
-  unsigned long long *lbr = s.lb + (int64_t)row * s.lb_n;
-  if (t < 32) {
-    if (t == 0)
-      st_relaxed_u64(&lbr[c], c == 0 ? lb_pack(2u, (uint32_t)tot[0], (uint32_t)tot[1])
-                                     : lb_pack(1u, (uint32_t)tot[0], (uint32_t)tot[1]));
-    unsigned long long ps = 0, pt = 0;
-    int p = c - 1;
-    while (p >= 0) {  // 32 predecessors per round, newest first
-      const int q = p - lane;
-      unsigned long long wv = 0;
-      if (q >= 0) {
-        do { wv = ld_relaxed_u64(&lbr[q]); } while ((wv >> 62) == 0ull);
-      } else {
-        wv = lb_pack(2u, 0u, 0u);
-      }
-      const unsigned incl = __ballot_sync(0xffffffffu, (wv >> 62) == 2ull);
-      const int stop = incl ? __ffs(incl) - 1 : 32;  // the newest inclusive prefix
-      unsigned long long vs = lane <= stop ? ((wv >> 31) & 0x7fffffffull) : 0ull;
-      unsigned long long vt = lane <= stop ? (wv & 0x7fffffffull) : 0ull;
-      vs = warp_sum_u64(vs);
-      vt = warp_sum_u64(vt);
-      ps += vs;
-      pt += vt;
-      if (incl) break;
-      p -= 32;
-    }
-    if (t == 0) {
-      if (c > 0) st_relaxed_u64(&lbr[c], lb_pack(2u, (uint32_t)(ps + tot[0]), (uint32_t)(pt + tot[1])));
-      s_pre = (ps << 32) | pt;
-    }
+  // (strict, tie) counts packed in one word (each <= 8192): block exclusive scan
+  uint32_t my = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) my += dl[u] < dstar ? (1u << 16) : (dl[u] == dstar && dstar != 0xffffffffu ? 1u : 0u);
+  uint32_t inc = my;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += o;
   }
+  if (lane == 31) sw[warp] = inc;
   __syncthreads();
-  const unsigned long long Sb = s_pre >> 32, Tb = s_pre & 0xffffffffull;
-  // in-chunk positions: strict tokens always, ties while fewer than r precede them globally
-  unsigned long long sb = Sb + x[0], tcount = Tb + x[1];
-  const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);  // first output slot of this chunk
-  const unsigned long long pos_end = Sb + tot[0] + (Tb + tot[1] < r ? Tb + tot[1] : r);
-  unsigned long long pos = sb + (tcount < r ? tcount : r);
+  uint32_t before = 0, total = 0;
 #pragma unroll
-  for (int q = 0; q < TPT; ++q) {
-    const bool strict = dl[q] < dstar;
-    const bool tie = dl[q] == dstar && dstar != 0xffffffffu;
-    const bool take = strict || (tie && tcount < r);
-    if (take) {
-      const unsigned long long ls = pos - pos0;
-      stg_d[ls] = dl[q];
-      stg_o[ls] = (uint16_t)(t * TPT + q);
+  for (int w = 0; w < kST / 32; ++w) {
+    const uint32_t v = sw[w];
+    before += w < warp ? v : 0u;
+    total += v;
+  }
+  const uint32_t ex = before + inc - my;
+  unsigned long long ts = Tb + (ex & 0xffffu);                      // ties before my first token
+  unsigned long long pos = Sb + (ex >> 16) + (ts < r ? ts : r);     // its output slot
+  const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
+  const unsigned long long tt = Tb + (total & 0xffffu);
+  const unsigned long long pos1 = Sb + (total >> 16) + (tt < r ? tt : r);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const bool strict = dl[u] < dstar;
+    const bool tie = dl[u] == dstar && dstar != 0xffffffffu;
+    if (strict || (tie && ts < r)) {
+      const unsigned ls = (unsigned)(pos - pos0);
+      stg_d[ls] = dl[u];
+      stg_o[ls] = (uint16_t)(t * 16 + u);
       ++pos;
     }
-    tcount += tie ? 1u : 0u;
+    ts += tie ? 1u : 0u;
   }
-  (void)my_s;
-  (void)my_t;
   __syncthreads();
-  const int kept = (int)(pos_end - pos0);
+  const int kept = (int)(pos1 - pos0);
   const float inv_den = (float)(1.0 / (s.renorm ? (double)hs->sel_mass : (double)hs->S));
   int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
   float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
@@ -595,49 +693,39 @@ __global__ void __launch_bounds__(kST) k_sel_compact(SelArgs s) {
 }
 
 // ---------------------------------------------------------------------------- launcher
-int select_lb_chunks(int64_t n) { return (int)((n + kST * 4 - 1) / (kST * 4)); }  // smallest chunk
-
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
-  // K1 / K2 work split: about 3 CTAs per SM over all rows, >= 4096 tokens per CTA
-  int64_t cpr = ((int64_t)num_sms * 3 + s.rows - 1) / s.rows;
-  const int64_t max_cpr = (s.n + 4095) / 4096;
-  if (cpr > max_cpr) cpr = max_cpr;
+  if (s.nch != select_chunks(s.n)) return cudaErrorInvalidValue;
+  // K1 / K2: one wave of 2 CTAs per SM over all rows, whole chunks per CTA
+  int64_t cpr = (2LL * num_sms) / s.rows;
   if (cpr < 1) cpr = 1;
-  int64_t per = (s.n + cpr - 1) / cpr;
-  per = (per + 63) / 64 * 64;
+  if (cpr > s.nch) cpr = s.nch;
+  const int64_t per = (s.nch + cpr - 1) / cpr * kSelChunk;
   cpr = (s.n + per - 1) / per;
   const dim3 g12((unsigned)cpr, (unsigned)s.rows);
-  // K3 chunk: 8192 tokens for long rows, 2048 when the rows are short
-  const int tpt3 = (int64_t)s.rows * ((s.n + 8191) / 8192) >= 2LL * num_sms ? 16 : 4;
-  const int64_t chunk3 = (int64_t)kST * tpt3;
-  const int64_t nch3 = (s.n + chunk3 - 1) / chunk3;
-  if (nch3 > s.lb_n) return cudaErrorInvalidValue;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaFuncSetAttribute(k_sel_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_sel_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_sel_write, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    configured[dev] = 1;
+  }
   if (nsplit > 1) {
     launch_chain(k_sel_minmax, g12, dim3(kST), 0, st, s, per);
     note_launch();
   }
   launch_chain(k_sel_mass, g12, dim3(kST), 0, st, s, per);
   note_launch();
-  static int configured[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(k_sel_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_sel_compact<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(k_sel_compact<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    configured[dev] = 1;
-  }
-  const size_t smem2 = (size_t)kNB * 12;
-  launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per, 0);
+  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4;
+  launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
-  launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per, 1);
+  const size_t smem4 = (size_t)s.nch * 8 + (size_t)kNB * 4;
+  if (smem4 > 200 * 1024) return cudaErrorInvalidValue;
+  launch_chain(k_sel_prefix, dim3((unsigned)s.rows), dim3(kST), smem4, st, s);
   note_launch();
-  const size_t smem3 = (size_t)chunk3 * 6;
-  if (tpt3 == 16)
-    launch_chain(k_sel_compact<16>, dim3((unsigned)nch3, (unsigned)s.rows), dim3(kST), smem3, st, s);
-  else
-    launch_chain(k_sel_compact<4>, dim3((unsigned)nch3, (unsigned)s.rows), dim3(kST), smem3, st, s);
+  launch_chain(k_sel_write, dim3((unsigned)s.nch, (unsigned)s.rows), dim3(kST), (size_t)kSelChunk * 6, st, s);
   note_launch();
   return cudaGetLastError();
 }

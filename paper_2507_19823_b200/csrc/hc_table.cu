@@ -216,11 +216,12 @@ __global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
   constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;  // centroids per thread
   constexpr int kTC = kT2Threads * CPT;           // centroids per CTA
   constexpr int kRows = t2_max_rows<DBAR>();
-  __shared__ float s_sc[kRows];           // 2^e per query head
+  __shared__ float s_sc[kRows];           // 2^e per query head (first: the bound's bits)
   __shared__ float s_q[kRows * DBAR];     // q̄_i (group i of this CTA) per query head
+  __shared__ float s_cabs[128 * DBAR];    // the codebook's per-dimension max |C| (R2 constant)
   pdl_trigger();
   pdl_wait();
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.x;
   const int i = blockIdx.y;
   const int m0 = blockIdx.x * kTC;
   const int rows = a.B * a.Hq, units = a.B * a.Hkv;
@@ -242,41 +243,7 @@ __global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
       reinterpret_cast<float4 *>(a.z + r * a.z_stride)[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  // ---- R2 scales: A_h = max_i fmaf-chain_e(|q_h[i*dbar+e]|, Cabs[ci][e]); one warp per head
-  for (int r = warp; r < rows; r += kT2Threads / 32) {
-    const uint16_t *qh = a.q + (int64_t)r * a.d;
-    float bnd = 0.0f;
-    for (int gi = lane; gi < a.g; gi += 32) {
-      const float *ca = a.cb_absmax + (int64_t)(a.cbg == 1 ? 0 : gi) * DBAR;
-      float bb = __fmul_rn(fabsf(h2f(__ldg(qh + gi * DBAR))), __ldg(ca));
-#pragma unroll
-      for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(h2f(__ldg(qh + gi * DBAR + e))), __ldg(ca + e), bb);
-      bnd = fmaxf(bnd, bb);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) bnd = fmaxf(bnd, __shfl_xor_sync(0xffffffffu, bnd, off));
-    const int e = a.lut8 ? scale_exponent8(bnd) : scale_exponent(bnd);
-    if (lane == 0) {
-      s_sc[r] = pow2f(e);
-      if (cta == 0) {  // the heads' selection state for this layer
-        HeadState *hs = a.hs + r;
-        hs->e = e;
-        hs->kappa = __fmul_rn(a.kappa0, pow2f(-e));
-        hs->amax = __float_as_uint(bnd);
-        hs->M = INT_MIN;  // folded by the scan / resident epilogues (atomics)
-        hs->zmin = INT_MAX;
-        hs->S = 0ull;     // the selection's accumulators and counters (hc_select_pass.cu)
-        hs->mass_before = 0ull;
-        hs->c1_done = 0u;
-        hs->c2_done = 0u;
-        hs->ticket = 0u;
-        hs->state = 0u;
-      }
-    }
-    if (lane < DBAR) s_q[r * DBAR + lane] = h2f(__ldg(qh + i * DBAR + lane));
-  }
-  __syncthreads();
-  // ---- this CTA's codebook rows, once
+  // ---- this CTA's codebook rows: loads issued first (consumed after the scales)
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
   float cm[CPT][DBAR];
 #pragma unroll
@@ -285,6 +252,62 @@ __global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
 #pragma unroll
     for (int e = 0; e < DBAR; ++e) cm[k][e] = m < a.c ? __ldg(Ci + (int64_t)m * DBAR + e) : 0.0f;
   }
+  // ---- R2 scales: A_h = max_i fmaf-chain_e(|q_h[i*dbar+e]|, Cabs[ci][e]) over every (head,
+  // group) item, spread over all threads with their loads in flight together; the max over
+  // groups by shared atomics on the (non-negative) float bits
+  uint32_t *s_abits = reinterpret_cast<uint32_t *>(s_sc);
+  for (int k = t; k < rows; k += kT2Threads) s_abits[k] = 0u;
+  for (int k = t; k < a.cbg * DBAR; k += kT2Threads) s_cabs[k] = __ldg(a.cb_absmax + k);
+  __syncthreads();
+  const int items = rows * a.g;
+  constexpr int kIB = DBAR >= 8 ? 32 / DBAR : 8;  // items per thread per round, loads issued before use
+  for (int it0 = t; it0 < items; it0 += kT2Threads * kIB) {
+    float qv[kIB][DBAR];
+#pragma unroll
+    for (int ib = 0; ib < kIB; ++ib) {
+      const int it = it0 + ib * kT2Threads;
+      const int r = it / a.g, gi = it - r * a.g;
+#pragma unroll
+      for (int e = 0; e < DBAR; ++e)
+        qv[ib][e] = it < items ? h2f(__ldg(a.q + (int64_t)r * a.d + gi * DBAR + e)) : 0.0f;
+    }
+#pragma unroll
+    for (int ib = 0; ib < kIB; ++ib) {
+      const int it = it0 + ib * kT2Threads;
+      if (it >= items) break;
+      const int r = it / a.g, gi = it - r * a.g;
+      const float *ca = s_cabs + (a.cbg == 1 ? 0 : gi) * DBAR;
+      float bb = __fmul_rn(fabsf(qv[ib][0]), ca[0]);
+#pragma unroll
+      for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(qv[ib][e]), ca[e], bb);
+      atomicMax(&s_abits[r], __float_as_uint(bb));
+      if (gi == i) {
+#pragma unroll
+        for (int e = 0; e < DBAR; ++e) s_q[r * DBAR + e] = qv[ib][e];
+      }
+    }
+  }
+  __syncthreads();
+  for (int r = t; r < rows; r += kT2Threads) {
+    const float bnd = __uint_as_float(s_abits[r]);
+    const int e = a.lut8 ? scale_exponent8(bnd) : scale_exponent(bnd);
+    s_sc[r] = pow2f(e);  // (same slot: this thread read it just above)
+    if (cta == 0) {  // the heads' selection state for this layer
+      HeadState *hs = a.hs + r;
+      hs->e = e;
+      hs->kappa = __fmul_rn(a.kappa0, pow2f(-e));
+      hs->amax = __float_as_uint(bnd);
+      hs->M = INT_MIN;  // folded by the scan / resident epilogues (atomics)
+      hs->zmin = INT_MAX;
+      hs->S = 0ull;     // the selection's accumulators and counters (hc_select_pass.cu)
+      hs->mass_before = 0ull;
+      hs->c1_done = 0u;
+      hs->c2_done = 0u;
+      hs->ticket = 0u;
+      hs->state = 0u;
+    }
+  }
+  __syncthreads();
   // ---- every unit's entries for these centroids (entries m >= c are 0)
   for (int u = 0; u < units; ++u) {
     const int b = u / a.Hkv, kv = u - b * a.Hkv;

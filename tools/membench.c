@@ -8,7 +8,12 @@
  *                   (xorshift64*), `batch` rows prefetched before they are read (the memory-
  *                   level parallelism a row gather can have), each row summed as uint64 words
  *                   so the loads cannot be elided;
- *   hm_sequential:  every thread streams its contiguous slice once (uint64 sums).
+ *   hm_sorted_rows: the Eq. 5 access SHAPE without its arithmetic: every thread walks its
+ *                   contiguous slice keeping each row with probability 1/stride (a sorted
+ *                   random subset, like a kept list at density 1/stride), 16 rows prefetched
+ *                   ahead, row words summed;
+ *   hm_sequential:  every thread streams its contiguous slice once (uint64 sums, 8 streams,
+ *                   software prefetch 1 KiB ahead).
  * Returns GB/s (1e9 B/s) of bytes read; `sink` receives the checksum.
  * Build: gcc -O2 -fopenmp -march=native -shared -fPIC -o libmembench.so membench.c */
 #include <omp.h>
@@ -73,6 +78,54 @@ double hm_random_rows(const void *buf, uint64_t bytes, uint64_t row_bytes, uint6
     return rows_read * (double)row_bytes / (t1 - t0) / 1e9;
 }
 
+double hm_sorted_rows(const void *buf, uint64_t bytes, uint64_t row_bytes, uint32_t stride, int threads,
+                      uint64_t *sink)
+{
+    if (!buf || row_bytes < 64 || row_bytes % 64 || bytes < row_bytes || threads < 1 || stride < 1) return -1.0;
+    const uint64_t nrows = bytes / row_bytes, words = row_bytes / 8;
+    uint64_t total = 0, kept = 0;
+    double t0 = 0, t1 = 0;
+#pragma omp parallel num_threads(threads) reduction(+ : total, kept)
+    {
+        const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+        const uint64_t lo = nrows * (uint64_t)t / (uint64_t)nt, hi = nrows * (uint64_t)(t + 1) / (uint64_t)nt;
+        uint64_t s = 0x9E3779B97F4A7C15ull * (uint64_t)(t + 1), acc = 0, nk = 0;
+        const char *base = (const char *)buf;
+        uint64_t ring[16];
+        int head = 0, fill = 0;
+#pragma omp barrier
+#pragma omp master
+        t0 = now_s();
+#pragma omp barrier
+        for (uint64_t r = lo; r < hi; ++r) {
+            if ((uint32_t)(xs64(&s) >> 32) % stride) continue;
+            const char *p = base + r * row_bytes;
+            for (uint64_t o = 0; o < row_bytes; o += 64) __builtin_prefetch(p + o, 0, 0);
+            if (fill == 16) {  /* consume the row prefetched 16 kept rows ago */
+                const uint64_t *w = (const uint64_t *)(base + ring[head] * row_bytes);
+                for (uint64_t k = 0; k < words; ++k) acc += w[k];
+                ++nk;
+            } else {
+                ++fill;
+            }
+            ring[head] = r;
+            head = (head + 1) & 15;
+        }
+        for (int i = 0; i < fill; ++i) {
+            const uint64_t *w = (const uint64_t *)(base + ring[(head + i) & 15] * row_bytes);
+            for (uint64_t k = 0; k < words; ++k) acc += w[k];
+            ++nk;
+        }
+#pragma omp barrier
+#pragma omp master
+        t1 = now_s();
+        total += acc;
+        kept += nk;
+    }
+    if (sink) *sink = total;
+    return (double)kept * (double)row_bytes / (t1 - t0) / 1e9;
+}
+
 double hm_sequential(const void *buf, uint64_t bytes, int threads, uint64_t *sink)
 {
     if (!buf || bytes < 4096 || threads < 1) return -1.0;
@@ -84,23 +137,21 @@ double hm_sequential(const void *buf, uint64_t bytes, int threads, uint64_t *sin
         const int t = omp_get_thread_num(), nt = omp_get_num_threads();
         const uint64_t lo = words * (uint64_t)t / (uint64_t)nt, hi = words * (uint64_t)(t + 1) / (uint64_t)nt;
         const uint64_t *w = (const uint64_t *)buf;
-        uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        uint64_t a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma omp barrier
 #pragma omp master
         t0 = now_s();
 #pragma omp barrier
         uint64_t k = lo;
-        for (; k + 4 <= hi; k += 4) {
-            a0 += w[k];
-            a1 += w[k + 1];
-            a2 += w[k + 2];
-            a3 += w[k + 3];
+        for (; k + 8 <= hi; k += 8) {
+            __builtin_prefetch(w + k + 128, 0, 0);
+            for (int u = 0; u < 8; ++u) a[u] += w[k + u];
         }
-        for (; k < hi; ++k) a0 += w[k];
+        for (; k < hi; ++k) a[0] += w[k];
 #pragma omp barrier
 #pragma omp master
         t1 = now_s();
-        total += a0 + a1 + a2 + a3;
+        for (int u = 0; u < 8; ++u) total += a[u];
     }
     if (sink) *sink = total;
     return (double)(words * 8) / (t1 - t0) / 1e9;

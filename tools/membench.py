@@ -16,7 +16,7 @@ _lib = None
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", LIB + ".tmp", SRC])
+        subprocess.check_call(["gcc", "-O3", "-fopenmp", "-shared", "-fPIC", "-o", LIB + ".tmp", SRC])
         os.replace(LIB + ".tmp", LIB)
     return LIB
 
@@ -30,6 +30,9 @@ def lib():
                                      C.POINTER(C.c_uint64)]
         L.hm_random_rows.restype = C.c_double
         L.hm_sequential.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64)]
+        L.hm_sorted_rows.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_int,
+                                     C.POINTER(C.c_uint64)]
+        L.hm_sorted_rows.restype = C.c_double
         L.hm_sequential.restype = C.c_double
         _lib = L
     return _lib
@@ -64,7 +67,7 @@ def host_topology() -> dict:
 
 
 def measure(ptr: int, nbytes: int, threads: int | None = None, row_bytes: int = 256,
-            rows_per_thread: int = 1 << 20, batch: int = 16, reps: int = 3) -> dict:
+            rows_per_thread: int = 1 << 20, batch: int = 16, reps: int = 3, sorted_stride: int = 8) -> dict:
     """Best-of-reps GB/s of random `row_bytes` rows and of one sequential pass (capped at
     16 GiB) over [ptr, ptr + nbytes), on `threads` threads (default: all usable cores)."""
     L = lib()
@@ -74,9 +77,14 @@ def measure(ptr: int, nbytes: int, threads: int | None = None, row_bytes: int = 
                                C.byref(sink)) for _ in range(reps))
     seq_bytes = min(nbytes, 16 << 30)
     seq = max(L.hm_sequential(C.c_void_p(ptr), seq_bytes, thr, C.byref(sink)) for _ in range(reps))
-    return {"random_rows_gbs": rnd, "sequential_gbs": seq, "threads": thr, "row_bytes": row_bytes,
+    srt = max(L.hm_sorted_rows(C.c_void_p(ptr), nbytes, row_bytes, sorted_stride, thr, C.byref(sink))
+              for _ in range(reps))
+    return {"random_rows_gbs": rnd, "sorted_rows_gbs": srt, "sorted_rows_density": 1.0 / sorted_stride,
+            "sequential_gbs": seq, "peak_gbs": max(rnd, srt, seq), "threads": thr, "row_bytes": row_bytes,
             "rows_in_flight_per_thread": batch, "buffer_gb": nbytes / 1e9,
-            "how": "tools/membench.c: all threads read random 256-B rows (16 prefetched per thread, "
-                   "uint64 sums, no Eq. 5 arithmetic) / stream contiguous slices, over the value "
-                   "store's own pinned memory; best of %d" % reps,
+            "how": "tools/membench.c, all host threads, over the value store's own pinned memory, no "
+                   "Eq. 5 arithmetic (uint64 sums of the bytes read): uniformly random 256-B rows (16 "
+                   "prefetched per thread); a sorted random subset of rows at density 1/%d (the kept "
+                   "lists' shape); one sequential pass; best of %d each; peak = the best of the three"
+                   % (sorted_stride, reps),
             **host_topology()}
