@@ -193,7 +193,7 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
                                 int num_sms, cudaStream_t st);
 // rows a3-a4 as three passes (hc_select_pass.cu, the default); nsplit > 1 adds a max/min pass
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st);
-constexpr int kSelChunk = 8192;  // tokens per write chunk
+constexpr int kSelChunk = 4096;  // tokens per chunk of the selection passes (16 KB of z)
 inline int64_t select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChunk; }
 inline int64_t select_list_cap(int64_t n) { int64_t c = n / 16; return c < 4096 ? 4096 : c; }
 

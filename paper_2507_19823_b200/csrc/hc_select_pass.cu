@@ -31,6 +31,8 @@
 // Every decision is integer arithmetic on exact quantities (counts, u64 masses, the
 // 128-bit threshold Θ), so the kept set equals the oracle's bit for bit (or_select: sort by
 // (Δ asc, index asc), prefix to Θ, cap) -- the bounds only choose WHERE to look.
+#include <type_traits>
+
 #include "hc_internal.h"
 
 namespace hc {
@@ -39,10 +41,19 @@ constexpr int kST = 512;             // threads per CTA (all three kernels)
 constexpr int kBPT = kNB / kST;      // histogram bins per thread in the block-wide walks (8)
 constexpr uint32_t kStRefine1 = 1, kStRefine2 = 2, kStDone = 3, kStError = 4;
 
+// R4's mass W(Δ) = trunc(p(f) * 2^(40+n)), x = -(float)Δ*κ, n = floor(x), f = x - n, 0 for
+// x < -40 -- the same IEEE steps as mass() / mass_d() (hc_device.cuh), bit for bit, with the
+// floor, the int->float of n and the final truncation on the conversion pipe (F2I / I2F),
+// which runs beside the FMA / ALU pipes this pass is otherwise bound by.
 __device__ __forceinline__ uint64_t wmass(uint32_t dl, float kappa) {
-  uint32_t lo, hi;
-  mass_parts(dl, kappa, lo, hi);  // == mass_d(dl, kappa), branch-free
-  return ((uint64_t)hi << 32) | lo;
+  const float df = __fsub_rn(__int_as_float(0x4B000000 + (int)dl), 8388608.0f);  // exact, Δ <= 2^23
+  const float x0 = -__fmul_rn(df, kappa);
+  const float x = fmaxf(x0, -64.0f);          // keeps 2^(40+n) normal; x0 < -40 -> 0 below
+  const int ni = __float2int_rd(x);            // floor (exact for |x| <= 64)
+  const float f = __fsub_rn(x, __int2float_rn(ni));
+  const float v = __fmul_rn(exp2_poly(f), pow2f(40 + ni));
+  const uint64_t w = __float2ull_rz(v);        // truncation toward zero, v < 2^41
+  return x0 < -40.0f ? 0ull : w;
 }
 
 __device__ __forceinline__ int sel_shift(int M, int zmin) {
@@ -131,6 +142,47 @@ __device__ __forceinline__ void sel_tokens(const float *zr, int64_t j0, int64_t 
   }
   for (int64_t t = j14 + threadIdx.x; t < j1; t += kST) f(zr[t]);
 }
+
+// TMA-staged stream of one z row's chunks (kSelChunk tokens = 16 KB each) through NB shared
+// buffers: chunk k+NB is requested (cp.async.bulk, one mbarrier per buffer) as soon as every
+// thread is done with chunk k, so the HBM reads run ahead of the per-token work without
+// registers.  In a chunk thread t owns tokens 4t + 2048u .. +3 (u = 0, 1): each LDS.128 of a
+// warp reads 512 contiguous bytes (conflict-free).
+template <int NB>
+struct ZStream {
+  float *buf;      // [NB][kSelChunk]
+  uint64_t *bar;   // [NB]
+  const float *zr;
+  int64_t n;
+  uint32_t ph;
+  __device__ void init(float *b, uint64_t *br, const float *z, int64_t n_) {
+    buf = b; bar = br; zr = z; n = n_; ph = 0u;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < NB; ++i) mbar_init(&bar[i], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  __device__ void request(int64_t c, int slot) {  // one thread
+    const int64_t j0 = c * kSelChunk;
+    const int64_t cnt = min((int64_t)kSelChunk, n - j0);
+    const uint32_t bytes = (uint32_t)((cnt * 4 + 15) & ~(int64_t)15);  // z rows are padded to 64
+    mbar_expect_tx(&bar[slot], bytes);
+    bulk_g2s(buf + (size_t)slot * kSelChunk, zr + j0, bytes, &bar[slot]);
+  }
+  __device__ const float *wait(int slot) {
+    mbar_wait(&bar[slot], (ph >> slot) & 1u);
+    ph ^= 1u << slot;
+    return buf + (size_t)slot * kSelChunk;
+  }
+  // after a __syncthreads() that retired every read of `slot`: refill it with chunk c
+  __device__ void refill(int64_t c, int slot) {
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async write
+      request(c, slot);
+    }
+  }
+};
 
 // Resolve the cut exactly over consecutive Δ values base .. base + kNB - 1 whose counts are
 // cnt[] (shared) and whose per-token mass is W(base + b) -- or, if `mass` is given, whose
@@ -222,8 +274,13 @@ __global__ void __launch_bounds__(kST) k_sel_minmax(SelArgs s, int64_t per) {
 }
 
 // ---------------------------------------------------------------------------- K1
+constexpr int kZB = 3;  // z stream buffers per CTA
+
 __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
+  extern __shared__ __align__(128) uint8_t sm1[];
+  float *zbuf = reinterpret_cast<float *>(sm1);                                 // [kZB][kSelChunk]
   __shared__ uint32_t hist[kNB];
+  __shared__ uint64_t zbar[kZB];
   __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
   pdl_trigger();
@@ -245,13 +302,36 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
     const int64_t l0 = nl * blockIdx.x / gridDim.x, l1 = nl * (blockIdx.x + 1) / gridDim.x;
     for (int64_t i = l0 + t; i < l1; i += kST) s.cntlo[(int64_t)row * nl + i] = 0u;
   }
-  __syncthreads();
+  ZStream<kZB> zs;
+  zs.init(zbuf, zbar, s.z + (int64_t)row * s.z_stride, s.n);  // (its __syncthreads also covers the zeroing)
+  const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
+  if (t == 0)
+    for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
   unsigned long long S = 0;
-  sel_tokens(s.z + (int64_t)row * s.z_stride, j0, j1, [&](float zf) {
-    const uint32_t dl = (uint32_t)(M - zint(zf));
-    S += wmass(dl, kappa);
-    atomicAdd(&hist[dl >> shift], 1u);
-  });
+  for (int64_t c = c0; c < c1; ++c) {
+    const int slot = (int)((c - c0) % kZB);
+    const float *zc = zs.wait(slot);
+    const int nv = (int)min((int64_t)kSelChunk, s.n - c * kSelChunk);
+    auto body = [&](auto full) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i0 = 4 * t + 2048 * u;
+        const float4 v = *reinterpret_cast<const float4 *>(zc + i0);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (decltype(full)::value || i0 + e < nv) {
+            const uint32_t dl = (uint32_t)(M - zint(vv[e]));
+            S += wmass(dl, kappa);
+            atomicAdd(&hist[dl >> shift], 1u);
+          }
+        }
+      }
+    };
+    if (nv == kSelChunk) body(std::true_type{}); else body(std::false_type{});
+    __syncthreads();
+    if (c + kZB < c1) zs.refill(c + kZB, slot);
+  }
   S = warp_sum_u64(S);
   if ((t & 31) == 0) s_red[t >> 5] = S;
   __syncthreads();
@@ -395,6 +475,8 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   uint32_t *fmh = reinterpret_cast<uint32_t *>(sm2 + kNB * 8);      // [kNB] high word
   unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(sm2 + kNB * 4);  // resolve: over fml/fmh
   uint32_t *wq = reinterpret_cast<uint32_t *>(sm2 + kNB * 12);      // [kST/32][64] per-warp Δ queues
+  float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12 + kST * 8);  // [kZB][kSelChunk]
+  __shared__ uint64_t zbar[kZB];
   __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
   __shared__ int s_found;
@@ -409,74 +491,75 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   const int f = hs->fshift;
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
   for (int i = t; i < kNB; i += kST) { fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u; }
-  __syncthreads();
-  const float *zr = s.z + (int64_t)row * s.z_stride;
+  ZStream<kZB> zs;
+  zs.init(zbuf, zbar, s.z + (int64_t)row * s.z_stride, s.n);
+  const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
+  if (t == 0)
+    for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
   uint32_t *q = wq + warp * 64;
   int qn = 0;                 // warp-uniform queue length
   unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
   unsigned long long *lst = s.list + (int64_t)row * s.cap;
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t cb = j0; cb < j1; cb += kSelChunk) {
-    const int64_t tb = cb + (int64_t)t * 16;
-    const int64_t ce = min(j1, cb + (int64_t)kSelChunk);
-    float v[16];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t p = tb + 4 * k;
-      if (p + 4 <= ce) {
-        const float4 x = *reinterpret_cast<const float4 *>(zr + p);
-        v[4 * k] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[4 * k + u] = p + u < ce ? zr[p + u] : 0.0f;
-      }
-    }
+  for (int64_t c = c0; c < c1; ++c) {
+    const int slot = (int)((c - c0) % kZB);
+    const float *zc = zs.wait(slot);
+    const int64_t cb = c * kSelChunk;
+    const int nv = (int)min((int64_t)kSelChunk, s.n - cb);
     uint32_t nlo = 0;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const bool valid = tb + u < ce;
-      const uint32_t dl = (uint32_t)(M - zint(v[u]));
-      const bool above = valid && dl < lo;
-      const bool inr = valid && dl >= lo && dl <= hi;
-      nlo += above ? 1u : 0u;
-      // the exact W of the tokens above the range, 32 at a time from the warp's queue
-      const unsigned ma = __ballot_sync(0xffffffffu, above);
-      if (ma) {
-        if (above) q[qn + __popc(ma & lt)] = dl;
-        qn += __popc(ma);
-        if (qn >= 32) {
-          __syncwarp();
-          P += wmass(q[lane], kappa);
-          const uint32_t rest = lane + 32 < qn ? q[lane + 32] : 0u;
-          __syncwarp();
-          if (lane + 32 < qn) q[lane] = rest;
-          qn -= 32;
-          __syncwarp();
-        }
-      }
-      const unsigned mr = __ballot_sync(0xffffffffu, inr);
-      if (mr) {  // in-range: fine histogram + the row's in-range list (warp-aggregated append)
-        unsigned base = 0;
-        if (lane == __ffs(mr) - 1) base = atomicAdd(&hs->ticket, (unsigned)__popc(mr));
-        base = __shfl_sync(0xffffffffu, base, __ffs(mr) - 1);
-        if (inr) {
-          const uint32_t fb = (dl - lo) >> f;
-          atomicAdd(&fc[fb], 1u);
-          if (f > 0) {  // fine bins of several Δ values: their exact mass too
-            uint32_t wl, wh;
-            mass_parts(dl, kappa, wl, wh);
-            const uint32_t old = atomicAdd(&fml[fb], wl);
-            wh += (old + wl < old) ? 1u : 0u;
-            if (wh) atomicAdd(&fmh[fb], wh);
+    for (int u2 = 0; u2 < 2; ++u2) {
+      const int i0 = 4 * t + 2048 * u2;
+      const float4 v4 = *reinterpret_cast<const float4 *>(zc + i0);
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool valid = i0 + e < nv;
+        const uint32_t dl = (uint32_t)(M - zint(vv[e]));
+        const bool above = valid && dl < lo;
+        const bool inr = valid && dl >= lo && dl <= hi;
+        nlo += above ? 1u : 0u;
+        // the exact W of the tokens above the range, 32 at a time from the warp's queue
+        const unsigned ma = __ballot_sync(0xffffffffu, above);
+        if (ma) {
+          if (above) q[qn + __popc(ma & lt)] = dl;
+          qn += __popc(ma);
+          if (qn >= 32) {
+            __syncwarp();
+            P += wmass(q[lane], kappa);
+            const uint32_t rest = lane + 32 < qn ? q[lane + 32] : 0u;
+            __syncwarp();
+            if (lane + 32 < qn) q[lane] = rest;
+            qn -= 32;
+            __syncwarp();
           }
-          const unsigned pos = base + __popc(mr & lt);
-          if (pos < (unsigned)s.cap) lst[pos] = ((unsigned long long)(tb + u) << 32) | dl;
+        }
+        const unsigned mr = __ballot_sync(0xffffffffu, inr);
+        if (mr) {  // in-range: fine histogram + the row's in-range list (warp-aggregated append)
+          unsigned base = 0;
+          if (lane == __ffs(mr) - 1) base = atomicAdd(&hs->ticket, (unsigned)__popc(mr));
+          base = __shfl_sync(0xffffffffu, base, __ffs(mr) - 1);
+          if (inr) {
+            const uint32_t fb = (dl - lo) >> f;
+            atomicAdd(&fc[fb], 1u);
+            if (f > 0) {  // fine bins of several Δ values: their exact mass too
+              uint32_t wl, wh;
+              mass_parts(dl, kappa, wl, wh);
+              const uint32_t old = atomicAdd(&fml[fb], wl);
+              wh += (old + wl < old) ? 1u : 0u;
+              if (wh) atomicAdd(&fmh[fb], wh);
+            }
+            const unsigned pos = base + __popc(mr & lt);
+            if (pos < (unsigned)s.cap) lst[pos] = ((unsigned long long)(cb + i0 + e) << 32) | dl;
+          }
         }
       }
     }
     // the chunk's count of tokens above the range (K4 adds its in-range tokens below Δ*)
     nlo = __reduce_add_sync(0xffffffffu, nlo);
-    if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + cb / kSelChunk], nlo);
+    if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + c], nlo);
+    __syncthreads();
+    if (c + kZB < c1) zs.refill(c + kZB, slot);
   }
   __syncwarp();
   if (lane < qn) P += wmass(q[lane], kappa);
@@ -608,46 +691,11 @@ __global__ void __launch_bounds__(kST) k_sel_prefix(SelArgs s) {
 }
 
 // ---------------------------------------------------------------------------- K3
-// CTA = (chunk, row); 16 consecutive tokens per thread.
-__global__ void __launch_bounds__(kST) k_sel_write(SelArgs s) {
-  extern __shared__ __align__(16) uint8_t sm3[];
-  uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3);                  // [kSelChunk] Δ of kept tokens
-  uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm3 + kSelChunk * 4);  // [kSelChunk] offsets
-  __shared__ uint32_t sw[kST / 32];
-  pdl_trigger();
-  pdl_wait();
-  const int row = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t c = blockIdx.x;
-  HeadState *hs = s.hs + row;
-  if (hs->state != kStDone) return;  // (an error state writes nothing: sel_k stays unset)
-  const int M = hs->M;
-  const float kappa = hs->kappa;
-  const uint32_t dstar = hs->delta_star;
-  const unsigned long long r = hs->r_ties;
-  const unsigned long long pw = s.pre[(int64_t)row * s.nch + c];
-  const unsigned long long Sb = pw >> 32, Tb = pw & 0xffffffffull;
-  const int64_t j0 = c * kSelChunk, j1 = min(s.n, j0 + kSelChunk);
-  const float *zr = s.z + (int64_t)row * s.z_stride;
-  const int64_t tb = j0 + (int64_t)t * 16;
-  uint32_t dl[16];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int64_t p = tb + 4 * k;
-    float v[4];
-    if (p + 4 <= j1) {
-      const float4 x = *reinterpret_cast<const float4 *>(zr + p);
-      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    } else {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = p + u < j1 ? zr[p + u] : 0.0f;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) dl[4 * k + u] = p + u < j1 ? (uint32_t)(M - zint(v[u])) : 0xffffffffu;
-  }
-  // (strict, tie) counts packed in one word (each <= 8192): block exclusive scan
-  uint32_t my = 0;
-#pragma unroll
-  for (int u = 0; u < 16; ++u) my += dl[u] < dstar ? (1u << 16) : (dl[u] == dstar && dstar != 0xffffffffu ? 1u : 0u);
+// Persistent CTAs over the (row, chunk) items; the next item's z chunk streams into the other
+// shared buffer (cp.async.bulk) while this one is compacted.  In a chunk thread t owns tokens
+// 4t .. 4t+3 of each 2048-token slab (index order = slab, thread, element).
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t my, uint32_t &total, uint32_t *sw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t inc = my;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -656,39 +704,114 @@ __global__ void __launch_bounds__(kST) k_sel_write(SelArgs s) {
   }
   if (lane == 31) sw[warp] = inc;
   __syncthreads();
-  uint32_t before = 0, total = 0;
+  uint32_t before = 0;
+  total = 0;
 #pragma unroll
   for (int w = 0; w < kST / 32; ++w) {
     const uint32_t v = sw[w];
     before += w < warp ? v : 0u;
     total += v;
   }
-  const uint32_t ex = before + inc - my;
-  unsigned long long ts = Tb + (ex & 0xffffu);                      // ties before my first token
-  unsigned long long pos = Sb + (ex >> 16) + (ts < r ? ts : r);     // its output slot
-  const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
-  const unsigned long long tt = Tb + (total & 0xffffu);
-  const unsigned long long pos1 = Sb + (total >> 16) + (tt < r ? tt : r);
-#pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    const bool strict = dl[u] < dstar;
-    const bool tie = dl[u] == dstar && dstar != 0xffffffffu;
-    if (strict || (tie && ts < r)) {
-      const unsigned ls = (unsigned)(pos - pos0);
-      stg_d[ls] = dl[u];
-      stg_o[ls] = (uint16_t)(t * 16 + u);
-      ++pos;
-    }
-    ts += tie ? 1u : 0u;
+  __syncthreads();  // sw is reused by the next scan
+  return before + inc - my;
+}
+
+__global__ void __launch_bounds__(kST, 2) k_sel_write(SelArgs s) {
+  extern __shared__ __align__(128) uint8_t sm3[];
+  float *zbuf = reinterpret_cast<float *>(sm3);                                        // [2][kSelChunk]
+  uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3 + 2 * kSelChunk * 4);            // [kSelChunk]
+  uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm3 + 3 * kSelChunk * 4);            // [kSelChunk]
+  __shared__ uint64_t zbar[2];
+  __shared__ uint32_t sw[kST / 32];
+  pdl_trigger();
+  pdl_wait();
+  const int t = threadIdx.x;
+  const int64_t items = (int64_t)s.rows * s.nch;
+  if (t == 0) {
+    mbar_init(&zbar[0], 1);
+    mbar_init(&zbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int kept = (int)(pos1 - pos0);
-  const float inv_den = (float)(1.0 / (s.renorm ? (double)hs->sel_mass : (double)hs->S));
-  int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
-  float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
-  for (int i = t; i < kept; i += kST) {
-    oi[i] = (int32_t)(j0 + stg_o[i]);
-    ow[i] = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
+  auto request = [&](int64_t it, int slot) {  // thread 0: the item's z chunk -> buffer `slot`
+    const int64_t row = it / s.nch, c = it - row * s.nch;
+    const int64_t j0 = c * kSelChunk;
+    const int64_t cnt = min((int64_t)kSelChunk, s.n - j0);
+    const uint32_t bytes = (uint32_t)((cnt * 4 + 15) & ~(int64_t)15);
+    mbar_expect_tx(&zbar[slot], bytes);
+    bulk_g2s(zbuf + (size_t)slot * kSelChunk, s.z + row * s.z_stride + j0, bytes, &zbar[slot]);
+  };
+  if (t == 0) {
+    if ((int64_t)blockIdx.x < items) request(blockIdx.x, 0);
+    if ((int64_t)blockIdx.x + gridDim.x < items) request((int64_t)blockIdx.x + gridDim.x, 1);
+  }
+  uint32_t ph = 0u;
+  int slot = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, slot ^= 1) {
+    const int row = (int)(it / s.nch);
+    const int64_t c = it - (int64_t)row * s.nch;
+    HeadState *hs = s.hs + row;
+    const uint32_t state = hs->state;
+    const int M = hs->M;
+    const float kappa = hs->kappa;
+    const uint32_t dstar = hs->delta_star;
+    const unsigned long long r = hs->r_ties;
+    const unsigned long long pw = s.pre[(int64_t)row * s.nch + c];
+    const float inv_den = (float)(1.0 / (s.renorm ? (double)hs->sel_mass : (double)hs->S));
+    mbar_wait(&zbar[slot], (ph >> slot) & 1u);
+    ph ^= 1u << slot;
+    const float *zc = zbuf + (size_t)slot * kSelChunk;
+    const int64_t j0 = c * kSelChunk;
+    const int nv = (int)min((int64_t)kSelChunk, s.n - j0);
+    if (state == kStDone) {  // (an error state writes nothing: sel_k stays unset)
+      unsigned long long Sb = pw >> 32, Tb = pw & 0xffffffffull;
+      const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
+      unsigned long long wr = 0;  // kept tokens staged so far (slabs before)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i0 = 2048 * u + 4 * t;
+        const float4 v4 = *reinterpret_cast<const float4 *>(zc + i0);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        uint32_t dl[4], my = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          dl[e] = i0 + e < nv ? (uint32_t)(M - zint(vv[e])) : 0xffffffffu;
+          my += dl[e] < dstar ? (1u << 16) : ((dl[e] == dstar && dstar != 0xffffffffu) ? 1u : 0u);
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_u32(my, tot, sw);  // (strict << 16 | ties), each <= 2048
+        unsigned long long ts = Tb + (ex & 0xffffu);
+        unsigned long long pos = Sb + (ex >> 16) + (ts < r ? ts : r);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool strict = dl[e] < dstar;
+          const bool tie = dl[e] == dstar && dstar != 0xffffffffu;
+          if (strict || (tie && ts < r)) {
+            const unsigned ls = (unsigned)(pos - pos0);
+            stg_d[ls] = dl[e];
+            stg_o[ls] = (uint16_t)(i0 + e);
+            ++pos;
+          }
+          ts += tie ? 1u : 0u;
+        }
+        Sb += tot >> 16;
+        Tb += tot & 0xffffu;
+        (void)wr;
+      }
+      __syncthreads();
+      const int kept = (int)(Sb + (Tb < r ? Tb : r) - pos0);
+      int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
+      float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
+      for (int i = t; i < kept; i += kST) {
+        oi[i] = (int32_t)(j0 + stg_o[i]);
+        ow[i] = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
+      }
+    }
+    __syncthreads();  // every read of zc / the staging retired
+    if (t == 0 && it + 2 * (int64_t)gridDim.x < items) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request(it + 2 * (int64_t)gridDim.x, slot);
+    }
   }
 }
 
@@ -707,7 +830,8 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(k_sel_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_sel_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_sel_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_sel_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_sel_write, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     configured[dev] = 1;
@@ -716,16 +840,19 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
     launch_chain(k_sel_minmax, g12, dim3(kST), 0, st, s, per);
     note_launch();
   }
-  launch_chain(k_sel_mass, g12, dim3(kST), 0, st, s, per);
+  const size_t smem1 = (size_t)kZB * kSelChunk * 4;
+  launch_chain(k_sel_mass, g12, dim3(kST), smem1, st, s, per);
   note_launch();
-  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4;
+  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4 + (size_t)kZB * kSelChunk * 4;
   launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
   const size_t smem4 = (size_t)s.nch * 8 + (size_t)kNB * 4;
   if (smem4 > 200 * 1024) return cudaErrorInvalidValue;
   launch_chain(k_sel_prefix, dim3((unsigned)s.rows), dim3(kST), smem4, st, s);
   note_launch();
-  launch_chain(k_sel_write, dim3((unsigned)s.nch, (unsigned)s.rows), dim3(kST), (size_t)kSelChunk * 6, st, s);
+  const int64_t items3 = (int64_t)s.rows * s.nch;
+  const int64_t grid3 = items3 < 2LL * num_sms ? items3 : 2LL * num_sms;
+  launch_chain(k_sel_write, dim3((unsigned)grid3), dim3(kST), (size_t)kSelChunk * 14, st, s);
   note_launch();
   return cudaGetLastError();
 }
