@@ -151,14 +151,15 @@ __device__ __forceinline__ void sel_tokens(const float *zr, int64_t j0, int64_t 
 template <int NB>
 struct ZStream {
   float *buf;      // [NB][kSelChunk]
-  uint64_t *bar;   // [NB]
+  uint64_t *bar;   // [NB] "full" barriers
+  uint32_t *done;  // [NB] warps finished with the slot's chunk
   const float *zr;
   int64_t n;
   uint32_t ph;
-  __device__ void init(float *b, uint64_t *br, const float *z, int64_t n_) {
-    buf = b; bar = br; zr = z; n = n_; ph = 0u;
+  __device__ void init(float *b, uint64_t *br, uint32_t *dn, const float *z, int64_t n_) {
+    buf = b; bar = br; done = dn; zr = z; n = n_; ph = 0u;
     if (threadIdx.x == 0) {
-      for (int i = 0; i < NB; ++i) mbar_init(&bar[i], 1);
+      for (int i = 0; i < NB; ++i) { mbar_init(&bar[i], 1); done[i] = 0u; }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -175,11 +176,20 @@ struct ZStream {
     ph ^= 1u << slot;
     return buf + (size_t)slot * kSelChunk;
   }
-  // after a __syncthreads() that retired every read of `slot`: refill it with chunk c
-  __device__ void refill(int64_t c, int slot) {
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async write
-      request(c, slot);
+  // a warp is done with `slot` (every value it read from it has been consumed); the last warp
+  // out refills the slot with chunk c (c < 0: nothing left) -- no CTA-wide barrier, so warps
+  // drift up to NB chunks apart
+  __device__ void release(int64_t c, int slot) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const uint32_t old = atomicAdd(&done[slot], 1u);
+      if (old == blockDim.x / 32 - 1) {
+        done[slot] = 0u;
+        if (c >= 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async write
+          request(c, slot);
+        }
+      }
     }
   }
 };
@@ -275,12 +285,14 @@ __global__ void __launch_bounds__(kST) k_sel_minmax(SelArgs s, int64_t per) {
 
 // ---------------------------------------------------------------------------- K1
 constexpr int kZB = 3;  // z stream buffers per CTA
+constexpr int64_t kFinishInK2 = kZB * kSelChunk / 2;  // chunks whose counters fit the z buffers
 
 __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   extern __shared__ __align__(128) uint8_t sm1[];
   float *zbuf = reinterpret_cast<float *>(sm1);                                 // [kZB][kSelChunk]
   __shared__ uint32_t hist[kNB];
   __shared__ uint64_t zbar[kZB];
+  __shared__ uint32_t zdone[kZB];
   __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
   pdl_trigger();
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
     for (int64_t i = l0 + t; i < l1; i += kST) s.cntlo[(int64_t)row * nl + i] = 0u;
   }
   ZStream<kZB> zs;
-  zs.init(zbuf, zbar, s.z + (int64_t)row * s.z_stride, s.n);  // (its __syncthreads also covers the zeroing)
+  zs.init(zbuf, zbar, zdone, s.z + (int64_t)row * s.z_stride, s.n);  // (its __syncthreads also covers the zeroing)
   const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
   if (t == 0)
     for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
@@ -329,8 +341,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
       }
     };
     if (nv == kSelChunk) body(std::true_type{}); else body(std::false_type{});
-    __syncthreads();
-    if (c + kZB < c1) zs.refill(c + kZB, slot);
+    zs.release(c + kZB < c1 ? c + kZB : -1, slot);
   }
   S = warp_sum_u64(S);
   if ((t & 31) == 0) s_red[t >> 5] = S;
@@ -370,6 +381,8 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   }
   __syncthreads();
   if (tau_all && cap_all) {  // everything is kept
+    for (int64_t c = t; c < s.nch; c += kST)  // chunk c: c*kSelChunk tokens before it, all strict
+      s.pre[(int64_t)row * s.nch + c] = (unsigned long long)(c * kSelChunk) << 32;
     if (t == 0) {
       hs->delta_star = 0xffffffffu;
       hs->r_ties = 0u;
@@ -477,6 +490,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   uint32_t *wq = reinterpret_cast<uint32_t *>(sm2 + kNB * 12);      // [kST/32][64] per-warp Δ queues
   float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12 + kST * 8);  // [kZB][kSelChunk]
   __shared__ uint64_t zbar[kZB];
+  __shared__ uint32_t zdone[kZB];
   __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
   __shared__ int s_found;
@@ -492,7 +506,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
   for (int i = t; i < kNB; i += kST) { fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u; }
   ZStream<kZB> zs;
-  zs.init(zbuf, zbar, s.z + (int64_t)row * s.z_stride, s.n);
+  zs.init(zbuf, zbar, zdone, s.z + (int64_t)row * s.z_stride, s.n);
   const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
   if (t == 0)
     for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
@@ -558,8 +572,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     // the chunk's count of tokens above the range (K4 adds its in-range tokens below Δ*)
     nlo = __reduce_add_sync(0xffffffffu, nlo);
     if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + c], nlo);
-    __syncthreads();
-    if (c + kZB < c1) zs.refill(c + kZB, slot);
+    zs.release(c + kZB < c1 ? c + kZB : -1, slot);
   }
   __syncwarp();
   if (lane < qn) P += wmass(q[lane], kappa);
@@ -603,21 +616,21 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   const unsigned long long cc0 = hs->cnt_before, cm0 = __ldcg((const unsigned long long *)&hs->mass_before);
   resolve_bins(fc, f > 0 ? s_mass : nullptr, f, lo, hi, cc0, cm0, s, hs, row, kappa, theta, tau_all,
                cap_all, Sx, &s_found);
+  if (s.nch <= kFinishInK2) {  // the row's finish here (no K4 launch): counters over the z buffers
+    __syncthreads();
+    finish_row(s, row, reinterpret_cast<uint32_t *>(zbuf), reinterpret_cast<uint32_t *>(zbuf) + s.nch, fc);
+  }
 }
 
 // ---------------------------------------------------------------------------- K4
 // One CTA per row.  Dynamic shared memory: strict / tie counts per chunk [2][nch] (+ the
 // second refine's fine counts [kNB]).
-__global__ void __launch_bounds__(kST) k_sel_prefix(SelArgs s) {
-  extern __shared__ __align__(16) uint8_t sm4[];
-  uint32_t *cs = reinterpret_cast<uint32_t *>(sm4);       // [nch] strict
-  uint32_t *ct = cs + s.nch;                               // [nch] ties
-  uint32_t *fc = ct + s.nch;                               // [kNB] second-refine counts
+// The row's finish, by one whole CTA: (if narrowed) the second refine; then per chunk the
+// (strict, tie) counts and their exclusive prefix.  cs / ct: [nch] shared, fc: [kNB] shared.
+__device__ void finish_row(const SelArgs &s, int row, uint32_t *cs, uint32_t *ct, uint32_t *fc) {
   __shared__ unsigned long long sw[2][kST / 32];
   __shared__ int s_found;
-  pdl_trigger();
-  pdl_wait();
-  const int row = blockIdx.x, t = threadIdx.x;
+  const int t = threadIdx.x;
   HeadState *hs = s.hs + row;
   const float *zr = s.z + (int64_t)row * s.z_stride;
   const unsigned long long *lst = s.list + (int64_t)row * s.cap;
@@ -690,42 +703,34 @@ __global__ void __launch_bounds__(kST) k_sel_prefix(SelArgs s) {
   }
 }
 
-// ---------------------------------------------------------------------------- K3
-// Persistent CTAs over the (row, chunk) items; the next item's z chunk streams into the other
-// shared buffer (cp.async.bulk) while this one is compacted.  In a chunk thread t owns tokens
-// 4t .. 4t+3 of each 2048-token slab (index order = slab, thread, element).
-__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t my, uint32_t &total, uint32_t *sw) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t inc = my;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
-    if (lane >= off) inc += o;
-  }
-  if (lane == 31) sw[warp] = inc;
-  __syncthreads();
-  uint32_t before = 0;
-  total = 0;
-#pragma unroll
-  for (int w = 0; w < kST / 32; ++w) {
-    const uint32_t v = sw[w];
-    before += w < warp ? v : 0u;
-    total += v;
-  }
-  __syncthreads();  // sw is reused by the next scan
-  return before + inc - my;
+// K4 (only when a row's chunk counters do not fit K2's shared memory): one CTA per row
+__global__ void __launch_bounds__(kST) k_sel_prefix(SelArgs s) {
+  extern __shared__ __align__(16) uint8_t sm4[];
+  uint32_t *cs = reinterpret_cast<uint32_t *>(sm4);       // [nch] strict
+  uint32_t *ct = cs + s.nch;                               // [nch] ties
+  uint32_t *fc = ct + s.nch;                               // [kNB] second-refine counts
+  pdl_trigger();
+  pdl_wait();
+  finish_row(s, blockIdx.x, cs, ct, fc);
 }
 
-__global__ void __launch_bounds__(kST, 2) k_sel_write(SelArgs s) {
+// ---------------------------------------------------------------------------- K3
+// Persistent CTAs of kWT threads over the (row, chunk) items; the next item's z chunk streams
+// into the other shared buffer (cp.async.bulk) while this one is compacted.  Thread t owns the
+// 16 consecutive tokens 16t .. 16t+15 of the chunk, so one block scan of its (strict, tie)
+// counts orders the chunk.
+constexpr int kWT = 256;
+
+__global__ void __launch_bounds__(kWT, 4) k_sel_write(SelArgs s) {
   extern __shared__ __align__(128) uint8_t sm3[];
   float *zbuf = reinterpret_cast<float *>(sm3);                                        // [2][kSelChunk]
   uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3 + 2 * kSelChunk * 4);            // [kSelChunk]
   uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm3 + 3 * kSelChunk * 4);            // [kSelChunk]
   __shared__ uint64_t zbar[2];
-  __shared__ uint32_t sw[kST / 32];
+  __shared__ uint32_t sw[kWT / 32];
   pdl_trigger();
   pdl_wait();
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t items = (int64_t)s.rows * s.nch;
   if (t == 0) {
     mbar_init(&zbar[0], 1);
@@ -750,64 +755,79 @@ __global__ void __launch_bounds__(kST, 2) k_sel_write(SelArgs s) {
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x, slot ^= 1) {
     const int row = (int)(it / s.nch);
     const int64_t c = it - (int64_t)row * s.nch;
-    HeadState *hs = s.hs + row;
+    const HeadState *hs = s.hs + row;
     const uint32_t state = hs->state;
     const int M = hs->M;
     const float kappa = hs->kappa;
     const uint32_t dstar = hs->delta_star;
     const unsigned long long r = hs->r_ties;
     const unsigned long long pw = s.pre[(int64_t)row * s.nch + c];
-    const float inv_den = (float)(1.0 / (s.renorm ? (double)hs->sel_mass : (double)hs->S));
-    mbar_wait(&zbar[slot], (ph >> slot) & 1u);
-    ph ^= 1u << slot;
-    const float *zc = zbuf + (size_t)slot * kSelChunk;
+    const unsigned long long den = s.renorm ? hs->sel_mass : hs->S;
     const int64_t j0 = c * kSelChunk;
     const int nv = (int)min((int64_t)kSelChunk, s.n - j0);
+    mbar_wait(&zbar[slot], (ph >> slot) & 1u);
+    ph ^= 1u << slot;
+    const float *zc = zbuf + (size_t)slot * kSelChunk + 16 * t;
     if (state == kStDone) {  // (an error state writes nothing: sel_k stays unset)
-      unsigned long long Sb = pw >> 32, Tb = pw & 0xffffffffull;
-      const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
-      unsigned long long wr = 0;  // kept tokens staged so far (slabs before)
+      uint32_t dl[16], my = 0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int i0 = 2048 * u + 4 * t;
-        const float4 v4 = *reinterpret_cast<const float4 *>(zc + i0);
+      for (int k = 0; k < 4; ++k) {
+        const float4 v4 = *reinterpret_cast<const float4 *>(zc + 4 * k);
         const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-        uint32_t dl[4], my = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          dl[e] = i0 + e < nv ? (uint32_t)(M - zint(vv[e])) : 0xffffffffu;
-          my += dl[e] < dstar ? (1u << 16) : ((dl[e] == dstar && dstar != 0xffffffffu) ? 1u : 0u);
+          const int i = 16 * t + 4 * k + e;
+          dl[4 * k + e] = i < nv ? (uint32_t)(M - zint(vv[e])) : 0xffffffffu;
         }
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan_u32(my, tot, sw);  // (strict << 16 | ties), each <= 2048
-        unsigned long long ts = Tb + (ex & 0xffffu);
-        unsigned long long pos = Sb + (ex >> 16) + (ts < r ? ts : r);
+      }
+      const bool ties_on = dstar != 0xffffffffu;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const bool strict = dl[e] < dstar;
-          const bool tie = dl[e] == dstar && dstar != 0xffffffffu;
-          if (strict || (tie && ts < r)) {
-            const unsigned ls = (unsigned)(pos - pos0);
-            stg_d[ls] = dl[e];
-            stg_o[ls] = (uint16_t)(i0 + e);
-            ++pos;
-          }
-          ts += tie ? 1u : 0u;
+      for (int u = 0; u < 16; ++u) my += dl[u] < dstar ? (1u << 16) : ((ties_on && dl[u] == dstar) ? 1u : 0u);
+      // block exclusive scan of the packed (strict << 16 | ties) counts (each <= kSelChunk)
+      uint32_t inc = my;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += o;
+      }
+      if (lane == 31) sw[warp] = inc;
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kWT / 32; ++w) {
+        const uint32_t v = sw[w];
+        before += w < warp ? v : 0u;
+        total += v;
+      }
+      const uint32_t ex = before + inc - my;
+      const unsigned long long Sb = pw >> 32, Tb = pw & 0xffffffffull;
+      const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
+      unsigned long long ts = Tb + (ex & 0xffffu);
+      unsigned long long pos = Sb + (ex >> 16) + (ts < r ? ts : r);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const bool strict = dl[u] < dstar;
+        const bool tie = ties_on && dl[u] == dstar;
+        if (strict || (tie && ts < r)) {
+          const unsigned ls = (unsigned)(pos - pos0);
+          stg_d[ls] = dl[u];
+          stg_o[ls] = (uint16_t)(16 * t + u);
+          ++pos;
         }
-        Sb += tot >> 16;
-        Tb += tot & 0xffffu;
-        (void)wr;
+        ts += tie ? 1u : 0u;
       }
       __syncthreads();
-      const int kept = (int)(Sb + (Tb < r ? Tb : r) - pos0);
+      const unsigned long long tt = Tb + (total & 0xffffu);
+      const int kept = (int)(Sb + (total >> 16) + (tt < r ? tt : r) - pos0);
+      const float inv_den = (float)(1.0 / (double)den);
       int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
       float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
-      for (int i = t; i < kept; i += kST) {
+      for (int i = t; i < kept; i += kWT) {
         oi[i] = (int32_t)(j0 + stg_o[i]);
         ow[i] = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
       }
     }
-    __syncthreads();  // every read of zc / the staging retired
+    __syncthreads();  // every read of zc / the staging / sw retired
     if (t == 0 && it + 2 * (int64_t)gridDim.x < items) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       request(it + 2 * (int64_t)gridDim.x, slot);
@@ -846,13 +866,15 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
   const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4 + (size_t)kZB * kSelChunk * 4;
   launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
-  const size_t smem4 = (size_t)s.nch * 8 + (size_t)kNB * 4;
-  if (smem4 > 200 * 1024) return cudaErrorInvalidValue;
-  launch_chain(k_sel_prefix, dim3((unsigned)s.rows), dim3(kST), smem4, st, s);
-  note_launch();
+  if (s.nch > kFinishInK2) {  // rows too long for K2's in-place finish
+    const size_t smem4 = (size_t)s.nch * 8 + (size_t)kNB * 4;
+    if (smem4 > 200 * 1024) return cudaErrorInvalidValue;
+    launch_chain(k_sel_prefix, dim3((unsigned)s.rows), dim3(kST), smem4, st, s);
+    note_launch();
+  }
   const int64_t items3 = (int64_t)s.rows * s.nch;
-  const int64_t grid3 = items3 < 2LL * num_sms ? items3 : 2LL * num_sms;
-  launch_chain(k_sel_write, dim3((unsigned)grid3), dim3(kST), (size_t)kSelChunk * 14, st, s);
+  const int64_t grid3 = items3 < 4LL * num_sms ? items3 : 4LL * num_sms;
+  launch_chain(k_sel_write, dim3((unsigned)grid3), dim3(kWT), (size_t)kSelChunk * 14, st, s);
   note_launch();
   return cudaGetLastError();
 }
