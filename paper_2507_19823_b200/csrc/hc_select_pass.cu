@@ -480,6 +480,8 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
 }
 
 // ---------------------------------------------------------------------------- K2
+__device__ void finish_row(const SelArgs &s, int row, uint32_t *cs, uint32_t *ct, uint32_t *fc);
+
 // The CTA's token range is whole chunks; per chunk every thread holds 16 consecutive tokens.
 __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   extern __shared__ __align__(16) uint8_t sm2[];
