@@ -294,9 +294,19 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_pipe(LayerArgs a, int 
         r[k] = v ? ld_stream(c.P + (int64_t)c.i * a.n_cap + k * 256) : make_uint4(0, 0, 0, 0);
     }
   };
-  // one thread: bulk-copy c's slice into `slot`.  No proxy fence: every generic read of the
-  // slot has returned its data before the refilling warp observes the last release (see
-  // below), and a fence.proxy.async would also stall on this thread's in-flight loads.
+  // one thread: bulk-copy c's slice into `slot`.  Why no fence.proxy.async before this async-
+  // proxy write into a slot the warps just read through the generic proxy (a WAR hazard across
+  // proxies): every warp releases the slot only after ALL of its lookup results have been
+  // consumed -- the empty asm statements below take every accumulator as an input, so each
+  // LDS of the slot has returned its data into a register before the warp's counter
+  // increment is even issued, and the refill is issued only by the warp that observes the
+  // 16th increment.  No read of the slot is in flight when the bulk copy starts, so there is
+  // nothing for the async write to overtake.  This is the ordering CUTLASS's TMA pipelines
+  // rely on as well (the consumer's release is an mbarrier arrive after its reads; the
+  // producer's refill carries no proxy fence).  A fence.proxy.async here would also wait for
+  // this thread's own in-flight global loads (the code prefetch two steps ahead).  The
+  // selection's z streams (hc_select_pass.cu), whose release is not data-dependent in the
+  // same way, do issue the proxy fence.
   auto cslice = [&](const ScanCursor &c, int slot) {
     if (c.item < total_tiles) {
       mbar_expect_tx(&full[slot], slice_bytes);

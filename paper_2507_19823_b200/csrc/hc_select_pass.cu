@@ -397,17 +397,23 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   }
   __shared__ unsigned long long sw[3][kST / 32];
   __shared__ int s_ba, s_bb, s_bcap;
-  // per coarse bin b (Δ in [d0, d1]): count c and mass bounds c*W_lo <= mass <= c*W_hi.  W is
+  // per coarse bin b (Δ in [d0, d0 + 2^shift)): count c and mass bounds c*W_lo <= mass <=
+  // c*W_hi with W_hi = W(d0) and W_lo = W(next bin's d0) (<= W at the bin's last Δ).  W is
   // non-increasing in Δ up to the polynomial's rounding (rel. 2^-22) and the truncation: the
-  // bounds are widened by 2^-20 relative + 2 so they hold for every Δ of the bin
+  // bounds are widened by 2^-20 relative + 2 so they hold for every Δ of the bin.  W at every
+  // bin start is computed once into shared memory (over the idle z buffers).
+  unsigned long long *wb = reinterpret_cast<unsigned long long *>(zbuf);  // [kNB + 1]
+  for (int b = t; b <= kNB; b += kST) {
+    const uint32_t d0 = (uint32_t)b << shift;
+    wb[b] = (b < kNB && hist[b]) || (b > 0 && hist[b - 1]) ? wmass(min(d0, dmax), kappa) : 0ull;
+  }
+  __syncthreads();
   auto bin = [&](int k, uint32_t &c, unsigned long long &lo, unsigned long long &hi) {
     const uint32_t b = (uint32_t)(t * kBPT + k);
-    const uint32_t d0 = b << shift;
-    c = d0 <= dmax ? hist[b] : 0u;
+    c = ((b << shift) <= dmax) ? hist[b] : 0u;
     lo = hi = 0ull;
     if (c) {
-      const uint32_t d1 = min(d0 + ((1u << shift) - 1u), dmax);
-      const unsigned long long wh = wmass(d0, kappa), wl = wmass(d1, kappa);
+      const unsigned long long wh = wb[b], wl = wb[b + 1];
       hi = c * (wh + (wh >> 20) + 2ull);
       lo = c * (wl > (wl >> 20) + 2ull ? wl - (wl >> 20) - 2ull : 0ull);
     }
@@ -491,6 +497,8 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(sm2 + kNB * 4);  // resolve: over fml/fmh
   uint32_t *wq = reinterpret_cast<uint32_t *>(sm2 + kNB * 12);      // [kST/32][64] per-warp Δ queues
   float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12 + kST * 8);  // [kZB][kSelChunk]
+  unsigned long long *lq_all =                                          // [kST/32][64] per-warp list queues
+      reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kST * 8 + kZB * kSelChunk * 4);
   __shared__ uint64_t zbar[kZB];
   __shared__ uint32_t zdone[kZB];
   __shared__ unsigned long long s_red[kST / 32];
@@ -514,6 +522,8 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
   uint32_t *q = wq + warp * 64;
   int qn = 0;                 // warp-uniform queue length
+  unsigned long long *lq = lq_all + warp * 64;
+  int lqn = 0;                // warp-uniform list-queue length (flushed 32 entries per global atomic)
   unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
   unsigned long long *lst = s.list + (int64_t)row * s.cap;
   const unsigned lt = (1u << lane) - 1u;
@@ -551,10 +561,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
           }
         }
         const unsigned mr = __ballot_sync(0xffffffffu, inr);
-        if (mr) {  // in-range: fine histogram + the row's in-range list (warp-aggregated append)
-          unsigned base = 0;
-          if (lane == __ffs(mr) - 1) base = atomicAdd(&hs->ticket, (unsigned)__popc(mr));
-          base = __shfl_sync(0xffffffffu, base, __ffs(mr) - 1);
+        if (mr) {  // in-range: fine histogram + the row's in-range list (via the warp's queue)
           if (inr) {
             const uint32_t fb = (dl - lo) >> f;
             atomicAdd(&fc[fb], 1u);
@@ -565,8 +572,20 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
               wh += (old + wl < old) ? 1u : 0u;
               if (wh) atomicAdd(&fmh[fb], wh);
             }
-            const unsigned pos = base + __popc(mr & lt);
-            if (pos < (unsigned)s.cap) lst[pos] = ((unsigned long long)(cb + i0 + e) << 32) | dl;
+            lq[lqn + __popc(mr & lt)] = ((unsigned long long)(cb + i0 + e) << 32) | dl;
+          }
+          lqn += __popc(mr);
+          if (lqn >= 32) {  // one global atomic reserves 32 list slots for the warp
+            __syncwarp();
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&hs->ticket, 32u);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
+            const unsigned long long rest = lane + 32 < lqn ? lq[lane + 32] : 0ull;
+            __syncwarp();
+            if (lane + 32 < lqn) lq[lane] = rest;
+            lqn -= 32;
+            __syncwarp();
           }
         }
       }
@@ -578,6 +597,12 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   }
   __syncwarp();
   if (lane < qn) P += wmass(q[lane], kappa);
+  if (lqn > 0) {  // the warp's last list entries
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&hs->ticket, (unsigned)lqn);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < lqn && base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
+  }
   P = warp_sum_u64(P);
   if (lane == 0) s_red[warp] = P;
   __syncthreads();
@@ -865,7 +890,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
   const size_t smem1 = (size_t)kZB * kSelChunk * 4;
   launch_chain(k_sel_mass, g12, dim3(kST), smem1, st, s, per);
   note_launch();
-  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4 + (size_t)kZB * kSelChunk * 4;
+  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4 + (size_t)kZB * kSelChunk * 4 + (kST / 32) * 64 * 8;
   launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
   if (s.nch > kFinishInK2) {  // rows too long for K2's in-place finish

@@ -211,8 +211,16 @@ constexpr int kT2Threads = 256;
 template <int DBAR>
 constexpr int t2_max_rows() { return DBAR <= 8 ? 1024 : 512; }
 
+// quant_t_d without its +-2^16 pre-clamp when the head's bound guarantees |t * 2^e| < 2^15
+// (R2: A * 2^e < 2^15 unless the exponent clamped at -100) -- same result, two fewer ops
+__device__ __forceinline__ int quant_fast(float t, float s, bool preclamp) {
+  float x = __fmul_rn(t, s);
+  if (preclamp) x = fminf(fmaxf(x, -65536.0f), 65536.0f);
+  return min(max(rint_small(x), -32767), 32767);
+}
+
 template <int G, int DBAR>
-__global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
+__global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
   constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;  // centroids per thread
   constexpr int kTC = kT2Threads * CPT;           // centroids per CTA
   constexpr int kRows = t2_max_rows<DBAR>();
@@ -313,9 +321,11 @@ __global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
     const int b = u / a.Hkv, kv = u - b * a.Hkv;
     const int r0 = b * a.Hq + kv * G;
     float qs[G][DBAR], sc[G];
+    bool pre = false;  // the -100 exponent clamp: keep quant_t_d's pre-clamp (uniform per unit)
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       sc[h] = s_sc[r0 + h];
+      pre |= sc[h] == 0x1p-100f;
 #pragma unroll
       for (int e = 0; e < DBAR; ++e) qs[h][e] = s_q[(r0 + h) * DBAR + e];
     }
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(kT2Threads) k_table2(LayerArgs a) {
       }
       int16_t pk[G];
 #pragma unroll
-      for (int h = 0; h < G; ++h) pk[h] = (int16_t)quant_t_d(tv[h], sc[h]);
+      for (int h = 0; h < G; ++h) pk[h] = (int16_t)quant_fast(tv[h], sc[h], pre);
       int16_t *dst = Tu + (int64_t)m * G;
       if constexpr (G == 4) {  // even heads +32768-biased (hc_scan.cu Lut)
         uint2 v;
