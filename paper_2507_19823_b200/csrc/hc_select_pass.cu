@@ -11,9 +11,9 @@
 //                    by a slack that covers the exp2 polynomial's rounding), and keeps the
 //                    range of bins the exact cut can fall in (plus the k_max cap's bin, from
 //                    exact counts).  shift == 0 (bins = exact Δ values) resolves right there.
-//   K2 k_sel_refine  the exact mass of every token above that range (P_above; the W of
-//                    those ~15 % of the tokens computed 32 at a time from a warp queue, not
-//                    under divergence), exact counts (and exact masses if the range spans
+//   K2 k_sel_refine  the exact mass of every token above that range (P_above; W is
+//                    evaluated branch-free for every token -- cheaper than compacting the ~15 %
+//                    above the range), exact counts (and exact masses if the range spans
 //                    more than kNB values) of the tokens inside it, per K3-chunk counts of the
 //                    tokens above the range, and the in-range tokens themselves (index, Δ) on
 //                    a per-row list; the last CTA walks the fine bins to the exact Δ*, the
@@ -199,7 +199,7 @@ struct ZStream {
 // per-bin exact masses are mass[] and bin b spans Δ in [base + (b << f), base + ((b+1) << f)).
 // cc0 / cm0 = count / exact mass of every candidate with Δ below base.  Called by a whole CTA;
 // the thread that finds the cut writes the row's state.
-__device__ __noinline__ void resolve_bins(const uint32_t *cnt, const unsigned long long *mass, int f, uint32_t base,
+__device__ void resolve_bins(const uint32_t *cnt, const unsigned long long *mass, int f, uint32_t base,
                              uint32_t top, unsigned long long cc0, unsigned long long cm0,
                              const SelArgs &s, HeadState *hs, int row, float kappa,
                              unsigned long long theta, bool tau_all, bool cap_all,
@@ -284,75 +284,94 @@ __global__ void __launch_bounds__(kST) k_sel_minmax(SelArgs s, int64_t per) {
 }
 
 // ---------------------------------------------------------------------------- K1
-// K1 / K2 work decomposition: the (row, chunk) items of all rows, flattened, in equal
-// contiguous shares per CTA (a CTA's share may span a row boundary); a row's accumulators are
-// flushed when the CTA leaves the row, and the CTA whose flush completes the row's chunk
-// count runs the row's bound (K1) / resolve + finish (K2).
 constexpr int kZB = 3;  // z stream buffers per CTA
-constexpr int64_t kFinishInK2 = 4096;  // chunks whose counters fit K2's shared scratch (32 KB)
+constexpr int64_t kFinishInK2 = kZB * kSelChunk / 2;  // chunks whose counters fit the z buffers
 
-// the TMA chunk stream over flattened items (row = item / nch)
-template <int NB>
-struct ItemStream {
-  float *buf;
-  uint64_t *bar;
-  uint32_t *done;
-  const SelArgs *s;
-  uint32_t ph;
-  __device__ void init(float *b, uint64_t *br, uint32_t *dn, const SelArgs *s_) {
-    buf = b; bar = br; done = dn; s = s_; ph = 0u;
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < NB; ++i) { mbar_init(&bar[i], 1); done[i] = 0u; }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
-  __device__ void request(int64_t it, int slot) {  // one thread
-    const int64_t row = it / s->nch, c = it - row * s->nch;
-    const int64_t j0 = c * kSelChunk;
-    const int64_t cnt = min((int64_t)kSelChunk, s->n - j0);
-    const uint32_t bytes = (uint32_t)((cnt * 4 + 15) & ~(int64_t)15);  // z rows are padded to 64
-    mbar_expect_tx(&bar[slot], bytes);
-    bulk_g2s(buf + (size_t)slot * kSelChunk, s->z + row * s->z_stride + j0, bytes, &bar[slot]);
-  }
-  __device__ const float *wait(int slot) {
-    mbar_wait(&bar[slot], (ph >> slot) & 1u);
-    ph ^= 1u << slot;
-    return buf + (size_t)slot * kSelChunk;
-  }
-  // a warp is done with `slot`; the last warp out refills it with item `it` (< 0: none)
-  __device__ void release(int64_t it, int slot) {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) {
-      const uint32_t old = atomicAdd(&done[slot], 1u);
-      if (old == blockDim.x / 32 - 1) {
-        done[slot] = 0u;
-        if (it >= 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> async write
-          request(it, slot);
-        }
-      }
-    }
-  }
-};
-
-// K1 row bound (whole CTA, the row's last flusher): exact counts + exact S -> the coarse-bin
-// range the cut can fall in.  hist: the row's global counts, re-read; wb: [kNB + 1] scratch.
-__device__ __noinline__ void bound_row(const SelArgs &s, int row, uint32_t *hist, unsigned long long *wb) {
-  __shared__ unsigned long long sw[3][kST / 32];
-  __shared__ int s_ba, s_bb, s_bcap;
-  const int t = threadIdx.x;
+__global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
+  extern __shared__ __align__(128) uint8_t sm1[];
+  float *zbuf = reinterpret_cast<float *>(sm1);                                 // [kZB][kSelChunk]
+  __shared__ uint32_t hist[kNB];
+  __shared__ uint64_t zbar[kZB];
+  __shared__ uint32_t zdone[kZB];
+  __shared__ unsigned long long s_red[kST / 32];
+  __shared__ bool s_last;
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.y, t = threadIdx.x;
   HeadState *hs = s.hs + row;
   const int M = hs->M, zmin = hs->zmin;
   const float kappa = hs->kappa;
   const int shift = sel_shift(M, zmin);
-  const uint32_t dmax = (uint32_t)(M - zmin);
+  const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
+  for (int i = t; i < kNB; i += kST) hist[i] = 0u;
+  {  // this CTA's share of the row's refine histograms and chunk counters (used by K2 / K4)
+    const int64_t nf = (int64_t)kNB, nl = s.nch;
+    const int64_t f0 = nf * blockIdx.x / gridDim.x, f1 = nf * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t i = f0 + t; i < f1; i += kST) {
+      s.fcnt[(int64_t)row * kNB + i] = 0u;
+      s.fmass[(int64_t)row * kNB + i] = 0ull;
+    }
+    const int64_t l0 = nl * blockIdx.x / gridDim.x, l1 = nl * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t i = l0 + t; i < l1; i += kST) s.cntlo[(int64_t)row * nl + i] = 0u;
+  }
+  ZStream<kZB> zs;
+  zs.init(zbuf, zbar, zdone, s.z + (int64_t)row * s.z_stride, s.n);  // (its __syncthreads also covers the zeroing)
+  const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
+  if (t == 0)
+    for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
+  unsigned long long S = 0;
+  for (int64_t c = c0; c < c1; ++c) {
+    const int slot = (int)((c - c0) % kZB);
+    const float *zc = zs.wait(slot);
+    const int nv = (int)min((int64_t)kSelChunk, s.n - c * kSelChunk);
+    auto body = [&](auto full) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i0 = 4 * t + 2048 * u;
+        const float4 v = *reinterpret_cast<const float4 *>(zc + i0);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (decltype(full)::value || i0 + e < nv) {
+            const uint32_t dl = (uint32_t)(M - zint(vv[e]));
+            S += wmass(dl, kappa);
+            atomicAdd(&hist[dl >> shift], 1u);
+          }
+        }
+      }
+    };
+    if (nv == kSelChunk) body(std::true_type{}); else body(std::false_type{});
+    zs.release(c + kZB < c1 ? c + kZB : -1, slot);
+  }
+  S = warp_sum_u64(S);
+  if ((t & 31) == 0) s_red[t >> 5] = S;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
+    if (tot) atomicAdd((unsigned long long *)&hs->S, tot);
+  }
+  uint32_t *gh = s.ghist + (int64_t)row * kNB;
+  for (int i = t; i < kNB; i += kST) {
+    const uint32_t c = hist[i];
+    if (c) atomicAdd(&gh[i], c);
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    const uint32_t prev = atomicAdd(&hs->c1_done, 1u);
+    s_last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ---- the row's last CTA: exact counts, exact S, mass bounds per coarse bin
   const unsigned long long Sx = __ldcg((const unsigned long long *)&hs->S);
+  const uint32_t dmax = (uint32_t)(M - zmin);
   const bool tau_all = s.tau_q >= (1u << 24);
   const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
   const unsigned long long ntot = (unsigned long long)s.n;
   const bool cap_all = (unsigned long long)s.k_max >= ntot;
-  const uint32_t *gh = s.ghist + (int64_t)row * kNB;
   for (int i = t; i < kNB; i += kST) hist[i] = __ldcg(&gh[i]);
   if (t == 0) {
     hs->c1_done = 0u;
@@ -374,14 +393,16 @@ __device__ __noinline__ void bound_row(const SelArgs &s, int row, uint32_t *hist
       __threadfence();
       hs->state = kStDone;
     }
-    __syncthreads();
     return;
   }
+  __shared__ unsigned long long sw[3][kST / 32];
+  __shared__ int s_ba, s_bb, s_bcap;
   // per coarse bin b (Δ in [d0, d0 + 2^shift)): count c and mass bounds c*W_lo <= mass <=
   // c*W_hi with W_hi = W(d0) and W_lo = W(next bin's d0) (<= W at the bin's last Δ).  W is
   // non-increasing in Δ up to the polynomial's rounding (rel. 2^-22) and the truncation: the
   // bounds are widened by 2^-20 relative + 2 so they hold for every Δ of the bin.  W at every
-  // bin start is computed once.
+  // bin start is computed once into shared memory (over the idle z buffers).
+  unsigned long long *wb = reinterpret_cast<unsigned long long *>(zbuf);  // [kNB + 1]
   for (int b = t; b <= kNB; b += kST) {
     const uint32_t d0 = (uint32_t)b << shift;
     wb[b] = (b < kNB && hist[b]) || (b > 0 && hist[b - 1]) ? wmass(min(d0, dmax), kappa) : 0ull;
@@ -444,7 +465,6 @@ __device__ __noinline__ void bound_row(const SelArgs &s, int row, uint32_t *hist
   }
   if (lo_b >= kNB) {  // cannot happen: Θ <= S and k_max < n are always reached
     if (t == 0) hs->state = kStError;
-    __syncthreads();
     return;
   }
   // the count before the range (exact): the owner of bin lo_b has it
@@ -463,113 +483,22 @@ __device__ __noinline__ void bound_row(const SelArgs &s, int row, uint32_t *hist
     __threadfence();
     hs->state = kStRefine1;
   }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s) {
-  extern __shared__ __align__(128) uint8_t sm1[];
-  float *zbuf = reinterpret_cast<float *>(sm1);                                          // [kZB][kSelChunk]
-  unsigned long long *wb = reinterpret_cast<unsigned long long *>(sm1 + kZB * kSelChunk * 4);  // [kNB + 1]
-  __shared__ uint32_t hist[kNB];
-  __shared__ uint64_t zbar[kZB];
-  __shared__ uint32_t zdone[kZB];
-  __shared__ unsigned long long s_red[kST / 32];
-  __shared__ bool s_last;
-  pdl_trigger();
-  pdl_wait();
-  const int t = threadIdx.x;
-  const int64_t T = (int64_t)s.rows * s.nch;
-  const int64_t i0 = T * blockIdx.x / gridDim.x, i1 = T * (blockIdx.x + 1) / gridDim.x;
-  for (int i = t; i < kNB; i += kST) hist[i] = 0u;
-  ItemStream<kZB> zs;
-  zs.init(zbuf, zbar, zdone, &s);  // (its __syncthreads also covers the zeroing)
-  if (t == 0)
-    for (int i = 0; i < kZB && i0 + i < i1; ++i) zs.request(i0 + i, i);
-  int64_t it = i0;
-  while (it < i1) {
-    const int row = (int)(it / s.nch);
-    const int64_t r_end = min(i1, (int64_t)(row + 1) * s.nch);  // this CTA's items of the row
-    HeadState *hs = s.hs + row;
-    const int M = hs->M, zmin = hs->zmin;
-    const float kappa = hs->kappa;
-    const int shift = sel_shift(M, zmin);
-    unsigned long long S = 0;
-    for (; it < r_end; ++it) {
-      const int64_t c = it - (int64_t)row * s.nch;
-      const int slot = (int)((it - i0) % kZB);
-      const float *zc = zs.wait(slot);
-      if (threadIdx.x < 128) {  // K2 / K4 state of this chunk (and the row's fine histogram)
-        if (t == 0) s.cntlo[(int64_t)row * s.nch + c] = 0u;
-        if (c == 0)
-          for (int i = t; i < kNB; i += 128) {
-            s.fcnt[(int64_t)row * kNB + i] = 0u;
-            s.fmass[(int64_t)row * kNB + i] = 0ull;
-          }
-      }
-      const int nv = (int)min((int64_t)kSelChunk, s.n - c * kSelChunk);
-      auto body = [&](auto full) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k0 = 4 * t + 2048 * u;
-          const float4 v = *reinterpret_cast<const float4 *>(zc + k0);
-          const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (decltype(full)::value || k0 + e < nv) {
-              const uint32_t dl = (uint32_t)(M - zint(vv[e]));
-              S += wmass(dl, kappa);
-              atomicAdd(&hist[dl >> shift], 1u);
-            }
-          }
-        }
-      };
-      if (nv == kSelChunk) body(std::true_type{}); else body(std::false_type{});
-      zs.release(it + kZB < i1 ? it + kZB : -1, slot);
-    }
-    // ---- leave the row: flush S and the counts, count my chunks toward the row's total
-    const int64_t mine = r_end - max(i0, (int64_t)row * s.nch);
-    S = warp_sum_u64(S);
-    if ((t & 31) == 0) s_red[t >> 5] = S;
-    __syncthreads();
-    if (t == 0) {
-      unsigned long long tot = 0;
-      for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
-      if (tot) atomicAdd((unsigned long long *)&hs->S, tot);
-    }
-    uint32_t *gh = s.ghist + (int64_t)row * kNB;
-    for (int i = t; i < kNB; i += kST) {
-      const uint32_t c = hist[i];
-      if (c) atomicAdd(&gh[i], c);
-      hist[i] = 0u;
-    }
-    __threadfence();
-    __syncthreads();
-    if (t == 0) {
-      const uint32_t prev = atomicAdd(&hs->c1_done, (uint32_t)mine);
-      s_last = prev + (uint32_t)mine == (uint32_t)s.nch;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      bound_row(s, row, hist, wb);
-      for (int i = t; i < kNB; i += kST) hist[i] = 0u;
-      __syncthreads();
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------- K2
 __device__ void finish_row(const SelArgs &s, int row, uint32_t *cs, uint32_t *ct, uint32_t *fc);
 
-__global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s) {
-  extern __shared__ __align__(128) uint8_t sm2[];
-  float *zbuf = reinterpret_cast<float *>(sm2);                                        // [kZB][kSelChunk]
-  uint32_t *fc = reinterpret_cast<uint32_t *>(sm2 + kZB * kSelChunk * 4);             // [kNB] fine counts
-  uint32_t *fml = fc + kNB;                                                            // [kNB] fine mass, low
-  uint32_t *fmh = fc + 2 * kNB;                                                        // [kNB] high word
-  unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(fml);           // resolve: over fml/fmh
-  uint32_t *wq = fc + 3 * kNB;                                                         // [kST/32][64] Δ queues
-  unsigned long long *lq_all = reinterpret_cast<unsigned long long *>(wq + kST * 2);  // [kST/32][64] list queues
+// The CTA's token range is whole chunks; per chunk every thread holds 16 consecutive tokens.
+__global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
+  extern __shared__ __align__(16) uint8_t sm2[];
+  uint32_t *fc = reinterpret_cast<uint32_t *>(sm2);                 // [kNB] fine counts
+  uint32_t *fml = reinterpret_cast<uint32_t *>(sm2 + kNB * 4);      // [kNB] fine mass, low word
+  uint32_t *fmh = reinterpret_cast<uint32_t *>(sm2 + kNB * 8);      // [kNB] high word
+  unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(sm2 + kNB * 4);  // resolve: over fml/fmh
+  uint32_t *wq = reinterpret_cast<uint32_t *>(sm2 + kNB * 12);      // [kST/32][64] per-warp Δ queues
+  float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12 + kST * 8);  // [kZB][kSelChunk]
+  unsigned long long *lq_all =                                          // [kST/32][64] per-warp list queues
+      reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kST * 8 + kZB * kSelChunk * 4);
   __shared__ uint64_t zbar[kZB];
   __shared__ uint32_t zdone[kZB];
   __shared__ unsigned long long s_red[kST / 32];
@@ -577,158 +506,132 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s) {
   __shared__ int s_found;
   pdl_trigger();
   pdl_wait();
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int64_t T = (int64_t)s.rows * s.nch;
-  const int64_t i0 = T * blockIdx.x / gridDim.x, i1 = T * (blockIdx.x + 1) / gridDim.x;
+  const int row = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  HeadState *hs = s.hs + row;
+  if (hs->state != kStRefine1) return;
+  const int M = hs->M;
+  const float kappa = hs->kappa;
+  const uint32_t lo = hs->r_lo, hi = hs->r_hi;
+  const int f = hs->fshift;
+  const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
   for (int i = t; i < kNB; i += kST) { fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u; }
-  ItemStream<kZB> zs;
-  zs.init(zbuf, zbar, zdone, &s);
+  ZStream<kZB> zs;
+  zs.init(zbuf, zbar, zdone, s.z + (int64_t)row * s.z_stride, s.n);
+  const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
   if (t == 0)
-    for (int i = 0; i < kZB && i0 + i < i1; ++i) zs.request(i0 + i, i);
-  uint32_t *q = wq + warp * 64;
+    for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
   unsigned long long *lq = lq_all + warp * 64;
-  int64_t it = i0;
-  while (it < i1) {
-    const int row = (int)(it / s.nch);
-    const int64_t r_end = min(i1, (int64_t)(row + 1) * s.nch);
-    HeadState *hs = s.hs + row;
-    const bool active = hs->state == kStRefine1;
-    const int M = hs->M;
-    const float kappa = hs->kappa;
-    const uint32_t lo = hs->r_lo, hi = hs->r_hi;
-    const int f = hs->fshift;
-    unsigned long long *lst = s.list + (int64_t)row * s.cap;
-    int qn = 0;                 // warp-uniform mass-queue length
-    int lqn = 0;                // warp-uniform list-queue length (32 entries per global atomic)
-    unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
-    for (; it < r_end; ++it) {
-      const int64_t c = it - (int64_t)row * s.nch;
-      const int slot = (int)((it - i0) % kZB);
-      const float *zc = zs.wait(slot);
-      if (active) {
-        const int64_t cb = c * kSelChunk;
-        const int nv = (int)min((int64_t)kSelChunk, s.n - cb);
-        uint32_t nlo = 0;
+  int lqn = 0;                // warp-uniform list-queue length (flushed 32 entries per global atomic)
+  unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
+  unsigned long long *lst = s.list + (int64_t)row * s.cap;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t c = c0; c < c1; ++c) {
+    const int slot = (int)((c - c0) % kZB);
+    const float *zc = zs.wait(slot);
+    const int64_t cb = c * kSelChunk;
+    const int nv = (int)min((int64_t)kSelChunk, s.n - cb);
+    uint32_t nlo = 0;
 #pragma unroll
-        for (int u2 = 0; u2 < 2; ++u2) {
-          const int k0 = 4 * t + 2048 * u2;
-          const float4 v4 = *reinterpret_cast<const float4 *>(zc + k0);
-          const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+    for (int u2 = 0; u2 < 2; ++u2) {
+      const int i0 = 4 * t + 2048 * u2;
+      const float4 v4 = *reinterpret_cast<const float4 *>(zc + i0);
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const bool valid = k0 + e < nv;
-            const uint32_t dl = (uint32_t)(M - zint(vv[e]));
-            const bool above = valid && dl < lo;
-            const bool inr = valid && dl >= lo && dl <= hi;
-            nlo += above ? 1u : 0u;
-            // the exact W of the tokens above the range, 32 at a time from the warp's queue
-            const unsigned ma = __ballot_sync(0xffffffffu, above);
-            if (ma) {
-              if (above) q[qn + __popc(ma & lt)] = dl;
-              qn += __popc(ma);
-              if (qn >= 32) {
-                __syncwarp();
-                P += wmass(q[lane], kappa);
-                const uint32_t rest = lane + 32 < qn ? q[lane + 32] : 0u;
-                __syncwarp();
-                if (lane + 32 < qn) q[lane] = rest;
-                qn -= 32;
-                __syncwarp();
-              }
+      for (int e = 0; e < 4; ++e) {
+        const bool valid = i0 + e < nv;
+        const uint32_t dl = (uint32_t)(M - zint(vv[e]));
+        const bool above = valid && dl < lo;
+        const bool inr = valid && dl >= lo && dl <= hi;
+        nlo += above ? 1u : 0u;
+        // the exact W of the tokens above the range: evaluated for every token, branch-free
+        // (cheaper than compacting the ~15 % above the range: no ballots, no divergence)
+        const unsigned long long w = wmass(dl, kappa);
+        P += above ? w : 0ull;
+        const unsigned mr = __ballot_sync(0xffffffffu, inr);
+        if (mr) {  // in-range: fine histogram + the row's in-range list (via the warp's queue)
+          if (inr) {
+            const uint32_t fb = (dl - lo) >> f;
+            atomicAdd(&fc[fb], 1u);
+            if (f > 0) {  // fine bins of several Δ values: their exact mass too
+              uint32_t wl, wh;
+              mass_parts(dl, kappa, wl, wh);
+              const uint32_t old = atomicAdd(&fml[fb], wl);
+              wh += (old + wl < old) ? 1u : 0u;
+              if (wh) atomicAdd(&fmh[fb], wh);
             }
-            const unsigned mr = __ballot_sync(0xffffffffu, inr);
-            if (mr) {  // in-range: fine histogram + the row's in-range list (via the warp's queue)
-              if (inr) {
-                const uint32_t fb = (dl - lo) >> f;
-                atomicAdd(&fc[fb], 1u);
-                if (f > 0) {  // fine bins of several Δ values: their exact mass too
-                  uint32_t wl, wh;
-                  mass_parts(dl, kappa, wl, wh);
-                  const uint32_t old = atomicAdd(&fml[fb], wl);
-                  wh += (old + wl < old) ? 1u : 0u;
-                  if (wh) atomicAdd(&fmh[fb], wh);
-                }
-                lq[lqn + __popc(mr & lt)] = ((unsigned long long)(cb + k0 + e) << 32) | dl;
-              }
-              lqn += __popc(mr);
-              if (lqn >= 32) {  // one global atomic reserves 32 list slots for the warp
-                __syncwarp();
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&hs->ticket, 32u);
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
-                const unsigned long long rest = lane + 32 < lqn ? lq[lane + 32] : 0ull;
-                __syncwarp();
-                if (lane + 32 < lqn) lq[lane] = rest;
-                lqn -= 32;
-                __syncwarp();
-              }
-            }
+            lq[lqn + __popc(mr & lt)] = ((unsigned long long)(cb + i0 + e) << 32) | dl;
+          }
+          lqn += __popc(mr);
+          if (lqn >= 32) {  // one global atomic reserves 32 list slots for the warp
+            __syncwarp();
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&hs->ticket, 32u);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
+            const unsigned long long rest = lane + 32 < lqn ? lq[lane + 32] : 0ull;
+            __syncwarp();
+            if (lane + 32 < lqn) lq[lane] = rest;
+            lqn -= 32;
+            __syncwarp();
           }
         }
-        // the chunk's count of tokens above the range (the finish adds its in-range tokens below Δ*)
-        nlo = __reduce_add_sync(0xffffffffu, nlo);
-        if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + c], nlo);
       }
-      zs.release(it + kZB < i1 ? it + kZB : -1, slot);
     }
-    if (!active) continue;  // (uniform: every thread read the same state)
-    // ---- leave the row: flush the queues, P, the fine histogram; count my chunks
-    const int64_t mine = r_end - max(i0, (int64_t)row * s.nch);
-    __syncwarp();
-    if (lane < qn) P += wmass(q[lane], kappa);
-    if (lqn > 0) {  // the warp's last list entries
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(&hs->ticket, (unsigned)lqn);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (lane < lqn && base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
+    // the chunk's count of tokens above the range (K4 adds its in-range tokens below Δ*)
+    nlo = __reduce_add_sync(0xffffffffu, nlo);
+    if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + c], nlo);
+    zs.release(c + kZB < c1 ? c + kZB : -1, slot);
+  }
+  __syncwarp();
+  if (lqn > 0) {  // the warp's last list entries
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&hs->ticket, (unsigned)lqn);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < lqn && base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
+  }
+  P = warp_sum_u64(P);
+  if (lane == 0) s_red[warp] = P;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
+    if (tot) atomicAdd((unsigned long long *)&hs->mass_before, tot);
+  }
+  uint32_t *gc = s.fcnt + (int64_t)row * kNB;
+  unsigned long long *gm = s.fmass + (int64_t)row * kNB;
+  for (int i = t; i < kNB; i += kST) {
+    const uint32_t c = fc[i];
+    if (c) {
+      atomicAdd(&gc[i], c);
+      if (f > 0) atomicAdd(&gm[i], ((unsigned long long)fmh[i] << 32) + fml[i]);
     }
-    P = warp_sum_u64(P);
-    if (lane == 0) s_red[warp] = P;
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) {
+    const uint32_t prev = atomicAdd(&hs->c2_done, 1u);
+    s_last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // ---- the row's last CTA: walk the fine bins to the exact cut
+  __syncthreads();  // (s_mass overlays fml / fmh)
+  for (int i = t; i < kNB; i += kST) {
+    fc[i] = __ldcg(&gc[i]);
+    s_mass[i] = f > 0 ? __ldcg(&gm[i]) : 0ull;
+  }
+  if (t == 0) hs->c2_done = 0u;
+  __syncthreads();
+  const unsigned long long Sx = hs->S, theta = hs->theta;
+  const bool tau_all = s.tau_q >= (1u << 24);
+  const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
+  const unsigned long long cc0 = hs->cnt_before, cm0 = __ldcg((const unsigned long long *)&hs->mass_before);
+  resolve_bins(fc, f > 0 ? s_mass : nullptr, f, lo, hi, cc0, cm0, s, hs, row, kappa, theta, tau_all,
+               cap_all, Sx, &s_found);
+  if (s.nch <= kFinishInK2) {  // the row's finish here (no K4 launch): counters over the z buffers
     __syncthreads();
-    if (t == 0) {
-      unsigned long long tot = 0;
-      for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
-      if (tot) atomicAdd((unsigned long long *)&hs->mass_before, tot);
-    }
-    uint32_t *gc = s.fcnt + (int64_t)row * kNB;
-    unsigned long long *gm = s.fmass + (int64_t)row * kNB;
-    for (int i = t; i < kNB; i += kST) {
-      const uint32_t cc = fc[i];
-      if (cc) {
-        atomicAdd(&gc[i], cc);
-        if (f > 0) atomicAdd(&gm[i], ((unsigned long long)fmh[i] << 32) + fml[i]);
-      }
-      fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u;
-    }
-    __threadfence();
-    __syncthreads();
-    if (t == 0) {
-      const uint32_t prev = atomicAdd(&hs->c2_done, (uint32_t)mine);
-      s_last = prev + (uint32_t)mine == (uint32_t)s.nch;
-    }
-    __syncthreads();
-    if (!s_last) continue;
-    __threadfence();
-    // ---- the row's last flusher: walk the fine bins to the exact cut, then the row's finish
-    for (int i = t; i < kNB; i += kST) {
-      fc[i] = __ldcg(&gc[i]);
-      s_mass[i] = f > 0 ? __ldcg(&gm[i]) : 0ull;
-    }
-    if (t == 0) hs->c2_done = 0u;
-    __syncthreads();
-    const bool tau_all = s.tau_q >= (1u << 24);
-    const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
-    const unsigned long long cc0 = hs->cnt_before, cm0 = __ldcg((const unsigned long long *)&hs->mass_before);
-    resolve_bins(fc, f > 0 ? s_mass : nullptr, f, lo, hi, cc0, cm0, s, hs, row, kappa, hs->theta, tau_all,
-                 cap_all, hs->S, &s_found);
-    __syncthreads();
-    if (s.nch <= kFinishInK2)  // the row's finish here (no K4 launch): counters over fml / fmh
-      finish_row(s, row, fml, fml + s.nch, fc);
-    __syncthreads();
-    for (int i = t; i < kNB; i += kST) { fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u; }
-    __syncthreads();
+    finish_row(s, row, reinterpret_cast<uint32_t *>(zbuf), reinterpret_cast<uint32_t *>(zbuf) + s.nch, fc);
   }
 }
 
@@ -737,7 +640,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s) {
 // second refine's fine counts [kNB]).
 // The row's finish, by one whole CTA: (if narrowed) the second refine; then per chunk the
 // (strict, tie) counts and their exclusive prefix.  cs / ct: [nch] shared, fc: [kNB] shared.
-__device__ __noinline__ void finish_row(const SelArgs &s, int row, uint32_t *cs, uint32_t *ct, uint32_t *fc) {
+__device__ void finish_row(const SelArgs &s, int row, uint32_t *cs, uint32_t *ct, uint32_t *fc) {
   __shared__ unsigned long long sw[2][kST / 32];
   __shared__ int s_found;
   const int t = threadIdx.x;
@@ -957,36 +860,32 @@ __global__ void __launch_bounds__(kWT, 4) k_sel_write(SelArgs s) {
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
   if (s.nch != select_chunks(s.n)) return cudaErrorInvalidValue;
-  // K1 / K2: the flattened (row, chunk) items in equal shares, one wave of 2 CTAs per SM, at
-  // least 8 chunks per CTA (the per-CTA histogram flushes stay amortised on short rows)
-  const int64_t T = (int64_t)s.rows * s.nch;
-  int64_t g12 = 2LL * num_sms;
-  if (g12 > (T + 7) / 8) g12 = (T + 7) / 8;
-  if (g12 < 1) g12 = 1;
+  // K1 / K2: one wave of 2 CTAs per SM over all rows, whole chunks per CTA
+  int64_t cpr = (2LL * num_sms) / s.rows;
+  if (cpr < 1) cpr = 1;
+  if (cpr > s.nch) cpr = s.nch;
+  const int64_t per = (s.nch + cpr - 1) / cpr * kSelChunk;
+  cpr = (s.n + per - 1) / per;
+  const dim3 g12((unsigned)cpr, (unsigned)s.rows);
   static int configured[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t smem1 = (size_t)kZB * kSelChunk * 4 + (size_t)(kNB + 1) * 8;
-  const size_t smem2 = (size_t)kZB * kSelChunk * 4 + (size_t)kNB * 12 + (size_t)kST * 8 + (size_t)kST * 16;
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(k_sel_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-    cudaFuncSetAttribute(k_sel_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    cudaFuncSetAttribute(k_sel_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_sel_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_sel_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_sel_write, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     configured[dev] = 1;
   }
-  if (nsplit > 1) {  // (per-row grid for the plain max / min pass)
-    int64_t cpr = (2LL * num_sms) / s.rows;
-    if (cpr < 1) cpr = 1;
-    if (cpr > s.nch) cpr = s.nch;
-    const int64_t per = (s.nch + cpr - 1) / cpr * kSelChunk;
-    cpr = (s.n + per - 1) / per;
-    launch_chain(k_sel_minmax, dim3((unsigned)cpr, (unsigned)s.rows), dim3(kST), 0, st, s, per);
+  if (nsplit > 1) {
+    launch_chain(k_sel_minmax, g12, dim3(kST), 0, st, s, per);
     note_launch();
   }
-  launch_chain(k_sel_mass, dim3((unsigned)g12), dim3(kST), smem1, st, s);
+  const size_t smem1 = (size_t)kZB * kSelChunk * 4;
+  launch_chain(k_sel_mass, g12, dim3(kST), smem1, st, s, per);
   note_launch();
-  launch_chain(k_sel_refine, dim3((unsigned)g12), dim3(kST), smem2, st, s);
+  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4 + (size_t)kZB * kSelChunk * 4 + (kST / 32) * 64 * 8;
+  launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
   if (s.nch > kFinishInK2) {  // rows too long for K2's in-place finish
     const size_t smem4 = (size_t)s.nch * 8 + (size_t)kNB * 4;
@@ -994,7 +893,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
     launch_chain(k_sel_prefix, dim3((unsigned)s.rows), dim3(kST), smem4, st, s);
     note_launch();
   }
-  const int64_t items3 = T;
+  const int64_t items3 = (int64_t)s.rows * s.nch;
   const int64_t grid3 = items3 < 4LL * num_sms ? items3 : 4LL * num_sms;
   launch_chain(k_sel_write, dim3((unsigned)grid3), dim3(kWT), (size_t)kSelChunk * 14, st, s);
   note_launch();

@@ -233,12 +233,7 @@ __global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
   const int i = blockIdx.y;
   const int m0 = blockIdx.x * kTC;
   const int rows = a.B * a.Hq, units = a.B * a.Hkv;
-  // this CTA's block of units [u0, u1) -- their query heads are the rows [u0*G, u1*G)
-  const int upb = (units + gridDim.z - 1) / gridDim.z;
-  const int u0 = blockIdx.z * upb, u1 = min(units, u0 + upb);
-  const int r0b = u0 * G, nr = (u1 - u0) * G;
-  const int64_t cta = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  const int64_t nct = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x, nct = (int64_t)gridDim.x * gridDim.y;
   // ---- housekeeping of this layer's later kernels, spread over the CTAs
   if (a.gdone && cta == 0)
     for (int k = t; k < a.gdone_n; k += kT2Threads) a.gdone[k] = 0u;
@@ -269,10 +264,10 @@ __global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
   // group) item, spread over all threads with their loads in flight together; the max over
   // groups by shared atomics on the (non-negative) float bits
   uint32_t *s_abits = reinterpret_cast<uint32_t *>(s_sc);
-  for (int k = t; k < nr; k += kT2Threads) s_abits[k] = 0u;
+  for (int k = t; k < rows; k += kT2Threads) s_abits[k] = 0u;
   for (int k = t; k < a.cbg * DBAR; k += kT2Threads) s_cabs[k] = __ldg(a.cb_absmax + k);
   __syncthreads();
-  const int items = nr * a.g;  // (head of my units, group) pairs
+  const int items = rows * a.g;
   constexpr int kIB = DBAR >= 8 ? 32 / DBAR : 8;  // items per thread per round, loads issued before use
   for (int it0 = t; it0 < items; it0 += kT2Threads * kIB) {
     float qv[kIB][DBAR];
@@ -282,7 +277,7 @@ __global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
       const int r = it / a.g, gi = it - r * a.g;
 #pragma unroll
       for (int e = 0; e < DBAR; ++e)
-        qv[ib][e] = it < items ? h2f(__ldg(a.q + (int64_t)(r0b + r) * a.d + gi * DBAR + e)) : 0.0f;
+        qv[ib][e] = it < items ? h2f(__ldg(a.q + (int64_t)r * a.d + gi * DBAR + e)) : 0.0f;
     }
 #pragma unroll
     for (int ib = 0; ib < kIB; ++ib) {
@@ -301,12 +296,12 @@ __global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
     }
   }
   __syncthreads();
-  for (int r = t; r < nr; r += kT2Threads) {
+  for (int r = t; r < rows; r += kT2Threads) {
     const float bnd = __uint_as_float(s_abits[r]);
     const int e = a.lut8 ? scale_exponent8(bnd) : scale_exponent(bnd);
     s_sc[r] = pow2f(e);  // (same slot: this thread read it just above)
-    if (blockIdx.x == 0 && blockIdx.y == 0) {  // the heads' selection state for this layer
-      HeadState *hs = a.hs + r0b + r;
+    if (cta == 0) {  // the heads' selection state for this layer
+      HeadState *hs = a.hs + r;
       hs->e = e;
       hs->kappa = __fmul_rn(a.kappa0, pow2f(-e));
       hs->amax = __float_as_uint(bnd);
@@ -322,8 +317,9 @@ __global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
   }
   __syncthreads();
   // ---- every unit's entries for these centroids (entries m >= c are 0)
-  for (int u = u0; u < u1; ++u) {
-    const int r0 = u * G - r0b;  // local row of the unit's first head
+  for (int u = 0; u < units; ++u) {
+    const int b = u / a.Hkv, kv = u - b * a.Hkv;
+    const int r0 = b * a.Hq + kv * G;
     float qs[G][DBAR], sc[G];
     bool pre = false;  // the -100 exponent clamp: keep quant_t_d's pre-clamp (uniform per unit)
 #pragma unroll
@@ -385,12 +381,7 @@ static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
   if (table2_enabled() && a.B * a.Hq <= t2_max_rows<DBAR>()) {
     constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;
     constexpr int kTC = kT2Threads * CPT;
-    // unit blocks so the grid has ~1024 CTAs (each CTA stages the scales of its own heads only)
-    const int base = ((a.cpow2 + kTC - 1) / kTC) * a.g;
-    const int units = a.B * a.Hkv;
-    int ub = (1024 + base - 1) / base;
-    if (ub > units) ub = units;
-    dim3 grid((unsigned)((a.cpow2 + kTC - 1) / kTC), (unsigned)a.g, (unsigned)ub);
+    dim3 grid((unsigned)((a.cpow2 + kTC - 1) / kTC), (unsigned)a.g);
     launch_chain(k_table2<G, DBAR>, grid, dim3(kT2Threads), 0, s, a);
     note_launch();
     return cudaGetLastError();
