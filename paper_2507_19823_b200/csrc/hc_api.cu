@@ -85,6 +85,7 @@ int next_pow2(int c) {
 }
 
 constexpr int kMaxTSplit = 8;
+constexpr int64_t kSelFusedMaxN = 65536;  // longest row of the one-launch select kernel
 
 // Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
 // the group split so the work fills the SMs with the least shared-memory time, modelled
@@ -649,8 +650,12 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.cap = Lw.scap;
   // the round-1 fused select kernel stays reachable for A/B measurements (HC_SELECT=fused) and
   // for Eq. 5 inside the select kernel (HC_GATHER=fused)
-  static int sel_old = -1;
-  if (sel_old < 0) { const char *ev = getenv("HC_SELECT"); sel_old = (ev && !strcmp(ev, "fused")) ? 1 : 0; }
+  // Selection kernel by row length (measured): rows up to kSelFusedMaxN candidates
+  // take the one-launch cluster kernel (k_select_fused: latency-bound short rows, config 2),
+  // longer rows the three bandwidth-shaped passes (hc_select_pass.cu, configs 3-5).
+  // HC_SELECT=fused|pass forces one (read per call: the tests run both on the same shapes).
+  const char *sel_env = getenv("HC_SELECT");
+  const bool sel_old = sel_env ? !strcmp(sel_env, "fused") : n_cand <= kSelFusedMaxN;
   const bool fused_gather = !(budget.select_only || union_gather || rows_gather);
   if (shared) {
     if ((e = launch_group_select(a, n_q > 0 ? a.scan_split : 1, s)) != cudaSuccess)

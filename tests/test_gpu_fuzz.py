@@ -52,9 +52,14 @@ def _cases(k=None, seed=None):
     return out
 
 
+@pytest.mark.parametrize("sel", ["auto", "pass", "fused"])
 @pytest.mark.parametrize("kw", _cases(), ids=lambda kw: "-".join(f"{k}{v}" for k, v in kw.items()
                                                                 if k in ("d", "g", "G", "c", "n", "tau")))
-def test_fuzz_decode_parity(torch_cuda, kw):
+def test_fuzz_decode_parity(torch_cuda, kw, sel, monkeypatch):
+    """sel: the selection kernel -- auto (by row length), pass (hc_select_pass.cu's three passes)
+    or fused (the one-launch cluster kernel); both must be bit-exact on every shape."""
+    if sel != "auto":
+        monkeypatch.setenv("HC_SELECT", sel)
     case = Case(**kw)
     if case.n == 0 and case.n_res == 0:
         pytest.skip("empty")
