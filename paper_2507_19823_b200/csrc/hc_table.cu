@@ -53,6 +53,14 @@ __device__ __forceinline__ void table_entry(const float (&qs)[G][DBAR], const fl
 // each evaluate one group's chain; block max), then computes its centroids' entries
 // t (the same FMA chain as the oracle) and stores the packed G x int16
 // clamp(rint(t * 2^e_h)).  Each thread owns centroids m0+tid, m0+tid+256, ...
+// quant_t_d without its +-2^16 pre-clamp when the head's bound guarantees |t * 2^e| < 2^15
+// (R2: A * 2^e < 2^15 unless the exponent clamped at -100) -- same result, two fewer ops
+__device__ __forceinline__ int quant_fast(float t, float s, bool preclamp) {
+  float x = __fmul_rn(t, s);
+  if (preclamp) x = fminf(fmaxf(x, -65536.0f), 65536.0f);
+  return min(max(rint_small(x), -32767), 32767);
+}
+
 template <int G, int DBAR>
 __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   pdl_trigger();
@@ -136,11 +144,14 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
     }
   }
   float qs[G][DBAR];
+  bool pre[G];  // the -100 exponent clamp: keep quant_t_d's pre-clamp
 #pragma unroll
-  for (int h = 0; h < G; ++h)
+  for (int h = 0; h < G; ++h) {
+    pre[h] = sc[h] == 0x1p-100f;
 #pragma unroll
     for (int e = 0; e < DBAR; ++e)
       qs[h][e] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + i * DBAR + e));
+  }
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
   // batches of kTBatch centroids per thread: all their codebook loads issued before use
   constexpr int kTBatch = DBAR <= 4 ? 8 : 4;
@@ -150,8 +161,19 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   for (int ub = 0; ub < kTBatch; ++ub) {
     const int m = mb + ub * kTB;
     if (m < m0 + per && m < a.c) {
+      if constexpr (DBAR % 4 == 0) {  // 16-B codebook loads (rows are DBAR*4-B aligned)
 #pragma unroll
-      for (int e = 0; e < DBAR; ++e) cmb[ub][e] = __ldg(Ci + (int64_t)m * DBAR + e);
+        for (int e = 0; e < DBAR; e += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(Ci + (int64_t)m * DBAR + e));
+          cmb[ub][e] = v.x; cmb[ub][e + 1] = v.y; cmb[ub][e + 2] = v.z; cmb[ub][e + 3] = v.w;
+        }
+      } else if constexpr (DBAR == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2 *>(Ci + (int64_t)m * 2));
+        cmb[ub][0] = v.x; cmb[ub][1] = v.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < DBAR; ++e) cmb[ub][e] = __ldg(Ci + (int64_t)m * DBAR + e);
+      }
     } else {
 #pragma unroll
       for (int e = 0; e < DBAR; ++e) cmb[ub][e] = 0.0f;
@@ -178,7 +200,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
     }
     int16_t packed[G];
 #pragma unroll
-    for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_t_d(t[h], sc[h]);
+    for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_fast(t[h], sc[h], pre[h]);
     int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
     // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd head's
     // signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
@@ -198,194 +220,8 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// Codebook-stationary table build (default): CTA = (centroid chunk, group i).  The chunk's
-// codebook rows are loaded ONCE into registers and the CTA loops over every (b, kv) unit,
-// writing that unit's T entries for the chunk -- the codebook is read from L2 once per layer
-// instead of once per unit (config 3: 4 MiB instead of 128 MiB), and every store instruction
-// writes 256 consecutive 8-byte entries.  The per-head scale exponents (R2's bound, which
-// needs every group of q) are computed first by each CTA into shared memory: one warp per
-// head, lanes over groups.  Same arithmetic as k_table (the oracle's or_table_bits).
-constexpr int kT2Threads = 256;
-// query heads B*Hq whose scales and q̄_i a CTA stages (shared memory)
-template <int DBAR>
-constexpr int t2_max_rows() { return DBAR <= 8 ? 1024 : 512; }
-
-// quant_t_d without its +-2^16 pre-clamp when the head's bound guarantees |t * 2^e| < 2^15
-// (R2: A * 2^e < 2^15 unless the exponent clamped at -100) -- same result, two fewer ops
-__device__ __forceinline__ int quant_fast(float t, float s, bool preclamp) {
-  float x = __fmul_rn(t, s);
-  if (preclamp) x = fminf(fmaxf(x, -65536.0f), 65536.0f);
-  return min(max(rint_small(x), -32767), 32767);
-}
-
-template <int G, int DBAR>
-__global__ void __launch_bounds__(kT2Threads, 3) k_table2(LayerArgs a) {
-  constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;  // centroids per thread
-  constexpr int kTC = kT2Threads * CPT;           // centroids per CTA
-  constexpr int kRows = t2_max_rows<DBAR>();
-  __shared__ float s_sc[kRows];           // 2^e per query head (first: the bound's bits)
-  __shared__ float s_q[kRows * DBAR];     // q̄_i (group i of this CTA) per query head
-  __shared__ float s_cabs[128 * DBAR];    // the codebook's per-dimension max |C| (R2 constant)
-  pdl_trigger();
-  pdl_wait();
-  const int t = threadIdx.x;
-  const int i = blockIdx.y;
-  const int m0 = blockIdx.x * kTC;
-  const int rows = a.B * a.Hq, units = a.B * a.Hkv;
-  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x, nct = (int64_t)gridDim.x * gridDim.y;
-  // ---- housekeeping of this layer's later kernels, spread over the CTAs
-  if (a.gdone && cta == 0)
-    for (int k = t; k < a.gdone_n; k += kT2Threads) a.gdone[k] = 0u;
-  if (a.skctr && cta == 1 % nct)
-    for (int k = t; k < a.skctr_n; k += kT2Threads) a.skctr[k] = 0u;
-  if (a.sel_ghist) {
-    const int64_t nw = (int64_t)rows * kNB / 4;
-    uint4 *gh = reinterpret_cast<uint4 *>(a.sel_ghist);
-    for (int64_t k = nw * cta / nct + t; k < nw * (cta + 1) / nct; k += kT2Threads) gh[k] = make_uint4(0u, 0u, 0u, 0u);
-  }
-  if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
-    const int64_t nz4 = (a.n_q + 3) / 4, tot = (int64_t)rows * nz4;
-    for (int64_t k = tot * cta / nct + t; k < tot * (cta + 1) / nct; k += kT2Threads) {
-      const int64_t r = k / nz4, q4 = k - r * nz4;
-      reinterpret_cast<float4 *>(a.z + r * a.z_stride)[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  }
-  // ---- this CTA's codebook rows: loads issued first (consumed after the scales)
-  const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
-  float cm[CPT][DBAR];
-#pragma unroll
-  for (int k = 0; k < CPT; ++k) {
-    const int m = m0 + t + k * kT2Threads;
-#pragma unroll
-    for (int e = 0; e < DBAR; ++e) cm[k][e] = m < a.c ? __ldg(Ci + (int64_t)m * DBAR + e) : 0.0f;
-  }
-  // ---- R2 scales: A_h = max_i fmaf-chain_e(|q_h[i*dbar+e]|, Cabs[ci][e]) over every (head,
-  // group) item, spread over all threads with their loads in flight together; the max over
-  // groups by shared atomics on the (non-negative) float bits
-  uint32_t *s_abits = reinterpret_cast<uint32_t *>(s_sc);
-  for (int k = t; k < rows; k += kT2Threads) s_abits[k] = 0u;
-  for (int k = t; k < a.cbg * DBAR; k += kT2Threads) s_cabs[k] = __ldg(a.cb_absmax + k);
-  __syncthreads();
-  const int items = rows * a.g;
-  constexpr int kIB = DBAR >= 8 ? 32 / DBAR : 8;  // items per thread per round, loads issued before use
-  for (int it0 = t; it0 < items; it0 += kT2Threads * kIB) {
-    float qv[kIB][DBAR];
-#pragma unroll
-    for (int ib = 0; ib < kIB; ++ib) {
-      const int it = it0 + ib * kT2Threads;
-      const int r = it / a.g, gi = it - r * a.g;
-#pragma unroll
-      for (int e = 0; e < DBAR; ++e)
-        qv[ib][e] = it < items ? h2f(__ldg(a.q + (int64_t)r * a.d + gi * DBAR + e)) : 0.0f;
-    }
-#pragma unroll
-    for (int ib = 0; ib < kIB; ++ib) {
-      const int it = it0 + ib * kT2Threads;
-      if (it >= items) break;
-      const int r = it / a.g, gi = it - r * a.g;
-      const float *ca = s_cabs + (a.cbg == 1 ? 0 : gi) * DBAR;
-      float bb = __fmul_rn(fabsf(qv[ib][0]), ca[0]);
-#pragma unroll
-      for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(qv[ib][e]), ca[e], bb);
-      atomicMax(&s_abits[r], __float_as_uint(bb));
-      if (gi == i) {
-#pragma unroll
-        for (int e = 0; e < DBAR; ++e) s_q[r * DBAR + e] = qv[ib][e];
-      }
-    }
-  }
-  __syncthreads();
-  for (int r = t; r < rows; r += kT2Threads) {
-    const float bnd = __uint_as_float(s_abits[r]);
-    const int e = a.lut8 ? scale_exponent8(bnd) : scale_exponent(bnd);
-    s_sc[r] = pow2f(e);  // (same slot: this thread read it just above)
-    if (cta == 0) {  // the heads' selection state for this layer
-      HeadState *hs = a.hs + r;
-      hs->e = e;
-      hs->kappa = __fmul_rn(a.kappa0, pow2f(-e));
-      hs->amax = __float_as_uint(bnd);
-      hs->M = INT_MIN;  // folded by the scan / resident epilogues (atomics)
-      hs->zmin = INT_MAX;
-      hs->S = 0ull;     // the selection's accumulators and counters (hc_select_pass.cu)
-      hs->mass_before = 0ull;
-      hs->c1_done = 0u;
-      hs->c2_done = 0u;
-      hs->ticket = 0u;
-      hs->state = 0u;
-    }
-  }
-  __syncthreads();
-  // ---- every unit's entries for these centroids (entries m >= c are 0)
-  for (int u = 0; u < units; ++u) {
-    const int b = u / a.Hkv, kv = u - b * a.Hkv;
-    const int r0 = b * a.Hq + kv * G;
-    float qs[G][DBAR], sc[G];
-    bool pre = false;  // the -100 exponent clamp: keep quant_t_d's pre-clamp (uniform per unit)
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      sc[h] = s_sc[r0 + h];
-      pre |= sc[h] == 0x1p-100f;
-#pragma unroll
-      for (int e = 0; e < DBAR; ++e) qs[h][e] = s_q[(r0 + h) * DBAR + e];
-    }
-    int16_t *Tu = a.T + ((int64_t)u * a.g + i) * a.cpow2 * G;
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      const int m = m0 + t + k * kT2Threads;
-      if (m >= a.cpow2) break;
-      float tv[G];
-#pragma unroll
-      for (int h = 0; h < G; ++h) {  // the R2 FMA chain (or_table_bits)
-        float acc = __fmul_rn(qs[h][0], cm[k][0]);
-#pragma unroll
-        for (int e = 1; e < DBAR; ++e) acc = __fmaf_rn(qs[h][e], cm[k][e], acc);
-        tv[h] = m < a.c ? acc : 0.0f;
-      }
-      if (G == 4 && a.lut8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
-        uint32_t wv = 0;
-#pragma unroll
-        for (int h = 0; h < G; ++h) wv |= (uint32_t)(quant_t8_d(tv[h], sc[h]) + 128) << (8 * h);
-        reinterpret_cast<uint32_t *>(a.T)[((int64_t)u * a.g + i) * a.cpow2 + m] = wv;
-        continue;
-      }
-      int16_t pk[G];
-#pragma unroll
-      for (int h = 0; h < G; ++h) pk[h] = (int16_t)quant_fast(tv[h], sc[h], pre);
-      int16_t *dst = Tu + (int64_t)m * G;
-      if constexpr (G == 4) {  // even heads +32768-biased (hc_scan.cu Lut)
-        uint2 v;
-        v.x = (uint32_t)(pk[0] + 32768) | ((uint32_t)(uint16_t)pk[1] << 16);
-        v.y = (uint32_t)(pk[2] + 32768) | ((uint32_t)(uint16_t)pk[3] << 16);
-        *reinterpret_cast<uint2 *>(dst) = v;
-      } else if constexpr (G == 2) {
-        *reinterpret_cast<uint32_t *>(dst) = (uint32_t)(pk[0] + 32768) | ((uint32_t)(uint16_t)pk[1] << 16);
-      } else {
-        dst[0] = pk[0];
-      }
-    }
-  }
-}
-
-static bool table2_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char *ev = getenv("HC_TABLE");
-    v = (ev && !strcmp(ev, "old")) ? 0 : 1;
-  }
-  return v != 0;
-}
-
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
-  if (table2_enabled() && a.B * a.Hq <= t2_max_rows<DBAR>()) {
-    constexpr int CPT = DBAR >= 16 ? 1 : 16 / DBAR;
-    constexpr int kTC = kT2Threads * CPT;
-    dim3 grid((unsigned)((a.cpow2 + kTC - 1) / kTC), (unsigned)a.g);
-    launch_chain(k_table2<G, DBAR>, grid, dim3(kT2Threads), 0, s, a);
-    note_launch();
-    return cudaGetLastError();
-  }
   dim3 grid((unsigned)a.tsplit, (unsigned)a.g, (unsigned)(a.B * a.Hkv));
   launch_chain(k_table<G, DBAR>, grid, dim3(kTB), 0, s, a);
   note_launch();
