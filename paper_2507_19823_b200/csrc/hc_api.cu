@@ -85,7 +85,6 @@ int next_pow2(int c) {
 }
 
 constexpr int kMaxTSplit = 8;
-constexpr int64_t kSelFusedMaxN = 65536;  // longest row of the one-launch select kernel
 
 // Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
 // the group split so the work fills the SMs with the least shared-memory time, modelled
@@ -650,12 +649,13 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.cap = Lw.scap;
   // the round-1 fused select kernel stays reachable for A/B measurements (HC_SELECT=fused) and
   // for Eq. 5 inside the select kernel (HC_GATHER=fused)
-  // Selection kernel by row length (measured): rows up to kSelFusedMaxN candidates
-  // take the one-launch cluster kernel (k_select_fused: latency-bound short rows, config 2),
-  // longer rows the three bandwidth-shaped passes (hc_select_pass.cu, configs 3-5).
-  // HC_SELECT=fused|pass forces one (read per call: the tests run both on the same shapes).
+  // Selection kernel (hc_select_pass.cu): rows up to 64K candidates in one cluster
+  // kernel (k_sel_small: scores in registers, latency-bound short rows, configs 1-2), longer
+  // rows in three bandwidth-shaped passes (configs 3-5).  HC_SELECT=pass forces the passes,
+  // HC_SELECT=fused the round-1 cluster kernel (read per call: the tests run all of them).
   const char *sel_env = getenv("HC_SELECT");
-  const bool sel_old = sel_env ? !strcmp(sel_env, "fused") : n_cand <= kSelFusedMaxN;
+  const bool sel_old = sel_env && !strcmp(sel_env, "fused");
+  const int sel_force = (sel_env && !strcmp(sel_env, "pass")) ? 1 : 0;
   const bool fused_gather = !(budget.select_only || union_gather || rows_gather);
   if (shared) {
     if ((e = launch_group_select(a, n_q > 0 ? a.scan_split : 1, s)) != cudaSuccess)
@@ -664,7 +664,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, fused_gather ? 1 : 0, a.num_sms, s)) !=
         cudaSuccess)
       return cuda_check(e, "select");
-  } else if ((e = launch_select(sa, n_q > 0 ? a.scan_split : 1, a.num_sms, s)) != cudaSuccess) {
+  } else if ((e = launch_select(sa, n_q > 0 ? a.scan_split : 1, a.num_sms, s, sel_force)) != cudaSuccess) {
     return cuda_check(e, "select");
   }
   if (rows_gather) {

@@ -191,8 +191,9 @@ struct SelArgs {
 // partial planes in la.zpart
 cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nsplit, int do_gather,
                                 int num_sms, cudaStream_t st);
-// rows a3-a4 as three passes (hc_select_pass.cu, the default); nsplit > 1 adds a max/min pass
-cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st);
+// rows a3-a4 (hc_select_pass.cu): rows of <= 64K candidates in one cluster kernel, longer rows
+// in three passes (force = 1: the passes for any length); nsplit > 1: z carries no folded max/min
+cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force = 0);
 constexpr int kSelChunk = 4096;  // tokens per chunk of the selection passes (16 KB of z)
 inline int64_t select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChunk; }
 inline int64_t select_list_cap(int64_t n) { int64_t c = n / 16; return c < 4096 ? 4096 : c; }

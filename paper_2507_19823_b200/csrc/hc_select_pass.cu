@@ -31,9 +31,13 @@
 // Every decision is integer arithmetic on exact quantities (counts, u64 masses, the
 // 128-bit threshold Θ), so the kept set equals the oracle's bit for bit (or_select: sort by
 // (Δ asc, index asc), prefix to Θ, cap) -- the bounds only choose WHERE to look.
+#include <cooperative_groups.h>
+
 #include <type_traits>
 
 #include "hc_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace hc {
 
@@ -856,9 +860,419 @@ __global__ void __launch_bounds__(kWT, 4) k_sel_write(SelArgs s) {
   }
 }
 
+// ---------------------------------------------------------------------------- short rows
+// Rows of up to kSmallMaxN candidates (configs 1, 2): ONE kernel, a cluster of cs <= 8 CTAs per
+// row, every CTA holding its <= 8192 scores in registers (16 per thread) for all passes.  The
+// row-wide sums go through global atomics (histograms, L2-resident) and DSMEM (a few scalars per
+// CTA); after each cluster barrier every CTA re-reads the row's histogram and derives the same
+// bound / cut redundantly -- no single-CTA tail, no broadcast.  Same integer rules as the long-
+// row passes, so the same bit-exact result.
+constexpr int kSmTok = 8192;  // tokens per CTA
+constexpr int64_t kSmallMaxN = 8LL * kSmTok;
+
+struct CutResult {
+  int bin;  // kNB: none
+  unsigned long long cc, cm, c, m;  // count / mass before the bin, the bin's count / mass
+};
+
+// The cut over kNB consecutive bins (bin b covers Δ in [base + (b << f), ...); counts cnt[],
+// masses from mass[] or c * W(base + (b << f)); cc0 / cm0 before base) -- by the whole CTA,
+// result in *res (same on every CTA given the same inputs).
+__device__ void find_cut(const uint32_t *cnt, const unsigned long long *mass, int f, uint32_t base,
+                         uint32_t top, unsigned long long cc0, unsigned long long cm0, float kappa,
+                         unsigned long long theta, bool tau_all, bool cap_all, int64_t k_max,
+                         CutResult *res, unsigned long long (*sw)[kST / 32]) {
+  const int t = threadIdx.x;
+  unsigned long long c8[kBPT], m8[kBPT];
+  unsigned long long x[2] = {0, 0}, tot[2];
+#pragma unroll
+  for (int k = 0; k < kBPT; ++k) {
+    const int b = t * kBPT + k;
+    const uint32_t dl = base + ((uint32_t)b << f);
+    c8[k] = dl <= top ? cnt[b] : 0u;
+    m8[k] = mass ? mass[b] : (c8[k] ? c8[k] * wmass(dl, kappa) : 0ull);
+    x[0] += c8[k];
+    x[1] += m8[k];
+  }
+  if (t == 0) res->bin = kNB;
+  bscan<2>(x, tot, sw);
+  unsigned long long cc = cc0 + x[0], cm = cm0 + x[1];
+  int found = kNB;
+  unsigned long long fcc = 0, fcm = 0, fc = 0, fm = 0;
+#pragma unroll
+  for (int k = 0; k < kBPT; ++k) {
+    const bool trig = c8[k] && ((!tau_all && cm + m8[k] >= theta) || (!cap_all && cc + c8[k] >= (unsigned long long)k_max));
+    if (trig && found == kNB) { found = t * kBPT + k; fcc = cc; fcm = cm; fc = c8[k]; fm = m8[k]; }
+    cc += c8[k];
+    cm += m8[k];
+  }
+  if (found < kNB) atomicMin(&res->bin, found);
+  __syncthreads();
+  if (found < kNB && found == res->bin) { res->cc = fcc; res->cm = fcm; res->c = fc; res->m = fm; }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded) {
+  extern __shared__ __align__(16) uint8_t sm5[];
+  uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm5);                         // [kSmTok]
+  uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm5 + kSmTok * 4);           // [kSmTok]
+  unsigned long long *fm_s = reinterpret_cast<unsigned long long *>(sm5);    // [kNB] (over the staging)
+  __shared__ uint32_t hist[kNB];
+  __shared__ unsigned long long sw[2][kST / 32];
+  __shared__ struct { int M, zmin; unsigned long long S, P; uint32_t ns, nt; } slot;
+  __shared__ CutResult cr;
+  __shared__ int s_red_i[2][kST / 32];
+  __shared__ unsigned long long s_red[kST / 32];
+  cg::cluster_group cl = cg::this_cluster();
+  pdl_trigger();
+  pdl_wait();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.x / cs;
+  HeadState *hs = s.hs + row;
+  const int64_t j0 = (int64_t)rank * kSmTok + 16 * t;  // my 16 consecutive tokens
+  const float *zr = s.z + (int64_t)row * s.z_stride;
+  float zv[16];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t p = j0 + 4 * k;
+    if (p + 4 <= s.n) {
+      const float4 v = *reinterpret_cast<const float4 *>(zr + p);
+      zv[4 * k] = v.x; zv[4 * k + 1] = v.y; zv[4 * k + 2] = v.z; zv[4 * k + 3] = v.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zv[4 * k + u] = p + u < s.n ? zr[p + u] : 0.0f;
+    }
+  }
+  uint32_t vmask = 0;  // my valid tokens
+#pragma unroll
+  for (int u = 0; u < 16; ++u) vmask |= (j0 + u < s.n ? 1u : 0u) << u;
+  // zero my slice of the row's fine histograms (ordered before any use by the cluster barriers)
+  {
+    const int per = kNB / cs;
+    for (int i = rank * per + t; i < (rank + 1) * per; i += kST) {
+      s.fcnt[(int64_t)row * kNB + i] = 0u;
+      s.fmass[(int64_t)row * kNB + i] = 0ull;
+    }
+  }
+  // ---- M, zmin: folded by the scan epilogue, else a cluster reduction of my tokens' range
+  int M, zmin;
+  if (folded) {
+    M = hs->M;
+    zmin = hs->zmin;
+  } else {
+    int mx = INT_MIN, mn = INT_MAX;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (vmask >> u & 1u) { const int zi = zint(zv[u]); mx = max(mx, zi); mn = min(mn, zi); }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (lane == 0) { s_red_i[0][warp] = mx; s_red_i[1][warp] = mn; }
+    __syncthreads();
+    if (t == 0) {
+      for (int w = 1; w < kST / 32; ++w) { mx = max(mx, s_red_i[0][w]); mn = min(mn, s_red_i[1][w]); }
+      slot.M = mx;
+      slot.zmin = mn;
+    }
+    cl.sync();
+    M = INT_MIN; zmin = INT_MAX;
+    for (int r = 0; r < cs; ++r) {
+      const auto *o = cl.map_shared_rank(&slot, r);
+      M = max(M, o->M);
+      zmin = min(zmin, o->zmin);
+    }
+  }
+  const float kappa = hs->kappa;
+  const int shift = sel_shift(M, zmin);
+  const uint32_t dmax = (uint32_t)(M - zmin);
+  uint32_t dl[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) dl[u] = (vmask >> u & 1u) ? (uint32_t)(M - zint(zv[u])) : 0xffffffffu;
+  // ---- pass A: exact S, coarse counts -> the row's global histogram
+  for (int i = t; i < kNB; i += kST) hist[i] = 0u;
+  __syncthreads();
+  unsigned long long S = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    if (vmask >> u & 1u) {
+      S += wmass(dl[u], kappa);
+      atomicAdd(&hist[dl[u] >> shift], 1u);
+    }
+  }
+  S = warp_sum_u64(S);
+  if (lane == 0) s_red[warp] = S;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
+    slot.S = tot;
+  }
+  uint32_t *gh = s.ghist + (int64_t)row * kNB;
+  for (int i = t; i < kNB; i += kST) {
+    const uint32_t c = hist[i];
+    if (c) atomicAdd(&gh[i], c);
+  }
+  __threadfence();
+  cl.sync();
+  unsigned long long Sx = 0;
+  for (int r = 0; r < cs; ++r) Sx += cl.map_shared_rank(&slot, r)->S;
+  const bool tau_all = s.tau_q >= (1u << 24);
+  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
+  const unsigned long long ntot = (unsigned long long)s.n;
+  const bool cap_all = (unsigned long long)s.k_max >= ntot;
+  uint32_t dstar = 0xffffffffu;
+  unsigned long long r = 0, ksel = ntot, selmass = Sx;
+  long long kstar = (long long)ntot;
+  if (!(tau_all && cap_all)) {
+    // ---- the bound (every CTA, same inputs): candidate coarse bins of the cut
+    for (int i = t; i < kNB; i += kST) hist[i] = __ldcg(&gh[i]);
+    __syncthreads();
+    unsigned long long *wb = reinterpret_cast<unsigned long long *>(sm5);  // [kNB + 1] over the staging
+    for (int b = t; b <= kNB; b += kST) {
+      const uint32_t d0 = (uint32_t)b << shift;
+      wb[b] = (b < kNB && hist[b]) || (b > 0 && hist[b - 1]) ? wmass(min(d0, dmax), kappa) : 0ull;
+    }
+    __syncthreads();
+    __shared__ int s_ba, s_bb, s_bcap;
+    __shared__ unsigned long long s_cb;
+    if (t == 0) { s_ba = kNB; s_bb = -1; s_bcap = kNB; }
+    unsigned long long x[3] = {0, 0, 0}, tot3[3];
+    unsigned long long c8[kBPT];
+#pragma unroll
+    for (int k = 0; k < kBPT; ++k) {
+      const uint32_t b = (uint32_t)(t * kBPT + k);
+      c8[k] = ((b << shift) <= dmax) ? hist[b] : 0u;
+      if (c8[k]) {
+        const unsigned long long wh = wb[b], wl = wb[b + 1];
+        x[0] += c8[k];
+        x[1] += c8[k] * (wl > (wl >> 20) + 2ull ? wl - (wl >> 20) - 2ull : 0ull);
+        x[2] += c8[k] * (wh + (wh >> 20) + 2ull);
+      }
+    }
+    __shared__ unsigned long long sw3[3][kST / 32];
+    bscan<3>(x, tot3, sw3);
+    {
+      unsigned long long C = x[0], Lm = x[1], Um = x[2];
+      int ba = kNB, bb = -1, bcap = kNB;
+#pragma unroll
+      for (int k = 0; k < kBPT; ++k) {
+        const int b = t * kBPT + k;
+        unsigned long long lo = 0, hi = 0;
+        if (c8[k]) {
+          const unsigned long long wh = wb[b], wl = wb[b + 1];
+          hi = c8[k] * (wh + (wh >> 20) + 2ull);
+          lo = c8[k] * (wl > (wl >> 20) + 2ull ? wl - (wl >> 20) - 2ull : 0ull);
+          if (!tau_all && ba == kNB && Um + hi >= theta) ba = b;
+          if (!tau_all && Lm < theta) bb = b;
+          if (!cap_all && bcap == kNB && C + c8[k] >= (unsigned long long)s.k_max) bcap = b;
+        }
+        C += c8[k];
+        Lm += lo;
+        Um += hi;
+      }
+      if (ba < kNB) atomicMin(&s_ba, ba);
+      if (bb >= 0) atomicMax(&s_bb, bb);
+      if (bcap < kNB) atomicMin(&s_bcap, bcap);
+    }
+    __syncthreads();
+    int lo_b, hi_b;
+    if (tau_all || s_bcap < s_ba) {
+      lo_b = hi_b = s_bcap;
+    } else {
+      lo_b = s_ba;
+      hi_b = s_bb < lo_b ? lo_b : s_bb;
+      if (s_bcap < hi_b) hi_b = s_bcap;
+    }
+    if (lo_b / kBPT == t) {
+      unsigned long long C = x[0];
+      for (int k = 0; k < lo_b % kBPT; ++k) C += c8[k];
+      s_cb = C;
+    }
+    __syncthreads();
+    const uint32_t rlo = (uint32_t)lo_b << shift;
+    const uint32_t rhi = min(((uint32_t)(hi_b + 1) << shift) - 1u, dmax);
+    int f = 0;
+    while (((rhi - rlo) >> f) >= (uint32_t)kNB) ++f;
+    // ---- pass B: exact mass above the range, exact fine counts (+ masses) in it
+    unsigned long long P = 0;
+    uint32_t *gc = s.fcnt + (int64_t)row * kNB;
+    unsigned long long *gm = s.fmass + (int64_t)row * kNB;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (vmask >> u & 1u) {
+        if (dl[u] < rlo) {
+          P += wmass(dl[u], kappa);
+        } else if (dl[u] <= rhi) {
+          const uint32_t fb = (dl[u] - rlo) >> f;
+          atomicAdd(&gc[fb], 1u);
+          if (f > 0) atomicAdd(&gm[fb], (unsigned long long)wmass(dl[u], kappa));
+        }
+      }
+    }
+    P = warp_sum_u64(P);
+    if (lane == 0) s_red[warp] = P;
+    __syncthreads();
+    if (t == 0) {
+      unsigned long long tot = 0;
+      for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
+      slot.P = tot;
+    }
+    __threadfence();
+    cl.sync();
+    unsigned long long Px = 0;
+    for (int rr = 0; rr < cs; ++rr) Px += cl.map_shared_rank(&slot, rr)->P;
+    for (int i = t; i < kNB; i += kST) {
+      hist[i] = __ldcg(&gc[i]);
+      if (f > 0) fm_s[i] = __ldcg(&gm[i]);
+    }
+    __syncthreads();
+    find_cut(hist, f > 0 ? fm_s : nullptr, f, rlo, rhi, s_cb, Px, kappa, theta, tau_all, cap_all, s.k_max,
+             &cr, sw);
+    uint32_t base = rlo;
+    int bin = cr.bin;
+    if (f > 0 && bin < kNB) {  // narrow to the fine bin: exact per-Δ counts from my registers, summed over DSMEM
+      base = rlo + ((uint32_t)bin << f);
+      const uint32_t top2 = min(base + ((1u << f) - 1u), rhi);
+      const unsigned long long cc1 = cr.cc, cm1 = cr.cm;
+      __syncthreads();
+      for (int i = t; i < kNB; i += kST) hist[i] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if ((vmask >> u & 1u) && dl[u] >= base && dl[u] <= top2) atomicAdd(&hist[dl[u] - base], 1u);
+      cl.sync();
+      uint32_t *sum = reinterpret_cast<uint32_t *>(sm5 + kNB * 8);  // [kNB] over the staging
+      for (int i = t; i < kNB; i += kST) {
+        uint32_t c = 0;
+        for (int rr = 0; rr < cs; ++rr) c += cl.map_shared_rank(hist, rr)[i];
+        sum[i] = c;
+      }
+      cl.sync();  // peers done reading my hist
+      find_cut(sum, nullptr, 0, base, top2, cc1, cm1, kappa, theta, tau_all, cap_all, s.k_max, &cr, sw);
+      bin = cr.bin;
+    }
+    if (bin >= kNB) {  // cannot happen (the bounds hold): leave the row's state as an error
+      if (rank == 0 && t == 0) hs->state = kStError;
+      cl.sync();
+      return;
+    }
+    dstar = base + (uint32_t)bin;  // f == 0 here
+    const unsigned long long w = wmass(dstar, kappa);
+    unsigned long long r_tau = ~0ull, r_cap = ~0ull;
+    if (!tau_all && cr.cm + cr.m >= theta) r_tau = cr.cm >= theta ? 1ull : (theta - cr.cm + w - 1) / w;
+    if (r_tau == 0) r_tau = 1;
+    if (!cap_all && cr.cc + cr.c >= (unsigned long long)s.k_max) r_cap = (unsigned long long)s.k_max - cr.cc;
+    r = r_tau < r_cap ? r_tau : r_cap;
+    ksel = cr.cc + r;
+    kstar = r_tau <= r_cap ? (long long)(cr.cc + r_tau) : -1;
+    selmass = cr.cm + r * w;
+  }
+  // ---- pass C: ordered compaction (my 16 consecutive tokens; CTAs in rank order)
+  const bool ties_on = dstar != 0xffffffffu;
+  uint32_t ms = 0, mt = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    ms |= ((vmask >> u & 1u) && dl[u] < dstar ? 1u : 0u) << u;
+    mt |= ((vmask >> u & 1u) && ties_on && dl[u] == dstar ? 1u : 0u) << u;
+  }
+  const uint32_t my = ((uint32_t)__popc(ms) << 16) | (uint32_t)__popc(mt);
+  uint32_t inc = my;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += o;
+  }
+  __shared__ uint32_t swc[kST / 32];
+  if (lane == 31) swc[warp] = inc;
+  __syncthreads();
+  uint32_t before = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kST / 32; ++w) { before += w < warp ? swc[w] : 0u; total += swc[w]; }
+  if (t == 0) { slot.ns = total >> 16; slot.nt = total & 0xffffu; }
+  cl.sync();
+  unsigned long long Sb = 0, Tb = 0;
+  for (int rr = 0; rr < rank; ++rr) {
+    const auto *o = cl.map_shared_rank(&slot, rr);
+    Sb += o->ns;
+    Tb += o->nt;
+  }
+  const uint32_t ex = before + inc - my;
+  const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
+  unsigned long long ts = Tb + (ex & 0xffffu);
+  uint32_t keep = ms;
+  if (mt) {
+    const unsigned long long room = ts < r ? r - ts : 0ull;
+    uint32_t m = mt;
+    for (unsigned long long k = 0; k < room && m; ++k) { keep |= m & (0u - m); m &= m - 1u; }
+  }
+  const unsigned lb = (unsigned)(Sb + (ex >> 16) + (ts < r ? ts : r) - pos0);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    if (keep >> u & 1u) {
+      const unsigned ls = lb + __popc(keep & ((1u << u) - 1u));
+      stg_d[ls] = dl[u];
+      stg_o[ls] = (uint16_t)(16 * t + u);
+    }
+  }
+  __syncthreads();
+  const unsigned long long tt = Tb + (total & 0xffffu);
+  const int kept = (int)(Sb + (total >> 16) + (tt < r ? tt : r) - pos0);
+  const float inv_den = (float)(1.0 / (s.renorm ? (double)selmass : (double)Sx));
+  int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
+  float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
+  const int64_t cbase = (int64_t)rank * kSmTok;
+  for (int i = t; i < kept; i += kST) {
+    oi[i] = (int32_t)(cbase + stg_o[i]);
+    ow[i] = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
+  }
+  if (rank == 0 && t == 0) {
+    hs->M = M;
+    hs->zmin = zmin;
+    hs->shift = shift;
+    hs->S = Sx;
+    hs->theta = theta;
+    hs->delta_star = dstar;
+    hs->r_ties = (uint32_t)r;
+    hs->ksel = (int64_t)ksel;
+    hs->kstar = kstar;
+    hs->sel_mass = selmass;
+    hs->state = kStDone;
+    if (s.sel_k) s.sel_k[row] = (int64_t)ksel;
+  }
+  cl.sync();  // peers may still read my slot through DSMEM
+}
+
+cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st) {
+  const int cs = (int)((s.n + kSmTok - 1) / kSmTok);
+  if (cs < 1 || cs > 8) return cudaErrorInvalidValue;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaFuncSetAttribute(k_sel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTok * 6);
+    configured[dev] = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(s.rows * cs));
+  cfg.blockDim = dim3(kST);
+  cfg.dynamicSmemBytes = (size_t)kSmTok * 6;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sel_small, s, cs, folded);
+  note_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------- launcher
-cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st) {
+cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
+  if (force != 1 && s.n <= kSmallMaxN) return launch_select_small(s, nsplit > 1 ? 0 : 1, st);
   if (s.nch != select_chunks(s.n)) return cudaErrorInvalidValue;
   // K1 / K2: one wave of 2 CTAs per SM over all rows, whole chunks per CTA
   int64_t cpr = (2LL * num_sms) / s.rows;

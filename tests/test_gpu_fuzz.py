@@ -52,12 +52,13 @@ def _cases(k=None, seed=None):
     return out
 
 
-@pytest.mark.parametrize("sel", ["auto", "pass", "fused"])
+@pytest.mark.parametrize("sel", ["auto", "pass", "fused"])  # auto: k_sel_small for these short rows
 @pytest.mark.parametrize("kw", _cases(), ids=lambda kw: "-".join(f"{k}{v}" for k, v in kw.items()
                                                                 if k in ("d", "g", "G", "c", "n", "tau")))
 def test_fuzz_decode_parity(torch_cuda, kw, sel, monkeypatch):
-    """sel: the selection kernel -- auto (by row length), pass (hc_select_pass.cu's three passes)
-    or fused (the one-launch cluster kernel); both must be bit-exact on every shape."""
+    """sel: the selection kernel -- auto (by row length: the one-kernel cluster path k_sel_small
+    up to 64K candidates), pass (the three passes) or fused (round 1's cluster kernel); all
+    bit-exact on every shape."""
     if sel != "auto":
         monkeypatch.setenv("HC_SELECT", sel)
     case = Case(**kw)
