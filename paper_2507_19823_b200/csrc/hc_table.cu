@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
   }
   const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
   // batches of kTBatch centroids per thread: all their codebook loads issued before use
-  constexpr int kTBatch = DBAR <= 4 ? 8 : 4;
+  constexpr int kTBatch = DBAR <= 4 ? 16 : (DBAR == 8 ? 8 : 4);
   for (int mb = m0 + threadIdx.x; mb < m0 + per; mb += kTB * kTBatch) {
   float cmb[kTBatch][DBAR];
 #pragma unroll
