@@ -7,6 +7,7 @@
 #include <string.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "../../include/hc.h"
@@ -84,7 +85,6 @@ int next_pow2(int c) {
   return p;
 }
 
-constexpr int kMaxTSplit = 8;
 
 // Scan decomposition: choose tokens-per-thread (tile = 512*TPT tokens) and
 // the group split so the work fills the SMs with the least shared-memory time, modelled
@@ -543,16 +543,15 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
     if (e0 != cudaSuccess) return cuda_check(e0, "codebook absmax");
     a.cb_absmax = cba;
   }
-  {  // centroid splits only while units x groups leave SMs idle: every split repeats the
-     // CTA's scale-bound prologue (measured: 1 split per (unit, group) is fastest once the
-     // grid covers the SMs -- config 2 94.8 vs 98.4 us per layer with 4)
-    const int64_t base = B * H * g;
-    int ts = 1;
-    while (ts < kMaxTSplit && base * ts < 148 && Lw.cpow2 / (ts * 2) >= 256) ts *= 2;
+  {  // table parts per unit: about 4 resident CTAs per SM over all units (k_table streams
+     // its part of the unit's g * cpow2 entries; the scale prologue is per CTA)
+    const int64_t units = B * H, E = g * Lw.cpow2;
+    int64_t ts = (4 * (int64_t)num_sms() + units - 1) / units;
+    ts = std::max<int64_t>(1, std::min<int64_t>(ts, E / 256));
     static int ts_env = -1;  // dev override (HC_TSPLIT)
     if (ts_env < 0) { const char *ev = getenv("HC_TSPLIT"); ts_env = ev ? atoi(ev) : 0; }
-    if (ts_env > 0 && Lw.cpow2 / ts_env >= 256) ts = ts_env;
-    a.tsplit = ts;
+    if (ts_env > 0) ts = std::min<int64_t>(ts_env, std::max<int64_t>(1, E / 32));
+    a.tsplit = (int)ts;
   }
   a.z = (float *)(w8 + Lw.o_z);
   a.z_stride = Lw.z_stride;

@@ -118,7 +118,7 @@ struct LayerArgs {
   HeadState *hs;          // [B*Hq]
   int16_t *T;             // [units][g][cpow2][G]
   const float *cb_absmax; // layer [cbg][dbar]: max_m |C[ci][m][e]| (R2 bound)
-  int tsplit;             // centroid splits per (unit, group) in the table kernel
+  int tsplit;             // table CTAs per unit (k_table: contiguous parts of g * cpow2 entries)
   float *z;               // [B*Hq][z_stride]
   int64_t z_stride;
   // outputs

@@ -17,86 +17,112 @@ namespace hc {
 
 constexpr int kTB = 256;  // centroids per CTA
 
-template <int G, int DBAR>
-__device__ __forceinline__ void table_entry(const float (&qs)[G][DBAR], const float *Ci, int m,
-                                            int c, float (&t)[G]) {
+// One pass (R2).  CTA = (unit, part): part p of the unit's g * cpow2 entries, flattened as
+// e = i * cpow2 + m, split into gridDim.x contiguous 32-aligned ranges so every SM holds a few
+// CTAs with a long stream of stores each.  The CTA stages the unit's G query heads in shared
+// memory as floats [i][e][h], issues its first batch of codebook loads, derives the heads'
+// scale from the bound A_h = max_i fmaf-chain(|q̄_i,e|, Cabs[ci][e]) (threads t < g each
+// evaluate one group's chain; block max -- the same value in every CTA of the unit), then
+// computes each entry t (the oracle's FMA chain) and stores the packed G x int16
+// clamp(rint(t * 2^e_h)).  Thread tid owns entries e0 + tid, e0 + tid + 256, ...
+// quant_t_d in the magic-number domain ("magic quantizer"): y = fmaf(t, 2^e, 1.5 * 2^23) is
+// 1.5 * 2^23 + rint(t * 2^e) (t * 2^e is exact, or below 2^-126 and rounds to 0 either way;
+// the magic is even, so ties still go to even), clamped to +-32767 around the magic; the low
+// 16 bits of y's encoding are then rint's two's complement.  Equal to quant_t_d for every
+// finite t (a huge |t * 2^e| lands past the clamp, like quant_t_d's pre-clamp).  A magic of
+// 1.5 * 2^23 + 32768 (also even) yields r + 32768, the scan's biased even-head field.
+
+template <int DBAR>
+struct TBatch {  // codebook rows in flight per thread (registers: kTBatch * DBAR floats)
+  static constexpr int n = DBAR == 1 ? 16 : (DBAR == 2 ? 8 : (DBAR == 4 ? 4 : 2));
+};
+
+template <int DBAR>
+__device__ __forceinline__ void load_centroid(const float *cp, bool ok, float (&cm)[DBAR]) {
+  if (!ok) {
 #pragma unroll
-  for (int h = 0; h < G; ++h) t[h] = 0.0f;
-  if (m < c) {
-    float cm[DBAR];
-    const float *cp = Ci + (int64_t)m * DBAR;
-    if constexpr (DBAR % 4 == 0) {
+    for (int e = 0; e < DBAR; ++e) cm[e] = 0.0f;
+    return;
+  }
+  if constexpr (DBAR % 4 == 0) {  // 16-B codebook loads (rows are DBAR*4-B aligned)
 #pragma unroll
-      for (int e = 0; e < DBAR; e += 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(cp + e));
-        cm[e] = v.x; cm[e + 1] = v.y; cm[e + 2] = v.z; cm[e + 3] = v.w;
-      }
-    } else if constexpr (DBAR == 2) {
-      const float2 v = __ldg(reinterpret_cast<const float2 *>(cp));
-      cm[0] = v.x; cm[1] = v.y;
-    } else {
-#pragma unroll
-      for (int e = 0; e < DBAR; ++e) cm[e] = __ldg(cp + e);
+    for (int e = 0; e < DBAR; e += 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(cp + e));
+      cm[e] = v.x; cm[e + 1] = v.y; cm[e + 2] = v.z; cm[e + 3] = v.w;
     }
+  } else if constexpr (DBAR == 2) {
+    const float2 v = __ldg(reinterpret_cast<const float2 *>(cp));
+    cm[0] = v.x; cm[1] = v.y;
+  } else {
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float acc = __fmul_rn(qs[h][0], cm[0]);
-#pragma unroll
-      for (int e = 1; e < DBAR; ++e) acc = __fmaf_rn(qs[h][e], cm[e], acc);
-      t[h] = acc;
-    }
+    for (int e = 0; e < DBAR; ++e) cm[e] = __ldg(cp + e);
   }
 }
 
-// One pass (R2): every CTA = (unit, group i, centroid split) first derives its heads'
-// scale from the bound A_h = max_i fmaf-chain(|q̄_i,e|, Cabs[ci][e]) (threads t < g
-// each evaluate one group's chain; block max), then computes its centroids' entries
-// t (the same FMA chain as the oracle) and stores the packed G x int16
-// clamp(rint(t * 2^e_h)).  Each thread owns centroids m0+tid, m0+tid+256, ...
-// quant_t_d without its +-2^16 pre-clamp when the head's bound guarantees |t * 2^e| < 2^15
-// (R2: A * 2^e < 2^15 unless the exponent clamped at -100) -- same result, two fewer ops
-__device__ __forceinline__ int quant_fast(float t, float s, bool preclamp) {
-  float x = __fmul_rn(t, s);
-  if (preclamp) x = fminf(fmaxf(x, -65536.0f), 65536.0f);
-  return min(max(rint_small(x), -32767), 32767);
-}
-
-template <int G, int DBAR>
-__global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
+template <int G, int DBAR, bool L8>
+__global__ void __launch_bounds__(kTB, DBAR <= 4 ? 4 : 2) k_table(LayerArgs a) {
   pdl_trigger();
   pdl_wait();
-  if (a.gdone && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t nct = (int64_t)gridDim.x * gridDim.y;
+  if (a.gdone && cta == 0)
     for (int t = threadIdx.x; t < a.gdone_n; t += blockDim.x) a.gdone[t] = 0u;
-  if (a.skctr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 1 % gridDim.z)
+  if (a.skctr && cta == 1 % nct)
     for (int t = threadIdx.x; t < a.skctr_n; t += blockDim.x) a.skctr[t] = 0u;
   if (a.sel_ghist) {  // the selection's coarse histograms: every CTA clears its slice
     const int64_t nw = (int64_t)a.B * a.Hq * kNB / 4;  // uint4 words
-    const int64_t cta = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    const int64_t nct = (int64_t)gridDim.x * gridDim.y * gridDim.z;
     uint4 *gh = reinterpret_cast<uint4 *>(a.sel_ghist);
     for (int64_t t = nw * cta / nct + threadIdx.x; t < nw * (cta + 1) / nct; t += blockDim.x)
       gh[t] = make_uint4(0u, 0u, 0u, 0u);
   }
+  const int u = blockIdx.y;
+  const int b = u / a.Hkv, kv = u - b * a.Hkv;
+  const int part = blockIdx.x, parts = gridDim.x;
   if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
-    const int uu = blockIdx.z, bb = uu / a.Hkv, kk = uu - bb * a.Hkv;
     const int64_t nz4 = (a.n_q + 3) / 4;  // float4s per row (rows are 64-float aligned)
-    const int64_t part = (int64_t)blockIdx.y * gridDim.x + blockIdx.x, parts = (int64_t)gridDim.x * gridDim.y;
     for (int h = 0; h < G; ++h) {
-      float4 *zr = reinterpret_cast<float4 *>(a.z + ((int64_t)bb * a.Hq + kk * G + h) * a.z_stride);
-      for (int64_t q = part * blockDim.x + threadIdx.x; q < nz4; q += parts * blockDim.x)
+      float4 *zr = reinterpret_cast<float4 *>(a.z + ((int64_t)b * a.Hq + kv * G + h) * a.z_stride);
+      for (int64_t q = (int64_t)part * blockDim.x + threadIdx.x; q < nz4; q += (int64_t)parts * blockDim.x)
         zr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  const int u = blockIdx.z;
-  const int b = u / a.Hkv, kv = u - b * a.Hkv;
-  const int i = blockIdx.y;
-  const int split = blockIdx.x;
   const int hq0 = kv * G;
-  const int per = a.cpow2 / gridDim.x;          // centroids of this CTA
-  const int m0 = split * per;
-  HeadState *hs = a.hs + (int64_t)b * a.Hq + hq0;
-  // --- the per-head scale exponent from the bound
+  const int lg = 31 - __clz(a.cpow2);
+  const int E = a.g << lg;  // <= 2^24 (g <= 256, cpow2 <= 2^16)
+  const int e0 = (int)(((int64_t)E * part / parts) & ~(int64_t)31);
+  const int e1 = part + 1 == parts ? E : (int)(((int64_t)E * (part + 1) / parts) & ~(int64_t)31);
+  int16_t *Tu = a.T + (int64_t)u * E * G;  // this unit's [g][cpow2][G] slice
+  constexpr int NB = TBatch<DBAR>::n;
+  // the CTA walks its groups i in [i_lo, i_hi]; in group i it owns centroids [mlo, mhi)
+  const int i_lo = e0 >> lg, i_hi = e1 > e0 ? (e1 - 1) >> lg : i_lo - 1;
+  float cmb[NB][DBAR];  // one batch of codebook rows: centroids m + ub * kTB
+  auto load_batch = [&](int i, int m, int mc) {
+    const float *Cg = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
+#pragma unroll
+    for (int ub = 0; ub < NB; ++ub) {
+      const int mm = m + ub * kTB;
+      const bool ok = mm < mc;  // centroids m >= c are rows of zeros -> entries 0
+      load_centroid<DBAR>(Cg + (int64_t)(ok ? mm : 0) * DBAR, ok, cmb[ub]);
+    }
+  };
+  auto group_range = [&](int i, int &mlo, int &mhi) {
+    const int gb = i << lg;
+    mlo = max(e0 - gb, 0);
+    mhi = min(e1 - gb, a.cpow2);
+  };
+  {  // the first batch: in flight while the scale is derived
+    int mlo, mhi;
+    group_range(i_lo, mlo, mhi);
+    if (i_lo <= i_hi) load_batch(i_lo, mlo + (int)threadIdx.x, min(mhi, a.c));
+  }
+  __shared__ __align__(16) float qsm[256 * G];  // [d][G] = [i][e][h], d <= 256
   __shared__ float sA[G][kTB / 32];
+  for (int t = threadIdx.x; t < a.d * G; t += kTB) {
+    const int h = t % G, j = t / G;
+    qsm[t] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + j));
+  }
+  __syncthreads();
+  HeadState *hs = a.hs + (int64_t)b * a.Hq + hq0;
   float sc[G];
   {
     float bnd[G];
@@ -104,12 +130,12 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
     for (int h = 0; h < G; ++h) bnd[h] = 0.0f;
     for (int gi = threadIdx.x; gi < a.g; gi += kTB) {
       const float *ca = a.cb_absmax + (int64_t)(a.cbg == 1 ? 0 : gi) * DBAR;
+      const float *qg = qsm + gi * DBAR * G;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        const uint16_t *qh = a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + gi * DBAR;
-        float bb = __fmul_rn(fabsf(h2f(__ldg(qh))), __ldg(ca));
+        float bb = __fmul_rn(fabsf(qg[h]), __ldg(ca));
 #pragma unroll
-        for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(h2f(__ldg(qh + e))), __ldg(ca + e), bb);
+        for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(qg[e * G + h]), __ldg(ca + e), bb);
         bnd[h] = fmaxf(bnd[h], bb);
       }
     }
@@ -128,7 +154,7 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
       for (int w = 0; w < kTB / 32; ++w) A = fmaxf(A, sA[h][w]);
       const int e = a.lut8 ? scale_exponent8(A) : scale_exponent(A);
       sc[h] = pow2f(e);
-      if (i == 0 && split == 0 && threadIdx.x == 0) {
+      if (part == 0 && threadIdx.x == 0) {
         hs[h].e = e;
         hs[h].kappa = __fmul_rn(a.kappa0, pow2f(-e));
         hs[h].amax = __float_as_uint(A);
@@ -143,87 +169,84 @@ __global__ void __launch_bounds__(kTB) k_table(LayerArgs a) {
       }
     }
   }
-  float qs[G][DBAR];
-  bool pre[G];  // the -100 exponent clamp: keep quant_t_d's pre-clamp
+  // heads in pairs for the packed fp32x2 FMA (every lane an IEEE fmaf, as the oracle's chain)
+  constexpr int NP = G >= 2 ? G / 2 : 1;
+  float2 sp[NP], mg[NP], lo[NP], hi[NP];
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    pre[h] = sc[h] == 0x1p-100f;
-#pragma unroll
-    for (int e = 0; e < DBAR; ++e)
-      qs[h][e] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + i * DBAR + e));
+  for (int p = 0; p < NP; ++p) {
+    // the magic quantizer: even heads' magic carries the +32768 bias
+    const float me = G >= 2 ? 12582912.0f + 32768.0f : 12582912.0f;
+    sp[p] = make_float2(sc[2 * p], G >= 2 ? sc[2 * p + 1] : 1.0f);
+    mg[p] = make_float2(me, 12582912.0f);
+    lo[p] = make_float2(me - 32767.0f, 12582912.0f - 32767.0f);
+    hi[p] = make_float2(me + 32767.0f, 12582912.0f + 32767.0f);
   }
-  const float *Ci = a.C + (int64_t)(a.cbg == 1 ? 0 : i) * a.c * DBAR;
-  // batches of kTBatch centroids per thread: all their codebook loads issued before use
-  constexpr int kTBatch = DBAR <= 4 ? 16 : (DBAR == 8 ? 8 : 4);
-  for (int mb = m0 + threadIdx.x; mb < m0 + per; mb += kTB * kTBatch) {
-  float cmb[kTBatch][DBAR];
+  bool have = true;  // cmb holds the first batch of group i_lo
+  for (int i = i_lo; i <= i_hi; ++i) {
+    int mlo, mhi;
+    group_range(i, mlo, mhi);
+    const int mc = min(mhi, a.c);
+    float2 qp[NP][DBAR];  // (q_2p, q_2p+1) of group i, component k
 #pragma unroll
-  for (int ub = 0; ub < kTBatch; ++ub) {
-    const int m = mb + ub * kTB;
-    if (m < m0 + per && m < a.c) {
-      if constexpr (DBAR % 4 == 0) {  // 16-B codebook loads (rows are DBAR*4-B aligned)
+    for (int k = 0; k < DBAR; ++k)
 #pragma unroll
-        for (int e = 0; e < DBAR; e += 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(Ci + (int64_t)m * DBAR + e));
-          cmb[ub][e] = v.x; cmb[ub][e + 1] = v.y; cmb[ub][e + 2] = v.z; cmb[ub][e + 3] = v.w;
+      for (int p = 0; p < NP; ++p)
+        qp[p][k] = G >= 2 ? make_float2(qsm[(i * DBAR + k) * G + 2 * p], qsm[(i * DBAR + k) * G + 2 * p + 1])
+                          : make_float2(qsm[(i * DBAR + k) * G], 0.0f);
+    int16_t *Tg = Tu + (int64_t)(i << lg) * G;
+    for (int m = mlo + (int)threadIdx.x; m < mhi; m += kTB * NB) {
+      if (!have) load_batch(i, m, mc);
+      have = false;
+#pragma unroll
+      for (int ub = 0; ub < NB; ++ub) {
+        const int mm = m + ub * kTB;
+        if (mm >= mhi) break;
+        float2 t[NP];  // the R2 FMA chain
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          t[p] = __fmul2_rn(qp[p][0], make_float2(cmb[ub][0], cmb[ub][0]));
+#pragma unroll
+          for (int k = 1; k < DBAR; ++k) t[p] = __ffma2_rn(qp[p][k], make_float2(cmb[ub][k], cmb[ub][k]), t[p]);
         }
-      } else if constexpr (DBAR == 2) {
-        const float2 v = __ldg(reinterpret_cast<const float2 *>(Ci + (int64_t)m * 2));
-        cmb[ub][0] = v.x; cmb[ub][1] = v.y;
-      } else {
+        if constexpr (G == 4 && L8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
+          const float th[4] = {t[0].x, t[0].y, t[NP - 1].x, t[NP - 1].y};
+          uint32_t wv = 0;
 #pragma unroll
-        for (int e = 0; e < DBAR; ++e) cmb[ub][e] = __ldg(Ci + (int64_t)m * DBAR + e);
+          for (int h = 0; h < 4; ++h) wv |= (uint32_t)(quant_t8_d(th[h], sc[h]) + 128) << (8 * h);
+          reinterpret_cast<uint32_t *>(a.T)[(int64_t)u * E + (i << lg) + mm] = wv;
+          continue;
+        } else {
+        uint32_t w[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          float2 y = __ffma2_rn(t[p], sp[p], mg[p]);
+          y.x = fminf(fmaxf(y.x, lo[p].x), hi[p].x);
+          y.y = fminf(fmaxf(y.y, lo[p].y), hi[p].y);
+          w[p] = __byte_perm(__float_as_uint(y.x), __float_as_uint(y.y), 0x5410);
+        }
+        // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd
+        // head's signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
+        if constexpr (G == 4) {
+          *reinterpret_cast<uint2 *>(Tg + mm * 4) = make_uint2(w[0], w[NP - 1]);
+        } else if constexpr (G == 2) {
+          *reinterpret_cast<uint32_t *>(Tg + mm * 2) = w[0];
+        } else {
+          Tg[mm] = (int16_t)(uint16_t)w[0];
+        }
+        }
       }
-    } else {
-#pragma unroll
-      for (int e = 0; e < DBAR; ++e) cmb[ub][e] = 0.0f;
     }
-  }
-#pragma unroll
-  for (int ub = 0; ub < kTBatch; ++ub) {
-    const int m = mb + ub * kTB;
-    if (m >= m0 + per) break;
-    float t[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {  // the R2 FMA chain (table_entry), entries m >= c are 0
-      float acc = __fmul_rn(qs[h][0], cmb[ub][0]);
-#pragma unroll
-      for (int e = 1; e < DBAR; ++e) acc = __fmaf_rn(qs[h][e], cmb[ub][e], acc);
-      t[h] = m < a.c ? acc : 0.0f;
-    }
-    if (G == 4 && a.lut8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
-      uint32_t wv = 0;
-#pragma unroll
-      for (int h = 0; h < G; ++h) wv |= (uint32_t)(quant_t8_d(t[h], sc[h]) + 128) << (8 * h);
-      reinterpret_cast<uint32_t *>(a.T)[((int64_t)u * a.g + i) * a.cpow2 + m] = wv;
-      continue;
-    }
-    int16_t packed[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) packed[h] = (int16_t)quant_fast(t[h], sc[h], pre[h]);
-    int16_t *dst = a.T + (((int64_t)u * a.g + i) * a.cpow2 + m) * G;
-    // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd head's
-    // signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
-    if constexpr (G == 4) {
-      uint2 v;
-      v.x = (uint32_t)(packed[0] + 32768) | ((uint32_t)(uint16_t)packed[1] << 16);
-      v.y = (uint32_t)(packed[2] + 32768) | ((uint32_t)(uint16_t)packed[3] << 16);
-      *reinterpret_cast<uint2 *>(dst) = v;
-    } else if constexpr (G == 2) {
-      *reinterpret_cast<uint32_t *>(dst) =
-          (uint32_t)(packed[0] + 32768) | ((uint32_t)(uint16_t)packed[1] << 16);
-    } else {
-#pragma unroll
-      for (int h = 0; h < G; ++h) dst[h] = packed[h];
-    }
-  }
+    have = false;
   }
 }
 
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
-  dim3 grid((unsigned)a.tsplit, (unsigned)a.g, (unsigned)(a.B * a.Hkv));
-  launch_chain(k_table<G, DBAR>, grid, dim3(kTB), 0, s, a);
+  dim3 grid((unsigned)a.tsplit, (unsigned)(a.B * a.Hkv));
+  if (G == 4 && a.lut8)
+    launch_chain(k_table<G, DBAR, true>, grid, dim3(kTB), 0, s, a);
+  else
+    launch_chain(k_table<G, DBAR, false>, grid, dim3(kTB), 0, s, a);
   note_launch();
   return cudaGetLastError();
 }
