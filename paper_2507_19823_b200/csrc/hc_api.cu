@@ -543,15 +543,25 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
     if (e0 != cudaSuccess) return cuda_check(e0, "codebook absmax");
     a.cb_absmax = cba;
   }
-  {  // table parts per unit: about 4 resident CTAs per SM over all units (k_table streams
-     // its part of the unit's g * cpow2 entries; the scale prologue is per CTA)
+  {  // table grid: chunks of 2 units (each codebook row loaded once per chunk; measured
+     // 2 > 4 > 8 > 1 units at configs 2-4, profiles/r02_table_sweep.md), about 4 resident CTAs
+     // per SM, at least a full batch of rows per thread
     const int64_t units = B * H, E = g * Lw.cpow2;
-    int64_t ts = (4 * (int64_t)num_sms() + units - 1) / units;
-    ts = std::max<int64_t>(1, std::min<int64_t>(ts, E / 256));
+    int64_t tu = std::min<int64_t>({units, (int64_t)2, std::max<int64_t>(1, kTableQ / (d * G))});
+    const int64_t chunks = (units + tu - 1) / tu;
+    int64_t ts = (4 * (int64_t)num_sms() + chunks - 1) / chunks;
+    ts = std::max<int64_t>(1, std::min<int64_t>(ts, E / 1024));
     static int ts_env = -1;  // dev override (HC_TSPLIT)
     if (ts_env < 0) { const char *ev = getenv("HC_TSPLIT"); ts_env = ev ? atoi(ev) : 0; }
     if (ts_env > 0) ts = std::min<int64_t>(ts_env, std::max<int64_t>(1, E / 32));
+    static int tu_env = -1;  // dev override (HC_TUNITS)
+    if (tu_env < 0) { const char *ev = getenv("HC_TUNITS"); tu_env = ev ? atoi(ev) : 0; }
+    if (tu_env > 0 && tu_env <= std::min<int64_t>({units, (int64_t)kTableU, std::max<int64_t>(1, kTableQ / (d * G))})) {
+      tu = tu_env;
+      if (ts_env <= 0) ts = std::max<int64_t>(1, std::min<int64_t>((4 * (int64_t)num_sms() * tu + units - 1) / units, E / 1024));
+    }
     a.tsplit = (int)ts;
+    a.tunits = (int)tu;
   }
   a.z = (float *)(w8 + Lw.o_z);
   a.z_stride = Lw.z_stride;

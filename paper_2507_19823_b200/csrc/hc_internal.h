@@ -118,7 +118,8 @@ struct LayerArgs {
   HeadState *hs;          // [B*Hq]
   int16_t *T;             // [units][g][cpow2][G]
   const float *cb_absmax; // layer [cbg][dbar]: max_m |C[ci][m][e]| (R2 bound)
-  int tsplit;             // table CTAs per unit (k_table: contiguous parts of g * cpow2 entries)
+  int tsplit;             // k_table parts: contiguous ranges of the g * cpow2 entries
+  int tunits;             // k_table units per CTA (<= kTableU, tunits * d * G <= kTableQ)
   float *z;               // [B*Hq][z_stride]
   int64_t z_stride;
   // outputs
@@ -194,7 +195,9 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
 // rows a3-a4 (hc_select_pass.cu): rows of <= 64K candidates in one cluster kernel, longer rows
 // in three passes (force = 1: the passes for any length); nsplit > 1: z carries no folded max/min
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force = 0);
-constexpr int kSelChunk = 4096;  // tokens per chunk of the selection passes (16 KB of z)
+constexpr int kSelChunk = 4096;
+constexpr int kTableU = 8;     // k_table: units per CTA (max)
+constexpr int kTableQ = 8192;  // k_table: staged query floats per CTA (32 KiB)  // tokens per chunk of the selection passes (16 KB of z)
 inline int64_t select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChunk; }
 inline int64_t select_list_cap(int64_t n) { int64_t c = n / 16; return c < 4096 ? 4096 : c; }
 

@@ -499,10 +499,9 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   uint32_t *fml = reinterpret_cast<uint32_t *>(sm2 + kNB * 4);      // [kNB] fine mass, low word
   uint32_t *fmh = reinterpret_cast<uint32_t *>(sm2 + kNB * 8);      // [kNB] high word
   unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(sm2 + kNB * 4);  // resolve: over fml/fmh
-  uint32_t *wq = reinterpret_cast<uint32_t *>(sm2 + kNB * 12);      // [kST/32][64] per-warp Δ queues
-  float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12 + kST * 8);  // [kZB][kSelChunk]
+  float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12);          // [kZB][kSelChunk]
   unsigned long long *lq_all =                                          // [kST/32][64] per-warp list queues
-      reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kST * 8 + kZB * kSelChunk * 4);
+      reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kZB * kSelChunk * 4);
   __shared__ uint64_t zbar[kZB];
   __shared__ uint32_t zdone[kZB];
   __shared__ unsigned long long s_red[kST / 32];
@@ -1298,7 +1297,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, i
   const size_t smem1 = (size_t)kZB * kSelChunk * 4;
   launch_chain(k_sel_mass, g12, dim3(kST), smem1, st, s, per);
   note_launch();
-  const size_t smem2 = (size_t)kNB * 12 + (kST / 32) * 64 * 4 + (size_t)kZB * kSelChunk * 4 + (kST / 32) * 64 * 8;
+  const size_t smem2 = (size_t)kNB * 12 + (size_t)kZB * kSelChunk * 4 + (kST / 32) * 64 * 8;
   launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
   if (s.nch > kFinishInK2) {  // rows too long for K2's in-place finish

@@ -17,14 +17,16 @@ namespace hc {
 
 constexpr int kTB = 256;  // centroids per CTA
 
-// One pass (R2).  CTA = (unit, part): part p of the unit's g * cpow2 entries, flattened as
-// e = i * cpow2 + m, split into gridDim.x contiguous 32-aligned ranges so every SM holds a few
-// CTAs with a long stream of stores each.  The CTA stages the unit's G query heads in shared
-// memory as floats [i][e][h], issues its first batch of codebook loads, derives the heads'
-// scale from the bound A_h = max_i fmaf-chain(|q̄_i,e|, Cabs[ci][e]) (threads t < g each
-// evaluate one group's chain; block max -- the same value in every CTA of the unit), then
-// computes each entry t (the oracle's FMA chain) and stores the packed G x int16
-// clamp(rint(t * 2^e_h)).  Thread tid owns entries e0 + tid, e0 + tid + 256, ...
+// One pass (R2).  CTA = (part, unit chunk): part p of the g * cpow2 entries (flattened
+// e = i * cpow2 + m, contiguous 32-aligned ranges) for a chunk of up to 8 consecutive units
+// u = b * Hkv + kv.  A unit's entries depend on its own query but the codebook rows are
+// shared (C is [cbg][c][dbar], the same for every unit), so each codebook row is loaded once
+// per CTA and serves every unit of the chunk: the L2 latency of a batch of rows is covered by
+// units x rows entries of arithmetic.  The CTA stages its units' query heads in shared memory
+// as floats [unit][i][e][h], issues its first batch of rows, derives each head's scale from
+// the bound A_h = max_i fmaf-chain(|q̄_i,e|, Cabs[ci][e]) (one chain per (unit, group) per
+// thread, shared-memory max -- the same value in every CTA), then computes every entry t (the
+// oracle's FMA chain) and stores the packed G x int16 clamp(rint(t * 2^e_h)).
 // quant_t_d in the magic-number domain ("magic quantizer"): y = fmaf(t, 2^e, 1.5 * 2^23) is
 // 1.5 * 2^23 + rint(t * 2^e) (t * 2^e is exact, or below 2^-126 and rounds to 0 either way;
 // the magic is even, so ties still go to even), clamped to +-32767 around the magic; the low
@@ -75,23 +77,21 @@ __global__ void __launch_bounds__(kTB, DBAR <= 4 ? 4 : 2) k_table(LayerArgs a) {
     for (int64_t t = nw * cta / nct + threadIdx.x; t < nw * (cta + 1) / nct; t += blockDim.x)
       gh[t] = make_uint4(0u, 0u, 0u, 0u);
   }
-  const int u = blockIdx.y;
-  const int b = u / a.Hkv, kv = u - b * a.Hkv;
+  const int units = a.B * a.Hkv;
+  const int u0 = blockIdx.y * a.tunits, nu = min(a.tunits, units - u0);
   const int part = blockIdx.x, parts = gridDim.x;
   if (a.scan_split > 1 && a.n_q > 0) {  // the split scan accumulates into z: zero [0, n_q)
     const int64_t nz4 = (a.n_q + 3) / 4;  // float4s per row (rows are 64-float aligned)
-    for (int h = 0; h < G; ++h) {
-      float4 *zr = reinterpret_cast<float4 *>(a.z + ((int64_t)b * a.Hq + kv * G + h) * a.z_stride);
+    for (int r = 0; r < nu * G; ++r) {     // the chunk's rows b * Hq + kv * G + h = u * G + h
+      float4 *zr = reinterpret_cast<float4 *>(a.z + ((int64_t)u0 * G + r) * a.z_stride);
       for (int64_t q = (int64_t)part * blockDim.x + threadIdx.x; q < nz4; q += (int64_t)parts * blockDim.x)
         zr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  const int hq0 = kv * G;
   const int lg = 31 - __clz(a.cpow2);
   const int E = a.g << lg;  // <= 2^24 (g <= 256, cpow2 <= 2^16)
   const int e0 = (int)(((int64_t)E * part / parts) & ~(int64_t)31);
   const int e1 = part + 1 == parts ? E : (int)(((int64_t)E * (part + 1) / parts) & ~(int64_t)31);
-  int16_t *Tu = a.T + (int64_t)u * E * G;  // this unit's [g][cpow2][G] slice
   constexpr int NB = TBatch<DBAR>::n;
   // the CTA walks its groups i in [i_lo, i_hi]; in group i it owns centroids [mlo, mhi)
   const int i_lo = e0 >> lg, i_hi = e1 > e0 ? (e1 - 1) >> lg : i_lo - 1;
@@ -110,129 +110,123 @@ __global__ void __launch_bounds__(kTB, DBAR <= 4 ? 4 : 2) k_table(LayerArgs a) {
     mlo = max(e0 - gb, 0);
     mhi = min(e1 - gb, a.cpow2);
   };
-  {  // the first batch: in flight while the scale is derived
+  {  // the first batch: in flight while the scales are derived
     int mlo, mhi;
     group_range(i_lo, mlo, mhi);
     if (i_lo <= i_hi) load_batch(i_lo, mlo + (int)threadIdx.x, min(mhi, a.c));
   }
-  __shared__ __align__(16) float qsm[256 * G];  // [d][G] = [i][e][h], d <= 256
-  __shared__ float sA[G][kTB / 32];
-  for (int t = threadIdx.x; t < a.d * G; t += kTB) {
-    const int h = t % G, j = t / G;
-    qsm[t] = h2f(__ldg(a.q + ((int64_t)b * a.Hq + hq0 + h) * a.d + j));
+  // the chunk's query heads, [unit][d][G] floats (unit uu = u0 + uu: rows (u * G + h) of q)
+  __shared__ __align__(16) float qsm[kTableQ];
+  __shared__ int sA[kTableU][G];  // per-head bound A (non-negative floats order as ints)
+  const int dG = a.d * G;
+  for (int uu = 0; uu < nu; ++uu)  // consecutive threads write consecutive floats (no conflicts)
+    for (int t = threadIdx.x; t < dG; t += kTB)
+      qsm[uu * dG + t] = h2f(__ldg(a.q + ((int64_t)(u0 + uu) * G + t % G) * a.d + t / G));
+  if (threadIdx.x < kTableU * G) sA[threadIdx.x / G][threadIdx.x % G] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < nu * a.g; t += kTB) {  // one (unit, group) chain per thread
+    const int uu = t / a.g, gi = t - uu * a.g;
+    const float *ca = a.cb_absmax + (int64_t)(a.cbg == 1 ? 0 : gi) * DBAR;
+    const float *qg = qsm + uu * dG + gi * DBAR * G;
+    // lanes of the same unit reduce first (bounds are non-negative: they order as unsigned)
+    const unsigned grp = __match_any_sync(__activemask(), uu);
+    const bool lead = (threadIdx.x & 31) == __ffs(grp) - 1;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float bb = __fmul_rn(fabsf(qg[h]), __ldg(ca));
+#pragma unroll
+      for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(qg[e * G + h]), __ldg(ca + e), bb);
+      const unsigned mx = __reduce_max_sync(grp, __float_as_uint(bb));
+      if (lead) atomicMax(&sA[uu][h], (int)mx);
+    }
   }
   __syncthreads();
-  HeadState *hs = a.hs + (int64_t)b * a.Hq + hq0;
-  float sc[G];
-  {
-    float bnd[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) bnd[h] = 0.0f;
-    for (int gi = threadIdx.x; gi < a.g; gi += kTB) {
-      const float *ca = a.cb_absmax + (int64_t)(a.cbg == 1 ? 0 : gi) * DBAR;
-      const float *qg = qsm + gi * DBAR * G;
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        float bb = __fmul_rn(fabsf(qg[h]), __ldg(ca));
-#pragma unroll
-        for (int e = 1; e < DBAR; ++e) bb = __fmaf_rn(fabsf(qg[e * G + h]), __ldg(ca + e), bb);
-        bnd[h] = fmaxf(bnd[h], bb);
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float v = bnd[h];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-      if ((threadIdx.x & 31) == 0) sA[h][threadIdx.x >> 5] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float A = 0.0f;
-#pragma unroll
-      for (int w = 0; w < kTB / 32; ++w) A = fmaxf(A, sA[h][w]);
-      const int e = a.lut8 ? scale_exponent8(A) : scale_exponent(A);
-      sc[h] = pow2f(e);
-      if (part == 0 && threadIdx.x == 0) {
-        hs[h].e = e;
-        hs[h].kappa = __fmul_rn(a.kappa0, pow2f(-e));
-        hs[h].amax = __float_as_uint(A);
-        hs[h].M = INT_MIN;     // folded by the scan / resident epilogues (atomics)
-        hs[h].zmin = INT_MAX;
-        hs[h].S = 0ull;        // the selection's accumulators and counters (hc_select_pass.cu)
-        hs[h].mass_before = 0ull;
-        hs[h].c1_done = 0u;
-        hs[h].c2_done = 0u;
-        hs[h].ticket = 0u;
-        hs[h].state = 0u;
-      }
+  __shared__ float2 ssc[kTableU][G >= 2 ? G / 2 : 1];  // (2^e_2p, 2^e_2p+1) per unit
+  if (threadIdx.x < nu * G) {
+    const int uu = threadIdx.x / G, h = threadIdx.x % G;
+    const float A = __int_as_float(sA[uu][h]);
+    const int e = L8 ? scale_exponent8(A) : scale_exponent(A);
+    reinterpret_cast<float *>(&ssc[uu][0])[h] = pow2f(e);
+    if (part == 0) {
+      HeadState *hs = a.hs + (int64_t)(u0 + uu) * G + h;  // row b * Hq + kv * G + h
+      hs->e = e;
+      hs->kappa = __fmul_rn(a.kappa0, pow2f(-e));
+      hs->amax = __float_as_uint(A);
+      hs->M = INT_MIN;     // folded by the scan / resident epilogues (atomics)
+      hs->zmin = INT_MAX;
+      hs->S = 0ull;        // the selection's accumulators and counters (hc_select_pass.cu)
+      hs->mass_before = 0ull;
+      hs->c1_done = 0u;
+      hs->c2_done = 0u;
+      hs->ticket = 0u;
+      hs->state = 0u;
     }
   }
-  // heads in pairs for the packed fp32x2 FMA (every lane an IEEE fmaf, as the oracle's chain)
+  if (G == 1 && threadIdx.x < nu) ssc[threadIdx.x][0].y = 1.0f;
+  __syncthreads();
+  // heads in pairs for the packed fp32x2 FMA (every lane an IEEE fmaf, as the oracle's chain);
+  // the magic quantizer: even heads' magic carries the +32768 bias
   constexpr int NP = G >= 2 ? G / 2 : 1;
-  float2 sp[NP], mg[NP], lo[NP], hi[NP];
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    // the magic quantizer: even heads' magic carries the +32768 bias
-    const float me = G >= 2 ? 12582912.0f + 32768.0f : 12582912.0f;
-    sp[p] = make_float2(sc[2 * p], G >= 2 ? sc[2 * p + 1] : 1.0f);
-    mg[p] = make_float2(me, 12582912.0f);
-    lo[p] = make_float2(me - 32767.0f, 12582912.0f - 32767.0f);
-    hi[p] = make_float2(me + 32767.0f, 12582912.0f + 32767.0f);
-  }
+  constexpr float kMe = G >= 2 ? 12582912.0f + 32768.0f : 12582912.0f;
+  const float2 mg = make_float2(kMe, 12582912.0f);
   bool have = true;  // cmb holds the first batch of group i_lo
   for (int i = i_lo; i <= i_hi; ++i) {
     int mlo, mhi;
     group_range(i, mlo, mhi);
     const int mc = min(mhi, a.c);
-    float2 qp[NP][DBAR];  // (q_2p, q_2p+1) of group i, component k
-#pragma unroll
-    for (int k = 0; k < DBAR; ++k)
-#pragma unroll
-      for (int p = 0; p < NP; ++p)
-        qp[p][k] = G >= 2 ? make_float2(qsm[(i * DBAR + k) * G + 2 * p], qsm[(i * DBAR + k) * G + 2 * p + 1])
-                          : make_float2(qsm[(i * DBAR + k) * G], 0.0f);
-    int16_t *Tg = Tu + (int64_t)(i << lg) * G;
     for (int m = mlo + (int)threadIdx.x; m < mhi; m += kTB * NB) {
       if (!have) load_batch(i, m, mc);
       have = false;
+      for (int uu = 0; uu < nu; ++uu) {
+        float2 qp[NP][DBAR];  // (q_2p, q_2p+1) of unit uu, group i, component k
+        const float *qg = qsm + uu * dG + i * DBAR * G;
 #pragma unroll
-      for (int ub = 0; ub < NB; ++ub) {
-        const int mm = m + ub * kTB;
-        if (mm >= mhi) break;
-        float2 t[NP];  // the R2 FMA chain
+        for (int k = 0; k < DBAR; ++k)
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          t[p] = __fmul2_rn(qp[p][0], make_float2(cmb[ub][0], cmb[ub][0]));
+          for (int p = 0; p < NP; ++p)
+            qp[p][k] = G >= 2 ? make_float2(qg[k * G + 2 * p], qg[k * G + 2 * p + 1]) : make_float2(qg[k * G], 0.0f);
+        float2 sp[NP];
 #pragma unroll
-          for (int k = 1; k < DBAR; ++k) t[p] = __ffma2_rn(qp[p][k], make_float2(cmb[ub][k], cmb[ub][k]), t[p]);
-        }
-        if constexpr (G == 4 && L8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
-          const float th[4] = {t[0].x, t[0].y, t[NP - 1].x, t[NP - 1].y};
-          uint32_t wv = 0;
+        for (int p = 0; p < NP; ++p) sp[p] = ssc[uu][p];
+        const int64_t u = u0 + uu;
+        int16_t *Tg = a.T + ((int64_t)u * E + (i << lg)) * G;
 #pragma unroll
-          for (int h = 0; h < 4; ++h) wv |= (uint32_t)(quant_t8_d(th[h], sc[h]) + 128) << (8 * h);
-          reinterpret_cast<uint32_t *>(a.T)[(int64_t)u * E + (i << lg) + mm] = wv;
-          continue;
-        } else {
-        uint32_t w[NP];
+        for (int ub = 0; ub < NB; ++ub) {
+          const int mm = m + ub * kTB;
+          if (mm >= mhi) break;
+          float2 t[NP];  // the R2 FMA chain
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          float2 y = __ffma2_rn(t[p], sp[p], mg[p]);
-          y.x = fminf(fmaxf(y.x, lo[p].x), hi[p].x);
-          y.y = fminf(fmaxf(y.y, lo[p].y), hi[p].y);
-          w[p] = __byte_perm(__float_as_uint(y.x), __float_as_uint(y.y), 0x5410);
-        }
-        // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd
-        // head's signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
-        if constexpr (G == 4) {
-          *reinterpret_cast<uint2 *>(Tg + mm * 4) = make_uint2(w[0], w[NP - 1]);
-        } else if constexpr (G == 2) {
-          *reinterpret_cast<uint32_t *>(Tg + mm * 2) = w[0];
-        } else {
-          Tg[mm] = (int16_t)(uint16_t)w[0];
-        }
+          for (int p = 0; p < NP; ++p) {
+            t[p] = __fmul2_rn(qp[p][0], make_float2(cmb[ub][0], cmb[ub][0]));
+#pragma unroll
+            for (int k = 1; k < DBAR; ++k) t[p] = __ffma2_rn(qp[p][k], make_float2(cmb[ub][k], cmb[ub][k]), t[p]);
+          }
+          if constexpr (G == 4 && L8) {  // R2b: 4 x (int8 + 128) packed in one u32, head h at byte h
+            const float th[4] = {t[0].x, t[0].y, t[NP - 1].x, t[NP - 1].y};
+            const float sh[4] = {sp[0].x, sp[0].y, sp[NP - 1].x, sp[NP - 1].y};
+            uint32_t wv = 0;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) wv |= (uint32_t)(quant_t8_d(th[h], sh[h]) + 128) << (8 * h);
+            reinterpret_cast<uint32_t *>(a.T)[u * E + (i << lg) + mm] = wv;
+          } else {
+            uint32_t w[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+              float2 y = __ffma2_rn(t[p], sp[p], mg);
+              y.x = fminf(fmaxf(y.x, kMe - 32767.0f), kMe + 32767.0f);
+              y.y = fminf(fmaxf(y.y, 12582912.0f - 32767.0f), 12582912.0f + 32767.0f);
+              w[p] = __byte_perm(__float_as_uint(y.x), __float_as_uint(y.y), 0x5410);
+            }
+            // even heads are stored biased by +32768 (an unsigned 16-bit field under the odd
+            // head's signed one), so the scan adds a whole 32-bit word per head pair (hc_scan.cu Lut)
+            if constexpr (G == 4) {
+              *reinterpret_cast<uint2 *>(Tg + mm * 4) = make_uint2(w[0], w[NP - 1]);
+            } else if constexpr (G == 2) {
+              *reinterpret_cast<uint32_t *>(Tg + mm * 2) = w[0];
+            } else {
+              Tg[mm] = (int16_t)(uint16_t)w[0];
+            }
+          }
         }
       }
     }
@@ -242,7 +236,7 @@ __global__ void __launch_bounds__(kTB, DBAR <= 4 ? 4 : 2) k_table(LayerArgs a) {
 
 template <int G, int DBAR>
 static cudaError_t table_g_d(const LayerArgs &a, cudaStream_t s) {
-  dim3 grid((unsigned)a.tsplit, (unsigned)(a.B * a.Hkv));
+  dim3 grid((unsigned)a.tsplit, (unsigned)((a.B * a.Hkv + a.tunits - 1) / a.tunits));
   if (G == 4 && a.lut8)
     launch_chain(k_table<G, DBAR, true>, grid, dim3(kTB), 0, s, a);
   else
