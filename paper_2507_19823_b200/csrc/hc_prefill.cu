@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(kTThreads, 2) k_blockwise_attn_tc(PrefillArgs 
       *reinterpret_cast<uint4 *>(sQ + sw128_off(tid, cg)) = v;
     }
   }
+  fence_async_smem();  // generic smem writes -> visible to the tensor core (async proxy)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -3,22 +3,23 @@
 // P:240-252), as three bandwidth-shaped passes over the scores z instead of one cluster of
 // CTAs per row (the round-1 k_select_fused: 3-4 passes, 2-3 shared atomics per token).
 //
-//   K1 k_sel_mass    every token: W = mass(Δ), Δ = M - z (M folded by the scan epilogue)
-//                    -> the exact total S (u64 in registers, one global atomic per CTA) and a
-//                    COUNT-only coarse histogram of Δ >> shift (one shared atomic per token).
-//                    The row's last CTA bounds the prefix mass of every coarse bin from the
-//                    exact counts and W's monotonicity in Δ (W at the bin's two ends, widened
-//                    by a slack that covers the exp2 polynomial's rounding), and keeps the
-//                    range of bins the exact cut can fall in (plus the k_max cap's bin, from
-//                    exact counts).  shift == 0 (bins = exact Δ values) resolves right there.
-//   K2 k_sel_refine  the exact mass of every token above that range (P_above; W is
-//                    evaluated branch-free for every token -- cheaper than compacting the ~15 %
-//                    above the range), exact counts (and exact masses if the range spans
-//                    more than kNB values) of the tokens inside it, per K3-chunk counts of the
-//                    tokens above the range, and the in-range tokens themselves (index, Δ) on
-//                    a per-row list; the last CTA walks the fine bins to the exact Δ*, the
-//                    number r of Δ* ties kept (lowest indices), k_sel, k*, the kept mass -- or,
-//                    for a wide range, narrows it to one fine bin.
+//   K1 k_sel_mass    every token: Δ = M - z (M folded by the scan epilogue) -> a COUNT-only
+//                    coarse histogram of Δ >> shift (one shared atomic per token, no mass).
+//                    The row's last CTA bounds the mass of every coarse bin from the exact
+//                    counts and W's monotonicity in Δ (W at the bin's two ends, widened by a
+//                    slack that covers the exp2 polynomial's rounding) -- hence also the total
+//                    S in [S_lo, S_hi] and Θ in [Θ(S_lo), Θ(S_hi)] -- and keeps the range of
+//                    bins the exact cut can fall in for ANY Θ of that interval (plus the k_max
+//                    cap's bin, from exact counts).  (Keep-everything rows, τ >= 1 and
+//                    k_max >= n, need the exact S in K1 itself: only they sum W here.)
+//   K2 k_sel_refine  W of every token (branch-free): the exact total S and the exact mass of
+//                    every token above that range (P_above), exact counts (and exact masses
+//                    if the range spans more than kNB values) of the tokens inside it, per
+//                    K3-chunk counts of the tokens above the range, and the in-range tokens
+//                    themselves (index, Δ) on a per-row list; the last CTA forms the exact
+//                    Θ = ceil(τ_q S / 2^24), walks the fine bins to the exact Δ*, the number r
+//                    of Δ* ties kept (lowest indices), k_sel, k*, the kept mass -- or, for a
+//                    wide range, narrows it to one fine bin.
 //   K4 k_sel_prefix  one CTA per row: (if narrowed) the second refine from the in-range list;
 //                    then every chunk's (strict, tie) counts -- the count above the range plus
 //                    its in-range tokens classified against Δ* -- and their exclusive prefix.
@@ -323,12 +324,15 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
   if (t == 0)
     for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
+  const bool tau_all = s.tau_q >= (1u << 24);
+  const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
+  const bool need_S = tau_all && cap_all;  // keep-everything rows: no K2, S summed here
   unsigned long long S = 0;
   for (int64_t c = c0; c < c1; ++c) {
     const int slot = (int)((c - c0) % kZB);
     const float *zc = zs.wait(slot);
     const int nv = (int)min((int64_t)kSelChunk, s.n - c * kSelChunk);
-    auto body = [&](auto full) {
+    auto body = [&](auto full, auto sum) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int i0 = 4 * t + 2048 * u;
@@ -338,19 +342,23 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
         for (int e = 0; e < 4; ++e) {
           if (decltype(full)::value || i0 + e < nv) {
             const uint32_t dl = (uint32_t)(M - zint(vv[e]));
-            S += wmass(dl, kappa);
+            if constexpr (decltype(sum)::value) S += wmass(dl, kappa);
             atomicAdd(&hist[dl >> shift], 1u);
           }
         }
       }
     };
-    if (nv == kSelChunk) body(std::true_type{}); else body(std::false_type{});
+    if (need_S) body(std::false_type{}, std::true_type{});
+    else if (nv == kSelChunk) body(std::true_type{}, std::false_type{});
+    else body(std::false_type{}, std::false_type{});
     zs.release(c + kZB < c1 ? c + kZB : -1, slot);
   }
-  S = warp_sum_u64(S);
-  if ((t & 31) == 0) s_red[t >> 5] = S;
-  __syncthreads();
-  if (t == 0) {
+  if (need_S) {
+    S = warp_sum_u64(S);
+    if ((t & 31) == 0) s_red[t >> 5] = S;
+  }
+  __syncthreads();  // every token counted into hist (and s_red written)
+  if (need_S && t == 0) {
     unsigned long long tot = 0;
     for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
     if (tot) atomicAdd((unsigned long long *)&hs->S, tot);
@@ -369,22 +377,19 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // ---- the row's last CTA: exact counts, exact S, mass bounds per coarse bin
-  const unsigned long long Sx = __ldcg((const unsigned long long *)&hs->S);
+  // ---- the row's last CTA: exact counts, mass bounds per coarse bin
   const uint32_t dmax = (uint32_t)(M - zmin);
-  const bool tau_all = s.tau_q >= (1u << 24);
-  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
   const unsigned long long ntot = (unsigned long long)s.n;
-  const bool cap_all = (unsigned long long)s.k_max >= ntot;
   for (int i = t; i < kNB; i += kST) hist[i] = __ldcg(&gh[i]);
   if (t == 0) {
     hs->c1_done = 0u;
     hs->shift = shift;
-    hs->theta = theta;
     hs->ticket = 0u;
   }
   __syncthreads();
-  if (tau_all && cap_all) {  // everything is kept
+  if (need_S) {  // everything is kept
+    const unsigned long long Sx = __ldcg((const unsigned long long *)&hs->S);
+    if (t == 0) hs->theta = 0ull;
     for (int64_t c = t; c < s.nch; c += kST)  // chunk c: c*kSelChunk tokens before it, all strict
       s.pre[(int64_t)row * s.nch + c] = (unsigned long long)(c * kSelChunk) << 32;
     if (t == 0) {
@@ -434,6 +439,9 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   }
   if (t == 0) { s_ba = kNB; s_bb = -1; s_bcap = kNB; }
   bscan<3>(x, tot, sw);
+  // S in [tot[1], tot[2]] -> Θ in [th_lo, th_hi] (Θ is non-decreasing in S); K2 forms the exact one
+  const unsigned long long th_lo = tau_all ? 0ull : threshold(s.tau_q, tot[1]);
+  const unsigned long long th_hi = tau_all ? 0ull : threshold(s.tau_q, tot[2]);
   {
     unsigned long long C = x[0], Lm = x[1], Um = x[2];
     int ba = kNB, bb = -1, bcap = kNB;
@@ -444,8 +452,8 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
       unsigned long long lo, hi;
       bin(k, c, lo, hi);
       if (c) {
-        if (!tau_all && ba == kNB && Um + hi >= theta) ba = b;   // first bin the cut may end in
-        if (!tau_all && Lm < theta) bb = b;                       // last bin it may end in
+        if (!tau_all && ba == kNB && Um + hi >= th_lo) ba = b;   // first bin the cut may end in
+        if (!tau_all && Lm < th_hi) bb = b;                       // last bin it may end in
         if (!cap_all && bcap == kNB && C + c >= (unsigned long long)s.k_max) bcap = b;
       }
       C += c;
@@ -460,7 +468,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   int lo_b, hi_b;
   if (tau_all) {
     lo_b = hi_b = s_bcap;
-  } else if (s_bcap < s_ba) {  // the cap binds before the mass can reach Θ
+  } else if (s_bcap < s_ba) {  // the cap binds before the mass can reach any possible Θ
     lo_b = hi_b = s_bcap;
   } else {
     lo_b = s_ba;
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
       reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kZB * kSelChunk * 4);
   __shared__ uint64_t zbar[kZB];
   __shared__ uint32_t zdone[kZB];
-  __shared__ unsigned long long s_red[kST / 32];
+  __shared__ unsigned long long s_red[kST / 32], s_red2[kST / 32];
   __shared__ bool s_last;
   __shared__ int s_found;
   pdl_trigger();
@@ -526,6 +534,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   unsigned long long *lq = lq_all + warp * 64;
   int lqn = 0;                // warp-uniform list-queue length (flushed 32 entries per global atomic)
   unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
+  unsigned long long Sl = 0;  // exact mass of all this lane's tokens (-> S)
   unsigned long long *lst = s.list + (int64_t)row * s.cap;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t c = c0; c < c1; ++c) {
@@ -550,6 +559,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
         // (cheaper than compacting the ~15 % above the range: no ballots, no divergence)
         const unsigned long long w = wmass(dl, kappa);
         P += above ? w : 0ull;
+        Sl += valid ? w : 0ull;
         const unsigned mr = __ballot_sync(0xffffffffu, inr);
         if (mr) {  // in-range: fine histogram + the row's in-range list (via the warp's queue)
           if (inr) {
@@ -593,12 +603,14 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     if (lane < lqn && base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
   }
   P = warp_sum_u64(P);
-  if (lane == 0) s_red[warp] = P;
+  Sl = warp_sum_u64(Sl);
+  if (lane == 0) { s_red[warp] = P; s_red2[warp] = Sl; }
   __syncthreads();
   if (t == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
+    unsigned long long tot = 0, tS = 0;
+    for (int w = 0; w < kST / 32; ++w) { tot += s_red[w]; tS += s_red2[w]; }
     if (tot) atomicAdd((unsigned long long *)&hs->mass_before, tot);
+    if (tS) atomicAdd((unsigned long long *)&hs->S, tS);
   }
   uint32_t *gc = s.fcnt + (int64_t)row * kNB;
   unsigned long long *gm = s.fmass + (int64_t)row * kNB;
@@ -626,9 +638,11 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   }
   if (t == 0) hs->c2_done = 0u;
   __syncthreads();
-  const unsigned long long Sx = hs->S, theta = hs->theta;
   const bool tau_all = s.tau_q >= (1u << 24);
   const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
+  const unsigned long long Sx = __ldcg((const unsigned long long *)&hs->S);  // exact (every CTA's share)
+  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
+  if (t == 0) hs->theta = theta;  // read by the second refine (finish_row / K4)
   const unsigned long long cc0 = hs->cnt_before, cm0 = __ldcg((const unsigned long long *)&hs->mass_before);
   resolve_bins(fc, f > 0 ? s_mass : nullptr, f, lo, hi, cc0, cm0, s, hs, row, kappa, theta, tau_all,
                cap_all, Sx, &s_found);
