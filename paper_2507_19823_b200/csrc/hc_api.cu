@@ -162,7 +162,7 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
   // prefixes, the in-range token lists
   L.snch = select_chunks(ncand_max > 0 ? ncand_max : 1);
   L.scap = select_list_cap(ncand_max > 0 ? ncand_max : 1);
-  L.o_sgh = o; o += align256((size_t)rows * kNB * 4);
+  L.o_sgh = o; o += align256((size_t)rows * kNB * 12);  // ghist u32 then gmass u64
   L.o_sfc = o; o += align256((size_t)rows * kNB * 4);
   L.o_sfm = o; o += align256((size_t)rows * kNB * 8);
   L.o_scl = o; o += align256((size_t)rows * L.snch * 4);
@@ -649,6 +649,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   sa.tau_q = a.tau_q; sa.k_max = a.k_max; sa.renorm = a.renorm;
   sa.sel_idx = a.sel_idx; sa.sel_w = a.sel_w; sa.sel_k = sel_k;
   sa.ghist = (uint32_t *)((uint8_t *)ws + Lw.o_sgh);
+  sa.gmass = (unsigned long long *)(sa.ghist + rows * kNB);
   sa.fcnt = (uint32_t *)((uint8_t *)ws + Lw.o_sfc);
   sa.fmass = (unsigned long long *)((uint8_t *)ws + Lw.o_sfm);
   sa.cntlo = (uint32_t *)((uint8_t *)ws + Lw.o_scl);
@@ -854,7 +855,7 @@ size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {
   if (rows <= 0 || n <= 0) return 0;
   const int64_t zs = round_up(n, 64);
   return align256((size_t)rows * sizeof(HeadState)) + align256((size_t)rows * zs * 4) +
-         align256((size_t)rows * kNB * 4) * 2 + align256((size_t)rows * kNB * 8) +
+         align256((size_t)rows * kNB * 4) * 2 + align256((size_t)rows * kNB * 8) * 2 +
          align256((size_t)rows * select_chunks(n) * 4) + align256((size_t)rows * select_chunks(n) * 8) +
          align256((size_t)rows * select_list_cap(n) * 8);
 }
@@ -879,6 +880,7 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   float *z = (float *)(w8 + o); o += align256((size_t)rows * zs * 4);
   SelArgs sa{};
   sa.ghist = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
+  sa.gmass = (unsigned long long *)(w8 + o); o += align256((size_t)rows * kNB * 8);
   sa.fcnt = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
   sa.fmass = (unsigned long long *)(w8 + o); o += align256((size_t)rows * kNB * 8);
   sa.cntlo = (uint32_t *)(w8 + o); o += align256((size_t)rows * select_chunks(n) * 4);
@@ -888,7 +890,7 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   sa.cap = select_list_cap(n);
   cudaError_t e;
   const float kappa0 = (float)(1.4426950408889634 / sqrt((double)d));
-  if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s, sa.ghist)) != cudaSuccess)
+  if ((e = launch_select_float_prep(scores, rows, n, z, zs, hs, kappa0, s, sa.ghist, sa.gmass)) != cudaSuccess)
     return cuda_check(e, "prep");
   sa.hs = hs; sa.z = z; sa.z_stride = zs; sa.rows = (int)rows; sa.n = n;
   sa.tau_q = (uint32_t)rint((double)budget.tau * 16777216.0);

@@ -178,9 +178,10 @@ struct SelArgs {
   int32_t *sel_idx;       // [rows][k_max]
   float *sel_w;           // [rows][k_max]
   int64_t *sel_k;         // [rows] (may be null)
-  // hc_select_pass.cu state (workspace): coarse count histograms (zeroed before K1 by k_table
-  // / the float prep), refine histograms and look-back words (zeroed by K1)
-  uint32_t *ghist;             // [rows][kNB]
+  // hc_select_pass.cu state (workspace): coarse (count, mass) histograms (zeroed before K1 by
+  // k_table / the float prep), refine histograms and chunk counters (zeroed by K1)
+  uint32_t *ghist;             // [rows][kNB] coarse counts
+  unsigned long long *gmass;   // [rows][kNB] coarse exact masses (directly after ghist)
   uint32_t *fcnt;              // [rows][kNB]
   unsigned long long *fmass;   // [rows][kNB]
   uint32_t *cntlo;             // [rows][nch] per chunk: tokens above the refine range
@@ -239,6 +240,7 @@ cudaError_t launch_gather_rows(const LayerArgs &a, int64_t k_cap, float *part, u
 // standalone select (R5b): float scores -> fixed-point z, hs init (M, zmin, e, kappa)
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
                                      int64_t z_stride, HeadState *hs, float kappa0,
-                                     cudaStream_t s, uint32_t *ghist = nullptr);
+                                     cudaStream_t s, uint32_t *ghist = nullptr,
+                                     unsigned long long *gmass = nullptr);
 
 }  // namespace hc

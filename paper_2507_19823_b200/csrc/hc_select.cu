@@ -12,7 +12,8 @@ constexpr int kSelThreads = 256;
 // ---------------------------------------------------------------- standalone prep (R5b)
 __global__ void __launch_bounds__(kSelThreads) k_float_prep(const float *sc, int64_t n, float *z,
                                                              int64_t zs, HeadState *hs,
-                                                             float kappa0, uint32_t *ghist) {
+                                                             float kappa0, uint32_t *ghist,
+                                                             unsigned long long *gmass) {
   const int row = blockIdx.x;
   const float *src = sc + (int64_t)row * n;
   float A = 0.0f;
@@ -58,12 +59,15 @@ __global__ void __launch_bounds__(kSelThreads) k_float_prep(const float *sc, int
   }
   if (ghist)
     for (int i = threadIdx.x; i < kNB; i += kSelThreads) ghist[(int64_t)row * kNB + i] = 0u;
+  if (gmass)
+    for (int i = threadIdx.x; i < kNB; i += kSelThreads) gmass[(int64_t)row * kNB + i] = 0ull;
 }
 
 cudaError_t launch_select_float_prep(const float *scores, int64_t rows, int64_t n, float *z,
                                      int64_t z_stride, HeadState *hs, float kappa0,
-                                     cudaStream_t s, uint32_t *ghist) {
-  k_float_prep<<<(unsigned)rows, kSelThreads, 0, s>>>(scores, n, z, z_stride, hs, kappa0, ghist);
+                                     cudaStream_t s, uint32_t *ghist,
+                                     unsigned long long *gmass) {
+  k_float_prep<<<(unsigned)rows, kSelThreads, 0, s>>>(scores, n, z, z_stride, hs, kappa0, ghist, gmass);
   note_launch();
   return cudaGetLastError();
 }

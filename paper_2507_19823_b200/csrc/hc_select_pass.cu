@@ -295,10 +295,12 @@ constexpr int64_t kFinishInK2 = kZB * kSelChunk / 2;  // chunks whose counters f
 __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   extern __shared__ __align__(128) uint8_t sm1[];
   float *zbuf = reinterpret_cast<float *>(sm1);                                 // [kZB][kSelChunk]
+  uint32_t *mlo = reinterpret_cast<uint32_t *>(sm1 + kZB * kSelChunk * 4);      // [kNB] mass, low word
+  uint32_t *mhi = mlo + kNB;                                                    // [kNB] high word
+  unsigned long long *bmass = reinterpret_cast<unsigned long long *>(mlo);     // last CTA: [kNB] (overlay)
   __shared__ uint32_t hist[kNB];
   __shared__ uint64_t zbar[kZB];
   __shared__ uint32_t zdone[kZB];
-  __shared__ unsigned long long s_red[kST / 32];
   __shared__ bool s_last;
   pdl_trigger();
   pdl_wait();
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   const float kappa = hs->kappa;
   const int shift = sel_shift(M, zmin);
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
-  for (int i = t; i < kNB; i += kST) hist[i] = 0u;
+  for (int i = t; i < kNB; i += kST) { hist[i] = 0u; mlo[i] = 0u; mhi[i] = 0u; }
   {  // this CTA's share of the row's refine histograms and chunk counters (used by K2 / K4)
     const int64_t nf = (int64_t)kNB, nl = s.nch;
     const int64_t f0 = nf * blockIdx.x / gridDim.x, f1 = nf * (blockIdx.x + 1) / gridDim.x;
@@ -324,15 +326,11 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
   if (t == 0)
     for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
-  const bool tau_all = s.tau_q >= (1u << 24);
-  const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
-  const bool need_S = tau_all && cap_all;  // keep-everything rows: no K2, S summed here
-  unsigned long long S = 0;
   for (int64_t c = c0; c < c1; ++c) {
     const int slot = (int)((c - c0) % kZB);
     const float *zc = zs.wait(slot);
     const int nv = (int)min((int64_t)kSelChunk, s.n - c * kSelChunk);
-    auto body = [&](auto full, auto sum) {
+    auto body = [&](auto full) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int i0 = 4 * t + 2048 * u;
@@ -342,31 +340,30 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
         for (int e = 0; e < 4; ++e) {
           if (decltype(full)::value || i0 + e < nv) {
             const uint32_t dl = (uint32_t)(M - zint(vv[e]));
-            if constexpr (decltype(sum)::value) S += wmass(dl, kappa);
-            atomicAdd(&hist[dl >> shift], 1u);
+            const uint32_t b = dl >> shift;
+            const unsigned long long w = wmass(dl, kappa);
+            const uint32_t wl = (uint32_t)w;
+            uint32_t wh = (uint32_t)(w >> 32);
+            atomicAdd(&hist[b], 1u);
+            const uint32_t old = atomicAdd(&mlo[b], wl);  // exact u64 per bin: low word + carry
+            wh += (old + wl < old) ? 1u : 0u;
+            if (wh) atomicAdd(&mhi[b], wh);
           }
         }
       }
     };
-    if (need_S) body(std::false_type{}, std::true_type{});
-    else if (nv == kSelChunk) body(std::true_type{}, std::false_type{});
-    else body(std::false_type{}, std::false_type{});
+    if (nv == kSelChunk) body(std::true_type{}); else body(std::false_type{});
     zs.release(c + kZB < c1 ? c + kZB : -1, slot);
   }
-  if (need_S) {
-    S = warp_sum_u64(S);
-    if ((t & 31) == 0) s_red[t >> 5] = S;
-  }
-  __syncthreads();  // every token counted into hist (and s_red written)
-  if (need_S && t == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
-    if (tot) atomicAdd((unsigned long long *)&hs->S, tot);
-  }
+  __syncthreads();  // every token counted into hist / mlo / mhi
   uint32_t *gh = s.ghist + (int64_t)row * kNB;
+  unsigned long long *gm = s.gmass + (int64_t)row * kNB;
   for (int i = t; i < kNB; i += kST) {
     const uint32_t c = hist[i];
-    if (c) atomicAdd(&gh[i], c);
+    if (c) {
+      atomicAdd(&gh[i], c);
+      atomicAdd(&gm[i], ((unsigned long long)mhi[i] << 32) + mlo[i]);
+    }
   }
   __threadfence();
   __syncthreads();
@@ -377,22 +374,45 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // ---- the row's last CTA: exact counts, mass bounds per coarse bin
+  // ---- the row's last CTA: exact (count, mass) per coarse bin -> exact S, Θ and the one
+  // coarse bin the cut falls in (the first whose cumulative mass reaches Θ or cumulative
+  // count reaches k_max); K2 resolves it to the exact Δ* over its 2^shift values
   const uint32_t dmax = (uint32_t)(M - zmin);
   const unsigned long long ntot = (unsigned long long)s.n;
-  for (int i = t; i < kNB; i += kST) hist[i] = __ldcg(&gh[i]);
+  const bool tau_all = s.tau_q >= (1u << 24);
+  const bool cap_all = (unsigned long long)s.k_max >= ntot;
+  for (int i = t; i < kNB; i += kST) {
+    hist[i] = __ldcg(&gh[i]);
+    bmass[i] = __ldcg(&gm[i]);
+  }
   if (t == 0) {
     hs->c1_done = 0u;
     hs->shift = shift;
     hs->ticket = 0u;
   }
   __syncthreads();
-  if (need_S) {  // everything is kept
-    const unsigned long long Sx = __ldcg((const unsigned long long *)&hs->S);
-    if (t == 0) hs->theta = 0ull;
+  __shared__ unsigned long long sw[2][kST / 32];
+  __shared__ int s_found;
+  uint32_t c8[kBPT];
+  unsigned long long m8[kBPT], x[2] = {0, 0}, tot[2];
+#pragma unroll
+  for (int k = 0; k < kBPT; ++k) {
+    const uint32_t b = (uint32_t)(t * kBPT + k);
+    c8[k] = ((b << shift) <= dmax) ? hist[b] : 0u;
+    m8[k] = c8[k] ? bmass[b] : 0ull;
+    x[0] += c8[k];
+    x[1] += m8[k];
+  }
+  if (t == 0) s_found = kNB;
+  bscan<2>(x, tot, sw);
+  const unsigned long long Sx = tot[1];  // exact: every token's W in exactly one bin
+  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
+  if (tau_all && cap_all) {  // everything is kept
     for (int64_t c = t; c < s.nch; c += kST)  // chunk c: c*kSelChunk tokens before it, all strict
       s.pre[(int64_t)row * s.nch + c] = (unsigned long long)(c * kSelChunk) << 32;
     if (t == 0) {
+      hs->S = Sx;
+      hs->theta = 0ull;
       hs->delta_star = 0xffffffffu;
       hs->r_ties = 0u;
       hs->ksel = (int64_t)ntot;
@@ -404,94 +424,33 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
     }
     return;
   }
-  __shared__ unsigned long long sw[3][kST / 32];
-  __shared__ int s_ba, s_bb, s_bcap;
-  // per coarse bin b (Δ in [d0, d0 + 2^shift)): count c and mass bounds c*W_lo <= mass <=
-  // c*W_hi with W_hi = W(d0) and W_lo = W(next bin's d0) (<= W at the bin's last Δ).  W is
-  // non-increasing in Δ up to the polynomial's rounding (rel. 2^-22) and the truncation: the
-  // bounds are widened by 2^-20 relative + 2 so they hold for every Δ of the bin.  W at every
-  // bin start is computed once into shared memory (over the idle z buffers).
-  unsigned long long *wb = reinterpret_cast<unsigned long long *>(zbuf);  // [kNB + 1]
-  for (int b = t; b <= kNB; b += kST) {
-    const uint32_t d0 = (uint32_t)b << shift;
-    wb[b] = (b < kNB && hist[b]) || (b > 0 && hist[b - 1]) ? wmass(min(d0, dmax), kappa) : 0ull;
-  }
-  __syncthreads();
-  auto bin = [&](int k, uint32_t &c, unsigned long long &lo, unsigned long long &hi) {
-    const uint32_t b = (uint32_t)(t * kBPT + k);
-    c = ((b << shift) <= dmax) ? hist[b] : 0u;
-    lo = hi = 0ull;
-    if (c) {
-      const unsigned long long wh = wb[b], wl = wb[b + 1];
-      hi = c * (wh + (wh >> 20) + 2ull);
-      lo = c * (wl > (wl >> 20) + 2ull ? wl - (wl >> 20) - 2ull : 0ull);
-    }
-  };
-  unsigned long long x[3] = {0, 0, 0}, tot[3];
-#pragma unroll 1
+  unsigned long long cc = x[0], cm = x[1];
+  int found = kNB;
+  unsigned long long fcc = 0, fcm = 0;
+#pragma unroll
   for (int k = 0; k < kBPT; ++k) {
-    uint32_t c;
-    unsigned long long lo, hi;
-    bin(k, c, lo, hi);
-    x[0] += c;
-    x[1] += lo;
-    x[2] += hi;
+    const bool trig = c8[k] && ((!tau_all && cm + m8[k] >= theta) ||
+                                (!cap_all && cc + c8[k] >= (unsigned long long)s.k_max));
+    if (trig && found == kNB) { found = t * kBPT + k; fcc = cc; fcm = cm; }
+    cc += c8[k];
+    cm += m8[k];
   }
-  if (t == 0) { s_ba = kNB; s_bb = -1; s_bcap = kNB; }
-  bscan<3>(x, tot, sw);
-  // S in [tot[1], tot[2]] -> Θ in [th_lo, th_hi] (Θ is non-decreasing in S); K2 forms the exact one
-  const unsigned long long th_lo = tau_all ? 0ull : threshold(s.tau_q, tot[1]);
-  const unsigned long long th_hi = tau_all ? 0ull : threshold(s.tau_q, tot[2]);
-  {
-    unsigned long long C = x[0], Lm = x[1], Um = x[2];
-    int ba = kNB, bb = -1, bcap = kNB;
-#pragma unroll 1
-    for (int k = 0; k < kBPT; ++k) {
-      const int b = t * kBPT + k;
-      uint32_t c;
-      unsigned long long lo, hi;
-      bin(k, c, lo, hi);
-      if (c) {
-        if (!tau_all && ba == kNB && Um + hi >= th_lo) ba = b;   // first bin the cut may end in
-        if (!tau_all && Lm < th_hi) bb = b;                       // last bin it may end in
-        if (!cap_all && bcap == kNB && C + c >= (unsigned long long)s.k_max) bcap = b;
-      }
-      C += c;
-      Lm += lo;
-      Um += hi;
-    }
-    if (ba < kNB) atomicMin(&s_ba, ba);
-    if (bb >= 0) atomicMax(&s_bb, bb);
-    if (bcap < kNB) atomicMin(&s_bcap, bcap);
-  }
+  if (found < kNB) atomicMin(&s_found, found);
   __syncthreads();
-  int lo_b, hi_b;
-  if (tau_all) {
-    lo_b = hi_b = s_bcap;
-  } else if (s_bcap < s_ba) {  // the cap binds before the mass can reach any possible Θ
-    lo_b = hi_b = s_bcap;
-  } else {
-    lo_b = s_ba;
-    hi_b = s_bb < lo_b ? lo_b : s_bb;
-    if (s_bcap < hi_b) hi_b = s_bcap;
-  }
-  if (lo_b >= kNB) {  // cannot happen: Θ <= S and k_max < n are always reached
+  const int fb = s_found;
+  if (fb == kNB) {  // cannot happen: Θ <= S and k_max < n are always reached
     if (t == 0) hs->state = kStError;
     return;
   }
-  // the count before the range (exact): the owner of bin lo_b has it
-  if (lo_b / kBPT == t) {
-    unsigned long long C = x[0];
-    for (int k = 0; k < lo_b % kBPT; ++k) C += hist[t * kBPT + k];
-    const uint32_t rlo = (uint32_t)lo_b << shift;
-    const uint32_t rhi = min(((uint32_t)(hi_b + 1) << shift) - 1u, dmax);
-    int f = 0;
-    while (((rhi - rlo) >> f) >= (uint32_t)kNB) ++f;
-    hs->cnt_before = (uint32_t)C;
-    hs->mass_before = 0ull;  // K2's first pass accumulates the exact mass above the range
+  if (found == fb) {
+    const uint32_t rlo = (uint32_t)fb << shift;
+    hs->S = Sx;
+    hs->theta = theta;
+    hs->cnt_before = (uint32_t)fcc;
+    hs->mass_before = fcm;  // exact: the bins before the cut's
     hs->r_lo = rlo;
-    hs->r_hi = rhi;
-    hs->fshift = f;
+    hs->r_hi = min(rlo + ((1u << shift) - 1u), dmax);
+    hs->fshift = 0;         // 2^shift <= kNB: K2's fine bins are exact Δ values
     __threadfence();
     hs->state = kStRefine1;
   }
@@ -512,7 +471,6 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
       reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kZB * kSelChunk * 4);
   __shared__ uint64_t zbar[kZB];
   __shared__ uint32_t zdone[kZB];
-  __shared__ unsigned long long s_red[kST / 32], s_red2[kST / 32];
   __shared__ bool s_last;
   __shared__ int s_found;
   pdl_trigger();
@@ -533,8 +491,6 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
   unsigned long long *lq = lq_all + warp * 64;
   int lqn = 0;                // warp-uniform list-queue length (flushed 32 entries per global atomic)
-  unsigned long long P = 0;   // exact mass of this lane's share of the tokens above the range
-  unsigned long long Sl = 0;  // exact mass of all this lane's tokens (-> S)
   unsigned long long *lst = s.list + (int64_t)row * s.cap;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t c = c0; c < c1; ++c) {
@@ -555,11 +511,6 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
         const bool above = valid && dl < lo;
         const bool inr = valid && dl >= lo && dl <= hi;
         nlo += above ? 1u : 0u;
-        // the exact W of the tokens above the range: evaluated for every token, branch-free
-        // (cheaper than compacting the ~15 % above the range: no ballots, no divergence)
-        const unsigned long long w = wmass(dl, kappa);
-        P += above ? w : 0ull;
-        Sl += valid ? w : 0ull;
         const unsigned mr = __ballot_sync(0xffffffffu, inr);
         if (mr) {  // in-range: fine histogram + the row's in-range list (via the warp's queue)
           if (inr) {
@@ -602,16 +553,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (lane < lqn && base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
   }
-  P = warp_sum_u64(P);
-  Sl = warp_sum_u64(Sl);
-  if (lane == 0) { s_red[warp] = P; s_red2[warp] = Sl; }
-  __syncthreads();
-  if (t == 0) {
-    unsigned long long tot = 0, tS = 0;
-    for (int w = 0; w < kST / 32; ++w) { tot += s_red[w]; tS += s_red2[w]; }
-    if (tot) atomicAdd((unsigned long long *)&hs->mass_before, tot);
-    if (tS) atomicAdd((unsigned long long *)&hs->S, tS);
-  }
+  __syncthreads();  // every in-range token counted into fc / fml / fmh
   uint32_t *gc = s.fcnt + (int64_t)row * kNB;
   unsigned long long *gm = s.fmass + (int64_t)row * kNB;
   for (int i = t; i < kNB; i += kST) {
@@ -640,9 +582,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   __syncthreads();
   const bool tau_all = s.tau_q >= (1u << 24);
   const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
-  const unsigned long long Sx = __ldcg((const unsigned long long *)&hs->S);  // exact (every CTA's share)
-  const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
-  if (t == 0) hs->theta = theta;  // read by the second refine (finish_row / K4)
+  const unsigned long long Sx = hs->S, theta = hs->theta;  // exact (K1)
   const unsigned long long cc0 = hs->cnt_before, cm0 = __ldcg((const unsigned long long *)&hs->mass_before);
   resolve_bins(fc, f > 0 ? s_mass : nullptr, f, lo, hi, cc0, cm0, s, hs, row, kappa, theta, tau_all,
                cap_all, Sx, &s_found);
@@ -1308,7 +1248,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, i
     launch_chain(k_sel_minmax, g12, dim3(kST), 0, st, s, per);
     note_launch();
   }
-  const size_t smem1 = (size_t)kZB * kSelChunk * 4;
+  const size_t smem1 = (size_t)kZB * kSelChunk * 4 + (size_t)kNB * 8;
   launch_chain(k_sel_mass, g12, dim3(kST), smem1, st, s, per);
   note_launch();
   const size_t smem2 = (size_t)kNB * 12 + (size_t)kZB * kSelChunk * 4 + (kST / 32) * 64 * 8;

@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(kTB, DBAR <= 4 ? 4 : 2) k_table(LayerArgs a) {
     for (int t = threadIdx.x; t < a.gdone_n; t += blockDim.x) a.gdone[t] = 0u;
   if (a.skctr && cta == 1 % nct)
     for (int t = threadIdx.x; t < a.skctr_n; t += blockDim.x) a.skctr[t] = 0u;
-  if (a.sel_ghist) {  // the selection's coarse histograms: every CTA clears its slice
-    const int64_t nw = (int64_t)a.B * a.Hq * kNB / 4;  // uint4 words
+  if (a.sel_ghist) {  // the selection's coarse (count u32, mass u64) histograms: every CTA clears its slice
+    const int64_t nw = (int64_t)a.B * a.Hq * kNB * 3 / 4;  // uint4 words
     uint4 *gh = reinterpret_cast<uint4 *>(a.sel_ghist);
     for (int64_t t = nw * cta / nct + threadIdx.x; t < nw * (cta + 1) / nct; t += blockDim.x)
       gh[t] = make_uint4(0u, 0u, 0u, 0u);

@@ -51,6 +51,19 @@ def test_config4_full_size_sharded(R):
     torch.cuda.empty_cache()
 
 
+def test_config4_full_size_unsharded():
+    """BASELINE config 4 shape through hc_decode_attention on ONE GPU (the launch bench.py
+    --config 4 times: K1 count histogram, K2 exact S / refine, K3 write), sampled units."""
+    import torch
+    from harness import build_gpu, run_gpu_layer
+    case = _config4()
+    kc, vs, q = build_gpu(case)
+    gpu = run_gpu_layer(case, kc, vs, q, 0, with_debug=False)
+    _check(case, gpu, [(0, 0), (0, 5)], "c4")
+    del kc, vs, q
+    torch.cuda.empty_cache()
+
+
 def test_config5_one_layer_sharded_host_values():
     """BASELINE config 5: 4M-token context (2^22), g = 32, k_max = 524,288, values offloaded to
     host pinned memory, sequence-sharded R = 8 (here: 8 lock-step virtual shards on one GPU);
