@@ -869,13 +869,19 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   extern __shared__ __align__(16) uint8_t sm5[];
   uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm5);                         // [kSmTok]
   uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm5 + kSmTok * 4);           // [kSmTok]
-  unsigned long long *fm_s = reinterpret_cast<unsigned long long *>(sm5);    // [kNB] (over the staging)
+  uint32_t *mlo = reinterpret_cast<uint32_t *>(sm5 + kSmTok * 6);             // [kNB] mass, low word
+  uint32_t *mhi = mlo + kNB;                                                  // [kNB] high word
   __shared__ uint32_t hist[kNB];
   __shared__ unsigned long long sw[2][kST / 32];
-  __shared__ struct { int M, zmin; unsigned long long S, P; uint32_t ns, nt; } slot;
+  __shared__ struct {
+    int M, zmin;
+    unsigned long long tc, tm;  // my slice's exact count / mass
+    int cbin;                   // the cut's coarse bin (slice owner)
+    unsigned long long ccc, ccm;
+    uint32_t ns, nt;
+  } slot;
   __shared__ CutResult cr;
   __shared__ int s_red_i[2][kST / 32];
-  __shared__ unsigned long long s_red[kST / 32];
   cg::cluster_group cl = cg::this_cluster();
   pdl_trigger();
   pdl_wait();
@@ -900,14 +906,6 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   uint32_t vmask = 0;  // my valid tokens
 #pragma unroll
   for (int u = 0; u < 16; ++u) vmask |= (j0 + u < s.n ? 1u : 0u) << u;
-  // zero my slice of the row's fine histograms (ordered before any use by the cluster barriers)
-  {
-    const int per = kNB / cs;
-    for (int i = rank * per + t; i < (rank + 1) * per; i += kST) {
-      s.fcnt[(int64_t)row * kNB + i] = 0u;
-      s.fmass[(int64_t)row * kNB + i] = 0ull;
-    }
-  }
   // ---- M, zmin: folded by the scan epilogue, else a cluster reduction of my tokens' range
   int M, zmin;
   if (folded) {
@@ -941,34 +939,55 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   uint32_t dl[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) dl[u] = (vmask >> u & 1u) ? (uint32_t)(M - zint(zv[u])) : 0xffffffffu;
-  // ---- pass A: exact S, coarse counts -> the row's global histogram
-  for (int i = t; i < kNB; i += kST) hist[i] = 0u;
+  // ---- pass A: exact (count, mass) per coarse bin of my tokens (shared atomics, split words)
+  for (int i = t; i < kNB; i += kST) { hist[i] = 0u; mlo[i] = 0u; mhi[i] = 0u; }
   __syncthreads();
-  unsigned long long S = 0;
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     if (vmask >> u & 1u) {
-      S += wmass(dl[u], kappa);
-      atomicAdd(&hist[dl[u] >> shift], 1u);
+      const uint32_t bb = dl[u] >> shift;
+      const unsigned long long w = wmass(dl[u], kappa);
+      const uint32_t wl = (uint32_t)w;
+      uint32_t wh = (uint32_t)(w >> 32);
+      atomicAdd(&hist[bb], 1u);
+      const uint32_t old = atomicAdd(&mlo[bb], wl);
+      wh += (old + wl < old) ? 1u : 0u;
+      if (wh) atomicAdd(&mhi[bb], wh);
     }
   }
-  S = warp_sum_u64(S);
-  if (lane == 0) s_red[warp] = S;
-  __syncthreads();
-  if (t == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
-    slot.S = tot;
-  }
-  uint32_t *gh = s.ghist + (int64_t)row * kNB;
-  for (int i = t; i < kNB; i += kST) {
-    const uint32_t c = hist[i];
-    if (c) atomicAdd(&gh[i], c);
-  }
-  __threadfence();
   cl.sync();
+  // ---- my slice of the bins, summed over the cluster (DSMEM), and its totals
+  const int nbs = kNB / cs, b0 = rank * nbs, b1 = rank + 1 == cs ? kNB : b0 + nbs;
+  uint32_t *red_c = reinterpret_cast<uint32_t *>(sm5);                          // [kNB] over the staging
+  unsigned long long *red_m = reinterpret_cast<unsigned long long *>(sm5 + kNB * 4);  // [kNB]
+  {
+    unsigned long long tc = 0, tm = 0;
+    for (int i = b0 + t; i < b1; i += kST) {
+      uint32_t c = 0;
+      unsigned long long m = 0;
+      for (int rr = 0; rr < cs; ++rr) {
+        c += cl.map_shared_rank(hist, rr)[i];
+        m += ((unsigned long long)cl.map_shared_rank(mhi, rr)[i] << 32) + cl.map_shared_rank(mlo, rr)[i];
+      }
+      red_c[i - b0] = c;
+      red_m[i - b0] = m;
+      tc += c;
+      tm += m;
+    }
+    tc = warp_sum_u64(tc);
+    tm = warp_sum_u64(tm);
+    if (lane == 0) { sw[0][warp] = tc; sw[1][warp] = tm; }
+    __syncthreads();
+    if (t == 0) {
+      unsigned long long a0 = 0, a1 = 0;
+      for (int w = 0; w < kST / 32; ++w) { a0 += sw[0][w]; a1 += sw[1][w]; }
+      slot.tc = a0;
+      slot.tm = a1;
+    }
+  }
+  cl.sync();  // slice totals published; every peer is done reading my hist / mlo / mhi
   unsigned long long Sx = 0;
-  for (int r = 0; r < cs; ++r) Sx += cl.map_shared_rank(&slot, r)->S;
+  for (int rr = 0; rr < cs; ++rr) Sx += cl.map_shared_rank(&slot, rr)->tm;  // exact
   const bool tau_all = s.tau_q >= (1u << 24);
   const unsigned long long theta = tau_all ? 0ull : threshold(s.tau_q, Sx);
   const unsigned long long ntot = (unsigned long long)s.n;
@@ -977,139 +996,66 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   unsigned long long r = 0, ksel = ntot, selmass = Sx;
   long long kstar = (long long)ntot;
   if (!(tau_all && cap_all)) {
-    // ---- the bound (every CTA, same inputs): candidate coarse bins of the cut
-    for (int i = t; i < kNB; i += kST) hist[i] = __ldcg(&gh[i]);
-    __syncthreads();
-    unsigned long long *wb = reinterpret_cast<unsigned long long *>(sm5);  // [kNB + 1] over the staging
-    for (int b = t; b <= kNB; b += kST) {
-      const uint32_t d0 = (uint32_t)b << shift;
-      wb[b] = (b < kNB && hist[b]) || (b > 0 && hist[b - 1]) ? wmass(min(d0, dmax), kappa) : 0ull;
-    }
-    __syncthreads();
-    __shared__ int s_ba, s_bb, s_bcap;
-    __shared__ unsigned long long s_cb;
-    if (t == 0) { s_ba = kNB; s_bb = -1; s_bcap = kNB; }
-    unsigned long long x[3] = {0, 0, 0}, tot3[3];
-    unsigned long long c8[kBPT];
-#pragma unroll
-    for (int k = 0; k < kBPT; ++k) {
-      const uint32_t b = (uint32_t)(t * kBPT + k);
-      c8[k] = ((b << shift) <= dmax) ? hist[b] : 0u;
-      if (c8[k]) {
-        const unsigned long long wh = wb[b], wl = wb[b + 1];
-        x[0] += c8[k];
-        x[1] += c8[k] * (wl > (wl >> 20) + 2ull ? wl - (wl >> 20) - 2ull : 0ull);
-        x[2] += c8[k] * (wh + (wh >> 20) + 2ull);
+    // the slice the cut falls in (every CTA, same totals): first whose cumulative mass reaches Θ
+    // or cumulative count reaches k_max
+    int sc = cs;
+    unsigned long long cc0 = 0, cm0 = 0;
+    for (int rr = 0; rr < cs; ++rr) {
+      const auto *o = cl.map_shared_rank(&slot, rr);
+      if ((!tau_all && cm0 + o->tm >= theta) || (!cap_all && cc0 + o->tc >= (unsigned long long)s.k_max)) {
+        sc = rr;
+        break;
       }
+      cc0 += o->tc;
+      cm0 += o->tm;
     }
-    __shared__ unsigned long long sw3[3][kST / 32];
-    bscan<3>(x, tot3, sw3);
-    {
-      unsigned long long C = x[0], Lm = x[1], Um = x[2];
-      int ba = kNB, bb = -1, bcap = kNB;
-#pragma unroll
-      for (int k = 0; k < kBPT; ++k) {
-        const int b = t * kBPT + k;
-        unsigned long long lo = 0, hi = 0;
-        if (c8[k]) {
-          const unsigned long long wh = wb[b], wl = wb[b + 1];
-          hi = c8[k] * (wh + (wh >> 20) + 2ull);
-          lo = c8[k] * (wl > (wl >> 20) + 2ull ? wl - (wl >> 20) - 2ull : 0ull);
-          if (!tau_all && ba == kNB && Um + hi >= theta) ba = b;
-          if (!tau_all && Lm < theta) bb = b;
-          if (!cap_all && bcap == kNB && C + c8[k] >= (unsigned long long)s.k_max) bcap = b;
-        }
-        C += c8[k];
-        Lm += lo;
-        Um += hi;
-      }
-      if (ba < kNB) atomicMin(&s_ba, ba);
-      if (bb >= 0) atomicMax(&s_bb, bb);
-      if (bcap < kNB) atomicMin(&s_bcap, bcap);
-    }
-    __syncthreads();
-    int lo_b, hi_b;
-    if (tau_all || s_bcap < s_ba) {
-      lo_b = hi_b = s_bcap;
-    } else {
-      lo_b = s_ba;
-      hi_b = s_bb < lo_b ? lo_b : s_bb;
-      if (s_bcap < hi_b) hi_b = s_bcap;
-    }
-    if (lo_b / kBPT == t) {
-      unsigned long long C = x[0];
-      for (int k = 0; k < lo_b % kBPT; ++k) C += c8[k];
-      s_cb = C;
-    }
-    __syncthreads();
-    const uint32_t rlo = (uint32_t)lo_b << shift;
-    const uint32_t rhi = min(((uint32_t)(hi_b + 1) << shift) - 1u, dmax);
-    int f = 0;
-    while (((rhi - rlo) >> f) >= (uint32_t)kNB) ++f;
-    // ---- pass B: exact mass above the range, exact fine counts (+ masses) in it
-    unsigned long long P = 0;
-    uint32_t *gc = s.fcnt + (int64_t)row * kNB;
-    unsigned long long *gm = s.fmass + (int64_t)row * kNB;
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      if (vmask >> u & 1u) {
-        if (dl[u] < rlo) {
-          P += wmass(dl[u], kappa);
-        } else if (dl[u] <= rhi) {
-          const uint32_t fb = (dl[u] - rlo) >> f;
-          atomicAdd(&gc[fb], 1u);
-          if (f > 0) atomicAdd(&gm[fb], (unsigned long long)wmass(dl[u], kappa));
-        }
-      }
-    }
-    P = warp_sum_u64(P);
-    if (lane == 0) s_red[warp] = P;
-    __syncthreads();
-    if (t == 0) {
-      unsigned long long tot = 0;
-      for (int w = 0; w < kST / 32; ++w) tot += s_red[w];
-      slot.P = tot;
-    }
-    __threadfence();
-    cl.sync();
-    unsigned long long Px = 0;
-    for (int rr = 0; rr < cs; ++rr) Px += cl.map_shared_rank(&slot, rr)->P;
-    for (int i = t; i < kNB; i += kST) {
-      hist[i] = __ldcg(&gc[i]);
-      if (f > 0) fm_s[i] = __ldcg(&gm[i]);
-    }
-    __syncthreads();
-    find_cut(hist, f > 0 ? fm_s : nullptr, f, rlo, rhi, s_cb, Px, kappa, theta, tau_all, cap_all, s.k_max,
-             &cr, sw);
-    uint32_t base = rlo;
-    int bin = cr.bin;
-    if (f > 0 && bin < kNB) {  // narrow to the fine bin: exact per-Δ counts from my registers, summed over DSMEM
-      base = rlo + ((uint32_t)bin << f);
-      const uint32_t top2 = min(base + ((1u << f) - 1u), rhi);
-      const unsigned long long cc1 = cr.cc, cm1 = cr.cm;
-      __syncthreads();
-      for (int i = t; i < kNB; i += kST) hist[i] = 0u;
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if ((vmask >> u & 1u) && dl[u] >= base && dl[u] <= top2) atomicAdd(&hist[dl[u] - base], 1u);
-      cl.sync();
-      uint32_t *sum = reinterpret_cast<uint32_t *>(sm5 + kNB * 8);  // [kNB] over the staging
-      for (int i = t; i < kNB; i += kST) {
-        uint32_t c = 0;
-        for (int rr = 0; rr < cs; ++rr) c += cl.map_shared_rank(hist, rr)[i];
-        sum[i] = c;
-      }
-      cl.sync();  // peers done reading my hist
-      find_cut(sum, nullptr, 0, base, top2, cc1, cm1, kappa, theta, tau_all, cap_all, s.k_max, &cr, sw);
-      bin = cr.bin;
-    }
-    if (bin >= kNB) {  // cannot happen (the bounds hold): leave the row's state as an error
+    if (sc == cs) {  // cannot happen: Θ <= S and k_max < n are always reached
       if (rank == 0 && t == 0) hs->state = kStError;
       cl.sync();
       return;
     }
-    dstar = base + (uint32_t)bin;  // f == 0 here
+    if (rank == sc) {  // the owner walks its slice's exact bins to the cut bin
+      const int nb = (rank + 1 == cs ? kNB : b0 + nbs) - b0;
+      for (int i = nb + t; i < kNB; i += kST) { red_c[i] = 0u; red_m[i] = 0ull; }
+      __syncthreads();
+      find_cut(red_c, red_m, shift, (uint32_t)b0 << shift, dmax, cc0, cm0, kappa, theta, tau_all, cap_all,
+               s.k_max, &cr, sw);
+      if (t == 0) { slot.cbin = cr.bin; slot.ccc = cr.cc; slot.ccm = cr.cm; }
+    }
+    cl.sync();
+    const auto *oc = cl.map_shared_rank(&slot, sc);
+    const int cbin = oc->cbin;
+    const unsigned long long cc1 = oc->ccc, cm1 = oc->ccm;
+    if (cbin >= kNB) {
+      if (rank == 0 && t == 0) hs->state = kStError;
+      cl.sync();
+      return;
+    }
+    // ---- pass B: exact per-Δ counts over the cut bin's 2^shift values, summed over DSMEM
+    const uint32_t base = (uint32_t)(sc * nbs + cbin) << shift;  // the cut bin (global index)
+    const uint32_t top2 = min(base + ((1u << shift) - 1u), dmax);
+    for (int i = t; i < kNB; i += kST) hist[i] = 0u;  // (peers finished reading it before the last syncs)
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if ((vmask >> u & 1u) && dl[u] >= base && dl[u] <= top2) atomicAdd(&hist[dl[u] - base], 1u);
+    cl.sync();
+    uint32_t *sum = red_c;  // [kNB] (the slice sums are no longer needed)
+    for (int i = t; i < kNB; i += kST) {
+      uint32_t c = 0;
+      if (base + (uint32_t)i <= top2)
+        for (int rr = 0; rr < cs; ++rr) c += cl.map_shared_rank(hist, rr)[i];
+      sum[i] = c;
+    }
+    __syncthreads();
+    find_cut(sum, nullptr, 0, base, top2, cc1, cm1, kappa, theta, tau_all, cap_all, s.k_max, &cr, sw);
+    const int bin = cr.bin;
+    if (bin >= kNB) {
+      if (rank == 0 && t == 0) hs->state = kStError;
+      cl.sync();
+      return;
+    }
+    dstar = base + (uint32_t)bin;
     const unsigned long long w = wmass(dstar, kappa);
     unsigned long long r_tau = ~0ull, r_cap = ~0ull;
     if (!tau_all && cr.cm + cr.m >= theta) r_tau = cr.cm >= theta ? 1ull : (theta - cr.cm + w - 1) / w;
@@ -1202,13 +1148,13 @@ cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(k_sel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTok * 6);
+    cudaFuncSetAttribute(k_sel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTok * 6 + kNB * 8);
     configured[dev] = 1;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(s.rows * cs));
   cfg.blockDim = dim3(kST);
-  cfg.dynamicSmemBytes = (size_t)kSmTok * 6;
+  cfg.dynamicSmemBytes = (size_t)kSmTok * 6 + (size_t)kNB * 8;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
