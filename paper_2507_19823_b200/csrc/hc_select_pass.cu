@@ -272,6 +272,8 @@ __device__ void resolve_bins(const uint32_t *cnt, const unsigned long long *mass
 // ---------------------------------------------------------------------------- K0 (split scans)
 // group-split scans accumulate z with atomics and fold no max / min: one pass for them
 __global__ void __launch_bounds__(kST) k_sel_minmax(SelArgs s, int64_t per) {
+  pdl_trigger();
+  pdl_wait();  // z is the scan's output
   const int row = blockIdx.y;
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
   int mx = INT_MIN, mn = INT_MAX;
