@@ -134,7 +134,7 @@ struct Layout {
   int64_t z_stride;
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
-      o_rdone, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, o_sgh, o_sfc, o_sfm,
+      o_rdone, o_wpart, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, o_sgh, o_sfc, o_sfm,
       o_scl, o_spre, o_slist, total;
   int64_t snch, scap;
   int skctr_n;
@@ -181,6 +181,8 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
     const int64_t nchr = gather_rows_chunks(L.k_eff);
     L.o_rpart = o; o += align256((size_t)rows * nchr * 128 * 4);
     L.o_rdone = o; o += align256((size_t)rows * 4);
+    // K3 fused with Eq. 5 (k_sel_write_gather): one partial per (row, contributor CTA)
+    L.o_wpart = o; o += align256((size_t)rows * (select_chunks(ncand_max > 0 ? ncand_max : 1) + 1) * 128 * 4);
     L.o_grange = o; o += align256((size_t)rows * 16);  // sharded finish: list slice per row
     // stream-K scan (16-bit table): 2 partial tiles (8192 tokens x G int32) per CTA, one
     // counter per (tile, warp)
@@ -624,7 +626,7 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   const bool shared = budget.shared_kv != 0;
   const bool union_gather = !budget.select_only && (want_union || shared) && a.G > 1;
   const bool want_rows = gather_mode == 3 || (gather_mode == 2 && a.v_placement == 0);
-  const bool rows_gather = !budget.select_only && !union_gather && (want_rows || shared) && a.d == 128;
+  bool rows_gather = !budget.select_only && !union_gather && (want_rows || shared) && a.d == 128;
   if (shared && !budget.select_only && !union_gather && !rows_gather)
     return fail(HC_ERR_UNSUPPORTED, "shared_kv with G = 1 needs d = 128");
   // the gather's completion counters are zeroed by k_table (no memset between chain kernels)
@@ -674,8 +676,17 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
     if ((e = launch_select_fused(sa, a, n_q > 0 ? a.scan_split : 1, fused_gather ? 1 : 0, a.num_sms, s)) !=
         cudaSuccess)
       return cuda_check(e, "select");
-  } else if ((e = launch_select(sa, n_q > 0 ? a.scan_split : 1, a.num_sms, s, sel_force)) != cudaSuccess) {
-    return cuda_check(e, "select");
+  } else {
+    // HBM values, per-head rows gather: the long-row passes fuse Eq. 5 into their K3
+    // (k_sel_write_gather) unless HC_K3G=0
+    static int k3g_env = -1;
+    if (k3g_env < 0) { const char *ev = getenv("HC_K3G"); k3g_env = (ev && !strcmp(ev, "0")) ? 0 : 1; }
+    SelGather wg{&a, (float *)((uint8_t *)ws + Lw.o_wpart), (uint32_t *)((uint8_t *)ws + Lw.o_rdone), 0};
+    const bool try_wg = k3g_env && rows_gather && a.d == 128 && !a.g_cnt;
+    if ((e = launch_select(sa, n_q > 0 ? a.scan_split : 1, a.num_sms, s, sel_force, try_wg ? &wg : nullptr)) !=
+        cudaSuccess)
+      return cuda_check(e, "select");
+    if (wg.used) rows_gather = false;  // Eq. 5 done inside K3
   }
   if (rows_gather) {
     uint32_t *done = (uint32_t *)((uint8_t *)ws + Lw.o_rdone);

@@ -188,6 +188,15 @@ HC_HD uint64_t threshold(uint32_t tau_q, uint64_t S) {
   return (hi << 40) | (lo2 >> 24);
 }
 
+// 16-B read-only load that bypasses L1 (value rows: read once per head group)
+__device__ __forceinline__ uint4 ldg_nc16(const uint16_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // ---- mbarrier + bulk-copy (TMA engine) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -19,14 +19,6 @@ constexpr int kGC = 2048;     // tokens per chunk
 constexpr int kGT = 256;      // threads
 constexpr int kGUn = 4;       // rows in flight per half-warp
 
-__device__ __forceinline__ uint4 ldg_nc16(const uint16_t *p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t n, int64_t x) {
   int64_t lo = 0, hi = n;
   while (lo < hi) {

@@ -195,7 +195,13 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
                                 int num_sms, cudaStream_t st);
 // rows a3-a4 (hc_select_pass.cu): rows of <= 64K candidates in one cluster kernel, longer rows
 // in three passes (force = 1: the passes for any length); nsplit > 1: z carries no folded max/min
-cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force = 0);
+// wg: K3 fused with Eq. 5 over HBM values (k_sel_write_gather) when non-null: wg->out gets the
+// output, wpart [rows][select_wg_maxc][128] / wdone [rows] (zeroed) are its partials / counters
+struct SelGather { const LayerArgs *a; float *wpart; uint32_t *wdone; int used; };  // used: set when K3G ran
+cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force = 0,
+                          const SelGather *wg = nullptr);
+// contributor slots per row of k_sel_write_gather (CTAs over contiguous ranges of `per` items)
+inline int select_wg_maxc(int64_t nch, int64_t per) { return (int)((nch + per - 1) / per + 1); }
 constexpr int kSelChunk = 4096;
 constexpr int kTableU = 8;     // k_table: units per CTA (max)
 constexpr int kTableQ = 8192;  // k_table: staged query floats per CTA (32 KiB)  // tokens per chunk of the selection passes (16 KB of z)

@@ -815,6 +815,256 @@ __global__ void __launch_bounds__(kWT, 4) k_sel_write(SelArgs s) {
   }
 }
 
+// K3 + Eq. 5 for values in HBM (d = 128): "K3G".  Persistent CTAs over CONTIGUOUS ranges of
+// the (row, chunk) items (row-major), 3 per SM: each item is compacted exactly as in K3 (the
+// (index, W/S) lists are still written), then its kept value rows are gathered right away --
+// half-warp per row, 8 rows (16-B loads) in flight per half-warp -- into fp32 accumulators
+// that persist across the CTA's consecutive items of the same row.  When the row changes the
+// CTA writes one partial (its contributor slot) and the row's last contributor adds the
+// partials in CTA order (deterministic).  Concurrent CTAs sit at the same relative chunk of
+// neighbouring rows, so the G heads of a KV head read the same token range at about the same
+// time and shared kept rows hit in L2.  Replaces K3 + k_gather_rows (one pass over the kept
+// rows overlapping the compaction's z stream).
+constexpr int kGU = 8;  // value rows in flight per half-warp
+
+__global__ void __launch_bounds__(kWT, 3) k_sel_write_gather(SelArgs s, LayerArgs a, float *wpart,
+                                                              uint32_t *wdone, int64_t per, int maxc) {
+  extern __shared__ __align__(128) uint8_t sm3[];
+  float *zbuf = reinterpret_cast<float *>(sm3);                                        // [2][kSelChunk]
+  uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3 + 2 * kSelChunk * 4);            // [kSelChunk]
+  float *stg_w = reinterpret_cast<float *>(stg_d);                                    // (weights, in place)
+  uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm3 + 3 * kSelChunk * 4);            // [kSelChunk]
+  float *red = reinterpret_cast<float *>(sm3 + 3 * kSelChunk * 4 + kSelChunk * 2);    // [16][128]
+  __shared__ uint64_t zbar[2];
+  __shared__ uint32_t sw[kWT / 32];
+  __shared__ bool s_last;
+  pdl_trigger();
+  pdl_wait();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int hw = t >> 4, sub = t & 15;  // half-warp, its 8-dim slice
+  const int64_t items = (int64_t)s.rows * s.nch;
+  const int64_t it0 = (int64_t)blockIdx.x * per, it1 = min(items, it0 + per);
+  if (it0 >= it1) return;
+  if (t == 0) {
+    mbar_init(&zbar[0], 1);
+    mbar_init(&zbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto request = [&](int64_t it, int slot) {  // thread 0: the item's z chunk -> buffer `slot`
+    const int64_t row = it / s.nch, c = it - row * s.nch;
+    const int64_t j0 = c * kSelChunk;
+    const int64_t cnt = min((int64_t)kSelChunk, s.n - j0);
+    const uint32_t bytes = (uint32_t)((cnt * 4 + 15) & ~(int64_t)15);
+    mbar_expect_tx(&zbar[slot], bytes);
+    bulk_g2s(zbuf + (size_t)slot * kSelChunk, s.z + row * s.z_stride + j0, bytes, &zbar[slot]);
+  };
+  if (t == 0) {
+    request(it0, 0);
+    if (it0 + 1 < it1) request(it0 + 1, 1);
+  }
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+  // the row's partial -> my contributor slot; the row's last contributor sums them in order
+  auto flush = [&](int row) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[hw * 128 + sub * 8 + e] = acc[e];
+    __syncthreads();
+    const int64_t first = ((int64_t)row * s.nch) / per;
+    const int64_t lastc = ((int64_t)(row + 1) * s.nch - 1) / per;
+    const int cnt = (int)(lastc - first + 1), me = (int)(blockIdx.x - first);
+    if (t < 128) {
+      float v = 0.0f;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v += red[q * 128 + t];
+      wpart[((int64_t)row * maxc + me) * 128 + t] = v;
+      __threadfence();
+    }
+    __syncthreads();
+    if (t == 0) {
+      const uint32_t prev = atomicAdd(&wdone[row], 1u);
+      s_last = prev == (uint32_t)cnt - 1u;
+      if (s_last) wdone[row] = 0u;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if (t < 128) {
+        const float *p0 = wpart + (int64_t)row * maxc * 128 + t;
+        float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        int c = 0;
+        for (; c + 3 < cnt; c += 4) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s4[q] += __ldcg(p0 + (int64_t)(c + q) * 128);
+        }
+        for (; c < cnt; ++c) s4[0] += __ldcg(p0 + (int64_t)c * 128);
+        a.out[(int64_t)row * 128 + t] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+  };
+  uint32_t ph = 0u;
+  int slot = 0;
+  int cur_row = (int)(it0 / s.nch);
+  for (int64_t it = it0; it < it1; ++it, slot ^= 1) {
+    const int row = (int)(it / s.nch);
+    if (row != cur_row) {
+      flush(cur_row);
+      cur_row = row;
+    }
+    const int64_t c = it - (int64_t)row * s.nch;
+    const HeadState *hs = s.hs + row;
+    const uint32_t state = hs->state;
+    const int M = hs->M;
+    const float kappa = hs->kappa;
+    const uint32_t dstar = hs->delta_star;
+    const unsigned long long r = hs->r_ties;
+    const unsigned long long pw = s.pre[(int64_t)row * s.nch + c];
+    const unsigned long long den = s.renorm ? hs->sel_mass : hs->S;
+    const int64_t j0 = c * kSelChunk;
+    const int nv = (int)min((int64_t)kSelChunk, s.n - j0);
+    mbar_wait(&zbar[slot], (ph >> slot) & 1u);
+    ph ^= 1u << slot;
+    const float *zc = zbuf + (size_t)slot * kSelChunk + 16 * t;
+    int kept = 0;
+    if (state == kStDone) {
+      uint32_t dl[16], my = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4 v4 = *reinterpret_cast<const float4 *>(zc + 4 * k);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = 16 * t + 4 * k + e;
+          dl[4 * k + e] = i < nv ? (uint32_t)(M - zint(vv[e])) : 0xffffffffu;
+        }
+      }
+      const bool ties_on = dstar != 0xffffffffu;
+      uint32_t ms = 0, mt = 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        ms |= (dl[u] < dstar ? 1u : 0u) << u;
+        mt |= ((ties_on && dl[u] == dstar) ? 1u : 0u) << u;
+      }
+      my = ((uint32_t)__popc(ms) << 16) | (uint32_t)__popc(mt);
+      uint32_t inc = my;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += o;
+      }
+      if (lane == 31) sw[warp] = inc;
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kWT / 32; ++w) {
+        const uint32_t v = sw[w];
+        before += w < warp ? v : 0u;
+        total += v;
+      }
+      const uint32_t ex = before + inc - my;
+      const unsigned long long Sb = pw >> 32, Tb = pw & 0xffffffffull;
+      const unsigned long long pos0 = Sb + (Tb < r ? Tb : r);
+      unsigned long long ts = Tb + (ex & 0xffffu);
+      uint32_t keep = ms;
+      if (mt) {
+        const unsigned long long room = ts < r ? r - ts : 0ull;
+        uint32_t m = mt;
+        for (unsigned long long k = 0; k < room && m; ++k) { keep |= m & (0u - m); m &= m - 1u; }
+      }
+      const unsigned base = (unsigned)(Sb + (ex >> 16) + (ts < r ? ts : r) - pos0);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (keep >> u & 1u) {
+          const unsigned ls = base + __popc(keep & ((1u << u) - 1u));
+          stg_d[ls] = dl[u];
+          stg_o[ls] = (uint16_t)(16 * t + u);
+        }
+      }
+      __syncthreads();
+      const unsigned long long tt = Tb + (total & 0xffffu);
+      kept = (int)(Sb + (total >> 16) + (tt < r ? tt : r) - pos0);
+      const float inv_den = (float)(1.0 / (double)den);
+      int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
+      float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
+      for (int i = t; i < kept; i += kWT) {
+        const float w = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
+        oi[i] = (int32_t)(j0 + stg_o[i]);
+        ow[i] = w;
+        stg_w[i] = w;
+      }
+      __syncthreads();
+    }
+    // the chunk is consumed: refill its buffer with item it + 2 while the rows are gathered
+    if (t == 0 && it + 2 < it1) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request(it + 2, slot);
+    }
+    if (kept > 0) {  // Eq. 5 over the chunk's kept rows (CTA-uniform)
+      const int b = row / a.Hq, kv = (row - b * a.Hq) / a.G;
+      const uint16_t *Vb = a.V + (int64_t)b * a.v_b_stride + (int64_t)kv * a.v_kv_stride;
+      const uint16_t *Rb = a.res_v + (int64_t)b * a.res_b_stride + (int64_t)kv * a.res_cap * a.d;
+      for (int i0 = hw * kGU; i0 < kept; i0 += 16 * kGU) {
+        uint4 v[kGU];
+#pragma unroll
+        for (int q = 0; q < kGU; ++q) {
+          const int i = i0 + q;
+          if (i < kept) {
+            const int64_t j = j0 + stg_o[i];
+            const uint16_t *src;
+            if (j < a.n_q) {
+              src = Vb + j * 128;
+            } else {
+              const uint32_t sl = (uint32_t)(a.res_slot0 + (j - a.n_q)) % (uint32_t)a.res_cap;
+              src = Rb + (int64_t)sl * 128;
+            }
+            v[q] = ldg_nc16(src + sub * 8);
+          } else {
+            v[q] = make_uint4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kGU; ++q) {
+          const float w = i0 + q < kept ? stg_w[i0 + q] : 0.0f;
+          const uint32_t uu[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+          for (int p2 = 0; p2 < 4; ++p2) {
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&uu[p2]));
+            acc[2 * p2] = fmaf(w, f2.x, acc[2 * p2]);
+            acc[2 * p2 + 1] = fmaf(w, f2.y, acc[2 * p2 + 1]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // every read of zc / the staging / sw retired
+  }
+  flush(cur_row);
+}
+
+cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
+                                       int num_sms, cudaStream_t st) {
+  const int64_t items = (int64_t)s.rows * s.nch;
+  if (items <= 0) return cudaSuccess;
+  int64_t grid = 3LL * num_sms;
+  if (grid > items) grid = items;
+  const int64_t per = (items + grid - 1) / grid;
+  grid = (items + per - 1) / per;
+  const int maxc = select_wg_maxc(s.nch, per);
+  const size_t smem = (size_t)3 * kSelChunk * 4 + (size_t)kSelChunk * 2 + 16 * 128 * 4;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaFuncSetAttribute(k_sel_write_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured[dev] = 1;
+  }
+  launch_chain(k_sel_write_gather, dim3((unsigned)grid), dim3(kWT), smem, st, s, a, wpart, wdone, per, maxc);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------- short rows
 // Rows of up to kSmallMaxN candidates (configs 1, 2): ONE kernel, a cluster of cs <= 8 CTAs per
 // row, every CTA holding its <= 8192 scores in registers (16 per thread) for all passes.  The
@@ -1171,7 +1421,10 @@ cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------- launcher
-cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force) {
+cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
+                                       int num_sms, cudaStream_t st);
+
+cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force, const SelGather *wg) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
   if (force != 1 && s.n <= kSmallMaxN) return launch_select_small(s, nsplit > 1 ? 0 : 1, st);
   if (s.nch != select_chunks(s.n)) return cudaErrorInvalidValue;
@@ -1207,6 +1460,10 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, i
     if (smem4 > 200 * 1024) return cudaErrorInvalidValue;
     launch_chain(k_sel_prefix, dim3((unsigned)s.rows), dim3(kST), smem4, st, s);
     note_launch();
+  }
+  if (wg) {
+    const_cast<SelGather *>(wg)->used = 1;
+    return launch_select_write_gather(s, *wg->a, wg->wpart, wg->wdone, num_sms, st);
   }
   const int64_t items3 = (int64_t)s.rows * s.nch;
   const int64_t grid3 = items3 < 4LL * num_sms ? items3 : 4LL * num_sms;
