@@ -825,10 +825,9 @@ __global__ void __launch_bounds__(kWT, 4) k_sel_write(SelArgs s) {
 // neighbouring rows, so the G heads of a KV head read the same token range at about the same
 // time and shared kept rows hit in L2.  Replaces K3 + k_gather_rows (one pass over the kept
 // rows overlapping the compaction's z stream).
-constexpr int kGU = 8;  // value rows in flight per half-warp
-
-__global__ void __launch_bounds__(kWT, 3) k_sel_write_gather(SelArgs s, LayerArgs a, float *wpart,
-                                                              uint32_t *wdone, int64_t per, int maxc) {
+template <int kGU, int kMinB>  // value rows in flight per half-warp, CTAs per SM
+__global__ void __launch_bounds__(kWT, kMinB) k_sel_write_gather(SelArgs s, LayerArgs a, float *wpart,
+                                                                 uint32_t *wdone, int64_t per, int maxc) {
   extern __shared__ __align__(128) uint8_t sm3[];
   float *zbuf = reinterpret_cast<float *>(sm3);                                        // [2][kSelChunk]
   uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3 + 2 * kSelChunk * 4);            // [kSelChunk]
@@ -1043,11 +1042,12 @@ __global__ void __launch_bounds__(kWT, 3) k_sel_write_gather(SelArgs s, LayerArg
   flush(cur_row);
 }
 
-cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
-                                       int num_sms, cudaStream_t st) {
+template <int GU, int MB>
+static cudaError_t k3g_launch(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone, int num_sms,
+                              cudaStream_t st) {
   const int64_t items = (int64_t)s.rows * s.nch;
   if (items <= 0) return cudaSuccess;
-  int64_t grid = 3LL * num_sms;
+  int64_t grid = (int64_t)MB * num_sms;
   if (grid > items) grid = items;
   const int64_t per = (items + grid - 1) / grid;
   grid = (items + per - 1) / per;
@@ -1057,12 +1057,22 @@ cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, flo
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(k_sel_write_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_sel_write_gather<GU, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured[dev] = 1;
   }
-  launch_chain(k_sel_write_gather, dim3((unsigned)grid), dim3(kWT), smem, st, s, a, wpart, wdone, per, maxc);
+  launch_chain(k_sel_write_gather<GU, MB>, dim3((unsigned)grid), dim3(kWT), smem, st, s, a, wpart, wdone, per, maxc);
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
+                                       int num_sms, cudaStream_t st) {
+  static int v = -1;  // dev override (HC_K3G_GU = 8 | 12 | 16): rows in flight per half-warp
+  if (v < 0) { const char *ev = getenv("HC_K3G_GU"); v = ev ? atoi(ev) : 8; }
+  if (v == 16) return k3g_launch<16, 2>(s, a, wpart, wdone, num_sms, st);
+  if (v == 12) return k3g_launch<12, 2>(s, a, wpart, wdone, num_sms, st);
+  if (v == 4) return k3g_launch<4, 3>(s, a, wpart, wdone, num_sms, st);
+  return k3g_launch<8, 3>(s, a, wpart, wdone, num_sms, st);
 }
 
 // ---------------------------------------------------------------------------- short rows
