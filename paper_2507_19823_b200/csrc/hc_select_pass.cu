@@ -1127,7 +1127,8 @@ __device__ void find_cut(const uint32_t *cnt, const unsigned long long *mass, in
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded) {
+template <bool GATHER>  // GATHER: Eq. 5 over HBM values (d = 128) inside the kernel (la.out)
+__global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded, LayerArgs la) {
   extern __shared__ __align__(16) uint8_t sm5[];
   uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm5);                         // [kSmTok]
   uint16_t *stg_o = reinterpret_cast<uint16_t *>(sm5 + kSmTok * 4);           // [kSmTok]
@@ -1273,6 +1274,7 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
     }
     if (sc == cs) {  // cannot happen: Θ <= S and k_max < n are always reached
       if (rank == 0 && t == 0) hs->state = kStError;
+      if (GATHER && rank == 0 && t < 128) la.out[(int64_t)row * 128 + t] = 0.0f;
       cl.sync();
       return;
     }
@@ -1290,6 +1292,7 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
     const unsigned long long cc1 = oc->ccc, cm1 = oc->ccm;
     if (cbin >= kNB) {
       if (rank == 0 && t == 0) hs->state = kStError;
+      if (GATHER && rank == 0 && t < 128) la.out[(int64_t)row * 128 + t] = 0.0f;
       cl.sync();
       return;
     }
@@ -1314,6 +1317,7 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
     const int bin = cr.bin;
     if (bin >= kNB) {
       if (rank == 0 && t == 0) hs->state = kStError;
+      if (GATHER && rank == 0 && t < 128) la.out[(int64_t)row * 128 + t] = 0.0f;
       cl.sync();
       return;
     }
@@ -1382,9 +1386,70 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   int32_t *oi = s.sel_idx + (int64_t)row * s.k_max + pos0;
   float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
   const int64_t cbase = (int64_t)rank * kSmTok;
+  float *stg_w = reinterpret_cast<float *>(stg_d);  // weights in place of Δ (GATHER)
   for (int i = t; i < kept; i += kST) {
+    const float w = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
     oi[i] = (int32_t)(cbase + stg_o[i]);
-    ow[i] = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
+    ow[i] = w;
+    if (GATHER) stg_w[i] = w;
+  }
+  if constexpr (GATHER) {  // Eq. 5: my kept rows (half-warp per row, 8 in flight), cluster sum
+    __shared__ float gpart[128];
+    __syncthreads();
+    const int hw = t >> 4, sub = t & 15;
+    const int b = row / la.Hq, kv = (row - b * la.Hq) / la.G;
+    const uint16_t *Vb = la.V + (int64_t)b * la.v_b_stride + (int64_t)kv * la.v_kv_stride;
+    const uint16_t *Rb = la.res_v + (int64_t)b * la.res_b_stride + (int64_t)kv * la.res_cap * la.d;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+    for (int i0 = hw * 8; i0 < kept; i0 += (kST / 16) * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = i0 + q;
+        if (i < kept) {
+          const int64_t j = cbase + stg_o[i];
+          const uint16_t *src;
+          if (j < la.n_q) {
+            src = Vb + j * 128;
+          } else {
+            const uint32_t sl = (uint32_t)(la.res_slot0 + (j - la.n_q)) % (uint32_t)la.res_cap;
+            src = Rb + (int64_t)sl * 128;
+          }
+          v[q] = ldg_nc16(src + sub * 8);
+        } else {
+          v[q] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float w = i0 + q < kept ? stg_w[i0 + q] : 0.0f;
+        const uint32_t uu[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+        for (int p2 = 0; p2 < 4; ++p2) {
+          const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&uu[p2]));
+          acc[2 * p2] = fmaf(w, f2.x, acc[2 * p2]);
+          acc[2 * p2 + 1] = fmaf(w, f2.y, acc[2 * p2 + 1]);
+        }
+      }
+    }
+    __syncthreads();  // the staging is read: [kST/16][128] partials over it
+    float *red = reinterpret_cast<float *>(sm5);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[hw * 128 + sub * 8 + e] = acc[e];
+    __syncthreads();
+    if (t < 128) {
+      float v = 0.0f;
+      for (int q = 0; q < kST / 16; ++q) v += red[q * 128 + t];
+      gpart[t] = v;
+    }
+    cl.sync();
+    if (rank == 0 && t < 128) {
+      float o = 0.0f;
+      for (int rr = 0; rr < cs; ++rr) o += cl.map_shared_rank(gpart, rr)[t];
+      la.out[(int64_t)row * 128 + t] = o;
+    }
   }
   if (rank == 0 && t == 0) {
     hs->M = M;
@@ -1403,16 +1468,18 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   cl.sync();  // peers may still read my slot through DSMEM
 }
 
-cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st) {
+cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st, const LayerArgs *ga) {
   const int cs = (int)((s.n + kSmTok - 1) / kSmTok);
   if (cs < 1 || cs > 8) return cudaErrorInvalidValue;
   static int configured[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaFuncSetAttribute(k_sel_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTok * 6 + kNB * 8);
+    cudaFuncSetAttribute(k_sel_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTok * 6 + kNB * 8);
+    cudaFuncSetAttribute(k_sel_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTok * 6 + kNB * 8);
     configured[dev] = 1;
   }
+  LayerArgs dummy{};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(s.rows * cs));
   cfg.blockDim = dim3(kST);
@@ -1425,7 +1492,8 @@ cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sel_small, s, cs, folded);
+  cudaError_t e = ga ? cudaLaunchKernelEx(&cfg, k_sel_small<true>, s, cs, folded, *ga)
+                     : cudaLaunchKernelEx(&cfg, k_sel_small<false>, s, cs, folded, dummy);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -1436,7 +1504,10 @@ cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, flo
 
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force, const SelGather *wg) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
-  if (force != 1 && s.n <= kSmallMaxN) return launch_select_small(s, nsplit > 1 ? 0 : 1, st);
+  if (force != 1 && s.n <= kSmallMaxN) {
+    if (wg) const_cast<SelGather *>(wg)->used = 1;
+    return launch_select_small(s, nsplit > 1 ? 0 : 1, st, wg ? wg->a : nullptr);
+  }
   if (s.nch != select_chunks(s.n)) return cudaErrorInvalidValue;
   // K1 / K2: one wave of 2 CTAs per SM over all rows, whole chunks per CTA
   int64_t cpr = (2LL * num_sms) / s.rows;
