@@ -120,8 +120,11 @@ void choose_scan(int64_t units, int64_t n, int g, int cpow2, int G, int sms, int
                       scan_sk_enabled();
       const double waves = sk ? (double)items / sms : (double)((items + sms - 1) / sms);
       const double gper = (double)((g + sp - 1) / sp);
-      double item = tile * gper * wf / 32.0 + gper * (cpow2 * entry + tile * 4.0) / 128.0;
-      if (sp > 1) item += tile * G * 4.0 / 64.0;  // partial stores
+      // slice + code ingress arrives by bulk copy (TMA) at ~2x the LSU wavefront rate; a split
+      // item's exact partial is added to z with float atomics (~4x a store) -- weights fitted to
+      // config 2 (TPT 8 / 2 splits measured 383.6 vs 374.2 steps/s for TPT 16 / 4 splits)
+      double item = tile * gper * wf / 32.0 + gper * (cpow2 * entry + tile * 4.0) / 256.0;
+      if (sp > 1) item += tile * G * 4.0 / 16.0;  // partial atomics
       double cost = waves * item;
       if (sp > 1) cost += (double)units * n * G * 4.0 * (sp + 1) / (sms * 64.0);  // reduce pass
       if (cost < best * 0.999) { best = cost; *tpt = t; *split = sp; }
