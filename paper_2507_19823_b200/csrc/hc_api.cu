@@ -682,8 +682,8 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   } else {
     // HBM values, per-head rows gather: the long-row passes fuse Eq. 5 into their K3
     // (k_sel_write_gather) unless HC_K3G=0
-    static int k3g_env = -1;
-    if (k3g_env < 0) { const char *ev = getenv("HC_K3G"); k3g_env = (ev && !strcmp(ev, "0")) ? 0 : 1; }
+    const char *k3g_ev = getenv("HC_K3G");  // read per call (the tests run both)
+    const int k3g_env = (k3g_ev && !strcmp(k3g_ev, "0")) ? 0 : 1;
     SelGather wg{&a, (float *)((uint8_t *)ws + Lw.o_wpart), (uint32_t *)((uint8_t *)ws + Lw.o_rdone), 0};
     const bool try_wg = k3g_env && rows_gather && a.d == 128 && !a.g_cnt;
     if ((e = launch_select(sa, n_q > 0 ? a.scan_split : 1, a.num_sms, s, sel_force, try_wg ? &wg : nullptr)) !=

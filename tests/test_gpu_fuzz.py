@@ -52,15 +52,20 @@ def _cases(k=None, seed=None):
     return out
 
 
-@pytest.mark.parametrize("sel", ["auto", "pass", "fused"])  # auto: k_sel_small for these short rows
+@pytest.mark.parametrize("sel", ["auto", "pass", "fused", "auto-sep", "pass-sep"])
 @pytest.mark.parametrize("kw", _cases(), ids=lambda kw: "-".join(f"{k}{v}" for k, v in kw.items()
                                                                 if k in ("d", "g", "G", "c", "n", "tau")))
 def test_fuzz_decode_parity(torch_cuda, kw, sel, monkeypatch):
     """sel: the selection kernel -- auto (by row length: the one-kernel cluster path k_sel_small
     up to 64K candidates), pass (the three passes) or fused (round 1's cluster kernel); all
-    bit-exact on every shape."""
-    if sel != "auto":
-        monkeypatch.setenv("HC_SELECT", sel)
+    bit-exact on every shape.  With values in HBM (d = 128) auto / pass run Eq. 5 inside the
+    selection (k_sel_small's gather, K3G); the "-sep" variants (HC_K3G=0) use the separate
+    k_gather_rows instead."""
+    base = sel.split("-")[0]
+    if base != "auto":
+        monkeypatch.setenv("HC_SELECT", base)
+    if sel.endswith("-sep"):
+        monkeypatch.setenv("HC_K3G", "0")
     case = Case(**kw)
     if case.n == 0 and case.n_res == 0:
         pytest.skip("empty")
