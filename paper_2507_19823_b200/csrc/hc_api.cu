@@ -854,7 +854,8 @@ hc_status hc_shard_finish(const hc_kcache *kc, const hc_vstore *vs, int32_t laye
                                       (const unsigned long long *)allcnt, rank, shard_base,
                                       (float *)(w8 + Lw.o_part), out, s, (int64_t *)(w8 + Lw.o_grange),
                                       (float *)(w8 + Lw.o_rpart), (uint32_t *)(w8 + Lw.o_rdone),
-                                      (float *)(w8 + Lw.o_upart), (uint32_t *)(w8 + Lw.o_udone));
+                                      (float *)(w8 + Lw.o_upart), (uint32_t *)(w8 + Lw.o_udone),
+                                      (unsigned long long *)(w8 + Lw.o_spre), (float *)(w8 + Lw.o_wpart));
   if (e != cudaSuccess) return cuda_check(e, "shard finish");
   if (sel_k) {
     const int rows = a.B * a.Hq;

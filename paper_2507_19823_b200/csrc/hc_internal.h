@@ -200,9 +200,14 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
 struct SelGather { const LayerArgs *a; float *wpart; uint32_t *wdone; int used; };  // used: set when K3G ran
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force = 0,
                           const SelGather *wg = nullptr);
+// K3G alone (the sharded finish: s.pre built by the shard's counts, idx_base = the shard's base)
+cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
+                                       int num_sms, cudaStream_t st, int64_t idx_base);
 // contributor slots per row of k_sel_write_gather (CTAs over contiguous ranges of `per` items)
 inline int select_wg_maxc(int64_t nch, int64_t per) { return (int)((nch + per - 1) / per + 1); }
 constexpr int kSelChunk = 4096;
+// HeadState::state of the selection passes (hc_select_pass.cu; the sharded finish marks rows done)
+constexpr uint32_t kStRefine1 = 1, kStRefine2 = 2, kStDone = 3, kStError = 4;
 constexpr int kTableU = 8;     // k_table: units per CTA (max)
 constexpr int kTableQ = 8192;  // k_table: staged query floats per CTA (32 KiB)  // tokens per chunk of the selection passes (16 KB of z)
 inline int64_t select_chunks(int64_t n) { return (n + kSelChunk - 1) / kSelChunk; }
@@ -221,7 +226,8 @@ cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st, int64_t *grange = nullptr,
                                 float *rpart = nullptr, uint32_t *rdone = nullptr,
-                                float *upart = nullptr, uint32_t *udone = nullptr);
+                                float *upart = nullptr, uint32_t *udone = nullptr,
+                                unsigned long long *pre = nullptr, float *wpart = nullptr);
 
 // f4 (iii) App. B block-wise prefill attention (hc_prefill.cu), d = 128
 cudaError_t launch_blockwise_attn(const uint16_t *q, const uint16_t *k, const uint16_t *v, int64_t n,

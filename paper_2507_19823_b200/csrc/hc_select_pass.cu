@@ -44,7 +44,6 @@ namespace hc {
 
 constexpr int kST = 512;             // threads per CTA (all three kernels)
 constexpr int kBPT = kNB / kST;      // histogram bins per thread in the block-wide walks (8)
-constexpr uint32_t kStRefine1 = 1, kStRefine2 = 2, kStDone = 3, kStError = 4;
 
 // R4's mass W(Δ) = trunc(p(f) * 2^(40+n)), x = -(float)Δ*κ, n = floor(x), f = x - n, 0 for
 // x < -40 -- the same IEEE steps as mass() / mass_d() (hc_device.cuh), bit for bit, with the
@@ -827,7 +826,8 @@ __global__ void __launch_bounds__(kWT, 4) k_sel_write(SelArgs s) {
 // rows overlapping the compaction's z stream).
 template <int kGU, int kMinB>  // value rows in flight per half-warp, CTAs per SM
 __global__ void __launch_bounds__(kWT, kMinB) k_sel_write_gather(SelArgs s, LayerArgs a, float *wpart,
-                                                                 uint32_t *wdone, int64_t per, int maxc) {
+                                                                 uint32_t *wdone, int64_t per, int maxc,
+                                                                 int64_t idx_base) {
   extern __shared__ __align__(128) uint8_t sm3[];
   float *zbuf = reinterpret_cast<float *>(sm3);                                        // [2][kSelChunk]
   uint32_t *stg_d = reinterpret_cast<uint32_t *>(sm3 + 2 * kSelChunk * 4);            // [kSelChunk]
@@ -990,7 +990,7 @@ __global__ void __launch_bounds__(kWT, kMinB) k_sel_write_gather(SelArgs s, Laye
       float *ow = s.sel_w + (int64_t)row * s.k_max + pos0;
       for (int i = t; i < kept; i += kWT) {
         const float w = __fmul_rn((float)wmass(stg_d[i], kappa), inv_den);
-        oi[i] = (int32_t)(j0 + stg_o[i]);
+        oi[i] = (int32_t)(idx_base + j0 + stg_o[i]);  // global index (a shard's base + local)
         ow[i] = w;
         stg_w[i] = w;
       }
@@ -1044,7 +1044,7 @@ __global__ void __launch_bounds__(kWT, kMinB) k_sel_write_gather(SelArgs s, Laye
 
 template <int GU, int MB>
 static cudaError_t k3g_launch(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone, int num_sms,
-                              cudaStream_t st) {
+                              cudaStream_t st, int64_t idx_base) {
   const int64_t items = (int64_t)s.rows * s.nch;
   if (items <= 0) return cudaSuccess;
   int64_t grid = (int64_t)MB * num_sms;
@@ -1060,19 +1060,20 @@ static cudaError_t k3g_launch(const SelArgs &s, const LayerArgs &a, float *wpart
     cudaFuncSetAttribute(k_sel_write_gather<GU, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured[dev] = 1;
   }
-  launch_chain(k_sel_write_gather<GU, MB>, dim3((unsigned)grid), dim3(kWT), smem, st, s, a, wpart, wdone, per, maxc);
+  launch_chain(k_sel_write_gather<GU, MB>, dim3((unsigned)grid), dim3(kWT), smem, st, s, a, wpart, wdone, per, maxc,
+               idx_base);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
-                                       int num_sms, cudaStream_t st) {
+                                       int num_sms, cudaStream_t st, int64_t idx_base) {
   static int v = -1;  // dev override (HC_K3G_GU = 8 | 12 | 16): rows in flight per half-warp
   if (v < 0) { const char *ev = getenv("HC_K3G_GU"); v = ev ? atoi(ev) : 8; }
-  if (v == 16) return k3g_launch<16, 2>(s, a, wpart, wdone, num_sms, st);
-  if (v == 12) return k3g_launch<12, 2>(s, a, wpart, wdone, num_sms, st);
-  if (v == 4) return k3g_launch<4, 3>(s, a, wpart, wdone, num_sms, st);
-  return k3g_launch<8, 3>(s, a, wpart, wdone, num_sms, st);
+  if (v == 16) return k3g_launch<16, 2>(s, a, wpart, wdone, num_sms, st, idx_base);
+  if (v == 12) return k3g_launch<12, 2>(s, a, wpart, wdone, num_sms, st, idx_base);
+  if (v == 4) return k3g_launch<4, 3>(s, a, wpart, wdone, num_sms, st, idx_base);
+  return k3g_launch<8, 3>(s, a, wpart, wdone, num_sms, st, idx_base);
 }
 
 // ---------------------------------------------------------------------------- short rows
@@ -1499,8 +1500,6 @@ cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st, c
 }
 
 // ---------------------------------------------------------------------------- launcher
-cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
-                                       int num_sms, cudaStream_t st);
 
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force, const SelGather *wg) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
@@ -1544,7 +1543,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, i
   }
   if (wg) {
     const_cast<SelGather *>(wg)->used = 1;
-    return launch_select_write_gather(s, *wg->a, wg->wpart, wg->wdone, num_sms, st);
+    return launch_select_write_gather(s, *wg->a, wg->wpart, wg->wdone, num_sms, st, 0);
   }
   const int64_t items3 = (int64_t)s.rows * s.nch;
   const int64_t grid3 = items3 < 4LL * num_sms ? items3 : 4LL * num_sms;

@@ -12,6 +12,9 @@
 //                                                  -> all-reduce SUM fp32  (C5)
 // Every rank evaluates bound1 / bound2 on the same reduced integers, so all ranks
 // agree on (b*, Δ*, r) bit for bit: the index set is R-invariant.
+#include <stdlib.h>
+#include <string.h>
+
 #include "hc_internal.h"
 
 namespace hc {
@@ -523,6 +526,53 @@ __global__ void __launch_bounds__(kShT) k_sh_compact(LayerArgs a, SelArgs s, int
   }
 }
 
+// The fused finish's chunk prefixes (K3G, hc_select_pass.cu): per row, the GLOBAL (strict, tie)
+// counts before each of this rank's chunks -- the lower ranks' totals (all-gathered) plus this
+// rank's earlier chunks -- as (strict << 32 | ties); and the row marked resolved for K3G.
+__global__ void __launch_bounds__(256) k_sh_pre(SelArgs s, int nch, const uint32_t *chunk,
+                                                const unsigned long long *allcnt, int rank) {
+  const int row = blockIdx.x, t = threadIdx.x;
+  __shared__ unsigned long long base2[2];
+  __shared__ unsigned long long wsum[2][8];
+  if (t == 0) {
+    unsigned long long ps = 0, pt = 0;
+    for (int r = 0; r < rank; ++r) {
+      ps += allcnt[((int64_t)r * s.rows + row) * 2];
+      pt += allcnt[((int64_t)r * s.rows + row) * 2 + 1];
+    }
+    base2[0] = ps;
+    base2[1] = pt;
+    s.hs[row].state = kStDone;
+  }
+  // thread-contiguous runs of chunks, then a block scan of the run totals
+  const int per = (nch + 255) / 256;
+  const int c0 = min(nch, t * per), c1 = min(nch, c0 + per);
+  unsigned long long xs = 0, xt = 0;
+  for (int c = c0; c < c1; ++c) {
+    xs += chunk[((int64_t)row * nch + c) * 2];
+    xt += chunk[((int64_t)row * nch + c) * 2 + 1];
+  }
+  unsigned long long is = xs, it = xt;
+  const int lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long os = __shfl_up_sync(0xffffffffu, is, off);
+    const unsigned long long ot = __shfl_up_sync(0xffffffffu, it, off);
+    if (lane >= off) { is += os; it += ot; }
+  }
+  if (lane == 31) { wsum[0][w] = is; wsum[1][w] = it; }
+  __syncthreads();
+  unsigned long long bs = base2[0], bt = base2[1];
+  for (int q = 0; q < w; ++q) { bs += wsum[0][q]; bt += wsum[1][q]; }
+  bs += is - xs;
+  bt += it - xt;
+  for (int c = c0; c < c1; ++c) {
+    s.pre[(int64_t)row * nch + c] = (bs << 32) | bt;
+    bs += chunk[((int64_t)row * nch + c) * 2];
+    bt += chunk[((int64_t)row * nch + c) * 2 + 1];
+  }
+}
+
 // deterministic sum of the chunk partials -> out [rows][d] (this rank's numerator share)
 __global__ void k_sh_reduce(int rows, int nch, int d, const float *part, float *out) {
   const int row = blockIdx.x;
@@ -591,9 +641,27 @@ cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsi
 cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint32_t *chunk,
                                 const unsigned long long *allcnt, int rank, int64_t base,
                                 float *part, float *out, cudaStream_t st, int64_t *grange,
-                                float *rpart, uint32_t *rdone, float *upart, uint32_t *udone) {
+                                float *rpart, uint32_t *rdone, float *upart, uint32_t *udone,
+                                unsigned long long *pre, float *wpart) {
   const int rows = a.B * a.Hq;
   const int nch = shard_chunks(a.n_cand);
+  const char *k3g_ev = getenv("HC_K3G");
+  if (nch > 0 && pre && wpart && rdone && a.d == 128 && a.v_placement == 0 && !(k3g_ev && !strcmp(k3g_ev, "0")) &&
+      nch == select_chunks(a.n_cand)) {
+    // values in HBM: this rank's ordered compaction fused with its Eq. 5 share (K3G) over the
+    // chunk prefixes of the global order
+    SelArgs s2 = s;
+    s2.pre = pre;
+    s2.nch = nch;
+    s2.n = a.n_cand;
+    k_sh_pre<<<rows, 256, 0, st>>>(s2, nch, chunk, allcnt, rank);
+    note_launch();
+    cudaError_t e = cudaMemsetAsync(rdone, 0, (size_t)rows * 4, st);
+    if (e != cudaSuccess) return e;
+    LayerArgs g = a;
+    g.out = out;
+    return launch_select_write_gather(s2, g, wpart, rdone, a.num_sms, st, base);
+  }
   if (nch > 0 && grange && a.v_placement == 1 && a.G > 1 && upart && udone) {
     // host-resident values (config 5): the GQA union of this rank's kept rows is read once
     // over the host link (as in the unsharded decode), not once per head
