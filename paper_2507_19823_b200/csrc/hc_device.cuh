@@ -188,6 +188,21 @@ HC_HD uint64_t threshold(uint32_t tau_q, uint64_t S) {
   return (hi << 40) | (lo2 >> 24);
 }
 
+// R4's mass W(Δ) = trunc(p(f) * 2^(40+n)), x = -(float)Δ*κ, n = floor(x), f = x - n, 0 for
+// x < -40 -- the same IEEE steps as mass() / mass_d() (hc_device.cuh), bit for bit, with the
+// floor, the int->float of n and the final truncation on the conversion pipe (F2I / I2F),
+// which runs beside the FMA / ALU pipes this pass is otherwise bound by.
+__device__ __forceinline__ uint64_t wmass(uint32_t dl, float kappa) {
+  const float df = __fsub_rn(__int_as_float(0x4B000000 + (int)dl), 8388608.0f);  // exact, Δ <= 2^23
+  const float x0 = -__fmul_rn(df, kappa);
+  const float x = fmaxf(x0, -64.0f);          // keeps 2^(40+n) normal; x0 < -40 -> 0 below
+  const int ni = __float2int_rd(x);            // floor (exact for |x| <= 64)
+  const float f = __fsub_rn(x, __int2float_rn(ni));
+  const float v = __fmul_rn(exp2_poly(f), pow2f(40 + ni));
+  const uint64_t w = __float2ull_rz(v);        // truncation toward zero, v < 2^41
+  return x0 < -40.0f ? 0ull : w;
+}
+
 // 16-B read-only load that bypasses L1 (value rows: read once per head group)
 __device__ __forceinline__ uint4 ldg_nc16(const uint16_t *p) {
   uint4 v;

@@ -87,8 +87,9 @@ __global__ void __launch_bounds__(kShT) k_sh_hist1(LayerArgs a, const int32_t *g
     const uint32_t dl = (uint32_t)(M - zint(zf));
     const uint32_t bk = dl >> shift;
     atomicAdd(&cnt[bk], 1u);
-    uint32_t wl, wh;
-    mass_parts(dl, kappa, wl, wh);
+    const unsigned long long w = wmass(dl, kappa);  // conversion-pipe form of mass_d (bit-exact)
+    const uint32_t wl = (uint32_t)w;
+    uint32_t wh = (uint32_t)(w >> 32);
     const uint32_t old = atomicAdd(&mlo[bk], wl);
     wh += (old + wl < old) ? 1u : 0u;
     if (wh) atomicAdd(&mhi[bk], wh);
