@@ -630,7 +630,7 @@ def measure_config5_layers(args, layers: int, dev_index: int, h2d_peak: float) -
     return res
 
 
-HOST_FRAC_CANDIDATES = (0.65, 0.7, 0.75)
+HOST_FRAC_CANDIDATES = (0.6, 0.65, 0.7, 0.75)  # calibrated at start-up; box optima 0.65-0.7
 
 
 def calibrate_host_frac(wl, cfg):
@@ -649,7 +649,7 @@ def calibrate_host_frac(wl, cfg):
         wl.step()
         torch.cuda.synchronize()
         g, _ = wl.capture(wl.step)
-        ms = time_graph(g, 3, 1) / 3
+        ms = time_graph(g, 4, 1) / 4
         del g
         if best is None or ms < best[1]:
             best = (f, ms)
