@@ -290,8 +290,12 @@ class Workload:
         import paper_2507_19823_b200 as hc
         if self.parts:
             return self.step_pipelined(profile)
+        # plain decode: the append and the decode as ONE library call (hc_append_decode_attention:
+        # the append's encode overlaps the table build); HC_FUSED_APPEND=0 issues the two calls
+        fused = (self.is_last and self.hetero is None and self.shard is None and not self.cpu_gather
+                 and os.environ.get("HC_FUSED_APPEND", "1") != "0")
         for l in range(self.cfg["L"]):
-            if self.is_last:
+            if self.is_last and not fused:
                 self.kc.append(l, self.k_new[l], self.v_new[l], self.vs)
             if profile:
                 hc.profile_scan_events(*self.ev[l])
@@ -300,6 +304,9 @@ class Workload:
                 self._step_cpu_gather(l)
             elif self.hetero is not None:
                 self.hetero(self.q[l], l, self.bud, self.out[l], self.sel_k[l], self.ws)
+            elif fused:
+                hc.append_decode_attention(self.q[l], self.kc, self.vs, l, self.k_new[l], self.v_new[l],
+                                           self.bud, out=self.out[l], sel_k=self.sel_k[l], ws=self.ws)
             elif self.shard is None:
                 hc.decode_attention(self.q[l], self.kc, self.vs, l, self.bud, out=self.out[l],
                                     sel_k=self.sel_k[l], ws=self.ws)

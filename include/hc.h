@@ -242,6 +242,17 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
                               float *sel_w, int64_t *sel_k, const hc_decode_debug *dbg, void *ws,
                               size_t ws_bytes, hc_stream_t stream);
 
+/* hc_append_kv + hc_decode_attention in one call (a decode step appends the new token, then
+ * attends over the cache including it; PAPER.md P:227 then P:229-287): the append's encode /
+ * value copy runs on a library-owned side stream forked from `stream` (event edges; one side
+ * stream per device and host thread) concurrently with the table build, and the scan waits for
+ * it -- the result equals the two calls in sequence.  Arguments as in the two calls (no debug
+ * taps); kc->n_q / n_res advance as in hc_append_kv.  Graph-capturable. */
+hc_status hc_append_decode_attention(const uint16_t *q, hc_kcache *kc, const hc_vstore *vs, int32_t layer,
+                                     const uint16_t *k_new, const uint16_t *v_new, hc_budget budget, float *out,
+                                     int32_t *sel_idx, float *sel_w, int64_t *sel_k, void *ws, size_t ws_bytes,
+                                     hc_stream_t stream);
+
 /* Standalone Eq. 4 selection on real-valued scores (R5b):
  *   scores [rows][n] fp32 (z̃ = q·Kᵀ, unscaled; softmax uses 1/√d)
  *   idx [rows][k_max] int32 ascending, w [rows][k_max] fp32, k [rows] int64. */

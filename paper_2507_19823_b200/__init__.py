@@ -23,7 +23,8 @@ HC_V_DEVICE, HC_V_HOST_MAPPED = 0, 1
 EXPORTS = ["hc_last_error", "hc_version", "hc_launch_count", "hc_profile_scan_events",
            "hc_profile_eq3_events",
            "hc_codebook_absmax", "hc_quantize_keys", "hc_append_kv",
-           "hc_decode_workspace_bytes", "hc_decode_attention", "hc_select_workspace_bytes",
+           "hc_decode_workspace_bytes", "hc_decode_attention", "hc_append_decode_attention",
+           "hc_select_workspace_bytes",
            "hc_select_topk", "hc_host_weighted_sum", "hc_enqueue_host_weighted_sum",
            "hc_shard_workspace_bytes", "hc_shard_begin", "hc_shard_hist1",
            "hc_shard_hist2", "hc_shard_counts", "hc_shard_finish", "hc_kmeans_workspace_bytes",
@@ -100,6 +101,9 @@ def lib():
                                           hc_budget, p, p, p, p, C.POINTER(hc_decode_debug), p,
                                           C.c_size_t, p]
         L.hc_decode_attention.restype = i32
+        L.hc_append_decode_attention.argtypes = [p, C.POINTER(hc_kcache), C.POINTER(hc_vstore), i32, p, p,
+                                                 hc_budget, p, p, p, p, p, C.c_size_t, p]
+        L.hc_append_decode_attention.restype = i32
         L.hc_select_workspace_bytes.argtypes = [i64, i64, hc_budget]
         L.hc_select_workspace_bytes.restype = C.c_size_t
         L.hc_select_topk.argtypes = [p, i64, i64, i32, hc_budget, p, p, p, p, C.c_size_t, p]
@@ -533,6 +537,23 @@ def decode_attention(q, kc: KCache, vstore: VStore, layer: int, bud: hc_budget, 
                                    C.byref(dbg) if dbg is not None else None,
                                    _ptr(ws.t), ws.nbytes, _stream(stream))
     _check(st)
+    return out
+
+
+def append_decode_attention(q, kc: KCache, vstore: VStore, layer: int, k_new, v_new, bud: hc_budget,
+                            out=None, sel_idx=None, sel_w=None, sel_k=None, ws: Workspace | None = None,
+                            stream=None):
+    """hc_append_decode_attention: kc.append(layer, k_new, v_new) then decode_attention, with
+    the append overlapping the table build inside the library."""
+    import torch
+    if out is None:
+        out = torch.empty((kc.B, kc.Hq, kc.d), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = Workspace(kc.workspace_bytes(bud), device=q.device)
+    vs = vstore.struct()
+    _check(lib().hc_append_decode_attention(_ptr(q), C.byref(kc.s), C.byref(vs), layer, _ptr(k_new),
+                                            _ptr(v_new), bud, _ptr(out), _ptr(sel_idx), _ptr(sel_w),
+                                            _ptr(sel_k), _ptr(ws.t), ws.nbytes, _stream(stream)))
     return out
 
 

@@ -600,11 +600,65 @@ static hc_status prepare_layer(const uint16_t *q, const hc_kcache *kc, const hc_
   return HC_OK;
 }
 
+static hc_status decode_impl(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs, int32_t layer,
+                             hc_budget budget, float *out, int32_t *sel_idx, float *sel_w, int64_t *sel_k,
+                             const hc_decode_debug *dbg, void *ws, size_t ws_bytes, cudaStream_t s,
+                             cudaEvent_t join_before_scan);
+
 hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs,
                               int32_t layer, hc_budget budget, float *out, int32_t *sel_idx,
                               float *sel_w, int64_t *sel_k, const hc_decode_debug *dbg, void *ws,
                               size_t ws_bytes, hc_stream_t stream) {
+  return decode_impl(q, kc, vs, layer, budget, out, sel_idx, sel_w, sel_k, dbg, ws, ws_bytes,
+                     (cudaStream_t)stream, nullptr);
+}
+
+// hc_append_decode_attention: the append's encode / value copy runs on a library side stream
+// forked from `stream`, concurrently with the table build (both only read the layer's inputs
+// and the codebook); the scan waits for it.  Fork / join are event edges, so the call is
+// CUDA-graph capturable like the two calls it replaces.
+namespace {
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream *side_stream() {
+  thread_local SideStream ss[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  SideStream &x = ss[dev];
+  if (!x.st) {
+    if (cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+  }
+  return &x;
+}
+}  // namespace
+
+hc_status hc_append_decode_attention(const uint16_t *q, hc_kcache *kc, const hc_vstore *vs, int32_t layer,
+                                     const uint16_t *k_new, const uint16_t *v_new, hc_budget budget, float *out,
+                                     int32_t *sel_idx, float *sel_w, int64_t *sel_k, void *ws, size_t ws_bytes,
+                                     hc_stream_t stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  SideStream *ss = side_stream();
+  if (!ss) return fail(HC_ERR_CUDA, "side stream");
+  if (cudaEventRecord(ss->fork, s) != cudaSuccess || cudaStreamWaitEvent(ss->st, ss->fork, 0) != cudaSuccess)
+    return fail(HC_ERR_CUDA, "fork");
+  hc_status st = hc_append_kv(kc, vs, layer, k_new, v_new, (hc_stream_t)ss->st);
+  if (cudaEventRecord(ss->join, ss->st) != cudaSuccess) return fail(HC_ERR_CUDA, "join record");
+  if (st) {  // still join the side stream before returning the error
+    cudaStreamWaitEvent(s, ss->join, 0);
+    return st;
+  }
+  return decode_impl(q, kc, vs, layer, budget, out, sel_idx, sel_w, sel_k, nullptr, ws, ws_bytes, s, ss->join);
+}
+
+static hc_status decode_impl(const uint16_t *q, const hc_kcache *kc, const hc_vstore *vs, int32_t layer,
+                             hc_budget budget, float *out, int32_t *sel_idx, float *sel_w, int64_t *sel_k,
+                             const hc_decode_debug *dbg, void *ws, size_t ws_bytes, cudaStream_t s,
+                             cudaEvent_t join_before_scan) {
   LayerArgs a;
   Layout Lw;
   hc_status st = prepare_layer(q, kc, vs, layer, budget, out, sel_idx, sel_w, sel_k, ws, ws_bytes, s,
@@ -646,6 +700,8 @@ hc_status hc_decode_attention(const uint16_t *q, const hc_kcache *kc, const hc_v
   }
   if (e3b) cudaEventRecordWithFlags(e3b, s, e3flag);
   if ((e = launch_table(a, s)) != cudaSuccess) return cuda_check(e, "table");
+  if (join_before_scan && cudaStreamWaitEvent(s, join_before_scan, 0) != cudaSuccess)
+    return fail(HC_ERR_CUDA, "join");  // the append (side stream) wrote the new token
   if ((e = launch_resident(a, s)) != cudaSuccess) return cuda_check(e, "resident");
   if (n_q > 0 && (e = launch_scan(a, s)) != cudaSuccess) return cuda_check(e, "scan");
   if (e3e) cudaEventRecordWithFlags(e3e, s, e3flag);
