@@ -68,7 +68,7 @@ def _run(case, fused, graph):
                                 dict(B=1, Hkv=2, n=70001, k_max=9000, seed=92),
                                 dict(B=1, Hkv=1, n=5000, k_max=600, res_cap=64, n_res=17, seed=93)])
 def test_append_decode_equals_append_then_decode(torch_cuda, kw, graph):
-    case = Case(n_cap=kw["n"] + 64, **kw)
+    case = Case(n_cap=(kw["n"] + 64 + 63) // 64 * 64, **kw)
     a = _run(case, fused=False, graph=graph)
     b = _run(case, fused=True, graph=graph)
     assert np.array_equal(a["codes"], b["codes"])
