@@ -621,6 +621,11 @@ namespace {
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  ~SideStream() {  // thread exit (errors ignored: the context may already be gone at process exit)
+    if (join) cudaEventDestroy(join);
+    if (fork) cudaEventDestroy(fork);
+    if (st) cudaStreamDestroy(st);
+  }
 };
 SideStream *side_stream() {
   thread_local SideStream ss[64];

@@ -199,7 +199,7 @@ cudaError_t launch_select_fused(const SelArgs &s, const LayerArgs &la, int nspli
 // output, wpart [rows][select_wg_maxc][128] / wdone [rows] (zeroed) are its partials / counters
 struct SelGather { const LayerArgs *a; float *wpart; uint32_t *wdone; int used; };  // used: set when K3G ran
 cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force = 0,
-                          const SelGather *wg = nullptr);
+                          SelGather *wg = nullptr);
 // K3G alone (the sharded finish: s.pre built by the shard's counts, idx_base = the shard's base)
 cudaError_t launch_select_write_gather(const SelArgs &s, const LayerArgs &a, float *wpart, uint32_t *wdone,
                                        int num_sms, cudaStream_t st, int64_t idx_base);

@@ -1486,10 +1486,10 @@ cudaError_t launch_select_small(const SelArgs &s, int folded, cudaStream_t st, c
 
 // ---------------------------------------------------------------------------- launcher
 
-cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force, const SelGather *wg) {
+cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, int force, SelGather *wg) {
   if (s.rows <= 0 || s.n <= 0) return cudaSuccess;
   if (force != 1 && s.n <= kSmallMaxN) {
-    if (wg) const_cast<SelGather *>(wg)->used = 1;
+    if (wg) wg->used = 1;
     return launch_select_small(s, nsplit > 1 ? 0 : 1, st, wg ? wg->a : nullptr);
   }
   if (s.nch != select_chunks(s.n)) return cudaErrorInvalidValue;
@@ -1527,7 +1527,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, i
     note_launch();
   }
   if (wg) {
-    const_cast<SelGather *>(wg)->used = 1;
+    wg->used = 1;
     return launch_select_write_gather(s, *wg->a, wg->wpart, wg->wdone, num_sms, st, 0);
   }
   const int64_t items3 = (int64_t)s.rows * s.nch;
