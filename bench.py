@@ -588,11 +588,12 @@ def measure_gpu_only(wl, args, dev_index, h2d_peak):
             "clocks": clk.summary()}
 
 
-def measure_config5_layers(args, layers: int, dev_index: int, h2d_peak: float) -> dict:
+def measure_config5_layers(args, layers: int, dev_index: int, h2d_peak: float, host_frac: float = 0.0) -> dict:
     """BASELINE config 5 (4M-token context, g = 32, k_max = 524,288, values in host pinned
     memory) on ONE GPU with the layer count reduced to `layers` (the full 32-layer store, 275
     GB of host values, needs >= 4 ranks): per-layer time of the unsharded decode with the
-    GPU-only Eq. 5 pull, and its Eq. 3 stage."""
+    GPU-only Eq. 5 pull, and its Eq. 3 stage; with host_frac > 0 also the heterogeneous split
+    (host threads + GPU pull, the default bench's share) on the same store."""
     import torch
     cfg = dict(CONFIGS[5])
     cfg.update(L=layers, lut_bits=16, vo_only=False, cpu_gather=False, shared_kv=False, code_bits=16,
@@ -630,6 +631,28 @@ def measure_config5_layers(args, layers: int, dev_index: int, h2d_peak: float) -
                          "peak_gbs": h2d_peak, "frac": v_bytes / (ms * 1e-3) / 1e9 / h2d_peak},
            "selection": {"mean_k_sel": ksel, "k_sel_over_n": ksel / cfg["n"]},
            "gpu_launches_per_step": launches, "clocks": clk.summary()}
+    if host_frac > 0.0:  # the paper's split on the same 4M-token layer
+        from paper_2507_19823_b200.hetero import HeteroEq5
+        nthr = max(1, os.cpu_count() or 1)
+        wl.hetero = HeteroEq5(wl.kc, wl.vs, cfg["k_max"], host_frac, threads=nthr)
+        try:
+            wl.reset_counts()
+            wl.step()
+            torch.cuda.synchronize()
+            g, _ = wl.capture(wl.step)
+            with ClockSampler(dev_index) as clk2:
+                ms2 = time_graph(g, K, 3) / K
+            del g
+            wl.hetero.check()
+            res["hetero"] = {"host_frac": host_frac, "ms_per_layer": ms2 / layers,
+                             "steps_per_s_at_32_layers_extrapolated": 1000.0 / (32 * ms2 / layers),
+                             "eq5": "host threads sum the kept rows of the first host_frac of the tokens "
+                                    "over host DRAM while the GPU pulls the rest (as the default bench)",
+                             "clocks": clk2.summary()}
+        finally:
+            if wl.hetero.mode == "doorbell":
+                wl.hetero.worker.close()
+            wl.hetero = None
     if wl.vs.host is not None:
         wl.vs.host.close()
     del wl
@@ -1103,7 +1126,8 @@ def main():
         gc.collect()
         torch.cuda.empty_cache()
         try:
-            line["config5_layer"] = measure_config5_layers(args, 1, local, pk or measure_h2d_gbs())
+            line["config5_layer"] = measure_config5_layers(args, 1, local, pk or measure_h2d_gbs(),
+                                                           host_frac=float(cfg.get("host_frac") or 0.0))
         except Exception as ex:  # report, never silently drop
             line["config5_layer"] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0:
