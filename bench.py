@@ -1002,6 +1002,8 @@ def main():
     torch.cuda.synchronize()
     scan_ms = [event_ms(b, e) for (b, e) in wl.ev]
     scan_avg_ms = statistics.mean(scan_ms)
+    if os.environ.get("HC_BENCH_DEBUG"):
+        print("scan_ms per layer:", [round(x, 4) for x in scan_ms], file=sys.stderr)
     eq3_avg_ms = statistics.mean(event_ms(b, e) for (b, e) in wl.ev3)
     K2 = args.e2e_steps or max(args.steps // 2, 3)
     ms_e2e = time_graph(g_e2e, K2, args.warmup, dist) / K2
