@@ -203,6 +203,28 @@ __device__ __forceinline__ uint64_t wmass(uint32_t dl, float kappa) {
   return x0 < -40.0f ? 0ull : w;
 }
 
+// wmass for two tokens at once: the same IEEE steps with the adds / multiplies / polynomial on
+// the packed fp32x2 pipe (FADD2 / FMUL2 / FFMA2: each lane rounds as the scalar op), so both
+// results are bit-identical to wmass() (x - float(n) == x + (-float(n)); -(df κ) == df (-κ)).
+__device__ __forceinline__ void wmass2(uint32_t d0, uint32_t d1, float kappa, uint64_t &w0, uint64_t &w1) {
+  const float2 df = __fadd2_rn(make_float2(__int_as_float(0x4B000000 + (int)d0), __int_as_float(0x4B000000 + (int)d1)),
+                               make_float2(-8388608.0f, -8388608.0f));
+  const float2 x0 = __fmul2_rn(df, make_float2(-kappa, -kappa));
+  const float xa = fmaxf(x0.x, -64.0f), xb = fmaxf(x0.y, -64.0f);
+  const int na = __float2int_rd(xa), nb = __float2int_rd(xb);
+  const float2 f = __fadd2_rn(make_float2(xa, xb), make_float2(-__int2float_rn(na), -__int2float_rn(nb)));
+  float2 p = make_float2(0x1.c6e292p-13f, 0x1.c6e292p-13f);  // exp2_poly, Horner in pairs
+  p = __ffma2_rn(p, f, make_float2(0x1.46301cp-10f, 0x1.46301cp-10f));
+  p = __ffma2_rn(p, f, make_float2(0x1.3d24eap-7f, 0x1.3d24eap-7f));
+  p = __ffma2_rn(p, f, make_float2(0x1.c68562p-5f, 0x1.c68562p-5f));
+  p = __ffma2_rn(p, f, make_float2(0x1.ebfd9ap-3f, 0x1.ebfd9ap-3f));
+  p = __ffma2_rn(p, f, make_float2(0x1.62e42ap-1f, 0x1.62e42ap-1f));
+  p = __ffma2_rn(p, f, make_float2(0x1.000000p+0f, 0x1.000000p+0f));
+  const float2 v = __fmul2_rn(p, make_float2(pow2f(40 + na), pow2f(40 + nb)));
+  w0 = x0.x < -40.0f ? 0ull : __float2ull_rz(v.x);
+  w1 = x0.y < -40.0f ? 0ull : __float2ull_rz(v.y);
+}
+
 // 16-B read-only load that bypasses L1 (value rows: read once per head group)
 __device__ __forceinline__ uint4 ldg_nc16(const uint16_t *p) {
   uint4 v;

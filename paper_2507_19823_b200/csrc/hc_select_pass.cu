@@ -323,17 +323,22 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
         const float4 v = *reinterpret_cast<const float4 *>(zc + i0);
         const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (decltype(full)::value || i0 + e < nv) {
-            const uint32_t dl = (uint32_t)(M - zint(vv[e]));
-            const uint32_t b = dl >> shift;
-            const unsigned long long w = wmass(dl, kappa);
-            const uint32_t wl = (uint32_t)w;
-            uint32_t wh = (uint32_t)(w >> 32);
-            atomicAdd(&hist[b], 1u);
-            const uint32_t old = atomicAdd(&mlo[b], wl);  // exact u64 per bin: low word + carry
-            wh += (old + wl < old) ? 1u : 0u;
-            if (wh) atomicAdd(&mhi[b], wh);
+        for (int e = 0; e < 4; e += 2) {  // token pairs: the mass on the packed fp32x2 pipe
+          const uint32_t d0 = (uint32_t)(M - zint(vv[e])), d1 = (uint32_t)(M - zint(vv[e + 1]));
+          uint64_t wp[2];
+          wmass2(d0, d1, kappa, wp[0], wp[1]);
+          const uint32_t dd[2] = {d0, d1};
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (decltype(full)::value || i0 + e + q < nv) {
+              const uint32_t b = dd[q] >> shift;
+              const uint32_t wl = (uint32_t)wp[q];
+              uint32_t wh = (uint32_t)(wp[q] >> 32);
+              atomicAdd(&hist[b], 1u);
+              const uint32_t old = atomicAdd(&mlo[b], wl);  // exact u64 per bin: low word + carry
+              wh += (old + wl < old) ? 1u : 0u;
+              if (wh) atomicAdd(&mhi[b], wh);
+            }
           }
         }
       }
@@ -1192,16 +1197,20 @@ __global__ void __launch_bounds__(kST) k_sel_small(SelArgs s, int cs, int folded
   for (int i = t; i < kNB; i += kST) { hist[i] = 0u; mlo[i] = 0u; mhi[i] = 0u; }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 16; ++u) {
-    if (vmask >> u & 1u) {
-      const uint32_t bb = dl[u] >> shift;
-      const unsigned long long w = wmass(dl[u], kappa);
-      const uint32_t wl = (uint32_t)w;
-      uint32_t wh = (uint32_t)(w >> 32);
-      atomicAdd(&hist[bb], 1u);
-      const uint32_t old = atomicAdd(&mlo[bb], wl);
-      wh += (old + wl < old) ? 1u : 0u;
-      if (wh) atomicAdd(&mhi[bb], wh);
+  for (int u = 0; u < 16; u += 2) {  // token pairs: the mass on the packed fp32x2 pipe
+    uint64_t wp[2];
+    wmass2(dl[u], dl[u + 1], kappa, wp[0], wp[1]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (vmask >> (u + q) & 1u) {
+        const uint32_t bb = dl[u + q] >> shift;
+        const uint32_t wl = (uint32_t)wp[q];
+        uint32_t wh = (uint32_t)(wp[q] >> 32);
+        atomicAdd(&hist[bb], 1u);
+        const uint32_t old = atomicAdd(&mlo[bb], wl);
+        wh += (old + wl < old) ? 1u : 0u;
+        if (wh) atomicAdd(&mhi[bb], wh);
+      }
     }
   }
   cl.sync();
