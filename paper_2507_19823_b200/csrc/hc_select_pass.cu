@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(kST) k_sel_minmax(SelArgs s, int64_t per) {
 
 // ---------------------------------------------------------------------------- K1
 constexpr int kZB = 3;  // z stream buffers per CTA
-constexpr int64_t kFinishInK2 = kZB * kSelChunk / 2;  // chunks whose counters fit the z buffers
+constexpr int kZB2 = 5;  // z stream buffers of K2 (no mass histograms there: room for more in flight)
+constexpr int64_t kFinishInK2 = kZB2 * kSelChunk / 2;  // chunks whose counters fit K2's z buffers
 
 __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   extern __shared__ __align__(128) uint8_t sm1[];
@@ -453,15 +454,12 @@ __device__ void finish_row(const SelArgs &s, int row, uint32_t *cs, uint32_t *ct
 // The CTA's token range is whole chunks; per chunk every thread holds 16 consecutive tokens.
 __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   extern __shared__ __align__(16) uint8_t sm2[];
-  uint32_t *fc = reinterpret_cast<uint32_t *>(sm2);                 // [kNB] fine counts
-  uint32_t *fml = reinterpret_cast<uint32_t *>(sm2 + kNB * 4);      // [kNB] fine mass, low word
-  uint32_t *fmh = reinterpret_cast<uint32_t *>(sm2 + kNB * 8);      // [kNB] high word
-  unsigned long long *s_mass = reinterpret_cast<unsigned long long *>(sm2 + kNB * 4);  // resolve: over fml/fmh
-  float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 12);          // [kZB][kSelChunk]
+  uint32_t *fc = reinterpret_cast<uint32_t *>(sm2);                 // [kNB] exact counts per Δ
+  float *zbuf = reinterpret_cast<float *>(sm2 + kNB * 4);           // [kZB2][kSelChunk]
   unsigned long long *lq_all =                                          // [kST/32][64] per-warp list queues
-      reinterpret_cast<unsigned long long *>(sm2 + kNB * 12 + kZB * kSelChunk * 4);
-  __shared__ uint64_t zbar[kZB];
-  __shared__ uint32_t zdone[kZB];
+      reinterpret_cast<unsigned long long *>(sm2 + kNB * 4 + kZB2 * kSelChunk * 4);
+  __shared__ uint64_t zbar[kZB2];
+  __shared__ uint32_t zdone[kZB2];
   __shared__ bool s_last;
   __shared__ int s_found;
   pdl_trigger();
@@ -472,20 +470,24 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   const int M = hs->M;
   const float kappa = hs->kappa;
   const uint32_t lo = hs->r_lo, hi = hs->r_hi;
-  const int f = hs->fshift;
+  // K1 leaves one coarse bin of at most 2^11 Δ values: the fine bins are exact Δ values
+  if (hs->fshift != 0 || hi - lo >= (uint32_t)kNB) {
+    if (t == 0) hs->state = kStError;
+    return;
+  }
   const int64_t j0 = (int64_t)blockIdx.x * per, j1 = min(s.n, j0 + per);
-  for (int i = t; i < kNB; i += kST) { fc[i] = 0u; fml[i] = 0u; fmh[i] = 0u; }
-  ZStream<kZB> zs;
+  for (int i = t; i < kNB; i += kST) fc[i] = 0u;
+  ZStream<kZB2> zs;
   zs.init(zbuf, zbar, zdone, s.z + (int64_t)row * s.z_stride, s.n);
   const int64_t c0 = j0 / kSelChunk, c1 = (j1 + kSelChunk - 1) / kSelChunk;
   if (t == 0)
-    for (int i = 0; i < kZB && c0 + i < c1; ++i) zs.request(c0 + i, i);
+    for (int i = 0; i < kZB2 && c0 + i < c1; ++i) zs.request(c0 + i, i);
   unsigned long long *lq = lq_all + warp * 64;
   int lqn = 0;                // warp-uniform list-queue length (flushed 32 entries per global atomic)
   unsigned long long *lst = s.list + (int64_t)row * s.cap;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t c = c0; c < c1; ++c) {
-    const int slot = (int)((c - c0) % kZB);
+    const int slot = (int)((c - c0) % kZB2);
     const float *zc = zs.wait(slot);
     const int64_t cb = c * kSelChunk;
     const int nv = (int)min((int64_t)kSelChunk, s.n - cb);
@@ -505,15 +507,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
         const unsigned mr = __ballot_sync(0xffffffffu, inr);
         if (mr) {  // in-range: fine histogram + the row's in-range list (via the warp's queue)
           if (inr) {
-            const uint32_t fb = (dl - lo) >> f;
-            atomicAdd(&fc[fb], 1u);
-            if (f > 0) {  // fine bins of several Δ values: their exact mass too
-              uint32_t wl, wh;
-              mass_parts(dl, kappa, wl, wh);
-              const uint32_t old = atomicAdd(&fml[fb], wl);
-              wh += (old + wl < old) ? 1u : 0u;
-              if (wh) atomicAdd(&fmh[fb], wh);
-            }
+            atomicAdd(&fc[dl - lo], 1u);
             lq[lqn + __popc(mr & lt)] = ((unsigned long long)(cb + i0 + e) << 32) | dl;
           }
           lqn += __popc(mr);
@@ -535,7 +529,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     // the chunk's count of tokens above the range (K4 adds its in-range tokens below Δ*)
     nlo = __reduce_add_sync(0xffffffffu, nlo);
     if (lane == 0 && nlo) atomicAdd(&s.cntlo[(int64_t)row * s.nch + c], nlo);
-    zs.release(c + kZB < c1 ? c + kZB : -1, slot);
+    zs.release(c + kZB2 < c1 ? c + kZB2 : -1, slot);
   }
   __syncwarp();
   if (lqn > 0) {  // the warp's last list entries
@@ -544,15 +538,11 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
     base = __shfl_sync(0xffffffffu, base, 0);
     if (lane < lqn && base + lane < (unsigned)s.cap) lst[base + lane] = lq[lane];
   }
-  __syncthreads();  // every in-range token counted into fc / fml / fmh
+  __syncthreads();  // every in-range token counted into fc
   uint32_t *gc = s.fcnt + (int64_t)row * kNB;
-  unsigned long long *gm = s.fmass + (int64_t)row * kNB;
   for (int i = t; i < kNB; i += kST) {
     const uint32_t c = fc[i];
-    if (c) {
-      atomicAdd(&gc[i], c);
-      if (f > 0) atomicAdd(&gm[i], ((unsigned long long)fmh[i] << 32) + fml[i]);
-    }
+    if (c) atomicAdd(&gc[i], c);
   }
   __threadfence();
   __syncthreads();
@@ -563,20 +553,15 @@ __global__ void __launch_bounds__(kST, 2) k_sel_refine(SelArgs s, int64_t per) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // ---- the row's last CTA: walk the fine bins to the exact cut
-  __syncthreads();  // (s_mass overlays fml / fmh)
-  for (int i = t; i < kNB; i += kST) {
-    fc[i] = __ldcg(&gc[i]);
-    s_mass[i] = f > 0 ? __ldcg(&gm[i]) : 0ull;
-  }
+  // ---- the row's last CTA: walk the bin's Δ values to the exact cut
+  for (int i = t; i < kNB; i += kST) fc[i] = __ldcg(&gc[i]);
   if (t == 0) hs->c2_done = 0u;
   __syncthreads();
   const bool tau_all = s.tau_q >= (1u << 24);
   const bool cap_all = (unsigned long long)s.k_max >= (unsigned long long)s.n;
   const unsigned long long Sx = hs->S, theta = hs->theta;  // exact (K1)
   const unsigned long long cc0 = hs->cnt_before, cm0 = __ldcg((const unsigned long long *)&hs->mass_before);
-  resolve_bins(fc, f > 0 ? s_mass : nullptr, f, lo, hi, cc0, cm0, s, hs, row, kappa, theta, tau_all,
-               cap_all, Sx, &s_found);
+  resolve_bins(fc, nullptr, 0, lo, hi, cc0, cm0, s, hs, row, kappa, theta, tau_all, cap_all, Sx, &s_found);
   if (s.nch <= kFinishInK2) {  // the row's finish here (no K4 launch): counters over the z buffers
     __syncthreads();
     finish_row(s, row, reinterpret_cast<uint32_t *>(zbuf), reinterpret_cast<uint32_t *>(zbuf) + s.nch, fc);
@@ -1526,7 +1511,7 @@ cudaError_t launch_select(SelArgs s, int nsplit, int num_sms, cudaStream_t st, i
   const size_t smem1 = (size_t)kZB * kSelChunk * 4 + (size_t)kNB * 8;
   launch_chain(k_sel_mass, g12, dim3(kST), smem1, st, s, per);
   note_launch();
-  const size_t smem2 = (size_t)kNB * 12 + (size_t)kZB * kSelChunk * 4 + (kST / 32) * 64 * 8;
+  const size_t smem2 = (size_t)kNB * 4 + (size_t)kZB2 * kSelChunk * 4 + (kST / 32) * 64 * 8;
   launch_chain(k_sel_refine, g12, dim3(kST), smem2, st, s, per);
   note_launch();
   if (s.nch > kFinishInK2) {  // rows too long for K2's in-place finish
