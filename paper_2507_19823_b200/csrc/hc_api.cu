@@ -137,7 +137,7 @@ struct Layout {
   int64_t z_stride;
   int64_t k_eff;
   size_t o_hs, o_T, o_cbabs, o_z, o_zpart, o_idx, o_w, o_chunk, o_part, o_upart, o_udone, o_rpart,
-      o_rdone, o_wpart, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, o_sgh, o_sfc, o_sfm,
+      o_rdone, o_wpart, o_grp, o_ghist, o_gchunk, o_gkey, o_grange, o_skpart, o_skctr, o_sgh, o_sfc,
       o_scl, o_spre, o_slist, total;
   int64_t snch, scap;
   int skctr_n;
@@ -167,7 +167,6 @@ Layout make_layout(const hc_kcache *kc, int64_t k_max, int shared = 0) {
   L.scap = select_list_cap(ncand_max > 0 ? ncand_max : 1);
   L.o_sgh = o; o += align256((size_t)rows * kNB * 12);  // ghist u32 then gmass u64
   L.o_sfc = o; o += align256((size_t)rows * kNB * 4);
-  L.o_sfm = o; o += align256((size_t)rows * kNB * 8);
   L.o_scl = o; o += align256((size_t)rows * L.snch * 4);
   L.o_spre = o; o += align256((size_t)rows * L.snch * 8);
   L.o_slist = o; o += align256((size_t)rows * L.scap * 8);
@@ -717,7 +716,6 @@ static hc_status decode_impl(const uint16_t *q, const hc_kcache *kc, const hc_vs
   sa.ghist = (uint32_t *)((uint8_t *)ws + Lw.o_sgh);
   sa.gmass = (unsigned long long *)(sa.ghist + rows * kNB);
   sa.fcnt = (uint32_t *)((uint8_t *)ws + Lw.o_sfc);
-  sa.fmass = (unsigned long long *)((uint8_t *)ws + Lw.o_sfm);
   sa.cntlo = (uint32_t *)((uint8_t *)ws + Lw.o_scl);
   sa.pre = (unsigned long long *)((uint8_t *)ws + Lw.o_spre);
   sa.list = (unsigned long long *)((uint8_t *)ws + Lw.o_slist);
@@ -931,7 +929,7 @@ size_t hc_select_workspace_bytes(int64_t rows, int64_t n, hc_budget budget) {
   if (rows <= 0 || n <= 0) return 0;
   const int64_t zs = round_up(n, 64);
   return align256((size_t)rows * sizeof(HeadState)) + align256((size_t)rows * zs * 4) +
-         align256((size_t)rows * kNB * 4) * 2 + align256((size_t)rows * kNB * 8) * 2 +
+         align256((size_t)rows * kNB * 4) * 2 + align256((size_t)rows * kNB * 8) +
          align256((size_t)rows * select_chunks(n) * 4) + align256((size_t)rows * select_chunks(n) * 8) +
          align256((size_t)rows * select_list_cap(n) * 8);
 }
@@ -958,7 +956,6 @@ hc_status hc_select_topk(const float *scores, int64_t rows, int64_t n, int32_t d
   sa.ghist = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
   sa.gmass = (unsigned long long *)(w8 + o); o += align256((size_t)rows * kNB * 8);
   sa.fcnt = (uint32_t *)(w8 + o); o += align256((size_t)rows * kNB * 4);
-  sa.fmass = (unsigned long long *)(w8 + o); o += align256((size_t)rows * kNB * 8);
   sa.cntlo = (uint32_t *)(w8 + o); o += align256((size_t)rows * select_chunks(n) * 4);
   sa.pre = (unsigned long long *)(w8 + o); o += align256((size_t)rows * select_chunks(n) * 8);
   sa.list = (unsigned long long *)(w8 + o);

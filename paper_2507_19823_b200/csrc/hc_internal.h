@@ -183,7 +183,6 @@ struct SelArgs {
   uint32_t *ghist;             // [rows][kNB] coarse counts
   unsigned long long *gmass;   // [rows][kNB] coarse exact masses (directly after ghist)
   uint32_t *fcnt;              // [rows][kNB]
-  unsigned long long *fmass;   // [rows][kNB]
   uint32_t *cntlo;             // [rows][nch] per chunk: tokens above the refine range
   unsigned long long *pre;     // [rows][nch] per chunk: exclusive (strict << 32 | ties) prefix
   unsigned long long *list;    // [rows][cap] in-range tokens (index << 32 | Δ)

@@ -301,10 +301,7 @@ __global__ void __launch_bounds__(kST, 2) k_sel_mass(SelArgs s, int64_t per) {
   {  // this CTA's share of the row's refine histograms and chunk counters (used by K2 / K4)
     const int64_t nf = (int64_t)kNB, nl = s.nch;
     const int64_t f0 = nf * blockIdx.x / gridDim.x, f1 = nf * (blockIdx.x + 1) / gridDim.x;
-    for (int64_t i = f0 + t; i < f1; i += kST) {
-      s.fcnt[(int64_t)row * kNB + i] = 0u;
-      s.fmass[(int64_t)row * kNB + i] = 0ull;
-    }
+    for (int64_t i = f0 + t; i < f1; i += kST) s.fcnt[(int64_t)row * kNB + i] = 0u;
     const int64_t l0 = nl * blockIdx.x / gridDim.x, l1 = nl * (blockIdx.x + 1) / gridDim.x;
     for (int64_t i = l0 + t; i < l1; i += kST) s.cntlo[(int64_t)row * nl + i] = 0u;
   }
