@@ -3,35 +3,30 @@
 // P:240-252), as three bandwidth-shaped passes over the scores z instead of one cluster of
 // CTAs per row (the round-1 k_select_fused: 3-4 passes, 2-3 shared atomics per token).
 //
-//   K1 k_sel_mass    every token: Δ = M - z (M folded by the scan epilogue) -> a COUNT-only
-//                    coarse histogram of Δ >> shift (one shared atomic per token, no mass).
-//                    The row's last CTA bounds the mass of every coarse bin from the exact
-//                    counts and W's monotonicity in Δ (W at the bin's two ends, widened by a
-//                    slack that covers the exp2 polynomial's rounding) -- hence also the total
-//                    S in [S_lo, S_hi] and Θ in [Θ(S_lo), Θ(S_hi)] -- and keeps the range of
-//                    bins the exact cut can fall in for ANY Θ of that interval (plus the k_max
-//                    cap's bin, from exact counts).  (Keep-everything rows, τ >= 1 and
-//                    k_max >= n, need the exact S in K1 itself: only they sum W here.)
-//   K2 k_sel_refine  W of every token (branch-free): the exact total S and the exact mass of
-//                    every token above that range (P_above), exact counts (and exact masses
-//                    if the range spans more than kNB values) of the tokens inside it, per
-//                    K3-chunk counts of the tokens above the range, and the in-range tokens
-//                    themselves (index, Δ) on a per-row list; the last CTA forms the exact
-//                    Θ = ceil(τ_q S / 2^24), walks the fine bins to the exact Δ*, the number r
-//                    of Δ* ties kept (lowest indices), k_sel, k*, the kept mass -- or, for a
-//                    wide range, narrows it to one fine bin.
-//   K4 k_sel_prefix  one CTA per row: (if narrowed) the second refine from the in-range list;
-//                    then every chunk's (strict, tie) counts -- the count above the range plus
-//                    its in-range tokens classified against Δ* -- and their exclusive prefix.
-//   K3 k_sel_write   independent CTAs per (row, chunk): the chunk's kept tokens at their
-//                    global positions (prefix + in-chunk scan), staged in shared memory and
-//                    written coalesced as (index, W/S).
-// A row whose in-range list overflowed its capacity (degenerate score distributions: heavy
-// ties) is finished by K4 from a pass over its z instead -- slower, equally exact.
+//   K1 k_sel_mass    every token: Δ = M - z (M folded by the scan epilogue), its exact mass W
+//                    (R4; token pairs on the fp32x2 pipe, wmass2) -> an EXACT (count, mass)
+//                    histogram of Δ >> shift (count + the u64 mass as two u32 words: three
+//                    shared atomics per token).  The row's last CTA scans the exact bins: S, Θ =
+//                    ceil(τ_q S / 2^24) and the one coarse bin the cut falls in (the first
+//                    whose cumulative mass reaches Θ or whose cumulative count reaches k_max),
+//                    with the exact count and mass before it.
+//   K2 k_sel_refine  every token: Δ; per K3-chunk counts of the tokens before the cut bin, and
+//                    the cut bin's tokens themselves (exact per-Δ counts + (index, Δ) on a
+//                    per-row list); the last CTA walks the bin's <= 2^11 Δ values to the exact
+//                    Δ*, the number r of Δ* ties kept (lowest indices), k_sel, k*, the kept
+//                    mass, then every chunk's (strict, tie) counts and their exclusive prefix.
+//   K4 k_sel_prefix  (rows of more than kFinishInK2 chunks) that finish, one CTA per row.
+//   K3 k_sel_write   persistent CTAs over the (row, chunk) items: the chunk's kept tokens at
+//                    their global positions (prefix + in-chunk scan), staged in shared memory
+//                    and written coalesced as (index, W/S).  With values in HBM, K3G
+//                    (k_sel_write_gather) also sums Eq. 5 over the kept rows as it emits them.
+//   k_sel_small      rows of <= 64K candidates: all of the above in one cluster kernel per row.
+// A row whose in-range list overflowed its capacity (heavy ties) is finished from a pass over
+// its z instead -- slower, equally exact.
 //
 // Every decision is integer arithmetic on exact quantities (counts, u64 masses, the
 // 128-bit threshold Θ), so the kept set equals the oracle's bit for bit (or_select: sort by
-// (Δ asc, index asc), prefix to Θ, cap) -- the bounds only choose WHERE to look.
+// (Δ asc, index asc), prefix to Θ, cap).
 #include <cooperative_groups.h>
 
 #include <type_traits>
