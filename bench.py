@@ -951,21 +951,31 @@ def main():
     wl = Workload(cfg, dev, rank if sharded_mode else 0, world if sharded_mode else 1)
     if cfg.get("host_frac_auto") and wl.hetero is not None and not wl.parts:
         calibrate_host_frac(wl, cfg)
+    shard_path = None
     if sharded_mode:
         import paper_2507_19823_b200 as hc
+        from paper_2507_19823_b200.sharded import GpuShard, TorchComm, decode_layer
+
+        class _PhaseShard:  # the phase kernels with torch.distributed collectives between them
+            def __init__(self, wl_):
+                self.g, self.c, self.wl = GpuShard(wl_.kc, wl_.vs, wl_.bud), TorchComm(), wl_
+                self.sel_k = self.g.sel_k
+
+            def decode_layer(self, q, l):
+                return decode_layer(self.g, self.c, q, l, self.wl.base)
+
         if backend == "nccl":
-            wl.enable_sharding(hc.NcclComm.from_process_group(), rank, world)
+            try:
+                wl.enable_sharding(hc.NcclComm.from_process_group(), rank, world)
+                shard_path = "hc_decode_attention_sharded (NCCL issued by the library)"
+            except Exception as ex:  # fall back to torch's NCCL collectives, and say so
+                print(f"[bench] C-ABI NCCL path unavailable ({type(ex).__name__}: {ex}); "
+                      "phases with torch.distributed collectives", file=sys.stderr, flush=True)
+                wl.shard = _PhaseShard(wl)
+                shard_path = "hc_shard_* phases + torch.distributed NCCL collectives (fallback)"
         else:  # HC_BENCH_BACKEND=gloo code-path smoke on one GPU: the phases with gloo collectives
-            from paper_2507_19823_b200.sharded import GpuShard, TorchComm, decode_layer
-
-            class _PhaseShard:
-                def __init__(self, wl_):
-                    self.g, self.c, self.wl = GpuShard(wl_.kc, wl_.vs, wl_.bud), TorchComm(), wl_
-                    self.sel_k = self.g.sel_k
-
-                def decode_layer(self, q, l):
-                    return decode_layer(self.g, self.c, q, l, self.wl.base)
             wl.shard = _PhaseShard(wl)
+            shard_path = "hc_shard_* phases + gloo collectives (code-path smoke)"
     torch.cuda.synchronize()
     # eager correctness sanity (one step) then capture the step with scan events
     wl.reset_counts()
@@ -1073,6 +1083,7 @@ def main():
                    "l2": f"inputs > L2: P = {B * L * H * n * g * 2 / 1e9:.2f} GB/step, V = "
                          f"{B * L * H * n * d * 2 / 1e9:.2f} GB",
                    "graph": graph_mode,
+                   **({"shard_path": shard_path} if shard_path else {}),
                    **({"host_frac": round(cfg["host_frac"], 2),
                        "host_frac_from": "calibrated at start-up" if cfg.get("host_frac_auto") else "--host-frac"}
                       if cfg["host_frac"] > 0.0 else {})},
