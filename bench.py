@@ -2,9 +2,10 @@
 """Benchmark of the HCAttention decode hot path on B200 (one JSON line on rank 0).
 
 A "step" is one full decode step of a Llama-3-8B-shaped model (BASELINE.json
-configs): for each of the L = 32 layers in order, hc_append_kv (encode the new key
-into the quantized cache, append the value) then hc_decode_attention (table, Eq. 3
-scan, softmax mass, Eq. 4 selection, Eq. 5 gather) for all B x 32 query heads.
+configs): for each of the L = 32 layers in order, the append (encode the new key into the
+quantized cache, append the value) and the decode (table, Eq. 3 scan, softmax mass, Eq. 4
+selection, Eq. 5 gather) for all B x 32 query heads -- one hc_append_decode_attention call
+per layer (values in HBM), or hc_append_kv + the heterogeneous Eq. 5 (host-resident values).
 The step is captured once in a CUDA graph and replayed (steady state: the append
 rewrites position n-1, the decode covers n tokens).
 
@@ -17,8 +18,9 @@ runs heterogeneously (host threads + the GPU's zero-copy pull, share calibrated 
 --host-frac 0 = GPU only) and a `gpu_only` sub-record times the GPU-only pull too.
 N > 1 (torchrun): config 4 (1M context) sequence-sharded over the N ranks through the
 C-ABI sharded decode (NCCL collectives between the phase kernels), strong scaling;
---config 5 (4M, host-resident values) needs >= 4 ranks, --config5-layers times one layer of
-it on one GPU.  --impl reference times the CPU oracle (oracle/, plain C) as it stands.
+--config 5 (4M, host-resident values) needs >= 4 ranks; the default N = 1 line carries a
+`config5_layer` record (one 4M-token layer on one GPU, GPU-only pull and the heterogeneous
+split).  --impl reference times the CPU oracle (oracle/, plain C) as it stands.
 """
 from __future__ import annotations
 
