@@ -131,9 +131,11 @@ __device__ __forceinline__ void sh_scan2(unsigned long long &x, unsigned long lo
 
 // bound1 on the GLOBAL coarse histogram (identical on every rank) -> hs
 __global__ void __launch_bounds__(kShT) k_sh_bound1(SelArgs s, const int32_t *gstats,
-                                                    const unsigned long long *h1) {
+                                                    const unsigned long long *h1, unsigned long long *h2z) {
   const int row = blockIdx.x;
   HeadState *hs = s.hs + row;
+  // the next phase's fine histogram row, zeroed here (no memset node between the kernels)
+  for (int i = threadIdx.x; i < kNB; i += kShT) h2z[(int64_t)row * kNB + i] = 0ull;
   constexpr int kB = kNB / kShT;
   const unsigned long long *hr = h1 + (int64_t)row * kNB * 2;
   unsigned long long c[kB], m[kB], lc = 0, lm = 0;
@@ -202,9 +204,11 @@ __global__ void __launch_bounds__(kShT) k_sh_hist2(LayerArgs a, unsigned long lo
 }
 
 // bound2 on the GLOBAL fine histogram -> Δ*, r, k_sel (identical on every rank)
-__global__ void __launch_bounds__(kShT) k_sh_bound2(SelArgs s, const unsigned long long *h2) {
+__global__ void __launch_bounds__(kShT) k_sh_bound2(SelArgs s, const unsigned long long *h2,
+                                                    unsigned long long *cntz) {
   const int row = blockIdx.x;
   HeadState *hs = s.hs + row;
+  if (threadIdx.x < 2) cntz[(int64_t)row * 2 + threadIdx.x] = 0ull;  // the counts phase's totals
   const HeadState h = *hs;
   if (h.bstar >= kNB) return;
   constexpr int kB = kNB / kShT;
@@ -531,8 +535,9 @@ __global__ void __launch_bounds__(kShT) k_sh_compact(LayerArgs a, SelArgs s, int
 // counts before each of this rank's chunks -- the lower ranks' totals (all-gathered) plus this
 // rank's earlier chunks -- as (strict << 32 | ties); and the row marked resolved for K3G.
 __global__ void __launch_bounds__(256) k_sh_pre(SelArgs s, int nch, const uint32_t *chunk,
-                                                const unsigned long long *allcnt, int rank) {
+                                                const unsigned long long *allcnt, int rank, uint32_t *rdonez) {
   const int row = blockIdx.x, t = threadIdx.x;
+  if (t == 0) rdonez[row] = 0u;  // K3G's per-row completion counter (no memset node)
   __shared__ unsigned long long base2[2];
   __shared__ unsigned long long wsum[2][8];
   if (t == 0) {
@@ -615,9 +620,8 @@ cudaError_t launch_shard_hist1(const LayerArgs &a, const int32_t *gstats, unsign
 cudaError_t launch_shard_hist2(const LayerArgs &a, const SelArgs &s, const int32_t *gstats,
                                const unsigned long long *h1, unsigned long long *h2, cudaStream_t st) {
   const int rows = a.B * a.Hq;
-  k_sh_bound1<<<rows, kShT, 0, st>>>(s, gstats, h1);
+  k_sh_bound1<<<rows, kShT, 0, st>>>(s, gstats, h1, h2);
   note_launch();
-  cudaMemsetAsync(h2, 0, (size_t)rows * kNB * 8, st);
   k_sh_hist2<<<dim3(sh_grid(a.n_cand), rows), kShT, 0, st>>>(a, h2);
   note_launch();
   return cudaGetLastError();
@@ -628,9 +632,8 @@ int shard_chunks(int64_t n) { return (int)((n + kShChunk - 1) / kShChunk); }
 cudaError_t launch_shard_counts(const LayerArgs &a, const SelArgs &s, const unsigned long long *h2,
                                 uint32_t *chunk, unsigned long long *cnt, cudaStream_t st) {
   const int rows = a.B * a.Hq;
-  k_sh_bound2<<<rows, kShT, 0, st>>>(s, h2);
+  k_sh_bound2<<<rows, kShT, 0, st>>>(s, h2, cnt);
   note_launch();
-  cudaMemsetAsync(cnt, 0, (size_t)rows * 16, st);
   const int nch = shard_chunks(a.n_cand);
   if (nch > 0) {
     k_sh_counts<<<dim3(nch, rows), kShT, 0, st>>>(a, nch, chunk, cnt);
@@ -655,10 +658,8 @@ cudaError_t launch_shard_finish(const LayerArgs &a, const SelArgs &s, const uint
     s2.pre = pre;
     s2.nch = nch;
     s2.n = a.n_cand;
-    k_sh_pre<<<rows, 256, 0, st>>>(s2, nch, chunk, allcnt, rank);
+    k_sh_pre<<<rows, 256, 0, st>>>(s2, nch, chunk, allcnt, rank, rdone);
     note_launch();
-    cudaError_t e = cudaMemsetAsync(rdone, 0, (size_t)rows * 4, st);
-    if (e != cudaSuccess) return e;
     LayerArgs g = a;
     g.out = out;
     return launch_select_write_gather(s2, g, wpart, rdone, a.num_sms, st, base);
