@@ -981,8 +981,20 @@ def main():
     torch.cuda.synchronize()
     # eager correctness sanity (one step) then capture the step with scan events
     wl.reset_counts()
-    wl.step()
-    torch.cuda.synchronize()
+    try:
+        wl.step()
+        torch.cuda.synchronize()
+    except Exception as ex:
+        if not (sharded_mode and backend == "nccl" and shard_path and "library" in shard_path):
+            raise
+        # the C-ABI NCCL path failed at run time: the phases with torch's collectives, and say so
+        print(f"[bench] C-ABI NCCL step failed ({type(ex).__name__}: {ex}); phases with "
+              "torch.distributed collectives", file=sys.stderr, flush=True)
+        wl.shard = _PhaseShard(wl)
+        shard_path = "hc_shard_* phases + torch.distributed NCCL collectives (fallback)"
+        wl.reset_counts()
+        wl.step()
+        torch.cuda.synchronize()
     graph_mode = "one CUDA graph per step (32 x append + decode)"
     try:
         # the timed graph carries no event nodes (64 per step cost ~0.3 ms at config 2); the
